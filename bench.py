@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""Frame-render benchmark of the B200-native ray tracer (one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one frame of the workload `--config` (default C2: the paper's
+benchmark scene, 1280x720, 200 soft-shadow samples, 3 reflection bounces —
+BASELINE.json configs[1]).  `value` is frames/s with the scene resident in
+HBM (device-timed render kernels, CUDA events on the launching stream,
+L2 flushed between frames); `e2e` is frames/s through the public
+`render_frame` into a host Framebuffer (the reference's call, bench.py:65-78
+methodology: wall clock around the synchronous call, frame copied back).
+With N > 1 (torchrun, one process per GPU) every rank renders its
+interleaved 8-row blocks straight into rank 0's framebuffer over NVLink
+(CUDA IPC), and the step time is the max over ranks.
+
+`--impl reference` times the reference algorithm on the host CPU: the
+float64 C port of `render_frame` (oracle/, bit-identical to the reference's
+numba path) with every host thread, on a bounded row sample of the same
+workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965  # SMs x FP32 lanes x FMA x max SM clock (GHz) / 1e3
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse_args(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.split("\n\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other configurations' fps")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU-baseline sample budget")
+    return ap.parse_args(argv)
+
+
+def work_counts():
+    with open(os.path.join(ROOT, "paper_2305_07450_b200", "work_counts.json")) as f:
+        return json.load(f)["configs"]
+
+
+# --- clocks during the timed region ------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax = float(parts[2])
+                except ValueError:
+                    continue
+                for name, flag in zip(names, parts[5:9]):
+                    if flag.lower() == "active":
+                        reasons.add(name)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --- CPU: the reference algorithm on the host cores -------------------------------
+def cpu_reference_sample(cfg, budget_s, threads=0):
+    """Time the float64 C port of render_frame (oracle/, bit-identical to the
+    reference) on every `step`-th row of the workload; returns frames/s."""
+    import oracle
+    from paper_2305_07450_b200 import pack_scene
+
+    scene, cam = cfg.scene(), cfg.camera()
+    ps = vars(pack_scene(scene))
+
+    def run(step):
+        t = time.perf_counter()
+        oracle.render(ps, cam.position, cam.yaw, cam.pitch, cam.fov, cfg.width, cfg.height, cfg.samples, cfg.bounces,
+                      row0=step // 2, row_step=step, threads=threads)
+        return time.perf_counter() - t
+
+    step = max(1, cfg.height // 8)
+    dt = run(step)
+    # rows sampled scale linearly: pick the stride that fills the budget
+    rows = len(range(step // 2, cfg.height, step))
+    per_row = dt / rows
+    want_rows = max(1, min(cfg.height, int(budget_s / max(per_row, 1e-9))))
+    step = max(1, cfg.height // want_rows)
+    dt = run(step)
+    rows = len(range(step // 2, cfg.height, step))
+    frac = rows / cfg.height
+    return frac / dt, dict(rows=rows, row_step=step, seconds=dt, threads=threads or oracle.max_threads())
+
+
+def run_reference(args):
+    from paper_2305_07450_b200 import CONFIGS
+    import oracle
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    threads = oracle.max_threads()
+    per_step = max(2.0, args.cpu_seconds / max(1, args.steps))
+    vals = []
+    meta = None
+    for i in range(args.warmup + args.steps):
+        budget = 0.5 if i < args.warmup else per_step
+        v, meta_i = cpu_reference_sample(cfg, budget, threads)
+        if i >= args.warmup:
+            vals.append(v)
+            meta = meta_i
+    fps = statistics.mean(vals)
+    wc = work_counts()[args.config]
+    sample = (f"every {meta['row_step']}th row ({meta['rows']} of {cfg.height} rows) of {cfg.name} per step, "
+              f"float64 C port of render_frame (oracle/rt_oracle.c), OpenMP dynamic rows")
+    line = {
+        "impl": "reference",
+        "metric": "frames/s",
+        "value": fps,
+        "unit": "frames/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1000.0 / fps,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (the paper's benchmark scene, sceneio.py:314-333)",
+        "config": {"workload": cfg.name, "width": cfg.width, "height": cfg.height, "samples": cfg.samples,
+                   "bounces": cfg.bounces, "sky": cfg.sky},
+        "mrays_per_s": wc["rays"] * fps / 1e6,
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": meta["threads"], "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --- GPU ----------------------------------------------------------------------------
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return world, rank, local
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2305_07450_b200 as rt
+    from paper_2305_07450_b200 import _native
+
+    world, rank, local = _dist_env()
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    lib = _native.load()
+    ctx = _native.Context((local,))
+    cfg = rt.CONFIGS[args.config]
+    prec = _native.PRECISIONS[args.precision]
+    wc = work_counts()
+
+    def set_scene(scene):
+        ps = rt.pack_scene(scene)
+        P = _native.ptr
+        _native.check(lib.rt_set_scene_v1(ctx.handle, ps.n_bodies, P(ps.kinds), P(ps.positions), P(ps.sizes),
+                                          P(ps.colors), P(ps.refls), P(ps.light_pos), ps.light_radius,
+                                          P(ps.light_color), ps.ambient, ps.max_refl, P(ps.sky), ps.sky_w, ps.sky_h,
+                                          int(ps.has_sky)), "rt_set_scene_v1")
+        return ps
+
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+
+    # framebuffer: rank 0 owns it; other ranks map it over NVLink (CUDA IPC)
+    fb_ptr = ctypes.c_void_p()
+    frame_bytes = 4 * cfg.width * cfg.height
+    peer_ptr = None
+    if rank == 0:
+        _native.check(lib.rt_device_malloc(local, frame_bytes, ctypes.byref(fb_ptr)), "rt_device_malloc")
+    if world > 1:
+        import torch.distributed as dist
+        handle = (ctypes.c_uint8 * 64)()
+        if rank == 0:
+            _native.check(lib.rt_ipc_get_handle(fb_ptr, handle), "rt_ipc_get_handle")
+        obj = [bytes(handle)]
+        dist.broadcast_object_list(obj, src=0)
+        if rank != 0:
+            h = (ctypes.c_uint8 * 64).from_buffer_copy(obj[0])
+            peer = ctypes.c_void_p()
+            _native.check(lib.rt_ipc_open(h, ctypes.byref(peer)), "rt_ipc_open")
+            fb_ptr = peer
+            peer_ptr = peer
+    tiny = torch.zeros(1, device=dev)
+
+    def render_cfg(c, part=rank, n_parts=world):
+        cam = c.camera()
+        cp = np.array(cam.position, dtype=np.float64)
+        rc = lib.rt_render_device_v1(ctx.handle, 0, fb_ptr, c.width, None, c.width, c.height, _native.ptr(cp),
+                                     float(cam.yaw), float(cam.pitch), rt.camera_viewport_distance(cam.fov),
+                                     c.samples, c.bounces, part, n_parts, 8, prec, ctypes.c_void_p(stream.cuda_stream))
+        _native.check(rc, "rt_render_device_v1")
+        if world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(tiny)  # completes once every rank's band has landed
+
+    def time_config(c, warmup, steps, sample_clocks=False):
+        set_scene(c.scene())
+        for _ in range(warmup):
+            render_cfg(c)
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        clocks = ClockSampler(local).start() if sample_clocks else None
+        n0 = ctx.launch_count()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for e0, e1 in evs:
+            flush.zero_()  # L2 flush between frames (outside the event pair)
+            e0.record(stream)
+            render_cfg(c)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        launches = ctx.launch_count() - n0
+        clk = clocks.stop() if clocks else None
+        ms = [a.elapsed_time(b) for a, b in evs]
+        total = sum(ms)
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([total], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            total = float(t.item())
+        return dict(ms=ms, total_ms=total, wall_s=wall, launches=launches, clocks=clk)
+
+    # headline: device-resident frames/s
+    main = time_config(cfg, max(3, args.warmup), args.steps, sample_clocks=True)
+    fps = args.steps / (main["total_ms"] / 1e3)
+    ms_kernel = statistics.mean(main["ms"])
+    flops = wc[args.config]["flops"]
+    rays = wc[args.config]["rays"]
+
+    # e2e through the public API into a host framebuffer (rank 0's process)
+    e2e = None
+    if world == 1:
+        scene, cam, params = cfg.scene(), cfg.camera(), cfg.params()
+        fb = rt.Framebuffer.create(cfg.width, cfg.height)
+        for _ in range(max(3, args.warmup)):
+            rt.render_frame(scene, cam, params, fb, precision=args.precision)
+        ts = []
+        for _ in range(args.steps):
+            t = time.perf_counter()
+            rt.render_frame(scene, cam, params, fb, precision=args.precision)
+            ts.append(time.perf_counter() - t)
+        e2e_fps = args.steps / sum(ts)
+        h2d = 0  # scene unchanged between frames: cached on the device; kernel args travel with the launch
+        e2e = {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": frame_bytes,
+               "ms_per_step": 1e3 * statistics.mean(ts)}
+    else:
+        # rank 0 reads the gathered frame back into pinned host memory every step
+        import torch.distributed as dist
+        host = torch.empty(cfg.width * cfg.height, dtype=torch.int32, pin_memory=True) if rank == 0 else None
+        ts = []
+        for i in range(max(3, args.warmup) + args.steps):
+            dist.barrier()
+            t = time.perf_counter()
+            render_cfg(cfg)
+            if rank == 0:
+                _native.check(lib.rt_copy_to_host(ctx.handle, 0, ctypes.c_void_p(host.data_ptr()), fb_ptr,
+                                                  frame_bytes, ctypes.c_void_p(stream.cuda_stream)),
+                              "rt_copy_to_host")
+            torch.cuda.synchronize()
+            if i >= max(3, args.warmup):
+                ts.append(time.perf_counter() - t)
+        t = torch.tensor([sum(ts)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = {"value": args.steps / float(t.item()), "unit": "frames/s", "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": frame_bytes}
+
+    peak_meas = _native.fp32_peak_tflops(local)
+    achieved = flops / (ms_kernel * 1e-3) / 1e12
+    line = {
+        "metric": "frames/s",
+        "value": fps,
+        "unit": "frames/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": main["total_ms"] / args.steps,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32" if args.precision == "fp32" else "f64",
+        "data": "synthetic (the paper's benchmark scene and camera, sceneio.py:314-333)",
+        "config": {"workload": cfg.name, "width": cfg.width, "height": cfg.height, "samples": cfg.samples,
+                   "bounces": cfg.bounces, "sky": cfg.sky, "parallelism": f"row-blocks x{world} (8-row interleave)",
+                   "l2": "flushed between timed frames (256 MiB memset outside the event pair)"},
+        "mrays_per_s": rays * fps / 1e6,
+        "e2e": e2e,
+        "gpu_launches": main["launches"],
+        "clocks": main["clocks"],
+        "roofline": {
+            "bound": "fp32",
+            "achieved": achieved,
+            "peak": peak_meas,
+            "unit": "TFLOP/s",
+            "frac": achieved / peak_meas,
+            "peak_source": "measured FFMA stream on this GPU (rt_fp32_peak_tflops); MEASURED_PEAKS.json has no FP32 figure",
+            "peak_nominal": NOMINAL_FP32_TFLOPS,
+            "frac_of_nominal": achieved / NOMINAL_FP32_TFLOPS,
+            "flops_per_frame": flops,
+            "kernel_ms": ms_kernel,
+            "traffic": None,
+        },
+    }
+    if rank == 0 and not args.no_extra and world == 1:
+        extra = {}
+        for key in ("C1", "P720", "P1080", "P4K", "C3", "C4"):
+            c = rt.CONFIGS[key]
+            r = time_config(c, 3, 10 if key != "C4" else 5)
+            f = len(r["ms"]) / (r["total_ms"] / 1e3)
+            km = statistics.mean(r["ms"])
+            ach = wc[key]["flops"] / (km * 1e-3) / 1e12
+            extra[key] = {"workload": c.name, "fps": f, "kernel_ms": km, "mrays_per_s": wc[key]["rays"] * f / 1e6,
+                          "tflops": ach, "frac_of_measured_fp32": ach / peak_meas}
+            if key in rt.workloads.PAPER_FPS:
+                extra[key]["paper_fps_rtx2060"] = rt.workloads.PAPER_FPS[key]
+        line["extra"] = extra
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        v, meta = cpu_reference_sample(cfg, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": v, "unit": "frames/s", "cores": meta["threads"], "kind": "port",
+                                "sample": f"every {meta['row_step']}th row ({meta['rows']}/{cfg.height}) of "
+                                          f"{cfg.name}, float64 C port of render_frame (oracle/), "
+                                          f"{meta['seconds']:.1f} s"}
+    if peer_ptr is not None:
+        lib.rt_ipc_close(peer_ptr)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    if rank == 0:
+        lib.rt_device_free(fb_ptr)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,154 @@
+/*
+ * b200rt — C ABI of the B200-native frame render (libb200rt.so).
+ *
+ * Drop-in boundary for the reference's native render operator: the numba
+ * kernel `_render_kernel(pixels, width, height, cam_pos, yaw, pitch, vdist,
+ * kinds, positions, sizes, colors, refls, light_pos, light_radius,
+ * light_color, ambient, max_refl, sky, sky_w, sky_h, has_sky,
+ * shadow_samples, bounce_limit)` (/root/reference/pkg/src/raytracer/
+ * renderer.py:227-252), dispatched by `render_frame` (renderer.py:316-349),
+ * itself the paper's `Renderer::render(pixels, dimensions, camera, ...)`
+ * (/root/reference/PAPER.md:1008-1020).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Scene arrays are the reference's packed
+ *    structure-of-arrays (geometry.py:162-176): kinds int32[n] (0 sphere,
+ *    1 horizontal plane), positions f64[n][3], sizes f64[n], colors f64[n][3],
+ *    refls f64[n]; the skybox is f32[sky_h][sky_w][3] (scene.py:21-35).
+ *  - Pixels are uint32 0xAARRGGBB, index x + y*width (renderer.py:45-50,
+ *    scene.py:75-94); little-endian bytes are B,G,R,A.
+ *  - Every function returns RT_OK (0) or a negative RT_ERR_* code; the
+ *    message is in rt_last_error() (thread-local).  Nothing is ever computed
+ *    on the CPU: without a CUDA device every compute call fails with
+ *    RT_ERR_NO_DEVICE.
+ *  - Calls on one rt_ctx are serialised by an internal mutex; the library
+ *    never holds the Python GIL (ctypes.CDLL drops it), like the reference's
+ *    nogil=True kernel (renderer.py:227).
+ */
+#ifndef B200RT_H
+#define B200RT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RT_ABI_VERSION 1
+
+enum {
+    RT_OK = 0,
+    RT_ERR_INVALID = -1,   /* bad argument: the reference raises ValueError (renderer.py:322-328) */
+    RT_ERR_CUDA = -2,      /* CUDA runtime/kernel failure */
+    RT_ERR_NO_DEVICE = -3, /* no usable CUDA device */
+    RT_ERR_NOMEM = -4,     /* device or pinned allocation failed */
+    RT_ERR_LIMIT = -5      /* beyond a compiled limit (e.g. bounce_limit > 31, renderer.py:36) */
+};
+
+/* Arithmetic of the render.
+ *  RT_PREC_FP32: the product path — FP32 CUDA cores, cancellation-free sphere
+ *                discriminant; within ±1 per 8-bit channel of the reference.
+ *  RT_PREC_FP64: validation path — float64 in the reference's literal
+ *                operation order, no FMA contraction; bit-identical frames
+ *                (golden sha256, pkg/tests/test_acceptance.py:31). */
+enum { RT_PREC_FP32 = 0, RT_PREC_FP64 = 1 };
+
+#define RT_MAX_BOUNCE_LIMIT 31   /* renderer.py:36 */
+#define RT_DEFAULT_BLOCK_ROWS 8  /* row-block height of the multi-GPU interleave */
+
+typedef struct rt_ctx rt_ctx;
+
+int rt_version(void);
+const char *rt_last_error(void);
+
+/* Number of visible CUDA devices (0 on a GPU-less host; never an error). */
+int rt_device_count(int32_t *count);
+
+/* Create a context over `n_devices` CUDA devices (NULL `devices` = 0..n-1).
+ * Each device gets one stream, scene buffers and a staging framebuffer. */
+int rt_ctx_create(rt_ctx **out, const int32_t *devices, int32_t n_devices);
+int rt_ctx_destroy(rt_ctx *ctx);
+
+/* Upload (or keep, when unchanged) the scene on every device of ctx.
+ * Mirrors renderer._scene_args (renderer.py:282-300). */
+int rt_set_scene_v1(rt_ctx *ctx, int32_t n_bodies, const int32_t *kinds, const double *positions,
+                    const double *sizes, const double *colors, const double *refls, const double light_pos[3],
+                    double light_radius, const double light_color[3], double ambient, double max_refl,
+                    const float *sky, int32_t sky_w, int32_t sky_h, int32_t has_sky);
+
+/* The drop-in frame render: replaces `_render_kernel(...)` (renderer.py:227-279).
+ * Same argument list and meaning, plus
+ *   radiance   NULL, or host float[w*h*3] (RT_PREC_FP32) / double[w*h*3]
+ *              (RT_PREC_FP64): pre-quantisation colour per pixel;
+ *   n_parts    row-block partitions (the reference's `workers`,
+ *              renderer.py:344-349), spread round-robin over ctx's devices;
+ *              the frame does not depend on it;
+ *   precision  RT_PREC_FP32 or RT_PREC_FP64.
+ * Synchronous: the frame is complete in `pixels` on return. */
+int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, int32_t height,
+                 const double cam_pos[3], double yaw, double pitch, double vdist, int32_t n_bodies,
+                 const int32_t *kinds, const double *positions, const double *sizes, const double *colors,
+                 const double *refls, const double light_pos[3], double light_radius, const double light_color[3],
+                 double ambient, double max_refl, const float *sky, int32_t sky_w, int32_t sky_h, int32_t has_sky,
+                 int32_t shadow_samples, int32_t bounce_limit, int32_t n_parts, int32_t precision);
+
+/* Device-resident render of one row-block partition with the scene last set
+ * by rt_set_scene_v1 on device slot `slot`.  Row y is rendered iff
+ * (y / block_rows) % n_parts == part; pixel (x, y) is stored at
+ * d_out[y * out_pitch + x] — d_out may be a peer GPU's framebuffer mapped
+ * through rt_ipc_open (the render then writes over NVLink, no gather pass).
+ * Asynchronous on `stream` (a cudaStream_t; NULL = the slot's own stream). */
+int rt_render_device_v1(rt_ctx *ctx, int32_t slot, uint32_t *d_out, int64_t out_pitch, void *d_radiance,
+                        int32_t width, int32_t height, const double cam_pos[3], double yaw, double pitch,
+                        double vdist, int32_t shadow_samples, int32_t bounce_limit, int32_t part, int32_t n_parts,
+                        int32_t block_rows, int32_t precision, void *stream);
+
+/* Batched `ray_trace_iterative` (renderer.py:303-313): out_rgb[i] is the
+ * pre-quantisation colour of ray (origins[i], dirs[i]); host buffers,
+ * float[n*3] (FP32) or double[n*3] (FP64).  Synchronous. */
+int rt_trace_rays_v1(rt_ctx *ctx, const double *origins, const double *dirs, int64_t n_rays, void *out_rgb,
+                     int32_t n_bodies, const int32_t *kinds, const double *positions, const double *sizes,
+                     const double *colors, const double *refls, const double light_pos[3], double light_radius,
+                     const double light_color[3], double ambient, double max_refl, const float *sky,
+                     int32_t sky_w, int32_t sky_h, int32_t has_sky, int32_t shadow_samples, int32_t bounce_limit,
+                     int32_t precision);
+
+/* `skybox_sample` (renderer.py:60-79) for a batch of unit directions, in
+ * float64 (bit-identical to the reference). Synchronous, host buffers. */
+int rt_sky_sample_v1(rt_ctx *ctx, const double *dirs, int64_t n, double *out_rgb, const float *sky, int32_t sky_w,
+                     int32_t sky_h);
+
+/* Page-lock a host framebuffer so the device→host copy of rt_render_v1 runs
+ * at PCIe speed.  The caller keeps the memory alive until unregistered. */
+int rt_host_register(rt_ctx *ctx, void *ptr, size_t bytes);
+int rt_host_unregister(rt_ctx *ctx, void *ptr);
+
+/* Device time (CUDA events) of the render kernels of the last rt_render_v1 /
+ * rt_trace_rays_v1 call on ctx's first device, in milliseconds. */
+int rt_last_kernel_ms(rt_ctx *ctx, float *ms);
+/* Number of kernels this ctx has launched so far. */
+int rt_launch_count(rt_ctx *ctx, int64_t *count);
+
+/* CUDA IPC for the one-process-per-GPU row-band gather: export a device
+ * allocation (64-byte handle), map a peer's allocation into this process. */
+int rt_ipc_get_handle(void *d_ptr, uint8_t handle_out[64]);
+int rt_ipc_open(const uint8_t handle[64], void **d_ptr_out);
+int rt_ipc_close(void *d_ptr);
+
+/* Synchronous device->host copy of `bytes` from d_src on `stream` (NULL = the
+ * slot's stream): rank 0 reads the gathered frame back. */
+int rt_copy_to_host(rt_ctx *ctx, int32_t slot, void *host_dst, const void *d_src, size_t bytes, void *stream);
+
+/* Plain device allocations (cudaMalloc) — IPC-exportable framebuffers. */
+int rt_device_malloc(int32_t device, size_t bytes, void **d_ptr_out);
+int rt_device_free(void *d_ptr);
+
+/* Measured FP32 roofline denominator: dependent-free FFMA throughput of
+ * `device` in TFLOP/s (2 FLOP per FFMA). */
+int rt_fp32_peak_tflops(int32_t device, double *tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200RT_H */

@@ -25,6 +25,17 @@
 
 typedef struct { double x, y, z; } v3;
 
+/* Work counting build (-DRTO_COUNT, librt_oracle_count.so): tallies the
+ * reference's control flow for the roofline numerators. */
+enum { C_PIX, C_CH_RAYS, C_SH_RAYS, C_HITS, C_REFL, C_SHADE, C_CH_TCA, C_CH_DISC, C_CH_FULL, C_CH_PLANE,
+       C_SH_TCA, C_SH_DISC, C_SH_FULL, C_SH_PLANE, C_MISS, C_NCOUNT };
+#ifdef RTO_COUNT
+static _Thread_local long long *g_cnt;
+#define CNT(k) (g_cnt[k]++)
+#else
+#define CNT(k) ((void)0)
+#endif
+
 /* constants: renderer.py:33,36; shading.py:23-29; geometry.py:24 */
 #define REFLECT_EPS 1e-3
 #define SHADOW_EPS 1e-3
@@ -99,13 +110,14 @@ typedef struct {
 } scene_t;
 
 /* geometry.py:83-105 — geometric test, literal d2 = L.L - tca^2 */
-static inline double ray_sphere(v3 o, v3 d, v3 c, double r) {
+static inline double ray_sphere(v3 o, v3 d, v3 c, double r, int sh) {
     double lx = c.x - o.x, ly = c.y - o.y, lz = c.z - o.z;
     double tca = lx * d.x + ly * d.y + lz * d.z;
-    if (tca < 0.0) return INFINITY;
+    if (tca < 0.0) { CNT(sh ? C_SH_TCA : C_CH_TCA); return INFINITY; }
     double d2 = lx * lx + ly * ly + lz * lz - tca * tca;
     double rad = r * r - d2;
-    if (rad < -GRAZE_EPS) return INFINITY;
+    if (rad < -GRAZE_EPS) { CNT(sh ? C_SH_DISC : C_CH_DISC); return INFINITY; }
+    CNT(sh ? C_SH_FULL : C_CH_FULL);
     if (rad < 0.0) rad = 0.0;
     double t = tca - sqrt(rad);
     if (t < 0.0) return INFINITY;
@@ -113,7 +125,8 @@ static inline double ray_sphere(v3 o, v3 d, v3 c, double r) {
 }
 
 /* geometry.py:108-117 */
-static inline double ray_plane(v3 o, v3 d, double h) {
+static inline double ray_plane(v3 o, v3 d, double h, int sh) {
+    CNT(sh ? C_SH_PLANE : C_CH_PLANE);
     double dy = d.y;
     if (dy == 0.0) return INFINITY;
     double t = (h - o.y) / dy;
@@ -122,9 +135,10 @@ static inline double ray_plane(v3 o, v3 d, double h) {
 }
 
 /* geometry.py:179-188 */
-static inline double intersect(const scene_t *s, v3 o, v3 d, int i) {
-    if (s->kinds[i] == 0) return ray_sphere(o, d, mk(s->pos[3 * i], s->pos[3 * i + 1], s->pos[3 * i + 2]), s->size[i]);
-    return ray_plane(o, d, s->pos[3 * i + 1]);
+static inline double intersect(const scene_t *s, v3 o, v3 d, int i, int sh) {
+    if (s->kinds[i] == 0)
+        return ray_sphere(o, d, mk(s->pos[3 * i], s->pos[3 * i + 1], s->pos[3 * i + 2]), s->size[i], sh);
+    return ray_plane(o, d, s->pos[3 * i + 1], sh);
 }
 
 /* geometry.py:191-201 — strict '<': lowest index wins ties */
@@ -132,7 +146,7 @@ static inline int closest_hit(const scene_t *s, v3 o, v3 d, double *t_out) {
     double best_t = INFINITY;
     int best_i = -1;
     for (int i = 0; i < s->n; i++) {
-        double t = intersect(s, o, d, i);
+        double t = intersect(s, o, d, i, 0);
         if (t < best_t) { best_t = t; best_i = i; }
     }
     *t_out = best_t;
@@ -142,7 +156,7 @@ static inline int closest_hit(const scene_t *s, v3 o, v3 d, double *t_out) {
 /* geometry.py:204-210 */
 static inline int occluded(const scene_t *s, v3 o, v3 d, double limit) {
     for (int i = 0; i < s->n; i++)
-        if (intersect(s, o, d, i) < limit) return 1;
+        if (intersect(s, o, d, i, 1) < limit) return 1;
     return 0;
 }
 
@@ -182,6 +196,7 @@ static double shadow_coeff(const scene_t *s, v3 surface, v3 normal) {
         v3 sp = (n == 1) ? s->light_pos : disc_point(i, n, s->light_pos, s->light_radius, bu, bv, s->ga);
         v3 dir = vnormalize(vsub(sp, origin));
         double limit = vdistance(surface, sp);
+        CNT(C_SH_RAYS);
         if (!occluded(s, origin, dir, limit)) unblocked += 1;
     }
     return (double)unblocked / (double)n;
@@ -208,6 +223,7 @@ static inline double clamp01(double x) {
 
 /* shading.py:144-168 */
 static inline v3 shade_color(v3 base, v3 n, v3 view, double sc, v3 l, double refl, v3 lc, double ambient) {
+    CNT(C_SHADE);
     double d = diffuse_factor(n, l);
     double sp = specular_blinn(n, l, view, refl);
     double lum = ambient + sc * d * (1.0 - ambient);
@@ -244,11 +260,14 @@ static v3 trace(const scene_t *s, v3 origin, v3 dir) {
     v3 tail = mk(0.0, 0.0, 0.0);
     for (int k = 0; k < s->bounces + 1; k++) {
         double t;
+        CNT(C_CH_RAYS);
         int idx = closest_hit(s, origin, dir, &t);
         if (idx < 0) {
+            CNT(C_MISS);
             if (s->has_sky) tail = sky_sample(s, dir);
             break;
         }
+        CNT(C_HITS);
         v3 hit = mk(origin.x + dir.x * t, origin.y + dir.y * t, origin.z + dir.z * t);
         v3 normal;
         if (s->kinds[idx] == 0)
@@ -267,6 +286,7 @@ static v3 trace(const scene_t *s, v3 origin, v3 dir) {
         r->sc = sc;
         r->refl = s->refl[idx];
         if (k == s->bounces) { exhausted = 1; break; }
+        CNT(C_REFL);
         origin = mk(hit.x + REFLECT_EPS * normal.x, hit.y + REFLECT_EPS * normal.y, hit.z + REFLECT_EPS * normal.z);
         dir = vreflect(dir, normal);
     }
@@ -352,6 +372,7 @@ int rto_render(uint32_t *pixels, double *radiance, int w, int h, const double *c
         int y = row0 + ri * row_step;
         for (int x = 0; x < w; x++) {
             v3 d = primary_direction((double)x, (double)y, (double)w, (double)h, cb, sb, ca, sa, vdist);
+            CNT(C_PIX);
             v3 c = trace(&s, cam, d);
             size_t idx = (size_t)x + (size_t)y * (size_t)w;
             pixels[idx] = pack_color(c);
@@ -434,3 +455,46 @@ int rto_max_threads(void) {
     return 1;
 #endif
 }
+
+#ifdef RTO_COUNT
+/* Work tallies of rto_render over rows row0, row0+row_step, ... (single
+ * thread per row, summed): out[C_NCOUNT] in the enum order above. */
+int rto_count_work(long long *out, int w, int h, const double *cam_pos, double yaw, double pitch, double vdist,
+                   int n_bodies, const int32_t *kinds, const double *positions, const double *sizes,
+                   const double *colors, const double *refls, const double *light_pos, double light_radius,
+                   const double *light_color, double ambient, double max_refl, const float *sky, int sky_w,
+                   int sky_h, int has_sky, int samples, int bounces, int row0, int row_step, int nthreads) {
+    scene_t s;
+    fill_scene(&s, n_bodies, kinds, positions, sizes, colors, refls, light_pos, light_radius, light_color, ambient,
+               max_refl, sky, sky_w, sky_h, has_sky, samples, bounces);
+    double cb = cos(pitch), sb = sin(pitch), ca = cos(yaw), sa = sin(yaw);
+    v3 cam = mk(cam_pos[0], cam_pos[1], cam_pos[2]);
+    int nrows = row0 < h ? (h - 1 - row0) / row_step + 1 : 0;
+    memset(out, 0, sizeof(long long) * C_NCOUNT);
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel
+#endif
+    {
+        long long local[C_NCOUNT];
+        memset(local, 0, sizeof local);
+        g_cnt = local;
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 1)
+#endif
+        for (int ri = 0; ri < nrows; ri++) {
+            int y = row0 + ri * row_step;
+            for (int x = 0; x < w; x++) {
+                CNT(C_PIX);
+                v3 d = primary_direction((double)x, (double)y, (double)w, (double)h, cb, sb, ca, sa, vdist);
+                (void)trace(&s, cam, d);
+            }
+        }
+#ifdef _OPENMP
+#pragma omp critical
+#endif
+        for (int k = 0; k < C_NCOUNT; k++) out[k] += local[k];
+    }
+    return 0;
+}
+#endif

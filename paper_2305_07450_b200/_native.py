@@ -1,0 +1,196 @@
+"""ctypes binding of libb200rt.so (the C ABI declared in include/b200rt.h).
+
+There is no CPU fallback: if the library is missing, or no CUDA device is
+visible, every compute call raises.  ctypes.CDLL releases the GIL for the
+duration of each call, like the reference's nogil=True kernel
+(/root/reference/pkg/src/raytracer/renderer.py:227).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libb200rt.so")
+
+RT_OK = 0
+RT_ERR_INVALID = -1
+RT_ERR_CUDA = -2
+RT_ERR_NO_DEVICE = -3
+RT_ERR_NOMEM = -4
+RT_ERR_LIMIT = -5
+RT_PREC_FP32 = 0
+RT_PREC_FP64 = 1
+PRECISIONS = {"fp32": RT_PREC_FP32, "fp64": RT_PREC_FP64}
+
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_d = ctypes.c_double
+_p = ctypes.c_void_p
+
+# name -> (restype, argtypes); the exact export list of include/b200rt.h
+SIGNATURES = {
+    "rt_version": (ctypes.c_int, []),
+    "rt_last_error": (ctypes.c_char_p, []),
+    "rt_device_count": (ctypes.c_int, [_p]),
+    "rt_ctx_create": (ctypes.c_int, [_p, _p, _i32]),
+    "rt_ctx_destroy": (ctypes.c_int, [_p]),
+    "rt_set_scene_v1": (ctypes.c_int, [_p, _i32, _p, _p, _p, _p, _p, _p, _d, _p, _d, _d, _p, _i32, _i32, _i32]),
+    "rt_render_v1": (ctypes.c_int, [_p, _p, _p, _i32, _i32, _p, _d, _d, _d, _i32, _p, _p, _p, _p, _p, _p, _d, _p,
+                                    _d, _d, _p, _i32, _i32, _i32, _i32, _i32, _i32, _i32]),
+    "rt_render_device_v1": (ctypes.c_int, [_p, _i32, _p, _i64, _p, _i32, _i32, _p, _d, _d, _d, _i32, _i32, _i32,
+                                           _i32, _i32, _i32, _p]),
+    "rt_trace_rays_v1": (ctypes.c_int, [_p, _p, _p, _i64, _p, _i32, _p, _p, _p, _p, _p, _p, _d, _p, _d, _d, _p,
+                                        _i32, _i32, _i32, _i32, _i32, _i32]),
+    "rt_sky_sample_v1": (ctypes.c_int, [_p, _p, _i64, _p, _p, _i32, _i32]),
+    "rt_host_register": (ctypes.c_int, [_p, _p, ctypes.c_size_t]),
+    "rt_host_unregister": (ctypes.c_int, [_p, _p]),
+    "rt_last_kernel_ms": (ctypes.c_int, [_p, _p]),
+    "rt_launch_count": (ctypes.c_int, [_p, _p]),
+    "rt_ipc_get_handle": (ctypes.c_int, [_p, _p]),
+    "rt_ipc_open": (ctypes.c_int, [_p, _p]),
+    "rt_ipc_close": (ctypes.c_int, [_p]),
+    "rt_copy_to_host": (ctypes.c_int, [_p, _i32, _p, _p, ctypes.c_size_t, _p]),
+    "rt_device_malloc": (ctypes.c_int, [_i32, ctypes.c_size_t, _p]),
+    "rt_device_free": (ctypes.c_int, [_p]),
+    "rt_fp32_peak_tflops": (ctypes.c_int, [_i32, _p]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class NativeError(RuntimeError):
+    """A CUDA-side failure reported by libb200rt."""
+
+
+def load():
+    """Load libb200rt.so (in-tree); raise if it is not built."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(
+                    f"{LIB_PATH} is not built: run `python -m paper_2305_07450_b200.build` "
+                    "(there is no CPU fallback for the frame render)"
+                )
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def last_error() -> str:
+    return (load().rt_last_error() or b"").decode(errors="replace")
+
+
+def check(rc: int, what: str):
+    if rc == RT_OK:
+        return
+    msg = f"{what}: {last_error()}"
+    if rc in (RT_ERR_INVALID, RT_ERR_LIMIT):
+        raise ValueError(msg)
+    raise NativeError(msg)
+
+
+def ptr(a) -> ctypes.c_void_p | None:
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return ctypes.c_void_p(a.ctypes.data)
+    return ctypes.c_void_p(int(a))
+
+
+def device_count() -> int:
+    n = _i32(0)
+    check(load().rt_device_count(ctypes.byref(n)), "rt_device_count")
+    return n.value
+
+
+class Context:
+    """One rt_ctx: a stream, scene cache and staging framebuffer per device."""
+
+    def __init__(self, devices=(0,)):
+        self.devices = tuple(int(d) for d in devices)
+        lib = load()
+        h = ctypes.c_void_p()
+        arr = (_i32 * len(self.devices))(*self.devices)
+        check(lib.rt_ctx_create(ctypes.byref(h), arr, len(self.devices)), "rt_ctx_create")
+        self.handle = h
+        self._registered = {}  # id(array) -> array (kept alive while pinned)
+        self._reg_order = []
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib = load()
+            for a in list(self._registered.values()):
+                lib.rt_host_unregister(self.handle, ptr(a))
+            self._registered.clear()
+            lib.rt_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- pinned host framebuffers ------------------------------------------------
+    def pin(self, arr: np.ndarray, max_pinned: int = 4) -> bool:
+        """Page-lock `arr` (kept alive while pinned) so the frame copy runs at
+        PCIe speed; the oldest pinned buffer is released beyond `max_pinned`."""
+        key = id(arr)
+        if key in self._registered and self._registered[key] is arr:
+            return True
+        lib = load()
+        if lib.rt_host_register(self.handle, ptr(arr), arr.nbytes) != RT_OK:
+            return False
+        self._registered[key] = arr
+        self._reg_order.append(key)
+        while len(self._reg_order) > max_pinned:
+            old = self._reg_order.pop(0)
+            a = self._registered.pop(old, None)
+            if a is not None:
+                lib.rt_host_unregister(self.handle, ptr(a))
+        return True
+
+    def last_kernel_ms(self) -> float:
+        v = ctypes.c_float(0)
+        check(load().rt_last_kernel_ms(self.handle, ctypes.byref(v)), "rt_last_kernel_ms")
+        return float(v.value)
+
+    def launch_count(self) -> int:
+        v = _i64(0)
+        check(load().rt_launch_count(self.handle, ctypes.byref(v)), "rt_launch_count")
+        return int(v.value)
+
+
+_contexts = {}
+_ctx_lock = threading.Lock()
+
+
+def context(n_devices: int = 1) -> Context:
+    """Process-wide context over devices 0..n-1 (clamped to what is visible)."""
+    n_vis = device_count()
+    if n_vis < 1:
+        raise NativeError("no CUDA device visible: the b200rt frame render has no CPU path")
+    n = max(1, min(int(n_devices), n_vis))
+    with _ctx_lock:
+        ctx = _contexts.get(n)
+        if ctx is None:
+            ctx = Context(tuple(range(n)))
+            _contexts[n] = ctx
+        return ctx
+
+
+def fp32_peak_tflops(device: int = 0) -> float:
+    v = _d(0)
+    check(load().rt_fp32_peak_tflops(int(device), ctypes.byref(v)), "rt_fp32_peak_tflops")
+    return float(v.value)

@@ -1,0 +1,92 @@
+// Device-side shared definitions of the b200rt frame render (sm_100a).
+//
+// Layout in HBM (per device, per precision R = float | double):
+//   geo   R[n][4]   {cx, cy, cz, r^2} for spheres, {0, h, 0, -1} for planes
+//                   (a negative 4th lane marks the horizontal plane); read by
+//                   every closest-hit and shadow test, staged into shared
+//                   memory per CTA so warp-uniform body loops are broadcasts.
+//   mat   R[n][8]   {r, g, b, refl / max_refl, refl, 0, 0, 0}; read only at hits.
+//   table R[s][2]   sunflower disc offsets r_i (cos th_i, sin th_i)
+//                   (shading.py:89-100), computed on the host in float64 with
+//                   the same libm as the reference — a closed-form per-sample
+//                   table, there is no RNG in the reference.
+//   sky   float4[H][W]  texels pre-clamped to [0,1] (renderer.py:74), RGB + pad.
+//   out   uint32 framebuffer, pixel (x, y) at out[y * out_pitch + x].
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rt {
+
+constexpr int kMaxBounce = 31;  // renderer.py:36
+constexpr int kTileW = 16;      // CTA tile: 16 x 8 pixels, 4 warps of 8 x 4
+constexpr int kTileH = 8;
+constexpr int kThreads = 128;
+constexpr int kSmemGeoBytes = 32 * 1024;  // scenes up to this size are staged in shared memory
+
+// Camera + frame + partition (one launch renders one row-block partition).
+struct FrameArgs {
+    uint32_t *out;
+    int64_t out_pitch;
+    void *radiance;  // optional R[height*width*3], full-frame indexing y*width + x
+    int width, height;
+    int part, n_parts, block_rows;
+    int local_rows;  // rows of this partition, rounded up to whole blocks
+    double cam[3];
+    double cb, sb, ca, sa;  // cos/sin(pitch), cos/sin(yaw) (host libm, vecmath.py:99-110)
+    double vdist;           // camera.py:64-67
+    int samples, bounces;
+    int peer_out;  // out lives on another GPU: fence the stores at system scope
+};
+
+template <typename R>
+struct SceneArgs {
+    const R *geo;
+    const R *mat;
+    const R *table;
+    const float4 *sky;
+    int sky_w, sky_h, has_sky;
+    int n;
+    R light[3];
+    R light_radius;
+    R lc[3];
+    R ambient;
+};
+
+// Row-block interleave: local row ly of partition `part` -> frame row.
+__device__ __forceinline__ int map_row(int ly, const FrameArgs &a) {
+    if (a.n_parts == 1) return ly;
+    int jl = ly / a.block_rows;
+    int r = ly - jl * a.block_rows;
+    return (jl * a.n_parts + a.part) * a.block_rows + r;
+}
+
+// Thread -> pixel: each warp shades an 8 x 4 pixel patch (coherent rays),
+// the CTA a 16 x 8 tile.
+__device__ __forceinline__ void thread_pixel(int &x, int &ly) {
+    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    x = blockIdx.x * kTileW + (warp & 1) * 8 + (lane & 7);
+    ly = blockIdx.y * kTileH + (warp >> 1) * 4 + (lane >> 3);
+}
+
+// renderer.py:45-50
+template <typename R>
+__device__ __forceinline__ uint32_t pack_color(R r, R g, R b) {
+    uint32_t ri = (uint32_t)(int)(r * R(255.0) + R(0.5));
+    uint32_t gi = (uint32_t)(int)(g * R(255.0) + R(0.5));
+    uint32_t bi = (uint32_t)(int)(b * R(255.0) + R(0.5));
+    return 0xFF000000u | (ri << 16) | (gi << 8) | bi;
+}
+
+}  // namespace rt
+
+// Launchers (one translation unit per precision; the FP64 one is compiled
+// with -fmad=false so no a*b+c is contracted, as numba compiles the reference).
+cudaError_t rt_launch_render_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, cudaStream_t st);
+cudaError_t rt_launch_render_f64(const rt::FrameArgs &fa, const rt::SceneArgs<double> &sa, cudaStream_t st);
+cudaError_t rt_launch_trace_f32(const double *d_orig, const double *d_dir, int64_t n, float *d_out,
+                                const rt::SceneArgs<float> &sa, int samples, int bounces, cudaStream_t st);
+cudaError_t rt_launch_trace_f64(const double *d_orig, const double *d_dir, int64_t n, double *d_out,
+                                const rt::SceneArgs<double> &sa, int samples, int bounces, cudaStream_t st);
+cudaError_t rt_launch_sky_f64(const double *d_dir, int64_t n, double *d_out, const float4 *sky, int w, int h,
+                              cudaStream_t st);

@@ -1,0 +1,772 @@
+// Host side of libb200rt: the C ABI of include/b200rt.h.
+//
+// Per-device context (stream, events, scene buffers, staging framebuffer),
+// scene upload with change detection (the paper streams only per-frame state,
+// PAPER.md:562-564), row-block partitioning over devices, and the copy of the
+// finished frame into the caller's host framebuffer.  No pixel is ever
+// computed here: every compute entry point launches a CUDA kernel or fails.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "b200rt.h"
+#include "rt_device.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+#define RT_CK(call)                                                                                        \
+    do {                                                                                                   \
+        cudaError_t e_ = (call);                                                                           \
+        if (e_ != cudaSuccess) return fail(RT_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+struct DBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    int ensure(size_t bytes) {
+        if (bytes <= cap && p) return RT_OK;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        if (bytes == 0) bytes = 16;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            return fail(RT_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        }
+        cap = bytes;
+        return RT_OK;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+// Host-side canonical scene (float64, the reference's packed layout).
+struct HostScene {
+    int n = 0;
+    std::vector<double> geo;  // [n][4] {cx, cy, cz, r^2} / {0, h, 0, -1}
+    std::vector<double> mat;  // [n][8] {r, g, b, refl/max_refl, refl, 0, 0, 0}
+    double light[3] = {0, 0, 0}, light_radius = 1, lc[3] = {1, 1, 1}, ambient = 0.15, max_refl = 128;
+    std::vector<char> key;  // bytes compared to detect a changed scene
+    uint64_t version = 0;
+    // skybox identity
+    const float *sky_ptr = nullptr;
+    int sky_w = 1, sky_h = 1, has_sky = 0;
+    uint64_t sky_sig = 0;
+    uint64_t sky_version = 0;
+};
+
+template <typename R>
+struct DevScene {
+    DBuf geo, mat, table;
+    uint64_t version = ~0ull;
+    int table_n = -1;
+    double table_radius = NAN;
+};
+
+struct Dev {
+    int id = 0;
+    cudaStream_t st = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    DBuf frame, rad, rays_in, rays_out, sky_raw, sky;
+    uint64_t sky_version = ~0ull;
+    DevScene<float> s32;
+    DevScene<double> s64;
+};
+
+// renderer.py:60-74 clamp, applied once per texel at upload: RGB -> float4.
+__global__ void sky_to_float4(const float *raw, float4 *out, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float r = raw[3 * i], g = raw[3 * i + 1], b = raw[3 * i + 2];
+    // min(max(c, 0), 1) keeps NaN out of the [0,1] range test like Python's min/max
+    r = (0.f > r) ? 0.f : r;
+    g = (0.f > g) ? 0.f : g;
+    b = (0.f > b) ? 0.f : b;
+    r = (1.f < r) ? 1.f : r;
+    g = (1.f < g) ? 1.f : g;
+    b = (1.f < b) ? 1.f : b;
+    out[i] = make_float4(r, g, b, 0.f);
+}
+
+// Dependent-free FFMA stream: the measured FP32 roofline denominator.
+__global__ void ffma_peak_kernel(float *sink, int iters, float a, float b) {
+    float x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6,
+          x7 = x0 + 7;
+    for (int i = 0; i < iters; i++) {
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            x0 = fmaf(x0, a, b);
+            x1 = fmaf(x1, a, b);
+            x2 = fmaf(x2, a, b);
+            x3 = fmaf(x3, a, b);
+            x4 = fmaf(x4, a, b);
+            x5 = fmaf(x5, a, b);
+            x6 = fmaf(x6, a, b);
+            x7 = fmaf(x7, a, b);
+        }
+    }
+    float s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (s == 1234.5f) sink[threadIdx.x] = s;
+}
+
+}  // namespace
+
+struct rt_ctx {
+    std::vector<Dev> devs;
+    std::mutex mu;
+    HostScene scene;
+    float last_ms = 0.f;
+    int64_t launches = 0;
+};
+
+namespace {
+
+double golden_angle() { return M_PI * (3.0 - std::sqrt(5.0)); }  // shading.py:29
+
+// shading.py:89-100: (r_i cos th_i, r_i sin th_i) in float64 with the host libm.
+std::vector<double> disc_table(int n, double radius) {
+    std::vector<double> t(2 * (size_t)n);
+    double ga = golden_angle();
+    for (int i = 0; i < n; i++) {
+        double r = 2.0 * radius * std::sqrt((double)i / (double)n);
+        double theta = (double)i * ga;
+        t[2 * i] = r * std::cos(theta);
+        t[2 * i + 1] = r * std::sin(theta);
+    }
+    return t;
+}
+
+uint64_t fnv1a(const void *data, size_t n, uint64_t h = 1469598103934665603ull) {
+    const unsigned char *p = (const unsigned char *)data;
+    for (size_t i = 0; i < n; i++) h = (h ^ p[i]) * 1099511628211ull;
+    return h;
+}
+
+// Cheap identity of a skybox: dimensions, first/last rows and a strided
+// sample of texels (a full hash of a 25 MB panorama would cost ~10 ms/frame).
+uint64_t sky_signature(const float *sky, int w, int h) {
+    size_t n = (size_t)w * h * 3;
+    uint64_t s = fnv1a(&w, sizeof w);
+    s = fnv1a(&h, sizeof h, s);
+    size_t row = (size_t)w * 3;
+    s = fnv1a(sky, sizeof(float) * std::min(row, n), s);
+    s = fnv1a(sky + (n - std::min(row, n)), sizeof(float) * std::min(row, n), s);
+    size_t stride = std::max<size_t>(1, n / 4099);
+    for (size_t i = 0; i < n; i += stride) s = fnv1a(sky + i, sizeof(float), s);
+    return s;
+}
+
+int validate_scene(int32_t n_bodies, const int32_t *kinds, const double *positions, const double *sizes,
+                   const double *colors, const double *refls, const double *light_pos, const double *light_color,
+                   double max_refl, const float *sky, int32_t sky_w, int32_t sky_h, int32_t has_sky) {
+    if (n_bodies < 0) return fail(RT_ERR_INVALID, "n_bodies must be >= 0");
+    if (n_bodies > 0 && (!kinds || !positions || !sizes || !colors || !refls))
+        return fail(RT_ERR_INVALID, "null scene array");
+    if (!light_pos || !light_color) return fail(RT_ERR_INVALID, "null light array");
+    if (!(max_refl > 0)) return fail(RT_ERR_INVALID, "max reflectivity must be positive");
+    for (int i = 0; i < n_bodies; i++) {
+        if (kinds[i] != 0 && kinds[i] != 1) return fail(RT_ERR_INVALID, "body kind must be 0 (sphere) or 1 (plane)");
+        if (kinds[i] == 0 && !(sizes[i] > 0)) return fail(RT_ERR_INVALID, "sphere radius must be positive");
+    }
+    if (has_sky && (!sky || sky_w < 1 || sky_h < 1)) return fail(RT_ERR_INVALID, "bad skybox");
+    return RT_OK;
+}
+
+void set_host_scene(HostScene &s, int32_t n, const int32_t *kinds, const double *positions, const double *sizes,
+                    const double *colors, const double *refls, const double *light_pos, double light_radius,
+                    const double *light_color, double ambient, double max_refl, const float *sky, int32_t sky_w,
+                    int32_t sky_h, int32_t has_sky) {
+    std::vector<char> key;
+    auto put = [&key](const void *p, size_t b) {
+        const char *c = (const char *)p;
+        key.insert(key.end(), c, c + b);
+    };
+    put(&n, sizeof n);
+    if (n > 0) {
+        put(kinds, sizeof(int32_t) * n);
+        put(positions, sizeof(double) * 3 * n);
+        put(sizes, sizeof(double) * n);
+        put(colors, sizeof(double) * 3 * n);
+        put(refls, sizeof(double) * n);
+    }
+    put(light_pos, sizeof(double) * 3);
+    put(&light_radius, sizeof light_radius);
+    put(light_color, sizeof(double) * 3);
+    put(&ambient, sizeof ambient);
+    put(&max_refl, sizeof max_refl);
+    if (key != s.key) {
+        s.key.swap(key);
+        s.n = n;
+        s.geo.assign(4 * (size_t)n, 0.0);
+        s.mat.assign(8 * (size_t)n, 0.0);
+        for (int i = 0; i < n; i++) {
+            if (kinds[i] == 0) {
+                s.geo[4 * i] = positions[3 * i];
+                s.geo[4 * i + 1] = positions[3 * i + 1];
+                s.geo[4 * i + 2] = positions[3 * i + 2];
+                s.geo[4 * i + 3] = sizes[i] * sizes[i];  // geometry.py:97 radius * radius
+            } else {
+                s.geo[4 * i + 1] = positions[3 * i + 1];  // plane height = position.y (geometry.py:58-60)
+                s.geo[4 * i + 3] = -1.0;
+            }
+            s.mat[8 * i] = colors[3 * i];
+            s.mat[8 * i + 1] = colors[3 * i + 1];
+            s.mat[8 * i + 2] = colors[3 * i + 2];
+            s.mat[8 * i + 3] = refls[i] / max_refl;  // renderer.py:161
+            s.mat[8 * i + 4] = refls[i];
+        }
+        for (int c = 0; c < 3; c++) {
+            s.light[c] = light_pos[c];
+            s.lc[c] = light_color[c];
+        }
+        s.light_radius = light_radius;
+        s.ambient = ambient;
+        s.max_refl = max_refl;
+        s.version++;
+    }
+    uint64_t sig = has_sky ? sky_signature(sky, sky_w, sky_h) : 0;
+    if (has_sky != s.has_sky || sky != s.sky_ptr || sky_w != s.sky_w || sky_h != s.sky_h || sig != s.sky_sig) {
+        s.has_sky = has_sky;
+        s.sky_ptr = has_sky ? sky : nullptr;
+        s.sky_w = has_sky ? sky_w : 1;
+        s.sky_h = has_sky ? sky_h : 1;
+        s.sky_sig = sig;
+        s.sky_version++;
+    }
+}
+
+template <typename R>
+int upload_prec(Dev &d, DevScene<R> &ds, const HostScene &s, int samples) {
+    if (ds.version != s.version) {
+        std::vector<R> geo(s.geo.begin(), s.geo.end()), mat(s.mat.begin(), s.mat.end());
+        int rc;
+        if ((rc = ds.geo.ensure(sizeof(R) * geo.size())) || (rc = ds.mat.ensure(sizeof(R) * mat.size()))) return rc;
+        if (!geo.empty()) {
+            RT_CK(cudaMemcpyAsync(ds.geo.p, geo.data(), sizeof(R) * geo.size(), cudaMemcpyHostToDevice, d.st));
+            RT_CK(cudaMemcpyAsync(ds.mat.p, mat.data(), sizeof(R) * mat.size(), cudaMemcpyHostToDevice, d.st));
+        }
+        RT_CK(cudaStreamSynchronize(d.st));  // host vectors die at scope exit
+        ds.version = s.version;
+    }
+    if (samples > 1 && (ds.table_n != samples || !(ds.table_radius == s.light_radius))) {
+        std::vector<double> t64 = disc_table(samples, s.light_radius);
+        std::vector<R> t(t64.begin(), t64.end());
+        int rc = ds.table.ensure(sizeof(R) * t.size());
+        if (rc) return rc;
+        RT_CK(cudaMemcpyAsync(ds.table.p, t.data(), sizeof(R) * t.size(), cudaMemcpyHostToDevice, d.st));
+        RT_CK(cudaStreamSynchronize(d.st));
+        ds.table_n = samples;
+        ds.table_radius = s.light_radius;
+    }
+    return RT_OK;
+}
+
+int upload_sky(rt_ctx *ctx, Dev &d) {
+    const HostScene &s = ctx->scene;
+    if (d.sky_version == s.sky_version) return RT_OK;
+    int rc;
+    if (s.has_sky) {
+        int64_t n = (int64_t)s.sky_w * s.sky_h;
+        if ((rc = d.sky_raw.ensure(sizeof(float) * 3 * n)) || (rc = d.sky.ensure(sizeof(float4) * n))) return rc;
+        RT_CK(cudaMemcpyAsync(d.sky_raw.p, s.sky_ptr, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, d.st));
+        sky_to_float4<<<(unsigned)((n + 255) / 256), 256, 0, d.st>>>((const float *)d.sky_raw.p, (float4 *)d.sky.p,
+                                                                   n);
+        RT_CK(cudaGetLastError());
+        ctx->launches++;
+        RT_CK(cudaStreamSynchronize(d.st));
+        d.sky_raw.release();
+    } else {
+        if ((rc = d.sky.ensure(sizeof(float4)))) return rc;
+        RT_CK(cudaMemsetAsync(d.sky.p, 0, sizeof(float4), d.st));
+    }
+    d.sky_version = s.sky_version;
+    return RT_OK;
+}
+
+template <typename R>
+rt::SceneArgs<R> scene_args(const Dev &d, const DevScene<R> &ds, const HostScene &s) {
+    rt::SceneArgs<R> a;
+    a.geo = (const R *)ds.geo.p;
+    a.mat = (const R *)ds.mat.p;
+    a.table = (const R *)ds.table.p;
+    a.sky = (const float4 *)d.sky.p;
+    a.sky_w = s.sky_w;
+    a.sky_h = s.sky_h;
+    a.has_sky = s.has_sky;
+    a.n = s.n;
+    for (int c = 0; c < 3; c++) {
+        a.light[c] = (R)s.light[c];
+        a.lc[c] = (R)s.lc[c];
+    }
+    a.light_radius = (R)s.light_radius;
+    a.ambient = (R)s.ambient;
+    return a;
+}
+
+int prepare(rt_ctx *ctx, Dev &d, int precision, int samples) {
+    int rc;
+    RT_CK(cudaSetDevice(d.id));
+    if ((rc = upload_sky(ctx, d))) return rc;
+    if (precision == RT_PREC_FP64) return upload_prec(d, d.s64, ctx->scene, samples);
+    return upload_prec(d, d.s32, ctx->scene, samples);
+}
+
+// Rows of partition `part`, rounded up to whole blocks (the kernel skips rows
+// past the frame).
+int local_rows(int height, int part, int n_parts, int block_rows) {
+    if (n_parts == 1) return height;
+    int n_blocks = (height + block_rows - 1) / block_rows;
+    int mine = n_blocks > part ? (n_blocks - part + n_parts - 1) / n_parts : 0;
+    return mine * block_rows;
+}
+
+rt::FrameArgs frame_args(uint32_t *out, int64_t pitch, void *rad, int w, int h, const double *cam, double yaw,
+                         double pitch_angle, double vdist, int samples, int bounces, int part, int n_parts,
+                         int block_rows) {
+    rt::FrameArgs fa;
+    fa.out = out;
+    fa.out_pitch = pitch;
+    fa.radiance = rad;
+    fa.width = w;
+    fa.height = h;
+    fa.part = part;
+    fa.n_parts = n_parts;
+    fa.block_rows = block_rows;
+    fa.local_rows = local_rows(h, part, n_parts, block_rows);
+    for (int c = 0; c < 3; c++) fa.cam[c] = cam[c];
+    fa.cb = std::cos(pitch_angle);  // vecmath.py:101-106, host libm
+    fa.sb = std::sin(pitch_angle);
+    fa.ca = std::cos(yaw);
+    fa.sa = std::sin(yaw);
+    fa.vdist = vdist;
+    fa.samples = samples;
+    fa.bounces = bounces;
+    fa.peer_out = 0;
+    return fa;
+}
+
+int launch_frame(rt_ctx *ctx, Dev &d, const rt::FrameArgs &fa, int precision, cudaStream_t st) {
+    cudaError_t e;
+    if (fa.local_rows == 0) return RT_OK;
+    if (precision == RT_PREC_FP64)
+        e = rt_launch_render_f64(fa, scene_args(d, d.s64, ctx->scene), st);
+    else
+        e = rt_launch_render_f32(fa, scene_args(d, d.s32, ctx->scene), st);
+    if (e != cudaSuccess) return fail(RT_ERR_CUDA, std::string("render kernel launch: ") + cudaGetErrorString(e));
+    ctx->launches++;
+    return RT_OK;
+}
+
+int check_frame_args(int32_t w, int32_t h, int32_t samples, int32_t bounces, int32_t precision) {
+    if (w < 1 || h < 1) return fail(RT_ERR_INVALID, "frame dimensions must be positive");
+    if ((int64_t)w * h > (int64_t)1 << 31) return fail(RT_ERR_LIMIT, "frame too large");
+    if (samples < 1) return fail(RT_ERR_INVALID, "shadow sample count must be >= 1");
+    if (bounces < 0) return fail(RT_ERR_INVALID, "bounce limit must be >= 0");
+    if (bounces > RT_MAX_BOUNCE_LIMIT) return fail(RT_ERR_LIMIT, "bounce limit capped at 31");
+    if (precision != RT_PREC_FP32 && precision != RT_PREC_FP64) return fail(RT_ERR_INVALID, "bad precision");
+    return RT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rt_version(void) { return RT_ABI_VERSION; }
+
+const char *rt_last_error(void) { return g_err.c_str(); }
+
+int rt_device_count(int32_t *count) {
+    if (!count) return fail(RT_ERR_INVALID, "null count");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    *count = n;
+    return RT_OK;
+}
+
+int rt_ctx_create(rt_ctx **out, const int32_t *devices, int32_t n_devices) {
+    if (!out) return fail(RT_ERR_INVALID, "null ctx pointer");
+    *out = nullptr;
+    int avail = 0;
+    if (cudaGetDeviceCount(&avail) != cudaSuccess || avail == 0) {
+        cudaGetLastError();
+        return fail(RT_ERR_NO_DEVICE, "no CUDA device visible: libb200rt has no CPU path");
+    }
+    if (n_devices < 1) n_devices = 1;
+    rt_ctx *ctx = new rt_ctx();
+    for (int i = 0; i < n_devices; i++) {
+        int id = devices ? devices[i] : i;
+        if (id < 0 || id >= avail) {
+            rt_ctx_destroy(ctx);
+            return fail(RT_ERR_NO_DEVICE, "device index out of range");
+        }
+        Dev d;
+        d.id = id;
+        if (cudaSetDevice(id) != cudaSuccess || cudaStreamCreateWithFlags(&d.st, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreate(&d.e0) != cudaSuccess || cudaEventCreate(&d.e1) != cudaSuccess) {
+            std::string m = cudaGetErrorString(cudaGetLastError());
+            ctx->devs.push_back(d);
+            rt_ctx_destroy(ctx);
+            return fail(RT_ERR_CUDA, "device init: " + m);
+        }
+        ctx->devs.push_back(d);
+    }
+    *out = ctx;
+    return RT_OK;
+}
+
+int rt_ctx_destroy(rt_ctx *ctx) {
+    if (!ctx) return RT_OK;
+    for (Dev &d : ctx->devs) {
+        cudaSetDevice(d.id);
+        if (d.st) cudaStreamSynchronize(d.st);
+        for (DBuf *b : {&d.frame, &d.rad, &d.rays_in, &d.rays_out, &d.sky_raw, &d.sky, &d.s32.geo, &d.s32.mat,
+                        &d.s32.table, &d.s64.geo, &d.s64.mat, &d.s64.table})
+            b->release();
+        if (d.e0) cudaEventDestroy(d.e0);
+        if (d.e1) cudaEventDestroy(d.e1);
+        if (d.st) cudaStreamDestroy(d.st);
+    }
+    delete ctx;
+    return RT_OK;
+}
+
+int rt_set_scene_v1(rt_ctx *ctx, int32_t n_bodies, const int32_t *kinds, const double *positions,
+                    const double *sizes, const double *colors, const double *refls, const double light_pos[3],
+                    double light_radius, const double light_color[3], double ambient, double max_refl,
+                    const float *sky, int32_t sky_w, int32_t sky_h, int32_t has_sky) {
+    if (!ctx) return fail(RT_ERR_INVALID, "null ctx");
+    int rc = validate_scene(n_bodies, kinds, positions, sizes, colors, refls, light_pos, light_color, max_refl, sky,
+                            sky_w, sky_h, has_sky);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    set_host_scene(ctx->scene, n_bodies, kinds, positions, sizes, colors, refls, light_pos, light_radius, light_color,
+                   ambient, max_refl, sky, sky_w, sky_h, has_sky);
+    for (Dev &d : ctx->devs) {
+        RT_CK(cudaSetDevice(d.id));
+        if ((rc = upload_sky(ctx, d))) return rc;
+    }
+    return RT_OK;
+}
+
+int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, int32_t height,
+                 const double cam_pos[3], double yaw, double pitch, double vdist, int32_t n_bodies,
+                 const int32_t *kinds, const double *positions, const double *sizes, const double *colors,
+                 const double *refls, const double light_pos[3], double light_radius, const double light_color[3],
+                 double ambient, double max_refl, const float *sky, int32_t sky_w, int32_t sky_h, int32_t has_sky,
+                 int32_t shadow_samples, int32_t bounce_limit, int32_t n_parts, int32_t precision) {
+    if (!ctx || !pixels || !cam_pos) return fail(RT_ERR_INVALID, "null argument");
+    int rc = check_frame_args(width, height, shadow_samples, bounce_limit, precision);
+    if (rc) return rc;
+    if ((rc = validate_scene(n_bodies, kinds, positions, sizes, colors, refls, light_pos, light_color, max_refl, sky,
+                             sky_w, sky_h, has_sky)))
+        return rc;
+    if (n_parts < 1) n_parts = 1;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    set_host_scene(ctx->scene, n_bodies, kinds, positions, sizes, colors, refls, light_pos, light_radius, light_color,
+                   ambient, max_refl, sky, sky_w, sky_h, has_sky);
+    const int n_dev = std::min<int>((int)ctx->devs.size(), n_parts);
+    const int block_rows = RT_DEFAULT_BLOCK_ROWS;
+    const size_t px_bytes = sizeof(uint32_t) * (size_t)width * height;
+    const size_t rad_elem = precision == RT_PREC_FP64 ? sizeof(double) : sizeof(float);
+    const size_t rad_bytes = rad_elem * 3 * (size_t)width * height;
+    for (int g = 0; g < n_dev; g++) {
+        Dev &d = ctx->devs[g];
+        if ((rc = prepare(ctx, d, precision, shadow_samples))) return rc;
+        if ((rc = d.frame.ensure(px_bytes))) return rc;
+        if (radiance && (rc = d.rad.ensure(rad_bytes))) return rc;
+    }
+    // kernels: partition p runs on device p % n_dev
+    for (int g = 0; g < n_dev; g++) {
+        Dev &d = ctx->devs[g];
+        RT_CK(cudaSetDevice(d.id));
+        RT_CK(cudaEventRecord(d.e0, d.st));
+        for (int p = g; p < n_parts; p += n_dev) {
+            rt::FrameArgs fa = frame_args((uint32_t *)d.frame.p, width, radiance ? d.rad.p : nullptr, width, height,
+                                          cam_pos, yaw, pitch, vdist, shadow_samples, bounce_limit, p, n_parts,
+                                          block_rows);
+            if ((rc = launch_frame(ctx, d, fa, precision, d.st))) return rc;
+        }
+        RT_CK(cudaEventRecord(d.e1, d.st));
+    }
+    // copies: each device returns only its rows
+    for (int g = 0; g < n_dev; g++) {
+        Dev &d = ctx->devs[g];
+        RT_CK(cudaSetDevice(d.id));
+        if (n_dev == 1) {
+            RT_CK(cudaMemcpyAsync(pixels, d.frame.p, px_bytes, cudaMemcpyDeviceToHost, d.st));
+            if (radiance) RT_CK(cudaMemcpyAsync(radiance, d.rad.p, rad_bytes, cudaMemcpyDeviceToHost, d.st));
+            continue;
+        }
+        for (int p = g; p < n_parts; p += n_dev) {
+            int n_blocks = (height + block_rows - 1) / block_rows;
+            int full = 0;  // owned blocks that are complete
+            for (int j = p; j < n_blocks; j += n_parts)
+                if ((j + 1) * block_rows <= height) full++;
+            size_t row_b = sizeof(uint32_t) * (size_t)width;
+            size_t off = (size_t)p * block_rows * width;
+            if (full > 0)
+                RT_CK(cudaMemcpy2DAsync(pixels + off, row_b * block_rows * n_parts, (uint32_t *)d.frame.p + off,
+                                        row_b * block_rows * n_parts, row_b * block_rows, full,
+                                        cudaMemcpyDeviceToHost, d.st));
+            int last = p + full * n_parts;  // a trailing partial block, if this part owns it
+            if (last < n_blocks) {
+                int rows = height - last * block_rows;
+                size_t o2 = (size_t)last * block_rows * width;
+                RT_CK(cudaMemcpyAsync(pixels + o2, (uint32_t *)d.frame.p + o2, row_b * rows, cudaMemcpyDeviceToHost,
+                                      d.st));
+            }
+            if (radiance) {
+                size_t rrow = rad_elem * 3 * (size_t)width;
+                char *hr = (char *)radiance, *dr = (char *)d.rad.p;
+                size_t roff = (size_t)p * block_rows * rrow;
+                if (full > 0)
+                    RT_CK(cudaMemcpy2DAsync(hr + roff, rrow * block_rows * n_parts, dr + roff,
+                                            rrow * block_rows * n_parts, rrow * block_rows, full,
+                                            cudaMemcpyDeviceToHost, d.st));
+                if (last < n_blocks) {
+                    int rows = height - last * block_rows;
+                    size_t o2 = (size_t)last * block_rows * rrow;
+                    RT_CK(cudaMemcpyAsync(hr + o2, dr + o2, rrow * rows, cudaMemcpyDeviceToHost, d.st));
+                }
+            }
+        }
+    }
+    for (int g = 0; g < n_dev; g++) {
+        Dev &d = ctx->devs[g];
+        RT_CK(cudaSetDevice(d.id));
+        RT_CK(cudaStreamSynchronize(d.st));
+    }
+    RT_CK(cudaSetDevice(ctx->devs[0].id));
+    RT_CK(cudaEventElapsedTime(&ctx->last_ms, ctx->devs[0].e0, ctx->devs[0].e1));
+    return RT_OK;
+}
+
+int rt_render_device_v1(rt_ctx *ctx, int32_t slot, uint32_t *d_out, int64_t out_pitch, void *d_radiance,
+                        int32_t width, int32_t height, const double cam_pos[3], double yaw, double pitch,
+                        double vdist, int32_t shadow_samples, int32_t bounce_limit, int32_t part, int32_t n_parts,
+                        int32_t block_rows, int32_t precision, void *stream) {
+    if (!ctx || !d_out || !cam_pos) return fail(RT_ERR_INVALID, "null argument");
+    int rc = check_frame_args(width, height, shadow_samples, bounce_limit, precision);
+    if (rc) return rc;
+    if (slot < 0 || slot >= (int)ctx->devs.size()) return fail(RT_ERR_INVALID, "bad device slot");
+    if (n_parts < 1 || part < 0 || part >= n_parts || block_rows < 1)
+        return fail(RT_ERR_INVALID, "bad partition (part, n_parts, block_rows)");
+    if (out_pitch < width) return fail(RT_ERR_INVALID, "out_pitch < width");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    Dev &d = ctx->devs[slot];
+    if ((rc = prepare(ctx, d, precision, shadow_samples))) return rc;
+    cudaStream_t st = stream ? (cudaStream_t)stream : d.st;
+    rt::FrameArgs fa = frame_args(d_out, out_pitch, d_radiance, width, height, cam_pos, yaw, pitch, vdist,
+                                  shadow_samples, bounce_limit, part, n_parts, block_rows);
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, d_out) != cudaSuccess) {
+        cudaGetLastError();
+        fa.peer_out = 1;
+    } else {
+        fa.peer_out = (attr.type != cudaMemoryTypeDevice || attr.device != d.id) ? 1 : 0;
+    }
+    return launch_frame(ctx, d, fa, precision, st);
+}
+
+int rt_trace_rays_v1(rt_ctx *ctx, const double *origins, const double *dirs, int64_t n_rays, void *out_rgb,
+                     int32_t n_bodies, const int32_t *kinds, const double *positions, const double *sizes,
+                     const double *colors, const double *refls, const double light_pos[3], double light_radius,
+                     const double light_color[3], double ambient, double max_refl, const float *sky,
+                     int32_t sky_w, int32_t sky_h, int32_t has_sky, int32_t shadow_samples, int32_t bounce_limit,
+                     int32_t precision) {
+    if (!ctx || (n_rays > 0 && (!origins || !dirs || !out_rgb))) return fail(RT_ERR_INVALID, "null argument");
+    if (n_rays < 0) return fail(RT_ERR_INVALID, "n_rays < 0");
+    int rc = check_frame_args(1, 1, shadow_samples, bounce_limit, precision);
+    if (rc) return rc;
+    if ((rc = validate_scene(n_bodies, kinds, positions, sizes, colors, refls, light_pos, light_color, max_refl, sky,
+                             sky_w, sky_h, has_sky)))
+        return rc;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    set_host_scene(ctx->scene, n_bodies, kinds, positions, sizes, colors, refls, light_pos, light_radius, light_color,
+                   ambient, max_refl, sky, sky_w, sky_h, has_sky);
+    if (n_rays == 0) return RT_OK;
+    Dev &d = ctx->devs[0];
+    if ((rc = prepare(ctx, d, precision, shadow_samples))) return rc;
+    size_t in_b = sizeof(double) * 3 * (size_t)n_rays;
+    size_t out_b = (precision == RT_PREC_FP64 ? sizeof(double) : sizeof(float)) * 3 * (size_t)n_rays;
+    if ((rc = d.rays_in.ensure(2 * in_b)) || (rc = d.rays_out.ensure(out_b))) return rc;
+    double *d_o = (double *)d.rays_in.p, *d_d = d_o + 3 * n_rays;
+    RT_CK(cudaMemcpyAsync(d_o, origins, in_b, cudaMemcpyHostToDevice, d.st));
+    RT_CK(cudaMemcpyAsync(d_d, dirs, in_b, cudaMemcpyHostToDevice, d.st));
+    RT_CK(cudaEventRecord(d.e0, d.st));
+    cudaError_t e;
+    if (precision == RT_PREC_FP64)
+        e = rt_launch_trace_f64(d_o, d_d, n_rays, (double *)d.rays_out.p, scene_args(d, d.s64, ctx->scene),
+                                shadow_samples, bounce_limit, d.st);
+    else
+        e = rt_launch_trace_f32(d_o, d_d, n_rays, (float *)d.rays_out.p, scene_args(d, d.s32, ctx->scene),
+                                shadow_samples, bounce_limit, d.st);
+    if (e != cudaSuccess) return fail(RT_ERR_CUDA, std::string("trace kernel launch: ") + cudaGetErrorString(e));
+    ctx->launches++;
+    RT_CK(cudaEventRecord(d.e1, d.st));
+    RT_CK(cudaMemcpyAsync(out_rgb, d.rays_out.p, out_b, cudaMemcpyDeviceToHost, d.st));
+    RT_CK(cudaStreamSynchronize(d.st));
+    RT_CK(cudaEventElapsedTime(&ctx->last_ms, d.e0, d.e1));
+    return RT_OK;
+}
+
+int rt_sky_sample_v1(rt_ctx *ctx, const double *dirs, int64_t n, double *out_rgb, const float *sky, int32_t sky_w,
+                     int32_t sky_h) {
+    if (!ctx || !sky || (n > 0 && (!dirs || !out_rgb))) return fail(RT_ERR_INVALID, "null argument");
+    if (sky_w < 1 || sky_h < 1 || n < 0) return fail(RT_ERR_INVALID, "bad skybox / count");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    Dev &d = ctx->devs[0];
+    RT_CK(cudaSetDevice(d.id));
+    int64_t nt = (int64_t)sky_w * sky_h;
+    DBuf raw, tex, io;
+    int rc;
+    if ((rc = raw.ensure(sizeof(float) * 3 * nt)) || (rc = tex.ensure(sizeof(float4) * nt)) ||
+        (rc = io.ensure(sizeof(double) * 6 * (size_t)std::max<int64_t>(n, 1)))) {
+        raw.release();
+        tex.release();
+        io.release();
+        return rc;
+    }
+    double *d_in = (double *)io.p, *d_out = d_in + 3 * n;
+    cudaError_t e = cudaMemcpyAsync(raw.p, sky, sizeof(float) * 3 * nt, cudaMemcpyHostToDevice, d.st);
+    if (e == cudaSuccess && n > 0) e = cudaMemcpyAsync(d_in, dirs, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, d.st);
+    if (e == cudaSuccess) {
+        sky_to_float4<<<(unsigned)((nt + 255) / 256), 256, 0, d.st>>>((const float *)raw.p, (float4 *)tex.p, nt);
+        e = cudaGetLastError();
+        ctx->launches++;
+    }
+    if (e == cudaSuccess && n > 0) {
+        e = rt_launch_sky_f64(d_in, n, d_out, (const float4 *)tex.p, sky_w, sky_h, d.st);
+        ctx->launches++;
+    }
+    if (e == cudaSuccess && n > 0)
+        e = cudaMemcpyAsync(out_rgb, d_out, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, d.st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(d.st);
+    raw.release();
+    tex.release();
+    io.release();
+    if (e != cudaSuccess) return fail(RT_ERR_CUDA, std::string("sky sample: ") + cudaGetErrorString(e));
+    return RT_OK;
+}
+
+int rt_host_register(rt_ctx *ctx, void *ptr, size_t bytes) {
+    if (!ctx || !ptr || bytes == 0) return fail(RT_ERR_INVALID, "bad host range");
+    RT_CK(cudaSetDevice(ctx->devs[0].id));
+    RT_CK(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable));
+    return RT_OK;
+}
+
+int rt_host_unregister(rt_ctx *ctx, void *ptr) {
+    if (!ctx || !ptr) return fail(RT_ERR_INVALID, "bad host pointer");
+    RT_CK(cudaSetDevice(ctx->devs[0].id));
+    RT_CK(cudaHostUnregister(ptr));
+    return RT_OK;
+}
+
+int rt_last_kernel_ms(rt_ctx *ctx, float *ms) {
+    if (!ctx || !ms) return fail(RT_ERR_INVALID, "null argument");
+    *ms = ctx->last_ms;
+    return RT_OK;
+}
+
+int rt_launch_count(rt_ctx *ctx, int64_t *count) {
+    if (!ctx || !count) return fail(RT_ERR_INVALID, "null argument");
+    *count = ctx->launches;
+    return RT_OK;
+}
+
+int rt_ipc_get_handle(void *d_ptr, uint8_t handle_out[64]) {
+    if (!d_ptr || !handle_out) return fail(RT_ERR_INVALID, "null argument");
+    cudaIpcMemHandle_t h;
+    RT_CK(cudaIpcGetMemHandle(&h, d_ptr));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle_out, &h, 64);
+    return RT_OK;
+}
+
+int rt_ipc_open(const uint8_t handle[64], void **d_ptr_out) {
+    if (!handle || !d_ptr_out) return fail(RT_ERR_INVALID, "null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    RT_CK(cudaIpcOpenMemHandle(d_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+    return RT_OK;
+}
+
+int rt_ipc_close(void *d_ptr) {
+    if (!d_ptr) return fail(RT_ERR_INVALID, "null argument");
+    RT_CK(cudaIpcCloseMemHandle(d_ptr));
+    return RT_OK;
+}
+
+int rt_copy_to_host(rt_ctx *ctx, int32_t slot, void *host_dst, const void *d_src, size_t bytes, void *stream) {
+    if (!ctx || !host_dst || !d_src) return fail(RT_ERR_INVALID, "null argument");
+    if (slot < 0 || slot >= (int)ctx->devs.size()) return fail(RT_ERR_INVALID, "bad device slot");
+    Dev &d = ctx->devs[slot];
+    RT_CK(cudaSetDevice(d.id));
+    cudaStream_t st = stream ? (cudaStream_t)stream : d.st;
+    RT_CK(cudaMemcpyAsync(host_dst, d_src, bytes, cudaMemcpyDeviceToHost, st));
+    RT_CK(cudaStreamSynchronize(st));
+    return RT_OK;
+}
+
+int rt_device_malloc(int32_t device, size_t bytes, void **d_ptr_out) {
+    if (!d_ptr_out || bytes == 0) return fail(RT_ERR_INVALID, "bad allocation request");
+    *d_ptr_out = nullptr;
+    RT_CK(cudaSetDevice(device));
+    cudaError_t e = cudaMalloc(d_ptr_out, bytes);
+    if (e != cudaSuccess) return fail(RT_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    return RT_OK;
+}
+
+int rt_device_free(void *d_ptr) {
+    if (!d_ptr) return RT_OK;
+    RT_CK(cudaFree(d_ptr));
+    return RT_OK;
+}
+
+int rt_fp32_peak_tflops(int32_t device, double *tflops) {
+    if (!tflops) return fail(RT_ERR_INVALID, "null argument");
+    RT_CK(cudaSetDevice(device));
+    int sms = 0;
+    RT_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    float *sink = nullptr;
+    RT_CK(cudaMalloc(&sink, 1024 * sizeof(float)));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const int threads = 256, blocks = sms * 8, iters = 2048;
+    ffma_peak_kernel<<<blocks, threads>>>(sink, 64, 1.0001f, 0.5f);  // warm-up / clock ramp
+    ffma_peak_kernel<<<blocks, threads>>>(sink, iters, 1.0001f, 0.5f);
+    cudaEventRecord(a);
+    ffma_peak_kernel<<<blocks, threads>>>(sink, iters, 1.0001f, 0.5f);
+    cudaEventRecord(b);
+    cudaError_t e = cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(sink);
+    if (e != cudaSuccess) return fail(RT_ERR_CUDA, std::string("ffma peak: ") + cudaGetErrorString(e));
+    double flops = 2.0 * 8 * 16 * (double)iters * threads * blocks;
+    *tflops = flops / (ms * 1e-3) / 1e12;
+    return RT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,164 @@
+"""The reference's renderer API, executed by the sm_100a kernels of libb200rt.
+
+Drop-in for /root/reference/pkg/src/raytracer/renderer.py: same names,
+signatures, argument meaning and errors —
+
+    render_frame(scene, cam, params, out, workers=None)     renderer.py:316-349
+    ray_trace_iterative(ray, scene, params) -> (r, g, b)    renderer.py:303-313
+    skybox_sample(direction, sky) -> (r, g, b)              renderer.py:77-79
+    pack_color(c) -> int                                    renderer.py:53-57
+    MAX_BOUNCE_LIMIT, REFLECT_EPS                           renderer.py:33-36
+
+plus the batched `trace_rays` that backs `ray_trace_iterative`.  Inputs are
+duck-typed, so the reference's own Scene/Camera/RenderParams/Framebuffer
+objects work unchanged.
+
+`workers` keeps its meaning — how many parallel workers split the frame —
+and becomes the number of row-block partitions, spread over up to that many
+GPUs; as in the reference the pixels do not depend on it.
+
+`precision` (keyword, default "fp32", or $B200RT_PRECISION) picks the FP32
+product kernel or the FP64 validation kernel that reproduces the reference
+bit for bit.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+
+from . import _native
+from .model import MAX_BOUNCE_LIMIT, REFLECT_EPS, camera_viewport_distance, pack_scene
+
+__all__ = [
+    "MAX_BOUNCE_LIMIT",
+    "REFLECT_EPS",
+    "render_frame",
+    "ray_trace_iterative",
+    "trace_rays",
+    "skybox_sample",
+    "pack_color",
+    "default_precision",
+]
+
+_PIN_MIN_BYTES = 1 << 18  # page-lock framebuffers of >= 256 KiB
+
+
+def default_precision() -> str:
+    return os.environ.get("B200RT_PRECISION", "fp32")
+
+
+def _prec(precision) -> int:
+    p = precision or default_precision()
+    if p not in _native.PRECISIONS:
+        raise ValueError(f"precision must be one of {sorted(_native.PRECISIONS)}, got {p!r}")
+    return _native.PRECISIONS[p]
+
+
+def _scene_argv(ps):
+    P = _native.ptr
+    return [
+        ps.n_bodies, P(ps.kinds), P(ps.positions), P(ps.sizes), P(ps.colors), P(ps.refls), P(ps.light_pos),
+        ps.light_radius, P(ps.light_color), ps.ambient, ps.max_refl, P(ps.sky), ps.sky_w, ps.sky_h,
+        int(ps.has_sky),
+    ]
+
+
+def pack_color(c) -> int:
+    """Pack a [0,1] RGB triple into 0xAARRGGBB, alpha opaque (renderer.py:45-57)."""
+    if not all(0.0 <= ch <= 1.0 for ch in c):
+        raise ValueError(f"channels must be in [0, 1], got {c}")
+    r = int(c[0] * 255.0 + 0.5)
+    g = int(c[1] * 255.0 + 0.5)
+    b = int(c[2] * 255.0 + 0.5)
+    return 0xFF000000 | (r << 16) | (g << 8) | b
+
+
+def render_frame(scene, cam, params, out, workers=None, *, precision=None, radiance=None):
+    """Render one frame into `out`; pixel (x, y) lands at index x + y * width.
+
+    `workers` picks the number of row-block partitions (and GPUs, up to the
+    number visible); the result does not depend on it.  `radiance`, when
+    given, is filled with the pre-quantisation colours: float32[w*h, 3] for
+    precision "fp32", float64[w*h, 3] for "fp64".
+    """
+    if (out.width, out.height) != (params.width, params.height):
+        raise ValueError(
+            f"framebuffer {out.width}x{out.height} does not match params {params.width}x{params.height}"
+        )
+    if params.bounce_limit > MAX_BOUNCE_LIMIT:
+        raise ValueError(f"bounce limit capped at {MAX_BOUNCE_LIMIT}")
+    prec = _prec(precision)
+    pixels = out.pixels
+    if pixels.dtype != np.uint32 or not pixels.flags.c_contiguous or pixels.size != params.width * params.height:
+        raise ValueError("framebuffer pixels must be a contiguous uint32 array of width * height")
+    if radiance is not None:
+        want = np.float64 if prec == _native.RT_PREC_FP64 else np.float32
+        if radiance.dtype != want or not radiance.flags.c_contiguous or radiance.size != 3 * pixels.size:
+            raise ValueError(f"radiance must be a contiguous {np.dtype(want).name}[w*h, 3] array")
+    n_parts = 1 if workers is None else int(workers)
+    if n_parts < 1:
+        raise ValueError("workers must be >= 1")
+    ctx = _native.context(n_parts)
+    if pixels.nbytes >= _PIN_MIN_BYTES:
+        ctx.pin(pixels)
+    ps = pack_scene(scene)
+    cam_pos = np.array(cam.position, dtype=np.float64)
+    rc = _native.load().rt_render_v1(
+        ctx.handle, _native.ptr(pixels), _native.ptr(radiance), int(params.width), int(params.height),
+        _native.ptr(cam_pos), float(cam.yaw), float(cam.pitch), camera_viewport_distance(cam.fov),
+        *_scene_argv(ps), int(params.shadow_samples), int(params.bounce_limit), n_parts, prec,
+    )
+    _native.check(rc, "rt_render_v1")
+
+
+def trace_rays(origins, directions, scene, params, *, precision=None) -> np.ndarray:
+    """Batched `ray_trace_iterative`: colours of rays (origins[i], directions[i]).
+
+    Returns float32[n, 3] ("fp32") or float64[n, 3] ("fp64")."""
+    if params.bounce_limit > MAX_BOUNCE_LIMIT:
+        raise ValueError(f"bounce limit capped at {MAX_BOUNCE_LIMIT}")
+    prec = _prec(precision)
+    o = np.ascontiguousarray(origins, dtype=np.float64).reshape(-1, 3)
+    d = np.ascontiguousarray(directions, dtype=np.float64).reshape(-1, 3)
+    if o.shape != d.shape:
+        raise ValueError("origins and directions must have the same shape")
+    out = np.zeros(o.shape, dtype=np.float64 if prec == _native.RT_PREC_FP64 else np.float32)
+    ctx = _native.context(1)
+    ps = pack_scene(scene)
+    rc = _native.load().rt_trace_rays_v1(
+        ctx.handle, _native.ptr(o), _native.ptr(d), o.shape[0], _native.ptr(out), *_scene_argv(ps),
+        int(params.shadow_samples), int(params.bounce_limit), prec,
+    )
+    _native.check(rc, "rt_trace_rays_v1")
+    return out
+
+
+def ray_trace_iterative(ray, scene, params, *, precision=None):
+    """Colour gathered by one ray under the scene's light and bounce budget
+    (renderer.py:303-313); a tuple of Python floats."""
+    if params.bounce_limit > MAX_BOUNCE_LIMIT:
+        raise ValueError(f"bounce limit capped at {MAX_BOUNCE_LIMIT}")
+    c = trace_rays([ray.origin], [ray.direction], scene, params, precision=precision)[0]
+    return (float(c[0]), float(c[1]), float(c[2]))
+
+
+def skybox_sample(direction, sky):
+    """Equirectangular nearest-texel lookup, clamped to [0, 1] (renderer.py:60-79).
+    Evaluated on the GPU in float64, bit-identical to the reference."""
+    d = np.ascontiguousarray(direction, dtype=np.float64).reshape(-1, 3)
+    texels = np.ascontiguousarray(sky.texels, dtype=np.float32)
+    out = np.zeros(d.shape, dtype=np.float64)
+    ctx = _native.context(1)
+    rc = _native.load().rt_sky_sample_v1(ctx.handle, _native.ptr(d), d.shape[0], _native.ptr(out),
+                                         _native.ptr(texels), int(sky.width), int(sky.height))
+    _native.check(rc, "rt_sky_sample_v1")
+    if np.ndim(direction) == 1 or (len(direction) == 3 and np.ndim(direction[0]) == 0):
+        return (float(out[0, 0]), float(out[0, 1]), float(out[0, 2]))
+    return out
+
+
+def last_kernel_ms(workers=None) -> float:
+    """Device time of the render kernels of the last call (CUDA events)."""
+    return _native.context(1 if workers is None else int(workers)).last_kernel_ms()

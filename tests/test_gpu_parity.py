@@ -1,0 +1,246 @@
+"""GPU parity: the sm_100a kernels through the C ABI (render_frame /
+trace_rays / skybox_sample) against the reference's golden fixtures and the
+oracle, at fixture sizes and at BASELINE.json's full sizes.
+
+FP64 kernel: bit-identical framebuffers (the reference's golden sha256 and
+every fixture frame).  FP32 kernel: the north-star gates — per 8-bit channel
+|delta| <= 1 on >= 99.9% of pixels, radiance |delta| <= 1e-4*max(|ref|,1) on
+>= 99.9% of pixels (tests/parity.py).
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import golden_cases as G
+import oracle
+import parity
+import paper_2305_07450_b200 as rt
+from paper_2305_07450_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+CASES = [c["name"] for c in G.frame_cases()]
+
+
+class _Sky:
+    def __init__(self, texels):
+        self.texels = texels
+        self.height, self.width = texels.shape[:2]
+
+
+def scene_from_case(c):
+    """Reference-layout fixture -> this package's Scene (through the public types)."""
+    s = c["scene"]
+    bodies = []
+    for k, p, size, col, refl in zip(s["kinds"], s["positions"], s["sizes"], s["colors"], s["refls"]):
+        if k == 0:
+            bodies.append(rt.Body.sphere(tuple(p), size, tuple(col), refl))
+        else:
+            bodies.append(rt.Body.plane(p[1], tuple(col), refl))
+    sky = None
+    if c.get("sky"):
+        t = G.sky_texels(c["sky"])
+        sky = rt.Skybox(t.shape[1], t.shape[0], t)
+    return rt.Scene(bodies=bodies, light=rt.Light(tuple(s["light_pos"]), s["light_radius"], tuple(s["light_color"])),
+                    skybox=sky, ambient=s["ambient"], max_reflectivity=s["max_refl"])
+
+
+def render_case(c, precision, workers=None, radiance=False):
+    scene = scene_from_case(c)
+    cam = rt.Camera(**{**c["camera"], "position": tuple(c["camera"]["position"])})
+    params = rt.RenderParams(c["samples"], c["bounces"], c["width"], c["height"])
+    fb = rt.Framebuffer.create(c["width"], c["height"])
+    rad = None
+    if radiance:
+        rad = np.zeros((c["width"] * c["height"], 3), np.float64 if precision == "fp64" else np.float32)
+    rt.render_frame(scene, cam, params, fb, workers=workers, precision=precision, radiance=rad)
+    return fb.pixels.copy(), rad
+
+
+def test_device_visible_and_library_loaded():
+    assert _native.device_count() >= 1
+    assert _native.load().rt_version() == 1
+
+
+def test_golden_sha256_fp64():
+    c = G.frame_case("bench_128x72_s200_b3")
+    px, _ = render_case(c, "fp64")
+    assert hashlib.sha256(px.tobytes()).hexdigest() == G.GOLDEN_SHA_128x72_S200_B3
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_fp64_frames_bit_exact(name):
+    c = G.frame_case(name)
+    px, rad = render_case(c, "fp64", radiance=True)
+    np.testing.assert_array_equal(px, G.frame_pixels(name))
+    want = G.frame_radiance(name)
+    if want is not None:
+        # device pow/atan2/asin may differ from glibc in the last ulp
+        np.testing.assert_allclose(rad, want, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_fp32_frames_byte_and_radiance_gates(name):
+    c = G.frame_case(name)
+    px, rad = render_case(c, "fp32", radiance=True)
+    frac, worst = parity.assert_byte_gate(px, G.frame_pixels(name), name)
+    assert np.all(px >> 24 == 0xFF)
+    cam = c["camera"]
+    _, want = oracle.render(G.packed_scene(c), cam["position"], cam["yaw"], cam["pitch"], cam["fov"], c["width"],
+                            c["height"], c["samples"], c["bounces"], radiance=True)
+    parity.assert_radiance_gate(rad, want, name)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_worker_counts_do_not_change_pixels(precision):
+    # test_renderer.py:229-238 / test_acceptance.py:115-118 with workers = row-block partitions
+    c = G.frame_case("sweep_160x90_s16_b5_sky")
+    base, _ = render_case(c, precision)
+    for workers in (1, 2, 3, 8, 13):
+        px, _ = render_case(c, precision, workers=workers)
+        np.testing.assert_array_equal(px, base)
+
+
+def test_repeated_renders_bit_identical():
+    c = G.frame_case("bench_128x72_s200_b3")
+    first, _ = render_case(c, "fp32")
+    for _ in range(3):
+        again, _ = render_case(c, "fp32")
+        np.testing.assert_array_equal(again, first)
+
+
+@pytest.mark.parametrize("rc", [r["name"] for r in G.ray_cases()])
+def test_trace_rays_against_reference(rc):
+    entry = next(r for r in G.ray_cases() if r["name"] == rc)
+    a = G.ray_arrays(rc)
+    scene = scene_from_case(entry)
+    for lim in range(4):
+        m = a["limits"] == lim
+        params = rt.RenderParams(entry["samples"], lim, 1, 1)
+        got64 = rt.trace_rays(a["origins"][m], a["dirs"][m], scene, params, precision="fp64")
+        np.testing.assert_allclose(got64, a["iterative"][m], rtol=0, atol=1e-12)
+        got32 = rt.trace_rays(a["origins"][m], a["dirs"][m], scene, params, precision="fp32")
+        frac, _ = parity.radiance_gate(got32, a["iterative"][m])
+        # 15 rays per limit: at most one shadow-sample decision flip
+        assert frac >= 14 / 15
+
+
+def test_empty_scene_renders_black():
+    # test_renderer.py:217-221
+    scene = rt.Scene(bodies=[], light=rt.Light((0, 5, 0), 0.5))
+    for prec in ("fp32", "fp64"):
+        fb = rt.Framebuffer.create(1, 1)
+        rt.render_frame(scene, rt.Camera(), rt.RenderParams(1, 1, 1, 1), fb, precision=prec)
+        assert fb.pixels[0] == 0xFF000000
+
+
+def test_dimension_mismatch_and_bounce_cap_rejected():
+    scene = rt.build_benchmark_scene()
+    with pytest.raises(ValueError):
+        rt.render_frame(scene, rt.Camera(), rt.RenderParams(1, 1, 8, 8), rt.Framebuffer.create(4, 4))
+    with pytest.raises(ValueError):
+        rt.render_frame(scene, rt.Camera(), rt.RenderParams(1, 32, 4, 4), rt.Framebuffer.create(4, 4))
+    with pytest.raises(ValueError):
+        rt.ray_trace_iterative(rt.Ray((0, 1, -3), (0, 0, 1)), scene, rt.RenderParams(4, 32, 1, 1))
+
+
+def _small_scene(skybox=None):  # test_renderer.py:31-40
+    return rt.Scene(
+        bodies=[
+            rt.Body.sphere((0.0, 1.0, 4.0), 1.0, (0.8, 0.2, 0.1), 64.0),
+            rt.Body.sphere((1.5, 0.6, 2.5), 0.6, (0.2, 0.7, 0.3), 128.0),
+            rt.Body.plane(0.0, (0.5, 0.5, 0.55), 16.0),
+        ],
+        light=rt.Light((-3.0, 6.0, -1.0), 0.5),
+        skybox=skybox,
+    )
+
+
+def test_reductions_exact_fp64():
+    # test_acceptance.py:177-227, test_renderer.py:124-188
+    blocked = rt.Scene(
+        bodies=[rt.Body.sphere((0.0, 5.0, 0.0), 3.0, (0.3, 0.3, 0.3)), rt.Body.plane(0.0, (0.6, 0.5, 0.4))],
+        light=rt.Light((0.0, 10.0, 0.0), 0.5),
+        ambient=0.15,
+    )
+    down = np.array((0.0, -1.0, 0.02))
+    down /= np.sqrt(down @ down)
+    got = rt.ray_trace_iterative(rt.Ray((0.0, 1.0, 0.0), tuple(down)), blocked, rt.RenderParams(1, 0, 1, 1),
+                                 precision="fp64")
+    assert got == tuple(c * 0.15 for c in (0.6, 0.5, 0.4))
+    # zero-reflectivity scene: output invariant in the bounce limit, exactly
+    flat = rt.build_benchmark_scene()
+    for b in flat.bodies:
+        b.reflectivity = 0.0
+    for prec in ("fp32", "fp64"):
+        imgs = []
+        for limit in (0, 1, 3, 5):
+            fb = rt.Framebuffer.create(48, 27)
+            rt.render_frame(flat, rt.benchmark_camera(), rt.RenderParams(2, limit, 48, 27), fb, precision=prec)
+            imgs.append(fb.tobytes())
+        assert all(i == imgs[0] for i in imgs)
+    # miss: unshaded sky, or black without a sky
+    sky = _Sky(G.sky_texels("grad:8:4"))
+    d = np.array((0.3, 0.8, -0.5))
+    d /= np.sqrt(d @ d)
+    params = rt.RenderParams(4, 2, 1, 1)
+    sc = _small_scene(skybox=rt.Skybox(8, 4, sky.texels))
+    got = rt.ray_trace_iterative(rt.Ray((0.0, 1.0, -3.0), tuple(d)), sc, params, precision="fp64")
+    assert got == rt.skybox_sample(tuple(d), sky)
+    assert rt.ray_trace_iterative(rt.Ray((0.0, 1.0, -3.0), tuple(d)), _small_scene(), params,
+                                  precision="fp64") == (0.0, 0.0, 0.0)
+
+
+def test_skybox_sample_kats_and_oracle():
+    sky = _Sky(G.sky_texels("grad:8:4"))
+    assert rt.skybox_sample((0.0, 1.0, 0.0), sky)[1] == pytest.approx(0.0)
+    assert rt.skybox_sample((0.0, -1.0, 0.0), sky)[1] == pytest.approx(3 / 4)
+    got = rt.skybox_sample((0.0, 0.0, 1.0), sky)
+    assert got[0] == pytest.approx(4 / 8) and got[1] == pytest.approx(2 / 4)
+    assert rt.skybox_sample((0.0, 0.0, 1.0), _Sky(np.full((2, 2, 3), 7.5, np.float32))) == (1.0, 1.0, 1.0)
+    rng = np.random.default_rng(5)
+    dirs = rng.normal(size=(500, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    big = _Sky(G.sky_texels("hdr:64:32"))
+    np.testing.assert_array_equal(rt.skybox_sample(dirs, big), oracle.sky_samples(dirs, big.texels))
+
+
+@pytest.mark.slow
+def test_full_size_c2_fp64_bit_exact_vs_oracle_and_fp32_gate():
+    """C2 at its full size (1280x720 s200 b3): FP64 kernel == oracle bit for
+    bit, FP32 kernel within the byte gate."""
+    cfg = rt.CONFIGS["C2"]
+    scene, cam, params = cfg.scene(), cfg.camera(), cfg.params()
+    fb64 = rt.Framebuffer.create(cfg.width, cfg.height)
+    rt.render_frame(scene, cam, params, fb64, precision="fp64")
+    ps = rt.pack_scene(scene)
+    want = oracle.render(vars(ps), cam.position, cam.yaw, cam.pitch, cam.fov, cfg.width, cfg.height, cfg.samples,
+                         cfg.bounces)
+    np.testing.assert_array_equal(fb64.pixels, want)
+    fb32 = rt.Framebuffer.create(cfg.width, cfg.height)
+    rt.render_frame(scene, cam, params, fb32, precision="fp32")
+    parity.assert_byte_gate(fb32.pixels, want, "C2 fp32")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("key", ["C3", "C4"])
+def test_full_size_sky_configs_fp32_vs_fp64(key):
+    """C3/C4 at full size with the 2048x1024 sky: FP32 within the byte gate of
+    the bit-exact FP64 kernel; row-block partitions do not change a byte."""
+    cfg = rt.CONFIGS[key]
+    scene, cam, params = cfg.scene(), cfg.camera(), cfg.params()
+    fb64 = rt.Framebuffer.create(cfg.width, cfg.height)
+    rt.render_frame(scene, cam, params, fb64, precision="fp64")
+    fb32 = rt.Framebuffer.create(cfg.width, cfg.height)
+    rt.render_frame(scene, cam, params, fb32, precision="fp32")
+    parity.assert_byte_gate(fb32.pixels, fb64.pixels, f"{key} fp32 vs fp64")
+    fb8 = rt.Framebuffer.create(cfg.width, cfg.height)
+    rt.render_frame(scene, cam, params, fb8, workers=8, precision="fp32")
+    np.testing.assert_array_equal(fb8.pixels, fb32.pixels)
+    # exact on a strided row subset against the oracle
+    ps = rt.pack_scene(scene)
+    sub = oracle.render(vars(ps), cam.position, cam.yaw, cam.pitch, cam.fov, cfg.width, cfg.height, cfg.samples,
+                        cfg.bounces, row0=5, row_step=97).reshape(cfg.height, cfg.width)
+    np.testing.assert_array_equal(fb64.pixels.reshape(cfg.height, cfg.width)[5::97], sub[5::97])

@@ -38,6 +38,7 @@ sys.path.insert(0, ROOT)
 
 NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965  # SMs x FP32 lanes x FMA x max SM clock (GHz) / 1e3
 L2_FLUSH_BYTES = 256 << 20
+EXTRA_CONFIGS = ("C1", "P720", "P1080", "P4K", "C3", "C4")
 
 
 def parse_args(argv=None):
@@ -228,25 +229,16 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
 
-    # framebuffer: rank 0 owns it; other ranks map it over NVLink (CUDA IPC)
-    fb_ptr = ctypes.c_void_p()
+    # framebuffer: rank 0 owns it (sized for the largest frame measured);
+    # other ranks map it over NVLink (CUDA IPC) and render straight into it
+    from paper_2305_07450_b200 import bands
+
+    extra_keys = () if (args.no_extra or world > 1) else EXTRA_CONFIGS
+    max_px = max(rt.CONFIGS[k].width * rt.CONFIGS[k].height for k in (args.config, *extra_keys))
     frame_bytes = 4 * cfg.width * cfg.height
-    peer_ptr = None
-    if rank == 0:
-        _native.check(lib.rt_device_malloc(local, frame_bytes, ctypes.byref(fb_ptr)), "rt_device_malloc")
-    if world > 1:
-        import torch.distributed as dist
-        handle = (ctypes.c_uint8 * 64)()
-        if rank == 0:
-            _native.check(lib.rt_ipc_get_handle(fb_ptr, handle), "rt_ipc_get_handle")
-        obj = [bytes(handle)]
-        dist.broadcast_object_list(obj, src=0)
-        if rank != 0:
-            h = (ctypes.c_uint8 * 64).from_buffer_copy(obj[0])
-            peer = ctypes.c_void_p()
-            _native.check(lib.rt_ipc_open(h, ctypes.byref(peer)), "rt_ipc_open")
-            fb_ptr = peer
-            peer_ptr = peer
+    exchange = bands.torch_exchange if world > 1 else (lambda blob: blob)
+    ipc = bands.IpcFrame(local, 1, max_px, rank, exchange)
+    fb_ptr = ipc.ptr
     tiny = torch.zeros(1, device=dev)
 
     def render_cfg(c, part=rank, n_parts=world):
@@ -373,7 +365,7 @@ def run_ours(args):
     }
     if rank == 0 and not args.no_extra and world == 1:
         extra = {}
-        for key in ("C1", "P720", "P1080", "P4K", "C3", "C4"):
+        for key in extra_keys:
             c = rt.CONFIGS[key]
             r = time_config(c, 3, 10 if key != "C4" else 5)
             f = len(r["ms"]) / (r["total_ms"] / 1e3)
@@ -390,13 +382,11 @@ def run_ours(args):
                                 "sample": f"every {meta['row_step']}th row ({meta['rows']}/{cfg.height}) of "
                                           f"{cfg.name}, float64 C port of render_frame (oracle/), "
                                           f"{meta['seconds']:.1f} s"}
-    if peer_ptr is not None:
-        lib.rt_ipc_close(peer_ptr)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
+    ipc.close()
     if rank == 0:
-        lib.rt_device_free(fb_ptr)
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -226,7 +226,10 @@ def run_ours(args):
                                           int(ps.has_sky)), "rt_set_scene_v1")
         return ps
 
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated stream: the legacy default stream's handle is NULL, which the
+    # C ABI reads as "the library's own stream" (not ordered with our events)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
 
     # framebuffer: rank 0 owns it (sized for the largest frame measured);

@@ -27,7 +27,9 @@ HOST_CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else None
 
 SOURCES = {
     "rt_host.cu": [],
-    "render_f32.cu": [],
+    # FP32 product path: flush denormals, approximate sqrt/div (powf, atan2f
+    # and asinf stay full precision: no --use_fast_math)
+    "render_f32.cu": ["--ftz=true", "--prec-div=false", "--prec-sqrt=false"],
     "render_f64.cu": ["-fmad=false"],
 }
 

@@ -1,23 +1,35 @@
 // FP32 frame render — the product path on the B200 CUDA cores.
 //
-// One thread per pixel, a warp per 8x4 pixel patch, the scene's geometry
-// staged in shared memory so each warp-uniform body loop is a broadcast.
-// Same control flow as the reference (/root/reference/pkg/src/raytracer/
-// renderer.py:108-279): closest hit, sunflower soft-shadow coefficient,
-// bounded reflections with a register-resident record stack, skybox on miss,
-// Blinn-Phong unwind, pack to 0xAARRGGBB.
+// One thread per pixel, a warp per 8x4 pixel patch.  Same control flow as the
+// reference (/root/reference/pkg/src/raytracer/renderer.py:108-279): closest
+// hit, sunflower soft-shadow coefficient, bounded reflections with a
+// register-resident record stack, skybox on miss, Blinn-Phong unwind, pack to
+// 0xAARRGGBB.
 //
-// FP32-specific numerics (the reasons are measured in SURVEY.md §8c):
+// Scene residency: scenes of up to kParamSpheres spheres and kMaxPlanes
+// planes travel inside the kernel's launch parameters (constant bank 0), so
+// every warp-uniform body loop reads its operands straight from the constant
+// cache with no load instructions and no shared/global traffic; larger scenes
+// are staged in shared memory (or read through L1 when they do not fit).
+//
+// FP32-specific numerics (measured in SURVEY.md §8c):
 //  - the sphere test forms the squared ray-to-centre distance as
 //    |L - tca*d|^2 instead of L.L - tca^2 (geometry.py:96): algebraically
 //    identical, free of the cancellation that makes FP32 misjudge long shadow
 //    rays from far plane points and rays near silhouettes;
+//  - the any-hit shadow test decides `tca - sqrt(rad) in [0, limit)`
+//    (geometry.py:94-104, 204-210) without the square root:
+//    t >= 0  <=>  tca^2 >= rad,   t < limit  <=>  tca - limit < 0 or (tca - limit)^2 < rad;
+//    the plane test `0 < (h - o.y)/d.y < limit` without the division;
 //  - primary directions are formed in float64 (camera.py:70-77) and rounded;
 //  - the disc-sample table is built in float64 on the host and rounded.
 #include "rt_device.cuh"
 
 namespace {
 using namespace rt;
+
+constexpr int kMaxPlanes = 8;
+constexpr int kParamSpheres = 256;
 
 __device__ __forceinline__ float3 f3(float x, float y, float z) { return make_float3(x, y, z); }
 __device__ __forceinline__ float3 operator+(float3 a, float3 b) { return f3(a.x + b.x, a.y + b.y, a.z + b.z); }
@@ -54,65 +66,208 @@ __device__ __forceinline__ float3 primary_direction(int xi, int yi, const FrameA
     return f3((float)x2, (float)y2, (float)z3);
 }
 
-// geometry.py:83-105 with the cancellation-free perpendicular distance.
-__device__ __forceinline__ float ray_sphere(float3 o, float3 d, float4 g) {
+// geometry.py:83-105 — distance to the sphere, +inf on a miss.
+__device__ __forceinline__ float sphere_t(float3 o, float3 d, float4 g) {
     float3 L = f3(g.x - o.x, g.y - o.y, g.z - o.z);
     float tca = dot3(L, d);
-    if (tca < 0.f) return INFINITY;
     float3 p = L - d * tca;
     float rad = g.w - dot3(p, p);
-    if (rad < -1e-7f) return INFINITY;
-    rad = fmaxf(rad, 0.f);
-    float t = tca - sqrtf(rad);
-    if (t < 0.f) return INFINITY;
-    return t;
+    float t = tca - sqrtf(fmaxf(rad, 0.f));
+    bool hit = (tca >= 0.f) & (rad >= -1e-7f) & (t >= 0.f);
+    return hit ? t : INFINITY;
 }
 
 // geometry.py:108-117
-__device__ __forceinline__ float ray_plane(float3 o, float3 d, float h) {
-    if (d.y == 0.f) return INFINITY;
+__device__ __forceinline__ float plane_t(float3 o, float3 d, float h) {
     float t = (h - o.y) / d.y;
-    if (t <= 0.f) return INFINITY;
-    return t;
+    return (d.y != 0.f && t > 0.f) ? t : INFINITY;
 }
 
-__device__ __forceinline__ float intersect(float3 o, float3 d, float4 g) {
-    return g.w >= 0.f ? ray_sphere(o, d, g) : ray_plane(o, d, g.y);
+// occluded_packed's per-sphere predicate: intersect(...) < limit, sqrt-free,
+// with L = centre - origin.
+__device__ __forceinline__ bool sphere_blocks_L(float3 L, float3 d, float r2, float limit) {
+    float tca = L.x * d.x + L.y * d.y + L.z * d.z;
+    float px = fmaf(-tca, d.x, L.x), py = fmaf(-tca, d.y, L.y), pz = fmaf(-tca, d.z, L.z);
+    float rad = r2 - (px * px + py * py + pz * pz);
+    float radc = fmaxf(rad, 0.f);
+    float q = tca - limit;
+    bool front = (tca >= 0.f) & (rad >= -1e-7f) & (tca * tca >= radc);
+    return front & ((q < 0.f) | (q * q < radc));
 }
 
-// renderer.py:82-105; occluded_packed (geometry.py:204-210) is an any-hit
-// loop whose result does not depend on body order.
-__device__ float shadow_coeff(float3 surface, float3 normal, const float4 *__restrict__ geo,
-                              const SceneArgs<float> &sa, int n) {
-    float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
-    float3 origin = surface + normal * 1e-3f;
-    float3 bu = f3(1.f, 0.f, 0.f), bv = f3(0.f, 0.f, 1.f);
-    if (n > 1) {  // shading.py:76-86
-        float3 axis = normalize3(surface - lp);
-        float3 c = cross3(axis, f3(0.f, 1.f, 0.f));
-        float m2 = dot3(c, c);
-        if (m2 >= 1e-18f) bu = c * rsqrtf(m2);
-        bv = cross3(axis, bu);
-    }
-    const float2 *__restrict__ tab = reinterpret_cast<const float2 *>(sa.table);
-    int unblocked = 0;
-    for (int i = 0; i < n; i++) {
-        float3 s = lp;
-        if (n > 1) {
-            float2 ab = __ldg(tab + i);
-            s = lp + bu * ab.x + bv * ab.y;
-        }
-        float3 dir = normalize3(s - origin);
-        float3 e = surface - s;
-        float limit = sqrtf(dot3(e, e));
-        bool blocked = false;
-        for (int b = 0; b < sa.n; b++) {
-            if (intersect(origin, dir, geo[b]) < limit) {
-                blocked = true;
-                break;
+__device__ __forceinline__ bool sphere_blocks(float3 o, float3 d, float4 g, float limit) {
+    return sphere_blocks_L(f3(g.x - o.x, g.y - o.y, g.z - o.z), d, g.w, limit);
+}
+
+// ... and per plane: 0 < num/dy < limit with num = h - o.y, division-free.
+__device__ __forceinline__ bool plane_blocks(float num, float dy, float limit) {
+    return (num * dy > 0.f) & (fabsf(num) < limit * fabsf(dy));
+}
+
+// A closest hit: original body index (tie-break and materials), distance,
+// and the sphere centre (planes: w < 0).
+struct Hit {
+    int idx;
+    float t;
+    float4 g;
+};
+
+// --- scene accessors ---------------------------------------------------------------
+
+// Scene in the launch parameters: spheres in original relative order, planes
+// likewise, with their original indices for the lowest-index tie-break.
+template <int MAXS>
+struct ParamScene {
+    float4 sph[MAXS];
+    int sph_idx[MAXS];
+    float pl_h[kMaxPlanes];
+    int pl_idx[kMaxPlanes];
+    int ns, np;
+
+    __device__ __forceinline__ Hit closest(float3 o, float3 d) const {
+        Hit h{-1, INFINITY, make_float4(0.f, 0.f, 0.f, -1.f)};
+        int slot = -1;
+#pragma unroll(MAXS <= 8 ? MAXS : 4)
+        for (int b = 0; b < MAXS; b++) {
+            if (b >= ns) break;
+            float t = sphere_t(o, d, sph[b]);
+            if (t < h.t) {  // spheres ascend in original index: strict '<' keeps the lowest
+                h.t = t;
+                slot = b;
             }
         }
-        unblocked += blocked ? 0 : 1;
+        if (slot >= 0) {
+            h.idx = sph_idx[slot];
+            h.g = sph[slot];
+        }
+#pragma unroll
+        for (int j = 0; j < kMaxPlanes; j++) {
+            if (j >= np) break;
+            float t = plane_t(o, d, pl_h[j]);
+            if (t < h.t || (t == h.t && pl_idx[j] < h.idx)) {  // geometry.py:198 across kinds
+                h.t = t;
+                h.idx = pl_idx[j];
+                h.g = make_float4(0.f, pl_h[j], 0.f, -1.f);
+            }
+        }
+        return h;
+    }
+
+    // Per-hit constants of the any-hit loop: the shadow origin is shared by
+    // all samples of a hit, so L = c - o (and h - o.y) are formed once.
+    struct Local {
+        float3 o;
+        float3 L[MAXS <= 8 ? MAXS : 1];
+        float num[kMaxPlanes];
+    };
+
+    __device__ __forceinline__ Local localize(float3 o) const {
+        Local lc;
+        lc.o = o;
+        if constexpr (MAXS <= 8) {
+#pragma unroll
+            for (int b = 0; b < MAXS; b++) lc.L[b] = f3(sph[b].x - o.x, sph[b].y - o.y, sph[b].z - o.z);
+        }
+#pragma unroll
+        for (int j = 0; j < kMaxPlanes; j++) lc.num[j] = pl_h[j] - o.y;
+        return lc;
+    }
+
+    __device__ __forceinline__ bool occluded(const Local &lc, float3 d, float limit) const {
+        bool blocked = false;
+#pragma unroll
+        for (int j = 0; j < kMaxPlanes; j++) {
+            if (j >= np) break;
+            blocked |= plane_blocks(lc.num[j], d.y, limit);
+        }
+        if constexpr (MAXS <= 8) {
+#pragma unroll
+            for (int b = 0; b < MAXS; b++) {
+                if (b >= ns) break;
+                blocked |= sphere_blocks_L(lc.L[b], d, sph[b].w, limit);
+            }
+        } else {
+#pragma unroll 4
+            for (int b = 0; b < MAXS; b++) {
+                if (b >= ns) break;
+                blocked |= sphere_blocks(lc.o, d, sph[b], limit);
+                if ((b & 3) == 3 && blocked) break;
+            }
+        }
+        return blocked;
+    }
+};
+
+// Scene in shared memory / global memory in the reference's order:
+// {cx, cy, cz, r^2} spheres, {0, h, 0, -1} planes.
+struct MemScene {
+    const float4 *__restrict__ geo;
+    int n;
+
+    __device__ __forceinline__ Hit closest(float3 o, float3 d) const {
+        Hit h{-1, INFINITY, make_float4(0.f, 0.f, 0.f, -1.f)};
+        for (int b = 0; b < n; b++) {
+            float4 g = geo[b];
+            float t = g.w >= 0.f ? sphere_t(o, d, g) : plane_t(o, d, g.y);
+            if (t < h.t) {
+                h.t = t;
+                h.idx = b;
+                h.g = g;
+            }
+        }
+        return h;
+    }
+
+    struct Local {
+        float3 o;
+    };
+    __device__ __forceinline__ Local localize(float3 o) const { return Local{o}; }
+
+    __device__ __forceinline__ bool occluded(const Local &lc, float3 d, float limit) const {
+        for (int b = 0; b < n; b++) {
+            float4 g = geo[b];
+            bool blk = g.w >= 0.f ? sphere_blocks(lc.o, d, g, limit) : plane_blocks(g.y - lc.o.y, d.y, limit);
+            if (blk) return true;
+        }
+        return false;
+    }
+};
+
+// renderer.py:82-105 (+ shading.py:76-86 disc basis, 89-100 disc points)
+template <class Geo>
+__device__ float shadow_coeff(const Geo &geo, float3 surface, float3 normal, const SceneArgs<float> &sa, int n) {
+    float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
+    float3 origin = surface + normal * 1e-3f;
+    if (n == 1) {
+        float3 dir = normalize3(lp - origin);
+        float3 e = surface - lp;
+        float l2 = dot3(e, e);
+        float limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
+        return geo.occluded(geo.localize(origin), dir, limit) ? 0.f : 1.f;
+    }
+    float3 axis = normalize3(surface - lp);
+    float3 c = cross3(axis, f3(0.f, 1.f, 0.f));
+    float m2 = dot3(c, c);
+    float3 bu = m2 >= 1e-18f ? c * rsqrtf(m2) : f3(1.f, 0.f, 0.f);
+    float3 bv = cross3(axis, bu);
+    // shadow ray i: dir = normalize(s_i - origin), limit = |surface - s_i|,
+    // with s_i = lp + a_i bu + b_i bv; both share lp - origin / surface - lp.
+    float3 lo = lp - origin;
+    float3 ls = surface - lp;
+    const float2 *__restrict__ tab = reinterpret_cast<const float2 *>(sa.table);
+    const auto lc = geo.localize(origin);
+    int unblocked = 0;
+#pragma unroll 2
+    for (int i = 0; i < n; i++) {
+        float2 ab = __ldg(tab + i);
+        float3 off = bu * ab.x + bv * ab.y;
+        float3 dv = lo + off;
+        float r2 = dot3(dv, dv);
+        float3 dir = dv * (r2 > 0.f ? rsqrtf(r2) : 0.f);
+        float3 e = ls - off;
+        float l2 = dot3(e, e);
+        float limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
+        unblocked += geo.occluded(lc, dir, limit) ? 0 : 1;
     }
     return (float)unblocked / (float)n;
 }
@@ -132,48 +287,43 @@ __device__ float3 sky_sample(float3 d, const float4 *__restrict__ sky, int W, in
 
 __device__ __forceinline__ float clamp01(float x) { return fminf(fmaxf(x, 0.f), 1.f); }
 
-// renderer.py:108-224 with records (body, lum, spec) — see render_f64.cu.
-template <int BMAX>
-__device__ float3 trace(float3 origin, float3 dir, const float4 *__restrict__ geo, const SceneArgs<float> &sa,
-                        int samples, int bounces) {
+// renderer.py:108-224.  A record keeps (body, lum, spec): shade_color's
+// luminance and specular terms (shading.py:159-165) depend only on the hit,
+// so the unwind only mixes, scales and clamps.  The bounce loop is not
+// unrolled (it would copy the shadow loop per bounce); the 12-byte records
+// live in L1-resident local memory.
+template <int BMAX, class Geo>
+__device__ float3 trace(const Geo &geo, float3 origin, float3 dir, const SceneArgs<float> &sa, int samples,
+                        int bounces) {
     int ridx[BMAX + 1];
     float rlum[BMAX + 1], rspec[BMAX + 1];
     int m = 0;
     bool exhausted = false;
     float3 tail = f3(0.f, 0.f, 0.f);
     float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
-#pragma unroll(BMAX <= 8 ? BMAX + 1 : 1)
+#pragma unroll 1
     for (int k = 0; k <= BMAX; k++) {
         if (k > bounces) break;
-        float best_t = INFINITY;
-        int idx = -1;
-        for (int b = 0; b < sa.n; b++) {
-            float t = intersect(origin, dir, geo[b]);
-            if (t < best_t) {
-                best_t = t;
-                idx = b;
-            }
-        }
-        if (idx < 0) {
+        Hit h = geo.closest(origin, dir);
+        if (h.idx < 0) {
             if (sa.has_sky) tail = sky_sample(dir, sa.sky, sa.sky_w, sa.sky_h);
             break;
         }
-        float4 g = geo[idx];
-        float3 hit = origin + dir * best_t;
-        float3 normal = g.w >= 0.f ? normalize3(hit - f3(g.x, g.y, g.z)) : f3(0.f, 1.f, 0.f);
+        float3 hit = origin + dir * h.t;
+        float3 normal = h.g.w >= 0.f ? normalize3(hit - f3(h.g.x, h.g.y, h.g.z)) : f3(0.f, 1.f, 0.f);
         float3 l = normalize3(lp - hit);
-        float sc = shadow_coeff(hit, normal, geo, sa, samples);
+        float sc = shadow_coeff(geo, hit, normal, sa, samples);
         // shading.py:53-73, 159-162 (view = -dir)
         float dfs = fmaxf(dot3(normal, l), 0.f);
-        float3 h = l - dir;
-        float hm2 = dot3(h, h);
+        float3 hv = l - dir;
+        float hm2 = dot3(hv, hv);
         float s = 0.f;
         if (hm2 > 0.f) {
-            float dd = fmaxf(dot3(normal, h) * rsqrtf(hm2), 0.f);
-            s = powf(dd, __ldg(sa.mat + 8 * idx + 4));
+            float dd = fmaxf(dot3(normal, hv) * rsqrtf(hm2), 0.f);
+            s = powf(dd, __ldg(sa.mat + 8 * h.idx + 4));
         }
         float lum = fminf(sa.ambient + sc * dfs * (1.f - sa.ambient), 1.f);
-        ridx[k] = idx;
+        ridx[k] = h.idx;
         rlum[k] = lum;
         rspec[k] = sc * s;
         m = k + 1;
@@ -185,9 +335,8 @@ __device__ float3 trace(float3 origin, float3 dir, const float4 *__restrict__ ge
         dir = dir - normal * (2.f * dot3(normal, dir));
     }
     float3 col = tail;
-#pragma unroll(BMAX <= 8 ? BMAX + 1 : 1)
-    for (int k = BMAX; k >= 0; k--) {
-        if (k >= m) continue;
+#pragma unroll 1
+    for (int k = m - 1; k >= 0; k--) {
         const float4 mt = __ldg(reinterpret_cast<const float4 *>(sa.mat + 8 * ridx[k]));
         float br = mt.x, bg = mt.y, bb = mt.z;
         if (!(exhausted && k == m - 1)) {
@@ -203,28 +352,17 @@ __device__ float3 trace(float3 origin, float3 dir, const float4 *__restrict__ ge
     return col;
 }
 
-template <bool SMEM>
-__device__ __forceinline__ const float4 *stage_geo(const SceneArgs<float> &sa, float4 *smem) {
-    const float4 *g = reinterpret_cast<const float4 *>(sa.geo);
-    if constexpr (!SMEM) return g;
-    else {
-    for (int i = threadIdx.x; i < sa.n; i += blockDim.x) smem[i] = g[i];
-    __syncthreads();
-    return smem;
-    }
-}
-
-template <int BMAX, bool SMEM>
-__global__ void __launch_bounds__(kThreads) render_f32_kernel(const FrameArgs fa, const SceneArgs<float> sa) {
-    extern __shared__ float4 smem_geo[];
-    const float4 *__restrict__ geo = stage_geo<SMEM>(sa, smem_geo);
+template <int BMAX, class Geo>
+__device__ __forceinline__ void shade_pixel(const Geo &geo, const FrameArgs &fa, const SceneArgs<float> &sa) {
     int x, ly;
     thread_pixel(x, ly);
+    // heavy tiles first: the scene sits in the lower rows, sky tiles fill the tail
+    ly += (int)(gridDim.y - 1 - 2 * blockIdx.y) * kTileH;
     if (x >= fa.width || ly >= fa.local_rows) return;
     int y = map_row(ly, fa);
     if (y >= fa.height) return;
     float3 dir = primary_direction(x, y, fa);
-    float3 c = trace<BMAX>(f3((float)fa.cam[0], (float)fa.cam[1], (float)fa.cam[2]), dir, geo, sa, fa.samples,
+    float3 c = trace<BMAX>(geo, f3((float)fa.cam[0], (float)fa.cam[1], (float)fa.cam[2]), dir, sa, fa.samples,
                            fa.bounces);
     fa.out[(int64_t)y * fa.out_pitch + x] = pack_color(c.x, c.y, c.z);
     if (fa.radiance) {
@@ -236,16 +374,32 @@ __global__ void __launch_bounds__(kThreads) render_f32_kernel(const FrameArgs fa
     if (fa.peer_out) __threadfence_system();  // frame stores over NVLink land before the kernel retires
 }
 
-template <int BMAX, bool SMEM>
+template <int BMAX, int MAXS>
 __global__ void __launch_bounds__(kThreads)
-    trace_f32_kernel(const double *orig, const double *dirs, int64_t n_rays, float *out, const SceneArgs<float> sa,
-                     int samples, int bounces) {
+    render_f32_param_kernel(const FrameArgs fa, const SceneArgs<float> sa, const ParamScene<MAXS> ps) {
+    shade_pixel<BMAX>(ps, fa, sa);
+}
+
+template <int BMAX, bool SMEM>
+__global__ void __launch_bounds__(kThreads) render_f32_kernel(const FrameArgs fa, const SceneArgs<float> sa) {
     extern __shared__ float4 smem_geo[];
-    const float4 *__restrict__ geo = stage_geo<SMEM>(sa, smem_geo);
+    MemScene geo{reinterpret_cast<const float4 *>(sa.geo), sa.n};
+    if constexpr (SMEM) {
+        for (int i = threadIdx.x; i < sa.n; i += blockDim.x) smem_geo[i] = geo.geo[i];
+        __syncthreads();
+        geo.geo = smem_geo;
+    }
+    shade_pixel<BMAX>(geo, fa, sa);
+}
+
+template <int BMAX, int MAXS>
+__global__ void __launch_bounds__(kThreads)
+    trace_f32_param_kernel(const double *orig, const double *dirs, int64_t n_rays, float *out,
+                           const SceneArgs<float> sa, int samples, int bounces, const ParamScene<MAXS> ps) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_rays) return;
-    float3 c = trace<BMAX>(f3((float)orig[3 * i], (float)orig[3 * i + 1], (float)orig[3 * i + 2]),
-                           f3((float)dirs[3 * i], (float)dirs[3 * i + 1], (float)dirs[3 * i + 2]), geo, sa, samples,
+    float3 c = trace<BMAX>(ps, f3((float)orig[3 * i], (float)orig[3 * i + 1], (float)orig[3 * i + 2]),
+                           f3((float)dirs[3 * i], (float)dirs[3 * i + 1], (float)dirs[3 * i + 2]), sa, samples,
                            bounces);
     out[3 * i] = c.x;
     out[3 * i + 1] = c.y;
@@ -253,8 +407,65 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 template <int BMAX>
+__global__ void __launch_bounds__(kThreads)
+    trace_f32_kernel(const double *orig, const double *dirs, int64_t n_rays, float *out, const SceneArgs<float> sa,
+                     int samples, int bounces) {
+    MemScene geo{reinterpret_cast<const float4 *>(sa.geo), sa.n};
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_rays) return;
+    float3 c = trace<BMAX>(geo, f3((float)orig[3 * i], (float)orig[3 * i + 1], (float)orig[3 * i + 2]),
+                           f3((float)dirs[3 * i], (float)dirs[3 * i + 1], (float)dirs[3 * i + 2]), sa, samples,
+                           bounces);
+    out[3 * i] = c.x;
+    out[3 * i + 1] = c.y;
+    out[3 * i + 2] = c.z;
+}
+
+// Pack the host scene (float64 geo) into the launch-parameter layout; false
+// if it does not fit.
+template <int MAXS>
+bool pack_params(const SceneArgs<float> &sa, ParamScene<MAXS> &ps) {
+    ps.ns = ps.np = 0;
+    for (int b = 0; b < sa.n; b++) {
+        const double *g = sa.host_geo + 4 * b;
+        if (g[3] >= 0.0) {
+            if (ps.ns == MAXS) return false;
+            ps.sph[ps.ns] = make_float4((float)g[0], (float)g[1], (float)g[2], (float)g[3]);
+            ps.sph_idx[ps.ns++] = b;
+        } else {
+            if (ps.np == kMaxPlanes) return false;
+            ps.pl_h[ps.np] = (float)g[1];
+            ps.pl_idx[ps.np++] = b;
+        }
+    }
+    for (int b = ps.ns; b < MAXS; b++) {
+        ps.sph[b] = make_float4(0.f, 0.f, 0.f, 0.f);
+        ps.sph_idx[b] = 0;
+    }
+    for (int j = ps.np; j < kMaxPlanes; j++) {
+        ps.pl_h[j] = 0.f;
+        ps.pl_idx[j] = 0;
+    }
+    return true;
+}
+
+template <int BMAX>
 cudaError_t launch_render(const FrameArgs &fa, const SceneArgs<float> &sa, cudaStream_t st) {
     dim3 grid((fa.width + kTileW - 1) / kTileW, (fa.local_rows + kTileH - 1) / kTileH);
+    {
+        ParamScene<8> ps;
+        if (pack_params(sa, ps)) {
+            render_f32_param_kernel<BMAX, 8><<<grid, kThreads, 0, st>>>(fa, sa, ps);
+            return cudaGetLastError();
+        }
+    }
+    {
+        thread_local ParamScene<kParamSpheres> ps;  // 5 KB: keep it off the stack
+        if (pack_params(sa, ps)) {
+            render_f32_param_kernel<BMAX, kParamSpheres><<<grid, kThreads, 0, st>>>(fa, sa, ps);
+            return cudaGetLastError();
+        }
+    }
     size_t geo_bytes = sizeof(float4) * (size_t)sa.n;
     if (geo_bytes <= (size_t)kSmemGeoBytes)
         render_f32_kernel<BMAX, true><<<grid, kThreads, geo_bytes, st>>>(fa, sa);
@@ -267,26 +478,25 @@ template <int BMAX>
 cudaError_t launch_trace(const double *o, const double *d, int64_t n, float *out, const SceneArgs<float> &sa,
                          int samples, int bounces, cudaStream_t st) {
     unsigned blocks = (unsigned)((n + kThreads - 1) / kThreads);
-    size_t geo_bytes = sizeof(float4) * (size_t)sa.n;
-    if (geo_bytes <= (size_t)kSmemGeoBytes)
-        trace_f32_kernel<BMAX, true><<<blocks, kThreads, geo_bytes, st>>>(o, d, n, out, sa, samples, bounces);
-    else
-        trace_f32_kernel<BMAX, false><<<blocks, kThreads, 0, st>>>(o, d, n, out, sa, samples, bounces);
+    {
+        ParamScene<8> ps;
+        if (pack_params(sa, ps)) {
+            trace_f32_param_kernel<BMAX, 8><<<blocks, kThreads, 0, st>>>(o, d, n, out, sa, samples, bounces, ps);
+            return cudaGetLastError();
+        }
+    }
+    trace_f32_kernel<BMAX><<<blocks, kThreads, 0, st>>>(o, d, n, out, sa, samples, bounces);
     return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t rt_launch_render_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, cudaStream_t st) {
-    if (fa.bounces <= 1) return launch_render<1>(fa, sa, st);
-    if (fa.bounces <= 3) return launch_render<3>(fa, sa, st);
-    if (fa.bounces <= 8) return launch_render<8>(fa, sa, st);
     return launch_render<rt::kMaxBounce>(fa, sa, st);
 }
 
 cudaError_t rt_launch_trace_f32(const double *o, const double *d, int64_t n, float *out,
                                 const rt::SceneArgs<float> &sa, int samples, int bounces, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
-    if (bounces <= 3) return launch_trace<3>(o, d, n, out, sa, samples, bounces, st);
     return launch_trace<rt::kMaxBounce>(o, d, n, out, sa, samples, bounces, st);
 }

@@ -51,6 +51,7 @@ struct SceneArgs {
     R light_radius;
     R lc[3];
     R ambient;
+    const double *host_geo;  // host copy of geo (float64), for launch-parameter scene packing
 };
 
 // Row-block interleave: local row ly of partition `part` -> frame row.

@@ -314,6 +314,7 @@ rt::SceneArgs<R> scene_args(const Dev &d, const DevScene<R> &ds, const HostScene
     }
     a.light_radius = (R)s.light_radius;
     a.ambient = (R)s.ambient;
+    a.host_geo = s.geo.data();
     return a;
 }
 

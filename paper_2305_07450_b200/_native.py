@@ -15,7 +15,7 @@ import threading
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libb200rt.so")
+LIB_PATH = os.environ.get("B200RT_LIB") or os.path.join(_PKG, "libb200rt.so")
 
 RT_OK = 0
 RT_ERR_INVALID = -1

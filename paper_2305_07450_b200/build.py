@@ -45,32 +45,40 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = False, defines=(), out=None) -> str:
+    """Compile (incrementally) and link libb200rt.so.  `defines` (e.g.
+    ["RT_F32_MIN_BLOCKS=6"]) and `out` build an experimental variant into a
+    separate object directory."""
     if not os.path.exists(NVCC) and shutil.which("nvcc") is None:
         raise RuntimeError("nvcc not found: cannot build libb200rt.so")
     nvcc = NVCC if os.path.exists(NVCC) else shutil.which("nvcc")
-    os.makedirs(BUILD, exist_ok=True)
+    lib = out or LIB
+    bdir = BUILD if not defines else os.path.join(BUILD, "v_" + "_".join(d.replace("=", "") for d in defines))
+    os.makedirs(bdir, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
     headers = [os.path.join(CSRC, "rt_device.cuh"), os.path.join(INCLUDE, "b200rt.h")]
     objs = []
     for src, extra in SOURCES.items():
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(bdir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s, *headers, __file__]):
-            cmd = [nvcc, *_ccbin(), *COMMON, *extra, "-c", s, "-o", o]
+            cmd = [nvcc, *_ccbin(), *COMMON, *extra, *dflags, "-c", s, "-o", o]
             if ptxas_verbose:
                 cmd += ["-Xptxas", "-v"]
             if verbose:
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
-    if force or _stale(LIB, objs):
-        cmd = [nvcc, *_ccbin(), *ARCH, "-shared", "-o", LIB, *objs]
+    if force or _stale(lib, objs):
+        cmd = [nvcc, *_ccbin(), *ARCH, "-shared", "-o", lib, *objs]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(verbose="-v" in sys.argv, force="-f" in sys.argv, ptxas_verbose="--ptxas" in sys.argv)
-    print(LIB)
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, ptxas_verbose="--ptxas" in sys.argv,
+                defines=defs, out=outs[0] if outs else None))

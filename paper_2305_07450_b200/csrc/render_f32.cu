@@ -28,6 +28,10 @@
 namespace {
 using namespace rt;
 
+#ifndef RT_F32_MIN_BLOCKS
+#define RT_F32_MIN_BLOCKS 1  // __launch_bounds__ minimum resident CTAs per SM (register cap)
+#endif
+
 constexpr int kMaxPlanes = 8;
 constexpr int kParamSpheres = 256;
 
@@ -371,11 +375,8 @@ __device__ float3 trace(const Geo &geo, float3 origin, float3 dir, const SceneAr
 }
 
 template <int BMAX, class Geo>
-__device__ __forceinline__ void shade_pixel(const Geo &geo, const FrameArgs &fa, const SceneArgs<float> &sa) {
-    int x, ly;
-    thread_pixel(x, ly);
-    // heavy tiles first: the scene sits in the lower rows, sky tiles fill the tail
-    ly += (int)(gridDim.y - 1 - 2 * blockIdx.y) * kTileH;
+__device__ __forceinline__ void shade_pixel(const Geo &geo, const FrameArgs &fa, const SceneArgs<float> &sa, int x,
+                                            int ly) {
     if (x >= fa.width || ly >= fa.local_rows) return;
     int y = map_row(ly, fa);
     if (y >= fa.height) return;
@@ -389,13 +390,37 @@ __device__ __forceinline__ void shade_pixel(const Geo &geo, const FrameArgs &fa,
         r[1] = c.y;
         r[2] = c.z;
     }
+}
+
+// Persistent warps: every warp takes 8x4-pixel patches from a frame-wide
+// counter until the frame is done.  A patch's cost ranges from a handful of
+// instructions (sky) to ~10^5 per lane (four soft-shadowed hits), so
+// scheduling per warp instead of per CTA keeps every SM busy to the end;
+// patches are handed out bottom rows first (the scene, below the horizon)
+// so the cheap sky patches fill the tail.
+template <int BMAX, class Geo>
+__device__ __forceinline__ void render_patches(const Geo &geo, const FrameArgs &fa, const SceneArgs<float> &sa) {
+    const int lane = threadIdx.x & 31;
+    const int pw = (fa.width + 7) >> 3;
+    const int ph = (fa.local_rows + 3) >> 2;
+    const unsigned n_patches = (unsigned)pw * (unsigned)ph;
+    for (;;) {
+        unsigned p = 0;
+        if (lane == 0) p = atomicAdd(fa.work_counter, 1u);
+        p = __shfl_sync(0xffffffffu, p, 0);
+        if (p >= n_patches) break;
+        int prow = ph - 1 - (int)(p / (unsigned)pw);
+        int pcol = (int)(p % (unsigned)pw);
+        shade_pixel<BMAX>(geo, fa, sa, pcol * 8 + (lane & 7), prow * 4 + (lane >> 3));
+        __syncwarp();
+    }
     if (fa.peer_out) __threadfence_system();  // frame stores over NVLink land before the kernel retires
 }
 
 template <int BMAX, int MAXS>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, RT_F32_MIN_BLOCKS)
     render_f32_param_kernel(const FrameArgs fa, const SceneArgs<float> sa, const ParamScene<MAXS> ps) {
-    shade_pixel<BMAX>(ps, fa, sa);
+    render_patches<BMAX>(ps, fa, sa);
 }
 
 template <int BMAX, bool SMEM>
@@ -407,7 +432,7 @@ __global__ void __launch_bounds__(kThreads) render_f32_kernel(const FrameArgs fa
         __syncthreads();
         geo.geo = smem_geo;
     }
-    shade_pixel<BMAX>(geo, fa, sa);
+    render_patches<BMAX>(geo, fa, sa);
 }
 
 template <int BMAX, int MAXS>
@@ -467,28 +492,45 @@ bool pack_params(const SceneArgs<float> &sa, ParamScene<MAXS> &ps) {
     return true;
 }
 
+// Persistent grid: as many CTAs as fit on the device at once.
+template <typename K>
+int resident_ctas(K kernel, size_t smem) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+    return sms * (per_sm > 0 ? per_sm : 1);
+}
+
 template <int BMAX>
 cudaError_t launch_render(const FrameArgs &fa, const SceneArgs<float> &sa, cudaStream_t st) {
-    dim3 grid((fa.width + kTileW - 1) / kTileW, (fa.local_rows + kTileH - 1) / kTileH);
     {
         ParamScene<8> ps;
         if (pack_params(sa, ps)) {
-            render_f32_param_kernel<BMAX, 8><<<grid, kThreads, 0, st>>>(fa, sa, ps);
+            static thread_local int ctas = 0;
+            if (!ctas) ctas = resident_ctas(render_f32_param_kernel<BMAX, 8>, 0);
+            render_f32_param_kernel<BMAX, 8><<<ctas, kThreads, 0, st>>>(fa, sa, ps);
             return cudaGetLastError();
         }
     }
     {
         thread_local ParamScene<kParamSpheres> ps;  // 5 KB: keep it off the stack
         if (pack_params(sa, ps)) {
-            render_f32_param_kernel<BMAX, kParamSpheres><<<grid, kThreads, 0, st>>>(fa, sa, ps);
+            static thread_local int ctas = 0;
+            if (!ctas) ctas = resident_ctas(render_f32_param_kernel<BMAX, kParamSpheres>, 0);
+            render_f32_param_kernel<BMAX, kParamSpheres><<<ctas, kThreads, 0, st>>>(fa, sa, ps);
             return cudaGetLastError();
         }
     }
     size_t geo_bytes = sizeof(float4) * (size_t)sa.n;
-    if (geo_bytes <= (size_t)kSmemGeoBytes)
-        render_f32_kernel<BMAX, true><<<grid, kThreads, geo_bytes, st>>>(fa, sa);
-    else
-        render_f32_kernel<BMAX, false><<<grid, kThreads, 0, st>>>(fa, sa);
+    if (geo_bytes <= (size_t)kSmemGeoBytes) {
+        int ctas = resident_ctas(render_f32_kernel<BMAX, true>, geo_bytes);
+        render_f32_kernel<BMAX, true><<<ctas, kThreads, geo_bytes, st>>>(fa, sa);
+    } else {
+        static thread_local int ctas = 0;
+        if (!ctas) ctas = resident_ctas(render_f32_kernel<BMAX, false>, 0);
+        render_f32_kernel<BMAX, false><<<ctas, kThreads, 0, st>>>(fa, sa);
+    }
     return cudaGetLastError();
 }
 

@@ -23,6 +23,7 @@ constexpr int kTileW = 16;      // CTA tile: 16 x 8 pixels, 4 warps of 8 x 4
 constexpr int kTileH = 8;
 constexpr int kThreads = 128;
 constexpr int kSmemGeoBytes = 32 * 1024;  // scenes up to this size are staged in shared memory
+constexpr int kCounterRing = 64;          // work counters per device (one per in-flight launch)
 
 // Camera + frame + partition (one launch renders one row-block partition).
 struct FrameArgs {
@@ -37,6 +38,7 @@ struct FrameArgs {
     double vdist;           // camera.py:64-67
     int samples, bounces;
     int peer_out;  // out lives on another GPU: fence the stores at system scope
+    unsigned int *work_counter;  // zeroed before the launch: persistent warps take 8x4 patches from it
 };
 
 template <typename R>

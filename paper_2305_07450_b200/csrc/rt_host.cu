@@ -81,7 +81,8 @@ struct Dev {
     int id = 0;
     cudaStream_t st = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    DBuf frame, rad, rays_in, rays_out, sky_raw, sky;
+    DBuf frame, rad, rays_in, rays_out, sky_raw, sky, counters;
+    unsigned counter_slot = 0;
     uint64_t sky_version = ~0ull;
     DevScene<float> s32;
     DevScene<double> s64;
@@ -357,12 +358,17 @@ rt::FrameArgs frame_args(uint32_t *out, int64_t pitch, void *rad, int w, int h, 
     fa.samples = samples;
     fa.bounces = bounces;
     fa.peer_out = 0;
+    fa.work_counter = nullptr;
     return fa;
 }
 
-int launch_frame(rt_ctx *ctx, Dev &d, const rt::FrameArgs &fa, int precision, cudaStream_t st) {
+int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStream_t st) {
     cudaError_t e;
     if (fa.local_rows == 0) return RT_OK;
+    int rc = d.counters.ensure(sizeof(unsigned) * rt::kCounterRing);
+    if (rc) return rc;
+    fa.work_counter = (unsigned *)d.counters.p + (d.counter_slot++ % rt::kCounterRing);
+    RT_CK(cudaMemsetAsync(fa.work_counter, 0, sizeof(unsigned), st));
     if (precision == RT_PREC_FP64)
         e = rt_launch_render_f64(fa, scene_args(d, d.s64, ctx->scene), st);
     else
@@ -437,7 +443,7 @@ int rt_ctx_destroy(rt_ctx *ctx) {
     for (Dev &d : ctx->devs) {
         cudaSetDevice(d.id);
         if (d.st) cudaStreamSynchronize(d.st);
-        for (DBuf *b : {&d.frame, &d.rad, &d.rays_in, &d.rays_out, &d.sky_raw, &d.sky, &d.s32.geo, &d.s32.mat,
+        for (DBuf *b : {&d.frame, &d.rad, &d.rays_in, &d.rays_out, &d.sky_raw, &d.sky, &d.counters, &d.s32.geo, &d.s32.mat,
                         &d.s32.table, &d.s64.geo, &d.s64.mat, &d.s64.table})
             b->release();
         if (d.e0) cudaEventDestroy(d.e0);

@@ -1,0 +1,39 @@
+"""Median device time of the render kernel per configuration (A/B runs:
+select the library with $B200RT_LIB).
+
+    python tools/ab_kernel.py C2 C4 P720 [--frames 20] [--precision fp32]
+"""
+
+import argparse
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_2305_07450_b200 as rt  # noqa: E402
+from paper_2305_07450_b200 import _native  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="*", default=["C2", "C4"])
+    ap.add_argument("--frames", type=int, default=20)
+    ap.add_argument("--precision", default="fp32")
+    a = ap.parse_args()
+    tag = os.path.basename(_native.LIB_PATH)
+    for key in a.configs:
+        cfg = rt.CONFIGS[key]
+        scene, cam, params = cfg.scene(), cfg.camera(), cfg.params()
+        fb = rt.Framebuffer.create(cfg.width, cfg.height)
+        ms = []
+        for i in range(a.frames + 3):
+            rt.render_frame(scene, cam, params, fb, precision=a.precision)
+            if i >= 3:
+                ms.append(rt.last_kernel_ms())
+        print(f"{tag:>14} {key:>6} {a.precision} median {statistics.median(ms):8.4f} ms  min {min(ms):8.4f} ms",
+              flush=True)
+
+
+if __name__ == "__main__":
+    main()

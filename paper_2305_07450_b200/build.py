@@ -30,6 +30,7 @@ SOURCES = {
     # FP32 product path: flush denormals, approximate sqrt/div (powf, atan2f
     # and asinf stay full precision: no --use_fast_math)
     "render_f32.cu": ["--ftz=true", "--prec-div=false", "--prec-sqrt=false"],
+    "render_wave_f32.cu": ["--ftz=true", "--prec-div=false", "--prec-sqrt=false"],
     "render_f64.cu": ["-fmad=false"],
 }
 
@@ -56,7 +57,8 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
     bdir = BUILD if not defines else os.path.join(BUILD, "v_" + "_".join(d.replace("=", "") for d in defines))
     os.makedirs(bdir, exist_ok=True)
     dflags = [f"-D{d}" for d in defines]
-    headers = [os.path.join(CSRC, "rt_device.cuh"), os.path.join(INCLUDE, "b200rt.h")]
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
+    headers.append(os.path.join(INCLUDE, "b200rt.h"))
     objs = []
     for src, extra in SOURCES.items():
         s = os.path.join(CSRC, src)

@@ -23,237 +23,11 @@
 //    the plane test `0 < (h - o.y)/d.y < limit` without the division;
 //  - primary directions are formed in float64 (camera.py:70-77) and rounded;
 //  - the disc-sample table is built in float64 on the host and rounded.
-#include "rt_device.cuh"
+#include "rt_f32.cuh"
 
 namespace {
 using namespace rt;
-
-#ifndef RT_F32_MIN_BLOCKS
-#define RT_F32_MIN_BLOCKS 1  // __launch_bounds__ minimum resident CTAs per SM (register cap)
-#endif
-
-constexpr int kMaxPlanes = 8;
-constexpr int kParamSpheres = 256;
-
-__device__ __forceinline__ float3 f3(float x, float y, float z) { return make_float3(x, y, z); }
-__device__ __forceinline__ float3 operator+(float3 a, float3 b) { return f3(a.x + b.x, a.y + b.y, a.z + b.z); }
-__device__ __forceinline__ float3 operator-(float3 a, float3 b) { return f3(a.x - b.x, a.y - b.y, a.z - b.z); }
-__device__ __forceinline__ float3 operator*(float3 a, float s) { return f3(a.x * s, a.y * s, a.z * s); }
-__device__ __forceinline__ float dot3(float3 a, float3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
-__device__ __forceinline__ float3 cross3(float3 a, float3 b) {
-    return f3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
-}
-// vecmath.py:68-78: zero vector normalises to zero
-__device__ __forceinline__ float3 normalize3(float3 a) {
-    float m2 = dot3(a, a);
-    float inv = m2 > 0.f ? rsqrtf(m2) : 0.f;
-    return a * inv;
-}
-
-// camera.py:46-77 in float64 (exactly the reference's direction), then rounded
-__device__ __forceinline__ float3 primary_direction(int xi, int yi, const FrameArgs &fa) {
-    double x = (double)xi, y = (double)yi, w = (double)fa.width, h = (double)fa.height;
-    double u, v;
-    if (w > h) {
-        u = (x - w / 2 + h / 2) / h * 2 - 1;
-        v = -(y / h * 2 - 1);
-    } else {
-        u = x / w * 2 - 1;
-        v = -((y - h / 2 + w / 2) / w * 2 - 1);
-    }
-    double m = sqrt(u * u + v * v + fa.vdist * fa.vdist);
-    double dx = u / m, dy = v / m, dz = fa.vdist / m;
-    double y2 = dy * fa.cb - dz * fa.sb;
-    double z2 = dy * fa.sb + dz * fa.cb;
-    double x2 = dx * fa.ca + z2 * fa.sa;
-    double z3 = -dx * fa.sa + z2 * fa.ca;
-    return f3((float)x2, (float)y2, (float)z3);
-}
-
-// geometry.py:83-105 — distance to the sphere, +inf on a miss.
-__device__ __forceinline__ float sphere_t(float3 o, float3 d, float4 g) {
-    float3 L = f3(g.x - o.x, g.y - o.y, g.z - o.z);
-    float tca = dot3(L, d);
-    float3 p = L - d * tca;
-    float rad = g.w - dot3(p, p);
-    float t = tca - sqrtf(fmaxf(rad, 0.f));
-    bool hit = (tca >= 0.f) & (rad >= -1e-7f) & (t >= 0.f);
-    return hit ? t : INFINITY;
-}
-
-// geometry.py:108-117
-__device__ __forceinline__ float plane_t(float3 o, float3 d, float h) {
-    float t = (h - o.y) / d.y;
-    return (d.y != 0.f && t > 0.f) ? t : INFINITY;
-}
-
-// occluded_packed's per-body predicate `intersect(...) < limit`
-// (geometry.py:94-117, 204-210) as a signed margin: the body blocks the
-// shadow ray iff the returned value is > 0.  Written with FMA-pipe arithmetic
-// and min/max so a test costs ~13 FMA-pipe and ~4 ALU-pipe instructions and
-// no branch:
-//   sphere: tca >= 0, rad >= -GRAZE, origin outside (tca^2 >= rad), and
-//           t = tca - sqrt(max(rad, 0)) < limit  <=>  min(q, q^2 - rad) < 0, q = tca - limit;
-//   plane:  0 < (h - o.y)/d.y < limit  <=>  min(num*dy, limit*|dy| - |num|) > 0.
-constexpr float kGraze = 1e-7f;  // geometry.py:24
-
-// L = centre - origin; r2g = r^2 + GRAZE, or -inf when the origin is inside
-// the sphere (t < 0 for every direction: it never blocks).
-__device__ __forceinline__ float sphere_margin_L(float3 L, float3 d, float r2g, float limit) {
-    float tca = fmaf(L.z, d.z, fmaf(L.y, d.y, L.x * d.x));
-    float px = fmaf(-tca, d.x, L.x), py = fmaf(-tca, d.y, L.y), pz = fmaf(-tca, d.z, L.z);
-    float radg = fmaf(-pz, pz, fmaf(-py, py, fmaf(-px, px, r2g)));  // rad + GRAZE
-    float q = tca - limit;
-    float e = fmaf(q, q, kGraze) - radg;  // q^2 - rad
-    return fminf(fminf(tca, radg), -fminf(q, e));
-}
-
-__device__ __forceinline__ float sphere_r2g(float3 L, float r2) {
-    return dot3(L, L) >= r2 ? r2 + kGraze : -INFINITY;
-}
-
-__device__ __forceinline__ float sphere_margin(float3 o, float3 d, float4 g, float limit) {
-    float3 L = f3(g.x - o.x, g.y - o.y, g.z - o.z);
-    return sphere_margin_L(L, d, sphere_r2g(L, g.w), limit);
-}
-
-__device__ __forceinline__ float plane_margin(float num, float dy, float limit) {
-    return fminf(num * dy, fmaf(limit, fabsf(dy), -fabsf(num)));
-}
-
-// A closest hit: original body index (tie-break and materials), distance,
-// and the sphere centre (planes: w < 0).
-struct Hit {
-    int idx;
-    float t;
-    float4 g;
-};
-
-// --- scene accessors ---------------------------------------------------------------
-
-// Scene in the launch parameters: spheres in original relative order, planes
-// likewise, with their original indices for the lowest-index tie-break.
-template <int MAXS>
-struct ParamScene {
-    float4 sph[MAXS];
-    int sph_idx[MAXS];
-    float pl_h[kMaxPlanes];
-    int pl_idx[kMaxPlanes];
-    int ns, np;
-
-    __device__ __forceinline__ Hit closest(float3 o, float3 d) const {
-        Hit h{-1, INFINITY, make_float4(0.f, 0.f, 0.f, -1.f)};
-        int slot = -1;
-#pragma unroll(MAXS <= 8 ? MAXS : 4)
-        for (int b = 0; b < MAXS; b++) {
-            if (b >= ns) break;
-            float t = sphere_t(o, d, sph[b]);
-            if (t < h.t) {  // spheres ascend in original index: strict '<' keeps the lowest
-                h.t = t;
-                slot = b;
-            }
-        }
-        if (slot >= 0) {
-            h.idx = sph_idx[slot];
-            h.g = sph[slot];
-        }
-#pragma unroll
-        for (int j = 0; j < kMaxPlanes; j++) {
-            if (j >= np) break;
-            float t = plane_t(o, d, pl_h[j]);
-            if (t < h.t || (t == h.t && pl_idx[j] < h.idx)) {  // geometry.py:198 across kinds
-                h.t = t;
-                h.idx = pl_idx[j];
-                h.g = make_float4(0.f, pl_h[j], 0.f, -1.f);
-            }
-        }
-        return h;
-    }
-
-    // Per-hit constants of the any-hit loop: the shadow origin is shared by
-    // all samples of a hit, so L = c - o, the inside/outside decision and
-    // h - o.y are formed once per hit.
-    struct Local {
-        float3 o;
-        float4 L[MAXS <= 8 ? MAXS : 1];  // xyz = centre - origin, w = r2g
-        float num[kMaxPlanes];
-    };
-
-    __device__ __forceinline__ Local localize(float3 o) const {
-        Local lc;
-        lc.o = o;
-        if constexpr (MAXS <= 8) {
-#pragma unroll
-            for (int b = 0; b < MAXS; b++) {
-                float3 L = f3(sph[b].x - o.x, sph[b].y - o.y, sph[b].z - o.z);
-                lc.L[b] = make_float4(L.x, L.y, L.z, sphere_r2g(L, sph[b].w));
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < kMaxPlanes; j++) lc.num[j] = pl_h[j] - o.y;
-        return lc;
-    }
-
-    __device__ __forceinline__ bool occluded(const Local &lc, float3 d, float limit) const {
-        float m = -INFINITY;
-#pragma unroll
-        for (int j = 0; j < kMaxPlanes; j++) {
-            if (j >= np) break;
-            m = fmaxf(m, plane_margin(lc.num[j], d.y, limit));
-        }
-        if constexpr (MAXS <= 8) {
-#pragma unroll
-            for (int b = 0; b < MAXS; b++) {
-                if (b >= ns) break;
-                float4 L = lc.L[b];
-                m = fmaxf(m, sphere_margin_L(f3(L.x, L.y, L.z), d, L.w, limit));
-            }
-        } else {
-#pragma unroll 4
-            for (int b = 0; b < MAXS; b++) {
-                if (b >= ns) break;
-                m = fmaxf(m, sphere_margin(lc.o, d, sph[b], limit));
-                if ((b & 3) == 3 && m > 0.f) break;
-            }
-        }
-        return m > 0.f;
-    }
-};
-
-// Scene in shared memory / global memory in the reference's order:
-// {cx, cy, cz, r^2} spheres, {0, h, 0, -1} planes.
-struct MemScene {
-    const float4 *__restrict__ geo;
-    int n;
-
-    __device__ __forceinline__ Hit closest(float3 o, float3 d) const {
-        Hit h{-1, INFINITY, make_float4(0.f, 0.f, 0.f, -1.f)};
-        for (int b = 0; b < n; b++) {
-            float4 g = geo[b];
-            float t = g.w >= 0.f ? sphere_t(o, d, g) : plane_t(o, d, g.y);
-            if (t < h.t) {
-                h.t = t;
-                h.idx = b;
-                h.g = g;
-            }
-        }
-        return h;
-    }
-
-    struct Local {
-        float3 o;
-    };
-    __device__ __forceinline__ Local localize(float3 o) const { return Local{o}; }
-
-    __device__ __forceinline__ bool occluded(const Local &lc, float3 d, float limit) const {
-        for (int b = 0; b < n; b++) {
-            float4 g = geo[b];
-            float m = g.w >= 0.f ? sphere_margin(lc.o, d, g, limit) : plane_margin(g.y - lc.o.y, d.y, limit);
-            if (m > 0.f) return true;
-        }
-        return false;
-    }
-};
+using namespace rt32;
 
 // renderer.py:82-105 (+ shading.py:76-86 disc basis, 89-100 disc points)
 template <class Geo>
@@ -267,11 +41,8 @@ __device__ float shadow_coeff(const Geo &geo, float3 surface, float3 normal, con
         float limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
         return geo.occluded(geo.localize(origin), dir, limit) ? 0.f : 1.f;
     }
-    float3 axis = normalize3(surface - lp);
-    float3 c = cross3(axis, f3(0.f, 1.f, 0.f));
-    float m2 = dot3(c, c);
-    float3 bu = m2 >= 1e-18f ? c * rsqrtf(m2) : f3(1.f, 0.f, 0.f);
-    float3 bv = cross3(axis, bu);
+    DiscBasis db = disc_basis(surface, lp);
+    float3 bu = db.bu, bv = db.bv;
     // shadow ray i: dir = normalize(s_i - origin), limit = |surface - s_i|,
     // with s_i = lp + a_i bu + b_i bv; both share lp - origin / surface - lp.
     float3 lo = lp - origin;
@@ -293,21 +64,6 @@ __device__ float shadow_coeff(const Geo &geo, float3 surface, float3 normal, con
     }
     return (float)unblocked / (float)n;
 }
-
-// renderer.py:60-74
-__device__ float3 sky_sample(float3 d, const float4 *__restrict__ sky, int W, int H) {
-    float u = 0.5f + atan2f(d.x, d.z) * 0.15915494309189535f;
-    float dy = fminf(fmaxf(d.y, -1.f), 1.f);
-    float v = 0.5f - asinf(dy) * 0.3183098861837907f;
-    int tx = (int)floorf(u * (float)W);
-    tx = ((tx % W) + W) % W;
-    int ty = (int)floorf(v * (float)H);
-    ty = min(max(ty, 0), H - 1);
-    float4 t = __ldg(sky + (int64_t)ty * W + tx);
-    return f3(t.x, t.y, t.z);
-}
-
-__device__ __forceinline__ float clamp01(float x) { return fminf(fmaxf(x, 0.f), 1.f); }
 
 // renderer.py:108-224.  A record keeps (body, lum, spec): shade_color's
 // luminance and specular terms (shading.py:159-165) depend only on the hit,
@@ -462,44 +218,6 @@ __global__ void __launch_bounds__(kThreads)
     out[3 * i] = c.x;
     out[3 * i + 1] = c.y;
     out[3 * i + 2] = c.z;
-}
-
-// Pack the host scene (float64 geo) into the launch-parameter layout; false
-// if it does not fit.
-template <int MAXS>
-bool pack_params(const SceneArgs<float> &sa, ParamScene<MAXS> &ps) {
-    ps.ns = ps.np = 0;
-    for (int b = 0; b < sa.n; b++) {
-        const double *g = sa.host_geo + 4 * b;
-        if (g[3] >= 0.0) {
-            if (ps.ns == MAXS) return false;
-            ps.sph[ps.ns] = make_float4((float)g[0], (float)g[1], (float)g[2], (float)g[3]);
-            ps.sph_idx[ps.ns++] = b;
-        } else {
-            if (ps.np == kMaxPlanes) return false;
-            ps.pl_h[ps.np] = (float)g[1];
-            ps.pl_idx[ps.np++] = b;
-        }
-    }
-    for (int b = ps.ns; b < MAXS; b++) {
-        ps.sph[b] = make_float4(0.f, 0.f, 0.f, 0.f);
-        ps.sph_idx[b] = 0;
-    }
-    for (int j = ps.np; j < kMaxPlanes; j++) {
-        ps.pl_h[j] = 0.f;
-        ps.pl_idx[j] = 0;
-    }
-    return true;
-}
-
-// Persistent grid: as many CTAs as fit on the device at once.
-template <typename K>
-int resident_ctas(K kernel, size_t smem) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
-    return sms * (per_sm > 0 ? per_sm : 1);
 }
 
 template <int BMAX>

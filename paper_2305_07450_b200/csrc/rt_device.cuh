@@ -56,6 +56,20 @@ struct SceneArgs {
     const double *host_geo;  // host copy of geo (float64), for launch-parameter scene packing
 };
 
+// Wavefront queues (render_wave_f32.cu); slot = bounce * n_pix + local pixel.
+struct WaveArgs {
+    float4 *hit_p;     // {p.xyz, body index bits}
+    float4 *hit_n;     // {n.xyz, Lambert factor}
+    float *hit_s;      // Blinn factor
+    float *hit_sc;     // shadow coefficient
+    int *queue;        // slots holding a hit
+    unsigned *count;   // queue length
+    float4 *pix;       // {tail rgb, records | exhausted << 8}
+    int64_t n_pix;     // pixels of this partition (local_rows * width)
+};
+constexpr int kWaveMinSamples = 8;     // soft shadows at or above this take the wavefront path
+constexpr int kWaveSmemSamples = 4096;  // disc tables up to this size are staged in shared memory
+
 // Row-block interleave: local row ly of partition `part` -> frame row.
 __device__ __forceinline__ int map_row(int ly, const FrameArgs &a) {
     if (a.n_parts == 1) return ly;
@@ -87,6 +101,9 @@ __device__ __forceinline__ uint32_t pack_color(R r, R g, R b) {
 // with -fmad=false so no a*b+c is contracted, as numba compiles the reference).
 cudaError_t rt_launch_render_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, cudaStream_t st);
 cudaError_t rt_launch_render_f64(const rt::FrameArgs &fa, const rt::SceneArgs<double> &sa, cudaStream_t st);
+cudaError_t rt_launch_wave_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, const rt::WaveArgs &wa,
+                               cudaStream_t st);
+int rt_wave_lanes(int samples);
 cudaError_t rt_launch_trace_f32(const double *d_orig, const double *d_dir, int64_t n, float *d_out,
                                 const rt::SceneArgs<float> &sa, int samples, int bounces, cudaStream_t st);
 cudaError_t rt_launch_trace_f64(const double *d_orig, const double *d_dir, int64_t n, double *d_out,

@@ -7,6 +7,7 @@
 // computed here: every compute entry point launches a CUDA kernel or fails.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -82,6 +83,7 @@ struct Dev {
     cudaStream_t st = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     DBuf frame, rad, rays_in, rays_out, sky_raw, sky, counters;
+    DBuf w_p, w_n, w_s, w_sc, w_queue, w_count, w_pix;  // wavefront queues (FP32 soft shadows)
     unsigned counter_slot = 0;
     uint64_t sky_version = ~0ull;
     DevScene<float> s32;
@@ -128,6 +130,7 @@ __global__ void ffma_peak_kernel(float *sink, int iters, float a, float b) {
 
 struct rt_ctx {
     std::vector<Dev> devs;
+    bool wave = true;  // FP32 soft shadows take the wavefront path ($B200RT_WAVE=0: megakernel)
     std::mutex mu;
     HostScene scene;
     float last_ms = 0.f;
@@ -369,10 +372,29 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
     if (rc) return rc;
     fa.work_counter = (unsigned *)d.counters.p + (d.counter_slot++ % rt::kCounterRing);
     RT_CK(cudaMemsetAsync(fa.work_counter, 0, sizeof(unsigned), st));
-    if (precision == RT_PREC_FP64)
+    if (precision == RT_PREC_FP64) {
         e = rt_launch_render_f64(fa, scene_args(d, d.s64, ctx->scene), st);
-    else
+    } else if (fa.samples >= rt::kWaveMinSamples && ctx->wave) {
+        rt::WaveArgs wa;
+        wa.n_pix = (int64_t)fa.local_rows * fa.width;
+        size_t slots = (size_t)wa.n_pix * (fa.bounces + 1);
+        if ((rc = d.w_p.ensure(sizeof(float4) * slots)) || (rc = d.w_n.ensure(sizeof(float4) * slots)) ||
+            (rc = d.w_s.ensure(sizeof(float) * slots)) || (rc = d.w_sc.ensure(sizeof(float) * slots)) ||
+            (rc = d.w_queue.ensure(sizeof(int) * slots)) || (rc = d.w_count.ensure(sizeof(unsigned))) ||
+            (rc = d.w_pix.ensure(sizeof(float4) * (size_t)wa.n_pix)))
+            return rc;
+        wa.hit_p = (float4 *)d.w_p.p;
+        wa.hit_n = (float4 *)d.w_n.p;
+        wa.hit_s = (float *)d.w_s.p;
+        wa.hit_sc = (float *)d.w_sc.p;
+        wa.queue = (int *)d.w_queue.p;
+        wa.count = (unsigned *)d.w_count.p;
+        wa.pix = (float4 *)d.w_pix.p;
+        e = rt_launch_wave_f32(fa, scene_args(d, d.s32, ctx->scene), wa, st);
+        ctx->launches += 2;  // trace + shadow + shade
+    } else {
         e = rt_launch_render_f32(fa, scene_args(d, d.s32, ctx->scene), st);
+    }
     if (e != cudaSuccess) return fail(RT_ERR_CUDA, std::string("render kernel launch: ") + cudaGetErrorString(e));
     ctx->launches++;
     return RT_OK;
@@ -417,6 +439,7 @@ int rt_ctx_create(rt_ctx **out, const int32_t *devices, int32_t n_devices) {
     }
     if (n_devices < 1) n_devices = 1;
     rt_ctx *ctx = new rt_ctx();
+    if (const char *w = std::getenv("B200RT_WAVE")) ctx->wave = std::atoi(w) != 0;
     for (int i = 0; i < n_devices; i++) {
         int id = devices ? devices[i] : i;
         if (id < 0 || id >= avail) {
@@ -443,6 +466,8 @@ int rt_ctx_destroy(rt_ctx *ctx) {
     for (Dev &d : ctx->devs) {
         cudaSetDevice(d.id);
         if (d.st) cudaStreamSynchronize(d.st);
+        for (DBuf *b : {&d.w_p, &d.w_n, &d.w_s, &d.w_sc, &d.w_queue, &d.w_count, &d.w_pix})
+            b->release();
         for (DBuf *b : {&d.frame, &d.rad, &d.rays_in, &d.rays_out, &d.sky_raw, &d.sky, &d.counters, &d.s32.geo, &d.s32.mat,
                         &d.s32.table, &d.s64.geo, &d.s64.mat, &d.s64.table})
             b->release();

@@ -124,6 +124,17 @@ int rt_sky_sample_v1(rt_ctx *ctx, const double *dirs, int64_t n, double *out_rgb
 int rt_host_register(rt_ctx *ctx, void *ptr, size_t bytes);
 int rt_host_unregister(rt_ctx *ctx, void *ptr);
 
+/* Execution options of ctx (all default on except count_work):
+ *   "wave"        FP32 soft shadows (samples >= 8) run as trace / shadow /
+ *                 shade kernels over HBM queues instead of one megakernel;
+ *   "cull"        the wavefront shadow pass skips, per hit, the bodies that
+ *                 provably cannot block any of its shadow rays (exact);
+ *   "count_work"  tally the executed work of the culled pass (rt_work_counts). */
+int rt_set_option(rt_ctx *ctx, const char *name, int32_t value);
+/* Executed-work tallies since the last reset: hits, per-hit cull tests, hits
+ * that sampled, shadow rays traced, sphere tests, plane tests. */
+int rt_work_counts(rt_ctx *ctx, uint64_t *out, int32_t n, int32_t reset);
+
 /* Device time (CUDA events) of the render kernels of the last rt_render_v1 /
  * rt_trace_rays_v1 call on ctx's first device, in milliseconds. */
 int rt_last_kernel_ms(rt_ctx *ctx, float *ms);

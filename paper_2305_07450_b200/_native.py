@@ -49,6 +49,8 @@ SIGNATURES = {
     "rt_sky_sample_v1": (ctypes.c_int, [_p, _p, _i64, _p, _p, _i32, _i32]),
     "rt_host_register": (ctypes.c_int, [_p, _p, ctypes.c_size_t]),
     "rt_host_unregister": (ctypes.c_int, [_p, _p]),
+    "rt_set_option": (ctypes.c_int, [_p, ctypes.c_char_p, _i32]),
+    "rt_work_counts": (ctypes.c_int, [_p, _p, _i32, _i32]),
     "rt_last_kernel_ms": (ctypes.c_int, [_p, _p]),
     "rt_launch_count": (ctypes.c_int, [_p, _p]),
     "rt_ipc_get_handle": (ctypes.c_int, [_p, _p]),
@@ -161,6 +163,15 @@ class Context:
                 lib.rt_host_unregister(self.handle, ptr(a))
         return True
 
+    def set_option(self, name: str, value) -> None:
+        check(load().rt_set_option(self.handle, name.encode(), int(value)), "rt_set_option")
+
+    def work_counts(self, reset: bool = True) -> dict:
+        arr = (ctypes.c_uint64 * 6)()
+        check(load().rt_work_counts(self.handle, arr, 6, int(reset)), "rt_work_counts")
+        keys = ("hits", "cull_tests", "sampled_hits", "shadow_rays", "sphere_tests", "plane_tests")
+        return dict(zip(keys, (int(v) for v in arr)))
+
     def last_kernel_ms(self) -> float:
         v = ctypes.c_float(0)
         check(load().rt_last_kernel_ms(self.handle, ctypes.byref(v)), "rt_last_kernel_ms")
@@ -174,6 +185,21 @@ class Context:
 
 _contexts = {}
 _ctx_lock = threading.Lock()
+_options = {}  # execution options applied to every context (rt_set_option)
+
+
+def set_options(**opts) -> None:
+    """Execution options for every context, present and future:
+    wave (bool), cull (bool), count_work (bool) — see include/b200rt.h."""
+    with _ctx_lock:
+        _options.update({k: int(bool(v)) for k, v in opts.items()})
+        for ctx in _contexts.values():
+            for k, v in opts.items():
+                ctx.set_option(k, v)
+
+
+def get_options() -> dict:
+    return dict(_options)
 
 
 def context(n_devices: int = 1) -> Context:
@@ -186,6 +212,8 @@ def context(n_devices: int = 1) -> Context:
         ctx = _contexts.get(n)
         if ctx is None:
             ctx = Context(tuple(range(n)))
+            for k, v in _options.items():
+                ctx.set_option(k, v)
             _contexts[n] = ctx
         return ctx
 

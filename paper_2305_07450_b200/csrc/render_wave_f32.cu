@@ -123,12 +123,15 @@ __global__ void __launch_bounds__(kThreads)
 template <int LANES, class Geo>
 __device__ __forceinline__ void shadow_queue(const Geo &geo, const SceneArgs<float> &sa, const WaveArgs &wa,
                                              int n) {
+    // Control flow stays warp-uniform end to end (dead lanes of the last
+    // round compute a duplicate and drop it), so the body loops inside the
+    // any-hit test branch on uniform predicates only.
     extern __shared__ float2 smem_tab[];
-    const float2 *__restrict__ tab = reinterpret_cast<const float2 *>(sa.table);
-    if (n > 1 && n <= kWaveSmemSamples) {
-        for (int i = threadIdx.x; i < n; i += blockDim.x) smem_tab[i] = tab[i];
+    const float2 *__restrict__ gtab = reinterpret_cast<const float2 *>(sa.table);
+    const bool tab_in_smem = n > 1 && n <= kWaveSmemSamples;
+    if (tab_in_smem) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) smem_tab[i] = gtab[i];
         __syncthreads();
-        tab = smem_tab;
     }
     const unsigned count = *wa.count;
     const int lane = threadIdx.x & 31;
@@ -137,47 +140,230 @@ __device__ __forceinline__ void shadow_queue(const Geo &geo, const SceneArgs<flo
     const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned n_warps = (gridDim.x * blockDim.x) >> 5;
     const float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
+    const int rounds = (n + LANES - 1) / LANES;
     for (unsigned base = warp * kHitsPerWarp; base < count; base += n_warps * kHitsPerWarp) {
         const unsigned q = base + lane / LANES;
         const bool live = q < count;
+        const int slot = __ldg(wa.queue + (live ? q : count - 1));
+        const float4 P = __ldg(wa.hit_p + slot);
+        const float4 N = __ldg(wa.hit_n + slot);
+        const float3 surface = f3(P.x, P.y, P.z), normal = f3(N.x, N.y, N.z);
+        const float3 origin = surface + normal * 1e-3f;
+        const auto lc = geo.localize(origin);
         int unblocked = 0;
-        int slot = 0;
-        if (live) {
-            slot = __ldg(wa.queue + q);
-            float4 P = __ldg(wa.hit_p + slot);
-            float4 N = __ldg(wa.hit_n + slot);
-            float3 surface = f3(P.x, P.y, P.z), normal = f3(N.x, N.y, N.z);
-            float3 origin = surface + normal * 1e-3f;
-            const auto lc = geo.localize(origin);
-            if (n == 1) {
-                if (sub == 0) {
-                    float3 dir = normalize3(lp - origin);
-                    float3 e = surface - lp;
-                    float l2 = dot3(e, e);
-                    float limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
-                    unblocked = geo.occluded(lc, dir, limit) ? 0 : 1;
-                }
-            } else {
-                DiscBasis db = disc_basis(surface, lp);
-                float3 lo = lp - origin, ls = surface - lp;
+        if (n == 1) {
+            float3 dir = normalize3(lp - origin);
+            float3 e = surface - lp;
+            float l2 = dot3(e, e);
+            float limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
+            unblocked = (sub == 0 && !geo.occluded(lc, dir, limit)) ? 1 : 0;
+        } else {
+            const DiscBasis db = disc_basis(surface, lp);
+            const float3 lo = lp - origin, ls = surface - lp;
 #pragma unroll 2
-                for (int i = sub; i < n; i += LANES) {
-                    float2 ab = tab[i];
-                    float3 off = db.bu * ab.x + db.bv * ab.y;
-                    float3 dv = lo + off;
-                    float r2 = dot3(dv, dv);
-                    float3 dir = dv * (r2 > 0.f ? rsqrtf(r2) : 0.f);
-                    float3 e = ls - off;
-                    float l2 = dot3(e, e);
-                    float limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
-                    unblocked += geo.occluded(lc, dir, limit) ? 0 : 1;
-                }
+            for (int j = 0; j < rounds; j++) {
+                const int i = sub + j * LANES;
+                const bool valid = i < n;
+                const int ic = valid ? i : 0;
+                const float2 ab = tab_in_smem ? smem_tab[ic] : __ldg(gtab + ic);
+                float3 off = db.bu * ab.x + db.bv * ab.y;
+                float3 dv = lo + off;
+                float r2 = dot3(dv, dv);
+                float3 dir = dv * (r2 > 0.f ? rsqrtf(r2) : 0.f);
+                float3 e = ls - off;
+                float l2 = dot3(e, e);
+                float limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
+                unblocked += (valid && !geo.occluded(lc, dir, limit)) ? 1 : 0;
             }
         }
 #pragma unroll
         for (int o = LANES / 2; o > 0; o >>= 1) unblocked += __shfl_xor_sync(0xffffffffu, unblocked, o);
         if (live && sub == 0) wa.hit_sc[slot] = (float)unblocked / (float)n;
     }
+}
+
+// --- B': shadow coefficients with exact occluder culling ---------------------
+//
+// The shadow rays of one hit all leave the same origin o towards points of
+// the light disc (centre L, radius r_i <= 2R, shading.py:89-100) and stop at
+// limit = |p - s_i| <= |o - s_i| + 1e-3 (renderer.py:100-101).  Every such
+// segment lies in the union of balls B(o + t(L - o), 2R t), t in [0, T],
+// T = 1 + 1e-3/(H - 2R) — a solid cone with apex o, axis L - o (length H)
+// and half-angle phi, sin phi = 2R / H.  A body that stays outside that cone
+// (with a relative margin far above FP32 rounding) fails every one of the
+// hit's shadow tests, so skipping it leaves the coefficient unchanged; a
+// sphere that swallows the cone's whole cross-section between o and the disc
+// blocks every sample, so the coefficient is exactly 0.  Only hits with a
+// body in the penumbra test rays, and only against those bodies.
+//
+// One warp per hit (hits taken from an atomic counter — their costs now
+// differ): lanes test one body each for the cull, then take the samples
+// lane, lane + 32, ... against the surviving bodies (a warp-uniform mask).
+constexpr float kCullRel = 1e-4f;  // relative margin of the cull / full-block decisions
+constexpr float kCullAbs = 1e-5f;  // absolute margin (scene units)
+
+struct Cone {
+    float3 o, axis;   // apex, unit axis towards L
+    float H, rho;     // axis length, base radius (2R with margin)
+    float sin_phi, cos_phi, reach;  // reach = T (H + rho): farthest axial extent of a segment
+    bool ok;          // a proper cone (the light ball does not swallow the origin)
+};
+
+__device__ __forceinline__ Cone make_cone(float3 o, float3 lp, float light_radius) {
+    Cone c;
+    c.o = o;
+    float3 A = lp - o;
+    c.H = sqrtf(dot3(A, A));
+    c.rho = 2.f * light_radius * (1.f + kCullRel) + kCullAbs;
+    c.ok = c.H > 0.f && c.rho < 0.999f * c.H;
+    c.axis = A * (c.H > 0.f ? 1.f / c.H : 0.f);
+    c.sin_phi = c.ok ? c.rho / c.H : 1.f;
+    c.cos_phi = sqrtf(fmaxf(1.f - c.sin_phi * c.sin_phi, 0.f));
+    float T = 1.f + (1e-3f + kCullAbs) / fmaxf(c.H - c.rho, 1e-6f);
+    c.reach = T * (c.H + c.rho) * (1.f + kCullRel) + kCullAbs;
+    return c;
+}
+
+// 0: the sphere can block none of the hit's shadow rays; 1: some; 2: all.
+__device__ __forceinline__ int sphere_class(const Cone &k, float4 g) {
+    if (!k.ok) return 1;
+    float3 u = f3(g.x - k.o.x, g.y - k.o.y, g.z - k.o.z);
+    float u2 = dot3(u, u);
+    float r = sqrtf(g.w);
+    // the origin inside the sphere: t = tca - sqrt(rad) < 0 for every ray (geometry.py:102-103)
+    if (u2 < g.w * (1.f - 4.f * kCullRel) - kCullAbs) return 0;
+    float h = dot3(u, k.axis);
+    float3 w = u - k.axis * h;
+    float q = sqrtf(dot3(w, w));
+    // grazing rays (rad >= -1e-7, geometry.py:98) count as hits: pad the radius
+    float rp = sqrtf(g.w + 1e-7f) * (1.f + kCullRel) + kCullAbs + 1e-6f * (sqrtf(u2) + k.H);
+    if (h < -rp || h - rp > k.reach) return 0;
+    float dist = (h * k.cos_phi + q * k.sin_phi >= 0.f) ? q * k.cos_phi - h * k.sin_phi : sqrtf(u2);
+    if (dist >= rp) return 0;
+    // full block: origin clearly outside, sphere wholly before the disc, and
+    // the cone's cross-section at the centre's depth inside the great circle
+    float rm = r * (1.f - 10.f * kCullRel) - kCullAbs - 1e-6f * (sqrtf(u2) + k.H);
+    if (u2 > g.w * (1.f + 4.f * kCullRel) + kCullAbs && h > 0.f &&
+        h + r < (k.H - k.rho) * (1.f - kCullRel) - 2e-3f && q + (h / k.H) * k.rho * (1.f + kCullRel) < rm)
+        return 2;
+    return 1;
+}
+
+// Planes: a shadow segment crosses y = hp iff o.y and its far end (within
+// 1e-3 of a disc point, whose height is within rho of L.y) straddle it.
+__device__ __forceinline__ int plane_class(const Cone &k, float oy, float ly, float hp) {
+    float m = kCullAbs * (1.f + fabsf(hp) + fabsf(ly));
+    float lo = ly - k.rho - 1e-3f - m, hi = ly + k.rho + 1e-3f + m;
+    float a = oy - hp;
+    if ((a > m && lo > hp + m) || (a < -m && hi < hp - m)) return 0;
+    if ((a > m && hi < hp - m) || (a < -m && lo > hp + m)) return 2;
+    return 1;
+}
+
+template <int MAXS>
+__device__ __forceinline__ void shadow_queue_cull(const ParamScene<MAXS> &ps, const SceneArgs<float> &sa,
+                                                  const WaveArgs &wa, int n) {
+    constexpr int kWords = (MAXS + 31) / 32;
+    extern __shared__ float2 smem_tab[];
+    const float2 *__restrict__ gtab = reinterpret_cast<const float2 *>(sa.table);
+    const bool tab_in_smem = n <= kWaveSmemSamples;
+    if (tab_in_smem) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) smem_tab[i] = gtab[i];
+        __syncthreads();
+    }
+    const unsigned count = *wa.count;
+    const int lane = threadIdx.x & 31;
+    const float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
+    const int rounds = (n + 31) / 32;
+    for (;;) {
+        unsigned hidx = 0;
+        if (lane == 0) hidx = atomicAdd(wa.count + 1, 1u);
+        hidx = __shfl_sync(0xffffffffu, hidx, 0);
+        if (hidx >= count) break;
+        const int slot = __ldg(wa.queue + hidx);
+        const float4 P = __ldg(wa.hit_p + slot);
+        const float4 N = __ldg(wa.hit_n + slot);
+        const float3 surface = f3(P.x, P.y, P.z), normal = f3(N.x, N.y, N.z);
+        const float3 origin = surface + normal * 1e-3f;
+        const Cone k = make_cone(origin, lp, sa.light_radius);
+        // lane-parallel cull: one body per lane
+        unsigned cand[kWords];
+        bool full = false;
+#pragma unroll
+        for (int w = 0; w < kWords; w++) {
+            int b = w * 32 + lane;
+            int cls = b < ps.ns ? sphere_class(k, ps.sph[b < MAXS ? b : 0]) : 0;
+            cand[w] = __ballot_sync(0xffffffffu, cls == 1);
+            full |= __any_sync(0xffffffffu, cls == 2);
+        }
+        int pcls = lane < ps.np ? plane_class(k, origin.y, lp.y, ps.pl_h[lane < kMaxPlanes ? lane : 0]) : 0;
+        const unsigned pcand = __ballot_sync(0xffffffffu, pcls == 1);
+        full |= __any_sync(0xffffffffu, pcls == 2);
+        int n_cand = __popc(pcand);
+#pragma unroll
+        for (int w = 0; w < kWords; w++) n_cand += __popc(cand[w]);
+        float sc;
+        if (full) {
+            sc = 0.f;
+        } else if (n_cand == 0) {
+            sc = 1.f;
+        } else {
+            const DiscBasis db = disc_basis(surface, lp);
+            const float3 lo = lp - origin, ls = surface - lp;
+            int unblocked = 0;
+            for (int j = 0; j < rounds; j++) {
+                const int i = lane + 32 * j;
+                const bool valid = i < n;
+                const int ic = valid ? i : 0;
+                float3 dir, off = f3(0.f, 0.f, 0.f);
+                if (n > 1) {
+                    const float2 ab = tab_in_smem ? smem_tab[ic] : __ldg(gtab + ic);
+                    off = db.bu * ab.x + db.bv * ab.y;
+                }
+                float3 dv = lo + off;
+                float r2 = dot3(dv, dv);
+                dir = dv * (r2 > 0.f ? rsqrtf(r2) : 0.f);
+                float3 e = ls - off;
+                float l2 = dot3(e, e);
+                float limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
+                float m = -INFINITY;
+                for (unsigned pm = pcand; pm; pm &= pm - 1) {
+                    int j2 = __ffs(pm) - 1;
+                    m = fmaxf(m, plane_margin(ps.pl_h[j2] - origin.y, dir.y, limit));
+                }
+#pragma unroll
+                for (int w = 0; w < kWords; w++) {
+                    for (unsigned cm = cand[w]; cm; cm &= cm - 1) {
+                        int b = w * 32 + __ffs(cm) - 1;
+                        m = fmaxf(m, sphere_margin(origin, dir, ps.sph[b], limit));
+                    }
+                }
+                unblocked += (valid && !(m > 0.f)) ? 1 : 0;
+            }
+            unblocked = __reduce_add_sync(0xffffffffu, unblocked);
+            sc = (float)unblocked / (float)n;
+        }
+        if (lane == 0) {
+            wa.hit_sc[slot] = sc;
+            if (wa.work) {
+                atomicAdd(wa.work + kWorkHits, 1ull);
+                atomicAdd(wa.work + kWorkCullTests, (unsigned long long)(ps.ns + ps.np));
+                if (!full && n_cand > 0) {
+                    int ncs = n_cand - __popc(pcand);
+                    atomicAdd(wa.work + kWorkSampledHits, 1ull);
+                    atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);
+                    atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n * ncs);
+                    atomicAdd(wa.work + kWorkPlaneTests, (unsigned long long)n * __popc(pcand));
+                }
+            }
+        }
+    }
+}
+
+template <int MAXS>
+__global__ void __launch_bounds__(kThreads)
+    wave_shadow_cull(const SceneArgs<float> sa, const WaveArgs wa, int n, const ParamScene<MAXS> ps) {
+    shadow_queue_cull(ps, sa, wa, n);
 }
 
 #ifndef RT_WAVE_MIN_BLOCKS
@@ -239,6 +425,19 @@ __global__ void __launch_bounds__(kThreads) wave_shade(const FrameArgs fa, const
     if (fa.peer_out) __threadfence_system();
 }
 
+cudaError_t launch_shadow_cull(const SceneArgs<float> &sa, const WaveArgs &wa, int n, cudaStream_t st, bool param8,
+                               const ParamScene<8> &p8, const ParamScene<kParamSpheres> &p256) {
+    size_t smem = n <= kWaveSmemSamples ? sizeof(float2) * (size_t)n : 0;
+    if (param8) {
+        int ctas = resident_ctas(wave_shadow_cull<8>, smem);
+        wave_shadow_cull<8><<<ctas, kThreads, smem, st>>>(sa, wa, n, p8);
+    } else {
+        int ctas = resident_ctas(wave_shadow_cull<kParamSpheres>, smem);
+        wave_shadow_cull<kParamSpheres><<<ctas, kThreads, smem, st>>>(sa, wa, n, p256);
+    }
+    return cudaGetLastError();
+}
+
 template <int LANES>
 cudaError_t launch_shadow(const SceneArgs<float> &sa, const WaveArgs &wa, int n, cudaStream_t st, bool param8,
                           const ParamScene<8> &p8, bool param256, const ParamScene<kParamSpheres> &p256) {
@@ -268,7 +467,7 @@ int rt_wave_lanes(int samples) {
 
 cudaError_t rt_launch_wave_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, const rt::WaveArgs &wa,
                                cudaStream_t st) {
-    cudaError_t e = cudaMemsetAsync(wa.count, 0, sizeof(unsigned), st);
+    cudaError_t e = cudaMemsetAsync(wa.count, 0, 2 * sizeof(unsigned), st);
     if (e != cudaSuccess) return e;
     dim3 grid((fa.width + kTileW - 1) / kTileW, (fa.local_rows + kTileH - 1) / kTileH);
     ParamScene<8> p8;
@@ -284,6 +483,12 @@ cudaError_t rt_launch_wave_f32(const rt::FrameArgs &fa, const rt::SceneArgs<floa
     else
         wave_trace_mem<false><<<grid, kThreads, 0, st>>>(fa, sa, wa);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (wa.cull && (param8 || param256)) {
+        e = launch_shadow_cull(sa, wa, fa.samples, st, param8, p8, p256);
+        if (e != cudaSuccess) return e;
+        wave_shade<<<grid, kThreads, 0, st>>>(fa, sa, wa);
+        return cudaGetLastError();
+    }
     switch (rt_wave_lanes(fa.samples)) {
         case 1: e = launch_shadow<1>(sa, wa, fa.samples, st, param8, p8, param256, p256); break;
         case 2: e = launch_shadow<2>(sa, wa, fa.samples, st, param8, p8, param256, p256); break;

@@ -63,10 +63,14 @@ struct WaveArgs {
     float *hit_s;      // Blinn factor
     float *hit_sc;     // shadow coefficient
     int *queue;        // slots holding a hit
-    unsigned *count;   // queue length
+    unsigned *count;   // queue length (count[0]); count[1] = hits taken by the culled shadow kernel
     float4 *pix;       // {tail rgb, records | exhausted << 8}
     int64_t n_pix;     // pixels of this partition (local_rows * width)
+    unsigned long long *work;  // optional executed-work tallies of the culled path (kWork*), or null
+    int cull;          // exact per-hit occluder culling in the shadow kernel
 };
+// executed-work tallies of the culled shadow kernel (rt_work_counts)
+enum { kWorkHits = 0, kWorkCullTests, kWorkSampledHits, kWorkShadowRays, kWorkSphereTests, kWorkPlaneTests, kWorkN };
 constexpr int kWaveMinSamples = 8;     // soft shadows at or above this take the wavefront path
 constexpr int kWaveSmemSamples = 4096;  // disc tables up to this size are staged in shared memory
 

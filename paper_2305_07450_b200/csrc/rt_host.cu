@@ -83,7 +83,7 @@ struct Dev {
     cudaStream_t st = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     DBuf frame, rad, rays_in, rays_out, sky_raw, sky, counters;
-    DBuf w_p, w_n, w_s, w_sc, w_queue, w_count, w_pix;  // wavefront queues (FP32 soft shadows)
+    DBuf w_p, w_n, w_s, w_sc, w_queue, w_count, w_pix, w_work;  // wavefront queues (FP32 soft shadows)
     unsigned counter_slot = 0;
     uint64_t sky_version = ~0ull;
     DevScene<float> s32;
@@ -130,7 +130,9 @@ __global__ void ffma_peak_kernel(float *sink, int iters, float a, float b) {
 
 struct rt_ctx {
     std::vector<Dev> devs;
-    bool wave = true;  // FP32 soft shadows take the wavefront path ($B200RT_WAVE=0: megakernel)
+    bool wave = true;   // FP32 soft shadows take the wavefront path ($B200RT_WAVE=0: megakernel)
+    bool cull = true;   // exact per-hit occluder culling in the wavefront shadow pass ($B200RT_CULL=0: off)
+    bool count_work = false;  // tally the culled path's executed work (rt_work_counts)
     std::mutex mu;
     HostScene scene;
     float last_ms = 0.f;
@@ -380,7 +382,7 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         size_t slots = (size_t)wa.n_pix * (fa.bounces + 1);
         if ((rc = d.w_p.ensure(sizeof(float4) * slots)) || (rc = d.w_n.ensure(sizeof(float4) * slots)) ||
             (rc = d.w_s.ensure(sizeof(float) * slots)) || (rc = d.w_sc.ensure(sizeof(float) * slots)) ||
-            (rc = d.w_queue.ensure(sizeof(int) * slots)) || (rc = d.w_count.ensure(sizeof(unsigned))) ||
+            (rc = d.w_queue.ensure(sizeof(int) * slots)) || (rc = d.w_count.ensure(2 * sizeof(unsigned))) ||
             (rc = d.w_pix.ensure(sizeof(float4) * (size_t)wa.n_pix)))
             return rc;
         wa.hit_p = (float4 *)d.w_p.p;
@@ -390,6 +392,14 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         wa.queue = (int *)d.w_queue.p;
         wa.count = (unsigned *)d.w_count.p;
         wa.pix = (float4 *)d.w_pix.p;
+        wa.cull = ctx->cull;
+        wa.work = nullptr;
+        if (ctx->count_work) {
+            bool fresh = d.w_work.p == nullptr;
+            if ((rc = d.w_work.ensure(sizeof(unsigned long long) * rt::kWorkN))) return rc;
+            if (fresh) RT_CK(cudaMemsetAsync(d.w_work.p, 0, sizeof(unsigned long long) * rt::kWorkN, st));
+            wa.work = (unsigned long long *)d.w_work.p;
+        }
         e = rt_launch_wave_f32(fa, scene_args(d, d.s32, ctx->scene), wa, st);
         ctx->launches += 2;  // trace + shadow + shade
     } else {
@@ -440,6 +450,7 @@ int rt_ctx_create(rt_ctx **out, const int32_t *devices, int32_t n_devices) {
     if (n_devices < 1) n_devices = 1;
     rt_ctx *ctx = new rt_ctx();
     if (const char *w = std::getenv("B200RT_WAVE")) ctx->wave = std::atoi(w) != 0;
+    if (const char *c = std::getenv("B200RT_CULL")) ctx->cull = std::atoi(c) != 0;
     for (int i = 0; i < n_devices; i++) {
         int id = devices ? devices[i] : i;
         if (id < 0 || id >= avail) {
@@ -466,7 +477,7 @@ int rt_ctx_destroy(rt_ctx *ctx) {
     for (Dev &d : ctx->devs) {
         cudaSetDevice(d.id);
         if (d.st) cudaStreamSynchronize(d.st);
-        for (DBuf *b : {&d.w_p, &d.w_n, &d.w_s, &d.w_sc, &d.w_queue, &d.w_count, &d.w_pix})
+        for (DBuf *b : {&d.w_p, &d.w_n, &d.w_s, &d.w_sc, &d.w_queue, &d.w_count, &d.w_pix, &d.w_work})
             b->release();
         for (DBuf *b : {&d.frame, &d.rad, &d.rays_in, &d.rays_out, &d.sky_raw, &d.sky, &d.counters, &d.s32.geo, &d.s32.mat,
                         &d.s32.table, &d.s64.geo, &d.s64.mat, &d.s64.table})
@@ -709,6 +720,32 @@ int rt_host_unregister(rt_ctx *ctx, void *ptr) {
     if (!ctx || !ptr) return fail(RT_ERR_INVALID, "bad host pointer");
     RT_CK(cudaSetDevice(ctx->devs[0].id));
     RT_CK(cudaHostUnregister(ptr));
+    return RT_OK;
+}
+
+int rt_set_option(rt_ctx *ctx, const char *name, int32_t value) {
+    if (!ctx || !name) return fail(RT_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    std::string n(name);
+    if (n == "wave") ctx->wave = value != 0;
+    else if (n == "cull") ctx->cull = value != 0;
+    else if (n == "count_work") ctx->count_work = value != 0;
+    else return fail(RT_ERR_INVALID, "unknown option " + n);
+    return RT_OK;
+}
+
+int rt_work_counts(rt_ctx *ctx, uint64_t *out, int32_t n, int32_t reset) {
+    if (!ctx || !out || n < 1) return fail(RT_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    Dev &d = ctx->devs[0];
+    RT_CK(cudaSetDevice(d.id));
+    unsigned long long h[rt::kWorkN] = {0};
+    if (d.w_work.p) {
+        RT_CK(cudaStreamSynchronize(d.st));
+        RT_CK(cudaMemcpy(h, d.w_work.p, sizeof h, cudaMemcpyDeviceToHost));
+        if (reset) RT_CK(cudaMemset(d.w_work.p, 0, sizeof h));
+    }
+    for (int i = 0; i < n && i < rt::kWorkN; i++) out[i] = h[i];
     return RT_OK;
 }
 

@@ -23,6 +23,18 @@ pytestmark = pytest.mark.gpu
 
 CASES = [c["name"] for c in G.frame_cases()]
 
+# FP32 execution paths: wavefront + exact culling (default), wavefront without
+# culling, and the one-thread-per-pixel megakernel
+MODES = {"cull": dict(wave=True, cull=True), "wave": dict(wave=True, cull=False),
+         "mega": dict(wave=False, cull=False)}
+
+
+@pytest.fixture(params=list(MODES))
+def fp32_mode(request):
+    _native.set_options(**MODES[request.param])
+    yield request.param
+    _native.set_options(**MODES["cull"])
+
 
 class _Sky:
     def __init__(self, texels):
@@ -82,19 +94,33 @@ def test_fp64_frames_bit_exact(name):
 
 
 @pytest.mark.parametrize("name", CASES)
-def test_fp32_frames_byte_and_radiance_gates(name):
+def test_fp32_frames_byte_and_radiance_gates(name, fp32_mode):
     c = G.frame_case(name)
     px, rad = render_case(c, "fp32", radiance=True)
-    frac, worst = parity.assert_byte_gate(px, G.frame_pixels(name), name)
+    frac, worst = parity.assert_byte_gate(px, G.frame_pixels(name), f"{name} [{fp32_mode}]")
     assert np.all(px >> 24 == 0xFF)
     cam = c["camera"]
     _, want = oracle.render(G.packed_scene(c), cam["position"], cam["yaw"], cam["pitch"], cam["fov"], c["width"],
                             c["height"], c["samples"], c["bounces"], radiance=True)
-    parity.assert_radiance_gate(rad, want, name)
+    parity.assert_radiance_gate(rad, want, f"{name} [{fp32_mode}]")
+
+
+def test_culled_path_is_exact_against_unculled():
+    """Culling only skips bodies that cannot block: the culled FP32 frames
+    equal the unculled wavefront's bit for bit (same arithmetic per test)."""
+    for name in ("bench_128x72_s200_b3", "sweep_160x90_s16_b5_sky", "stress_96x54_s500_b8", "random4_64x36_s16_b4",
+                 "c3like_192x108_s200_b3_sky", "blocked_32x18_s4_b1"):
+        c = G.frame_case(name)
+        _native.set_options(wave=True, cull=False)
+        ref, rref = render_case(c, "fp32", radiance=True)
+        _native.set_options(wave=True, cull=True)
+        got, rgot = render_case(c, "fp32", radiance=True)
+        np.testing.assert_array_equal(got, ref, err_msg=name)
+        np.testing.assert_array_equal(rgot, rref, err_msg=name)
 
 
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
-def test_worker_counts_do_not_change_pixels(precision):
+def test_worker_counts_do_not_change_pixels(precision, fp32_mode):
     # test_renderer.py:229-238 / test_acceptance.py:115-118 with workers = row-block partitions
     c = G.frame_case("sweep_160x90_s16_b5_sky")
     base, _ = render_case(c, precision)

@@ -20,8 +20,13 @@ def main():
     ap.add_argument("configs", nargs="*", default=["C2", "C4"])
     ap.add_argument("--frames", type=int, default=20)
     ap.add_argument("--precision", default="fp32")
+    ap.add_argument("--mode", default=None, help="cull | wave | mega")
     a = ap.parse_args()
     tag = os.path.basename(_native.LIB_PATH)
+    if a.mode:
+        _native.set_options(**{"cull": dict(wave=1, cull=1), "wave": dict(wave=1, cull=0),
+                               "mega": dict(wave=0, cull=0)}[a.mode])
+        tag += f"[{a.mode}]"
     for key in a.configs:
         cfg = rt.CONFIGS[key]
         scene, cam, params = cfg.scene(), cfg.camera(), cfg.params()

@@ -360,6 +360,121 @@ __device__ __forceinline__ void shadow_queue_cull(const ParamScene<MAXS> &ps, co
     }
 }
 
+// Scenes of up to 16 spheres and 8 planes: one lane per hit classifies every
+// body (the cull costs a few instructions per hit), lanes whose hit is
+// decided write it at once, then the warp samples the undecided hits one at
+// a time, 32 samples abreast, against that hit's surviving bodies.
+template <int MAXS>
+__device__ __forceinline__ void shadow_lane_cull(const ParamScene<MAXS> &ps, const SceneArgs<float> &sa,
+                                                 const WaveArgs &wa, int n) {
+    static_assert(MAXS <= 16, "sphere mask is 16 bits");
+    extern __shared__ float2 smem_tab[];
+    const float2 *__restrict__ gtab = reinterpret_cast<const float2 *>(sa.table);
+    const bool tab_in_smem = n <= kWaveSmemSamples;
+    if (tab_in_smem) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) smem_tab[i] = gtab[i];
+        __syncthreads();
+    }
+    const unsigned count = *wa.count;
+    const int lane = threadIdx.x & 31;
+    const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned n_warps = (gridDim.x * blockDim.x) >> 5;
+    const float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
+    const int rounds = (n + 31) / 32;
+    for (unsigned base = warp * 32; base < count; base += n_warps * 32) {
+        const unsigned q = base + lane;
+        const bool live = q < count;
+        int slot = 0;
+        float3 surface = f3(0.f, 0.f, 0.f), normal = f3(0.f, 1.f, 0.f);
+        unsigned mask = 0;  // bits 0-15 spheres, 16-23 planes
+        bool full = false;
+        if (live) {
+            slot = __ldg(wa.queue + q);
+            const float4 P = __ldg(wa.hit_p + slot);
+            const float4 N = __ldg(wa.hit_n + slot);
+            surface = f3(P.x, P.y, P.z);
+            normal = f3(N.x, N.y, N.z);
+            const float3 origin = surface + normal * 1e-3f;
+            const Cone k = make_cone(origin, lp, sa.light_radius);
+#pragma unroll
+            for (int b = 0; b < MAXS; b++) {
+                if (b >= ps.ns) break;
+                int cls = sphere_class(k, ps.sph[b]);
+                mask |= (cls == 1 ? 1u : 0u) << b;
+                full |= cls == 2;
+            }
+#pragma unroll
+            for (int j = 0; j < kMaxPlanes; j++) {
+                if (j >= ps.np) break;
+                int cls = plane_class(k, origin.y, lp.y, ps.pl_h[j]);
+                mask |= (cls == 1 ? 1u : 0u) << (16 + j);
+                full |= cls == 2;
+            }
+            if (full || mask == 0) wa.hit_sc[slot] = full ? 0.f : 1.f;
+        }
+        const bool need = live && !full && mask != 0;
+        if (wa.work) {
+            unsigned nl = __popc(__ballot_sync(0xffffffffu, live));
+            if (lane == 0) {
+                atomicAdd(wa.work + kWorkHits, (unsigned long long)nl);
+                atomicAdd(wa.work + kWorkCullTests, (unsigned long long)nl * (ps.ns + ps.np));
+            }
+        }
+        for (unsigned todo = __ballot_sync(0xffffffffu, need); todo; todo &= todo - 1) {
+            const int src = __ffs(todo) - 1;
+            const float3 hs = f3(__shfl_sync(0xffffffffu, surface.x, src), __shfl_sync(0xffffffffu, surface.y, src),
+                                 __shfl_sync(0xffffffffu, surface.z, src));
+            const float3 hn = f3(__shfl_sync(0xffffffffu, normal.x, src), __shfl_sync(0xffffffffu, normal.y, src),
+                                 __shfl_sync(0xffffffffu, normal.z, src));
+            const unsigned hm = __shfl_sync(0xffffffffu, mask, src);
+            const int hslot = __shfl_sync(0xffffffffu, slot, src);
+            const float3 origin = hs + hn * 1e-3f;
+            const DiscBasis db = disc_basis(hs, lp);
+            const float3 lo = lp - origin, ls = hs - lp;
+            int unblocked = 0;
+            for (int j = 0; j < rounds; j++) {
+                const int i = lane + 32 * j;
+                const bool valid = i < n;
+                const int ic = valid ? i : 0;
+                float3 off = f3(0.f, 0.f, 0.f);
+                if (n > 1) {
+                    const float2 ab = tab_in_smem ? smem_tab[ic] : __ldg(gtab + ic);
+                    off = db.bu * ab.x + db.bv * ab.y;
+                }
+                float3 dv = lo + off;
+                float r2 = dot3(dv, dv);
+                float3 dir = dv * (r2 > 0.f ? rsqrtf(r2) : 0.f);
+                float3 e = ls - off;
+                float l2 = dot3(e, e);
+                float limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
+                float m = -INFINITY;
+                for (unsigned bm = hm; bm; bm &= bm - 1) {
+                    int b = __ffs(bm) - 1;
+                    m = fmaxf(m, b < 16 ? sphere_margin(origin, dir, ps.sph[b], limit)
+                                        : plane_margin(ps.pl_h[b - 16] - origin.y, dir.y, limit));
+                }
+                unblocked += (valid && !(m > 0.f)) ? 1 : 0;
+            }
+            unblocked = __reduce_add_sync(0xffffffffu, unblocked);
+            if (lane == 0) {
+                wa.hit_sc[hslot] = (float)unblocked / (float)n;
+                if (wa.work) {
+                    atomicAdd(wa.work + kWorkSampledHits, 1ull);
+                    atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);
+                    atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n * __popc(hm & 0xffffu));
+                    atomicAdd(wa.work + kWorkPlaneTests, (unsigned long long)n * __popc(hm >> 16));
+                }
+            }
+        }
+    }
+}
+
+template <int MAXS>
+__global__ void __launch_bounds__(kThreads)
+    wave_shadow_lane_cull(const SceneArgs<float> sa, const WaveArgs wa, int n, const ParamScene<MAXS> ps) {
+    shadow_lane_cull(ps, sa, wa, n);
+}
+
 template <int MAXS>
 __global__ void __launch_bounds__(kThreads)
     wave_shadow_cull(const SceneArgs<float> sa, const WaveArgs wa, int n, const ParamScene<MAXS> ps) {
@@ -429,8 +544,8 @@ cudaError_t launch_shadow_cull(const SceneArgs<float> &sa, const WaveArgs &wa, i
                                const ParamScene<8> &p8, const ParamScene<kParamSpheres> &p256) {
     size_t smem = n <= kWaveSmemSamples ? sizeof(float2) * (size_t)n : 0;
     if (param8) {
-        int ctas = resident_ctas(wave_shadow_cull<8>, smem);
-        wave_shadow_cull<8><<<ctas, kThreads, smem, st>>>(sa, wa, n, p8);
+        int ctas = resident_ctas(wave_shadow_lane_cull<8>, smem);
+        wave_shadow_lane_cull<8><<<ctas, kThreads, smem, st>>>(sa, wa, n, p8);
     } else {
         int ctas = resident_ctas(wave_shadow_cull<kParamSpheres>, smem);
         wave_shadow_cull<kParamSpheres><<<ctas, kThreads, smem, st>>>(sa, wa, n, p256);

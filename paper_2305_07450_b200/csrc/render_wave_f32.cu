@@ -277,7 +277,7 @@ __device__ __forceinline__ void shadow_queue_cull(const ParamScene<MAXS> &ps, co
     const int rounds = (n + 31) / 32;
     for (;;) {
         unsigned hidx = 0;
-        if (lane == 0) hidx = atomicAdd(wa.count + 1, 1u);
+        if (lane == 0) hidx = atomicAdd(wa.count + 2, 1u);
         hidx = __shfl_sync(0xffffffffu, hidx, 0);
         if (hidx >= count) break;
         const int slot = __ldg(wa.queue + hidx);
@@ -360,41 +360,33 @@ __device__ __forceinline__ void shadow_queue_cull(const ParamScene<MAXS> &ps, co
     }
 }
 
-// Scenes of up to 16 spheres and 8 planes: one lane per hit classifies every
-// body (the cull costs a few instructions per hit), lanes whose hit is
-// decided write it at once, then the warp samples the undecided hits one at
-// a time, 32 samples abreast, against that hit's surviving bodies.
+// Scenes of up to 16 spheres and 8 planes, two kernels:
+//  B1  one lane per hit classifies every body (a few instructions per hit);
+//      decided hits (nothing can block: 1, something blocks all: 0) are
+//      written at once, undecided ones go to a second queue with their
+//      body mask (warp-aggregated append);
+//  B2  one warp per undecided hit, 32 samples abreast, against that hit's
+//      surviving bodies only — every queued hit costs the same, so a static
+//      stride keeps the SMs evenly loaded.
 template <int MAXS>
-__device__ __forceinline__ void shadow_lane_cull(const ParamScene<MAXS> &ps, const SceneArgs<float> &sa,
-                                                 const WaveArgs &wa, int n) {
+__global__ void __launch_bounds__(kThreads)
+    wave_cull_classify(const SceneArgs<float> sa, const WaveArgs wa, const ParamScene<MAXS> ps) {
     static_assert(MAXS <= 16, "sphere mask is 16 bits");
-    extern __shared__ float2 smem_tab[];
-    const float2 *__restrict__ gtab = reinterpret_cast<const float2 *>(sa.table);
-    const bool tab_in_smem = n <= kWaveSmemSamples;
-    if (tab_in_smem) {
-        for (int i = threadIdx.x; i < n; i += blockDim.x) smem_tab[i] = gtab[i];
-        __syncthreads();
-    }
     const unsigned count = *wa.count;
     const int lane = threadIdx.x & 31;
-    const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const unsigned n_warps = (gridDim.x * blockDim.x) >> 5;
     const float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
-    const int rounds = (n + 31) / 32;
-    for (unsigned base = warp * 32; base < count; base += n_warps * 32) {
+    const unsigned stride = gridDim.x * blockDim.x;
+    for (unsigned base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < count; base += stride) {
         const unsigned q = base + lane;
         const bool live = q < count;
         int slot = 0;
-        float3 surface = f3(0.f, 0.f, 0.f), normal = f3(0.f, 1.f, 0.f);
         unsigned mask = 0;  // bits 0-15 spheres, 16-23 planes
         bool full = false;
         if (live) {
             slot = __ldg(wa.queue + q);
             const float4 P = __ldg(wa.hit_p + slot);
             const float4 N = __ldg(wa.hit_n + slot);
-            surface = f3(P.x, P.y, P.z);
-            normal = f3(N.x, N.y, N.z);
-            const float3 origin = surface + normal * 1e-3f;
+            const float3 origin = f3(P.x, P.y, P.z) + f3(N.x, N.y, N.z) * 1e-3f;
             const Cone k = make_cone(origin, lp, sa.light_radius);
 #pragma unroll
             for (int b = 0; b < MAXS; b++) {
@@ -413,6 +405,11 @@ __device__ __forceinline__ void shadow_lane_cull(const ParamScene<MAXS> &ps, con
             if (full || mask == 0) wa.hit_sc[slot] = full ? 0.f : 1.f;
         }
         const bool need = live && !full && mask != 0;
+        const unsigned nb = __ballot_sync(0xffffffffu, need);
+        unsigned base2 = 0;
+        if (lane == 0 && nb) base2 = atomicAdd(wa.count + 1, (unsigned)__popc(nb));
+        base2 = __shfl_sync(0xffffffffu, base2, 0);
+        if (need) wa.queue2[base2 + __popc(nb & lanemask_lt())] = make_int2(slot, (int)mask);
         if (wa.work) {
             unsigned nl = __popc(__ballot_sync(0xffffffffu, live));
             if (lane == 0) {
@@ -420,59 +417,70 @@ __device__ __forceinline__ void shadow_lane_cull(const ParamScene<MAXS> &ps, con
                 atomicAdd(wa.work + kWorkCullTests, (unsigned long long)nl * (ps.ns + ps.np));
             }
         }
-        for (unsigned todo = __ballot_sync(0xffffffffu, need); todo; todo &= todo - 1) {
-            const int src = __ffs(todo) - 1;
-            const float3 hs = f3(__shfl_sync(0xffffffffu, surface.x, src), __shfl_sync(0xffffffffu, surface.y, src),
-                                 __shfl_sync(0xffffffffu, surface.z, src));
-            const float3 hn = f3(__shfl_sync(0xffffffffu, normal.x, src), __shfl_sync(0xffffffffu, normal.y, src),
-                                 __shfl_sync(0xffffffffu, normal.z, src));
-            const unsigned hm = __shfl_sync(0xffffffffu, mask, src);
-            const int hslot = __shfl_sync(0xffffffffu, slot, src);
-            const float3 origin = hs + hn * 1e-3f;
-            const DiscBasis db = disc_basis(hs, lp);
-            const float3 lo = lp - origin, ls = hs - lp;
-            int unblocked = 0;
-            for (int j = 0; j < rounds; j++) {
-                const int i = lane + 32 * j;
-                const bool valid = i < n;
-                const int ic = valid ? i : 0;
-                float3 off = f3(0.f, 0.f, 0.f);
-                if (n > 1) {
-                    const float2 ab = tab_in_smem ? smem_tab[ic] : __ldg(gtab + ic);
-                    off = db.bu * ab.x + db.bv * ab.y;
-                }
-                float3 dv = lo + off;
-                float r2 = dot3(dv, dv);
-                float3 dir = dv * (r2 > 0.f ? rsqrtf(r2) : 0.f);
-                float3 e = ls - off;
-                float l2 = dot3(e, e);
-                float limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
-                float m = -INFINITY;
-                for (unsigned bm = hm; bm; bm &= bm - 1) {
-                    int b = __ffs(bm) - 1;
-                    m = fmaxf(m, b < 16 ? sphere_margin(origin, dir, ps.sph[b], limit)
-                                        : plane_margin(ps.pl_h[b - 16] - origin.y, dir.y, limit));
-                }
-                unblocked += (valid && !(m > 0.f)) ? 1 : 0;
-            }
-            unblocked = __reduce_add_sync(0xffffffffu, unblocked);
-            if (lane == 0) {
-                wa.hit_sc[hslot] = (float)unblocked / (float)n;
-                if (wa.work) {
-                    atomicAdd(wa.work + kWorkSampledHits, 1ull);
-                    atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);
-                    atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n * __popc(hm & 0xffffu));
-                    atomicAdd(wa.work + kWorkPlaneTests, (unsigned long long)n * __popc(hm >> 16));
-                }
-            }
-        }
     }
 }
 
 template <int MAXS>
 __global__ void __launch_bounds__(kThreads)
-    wave_shadow_lane_cull(const SceneArgs<float> sa, const WaveArgs wa, int n, const ParamScene<MAXS> ps) {
-    shadow_lane_cull(ps, sa, wa, n);
+    wave_cull_sample(const SceneArgs<float> sa, const WaveArgs wa, int n, const ParamScene<MAXS> ps) {
+    extern __shared__ float2 smem_tab[];
+    const float2 *__restrict__ gtab = reinterpret_cast<const float2 *>(sa.table);
+    const bool tab_in_smem = n <= kWaveSmemSamples;
+    if (tab_in_smem) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) smem_tab[i] = gtab[i];
+        __syncthreads();
+    }
+    const unsigned count = wa.count[1];
+    const int lane = threadIdx.x & 31;
+    const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned n_warps = (gridDim.x * blockDim.x) >> 5;
+    const float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
+    const int rounds = (n + 31) / 32;
+    for (unsigned h = warp; h < count; h += n_warps) {
+        const int2 e2 = __ldg(wa.queue2 + h);
+        const int hslot = e2.x;
+        const unsigned hm = (unsigned)e2.y;
+        const float4 P = __ldg(wa.hit_p + hslot);
+        const float4 N = __ldg(wa.hit_n + hslot);
+        const float3 hs = f3(P.x, P.y, P.z);
+        const float3 origin = hs + f3(N.x, N.y, N.z) * 1e-3f;
+        const DiscBasis db = disc_basis(hs, lp);
+        const float3 lo = lp - origin, ls = hs - lp;
+        int unblocked = 0;
+        for (int j = 0; j < rounds; j++) {
+            const int i = lane + 32 * j;
+            const bool valid = i < n;
+            const int ic = valid ? i : 0;
+            float3 off = f3(0.f, 0.f, 0.f);
+            if (n > 1) {
+                const float2 ab = tab_in_smem ? smem_tab[ic] : __ldg(gtab + ic);
+                off = db.bu * ab.x + db.bv * ab.y;
+            }
+            float3 dv = lo + off;
+            float r2 = dot3(dv, dv);
+            float3 dir = dv * (r2 > 0.f ? rsqrtf(r2) : 0.f);
+            float3 e = ls - off;
+            float l2 = dot3(e, e);
+            float limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
+            float m = -INFINITY;
+            for (unsigned bm = hm; bm; bm &= bm - 1) {
+                int b = __ffs(bm) - 1;
+                m = fmaxf(m, b < 16 ? sphere_margin(origin, dir, ps.sph[b], limit)
+                                    : plane_margin(ps.pl_h[b - 16] - origin.y, dir.y, limit));
+            }
+            unblocked += (valid && !(m > 0.f)) ? 1 : 0;
+        }
+        unblocked = __reduce_add_sync(0xffffffffu, unblocked);
+        if (lane == 0) {
+            wa.hit_sc[hslot] = (float)unblocked / (float)n;
+            if (wa.work) {
+                atomicAdd(wa.work + kWorkSampledHits, 1ull);
+                atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);
+                atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n * __popc(hm & 0xffffu));
+                atomicAdd(wa.work + kWorkPlaneTests, (unsigned long long)n * __popc(hm >> 16));
+            }
+        }
+    }
 }
 
 template <int MAXS>
@@ -544,8 +552,12 @@ cudaError_t launch_shadow_cull(const SceneArgs<float> &sa, const WaveArgs &wa, i
                                const ParamScene<8> &p8, const ParamScene<kParamSpheres> &p256) {
     size_t smem = n <= kWaveSmemSamples ? sizeof(float2) * (size_t)n : 0;
     if (param8) {
-        int ctas = resident_ctas(wave_shadow_lane_cull<8>, smem);
-        wave_shadow_lane_cull<8><<<ctas, kThreads, smem, st>>>(sa, wa, n, p8);
+        int ctas = resident_ctas(wave_cull_classify<8>, 0);
+        wave_cull_classify<8><<<ctas, kThreads, 0, st>>>(sa, wa, p8);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        ctas = resident_ctas(wave_cull_sample<8>, smem);
+        wave_cull_sample<8><<<ctas, kThreads, smem, st>>>(sa, wa, n, p8);
     } else {
         int ctas = resident_ctas(wave_shadow_cull<kParamSpheres>, smem);
         wave_shadow_cull<kParamSpheres><<<ctas, kThreads, smem, st>>>(sa, wa, n, p256);
@@ -581,8 +593,9 @@ int rt_wave_lanes(int samples) {
 }
 
 cudaError_t rt_launch_wave_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, const rt::WaveArgs &wa,
-                               cudaStream_t st) {
-    cudaError_t e = cudaMemsetAsync(wa.count, 0, 2 * sizeof(unsigned), st);
+                               cudaStream_t st, int *n_kernels) {
+    *n_kernels = 0;
+    cudaError_t e = cudaMemsetAsync(wa.count, 0, 4 * sizeof(unsigned), st);
     if (e != cudaSuccess) return e;
     dim3 grid((fa.width + kTileW - 1) / kTileW, (fa.local_rows + kTileH - 1) / kTileH);
     ParamScene<8> p8;
@@ -598,10 +611,13 @@ cudaError_t rt_launch_wave_f32(const rt::FrameArgs &fa, const rt::SceneArgs<floa
     else
         wave_trace_mem<false><<<grid, kThreads, 0, st>>>(fa, sa, wa);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    *n_kernels = 1;
     if (wa.cull && (param8 || param256)) {
         e = launch_shadow_cull(sa, wa, fa.samples, st, param8, p8, p256);
         if (e != cudaSuccess) return e;
+        *n_kernels += param8 ? 2 : 1;
         wave_shade<<<grid, kThreads, 0, st>>>(fa, sa, wa);
+        *n_kernels += 1;
         return cudaGetLastError();
     }
     switch (rt_wave_lanes(fa.samples)) {
@@ -614,5 +630,6 @@ cudaError_t rt_launch_wave_f32(const rt::FrameArgs &fa, const rt::SceneArgs<floa
     }
     if (e != cudaSuccess) return e;
     wave_shade<<<grid, kThreads, 0, st>>>(fa, sa, wa);
+    *n_kernels = 3;
     return cudaGetLastError();
 }

@@ -63,7 +63,8 @@ struct WaveArgs {
     float *hit_s;      // Blinn factor
     float *hit_sc;     // shadow coefficient
     int *queue;        // slots holding a hit
-    unsigned *count;   // queue length (count[0]); count[1] = hits taken by the culled shadow kernel
+    unsigned *count;   // [0] queue length, [1] queue2 length, [2] hits taken by the warp-per-hit cull
+    int2 *queue2;      // culled path: undecided hits {slot, body mask}
     float4 *pix;       // {tail rgb, records | exhausted << 8}
     int64_t n_pix;     // pixels of this partition (local_rows * width)
     unsigned long long *work;  // optional executed-work tallies of the culled path (kWork*), or null
@@ -106,7 +107,7 @@ __device__ __forceinline__ uint32_t pack_color(R r, R g, R b) {
 cudaError_t rt_launch_render_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, cudaStream_t st);
 cudaError_t rt_launch_render_f64(const rt::FrameArgs &fa, const rt::SceneArgs<double> &sa, cudaStream_t st);
 cudaError_t rt_launch_wave_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, const rt::WaveArgs &wa,
-                               cudaStream_t st);
+                               cudaStream_t st, int *n_kernels);
 int rt_wave_lanes(int samples);
 cudaError_t rt_launch_trace_f32(const double *d_orig, const double *d_dir, int64_t n, float *d_out,
                                 const rt::SceneArgs<float> &sa, int samples, int bounces, cudaStream_t st);

@@ -260,107 +260,7 @@ __device__ __forceinline__ int plane_class(const Cone &k, float oy, float ly, fl
     return 1;
 }
 
-template <int MAXS>
-__device__ __forceinline__ void shadow_queue_cull(const ParamScene<MAXS> &ps, const SceneArgs<float> &sa,
-                                                  const WaveArgs &wa, int n) {
-    constexpr int kWords = (MAXS + 31) / 32;
-    extern __shared__ float2 smem_tab[];
-    const float2 *__restrict__ gtab = reinterpret_cast<const float2 *>(sa.table);
-    const bool tab_in_smem = n <= kWaveSmemSamples;
-    if (tab_in_smem) {
-        for (int i = threadIdx.x; i < n; i += blockDim.x) smem_tab[i] = gtab[i];
-        __syncthreads();
-    }
-    const unsigned count = *wa.count;
-    const int lane = threadIdx.x & 31;
-    const float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
-    const int rounds = (n + 31) / 32;
-    for (;;) {
-        unsigned hidx = 0;
-        if (lane == 0) hidx = atomicAdd(wa.count + 2, 1u);
-        hidx = __shfl_sync(0xffffffffu, hidx, 0);
-        if (hidx >= count) break;
-        const int slot = __ldg(wa.queue + hidx);
-        const float4 P = __ldg(wa.hit_p + slot);
-        const float4 N = __ldg(wa.hit_n + slot);
-        const float3 surface = f3(P.x, P.y, P.z), normal = f3(N.x, N.y, N.z);
-        const float3 origin = surface + normal * 1e-3f;
-        const Cone k = make_cone(origin, lp, sa.light_radius);
-        // lane-parallel cull: one body per lane
-        unsigned cand[kWords];
-        bool full = false;
-#pragma unroll
-        for (int w = 0; w < kWords; w++) {
-            int b = w * 32 + lane;
-            int cls = b < ps.ns ? sphere_class(k, ps.sph[b < MAXS ? b : 0]) : 0;
-            cand[w] = __ballot_sync(0xffffffffu, cls == 1);
-            full |= __any_sync(0xffffffffu, cls == 2);
-        }
-        int pcls = lane < ps.np ? plane_class(k, origin.y, lp.y, ps.pl_h[lane < kMaxPlanes ? lane : 0]) : 0;
-        const unsigned pcand = __ballot_sync(0xffffffffu, pcls == 1);
-        full |= __any_sync(0xffffffffu, pcls == 2);
-        int n_cand = __popc(pcand);
-#pragma unroll
-        for (int w = 0; w < kWords; w++) n_cand += __popc(cand[w]);
-        float sc;
-        if (full) {
-            sc = 0.f;
-        } else if (n_cand == 0) {
-            sc = 1.f;
-        } else {
-            const DiscBasis db = disc_basis(surface, lp);
-            const float3 lo = lp - origin, ls = surface - lp;
-            int unblocked = 0;
-            for (int j = 0; j < rounds; j++) {
-                const int i = lane + 32 * j;
-                const bool valid = i < n;
-                const int ic = valid ? i : 0;
-                float3 dir, off = f3(0.f, 0.f, 0.f);
-                if (n > 1) {
-                    const float2 ab = tab_in_smem ? smem_tab[ic] : __ldg(gtab + ic);
-                    off = db.bu * ab.x + db.bv * ab.y;
-                }
-                float3 dv = lo + off;
-                float r2 = dot3(dv, dv);
-                dir = dv * (r2 > 0.f ? rsqrtf(r2) : 0.f);
-                float3 e = ls - off;
-                float l2 = dot3(e, e);
-                float limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
-                float m = -INFINITY;
-                for (unsigned pm = pcand; pm; pm &= pm - 1) {
-                    int j2 = __ffs(pm) - 1;
-                    m = fmaxf(m, plane_margin(ps.pl_h[j2] - origin.y, dir.y, limit));
-                }
-#pragma unroll
-                for (int w = 0; w < kWords; w++) {
-                    for (unsigned cm = cand[w]; cm; cm &= cm - 1) {
-                        int b = w * 32 + __ffs(cm) - 1;
-                        m = fmaxf(m, sphere_margin(origin, dir, ps.sph[b], limit));
-                    }
-                }
-                unblocked += (valid && !(m > 0.f)) ? 1 : 0;
-            }
-            unblocked = __reduce_add_sync(0xffffffffu, unblocked);
-            sc = (float)unblocked / (float)n;
-        }
-        if (lane == 0) {
-            wa.hit_sc[slot] = sc;
-            if (wa.work) {
-                atomicAdd(wa.work + kWorkHits, 1ull);
-                atomicAdd(wa.work + kWorkCullTests, (unsigned long long)(ps.ns + ps.np));
-                if (!full && n_cand > 0) {
-                    int ncs = n_cand - __popc(pcand);
-                    atomicAdd(wa.work + kWorkSampledHits, 1ull);
-                    atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);
-                    atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n * ncs);
-                    atomicAdd(wa.work + kWorkPlaneTests, (unsigned long long)n * __popc(pcand));
-                }
-            }
-        }
-    }
-}
-
-// Scenes of up to 16 spheres and 8 planes, two kernels:
+// Two kernels:
 //  B1  one lane per hit classifies every body (a few instructions per hit);
 //      decided hits (nothing can block: 1, something blocks all: 0) are
 //      written at once, undecided ones go to a second queue with their
@@ -371,7 +271,7 @@ __device__ __forceinline__ void shadow_queue_cull(const ParamScene<MAXS> &ps, co
 template <int MAXS>
 __global__ void __launch_bounds__(kThreads)
     wave_cull_classify(const SceneArgs<float> sa, const WaveArgs wa, const ParamScene<MAXS> ps) {
-    static_assert(MAXS <= 16, "sphere mask is 16 bits");
+    constexpr int kWords = (MAXS + 31) / 32;  // sphere mask words; one more word for planes
     const unsigned count = *wa.count;
     const int lane = threadIdx.x & 31;
     const float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
@@ -380,8 +280,10 @@ __global__ void __launch_bounds__(kThreads)
         const unsigned q = base + lane;
         const bool live = q < count;
         int slot = 0;
-        unsigned mask = 0;  // bits 0-15 spheres, 16-23 planes
-        bool full = false;
+        unsigned mask[kWords + 1];
+#pragma unroll
+        for (int w = 0; w <= kWords; w++) mask[w] = 0;
+        bool full = false, any = false;
         if (live) {
             slot = __ldg(wa.queue + q);
             const float4 P = __ldg(wa.hit_p + slot);
@@ -389,27 +291,38 @@ __global__ void __launch_bounds__(kThreads)
             const float3 origin = f3(P.x, P.y, P.z) + f3(N.x, N.y, N.z) * 1e-3f;
             const Cone k = make_cone(origin, lp, sa.light_radius);
 #pragma unroll
-            for (int b = 0; b < MAXS; b++) {
-                if (b >= ps.ns) break;
-                int cls = sphere_class(k, ps.sph[b]);
-                mask |= (cls == 1 ? 1u : 0u) << b;
-                full |= cls == 2;
+            for (int w = 0; w < kWords; w++) {
+#pragma unroll(MAXS <= 32 ? 32 : 4)
+                for (int bit = 0; bit < 32; bit++) {
+                    const int b = w * 32 + bit;
+                    if (b >= ps.ns) break;
+                    int cls = sphere_class(k, ps.sph[b]);  // b is warp-uniform: a constant-cache broadcast
+                    mask[w] |= (cls == 1 ? 1u : 0u) << bit;
+                    full |= cls == 2;
+                }
             }
 #pragma unroll
             for (int j = 0; j < kMaxPlanes; j++) {
                 if (j >= ps.np) break;
                 int cls = plane_class(k, origin.y, lp.y, ps.pl_h[j]);
-                mask |= (cls == 1 ? 1u : 0u) << (16 + j);
+                mask[kWords] |= (cls == 1 ? 1u : 0u) << j;
                 full |= cls == 2;
             }
-            if (full || mask == 0) wa.hit_sc[slot] = full ? 0.f : 1.f;
+#pragma unroll
+            for (int w = 0; w <= kWords; w++) any |= mask[w] != 0;
+            if (full || !any) wa.hit_sc[slot] = full ? 0.f : 1.f;
         }
-        const bool need = live && !full && mask != 0;
+        const bool need = live && !full && any;
         const unsigned nb = __ballot_sync(0xffffffffu, need);
         unsigned base2 = 0;
         if (lane == 0 && nb) base2 = atomicAdd(wa.count + 1, (unsigned)__popc(nb));
         base2 = __shfl_sync(0xffffffffu, base2, 0);
-        if (need) wa.queue2[base2 + __popc(nb & lanemask_lt())] = make_int2(slot, (int)mask);
+        if (need) {
+            const unsigned e = base2 + __popc(nb & lanemask_lt());
+            wa.queue2[e] = slot;
+#pragma unroll
+            for (int w = 0; w <= kWords; w++) wa.mask2[(size_t)w * wa.mask2_stride + e] = mask[w];
+        }
         if (wa.work) {
             unsigned nl = __popc(__ballot_sync(0xffffffffu, live));
             if (lane == 0) {
@@ -423,6 +336,7 @@ __global__ void __launch_bounds__(kThreads)
 template <int MAXS>
 __global__ void __launch_bounds__(kThreads)
     wave_cull_sample(const SceneArgs<float> sa, const WaveArgs wa, int n, const ParamScene<MAXS> ps) {
+    constexpr int kWords = (MAXS + 31) / 32;
     extern __shared__ float2 smem_tab[];
     const float2 *__restrict__ gtab = reinterpret_cast<const float2 *>(sa.table);
     const bool tab_in_smem = n <= kWaveSmemSamples;
@@ -437,9 +351,14 @@ __global__ void __launch_bounds__(kThreads)
     const float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
     const int rounds = (n + 31) / 32;
     for (unsigned h = warp; h < count; h += n_warps) {
-        const int2 e2 = __ldg(wa.queue2 + h);
-        const int hslot = e2.x;
-        const unsigned hm = (unsigned)e2.y;
+        const int hslot = __ldg(wa.queue2 + h);
+        unsigned hm[kWords + 1];
+        int nsph = 0;
+#pragma unroll
+        for (int w = 0; w <= kWords; w++) {
+            hm[w] = __ldg(wa.mask2 + (size_t)w * wa.mask2_stride + h);
+            if (w < kWords) nsph += __popc(hm[w]);
+        }
         const float4 P = __ldg(wa.hit_p + hslot);
         const float4 N = __ldg(wa.hit_n + hslot);
         const float3 hs = f3(P.x, P.y, P.z);
@@ -463,11 +382,12 @@ __global__ void __launch_bounds__(kThreads)
             float l2 = dot3(e, e);
             float limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
             float m = -INFINITY;
-            for (unsigned bm = hm; bm; bm &= bm - 1) {
-                int b = __ffs(bm) - 1;
-                m = fmaxf(m, b < 16 ? sphere_margin(origin, dir, ps.sph[b], limit)
-                                    : plane_margin(ps.pl_h[b - 16] - origin.y, dir.y, limit));
-            }
+            for (unsigned pm = hm[kWords]; pm; pm &= pm - 1)
+                m = fmaxf(m, plane_margin(ps.pl_h[__ffs(pm) - 1] - origin.y, dir.y, limit));
+#pragma unroll
+            for (int w = 0; w < kWords; w++)
+                for (unsigned bm = hm[w]; bm; bm &= bm - 1)
+                    m = fmaxf(m, sphere_margin(origin, dir, ps.sph[w * 32 + __ffs(bm) - 1], limit));
             unblocked += (valid && !(m > 0.f)) ? 1 : 0;
         }
         unblocked = __reduce_add_sync(0xffffffffu, unblocked);
@@ -476,17 +396,11 @@ __global__ void __launch_bounds__(kThreads)
             if (wa.work) {
                 atomicAdd(wa.work + kWorkSampledHits, 1ull);
                 atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);
-                atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n * __popc(hm & 0xffffu));
-                atomicAdd(wa.work + kWorkPlaneTests, (unsigned long long)n * __popc(hm >> 16));
+                atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n * nsph);
+                atomicAdd(wa.work + kWorkPlaneTests, (unsigned long long)n * __popc(hm[kWords]));
             }
         }
     }
-}
-
-template <int MAXS>
-__global__ void __launch_bounds__(kThreads)
-    wave_shadow_cull(const SceneArgs<float> sa, const WaveArgs wa, int n, const ParamScene<MAXS> ps) {
-    shadow_queue_cull(ps, sa, wa, n);
 }
 
 #ifndef RT_WAVE_MIN_BLOCKS
@@ -548,20 +462,16 @@ __global__ void __launch_bounds__(kThreads) wave_shade(const FrameArgs fa, const
     if (fa.peer_out) __threadfence_system();
 }
 
-cudaError_t launch_shadow_cull(const SceneArgs<float> &sa, const WaveArgs &wa, int n, cudaStream_t st, bool param8,
-                               const ParamScene<8> &p8, const ParamScene<kParamSpheres> &p256) {
+template <int MAXS>
+cudaError_t launch_cull(const SceneArgs<float> &sa, const WaveArgs &wa, int n, cudaStream_t st,
+                        const ParamScene<MAXS> &ps) {
     size_t smem = n <= kWaveSmemSamples ? sizeof(float2) * (size_t)n : 0;
-    if (param8) {
-        int ctas = resident_ctas(wave_cull_classify<8>, 0);
-        wave_cull_classify<8><<<ctas, kThreads, 0, st>>>(sa, wa, p8);
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-        ctas = resident_ctas(wave_cull_sample<8>, smem);
-        wave_cull_sample<8><<<ctas, kThreads, smem, st>>>(sa, wa, n, p8);
-    } else {
-        int ctas = resident_ctas(wave_shadow_cull<kParamSpheres>, smem);
-        wave_shadow_cull<kParamSpheres><<<ctas, kThreads, smem, st>>>(sa, wa, n, p256);
-    }
+    int ctas = resident_ctas(wave_cull_classify<MAXS>, 0);
+    wave_cull_classify<MAXS><<<ctas, kThreads, 0, st>>>(sa, wa, ps);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    ctas = resident_ctas(wave_cull_sample<MAXS>, smem);
+    wave_cull_sample<MAXS><<<ctas, kThreads, smem, st>>>(sa, wa, n, ps);
     return cudaGetLastError();
 }
 
@@ -613,9 +523,9 @@ cudaError_t rt_launch_wave_f32(const rt::FrameArgs &fa, const rt::SceneArgs<floa
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     *n_kernels = 1;
     if (wa.cull && (param8 || param256)) {
-        e = launch_shadow_cull(sa, wa, fa.samples, st, param8, p8, p256);
+        e = param8 ? launch_cull(sa, wa, fa.samples, st, p8) : launch_cull(sa, wa, fa.samples, st, p256);
         if (e != cudaSuccess) return e;
-        *n_kernels += param8 ? 2 : 1;
+        *n_kernels += 2;
         wave_shade<<<grid, kThreads, 0, st>>>(fa, sa, wa);
         *n_kernels += 1;
         return cudaGetLastError();

@@ -63,8 +63,10 @@ struct WaveArgs {
     float *hit_s;      // Blinn factor
     float *hit_sc;     // shadow coefficient
     int *queue;        // slots holding a hit
-    unsigned *count;   // [0] queue length, [1] queue2 length, [2] hits taken by the warp-per-hit cull
-    int2 *queue2;      // culled path: undecided hits {slot, body mask}
+    unsigned *count;   // [0] queue length, [1] queue2 length
+    int *queue2;          // culled path: undecided hits (slots)
+    unsigned *mask2;      // their candidate-body masks, word-major [words][mask2_stride]
+    int64_t mask2_stride;
     float4 *pix;       // {tail rgb, records | exhausted << 8}
     int64_t n_pix;     // pixels of this partition (local_rows * width)
     unsigned long long *work;  // optional executed-work tallies of the culled path (kWork*), or null
@@ -72,6 +74,8 @@ struct WaveArgs {
 };
 // executed-work tallies of the culled shadow kernel (rt_work_counts)
 enum { kWorkHits = 0, kWorkCullTests, kWorkSampledHits, kWorkShadowRays, kWorkSphereTests, kWorkPlaneTests, kWorkN };
+constexpr int kParamSpheres = 256;  // scenes up to this many spheres ride in the launch parameters
+constexpr int kMaskWords = kParamSpheres / 32;
 constexpr int kWaveMinSamples = 8;     // soft shadows at or above this take the wavefront path
 constexpr int kWaveSmemSamples = 4096;  // disc tables up to this size are staged in shared memory
 

@@ -14,7 +14,6 @@ namespace rt32 {
 using namespace rt;
 
 constexpr int kMaxPlanes = 8;
-constexpr int kParamSpheres = 256;
 
 __device__ __forceinline__ float3 f3(float x, float y, float z) { return make_float3(x, y, z); }
 __device__ __forceinline__ float3 operator+(float3 a, float3 b) { return f3(a.x + b.x, a.y + b.y, a.z + b.z); }

@@ -83,7 +83,7 @@ struct Dev {
     cudaStream_t st = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     DBuf frame, rad, rays_in, rays_out, sky_raw, sky, counters;
-    DBuf w_p, w_n, w_s, w_sc, w_queue, w_queue2, w_count, w_pix, w_work;  // wavefront queues (FP32 soft shadows)
+    DBuf w_p, w_n, w_s, w_sc, w_queue, w_queue2, w_mask2, w_count, w_pix, w_work;  // wavefront queues (FP32 soft shadows)
     unsigned counter_slot = 0;
     uint64_t sky_version = ~0ull;
     DevScene<float> s32;
@@ -383,7 +383,8 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         if ((rc = d.w_p.ensure(sizeof(float4) * slots)) || (rc = d.w_n.ensure(sizeof(float4) * slots)) ||
             (rc = d.w_s.ensure(sizeof(float) * slots)) || (rc = d.w_sc.ensure(sizeof(float) * slots)) ||
             (rc = d.w_queue.ensure(sizeof(int) * slots)) || (rc = d.w_count.ensure(4 * sizeof(unsigned))) ||
-            (rc = d.w_queue2.ensure(sizeof(int2) * slots)) ||
+            (rc = d.w_queue2.ensure(sizeof(int) * slots)) ||
+            (rc = d.w_mask2.ensure(sizeof(unsigned) * slots * (ctx->scene.n <= 8 ? 2 : rt::kMaskWords + 1))) ||
             (rc = d.w_pix.ensure(sizeof(float4) * (size_t)wa.n_pix)))
             return rc;
         wa.hit_p = (float4 *)d.w_p.p;
@@ -392,7 +393,9 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         wa.hit_sc = (float *)d.w_sc.p;
         wa.queue = (int *)d.w_queue.p;
         wa.count = (unsigned *)d.w_count.p;
-        wa.queue2 = (int2 *)d.w_queue2.p;
+        wa.queue2 = (int *)d.w_queue2.p;
+        wa.mask2 = (unsigned *)d.w_mask2.p;
+        wa.mask2_stride = (int64_t)slots;
         wa.pix = (float4 *)d.w_pix.p;
         wa.cull = ctx->cull;
         wa.work = nullptr;
@@ -480,7 +483,8 @@ int rt_ctx_destroy(rt_ctx *ctx) {
     for (Dev &d : ctx->devs) {
         cudaSetDevice(d.id);
         if (d.st) cudaStreamSynchronize(d.st);
-        for (DBuf *b : {&d.w_p, &d.w_n, &d.w_s, &d.w_sc, &d.w_queue, &d.w_queue2, &d.w_count, &d.w_pix, &d.w_work})
+        for (DBuf *b : {&d.w_p, &d.w_n, &d.w_s, &d.w_sc, &d.w_queue, &d.w_queue2, &d.w_mask2, &d.w_count, &d.w_pix,
+                        &d.w_work})
             b->release();
         for (DBuf *b : {&d.frame, &d.rad, &d.rays_in, &d.rays_out, &d.sky_raw, &d.sky, &d.counters, &d.s32.geo, &d.s32.mat,
                         &d.s32.table, &d.s64.geo, &d.s64.mat, &d.s64.table})

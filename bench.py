@@ -38,7 +38,7 @@ sys.path.insert(0, ROOT)
 
 NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # SMs x FP32 lanes x FMA x max SM clock
 L2_FLUSH_BYTES = 256 << 20
-EXTRA_CONFIGS = ("C1", "P720", "P1080", "P4K", "C3", "C4")
+EXTRA_CONFIGS = ("C1", "P720", "P1080", "P4K", "C3", "C4", "C5")
 
 
 def parse_args(argv=None):
@@ -309,12 +309,26 @@ def run_ours(args):
             total = float(t.item())
         return dict(ms=ms, total_ms=total, wall_s=wall, launches=launches, clocks=clk)
 
-    # headline: device-resident frames/s
-    main = time_config(cfg, max(3, args.warmup), args.steps, sample_clocks=True)
-    fps = args.steps / (main["total_ms"] / 1e3)
-    ms_kernel = statistics.mean(main["ms"])
-    flops = wc[args.config]["flops"]
-    rays = wc[args.config]["rays"]
+    def measure(c, warmup, steps, sample_clocks=False):
+        """Frames/s, per-phase device times and executed work of config c."""
+        r = time_config(c, warmup, steps, sample_clocks)
+        fps_c = len(r["ms"]) / (r["total_ms"] / 1e3)
+        phases = ctx.phase_ms()  # last timed frame
+        ctx.set_option("count_work", 1)
+        ctx.work_counts(reset=True)
+        render_cfg(c)
+        torch.cuda.synchronize()
+        work = ctx.work_counts(reset=True)
+        ctx.set_option("count_work", 0)
+        return r, fps_c, phases, work
+
+    # headline: device-resident frames/s on the default path (wavefront + exact culling)
+    main, fps, phases, work = measure(cfg, max(3, args.warmup), args.steps, sample_clocks=True)
+    ms_frame = statistics.mean(main["ms"])
+    wcc = wc[args.config]
+    rays = wcc["rays"]
+    peak_meas = _native.fp32_peak_tflops(local)
+    roof = roofline(wcc, phases, work, ms_frame, cfg.samples, peak_meas)
 
     # e2e through the public API into a host framebuffer (rank 0's process)
     e2e = None
@@ -331,7 +345,8 @@ def run_ours(args):
         e2e_fps = args.steps / sum(ts)
         h2d = 0  # scene unchanged between frames: cached on the device; kernel args travel with the launch
         e2e = {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": frame_bytes,
-               "ms_per_step": 1e3 * statistics.mean(ts)}
+               "ms_per_step": 1e3 * statistics.mean(ts),
+               "path": "paper_2305_07450_b200.render_frame -> rt_render_v1 (C ABI), pinned host framebuffer"}
     else:
         # rank 0 reads the gathered frame back into pinned host memory every step
         import torch.distributed as dist
@@ -351,10 +366,9 @@ def run_ours(args):
         t = torch.tensor([sum(ts)], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = {"value": args.steps / float(t.item()), "unit": "frames/s", "h2d_bytes_per_step": 0,
-               "d2h_bytes_per_step": frame_bytes}
+               "d2h_bytes_per_step": frame_bytes,
+               "path": "rt_render_device_v1 per rank into rank 0's framebuffer (CUDA IPC over NVLink) + D2H"}
 
-    peak_meas = _native.fp32_peak_tflops(local)
-    achieved = flops / (ms_kernel * 1e-3) / 1e12
     line = {
         "metric": "frames/s",
         "value": fps,
@@ -370,37 +384,38 @@ def run_ours(args):
         "data": "synthetic (the paper's benchmark scene and camera, sceneio.py:314-333)",
         "config": {"workload": cfg.name, "width": cfg.width, "height": cfg.height, "samples": cfg.samples,
                    "bounces": cfg.bounces, "sky": cfg.sky, "parallelism": f"row-blocks x{world} (8-row interleave)",
+                   "path": "wavefront + exact per-hit occluder culling (default)",
                    "l2": "flushed between timed frames (256 MiB memset outside the event pair)"},
         "mrays_per_s": rays * fps / 1e6,
         "e2e": e2e,
         "gpu_launches": main["launches"],
         "clocks": main["clocks"],
-        "roofline": {
-            "bound": "fp32",
-            "achieved": achieved,
-            "peak": peak_meas,
-            "unit": "TFLOP/s",
-            "frac": achieved / peak_meas,
-            "peak_source": "measured FFMA stream on this GPU (rt_fp32_peak_tflops); MEASURED_PEAKS.json has no FP32 figure",
-            "peak_nominal": NOMINAL_FP32_TFLOPS,
-            "frac_of_nominal": achieved / NOMINAL_FP32_TFLOPS,
-            "flops_per_frame": flops,
-            "kernel_ms": ms_kernel,
-            "traffic": None,
-        },
+        "roofline": roof,
+        "phases_ms": phases,
+        "executed_work": work,
     }
     if rank == 0 and not args.no_extra and world == 1:
         extra = {}
         for key in extra_keys:
             c = rt.CONFIGS[key]
-            r = time_config(c, 3, 10 if key != "C4" else 5)
-            f = len(r["ms"]) / (r["total_ms"] / 1e3)
+            r, f, ph, wk = measure(c, 3, 10 if key not in ("C4", "C5") else 5)
             km = statistics.mean(r["ms"])
-            ach = wc[key]["flops"] / (km * 1e-3) / 1e12
-            extra[key] = {"workload": c.name, "fps": f, "kernel_ms": km, "mrays_per_s": wc[key]["rays"] * f / 1e6,
-                          "tflops": ach, "frac_of_measured_fp32": ach / peak_meas}
+            extra[key] = {"workload": c.name, "fps": f, "ms_per_frame": km,
+                          "mrays_per_s": wc[key]["rays"] * f / 1e6, "phases_ms": ph,
+                          "roofline": roofline(wc[key], ph, wk, km, c.samples, peak_meas)}
             if key in rt.workloads.PAPER_FPS:
                 extra[key]["paper_fps_rtx2060"] = rt.workloads.PAPER_FPS[key]
+        # ablation on the headline config: the same frame without culling, and as one megakernel
+        for name, opts in (("no_cull", dict(wave=1, cull=0)), ("megakernel", dict(wave=0, cull=0))):
+            for k, v in opts.items():
+                ctx.set_option(k, v)
+            r, f, ph, wk = measure(cfg, 3, args.steps)
+            km = statistics.mean(r["ms"])
+            extra[f"{args.config}_{name}"] = {"fps": f, "ms_per_frame": km, "phases_ms": ph,
+                                              "roofline": roofline(wcc, ph, wk, km, cfg.samples, peak_meas,
+                                                                   culled=False)}
+        for k, v in dict(wave=1, cull=1).items():
+            ctx.set_option(k, v)
         line["extra"] = extra
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         v, meta = cpu_reference_sample(cfg, args.cpu_seconds)
@@ -419,6 +434,65 @@ def run_ours(args):
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
+
+
+# FLOPs per unit of the SURVEY.md §8d cost model (FMA = 2, add/mul/sqrt/div = 1)
+FLOP_SPHERE_FULL = 19   # a sphere test evaluated to the end (the kernels are branch-free: every test is full)
+FLOP_PLANE = 2
+FLOP_SHADOW_SETUP = 33  # sample point from the table, normalise, limit (n > 1); 21 for n = 1
+FLOP_HIT = 60           # hit point, normal, to-light, Lambert/Blinn inputs
+FLOP_BASIS = 39         # disc basis per hit (n > 1)
+FLOP_PRIMARY = 36       # primary direction + pack
+FLOP_REFLECT = 18
+FLOP_SHADE = 45
+FLOP_CULL = 40          # one body's cone classification (centre offset, axial/radial split, 2 sqrt, compares)
+
+
+def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True):
+    """Roofline of the dominant kernel: its executed FLOPs (cost model above,
+    counts from the reference's control flow or the culled pass's own
+    tallies) over its measured device time."""
+    c = wcc["counts"]
+    setup = FLOP_SHADOW_SETUP if samples > 1 else 21
+    ch_tests = c["CH_TCA"] + c["CH_DISC"] + c["CH_FULL"]
+    flops = {
+        "trace": ch_tests * FLOP_SPHERE_FULL + c["CH_PLANE"] * FLOP_PLANE + c["HITS"] * FLOP_HIT
+        + c["PIX"] * FLOP_PRIMARY + c["REFL"] * FLOP_REFLECT,
+        "shade": c["SHADE"] * FLOP_SHADE,
+    }
+    if culled and work.get("hits"):
+        flops["classify"] = work["cull_tests"] * FLOP_CULL
+        flops["shadow"] = (work["shadow_rays"] * setup + work["sampled_hits"] * (FLOP_BASIS if samples > 1 else 0)
+                           + work["sphere_tests"] * FLOP_SPHERE_FULL + work["plane_tests"] * FLOP_PLANE)
+    else:
+        sh_tests = c["SH_TCA"] + c["SH_DISC"] + c["SH_FULL"]
+        flops["classify"] = 0
+        flops["shadow"] = (c["SH_RAYS"] * setup + c["HITS"] * (FLOP_BASIS if samples > 1 else 0)
+                           + sh_tests * FLOP_SPHERE_FULL + c["SH_PLANE"] * FLOP_PLANE)
+    if phases and sum(phases.values()) > 0:
+        kernel = max(phases, key=phases.get)
+        kms = phases[kernel]
+        share = kms / max(sum(phases.values()), 1e-12)
+    else:  # megakernel: one kernel does everything
+        kernel, kms, share = "megakernel", ms_frame, 1.0
+        flops = {"megakernel": sum(flops.values())}
+    achieved = flops[kernel] / (kms * 1e-3) / 1e12 if kms > 0 else 0.0
+    return {
+        "bound": "fp32",
+        "kernel": kernel,
+        "achieved": achieved,
+        "peak": peak,
+        "unit": "TFLOP/s",
+        "frac": achieved / peak if peak else None,
+        "traffic": None,
+        "kernel_ms": kms,
+        "kernel_share_of_frame": share,
+        "flops_per_launch": flops[kernel],
+        "peak_source": "measured dependent-free FFMA stream on this GPU (rt_fp32_peak_tflops); "
+                       "MEASURED_PEAKS.json has no FP32 CUDA-core figure",
+        "peak_nominal": NOMINAL_FP32_TFLOPS,
+        "reference_equivalent_tflops": wcc["flops"] / (ms_frame * 1e-3) / 1e12,
+    }
 
 
 def main(argv=None):

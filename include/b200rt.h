@@ -138,6 +138,10 @@ int rt_work_counts(rt_ctx *ctx, uint64_t *out, int32_t n, int32_t reset);
 /* Device time (CUDA events) of the render kernels of the last rt_render_v1 /
  * rt_trace_rays_v1 call on ctx's first device, in milliseconds. */
 int rt_last_kernel_ms(rt_ctx *ctx, float *ms);
+/* Device time of the last wavefront frame's phases on ctx's first device, ms:
+ * out[0] trace, out[1] classify (culled path), out[2] shadow / sample,
+ * out[3] shade.  Zeros when no wavefront frame ran. */
+int rt_phase_ms(rt_ctx *ctx, float *out, int32_t n);
 /* Number of kernels this ctx has launched so far. */
 int rt_launch_count(rt_ctx *ctx, int64_t *count);
 

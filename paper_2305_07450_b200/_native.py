@@ -52,6 +52,7 @@ SIGNATURES = {
     "rt_set_option": (ctypes.c_int, [_p, ctypes.c_char_p, _i32]),
     "rt_work_counts": (ctypes.c_int, [_p, _p, _i32, _i32]),
     "rt_last_kernel_ms": (ctypes.c_int, [_p, _p]),
+    "rt_phase_ms": (ctypes.c_int, [_p, _p, _i32]),
     "rt_launch_count": (ctypes.c_int, [_p, _p]),
     "rt_ipc_get_handle": (ctypes.c_int, [_p, _p]),
     "rt_ipc_open": (ctypes.c_int, [_p, _p]),
@@ -177,6 +178,11 @@ class Context:
         check(load().rt_last_kernel_ms(self.handle, ctypes.byref(v)), "rt_last_kernel_ms")
         return float(v.value)
 
+    def phase_ms(self) -> dict:
+        arr = (ctypes.c_float * 4)()
+        check(load().rt_phase_ms(self.handle, arr, 4), "rt_phase_ms")
+        return dict(zip(("trace", "classify", "shadow", "shade"), (float(v) for v in arr)))
+
     def launch_count(self) -> int:
         v = _i64(0)
         check(load().rt_launch_count(self.handle, ctypes.byref(v)), "rt_launch_count")
@@ -203,15 +209,18 @@ def get_options() -> dict:
 
 
 def context(n_devices: int = 1) -> Context:
-    """Process-wide context over devices 0..n-1 (clamped to what is visible)."""
+    """Process-wide context over n visible devices (clamped), starting at this
+    process's local rank ($LOCAL_RANK, as set by torchrun) so that one process
+    per GPU renders on its own GPU."""
     n_vis = device_count()
     if n_vis < 1:
         raise NativeError("no CUDA device visible: the b200rt frame render has no CPU path")
     n = max(1, min(int(n_devices), n_vis))
+    first = int(os.environ.get("LOCAL_RANK", "0")) % n_vis
     with _ctx_lock:
         ctx = _contexts.get(n)
         if ctx is None:
-            ctx = Context(tuple(range(n)))
+            ctx = Context(tuple((first + i) % n_vis for i in range(n)))
             for k, v in _options.items():
                 ctx.set_option(k, v)
             _contexts[n] = ctx

@@ -464,15 +464,19 @@ __global__ void __launch_bounds__(kThreads) wave_shade(const FrameArgs fa, const
 
 template <int MAXS>
 cudaError_t launch_cull(const SceneArgs<float> &sa, const WaveArgs &wa, int n, cudaStream_t st,
-                        const ParamScene<MAXS> &ps) {
+                        const ParamScene<MAXS> &ps, cudaEvent_t *ev) {
     size_t smem = n <= kWaveSmemSamples ? sizeof(float2) * (size_t)n : 0;
-    int ctas = resident_ctas(wave_cull_classify<MAXS>, 0);
-    wave_cull_classify<MAXS><<<ctas, kThreads, 0, st>>>(sa, wa, ps);
+    static thread_local int ctas_c = 0;
+    if (!ctas_c) ctas_c = resident_ctas(wave_cull_classify<MAXS>, 0);
+    wave_cull_classify<MAXS><<<ctas_c, kThreads, 0, st>>>(sa, wa, ps);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    ctas = resident_ctas(wave_cull_sample<MAXS>, smem);
+    if (ev) cudaEventRecord(ev[2], st);
+    int ctas = resident_ctas(wave_cull_sample<MAXS>, smem);  // depends on the table size
     wave_cull_sample<MAXS><<<ctas, kThreads, smem, st>>>(sa, wa, n, ps);
-    return cudaGetLastError();
+    e = cudaGetLastError();
+    if (ev) cudaEventRecord(ev[3], st);
+    return e;
 }
 
 template <int LANES>
@@ -503,10 +507,14 @@ int rt_wave_lanes(int samples) {
 }
 
 cudaError_t rt_launch_wave_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, const rt::WaveArgs &wa,
-                               cudaStream_t st, int *n_kernels) {
+                               cudaStream_t st, int *n_kernels, cudaEvent_t *ev) {
     *n_kernels = 0;
     cudaError_t e = cudaMemsetAsync(wa.count, 0, 4 * sizeof(unsigned), st);
     if (e != cudaSuccess) return e;
+    auto mark = [&](int i) {
+        if (ev) cudaEventRecord(ev[i], st);
+    };
+    mark(0);
     dim3 grid((fa.width + kTileW - 1) / kTileW, (fa.local_rows + kTileH - 1) / kTileH);
     ParamScene<8> p8;
     thread_local ParamScene<kParamSpheres> p256;
@@ -522,14 +530,17 @@ cudaError_t rt_launch_wave_f32(const rt::FrameArgs &fa, const rt::SceneArgs<floa
         wave_trace_mem<false><<<grid, kThreads, 0, st>>>(fa, sa, wa);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     *n_kernels = 1;
+    mark(1);
     if (wa.cull && (param8 || param256)) {
-        e = param8 ? launch_cull(sa, wa, fa.samples, st, p8) : launch_cull(sa, wa, fa.samples, st, p256);
+        e = param8 ? launch_cull(sa, wa, fa.samples, st, p8, ev) : launch_cull(sa, wa, fa.samples, st, p256, ev);
         if (e != cudaSuccess) return e;
         *n_kernels += 2;
         wave_shade<<<grid, kThreads, 0, st>>>(fa, sa, wa);
         *n_kernels += 1;
+        mark(4);
         return cudaGetLastError();
     }
+    mark(2);
     switch (rt_wave_lanes(fa.samples)) {
         case 1: e = launch_shadow<1>(sa, wa, fa.samples, st, param8, p8, param256, p256); break;
         case 2: e = launch_shadow<2>(sa, wa, fa.samples, st, param8, p8, param256, p256); break;
@@ -539,7 +550,9 @@ cudaError_t rt_launch_wave_f32(const rt::FrameArgs &fa, const rt::SceneArgs<floa
         default: e = launch_shadow<32>(sa, wa, fa.samples, st, param8, p8, param256, p256); break;
     }
     if (e != cudaSuccess) return e;
+    mark(3);
     wave_shade<<<grid, kThreads, 0, st>>>(fa, sa, wa);
     *n_kernels = 3;
+    mark(4);
     return cudaGetLastError();
 }

@@ -111,7 +111,7 @@ __device__ __forceinline__ uint32_t pack_color(R r, R g, R b) {
 cudaError_t rt_launch_render_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, cudaStream_t st);
 cudaError_t rt_launch_render_f64(const rt::FrameArgs &fa, const rt::SceneArgs<double> &sa, cudaStream_t st);
 cudaError_t rt_launch_wave_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, const rt::WaveArgs &wa,
-                               cudaStream_t st, int *n_kernels);
+                               cudaStream_t st, int *n_kernels, cudaEvent_t *phase_events /* 5 or null */);
 int rt_wave_lanes(int samples);
 cudaError_t rt_launch_trace_f32(const double *d_orig, const double *d_dir, int64_t n, float *d_out,
                                 const rt::SceneArgs<float> &sa, int samples, int bounces, cudaStream_t st);

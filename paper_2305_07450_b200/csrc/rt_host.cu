@@ -82,6 +82,8 @@ struct Dev {
     int id = 0;
     cudaStream_t st = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEvent_t ph[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // wavefront phase boundaries
+    bool ph_valid = false;
     DBuf frame, rad, rays_in, rays_out, sky_raw, sky, counters;
     DBuf w_p, w_n, w_s, w_sc, w_queue, w_queue2, w_mask2, w_count, w_pix, w_work;  // wavefront queues (FP32 soft shadows)
     unsigned counter_slot = 0;
@@ -374,6 +376,7 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
     if (rc) return rc;
     fa.work_counter = (unsigned *)d.counters.p + (d.counter_slot++ % rt::kCounterRing);
     RT_CK(cudaMemsetAsync(fa.work_counter, 0, sizeof(unsigned), st));
+    d.ph_valid = false;
     if (precision == RT_PREC_FP64) {
         e = rt_launch_render_f64(fa, scene_args(d, d.s64, ctx->scene), st);
     } else if (fa.samples >= rt::kWaveMinSamples && ctx->wave) {
@@ -406,7 +409,10 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
             wa.work = (unsigned long long *)d.w_work.p;
         }
         int nk = 0;
-        e = rt_launch_wave_f32(fa, scene_args(d, d.s32, ctx->scene), wa, st, &nk);
+        if (!d.ph[0])
+            for (auto &ev : d.ph) RT_CK(cudaEventCreate(&ev));
+        e = rt_launch_wave_f32(fa, scene_args(d, d.s32, ctx->scene), wa, st, &nk, d.ph);
+        d.ph_valid = true;
         ctx->launches += nk - 1;  // the common increment below counts one
     } else {
         e = rt_launch_render_f32(fa, scene_args(d, d.s32, ctx->scene), st);
@@ -489,6 +495,8 @@ int rt_ctx_destroy(rt_ctx *ctx) {
         for (DBuf *b : {&d.frame, &d.rad, &d.rays_in, &d.rays_out, &d.sky_raw, &d.sky, &d.counters, &d.s32.geo, &d.s32.mat,
                         &d.s32.table, &d.s64.geo, &d.s64.mat, &d.s64.table})
             b->release();
+        for (auto ev : d.ph)
+            if (ev) cudaEventDestroy(ev);
         if (d.e0) cudaEventDestroy(d.e0);
         if (d.e1) cudaEventDestroy(d.e1);
         if (d.st) cudaStreamDestroy(d.st);
@@ -759,6 +767,18 @@ int rt_work_counts(rt_ctx *ctx, uint64_t *out, int32_t n, int32_t reset) {
 int rt_last_kernel_ms(rt_ctx *ctx, float *ms) {
     if (!ctx || !ms) return fail(RT_ERR_INVALID, "null argument");
     *ms = ctx->last_ms;
+    return RT_OK;
+}
+
+int rt_phase_ms(rt_ctx *ctx, float *out, int32_t n) {
+    if (!ctx || !out || n < 4) return fail(RT_ERR_INVALID, "need 4 outputs");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    Dev &d = ctx->devs[0];
+    for (int i = 0; i < 4; i++) out[i] = 0.f;
+    if (!d.ph_valid) return RT_OK;
+    RT_CK(cudaSetDevice(d.id));
+    RT_CK(cudaEventSynchronize(d.ph[4]));
+    for (int i = 0; i < 4; i++) RT_CK(cudaEventElapsedTime(&out[i], d.ph[i], d.ph[i + 1]));
     return RT_OK;
 }
 

@@ -32,34 +32,16 @@ using namespace rt32;
 // renderer.py:82-105 (+ shading.py:76-86 disc basis, 89-100 disc points)
 template <class Geo>
 __device__ float shadow_coeff(const Geo &geo, float3 surface, float3 normal, const SceneArgs<float> &sa, int n) {
-    float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
-    float3 origin = surface + normal * 1e-3f;
-    if (n == 1) {
-        float3 dir = normalize3(lp - origin);
-        float3 e = surface - lp;
-        float l2 = dot3(e, e);
-        float limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
-        return geo.occluded(geo.localize(origin), dir, limit) ? 0.f : 1.f;
-    }
-    DiscBasis db = disc_basis(surface, lp);
-    float3 bu = db.bu, bv = db.bv;
-    // shadow ray i: dir = normalize(s_i - origin), limit = |surface - s_i|,
-    // with s_i = lp + a_i bu + b_i bv; both share lp - origin / surface - lp.
-    float3 lo = lp - origin;
-    float3 ls = surface - lp;
-    const float2 *__restrict__ tab = reinterpret_cast<const float2 *>(sa.table);
-    const auto lc = geo.localize(origin);
+    const float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
+    const ShadowFrame f = shadow_frame(surface, normal, lp, n > 1);
+    const auto lc = geo.localize(f.origin);
+    const float4 *__restrict__ tab = reinterpret_cast<const float4 *>(sa.table);
     int unblocked = 0;
 #pragma unroll 2
     for (int i = 0; i < n; i++) {
-        float2 ab = __ldg(tab + i);
-        float3 off = bu * ab.x + bv * ab.y;
-        float3 dv = lo + off;
-        float r2 = dot3(dv, dv);
-        float3 dir = dv * (r2 > 0.f ? rsqrtf(r2) : 0.f);
-        float3 e = ls - off;
-        float l2 = dot3(e, e);
-        float limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
+        float3 dir;
+        float limit;
+        shadow_ray(f, n > 1 ? __ldg(tab + i) : make_float4(0.f, 0.f, 0.f, 0.f), dir, limit);
         unblocked += geo.occluded(lc, dir, limit) ? 0 : 1;
     }
     return (float)unblocked / (float)n;

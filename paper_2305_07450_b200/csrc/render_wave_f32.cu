@@ -126,8 +126,8 @@ __device__ __forceinline__ void shadow_queue(const Geo &geo, const SceneArgs<flo
     // Control flow stays warp-uniform end to end (dead lanes of the last
     // round compute a duplicate and drop it), so the body loops inside the
     // any-hit test branch on uniform predicates only.
-    extern __shared__ float2 smem_tab[];
-    const float2 *__restrict__ gtab = reinterpret_cast<const float2 *>(sa.table);
+    extern __shared__ float4 smem_tab[];
+    const float4 *__restrict__ gtab = reinterpret_cast<const float4 *>(sa.table);
     const bool tab_in_smem = n > 1 && n <= kWaveSmemSamples;
     if (tab_in_smem) {
         for (int i = threadIdx.x; i < n; i += blockDim.x) smem_tab[i] = gtab[i];
@@ -147,34 +147,19 @@ __device__ __forceinline__ void shadow_queue(const Geo &geo, const SceneArgs<flo
         const int slot = __ldg(wa.queue + (live ? q : count - 1));
         const float4 P = __ldg(wa.hit_p + slot);
         const float4 N = __ldg(wa.hit_n + slot);
-        const float3 surface = f3(P.x, P.y, P.z), normal = f3(N.x, N.y, N.z);
-        const float3 origin = surface + normal * 1e-3f;
-        const auto lc = geo.localize(origin);
+        const ShadowFrame f = shadow_frame(f3(P.x, P.y, P.z), f3(N.x, N.y, N.z), lp, n > 1);
+        const auto lc = geo.localize(f.origin);
         int unblocked = 0;
-        if (n == 1) {
-            float3 dir = normalize3(lp - origin);
-            float3 e = surface - lp;
-            float l2 = dot3(e, e);
-            float limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
-            unblocked = (sub == 0 && !geo.occluded(lc, dir, limit)) ? 1 : 0;
-        } else {
-            const DiscBasis db = disc_basis(surface, lp);
-            const float3 lo = lp - origin, ls = surface - lp;
 #pragma unroll 2
-            for (int j = 0; j < rounds; j++) {
-                const int i = sub + j * LANES;
-                const bool valid = i < n;
-                const int ic = valid ? i : 0;
-                const float2 ab = tab_in_smem ? smem_tab[ic] : __ldg(gtab + ic);
-                float3 off = db.bu * ab.x + db.bv * ab.y;
-                float3 dv = lo + off;
-                float r2 = dot3(dv, dv);
-                float3 dir = dv * (r2 > 0.f ? rsqrtf(r2) : 0.f);
-                float3 e = ls - off;
-                float l2 = dot3(e, e);
-                float limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
-                unblocked += (valid && !geo.occluded(lc, dir, limit)) ? 1 : 0;
-            }
+        for (int j = 0; j < rounds; j++) {
+            const int i = sub + j * LANES;
+            const bool valid = i < n;
+            const int ic = valid ? i : 0;
+            const float4 t = n == 1 ? make_float4(0.f, 0.f, 0.f, 0.f) : (tab_in_smem ? smem_tab[ic] : __ldg(gtab + ic));
+            float3 dir;
+            float limit;
+            shadow_ray(f, t, dir, limit);
+            unblocked += (valid && !geo.occluded(lc, dir, limit)) ? 1 : 0;
         }
 #pragma unroll
         for (int o = LANES / 2; o > 0; o >>= 1) unblocked += __shfl_xor_sync(0xffffffffu, unblocked, o);
@@ -333,74 +318,99 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
-template <int MAXS>
-__global__ void __launch_bounds__(kThreads)
-    wave_cull_sample(const SceneArgs<float> sa, const WaveArgs wa, int n, const ParamScene<MAXS> ps) {
+// The sampling loop of an undecided hit: up to kRegCand candidate spheres
+// (and the candidate planes) are held in registers as L = c - o and r^2
+// (+graze, or -inf if o is inside), uniform across the warp; a hit with more
+// candidates walks them kRegCand at a time, OR-ing each sample's verdict
+// into a per-lane bit set (one bit per round).
+constexpr int kRegCand = 4;
+
+template <int MAXS, bool SMEM_TAB>
+__device__ __forceinline__ void cull_sample_hit(const ParamScene<MAXS> &ps, const SceneArgs<float> &sa,
+                                                const WaveArgs &wa, int n, unsigned h, const float4 *tab) {
     constexpr int kWords = (MAXS + 31) / 32;
-    extern __shared__ float2 smem_tab[];
-    const float2 *__restrict__ gtab = reinterpret_cast<const float2 *>(sa.table);
-    const bool tab_in_smem = n <= kWaveSmemSamples;
-    if (tab_in_smem) {
-        for (int i = threadIdx.x; i < n; i += blockDim.x) smem_tab[i] = gtab[i];
-        __syncthreads();
-    }
-    const unsigned count = wa.count[1];
     const int lane = threadIdx.x & 31;
-    const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const unsigned n_warps = (gridDim.x * blockDim.x) >> 5;
     const float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
     const int rounds = (n + 31) / 32;
-    for (unsigned h = warp; h < count; h += n_warps) {
-        const int hslot = __ldg(wa.queue2 + h);
-        unsigned hm[kWords + 1];
-        int nsph = 0;
+    const int hslot = __ldg(wa.queue2 + h);
+    unsigned hm[kWords + 1];
+    int nsph = 0;
 #pragma unroll
-        for (int w = 0; w <= kWords; w++) {
-            hm[w] = __ldg(wa.mask2 + (size_t)w * wa.mask2_stride + h);
-            if (w < kWords) nsph += __popc(hm[w]);
-        }
-        const float4 P = __ldg(wa.hit_p + hslot);
-        const float4 N = __ldg(wa.hit_n + hslot);
-        const float3 hs = f3(P.x, P.y, P.z);
-        const float3 origin = hs + f3(N.x, N.y, N.z) * 1e-3f;
-        const DiscBasis db = disc_basis(hs, lp);
-        const float3 lo = lp - origin, ls = hs - lp;
-        int unblocked = 0;
-        for (int j = 0; j < rounds; j++) {
-            const int i = lane + 32 * j;
-            const bool valid = i < n;
-            const int ic = valid ? i : 0;
-            float3 off = f3(0.f, 0.f, 0.f);
-            if (n > 1) {
-                const float2 ab = tab_in_smem ? smem_tab[ic] : __ldg(gtab + ic);
-                off = db.bu * ab.x + db.bv * ab.y;
-            }
-            float3 dv = lo + off;
-            float r2 = dot3(dv, dv);
-            float3 dir = dv * (r2 > 0.f ? rsqrtf(r2) : 0.f);
-            float3 e = ls - off;
-            float l2 = dot3(e, e);
-            float limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
-            float m = -INFINITY;
-            for (unsigned pm = hm[kWords]; pm; pm &= pm - 1)
-                m = fmaxf(m, plane_margin(ps.pl_h[__ffs(pm) - 1] - origin.y, dir.y, limit));
+    for (int w = 0; w <= kWords; w++) {
+        hm[w] = __ldg(wa.mask2 + (size_t)w * wa.mask2_stride + h);
+        if (w < kWords) nsph += __popc(hm[w]);
+    }
+    const float4 P = __ldg(wa.hit_p + hslot);
+    const float4 N = __ldg(wa.hit_n + hslot);
+    const ShadowFrame f = shadow_frame(f3(P.x, P.y, P.z), f3(N.x, N.y, N.z), lp, n > 1);
+    int unblocked = 0;
+    // rounds in groups of 64 (a bit per round); candidates kRegCand at a time
+    for (int g0 = 0; g0 < rounds; g0 += 64) {
+        const int g1 = min(rounds, g0 + 64);
+        unsigned long long blocked = 0;  // bit j - g0: sample lane + 32 j is blocked
+        int w_cur = 0;
+        unsigned m_cur = hm[0];
+        for (int done = 0; done < nsph || done == 0; done += kRegCand) {
+            float4 c[kRegCand];
+            int k = 0;
 #pragma unroll
-            for (int w = 0; w < kWords; w++)
-                for (unsigned bm = hm[w]; bm; bm &= bm - 1)
-                    m = fmaxf(m, sphere_margin(origin, dir, ps.sph[w * 32 + __ffs(bm) - 1], limit));
-            unblocked += (valid && !(m > 0.f)) ? 1 : 0;
-        }
-        unblocked = __reduce_add_sync(0xffffffffu, unblocked);
-        if (lane == 0) {
-            wa.hit_sc[hslot] = (float)unblocked / (float)n;
-            if (wa.work) {
-                atomicAdd(wa.work + kWorkSampledHits, 1ull);
-                atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);
-                atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n * nsph);
-                atomicAdd(wa.work + kWorkPlaneTests, (unsigned long long)n * __popc(hm[kWords]));
+            for (int r = 0; r < kRegCand; r++) {
+                c[r] = make_float4(0.f, 0.f, 0.f, -INFINITY);
+                while (m_cur == 0 && w_cur + 1 < kWords) m_cur = hm[++w_cur];
+                if (m_cur != 0) {
+                    const float4 g = ps.sph[w_cur * 32 + __ffs(m_cur) - 1];
+                    m_cur &= m_cur - 1;
+                    const float3 L = f3(g.x - f.origin.x, g.y - f.origin.y, g.z - f.origin.z);
+                    c[r] = make_float4(L.x, L.y, L.z, sphere_r2g(L, g.w));
+                    k++;
+                }
             }
+            const unsigned pm = done == 0 ? hm[kWords] : 0u;  // planes ride with the first chunk
+            for (int j = g0; j < g1; j++) {
+                const int i = lane + 32 * j;
+                const int ic = i < n ? i : 0;
+                const float4 t = n == 1 ? make_float4(0.f, 0.f, 0.f, 0.f) : (SMEM_TAB ? tab[ic] : __ldg(tab + ic));
+                float3 dir;
+                float limit;
+                shadow_ray(f, t, dir, limit);
+                float m = -INFINITY;
+#pragma unroll
+                for (int r = 0; r < kRegCand; r++)
+                    if (r < k) m = fmaxf(m, sphere_margin_L(f3(c[r].x, c[r].y, c[r].z), dir, c[r].w, limit));
+                for (unsigned b = pm; b; b &= b - 1)
+                    m = fmaxf(m, plane_margin(ps.pl_h[__ffs(b) - 1] - f.origin.y, dir.y, limit));
+                if (m > 0.f) blocked |= 1ull << (j - g0);
+            }
+            if (nsph <= kRegCand) break;
+        }
+        for (int j = g0; j < g1; j++) unblocked += (lane + 32 * j < n && !((blocked >> (j - g0)) & 1ull)) ? 1 : 0;
+    }
+    unblocked = __reduce_add_sync(0xffffffffu, unblocked);
+    if (lane == 0) {
+        wa.hit_sc[hslot] = (float)unblocked / (float)n;
+        if (wa.work) {
+            atomicAdd(wa.work + kWorkSampledHits, 1ull);
+            atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);
+            atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n * nsph);
+            atomicAdd(wa.work + kWorkPlaneTests, (unsigned long long)n * __popc(hm[kWords]));
         }
     }
+}
+
+template <int MAXS, bool SMEM_TAB>
+__global__ void __launch_bounds__(kThreads)
+    wave_cull_sample(const SceneArgs<float> sa, const WaveArgs wa, int n, const ParamScene<MAXS> ps) {
+    extern __shared__ float4 smem_tab[];
+    const float4 *tab = reinterpret_cast<const float4 *>(sa.table);
+    if constexpr (SMEM_TAB) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) smem_tab[i] = tab[i];
+        __syncthreads();
+        tab = smem_tab;
+    }
+    const unsigned count = wa.count[1];
+    const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned n_warps = (gridDim.x * blockDim.x) >> 5;
+    for (unsigned h = warp; h < count; h += n_warps) cull_sample_hit<MAXS, SMEM_TAB>(ps, sa, wa, n, h, tab);
 }
 
 #ifndef RT_WAVE_MIN_BLOCKS
@@ -465,15 +475,21 @@ __global__ void __launch_bounds__(kThreads) wave_shade(const FrameArgs fa, const
 template <int MAXS>
 cudaError_t launch_cull(const SceneArgs<float> &sa, const WaveArgs &wa, int n, cudaStream_t st,
                         const ParamScene<MAXS> &ps, cudaEvent_t *ev) {
-    size_t smem = n <= kWaveSmemSamples ? sizeof(float2) * (size_t)n : 0;
+    size_t smem = n <= kWaveSmemSamples ? sizeof(float4) * (size_t)n : 0;
     static thread_local int ctas_c = 0;
     if (!ctas_c) ctas_c = resident_ctas(wave_cull_classify<MAXS>, 0);
     wave_cull_classify<MAXS><<<ctas_c, kThreads, 0, st>>>(sa, wa, ps);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[2], st);
-    int ctas = resident_ctas(wave_cull_sample<MAXS>, smem);  // depends on the table size
-    wave_cull_sample<MAXS><<<ctas, kThreads, smem, st>>>(sa, wa, n, ps);
+    if (n > 1 && n <= kWaveSmemSamples) {
+        int ctas = resident_ctas(wave_cull_sample<MAXS, true>, smem);  // depends on the table size
+        wave_cull_sample<MAXS, true><<<ctas, kThreads, smem, st>>>(sa, wa, n, ps);
+    } else {
+        static thread_local int ctas = 0;
+        if (!ctas) ctas = resident_ctas(wave_cull_sample<MAXS, false>, 0);
+        wave_cull_sample<MAXS, false><<<ctas, kThreads, 0, st>>>(sa, wa, n, ps);
+    }
     e = cudaGetLastError();
     if (ev) cudaEventRecord(ev[3], st);
     return e;
@@ -482,7 +498,7 @@ cudaError_t launch_cull(const SceneArgs<float> &sa, const WaveArgs &wa, int n, c
 template <int LANES>
 cudaError_t launch_shadow(const SceneArgs<float> &sa, const WaveArgs &wa, int n, cudaStream_t st, bool param8,
                           const ParamScene<8> &p8, bool param256, const ParamScene<kParamSpheres> &p256) {
-    size_t smem = (n > 1 && n <= kWaveSmemSamples) ? sizeof(float2) * (size_t)n : 0;
+    size_t smem = (n > 1 && n <= kWaveSmemSamples) ? sizeof(float4) * (size_t)n : 0;
     if (param8) {
         int ctas = resident_ctas(wave_shadow_param<LANES, 8>, smem);
         wave_shadow_param<LANES, 8><<<ctas, kThreads, smem, st>>>(sa, wa, n, p8);

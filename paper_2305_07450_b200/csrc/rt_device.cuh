@@ -77,7 +77,7 @@ enum { kWorkHits = 0, kWorkCullTests, kWorkSampledHits, kWorkShadowRays, kWorkSp
 constexpr int kParamSpheres = 256;  // scenes up to this many spheres ride in the launch parameters
 constexpr int kMaskWords = kParamSpheres / 32;
 constexpr int kWaveMinSamples = 8;     // soft shadows at or above this take the wavefront path
-constexpr int kWaveSmemSamples = 4096;  // disc tables up to this size are staged in shared memory
+constexpr int kWaveSmemSamples = 2048;  // disc tables (16 B/sample) up to this size are staged in shared memory
 
 // Row-block interleave: local row ly of partition `part` -> frame row.
 __device__ __forceinline__ int map_row(int ly, const FrameArgs &a) {

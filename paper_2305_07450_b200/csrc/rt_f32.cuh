@@ -295,6 +295,45 @@ inline bool pack_params(const SceneArgs<float> &sa, ParamScene<MAXS> &ps) {
 }
 
 
+// The shadow rays of one hit (renderer.py:82-105): origin o = p + 1e-3 n,
+// sample s_i = L + a_i u + b_i v on the disc.  Per ray the kernels need
+// dir = normalize(s_i - o) and limit = |p - s_i|; with p - L parallel to the
+// disc axis and u, v orthogonal to it, |p - s_i|^2 = |p - L|^2 + a_i^2 + b_i^2,
+// so a table entry {a_i, b_i, a_i^2 + b_i^2} (float64 on the host, rounded)
+// gives the limit with one FMA and a reciprocal square root.
+struct ShadowFrame {
+    float3 origin;  // o
+    float3 lo;      // L - o
+    float3 bu, bv;  // disc basis (zero for hard shadows: s = L)
+    float ls2;      // |p - L|^2
+};
+
+__device__ __forceinline__ ShadowFrame shadow_frame(float3 surface, float3 normal, float3 lp, bool soft) {
+    ShadowFrame f;
+    f.origin = surface + normal * 1e-3f;
+    f.lo = lp - f.origin;
+    float3 ls = surface - lp;
+    f.ls2 = dot3(ls, ls);
+    if (soft) {
+        DiscBasis db = disc_basis(surface, lp);
+        f.bu = db.bu;
+        f.bv = db.bv;
+    } else {
+        f.bu = f.bv = f3(0.f, 0.f, 0.f);
+    }
+    return f;
+}
+
+// t = {a_i, b_i, a_i^2 + b_i^2, 0}; all zero for hard shadows
+__device__ __forceinline__ void shadow_ray(const ShadowFrame &f, float4 t, float3 &dir, float &limit) {
+    float3 dv = f3(fmaf(f.bv.x, t.y, fmaf(f.bu.x, t.x, f.lo.x)), fmaf(f.bv.y, t.y, fmaf(f.bu.y, t.x, f.lo.y)),
+                   fmaf(f.bv.z, t.y, fmaf(f.bu.z, t.x, f.lo.z)));
+    float r2 = dot3(dv, dv);
+    dir = dv * (r2 > 0.f ? rsqrtf(r2) : 0.f);
+    float l2 = f.ls2 + t.z;
+    limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
+}
+
 // Persistent grid: as many CTAs as fit on the device at once.
 template <typename K>
 inline int resident_ctas(K kernel, size_t smem, int threads = kThreads) {

@@ -272,7 +272,15 @@ int upload_prec(Dev &d, DevScene<R> &ds, const HostScene &s, int samples) {
     }
     if (samples > 1 && (ds.table_n != samples || !(ds.table_radius == s.light_radius))) {
         std::vector<double> t64 = disc_table(samples, s.light_radius);
-        std::vector<R> t(t64.begin(), t64.end());
+        // FP64 kernel: {a_i, b_i}; FP32 kernels: {a_i, b_i, a_i^2 + b_i^2, 0} (float4 loads)
+        const int comp = sizeof(R) == sizeof(double) ? 2 : 4;
+        std::vector<R> t((size_t)comp * samples, R(0));
+        for (int i = 0; i < samples; i++) {
+            double a = t64[2 * i], b = t64[2 * i + 1];
+            t[comp * i] = (R)a;
+            t[comp * i + 1] = (R)b;
+            if (comp == 4) t[comp * i + 2] = (R)(a * a + b * b);
+        }
         int rc = ds.table.ensure(sizeof(R) * t.size());
         if (rc) return rc;
         RT_CK(cudaMemcpyAsync(ds.table.p, t.data(), sizeof(R) * t.size(), cudaMemcpyHostToDevice, d.st));

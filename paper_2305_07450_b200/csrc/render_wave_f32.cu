@@ -344,6 +344,24 @@ __device__ __forceinline__ void cull_sample_hit(const ParamScene<MAXS> &ps, cons
     const float4 N = __ldg(wa.hit_n + hslot);
     const ShadowFrame f = shadow_frame(f3(P.x, P.y, P.z), f3(N.x, N.y, N.z), lp, n > 1);
     int unblocked = 0;
+    if (nsph == 1 && hm[kWords] == 0) {
+        // the common penumbra case: one sphere against every sample
+        int w = 0;
+        while (hm[w] == 0) w++;
+        const float4 g = ps.sph[w * 32 + __ffs(hm[w]) - 1];
+        const float3 L = f3(g.x - f.origin.x, g.y - f.origin.y, g.z - f.origin.z);
+        const float r2g = sphere_r2g(L, g.w);
+#pragma unroll 2
+        for (int j = 0; j < rounds; j++) {
+            const int i = lane + 32 * j;
+            const int ic = i < n ? i : 0;
+            const float4 t = n == 1 ? make_float4(0.f, 0.f, 0.f, 0.f) : (SMEM_TAB ? tab[ic] : __ldg(tab + ic));
+            float3 dir;
+            float limit;
+            shadow_ray(f, t, dir, limit);
+            unblocked += (i < n && !(sphere_margin_L(L, dir, r2g, limit) > 0.f)) ? 1 : 0;
+        }
+    } else
     // rounds in groups of 64 (a bit per round); candidates kRegCand at a time
     for (int g0 = 0; g0 < rounds; g0 += 64) {
         const int g1 = min(rounds, g0 + 64);

@@ -117,7 +117,7 @@ __device__ __forceinline__ void shade_pixel(const Geo &geo, const FrameArgs &fa,
                                             int ly) {
     if (x >= fa.width || ly >= fa.local_rows) return;
     int y = map_row(ly, fa);
-    if (y >= fa.height) return;
+    if (y >= fa.row_end) return;
     float3 dir = primary_direction(x, y, fa);
     float3 c = trace<BMAX>(geo, f3((float)fa.cam[0], (float)fa.cam[1], (float)fa.cam[2]), dir, sa, fa.samples,
                            fa.bounces);

@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kThreads) render_f64_kernel(const FrameArgs fa
     thread_pixel(x, ly);
     if (x >= fa.width || ly >= fa.local_rows) return;
     int y = map_row(ly, fa);
-    if (y >= fa.height) return;
+    if (y >= fa.row_end) return;
     d3 dir = primary_direction(x, y, fa);
     d3 c = trace<BMAX>(mk(fa.cam[0], fa.cam[1], fa.cam[2]), dir, geo, sa, fa.samples, fa.bounces);
     fa.out[(int64_t)y * fa.out_pitch + x] = pack_color(c.x, c.y, c.z);

@@ -48,7 +48,7 @@ __device__ __forceinline__ void trace_chain(const Geo &geo, const FrameArgs &fa,
                                             const WaveArgs &wa, int x, int ly) {
     if (x >= fa.width || ly >= fa.local_rows) return;
     int y = map_row(ly, fa);
-    if (y >= fa.height) return;
+    if (y >= fa.row_end) return;
     const int64_t lp = (int64_t)ly * fa.width + x;
     float3 origin = f3((float)fa.cam[0], (float)fa.cam[1], (float)fa.cam[2]);
     float3 dir = primary_direction(x, y, fa);
@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(kThreads) wave_shade(const FrameArgs fa, const
     thread_pixel(x, ly);
     if (x >= fa.width || ly >= fa.local_rows) return;
     int y = map_row(ly, fa);
-    if (y >= fa.height) return;
+    if (y >= fa.row_end) return;
     const int64_t lp = (int64_t)ly * fa.width + x;
     float4 px = wa.pix[lp];
     int info = __float_as_int(px.w);

@@ -39,6 +39,8 @@ struct FrameArgs {
     int samples, bounces;
     int peer_out;  // out lives on another GPU: fence the stores at system scope
     unsigned int *work_counter;  // zeroed before the launch: persistent warps take 8x4 patches from it
+    int sub_part, sub_parts;     // within a band: rows interleaved in 8-row blocks (sub_parts = 1: all)
+    int row_end;                 // rows >= row_end are skipped (end of the band / frame)
 };
 
 template <typename R>
@@ -80,11 +82,31 @@ constexpr int kWaveMinSamples = 8;     // soft shadows at or above this take the
 constexpr int kWaveSmemSamples = 2048;  // disc tables (16 B/sample) up to this size are staged in shared memory
 
 // Row-block interleave: local row ly of partition `part` -> frame row.
-__device__ __forceinline__ int map_row(int ly, const FrameArgs &a) {
+// Partition `part` owns the blocks j = part, part + n_parts, ... of
+// block_rows rows; inside them, sub-partition `sub_part` owns the 8-row
+// blocks i = sub_part, sub_part + sub_parts, ... (a contiguous band split
+// among workers, rt_render_v1 on one device).
+__host__ __device__ __forceinline__ int map_row(int ly, const FrameArgs &a) {
+    if (a.sub_parts > 1) {  // one band: block_rows rows starting at part * block_rows
+        int jl = ly / 8, r = ly - jl * 8;
+        return a.part * a.block_rows + (jl * a.sub_parts + a.sub_part) * 8 + r;
+    }
     if (a.n_parts == 1) return ly;
     int jl = ly / a.block_rows;
     int r = ly - jl * a.block_rows;
     return (jl * a.n_parts + a.part) * a.block_rows + r;
+}
+
+// Rows of sub-partition p of band k (rounded up to whole 8-row blocks; the
+// kernels skip rows outside the band and the frame).
+inline int rt_band_local_rows(int height, int k, int bands, int band_rows, int p, int parts) {
+    int y0 = k * band_rows;
+    int rows = height - y0 < band_rows ? height - y0 : band_rows;
+    if (rows <= 0) return 0;
+    if (parts == 1) return rows;
+    int nb = (rows + 7) / 8;
+    int mine = nb > p ? (nb - p + parts - 1) / parts : 0;
+    return mine * 8;
 }
 
 // Thread -> pixel: each warp shades an 8 x 4 pixel patch (coherent rays),

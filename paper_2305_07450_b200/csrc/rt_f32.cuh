@@ -4,6 +4,9 @@
 // accessors, the skybox lookup.  Both translation units are compiled with
 // the same flags (--ftz=true --prec-div=false --prec-sqrt=false).
 #pragma once
+#include <map>
+#include <tuple>
+
 #include "rt_device.cuh"
 
 #ifndef RT_F32_MIN_BLOCKS
@@ -334,14 +337,23 @@ __device__ __forceinline__ void shadow_ray(const ShadowFrame &f, float4 t, float
     limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
 }
 
-// Persistent grid: as many CTAs as fit on the device at once.
+// Persistent grid: as many CTAs as fit on the device at once (memoised per
+// kernel, shared-memory size and device: the occupancy query costs
+// microseconds of host time per launch otherwise).
 template <typename K>
 inline int resident_ctas(K kernel, size_t smem, int threads = kThreads) {
-    int dev = 0, sms = 0, per_sm = 0;
+    int dev = 0;
     cudaGetDevice(&dev);
+    static thread_local std::map<std::tuple<const void *, size_t, int, int>, int> memo;
+    auto key = std::make_tuple((const void *)kernel, smem, threads, dev);
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+    int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
-    return sms * (per_sm > 0 ? per_sm : 1);
+    int ctas = sms * (per_sm > 0 ? per_sm : 1);
+    memo[key] = ctas;
+    return ctas;
 }
 
 }  // namespace rt32

@@ -577,7 +577,8 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
     if (n_dev == 1) {
         Dev &d = ctx->devs[0];
         RT_CK(cudaSetDevice(d.id));
-        int bands = px_bytes >= ((size_t)2 << 20) ? 4 : 1;
+        // (a band costs ~5 kernel boundaries; below ~16 MB that outweighs the hidden copy)
+        int bands = px_bytes >= ((size_t)16 << 20) ? 4 : 1;
         bands = std::max(1, std::min(bands, height / 8));
         const int band_rows = (height + bands - 1) / bands;
         RT_CK(cudaEventRecord(d.e0, d.st));

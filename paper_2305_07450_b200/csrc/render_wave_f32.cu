@@ -234,6 +234,21 @@ __device__ __forceinline__ int sphere_class(const Cone &k, float4 g) {
     return 1;
 }
 
+// A cluster bound the cone cannot reach: no member can block (the members'
+// own tests would all return 0).
+__device__ __forceinline__ bool bound_meets_cone(const Cone &k, float4 B) {
+    if (!k.ok) return true;
+    float3 u = f3(B.x - k.o.x, B.y - k.o.y, B.z - k.o.z);
+    float u2 = dot3(u, u);
+    float h = dot3(u, k.axis);
+    float3 w = u - k.axis * h;
+    float q = sqrtf(dot3(w, w));
+    float rp = B.w * (1.f + kCullRel) + kCullAbs + 1e-6f * (sqrtf(u2) + k.H);
+    if (h < -rp || h - rp > k.reach) return false;
+    float dist = (h * k.cos_phi + q * k.sin_phi >= 0.f) ? q * k.cos_phi - h * k.sin_phi : sqrtf(u2);
+    return dist < rp;
+}
+
 // Planes: a shadow segment crosses y = hp iff o.y and its far end (within
 // 1e-3 of a disc point, whose height is within rho of L.y) straddle it.
 __device__ __forceinline__ int plane_class(const Cone &k, float oy, float ly, float hp) {
@@ -275,15 +290,21 @@ __global__ void __launch_bounds__(kThreads)
             const float4 N = __ldg(wa.hit_n + slot);
             const float3 origin = f3(P.x, P.y, P.z) + f3(N.x, N.y, N.z) * 1e-3f;
             const Cone k = make_cone(origin, lp, sa.light_radius);
+            auto classify = [&](int b) {
+                int cls = sphere_class(k, ps.sph[b]);  // b is warp-uniform: a constant-cache broadcast
+                mask[b >> 5] |= (cls == 1 ? 1u : 0u) << (b & 31);
+                full |= cls == 2;
+            };
+            if constexpr (!ParamScene<MAXS>::kClustered) {
 #pragma unroll
-            for (int w = 0; w < kWords; w++) {
-#pragma unroll(MAXS <= 32 ? 32 : 4)
-                for (int bit = 0; bit < 32; bit++) {
-                    const int b = w * 32 + bit;
+                for (int b = 0; b < MAXS; b++) {
                     if (b >= ps.ns) break;
-                    int cls = sphere_class(k, ps.sph[b]);  // b is warp-uniform: a constant-cache broadcast
-                    mask[w] |= (cls == 1 ? 1u : 0u) << bit;
-                    full |= cls == 2;
+                    classify(b);
+                }
+            } else {
+                for (int c = 0; c < ps.nc; c++) {
+                    if (!bound_meets_cone(k, ps.cl[c])) continue;
+                    for (int b = ps.cl_begin[c]; b < ps.cl_begin[c + 1]; b++) classify(b);
                 }
             }
 #pragma unroll

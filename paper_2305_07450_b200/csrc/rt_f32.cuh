@@ -4,8 +4,12 @@
 // accessors, the skybox lookup.  Both translation units are compiled with
 // the same flags (--ftz=true --prec-div=false --prec-sqrt=false).
 #pragma once
+#include <algorithm>
+#include <cmath>
 #include <map>
 #include <tuple>
+#include <utility>
+#include <vector>
 
 #include "rt_device.cuh"
 
@@ -116,30 +120,70 @@ struct Hit {
 
 // Scene in the launch parameters: spheres in original relative order, planes
 // likewise, with their original indices for the lowest-index tie-break.
+// Spheres of scenes with more than 8 spheres are grouped into clusters of
+// up to kClusterSize (median splits on the host) with a conservative bounding
+// sphere, stored cluster-major: closest-hit and any-hit loops skip every
+// member of a cluster whose bound the ray cannot reach in time, and the
+// shadow-cone classifier skips clusters outside the cone.  Skipping only
+// bodies that provably cannot win (or block) leaves every result unchanged.
+constexpr int kClusterSize = 16;
+constexpr int kMaxClusters = 32;
+constexpr float kBoundRel = 1e-4f;  // slack on cluster-skip decisions (FP32 rounding is ~1e-6)
+
+// Entry distance of the ray into the bound (a lower bound of every member's
+// hit distance), +inf if the ray misses it, <= 0 if it starts inside.
+__device__ __forceinline__ float bound_entry(float3 o, float3 d, float4 B) {
+    float3 L = f3(B.x - o.x, B.y - o.y, B.z - o.z);
+    float tca = dot3(L, d);
+    float3 p = L - d * tca;
+    float rad = B.w * B.w - dot3(p, p);
+    if (rad < 0.f) return INFINITY;
+    float s = sqrtf(rad);
+    if (tca + s < 0.f) return INFINITY;  // wholly behind the origin
+    return tca - s - kBoundRel * (fabsf(tca) + B.w);
+}
+
 template <int MAXS>
 struct ParamScene {
+    static constexpr bool kClustered = MAXS > 8;
+    static constexpr int kNC = kClustered ? kMaxClusters : 1;
     float4 sph[MAXS];
     int sph_idx[MAXS];
     float pl_h[kMaxPlanes];
     int pl_idx[kMaxPlanes];
-    int ns, np;
+    float4 cl[kNC];          // cluster bounds {centre, radius}
+    int cl_begin[kNC + 1];   // members of cluster c: slots [cl_begin[c], cl_begin[c+1])
+    int ns, np, nc;
 
     __device__ __forceinline__ Hit closest(float3 o, float3 d) const {
         Hit h{-1, INFINITY, make_float4(0.f, 0.f, 0.f, -1.f)};
         int slot = -1;
-#pragma unroll(MAXS <= 8 ? MAXS : 4)
-        for (int b = 0; b < MAXS; b++) {
-            if (b >= ns) break;
-            float t = sphere_t(o, d, sph[b]);
-            if (t < h.t) {  // spheres ascend in original index: strict '<' keeps the lowest
-                h.t = t;
-                slot = b;
+        if constexpr (!kClustered) {
+#pragma unroll
+            for (int b = 0; b < MAXS; b++) {
+                if (b >= ns) break;
+                float t = sphere_t(o, d, sph[b]);
+                if (t < h.t) {  // spheres ascend in original index: strict '<' keeps the lowest
+                    h.t = t;
+                    slot = b;
+                }
+            }
+            if (slot >= 0) h.idx = sph_idx[slot];
+        } else {
+            for (int c = 0; c < nc; c++) {
+                if (bound_entry(o, d, cl[c]) > h.t) continue;
+                for (int b = cl_begin[c]; b < cl_begin[c + 1]; b++) {
+                    float t = sphere_t(o, d, sph[b]);
+                    int id = sph_idx[b];
+                    if (t < h.t || (t == h.t && id < h.idx)) {  // lowest original index wins ties
+                        h.t = t;
+                        h.idx = id;
+                        slot = b;
+                    }
+                }
             }
         }
-        if (slot >= 0) {
-            h.idx = sph_idx[slot];
-            h.g = sph[slot];
-        }
+        if (slot >= 0) h.g = sph[slot];
 #pragma unroll
         for (int j = 0; j < kMaxPlanes; j++) {
             if (j >= np) break;
@@ -158,14 +202,14 @@ struct ParamScene {
     // h - o.y are formed once per hit.
     struct Local {
         float3 o;
-        float4 L[MAXS <= 8 ? MAXS : 1];  // xyz = centre - origin, w = r2g
+        float4 L[kClustered ? 1 : MAXS];  // xyz = centre - origin, w = r2g
         float num[kMaxPlanes];
     };
 
     __device__ __forceinline__ Local localize(float3 o) const {
         Local lc;
         lc.o = o;
-        if constexpr (MAXS <= 8) {
+        if constexpr (!kClustered) {
 #pragma unroll
             for (int b = 0; b < MAXS; b++) {
                 float3 L = f3(sph[b].x - o.x, sph[b].y - o.y, sph[b].z - o.z);
@@ -184,7 +228,7 @@ struct ParamScene {
             if (j >= np) break;
             m = fmaxf(m, plane_margin(lc.num[j], d.y, limit));
         }
-        if constexpr (MAXS <= 8) {
+        if constexpr (!kClustered) {
 #pragma unroll
             for (int b = 0; b < MAXS; b++) {
                 if (b >= ns) break;
@@ -192,11 +236,9 @@ struct ParamScene {
                 m = fmaxf(m, sphere_margin_L(f3(L.x, L.y, L.z), d, L.w, limit));
             }
         } else {
-#pragma unroll 4
-            for (int b = 0; b < MAXS; b++) {
-                if (b >= ns) break;
-                m = fmaxf(m, sphere_margin(lc.o, d, sph[b], limit));
-                if ((b & 3) == 3 && m > 0.f) break;
+            for (int c = 0; c < nc && !(m > 0.f); c++) {
+                if (bound_entry(lc.o, d, cl[c]) >= limit) continue;  // no member within [0, limit)
+                for (int b = cl_begin[c]; b < cl_begin[c + 1]; b++) m = fmaxf(m, sphere_margin(lc.o, d, sph[b], limit));
             }
         }
         return m > 0.f;
@@ -271,20 +313,89 @@ __device__ __forceinline__ DiscBasis disc_basis(float3 surface, float3 lp) {
 
 // Pack the host scene (float64 geo) into the launch-parameter layout; false
 // if it does not fit.
+// Median-split clustering of spheres (host): slots [b0, b1) of `order`
+// become clusters of at most kClusterSize, split on the longest axis.
+inline void split_clusters(const std::vector<float4> &c, std::vector<int> &order, int b0, int b1,
+                           std::vector<std::pair<int, int>> &out) {
+    if (b1 - b0 <= kClusterSize) {
+        out.emplace_back(b0, b1);
+        return;
+    }
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int i = b0; i < b1; i++) {
+        const float4 &p = c[order[i]];
+        const float v[3] = {p.x, p.y, p.z};
+        for (int a = 0; a < 3; a++) {
+            lo[a] = std::min(lo[a], v[a]);
+            hi[a] = std::max(hi[a], v[a]);
+        }
+    }
+    int ax = 0;
+    for (int a = 1; a < 3; a++)
+        if (hi[a] - lo[a] > hi[ax] - lo[ax]) ax = a;
+    int mid = (b0 + b1) / 2;
+    auto key = [&](int i) { return ax == 0 ? c[i].x : ax == 1 ? c[i].y : c[i].z; };
+    std::nth_element(order.begin() + b0, order.begin() + mid, order.begin() + b1,
+                     [&](int a, int b) { return key(a) < key(b) || (key(a) == key(b) && a < b); });
+    split_clusters(c, order, b0, mid, out);
+    split_clusters(c, order, mid, b1, out);
+}
+
+// Pack the host scene (float64 geo) into the launch-parameter layout; false
+// if it does not fit.
 template <int MAXS>
 inline bool pack_params(const SceneArgs<float> &sa, ParamScene<MAXS> &ps) {
     ps.ns = ps.np = 0;
+    std::vector<float4> sph;
+    std::vector<int> idx;
     for (int b = 0; b < sa.n; b++) {
         const double *g = sa.host_geo + 4 * b;
         if (g[3] >= 0.0) {
-            if (ps.ns == MAXS) return false;
-            ps.sph[ps.ns] = make_float4((float)g[0], (float)g[1], (float)g[2], (float)g[3]);
-            ps.sph_idx[ps.ns++] = b;
+            if ((int)sph.size() == MAXS) return false;
+            sph.push_back(make_float4((float)g[0], (float)g[1], (float)g[2], (float)g[3]));
+            idx.push_back(b);
         } else {
             if (ps.np == kMaxPlanes) return false;
             ps.pl_h[ps.np] = (float)g[1];
             ps.pl_idx[ps.np++] = b;
         }
+    }
+    ps.ns = (int)sph.size();
+    std::vector<int> order(ps.ns);
+    for (int i = 0; i < ps.ns; i++) order[i] = i;
+    ps.nc = 0;
+    if constexpr (ParamScene<MAXS>::kClustered) {
+        std::vector<std::pair<int, int>> ranges;
+        if (ps.ns > 0) split_clusters(sph, order, 0, ps.ns, ranges);
+        if ((int)ranges.size() > kMaxClusters) return false;
+        for (auto &r : ranges) {
+            // each cluster keeps its members in ascending original order
+            std::sort(order.begin() + r.first, order.begin() + r.second);
+            double cx = 0, cy = 0, cz = 0;
+            for (int i = r.first; i < r.second; i++) {
+                cx += sph[order[i]].x;
+                cy += sph[order[i]].y;
+                cz += sph[order[i]].z;
+            }
+            double k = 1.0 / (r.second - r.first);
+            cx *= k;
+            cy *= k;
+            cz *= k;
+            double R = 0;
+            for (int i = r.first; i < r.second; i++) {
+                const float4 &p = sph[order[i]];
+                double dx = p.x - cx, dy = p.y - cy, dz = p.z - cz;
+                R = std::max(R, std::sqrt(dx * dx + dy * dy + dz * dz) + std::sqrt((double)p.w + 1e-7));
+            }
+            ps.cl[ps.nc] = make_float4((float)cx, (float)cy, (float)cz, (float)(R * (1.0 + 1e-4) + 1e-4));
+            ps.cl_begin[ps.nc] = r.first;
+            ps.nc++;
+        }
+        ps.cl_begin[ps.nc] = ps.ns;
+    }
+    for (int i = 0; i < ps.ns; i++) {
+        ps.sph[i] = sph[order[i]];
+        ps.sph_idx[i] = idx[order[i]];
     }
     for (int b = ps.ns; b < MAXS; b++) {
         ps.sph[b] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -294,9 +405,12 @@ inline bool pack_params(const SceneArgs<float> &sa, ParamScene<MAXS> &ps) {
         ps.pl_h[j] = 0.f;
         ps.pl_idx[j] = 0;
     }
+    for (int c = ps.nc; c < ParamScene<MAXS>::kNC; c++) {
+        ps.cl[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        ps.cl_begin[c + 1] = ps.ns;
+    }
     return true;
 }
-
 
 // The shadow rays of one hit (renderer.py:82-105): origin o = p + 1e-3 n,
 // sample s_i = L + a_i u + b_i v on the disc.  Per ray the kernels need

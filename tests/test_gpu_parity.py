@@ -270,3 +270,43 @@ def test_full_size_sky_configs_fp32_vs_fp64(key):
     sub = oracle.render(vars(ps), cam.position, cam.yaw, cam.pitch, cam.fov, cfg.width, cfg.height, cfg.samples,
                         cfg.bounces, row0=5, row_step=97).reshape(cfg.height, cfg.width)
     np.testing.assert_array_equal(fb64.pixels.reshape(cfg.height, cfg.width)[5::97], sub[5::97])
+
+
+@pytest.mark.slow
+def test_full_size_c5_stress_row_subset_vs_oracle():
+    """C5 (256 spheres + plane, s500 b8) at its full 3840x2160: every 216th row
+    against the oracle — the clustered closest hit and the cluster-level cone
+    cull must leave the FP32 frame within the byte gate; the FP64 kernel is
+    exact on the same rows."""
+    cfg = rt.CONFIGS["C5"]
+    scene, cam, params = cfg.scene(), cfg.camera(), cfg.params()
+    fb = rt.Framebuffer.create(cfg.width, cfg.height)
+    rt.render_frame(scene, cam, params, fb, precision="fp32")
+    ps = rt.pack_scene(scene)
+    want = oracle.render(vars(ps), cam.position, cam.yaw, cam.pitch, cam.fov, cfg.width, cfg.height, cfg.samples,
+                         cfg.bounces, row0=100, row_step=216).reshape(cfg.height, cfg.width)[100::216]
+    got = fb.pixels.reshape(cfg.height, cfg.width)[100::216]
+    parity.assert_byte_gate(got.reshape(-1), want.reshape(-1), "C5 fp32 rows")
+    fb64 = rt.Framebuffer.create(cfg.width, cfg.height)
+    rt.render_frame(scene, cam, params, fb64, precision="fp64")
+    np.testing.assert_array_equal(fb64.pixels.reshape(cfg.height, cfg.width)[100::216], want)
+
+
+def test_clustered_scene_modes_agree():
+    """A 40-sphere scene (clustered: > 8 spheres) renders the same bytes on the
+    culled wavefront, the unculled wavefront and the megakernel."""
+    s = rt.stress_scene(count=40, seed=7)
+    cam = rt.Camera(position=(0.0, 2.0, -6.0), yaw=0.1, pitch=-0.12, fov=70.0)
+    params = rt.RenderParams(32, 4, 160, 90)
+    frames = {}
+    for mode, opts in MODES.items():
+        _native.set_options(**opts)
+        fb = rt.Framebuffer.create(160, 90)
+        rt.render_frame(s, cam, params, fb)
+        frames[mode] = fb.pixels.copy()
+    _native.set_options(**MODES["cull"])
+    np.testing.assert_array_equal(frames["cull"], frames["wave"])
+    fb64 = rt.Framebuffer.create(160, 90)
+    rt.render_frame(s, cam, params, fb64, precision="fp64")
+    for mode, px in frames.items():
+        parity.assert_byte_gate(px, fb64.pixels, f"clustered [{mode}]")

@@ -36,8 +36,10 @@ def main():
             rt.render_frame(scene, cam, params, fb, precision=a.precision)
             if i >= 3:
                 ms.append(rt.last_kernel_ms())
-        print(f"{tag:>14} {key:>6} {a.precision} median {statistics.median(ms):8.4f} ms  min {min(ms):8.4f} ms",
-              flush=True)
+        ph = _native.context(1).phase_ms()
+        phs = " ".join(f"{k} {v:.4f}" for k, v in ph.items()) if sum(ph.values()) else "single kernel"
+        print(f"{tag:>14} {key:>6} {a.precision} median {statistics.median(ms):8.4f} ms  min {min(ms):8.4f} ms"
+              f"  [{phs}]", flush=True)
 
 
 if __name__ == "__main__":

@@ -129,7 +129,10 @@ int rt_host_unregister(rt_ctx *ctx, void *ptr);
  *                 shade kernels over HBM queues instead of one megakernel;
  *   "cull"        the wavefront shadow pass skips, per hit, the bodies that
  *                 provably cannot block any of its shadow rays (exact);
- *   "count_work"  tally the executed work of the culled pass (rt_work_counts). */
+ *   "count_work"  tally the executed work of the culled pass (rt_work_counts);
+ *   "bands"       rt_render_v1 on one device renders this many contiguous row
+ *                 bands (1-4) and copies each to the host while the next
+ *                 renders; 0 (default) = 4 for frames of >= 16 MB, else 1. */
 int rt_set_option(rt_ctx *ctx, const char *name, int32_t value);
 /* Executed-work tallies since the last reset: hits, per-hit cull tests, hits
  * that sampled, shadow rays traced, sphere tests, plane tests. */

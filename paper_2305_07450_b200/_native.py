@@ -196,9 +196,10 @@ _options = {}  # execution options applied to every context (rt_set_option)
 
 def set_options(**opts) -> None:
     """Execution options for every context, present and future:
-    wave (bool), cull (bool), count_work (bool) — see include/b200rt.h."""
+    wave (bool), cull (bool), count_work (bool), bands (0-4) — see
+    include/b200rt.h (rt_set_option)."""
     with _ctx_lock:
-        _options.update({k: int(bool(v)) for k, v in opts.items()})
+        _options.update({k: int(v) for k, v in opts.items()})
         for ctx in _contexts.values():
             for k, v in opts.items():
                 ctx.set_option(k, v)

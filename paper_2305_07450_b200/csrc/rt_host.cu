@@ -137,6 +137,7 @@ struct rt_ctx {
     bool wave = true;   // FP32 soft shadows take the wavefront path ($B200RT_WAVE=0: megakernel)
     bool cull = true;   // exact per-hit occluder culling in the wavefront shadow pass ($B200RT_CULL=0: off)
     bool count_work = false;  // tally the culled path's executed work (rt_work_counts)
+    int bands = 0;            // single-device row bands for copy overlap (0: by frame size)
     std::mutex mu;
     HostScene scene;
     float last_ms = 0.f;
@@ -578,7 +579,7 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
         Dev &d = ctx->devs[0];
         RT_CK(cudaSetDevice(d.id));
         // (a band costs ~5 kernel boundaries; below ~16 MB that outweighs the hidden copy)
-        int bands = px_bytes >= ((size_t)16 << 20) ? 4 : 1;
+        int bands = ctx->bands > 0 ? ctx->bands : (px_bytes >= ((size_t)16 << 20) ? 4 : 1);
         bands = std::max(1, std::min(bands, height / 8));
         const int band_rows = (height + bands - 1) / bands;
         RT_CK(cudaEventRecord(d.e0, d.st));
@@ -805,6 +806,7 @@ int rt_set_option(rt_ctx *ctx, const char *name, int32_t value) {
     if (n == "wave") ctx->wave = value != 0;
     else if (n == "cull") ctx->cull = value != 0;
     else if (n == "count_work") ctx->count_work = value != 0;
+    else if (n == "bands") ctx->bands = std::max(0, std::min((int)value, 4));
     else return fail(RT_ERR_INVALID, "unknown option " + n);
     return RT_OK;
 }

@@ -168,31 +168,49 @@ struct ParamScene {
                     slot = b;
                 }
             }
-            if (slot >= 0) h.idx = sph_idx[slot];
+            if (slot >= 0) {
+                h.idx = sph_idx[slot];
+                h.g = sph[slot];
+            }
+#pragma unroll
+            for (int j = 0; j < kMaxPlanes; j++) {
+                if (j >= np) break;
+                float t = plane_t(o, d, pl_h[j]);
+                if (t < h.t || (t == h.t && pl_idx[j] < h.idx)) {  // geometry.py:198 across kinds
+                    h.t = t;
+                    h.idx = pl_idx[j];
+                    h.g = make_float4(0.f, pl_h[j], 0.f, -1.f);
+                }
+            }
         } else {
+            // planes first: a floor hit bounds the cluster walk
+#pragma unroll
+            for (int j = 0; j < kMaxPlanes; j++) {
+                if (j >= np) break;
+                float t = plane_t(o, d, pl_h[j]);
+                if (t < h.t || (t == h.t && pl_idx[j] < h.idx)) {
+                    h.t = t;
+                    h.idx = pl_idx[j];
+                    h.g = make_float4(0.f, pl_h[j], 0.f, -1.f);
+                }
+            }
             for (int c = 0; c < nc; c++) {
                 if (bound_entry(o, d, cl[c]) > h.t) continue;
-                for (int b = cl_begin[c]; b < cl_begin[c + 1]; b++) {
+                const int b1 = cl_begin[c + 1];
+#pragma unroll 4
+                for (int b = cl_begin[c]; b < b1; b++) {
                     float t = sphere_t(o, d, sph[b]);
-                    int id = sph_idx[b];
-                    if (t < h.t || (t == h.t && id < h.idx)) {  // lowest original index wins ties
-                        h.t = t;
-                        h.idx = id;
-                        slot = b;
+                    if (t <= h.t) {
+                        int id = sph_idx[b];
+                        if (t < h.t || id < h.idx) {  // (t, index) order: lowest original index wins ties
+                            h.t = t;
+                            h.idx = id;
+                            slot = b;
+                        }
                     }
                 }
             }
-        }
-        if (slot >= 0) h.g = sph[slot];
-#pragma unroll
-        for (int j = 0; j < kMaxPlanes; j++) {
-            if (j >= np) break;
-            float t = plane_t(o, d, pl_h[j]);
-            if (t < h.t || (t == h.t && pl_idx[j] < h.idx)) {  // geometry.py:198 across kinds
-                h.t = t;
-                h.idx = pl_idx[j];
-                h.g = make_float4(0.f, pl_h[j], 0.f, -1.f);
-            }
+            if (slot >= 0 && h.idx == sph_idx[slot]) h.g = sph[slot];
         }
         return h;
     }

@@ -94,12 +94,166 @@ __device__ __forceinline__ void trace_chain(const Geo &geo, const FrameArgs &fa,
     wa.pix[lp] = make_float4(tail.x, tail.y, tail.z, __int_as_float(m | (exhausted << 8)));
 }
 
+// Many-sphere scenes (> 8 spheres): closest hits against a warp-uniform
+// candidate list.  Per bounce the warp bounds its live rays — origins within
+// rho of their mean Co, directions within theta of their mean A — so every
+// point a ray can reach lies in the cone (Co, A, theta) dilated by rho; a
+// sphere farther than its (grazing-padded) radius from that set cannot be
+// hit by any of the warp's rays and is skipped.  The 32 lanes classify 32
+// spheres at a time; the survivors (a uniform bit mask) are tested by every
+// lane in lockstep, ties broken by the lowest original index.
+template <int MAXS>
+__device__ __forceinline__ bool sphere_meets_bundle(float4 g, float3 co, float3 A, float cos_t, float sin_t,
+                                                    float rho) {
+    float3 u = f3(g.x - co.x, g.y - co.y, g.z - co.z);
+    float u2 = dot3(u, u);
+    float h = dot3(u, A);
+    float3 w = u - A * h;
+    float q = sqrtf(dot3(w, w));
+    float un = sqrtf(u2);
+    float R = (sqrtf(g.w + 1e-7f) + rho) * (1.f + kBoundRel) + kBoundRel * (1.f + un);
+    if (h < -R) return false;
+    float dist = (h * cos_t + q * sin_t >= 0.f) ? q * cos_t - h * sin_t : un;
+    return dist < R;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_min(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+template <int MAXS>
+__device__ __forceinline__ void trace_chain_bundle(const ParamScene<MAXS> &ps, const FrameArgs &fa,
+                                                   const SceneArgs<float> &sa, const WaveArgs &wa, int x, int ly) {
+    constexpr int kWords = (MAXS + 31) / 32;
+    const int lane = threadIdx.x & 31;
+    int y = 0;
+    bool alive = x < fa.width && ly < fa.local_rows;
+    if (alive) {
+        y = map_row(ly, fa);
+        alive = y < fa.row_end;
+    }
+    const bool valid = alive;
+    const int64_t lp = (int64_t)ly * fa.width + x;
+    float3 origin = f3((float)fa.cam[0], (float)fa.cam[1], (float)fa.cam[2]);
+    float3 dir = valid ? primary_direction(x, y, fa) : f3(0.f, 0.f, 1.f);
+    const float3 light = f3(sa.light[0], sa.light[1], sa.light[2]);
+    float3 tail = f3(0.f, 0.f, 0.f);
+    int m = 0, exhausted = 0;
+    for (int k = 0; k <= fa.bounces; k++) {
+        const unsigned live = __ballot_sync(0xffffffffu, alive);
+        if (!live) break;
+        // bundle of the live rays
+        float3 sd = f3(warp_sum(alive ? dir.x : 0.f), warp_sum(alive ? dir.y : 0.f), warp_sum(alive ? dir.z : 0.f));
+        float sn = dot3(sd, sd);
+        float3 A = sd * (sn > 0.f ? rsqrtf(sn) : 0.f);
+        float cos_t = warp_min(alive ? dot3(dir, A) : 1.f);
+        const float inv_n = 1.f / (float)__popc(live);
+        float3 co = f3(warp_sum(alive ? origin.x : 0.f) * inv_n, warp_sum(alive ? origin.y : 0.f) * inv_n,
+                       warp_sum(alive ? origin.z : 0.f) * inv_n);
+        float3 dco = origin - co;
+        float rho = warp_max(alive ? sqrtf(dot3(dco, dco)) : 0.f);
+        const bool cull = cos_t > 0.25f && sn > 0.f;
+        cos_t = fminf(cos_t * (1.f - kBoundRel), 1.f);  // widen the cone for rounding
+        const float sin_t = sqrtf(fmaxf(1.f - cos_t * cos_t, 0.f));
+        unsigned mask[kWords];
+#pragma unroll
+        for (int w = 0; w < kWords; w++) {
+            const int b = w * 32 + lane;
+            bool cand = b < ps.ns && (!cull || sphere_meets_bundle<MAXS>(ps.sph[b < MAXS ? b : 0], co, A, cos_t,
+                                                                          sin_t, rho));
+            mask[w] = __ballot_sync(0xffffffffu, cand);
+        }
+        Hit h{-1, INFINITY, make_float4(0.f, 0.f, 0.f, -1.f)};
+        if (alive) {
+#pragma unroll
+            for (int j = 0; j < kMaxPlanes; j++) {
+                if (j >= ps.np) break;
+                float t = plane_t(origin, dir, ps.pl_h[j]);
+                if (t < h.t || (t == h.t && ps.pl_idx[j] < h.idx)) {
+                    h.t = t;
+                    h.idx = ps.pl_idx[j];
+                    h.g = make_float4(0.f, ps.pl_h[j], 0.f, -1.f);
+                }
+            }
+            int slot = -1;
+#pragma unroll
+            for (int w = 0; w < kWords; w++) {
+                for (unsigned bm = mask[w]; bm; bm &= bm - 1) {
+                    const int b = w * 32 + __ffs(bm) - 1;
+                    float t = sphere_t(origin, dir, ps.sph[b]);
+                    if (t <= h.t) {
+                        int id = ps.sph_idx[b];
+                        if (t < h.t || id < h.idx) {  // (t, index) order: lowest original index wins ties
+                            h.t = t;
+                            h.idx = id;
+                            slot = b;
+                        }
+                    }
+                }
+            }
+            if (slot >= 0 && h.idx == ps.sph_idx[slot]) h.g = ps.sph[slot];
+        }
+        const bool hit_now = alive && h.idx >= 0;
+        if (alive && !hit_now) {
+            if (sa.has_sky) tail = sky_sample(dir, sa.sky, sa.sky_w, sa.sky_h);
+            alive = false;
+        }
+        int64_t slot_id = 0;
+        if (hit_now) {
+            float3 hit = origin + dir * h.t;
+            float3 normal = h.g.w >= 0.f ? normalize3(hit - f3(h.g.x, h.g.y, h.g.z)) : f3(0.f, 1.f, 0.f);
+            float3 l = normalize3(light - hit);
+            float dfs = fmaxf(dot3(normal, l), 0.f);
+            float3 hv = l - dir;
+            float hm2 = dot3(hv, hv);
+            float s = 0.f;
+            if (hm2 > 0.f) {
+                float dd = fmaxf(dot3(normal, hv) * rsqrtf(hm2), 0.f);
+                s = powf(dd, __ldg(sa.mat + 8 * h.idx + 4));
+            }
+            slot_id = (int64_t)k * wa.n_pix + lp;
+            wa.hit_p[slot_id] = make_float4(hit.x, hit.y, hit.z, __int_as_float(h.idx));
+            wa.hit_n[slot_id] = make_float4(normal.x, normal.y, normal.z, dfs);
+            wa.hit_s[slot_id] = s;
+            m = k + 1;
+            if (k == fa.bounces) {
+                exhausted = 1;
+                alive = false;
+            } else {
+                origin = hit + normal * 1e-3f;
+                dir = dir - normal * (2.f * dot3(normal, dir));
+            }
+        }
+        const unsigned hb = __ballot_sync(0xffffffffu, hit_now);
+        unsigned base = 0;
+        if (lane == 0 && hb) base = atomicAdd(wa.count, (unsigned)__popc(hb));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (hit_now) wa.queue[base + __popc(hb & lanemask_lt())] = (int)slot_id;
+    }
+    if (valid) wa.pix[lp] = make_float4(tail.x, tail.y, tail.z, __int_as_float(m | (exhausted << 8)));
+}
+
 template <int MAXS>
 __global__ void __launch_bounds__(kThreads)
     wave_trace_param(const FrameArgs fa, const SceneArgs<float> sa, const WaveArgs wa, const ParamScene<MAXS> ps) {
     int x, ly;
     thread_pixel(x, ly);
-    trace_chain(ps, fa, sa, wa, x, ly);
+    if constexpr (ParamScene<MAXS>::kClustered)
+        trace_chain_bundle(ps, fa, sa, wa, x, ly);
+    else
+        trace_chain(ps, fa, sa, wa, x, ly);
 }
 
 template <bool SMEM>

@@ -175,6 +175,14 @@ __device__ __forceinline__ void trace_chain_bundle(const ParamScene<MAXS> &ps, c
                                                                           sin_t, rho));
             mask[w] = __ballot_sync(0xffffffffu, cand);
         }
+        if (wa.work && lane == 0) {
+            int nc = 0;
+#pragma unroll
+            for (int w = 0; w < kWords; w++) nc += __popc(mask[w]);
+            atomicAdd(wa.work + kWorkTraceRays, (unsigned long long)__popc(live));
+            atomicAdd(wa.work + kWorkTraceTests, (unsigned long long)__popc(live) * nc);
+            if (!cull) atomicAdd(wa.work + kWorkTraceFullWarps, 1ull);
+        }
         Hit h{-1, INFINITY, make_float4(0.f, 0.f, 0.f, -1.f)};
         if (alive) {
 #pragma unroll

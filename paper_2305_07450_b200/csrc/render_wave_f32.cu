@@ -138,6 +138,10 @@ __device__ __forceinline__ void trace_chain_bundle(const ParamScene<MAXS> &ps, c
                                                    const SceneArgs<float> &sa, const WaveArgs &wa, int x, int ly) {
     constexpr int kWords = (MAXS + 31) / 32;
     const int lane = threadIdx.x & 31;
+    __shared__ float4 s_cand_sph[kThreads / 32][MAXS];
+    __shared__ int s_cand_idx[kThreads / 32][MAXS];
+    float4 *cand_sph = s_cand_sph[threadIdx.x >> 5];
+    int *cand_idx = s_cand_idx[threadIdx.x >> 5];
     int y = 0;
     bool alive = x < fa.width && ly < fa.local_rows;
     if (alive) {
@@ -167,20 +171,26 @@ __device__ __forceinline__ void trace_chain_bundle(const ParamScene<MAXS> &ps, c
         const bool cull = cos_t > 0.25f && sn > 0.f;
         cos_t = fminf(cos_t * (1.f - kBoundRel), 1.f);  // widen the cone for rounding
         const float sin_t = sqrtf(fmaxf(1.f - cos_t * cos_t, 0.f));
-        unsigned mask[kWords];
+        // compact the candidates into this warp's shared-memory list: every
+        // lane then walks the same entries (broadcast LDS, unrolled)
+        int ncand = 0;
 #pragma unroll
         for (int w = 0; w < kWords; w++) {
             const int b = w * 32 + lane;
             bool cand = b < ps.ns && (!cull || sphere_meets_bundle<MAXS>(ps.sph[b < MAXS ? b : 0], co, A, cos_t,
                                                                           sin_t, rho));
-            mask[w] = __ballot_sync(0xffffffffu, cand);
+            const unsigned bm = __ballot_sync(0xffffffffu, cand);
+            if (cand) {
+                const int at = ncand + __popc(bm & lanemask_lt());
+                cand_sph[at] = ps.sph[b];
+                cand_idx[at] = ps.sph_idx[b];
+            }
+            ncand += __popc(bm);
         }
+        __syncwarp();
         if (wa.work && lane == 0) {
-            int nc = 0;
-#pragma unroll
-            for (int w = 0; w < kWords; w++) nc += __popc(mask[w]);
             atomicAdd(wa.work + kWorkTraceRays, (unsigned long long)__popc(live));
-            atomicAdd(wa.work + kWorkTraceTests, (unsigned long long)__popc(live) * nc);
+            atomicAdd(wa.work + kWorkTraceTests, (unsigned long long)__popc(live) * ncand);
             if (!cull) atomicAdd(wa.work + kWorkTraceFullWarps, 1ull);
         }
         Hit h{-1, INFINITY, make_float4(0.f, 0.f, 0.f, -1.f)};
@@ -195,24 +205,22 @@ __device__ __forceinline__ void trace_chain_bundle(const ParamScene<MAXS> &ps, c
                     h.g = make_float4(0.f, ps.pl_h[j], 0.f, -1.f);
                 }
             }
-            int slot = -1;
-#pragma unroll
-            for (int w = 0; w < kWords; w++) {
-                for (unsigned bm = mask[w]; bm; bm &= bm - 1) {
-                    const int b = w * 32 + __ffs(bm) - 1;
-                    float t = sphere_t(origin, dir, ps.sph[b]);
-                    if (t <= h.t) {
-                        int id = ps.sph_idx[b];
-                        if (t < h.t || id < h.idx) {  // (t, index) order: lowest original index wins ties
-                            h.t = t;
-                            h.idx = id;
-                            slot = b;
-                        }
+            int best = -1;
+#pragma unroll 4
+            for (int c = 0; c < ncand; c++) {
+                float t = sphere_t(origin, dir, cand_sph[c]);
+                if (t <= h.t) {
+                    int id = cand_idx[c];
+                    if (t < h.t || id < h.idx) {  // (t, index) order: lowest original index wins ties
+                        h.t = t;
+                        h.idx = id;
+                        best = c;
                     }
                 }
             }
-            if (slot >= 0 && h.idx == ps.sph_idx[slot]) h.g = ps.sph[slot];
+            if (best >= 0 && h.idx == cand_idx[best]) h.g = cand_sph[best];
         }
+        __syncwarp();
         const bool hit_now = alive && h.idx >= 0;
         if (alive && !hit_now) {
             if (sa.has_sky) tail = sky_sample(dir, sa.sky, sa.sky_w, sa.sky_h);

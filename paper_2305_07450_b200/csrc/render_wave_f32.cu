@@ -142,6 +142,15 @@ __device__ __forceinline__ void trace_chain_bundle(const ParamScene<MAXS> &ps, c
     __shared__ int s_cand_idx[kThreads / 32][MAXS];
     float4 *cand_sph = s_cand_sph[threadIdx.x >> 5];
     int *cand_idx = s_cand_idx[threadIdx.x >> 5];
+    // the lane-parallel bundle test reads 32 different spheres at once: from
+    // shared memory (constant-bank reads with divergent addresses serialise)
+    __shared__ float4 s_sph[MAXS];
+    __shared__ int s_idx[MAXS];
+    for (int i = threadIdx.x; i < ps.ns; i += blockDim.x) {
+        s_sph[i] = ps.sph[i];
+        s_idx[i] = ps.sph_idx[i];
+    }
+    __syncthreads();
     int y = 0;
     bool alive = x < fa.width && ly < fa.local_rows;
     if (alive) {
@@ -177,13 +186,13 @@ __device__ __forceinline__ void trace_chain_bundle(const ParamScene<MAXS> &ps, c
 #pragma unroll
         for (int w = 0; w < kWords; w++) {
             const int b = w * 32 + lane;
-            bool cand = b < ps.ns && (!cull || sphere_meets_bundle<MAXS>(ps.sph[b < MAXS ? b : 0], co, A, cos_t,
-                                                                          sin_t, rho));
+            const float4 g = s_sph[b < ps.ns ? b : 0];
+            bool cand = b < ps.ns && (!cull || sphere_meets_bundle<MAXS>(g, co, A, cos_t, sin_t, rho));
             const unsigned bm = __ballot_sync(0xffffffffu, cand);
             if (cand) {
                 const int at = ncand + __popc(bm & lanemask_lt());
-                cand_sph[at] = ps.sph[b];
-                cand_idx[at] = ps.sph_idx[b];
+                cand_sph[at] = g;
+                cand_idx[at] = s_idx[b];
             }
             ncand += __popc(bm);
         }

@@ -370,6 +370,7 @@ struct Cone {
     float3 o, axis;   // apex, unit axis towards L
     float H, rho;     // axis length, base radius (2R with margin)
     float sin_phi, cos_phi, reach;  // reach = T (H + rho): farthest axial extent of a segment
+    float inv_H;
     bool ok;          // a proper cone (the light ball does not swallow the origin)
 };
 
@@ -381,7 +382,8 @@ __device__ __forceinline__ Cone make_cone(float3 o, float3 lp, float light_radiu
     c.rho = 2.f * light_radius * (1.f + kCullRel) + kCullAbs;
     c.ok = c.H > 0.f && c.rho < 0.999f * c.H;
     c.axis = A * (c.H > 0.f ? 1.f / c.H : 0.f);
-    c.sin_phi = c.ok ? c.rho / c.H : 1.f;
+    c.inv_H = c.H > 0.f ? 1.f / c.H : 0.f;
+    c.sin_phi = c.ok ? c.rho * c.inv_H : 1.f;
     c.cos_phi = sqrtf(fmaxf(1.f - c.sin_phi * c.sin_phi, 0.f));
     float T = 1.f + (1e-3f + kCullAbs) / fmaxf(c.H - c.rho, 1e-6f);
     c.reach = T * (c.H + c.rho) * (1.f + kCullRel) + kCullAbs;
@@ -389,26 +391,30 @@ __device__ __forceinline__ Cone make_cone(float3 o, float3 lp, float light_radiu
 }
 
 // 0: the sphere can block none of the hit's shadow rays; 1: some; 2: all.
-__device__ __forceinline__ int sphere_class(const Cone &k, float4 g) {
+// rr = {r, sqrt(r^2 + 1e-7)} (formed on the host): one square root per test.
+__device__ __forceinline__ int sphere_class(const Cone &k, float4 g, float2 rr) {
     if (!k.ok) return 1;
     float3 u = f3(g.x - k.o.x, g.y - k.o.y, g.z - k.o.z);
     float u2 = dot3(u, u);
-    float r = sqrtf(g.w);
     // the origin inside the sphere: t = tca - sqrt(rad) < 0 for every ray (geometry.py:102-103)
     if (u2 < g.w * (1.f - 4.f * kCullRel) - kCullAbs) return 0;
     float h = dot3(u, k.axis);
     float3 w = u - k.axis * h;
     float q = sqrtf(dot3(w, w));
+    float un = fabsf(h) + q;  // >= |u|
     // grazing rays (rad >= -1e-7, geometry.py:98) count as hits: pad the radius
-    float rp = sqrtf(g.w + 1e-7f) * (1.f + kCullRel) + kCullAbs + 1e-6f * (sqrtf(u2) + k.H);
+    float rp = rr.y * (1.f + kCullRel) + kCullAbs + 1e-6f * (un + k.H);
     if (h < -rp || h - rp > k.reach) return 0;
-    float dist = (h * k.cos_phi + q * k.sin_phi >= 0.f) ? q * k.cos_phi - h * k.sin_phi : sqrtf(u2);
-    if (dist >= rp) return 0;
+    if (h * k.cos_phi + q * k.sin_phi >= 0.f) {
+        if (q * k.cos_phi - h * k.sin_phi >= rp) return 0;
+    } else if (u2 >= rp * rp) {
+        return 0;  // nearest point of the cone is its apex
+    }
     // full block: origin clearly outside, sphere wholly before the disc, and
     // the cone's cross-section at the centre's depth inside the great circle
-    float rm = r * (1.f - 10.f * kCullRel) - kCullAbs - 1e-6f * (sqrtf(u2) + k.H);
+    float rm = rr.x * (1.f - 10.f * kCullRel) - kCullAbs - 1e-6f * (un + k.H);
     if (u2 > g.w * (1.f + 4.f * kCullRel) + kCullAbs && h > 0.f &&
-        h + r < (k.H - k.rho) * (1.f - kCullRel) - 2e-3f && q + (h / k.H) * k.rho * (1.f + kCullRel) < rm)
+        h + rr.x < (k.H - k.rho) * (1.f - kCullRel) - 2e-3f && q + h * k.inv_H * k.rho * (1.f + kCullRel) < rm)
         return 2;
     return 1;
 }
@@ -422,10 +428,10 @@ __device__ __forceinline__ bool bound_meets_cone(const Cone &k, float4 B) {
     float h = dot3(u, k.axis);
     float3 w = u - k.axis * h;
     float q = sqrtf(dot3(w, w));
-    float rp = B.w * (1.f + kCullRel) + kCullAbs + 1e-6f * (sqrtf(u2) + k.H);
+    float rp = B.w * (1.f + kCullRel) + kCullAbs + 1e-6f * (fabsf(h) + q + k.H);
     if (h < -rp || h - rp > k.reach) return false;
-    float dist = (h * k.cos_phi + q * k.sin_phi >= 0.f) ? q * k.cos_phi - h * k.sin_phi : sqrtf(u2);
-    return dist < rp;
+    if (h * k.cos_phi + q * k.sin_phi >= 0.f) return q * k.cos_phi - h * k.sin_phi < rp;
+    return u2 < rp * rp;
 }
 
 // Planes: a shadow segment crosses y = hp iff o.y and its far end (within
@@ -470,7 +476,7 @@ __global__ void __launch_bounds__(kThreads)
             const float3 origin = f3(P.x, P.y, P.z) + f3(N.x, N.y, N.z) * 1e-3f;
             const Cone k = make_cone(origin, lp, sa.light_radius);
             auto classify = [&](int b) {
-                int cls = sphere_class(k, ps.sph[b]);  // b is warp-uniform: a constant-cache broadcast
+                int cls = sphere_class(k, ps.sph[b], ps.sph_rad[b]);  // b warp-uniform: constant-cache broadcast
                 mask[b >> 5] |= (cls == 1 ? 1u : 0u) << (b & 31);
                 full |= cls == 2;
             };

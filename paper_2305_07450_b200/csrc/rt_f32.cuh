@@ -149,6 +149,7 @@ struct ParamScene {
     static constexpr int kNC = kClustered ? kMaxClusters : 1;
     float4 sph[MAXS];
     int sph_idx[MAXS];
+    float2 sph_rad[MAXS];    // {r, sqrt(r^2 + 1e-7)} for the shadow-cone classifier
     float pl_h[kMaxPlanes];
     int pl_idx[kMaxPlanes];
     float4 cl[kNC];          // cluster bounds {centre, radius}
@@ -414,10 +415,13 @@ inline bool pack_params(const SceneArgs<float> &sa, ParamScene<MAXS> &ps) {
     for (int i = 0; i < ps.ns; i++) {
         ps.sph[i] = sph[order[i]];
         ps.sph_idx[i] = idx[order[i]];
+        const double r2 = sa.host_geo[4 * idx[order[i]] + 3];
+        ps.sph_rad[i] = make_float2((float)std::sqrt(r2), (float)std::sqrt(r2 + 1e-7));
     }
     for (int b = ps.ns; b < MAXS; b++) {
         ps.sph[b] = make_float4(0.f, 0.f, 0.f, 0.f);
         ps.sph_idx[b] = 0;
+        ps.sph_rad[b] = make_float2(0.f, 0.f);
     }
     for (int j = ps.np; j < kMaxPlanes; j++) {
         ps.pl_h[j] = 0.f;

@@ -19,8 +19,12 @@ def main():
     ap.add_argument("--frames", type=int, default=3)
     ap.add_argument("--precision", default="fp32")
     ap.add_argument("--workers", type=int, default=None)
+    ap.add_argument("--bands", type=int, default=1, help="rt_render_v1 row bands (0 = by frame size)")
     a = ap.parse_args()
     cfg = rt.CONFIGS[a.config]
+    from paper_2305_07450_b200 import _native
+
+    _native.set_options(bands=a.bands)
     scene, cam, params = cfg.scene(), cfg.camera(), cfg.params()
     fb = rt.Framebuffer.create(cfg.width, cfg.height)
     for i in range(a.frames):

@@ -567,6 +567,39 @@ __device__ __forceinline__ void cull_sample_hit(const ParamScene<MAXS> &ps, cons
             shadow_ray(f, t, dir, limit);
             unblocked += (i < n && !(sphere_margin_L(L, dir, r2g, limit) > 0.f)) ? 1 : 0;
         }
+    } else if (nsph <= kRegCand) {
+        // up to kRegCand spheres (+ planes): one pass, counted directly
+        float4 c[kRegCand];
+        int k = 0, w = 0;
+        unsigned mw = hm[0];
+#pragma unroll
+        for (int r = 0; r < kRegCand; r++) {
+            c[r] = make_float4(0.f, 0.f, 0.f, -INFINITY);
+            while (mw == 0 && w + 1 < kWords) mw = hm[++w];
+            if (mw != 0) {
+                const float4 g = ps.sph[w * 32 + __ffs(mw) - 1];
+                mw &= mw - 1;
+                const float3 L = f3(g.x - f.origin.x, g.y - f.origin.y, g.z - f.origin.z);
+                c[r] = make_float4(L.x, L.y, L.z, sphere_r2g(L, g.w));
+                k++;
+            }
+        }
+        const unsigned pm = hm[kWords];
+        for (int j = 0; j < rounds; j++) {
+            const int i = lane + 32 * j;
+            const int ic = i < n ? i : 0;
+            const float4 t = n == 1 ? make_float4(0.f, 0.f, 0.f, 0.f) : (SMEM_TAB ? tab[ic] : __ldg(tab + ic));
+            float3 dir;
+            float limit;
+            shadow_ray(f, t, dir, limit);
+            float m = -INFINITY;
+#pragma unroll
+            for (int r = 0; r < kRegCand; r++)
+                if (r < k) m = fmaxf(m, sphere_margin_L(f3(c[r].x, c[r].y, c[r].z), dir, c[r].w, limit));
+            for (unsigned b = pm; b; b &= b - 1)
+                m = fmaxf(m, plane_margin(ps.pl_h[__ffs(b) - 1] - f.origin.y, dir.y, limit));
+            unblocked += (i < n && !(m > 0.f)) ? 1 : 0;
+        }
     } else
     // rounds in groups of 64 (a bit per round); candidates kRegCand at a time
     for (int g0 = 0; g0 < rounds; g0 += 64) {

@@ -36,6 +36,7 @@ struct FrameArgs {
     double cam[3];
     double cb, sb, ca, sa;  // cos/sin(pitch), cos/sin(yaw) (host libm, vecmath.py:99-110)
     double vdist;           // camera.py:64-67
+    double ndc[4];          // FP32 kernels: u = x*ndc[0] + ndc[1], v = y*ndc[2] + ndc[3] (camera.py:46-54)
     int samples, bounces;
     int peer_out;  // out lives on another GPU: fence the stores at system scope
     unsigned int *work_counter;  // zeroed before the launch: persistent warps take 8x4 patches from it

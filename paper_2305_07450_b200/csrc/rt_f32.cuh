@@ -39,21 +39,17 @@ __device__ __forceinline__ float3 normalize3(float3 a) {
 
 // camera.py:46-77 in float64 (exactly the reference's direction), then rounded
 __device__ __forceinline__ float3 primary_direction(int xi, int yi, const FrameArgs &fa) {
-    double x = (double)xi, y = (double)yi, w = (double)fa.width, h = (double)fa.height;
-    double u, v;
-    if (w > h) {
-        u = (x - w / 2 + h / 2) / h * 2 - 1;
-        v = -(y / h * 2 - 1);
-    } else {
-        u = x / w * 2 - 1;
-        v = -((y - h / 2 + w / 2) / w * 2 - 1);
-    }
-    double m = sqrt(u * u + v * v + fa.vdist * fa.vdist);
-    double dx = u / m, dy = v / m, dz = fa.vdist / m;
-    double y2 = dy * fa.cb - dz * fa.sb;
-    double z2 = dy * fa.sb + dz * fa.cb;
-    double x2 = dx * fa.ca + z2 * fa.sa;
-    double z3 = -dx * fa.sa + z2 * fa.ca;
+    // float64 throughout (u, v, normalisation, pitch/yaw rotation), one FMA per
+    // NDC coordinate and a reciprocal square root instead of the reference's
+    // five divisions and a square root; rounded to float at the end
+    const double u = fma((double)xi, fa.ndc[0], fa.ndc[1]);
+    const double v = fma((double)yi, fa.ndc[2], fa.ndc[3]);
+    const double inv = rsqrt(fma(u, u, fma(v, v, fa.vdist * fa.vdist)));
+    const double dx = u * inv, dy = v * inv, dz = fa.vdist * inv;
+    const double y2 = dy * fa.cb - dz * fa.sb;
+    const double z2 = dy * fa.sb + dz * fa.cb;
+    const double x2 = dx * fa.ca + z2 * fa.sa;
+    const double z3 = -dx * fa.sa + z2 * fa.ca;
     return f3((float)x2, (float)y2, (float)z3);
 }
 

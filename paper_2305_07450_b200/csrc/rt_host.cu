@@ -373,6 +373,22 @@ rt::FrameArgs frame_args(uint32_t *out, int64_t pitch, void *rad, int w, int h, 
     fa.ca = std::cos(yaw);
     fa.sa = std::sin(yaw);
     fa.vdist = vdist;
+    // camera.py:46-54 as one FMA per coordinate (the FP32 kernels round the
+    // direction to float anyway; the FP64 kernel keeps the literal formula)
+    {
+        double W = w, Hh = h;
+        if (W > Hh) {
+            fa.ndc[0] = 2.0 / Hh;
+            fa.ndc[1] = (Hh / 2 - W / 2) / Hh * 2 - 1;
+            fa.ndc[2] = -2.0 / Hh;
+            fa.ndc[3] = 1.0;
+        } else {
+            fa.ndc[0] = 2.0 / W;
+            fa.ndc[1] = -1.0;
+            fa.ndc[2] = -2.0 / W;
+            fa.ndc[3] = -((W / 2 - Hh / 2) / W * 2 - 1);
+        }
+    }
     fa.samples = samples;
     fa.bounces = bounces;
     fa.peer_out = 0;

@@ -551,22 +551,31 @@ __device__ __forceinline__ void cull_sample_hit(const ParamScene<MAXS> &ps, cons
     const ShadowFrame f = shadow_frame(f3(P.x, P.y, P.z), f3(N.x, N.y, N.z), lp, n > 1);
     int unblocked = 0;
     if (nsph == 1 && hm[kWords] == 0) {
-        // the common penumbra case: one sphere against every sample
+        // the common penumbra case: one sphere against every sample; full
+        // rounds of 32 samples without bounds checks, then the remainder
+        static_assert(kWaveMinSamples > 1, "the wavefront path assumes soft shadows");
         int w = 0;
         while (hm[w] == 0) w++;
         const float4 g = ps.sph[w * 32 + __ffs(hm[w]) - 1];
         const float3 L = f3(g.x - f.origin.x, g.y - f.origin.y, g.z - f.origin.z);
         const float r2g = sphere_r2g(L, g.w);
-#pragma unroll 2
-        for (int j = 0; j < rounds; j++) {
-            const int i = lane + 32 * j;
-            const int ic = i < n ? i : 0;
-            const float4 t = n == 1 ? make_float4(0.f, 0.f, 0.f, 0.f) : (SMEM_TAB ? tab[ic] : __ldg(tab + ic));
+        auto sample = [&](int i) -> int {
+            float4 t;
+            if constexpr (SMEM_TAB) {
+                extern __shared__ float4 smem_tab_s[];
+                t = smem_tab_s[i];
+            } else {
+                t = __ldg(tab + i);
+            }
             float3 dir;
             float limit;
-            shadow_ray(f, t, dir, limit);
-            unblocked += (i < n && !(sphere_margin_L(L, dir, r2g, limit) > 0.f)) ? 1 : 0;
-        }
+            shadow_ray_unguarded(f, t, dir, limit);
+            return sphere_margin_L(L, dir, r2g, limit) > 0.f ? 0 : 1;
+        };
+        const int full = n >> 5;
+#pragma unroll 2
+        for (int j = 0; j < full; j++) unblocked += sample(lane + 32 * j);
+        if (lane + 32 * full < n) unblocked += sample(lane + 32 * full);
     } else if (nsph <= kRegCand) {
         // up to kRegCand spheres (+ planes): one pass, counted directly
         float4 c[kRegCand];

@@ -37,7 +37,7 @@ __device__ __forceinline__ float3 normalize3(float3 a) {
     return a * inv;
 }
 
-// camera.py:46-77 in float64 (exactly the reference's direction), then rounded
+// camera.py:46-77 in float64, then rounded
 __device__ __forceinline__ float3 primary_direction(int xi, int yi, const FrameArgs &fa) {
     // float64 throughout (u, v, normalisation, pitch/yaw rotation), one FMA per
     // NDC coordinate and a reciprocal square root instead of the reference's
@@ -467,6 +467,18 @@ __device__ __forceinline__ void shadow_ray(const ShadowFrame &f, float4 t, float
     dir = dv * (r2 > 0.f ? rsqrtf(r2) : 0.f);
     float l2 = f.ls2 + t.z;
     limit = l2 > 0.f ? l2 * rsqrtf(l2) : 0.f;
+}
+
+// The same without the zero-length guards, for the soft-shadow loops: a
+// zero-length vector needs the surface point on the light disc itself, where
+// the NaN it produces makes every margin comparison false — unblocked, as the
+// reference's zero direction / zero limit give.
+__device__ __forceinline__ void shadow_ray_unguarded(const ShadowFrame &f, float4 t, float3 &dir, float &limit) {
+    float3 dv = f3(fmaf(f.bv.x, t.y, fmaf(f.bu.x, t.x, f.lo.x)), fmaf(f.bv.y, t.y, fmaf(f.bu.y, t.x, f.lo.y)),
+                   fmaf(f.bv.z, t.y, fmaf(f.bu.z, t.x, f.lo.z)));
+    dir = dv * rsqrtf(dot3(dv, dv));
+    float l2 = f.ls2 + t.z;
+    limit = l2 * rsqrtf(l2);
 }
 
 // Persistent grid: as many CTAs as fit on the device at once (memoised per

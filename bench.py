@@ -469,6 +469,9 @@ def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True):
         flops["classify"] = 0
         flops["shadow"] = (c["SH_RAYS"] * setup + c["HITS"] * (FLOP_BASIS if samples > 1 else 0)
                            + sh_tests * FLOP_SPHERE_FULL + c["SH_PLANE"] * FLOP_PLANE)
+    if phases and phases.get("classify", 0) == 0 and flops.get("classify"):
+        flops["trace"] += flops["classify"]  # fused path: the trace kernel classifies its hits
+        flops["classify"] = 0
     if phases and sum(phases.values()) > 0:
         kernel = max(phases, key=phases.get)
         kms = phases[kernel]

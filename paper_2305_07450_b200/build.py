@@ -31,6 +31,7 @@ SOURCES = {
     # and asinf stay full precision: no --use_fast_math)
     "render_f32.cu": ["--ftz=true", "--prec-div=false", "--prec-sqrt=false"],
     "render_wave_f32.cu": ["--ftz=true", "--prec-div=false", "--prec-sqrt=false"],
+    "render_fused_f32.cu": ["--ftz=true", "--prec-div=false", "--prec-sqrt=false"],
     "render_f64.cu": ["-fmad=false"],
 }
 

@@ -1,0 +1,453 @@
+// FP32 soft shadows with exact occluder culling — the default product path
+// for shadow_samples >= kWaveMinSamples.  Two kernels per frame:
+//
+//   A  trace   one thread per pixel: the bounce chain (closest hit,
+//              geometry.py:191-201; a warp ray-bundle candidate list in scenes
+//              of more than 8 spheres), per hit the Lambert and Blinn factors
+//              (shading.py:53-73) and the exact classification of every body
+//              against the hit's shadow cone (rt_wave.cuh): nothing can block
+//              -> coefficient 1, something blocks every sample -> 0, else the
+//              hit is queued with its candidate-body mask.  A pixel whose hits
+//              are all decided is unwound (renderer.py:185-224) and packed
+//              (renderer.py:45-50) right here; otherwise its records are parked
+//              in HBM with a count of pending hits.
+//   B  sample  one warp per queued hit, 32 disc samples abreast against that
+//              hit's candidate bodies (held in registers); the warp that
+//              settles a pixel's last pending hit unwinds and packs it.
+//
+// Arithmetic per shadow test is the unculled kernels' (render_wave_f32.cu,
+// render_f32.cu) operation for operation: the frames are bit-identical.
+//
+// HBM, slot = bounce * n_pix + local pixel:
+//   hit_p float4 {p, body}, hit_n float4 {n, Lambert}   queued (undecided) hits only
+//   rec   float4 {body, Lambert, Blinn, coefficient}    every hit of a pending pixel
+//   pix   float4 {tail rgb, records | exhausted << 8}   pending pixels
+//   pending int per pixel; queue2 slots + candidate masks (word-major)
+#include "rt_wave.cuh"
+
+namespace {
+using namespace rt;
+using namespace rt32;
+
+constexpr int kRegCand = 4;  // candidate spheres a sampling warp keeps in registers
+
+// Classify every body against one hit's shadow cone (a single lane).
+// Returns 0 (nothing can block), 2 (a body blocks every sample) or 1
+// (undecided; mask[] holds the candidates: sphere slots in words
+// 0..kWords-1, planes in word kWords).
+template <int MAXS>
+__device__ __forceinline__ int classify_hit(const ParamScene<MAXS> &ps, const Cone &k, float oy, float ly,
+                                            unsigned *mask) {
+    constexpr int kWords = (MAXS + 31) / 32;
+#pragma unroll
+    for (int w = 0; w <= kWords; w++) mask[w] = 0;
+    bool full = false;
+    auto classify = [&](int b) {
+        int cls = sphere_class(k, ps.sph[b], ps.sph_rad[b]);
+        mask[b >> 5] |= (cls == 1 ? 1u : 0u) << (b & 31);
+        full |= cls == 2;
+    };
+    if constexpr (!ParamScene<MAXS>::kClustered) {
+#pragma unroll
+        for (int b = 0; b < MAXS; b++) {
+            if (b >= ps.ns) break;
+            classify(b);
+        }
+    } else {
+        for (int c = 0; c < ps.nc; c++) {
+            if (!bound_meets_cone(k, ps.cl[c])) continue;
+            for (int b = ps.cl_begin[c]; b < ps.cl_begin[c + 1]; b++) classify(b);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxPlanes; j++) {
+        if (j >= ps.np) break;
+        int cls = plane_class(k, oy, ly, ps.pl_h[j]);
+        mask[kWords] |= (cls == 1 ? 1u : 0u) << j;
+        full |= cls == 2;
+    }
+    if (full) return 2;
+    bool any = false;
+#pragma unroll
+    for (int w = 0; w <= kWords; w++) any |= mask[w] != 0;
+    return any ? 1 : 0;
+}
+
+// --- A ----------------------------------------------------------------------------
+template <int MAXS>
+__global__ void __launch_bounds__(kThreads)
+    fused_trace(const FrameArgs fa, const SceneArgs<float> sa, const WaveArgs wa, const ParamScene<MAXS> ps) {
+    constexpr int kWords = (MAXS + 31) / 32;
+    constexpr bool kBundle = ParamScene<MAXS>::kClustered;
+    constexpr int kCandCap = kBundle ? MAXS : 1;
+    const int lane = threadIdx.x & 31;
+    // many-sphere scenes: spheres staged in shared memory for the lane-parallel
+    // bundle test, and a per-warp candidate list (see trace_chain_bundle)
+    __shared__ float4 s_sph[kCandCap];
+    __shared__ int s_idx[kCandCap];
+    __shared__ float4 s_cand_sph[kThreads / 32][kCandCap];
+    __shared__ int s_cand_idx[kThreads / 32][kCandCap];
+    if constexpr (kBundle) {
+        for (int i = threadIdx.x; i < ps.ns; i += blockDim.x) {
+            s_sph[i] = ps.sph[i];
+            s_idx[i] = ps.sph_idx[i];
+        }
+        __syncthreads();
+    }
+    float4 *cand_sph = s_cand_sph[threadIdx.x >> 5];
+    int *cand_idx = s_cand_idx[threadIdx.x >> 5];
+
+    int x, ly;
+    thread_pixel(x, ly);
+    int y = 0;
+    bool alive = x < fa.width && ly < fa.local_rows;
+    if (alive) {
+        y = map_row(ly, fa);
+        alive = y < fa.row_end;
+    }
+    const bool valid = alive;
+    const int64_t lp = (int64_t)ly * fa.width + x;
+    const float3 light = f3(sa.light[0], sa.light[1], sa.light[2]);
+    float3 origin = f3((float)fa.cam[0], (float)fa.cam[1], (float)fa.cam[2]);
+    float3 dir = valid ? primary_direction(x, y, fa) : f3(0.f, 0.f, 1.f);
+    float3 tail = f3(0.f, 0.f, 0.f);
+    int m = 0, exhausted = 0, npend = 0;
+    int ridx[kMaxBounce + 1];
+    float rdfs[kMaxBounce + 1], rs[kMaxBounce + 1], rsc[kMaxBounce + 1];
+    for (int k = 0; k <= fa.bounces; k++) {
+        const unsigned live = __ballot_sync(0xffffffffu, alive);
+        if (!live) break;
+        Hit h{-1, INFINITY, make_float4(0.f, 0.f, 0.f, -1.f)};
+        if constexpr (!kBundle) {
+            if (alive) h = ps.closest(origin, dir);
+        } else {
+            // warp bundle of the live rays -> uniform candidate list
+            float3 sd = f3(warp_sum(alive ? dir.x : 0.f), warp_sum(alive ? dir.y : 0.f),
+                           warp_sum(alive ? dir.z : 0.f));
+            float sn = dot3(sd, sd);
+            float3 A = sd * (sn > 0.f ? rsqrtf(sn) : 0.f);
+            float cos_t = warp_min(alive ? dot3(dir, A) : 1.f);
+            const float inv_n = 1.f / (float)__popc(live);
+            float3 co = f3(warp_sum(alive ? origin.x : 0.f) * inv_n, warp_sum(alive ? origin.y : 0.f) * inv_n,
+                           warp_sum(alive ? origin.z : 0.f) * inv_n);
+            float3 dco = origin - co;
+            float rho = warp_max(alive ? sqrtf(dot3(dco, dco)) : 0.f);
+            const bool cull = cos_t > 0.25f && sn > 0.f;
+            cos_t = fminf(cos_t * (1.f - kBoundRel), 1.f);
+            const float sin_t = sqrtf(fmaxf(1.f - cos_t * cos_t, 0.f));
+            int ncand = 0;
+#pragma unroll
+            for (int w = 0; w < kWords; w++) {
+                const int b = w * 32 + lane;
+                const float4 g = s_sph[b < ps.ns ? b : 0];
+                bool cand = b < ps.ns && (!cull || sphere_meets_bundle<MAXS>(g, co, A, cos_t, sin_t, rho));
+                const unsigned bm = __ballot_sync(0xffffffffu, cand);
+                if (cand) {
+                    const int at = ncand + __popc(bm & lanemask_lt());
+                    cand_sph[at] = g;
+                    cand_idx[at] = s_idx[b];
+                }
+                ncand += __popc(bm);
+            }
+            __syncwarp();
+            if (wa.work && lane == 0) {
+                atomicAdd(wa.work + kWorkTraceRays, (unsigned long long)__popc(live));
+                atomicAdd(wa.work + kWorkTraceTests, (unsigned long long)__popc(live) * ncand);
+                if (!cull) atomicAdd(wa.work + kWorkTraceFullWarps, 1ull);
+            }
+            if (alive) {
+#pragma unroll
+                for (int j = 0; j < kMaxPlanes; j++) {
+                    if (j >= ps.np) break;
+                    float t = plane_t(origin, dir, ps.pl_h[j]);
+                    if (t < h.t || (t == h.t && ps.pl_idx[j] < h.idx)) {
+                        h.t = t;
+                        h.idx = ps.pl_idx[j];
+                        h.g = make_float4(0.f, ps.pl_h[j], 0.f, -1.f);
+                    }
+                }
+                int best = -1;
+#pragma unroll 4
+                for (int c = 0; c < ncand; c++) {
+                    float t = sphere_t(origin, dir, cand_sph[c]);
+                    if (t <= h.t) {
+                        int id = cand_idx[c];
+                        if (t < h.t || id < h.idx) {  // (t, index) order: lowest original index wins ties
+                            h.t = t;
+                            h.idx = id;
+                            best = c;
+                        }
+                    }
+                }
+                if (best >= 0 && h.idx == cand_idx[best]) h.g = cand_sph[best];
+            }
+            __syncwarp();
+        }
+        const bool hit_now = alive && h.idx >= 0;
+        if (alive && !hit_now) {
+            if (sa.has_sky) tail = sky_sample(dir, sa.sky, sa.sky_w, sa.sky_h);
+            alive = false;
+        }
+        int cls = 0;
+        int64_t slot = 0;
+        unsigned mask[kWords + 1];
+        if (hit_now) {
+            float3 hit = origin + dir * h.t;
+            float3 normal = h.g.w >= 0.f ? normalize3(hit - f3(h.g.x, h.g.y, h.g.z)) : f3(0.f, 1.f, 0.f);
+            float3 l = normalize3(light - hit);
+            float dfs = fmaxf(dot3(normal, l), 0.f);
+            float3 hv = l - dir;
+            float hm2 = dot3(hv, hv);
+            float s = 0.f;
+            if (hm2 > 0.f) {
+                float dd = fmaxf(dot3(normal, hv) * rsqrtf(hm2), 0.f);
+                s = powf(dd, __ldg(sa.mat + 8 * h.idx + 4));
+            }
+            const float3 so = hit + normal * 1e-3f;  // shadow (and reflection) origin
+            const Cone cone = make_cone(so, light, sa.light_radius);
+            cls = classify_hit(ps, cone, so.y, light.y, mask);
+            slot = (int64_t)k * wa.n_pix + lp;
+            ridx[k] = h.idx;
+            rdfs[k] = dfs;
+            rs[k] = s;
+            rsc[k] = cls == 2 ? 0.f : 1.f;
+            if (cls == 1) {
+                wa.hit_p[slot] = make_float4(hit.x, hit.y, hit.z, __int_as_float(h.idx));
+                wa.hit_n[slot] = make_float4(normal.x, normal.y, normal.z, dfs);
+                npend++;
+            }
+            m = k + 1;
+            if (k == fa.bounces) {
+                exhausted = 1;
+                alive = false;
+            } else {
+                origin = so;
+                dir = dir - normal * (2.f * dot3(normal, dir));
+            }
+        }
+        // queue the undecided hits: one atomic per warp and bounce
+        const bool need = hit_now && cls == 1;
+        const unsigned nb = __ballot_sync(0xffffffffu, need);
+        if (nb) {
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(wa.count + 1, (unsigned)__popc(nb));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (need) {
+                const unsigned e = base + __popc(nb & lanemask_lt());
+                wa.queue2[e] = (int)slot;
+#pragma unroll
+                for (int w = 0; w <= kWords; w++) wa.mask2[(size_t)w * wa.mask2_stride + e] = mask[w];
+            }
+        }
+        if (wa.work) {
+            const unsigned nh = __popc(__ballot_sync(0xffffffffu, hit_now));
+            if (lane == 0 && nh) {
+                atomicAdd(wa.work + kWorkHits, (unsigned long long)nh);
+                atomicAdd(wa.work + kWorkCullTests, (unsigned long long)nh * (ps.ns + ps.np));
+            }
+        }
+    }
+    if (!valid) return;
+    if (npend == 0) {
+        const float3 c = unwind(m, exhausted, tail, sa, [&](int k) { return Record{ridx[k], rdfs[k], rs[k], rsc[k]}; });
+        store_pixel(fa, x, y, c);
+        if (fa.peer_out) __threadfence_system();
+    } else {
+        wa.pix[lp] = make_float4(tail.x, tail.y, tail.z, __int_as_float(m | (exhausted << 8)));
+        wa.pending[lp] = npend;
+        for (int k = 0; k < m; k++)
+            wa.rec[(int64_t)k * wa.n_pix + lp] = make_float4(__int_as_float(ridx[k]), rdfs[k], rs[k], rsc[k]);
+    }
+}
+
+// --- B ----------------------------------------------------------------------------
+// Sampling of one queued hit by a warp; returns the unblocked count (all lanes).
+template <int MAXS, bool SMEM_TAB>
+__device__ __forceinline__ int sample_hit(const ParamScene<MAXS> &ps, const ShadowFrame &f, const unsigned *hm,
+                                          int n, const float4 *gtab, int &nsph_out) {
+    constexpr int kWords = (MAXS + 31) / 32;
+    const int lane = threadIdx.x & 31;
+    const int rounds = (n + 31) / 32;
+    int nsph = 0;
+#pragma unroll
+    for (int w = 0; w < kWords; w++) nsph += __popc(hm[w]);
+    nsph_out = nsph;
+    auto table = [&](int i) -> float4 {
+        if constexpr (SMEM_TAB) {
+            extern __shared__ float4 smem_tab_f[];
+            return smem_tab_f[i];
+        } else {
+            return __ldg(gtab + i);
+        }
+    };
+    int unblocked = 0;
+    if (nsph == 1 && hm[kWords] == 0) {
+        // the common penumbra case: one sphere against every sample; full
+        // rounds of 32 samples without bounds checks, then the remainder
+        static_assert(kWaveMinSamples > 1, "the wavefront path assumes soft shadows");
+        int w = 0;
+        while (hm[w] == 0) w++;
+        const float4 g = ps.sph[w * 32 + __ffs(hm[w]) - 1];
+        const float3 L = f3(g.x - f.origin.x, g.y - f.origin.y, g.z - f.origin.z);
+        const float r2g = sphere_r2g(L, g.w);
+        auto sample = [&](int i) -> int {
+            float3 dir;
+            float limit;
+            shadow_ray_unguarded(f, table(i), dir, limit);
+            return sphere_margin_L(L, dir, r2g, limit) > 0.f ? 0 : 1;
+        };
+        const int full = n >> 5;
+#pragma unroll 2
+        for (int j = 0; j < full; j++) unblocked += sample(lane + 32 * j);
+        if (lane + 32 * full < n) unblocked += sample(lane + 32 * full);
+        return unblocked;
+    }
+    // rounds in groups of 64 (a bit per round); candidates kRegCand at a time
+    for (int g0 = 0; g0 < rounds; g0 += 64) {
+        const int g1 = min(rounds, g0 + 64);
+        unsigned long long blocked = 0;  // bit j - g0: sample lane + 32 j is blocked
+        int w_cur = 0;
+        unsigned m_cur = hm[0];
+        for (int done = 0; done < nsph || done == 0; done += kRegCand) {
+            float4 c[kRegCand];
+            int k = 0;
+#pragma unroll
+            for (int r = 0; r < kRegCand; r++) {
+                c[r] = make_float4(0.f, 0.f, 0.f, -INFINITY);
+                while (m_cur == 0 && w_cur + 1 < kWords) m_cur = hm[++w_cur];
+                if (m_cur != 0) {
+                    const float4 g = ps.sph[w_cur * 32 + __ffs(m_cur) - 1];
+                    m_cur &= m_cur - 1;
+                    const float3 L = f3(g.x - f.origin.x, g.y - f.origin.y, g.z - f.origin.z);
+                    c[r] = make_float4(L.x, L.y, L.z, sphere_r2g(L, g.w));
+                    k++;
+                }
+            }
+            const unsigned pm = done == 0 ? hm[kWords] : 0u;  // planes ride with the first chunk
+            for (int j = g0; j < g1; j++) {
+                const int i = lane + 32 * j;
+                float3 dir;
+                float limit;
+                shadow_ray_unguarded(f, table(i < n ? i : 0), dir, limit);
+                float mg = -INFINITY;
+#pragma unroll
+                for (int r = 0; r < kRegCand; r++)
+                    if (r < k) mg = fmaxf(mg, sphere_margin_L(f3(c[r].x, c[r].y, c[r].z), dir, c[r].w, limit));
+                for (unsigned b = pm; b; b &= b - 1)
+                    mg = fmaxf(mg, plane_margin(ps.pl_h[__ffs(b) - 1] - f.origin.y, dir.y, limit));
+                if (mg > 0.f) blocked |= 1ull << (j - g0);
+            }
+            if (nsph <= kRegCand) break;
+        }
+        for (int j = g0; j < g1; j++) unblocked += (lane + 32 * j < n && !((blocked >> (j - g0)) & 1ull)) ? 1 : 0;
+    }
+    return unblocked;
+}
+
+template <int MAXS, bool SMEM_TAB>
+__global__ void __launch_bounds__(kThreads)
+    fused_sample(const FrameArgs fa, const SceneArgs<float> sa, const WaveArgs wa, const ParamScene<MAXS> ps) {
+    constexpr int kWords = (MAXS + 31) / 32;
+    const int n = fa.samples;
+    const float4 *gtab = reinterpret_cast<const float4 *>(sa.table);
+    if constexpr (SMEM_TAB) {
+        extern __shared__ float4 smem_tab_k[];
+        for (int i = threadIdx.x; i < n; i += blockDim.x) smem_tab_k[i] = gtab[i];
+        __syncthreads();
+    }
+    const unsigned count = wa.count[1];
+    const int lane = threadIdx.x & 31;
+    const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned n_warps = (gridDim.x * blockDim.x) >> 5;
+    const float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
+    for (unsigned h = warp; h < count; h += n_warps) {
+        const int slot = __ldg(wa.queue2 + h);
+        unsigned hm[kWords + 1];
+#pragma unroll
+        for (int w = 0; w <= kWords; w++) hm[w] = __ldg(wa.mask2 + (size_t)w * wa.mask2_stride + h);
+        const float4 P = __ldg(wa.hit_p + slot);
+        const float4 N = __ldg(wa.hit_n + slot);
+        const ShadowFrame f = shadow_frame(f3(P.x, P.y, P.z), f3(N.x, N.y, N.z), lp, true);
+        int nsph = 0;
+        int unblocked = sample_hit<MAXS, SMEM_TAB>(ps, f, hm, n, gtab, nsph);
+        unblocked = __reduce_add_sync(0xffffffffu, unblocked);
+        if (lane != 0) continue;
+        reinterpret_cast<float *>(wa.rec + slot)[3] = (float)unblocked / (float)n;
+        if (wa.work) {
+            atomicAdd(wa.work + kWorkSampledHits, 1ull);
+            atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);
+            atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n * nsph);
+            atomicAdd(wa.work + kWorkPlaneTests, (unsigned long long)n * __popc(hm[kWords]));
+        }
+        // the pixel's last pending hit: unwind and pack it (release / acquire
+        // fences around the count pair with the other hits' writes)
+        const int64_t lpix = slot % wa.n_pix;
+        __threadfence();
+        if (atomicSub(wa.pending + lpix, 1) != 1) continue;
+        __threadfence();
+        const float4 px = __ldcg(wa.pix + lpix);
+        const int info = __float_as_int(px.w);
+        const float3 c = unwind(info & 0xff, (info >> 8) & 1, f3(px.x, px.y, px.z), sa, [&](int k) {
+            const float4 r = __ldcg(wa.rec + (int64_t)k * wa.n_pix + lpix);
+            return Record{__float_as_int(r.x), r.y, r.z, r.w};
+        });
+        const int ly = (int)(lpix / fa.width), x = (int)(lpix - (int64_t)ly * fa.width);
+        store_pixel(fa, x, map_row(ly, fa), c);
+        if (fa.peer_out) __threadfence_system();
+    }
+}
+
+template <int MAXS>
+cudaError_t launch(const FrameArgs &fa, const SceneArgs<float> &sa, const WaveArgs &wa, const ParamScene<MAXS> &ps,
+                   cudaStream_t st, cudaEvent_t *ev) {
+    dim3 grid((fa.width + kTileW - 1) / kTileW, (fa.local_rows + kTileH - 1) / kTileH);
+    fused_trace<MAXS><<<grid, kThreads, 0, st>>>(fa, sa, wa, ps);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (ev) {
+        cudaEventRecord(ev[1], st);
+        cudaEventRecord(ev[2], st);
+    }
+    const int n = fa.samples;
+    if (n <= kWaveSmemSamples) {
+        const size_t smem = sizeof(float4) * (size_t)n;
+        fused_sample<MAXS, true><<<resident_ctas(fused_sample<MAXS, true>, smem), kThreads, smem, st>>>(fa, sa, wa,
+                                                                                                         ps);
+    } else {
+        fused_sample<MAXS, false><<<resident_ctas(fused_sample<MAXS, false>, 0), kThreads, 0, st>>>(fa, sa, wa, ps);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+// The culled soft-shadow frame; false if the scene does not fit the
+// launch-parameter layout (the caller then takes the unculled wavefront).
+bool rt_fused_fits(const rt::SceneArgs<float> &sa) {
+    static thread_local ParamScene<kParamSpheres> probe;
+    ParamScene<8> p8;
+    return pack_params(sa, p8) || pack_params(sa, probe);
+}
+
+cudaError_t rt_launch_fused_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, const rt::WaveArgs &wa,
+                                cudaStream_t st, int *n_kernels, cudaEvent_t *ev) {
+    *n_kernels = 0;
+    cudaError_t e = cudaMemsetAsync(wa.count, 0, 4 * sizeof(unsigned), st);
+    if (e != cudaSuccess) return e;
+    if (ev) cudaEventRecord(ev[0], st);
+    ParamScene<8> p8;
+    thread_local ParamScene<kParamSpheres> p256;
+    if (pack_params(sa, p8))
+        e = launch(fa, sa, wa, p8, st, ev);
+    else if (pack_params(sa, p256))
+        e = launch(fa, sa, wa, p256, st, ev);
+    else
+        return cudaErrorInvalidValue;
+    if (e != cudaSuccess) return e;
+    *n_kernels = 2;
+    if (ev) {
+        cudaEventRecord(ev[3], st);
+        cudaEventRecord(ev[4], st);
+    }
+    return cudaSuccess;
+}

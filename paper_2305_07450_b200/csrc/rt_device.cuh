@@ -71,6 +71,8 @@ struct WaveArgs {
     unsigned *mask2;      // their candidate-body masks, word-major [words][mask2_stride]
     int64_t mask2_stride;
     float4 *pix;       // {tail rgb, records | exhausted << 8}
+    float4 *rec;       // culled path: {body, Lambert, Blinn, coefficient} per hit of a pending pixel
+    int *pending;      // culled path: undecided hits left per pixel
     int64_t n_pix;     // pixels of this partition (local_rows * width)
     unsigned long long *work;  // optional executed-work tallies of the culled path (kWork*), or null
     int cull;          // exact per-hit occluder culling in the shadow kernel
@@ -137,6 +139,9 @@ cudaError_t rt_launch_render_f64(const rt::FrameArgs &fa, const rt::SceneArgs<do
 cudaError_t rt_launch_wave_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, const rt::WaveArgs &wa,
                                cudaStream_t st, int *n_kernels, cudaEvent_t *phase_events /* 5 or null */);
 int rt_wave_lanes(int samples);
+bool rt_fused_fits(const rt::SceneArgs<float> &sa);
+cudaError_t rt_launch_fused_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, const rt::WaveArgs &wa,
+                                cudaStream_t st, int *n_kernels, cudaEvent_t *phase_events /* 5 or null */);
 cudaError_t rt_launch_trace_f32(const double *d_orig, const double *d_dir, int64_t n, float *d_out,
                                 const rt::SceneArgs<float> &sa, int samples, int bounces, cudaStream_t st);
 cudaError_t rt_launch_trace_f64(const double *d_orig, const double *d_dir, int64_t n, double *d_out,

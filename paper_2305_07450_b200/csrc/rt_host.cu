@@ -87,7 +87,7 @@ struct Dev {
     cudaEvent_t band_ev[4] = {nullptr, nullptr, nullptr, nullptr};
     bool ph_valid = false;
     DBuf frame, rad, rays_in, rays_out, sky_raw, sky, counters;
-    DBuf w_p, w_n, w_s, w_sc, w_queue, w_queue2, w_mask2, w_count, w_pix, w_work;  // wavefront queues (FP32 soft shadows)
+    DBuf w_p, w_n, w_s, w_sc, w_queue, w_queue2, w_mask2, w_count, w_pix, w_work, w_rec, w_pending;  // wavefront queues (FP32 soft shadows)
     unsigned counter_slot = 0;
     uint64_t sky_version = ~0ull;
     DevScene<float> s32;
@@ -410,16 +410,25 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
     if (precision == RT_PREC_FP64) {
         e = rt_launch_render_f64(fa, scene_args(d, d.s64, ctx->scene), st);
     } else if (fa.samples >= rt::kWaveMinSamples && ctx->wave) {
-        rt::WaveArgs wa;
+        const rt::SceneArgs<float> sa = scene_args(d, d.s32, ctx->scene);
+        const bool fused = ctx->cull && rt_fused_fits(sa);
+        rt::WaveArgs wa = {};
         wa.n_pix = (int64_t)fa.local_rows * fa.width;
         size_t slots = (size_t)wa.n_pix * (fa.bounces + 1);
         if ((rc = d.w_p.ensure(sizeof(float4) * slots)) || (rc = d.w_n.ensure(sizeof(float4) * slots)) ||
-            (rc = d.w_s.ensure(sizeof(float) * slots)) || (rc = d.w_sc.ensure(sizeof(float) * slots)) ||
-            (rc = d.w_queue.ensure(sizeof(int) * slots)) || (rc = d.w_count.ensure(4 * sizeof(unsigned))) ||
-            (rc = d.w_queue2.ensure(sizeof(int) * slots)) ||
-            (rc = d.w_mask2.ensure(sizeof(unsigned) * slots * (ctx->scene.n <= 8 ? 2 : rt::kMaskWords + 1))) ||
-            (rc = d.w_pix.ensure(sizeof(float4) * (size_t)wa.n_pix)))
+            (rc = d.w_count.ensure(4 * sizeof(unsigned))) || (rc = d.w_pix.ensure(sizeof(float4) * (size_t)wa.n_pix)))
             return rc;
+        if (fused) {
+            if ((rc = d.w_queue2.ensure(sizeof(int) * slots)) ||
+                (rc = d.w_mask2.ensure(sizeof(unsigned) * slots * (ctx->scene.n <= 8 ? 2 : rt::kMaskWords + 1))) ||
+                (rc = d.w_rec.ensure(sizeof(float4) * slots)) ||
+                (rc = d.w_pending.ensure(sizeof(int) * (size_t)wa.n_pix)))
+                return rc;
+        } else {
+            if ((rc = d.w_s.ensure(sizeof(float) * slots)) || (rc = d.w_sc.ensure(sizeof(float) * slots)) ||
+                (rc = d.w_queue.ensure(sizeof(int) * slots)))
+                return rc;
+        }
         wa.hit_p = (float4 *)d.w_p.p;
         wa.hit_n = (float4 *)d.w_n.p;
         wa.hit_s = (float *)d.w_s.p;
@@ -430,7 +439,9 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         wa.mask2 = (unsigned *)d.w_mask2.p;
         wa.mask2_stride = (int64_t)slots;
         wa.pix = (float4 *)d.w_pix.p;
-        wa.cull = ctx->cull;
+        wa.rec = (float4 *)d.w_rec.p;
+        wa.pending = (int *)d.w_pending.p;
+        wa.cull = fused;
         wa.work = nullptr;
         if (ctx->count_work) {
             bool fresh = d.w_work.p == nullptr;
@@ -441,7 +452,7 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         int nk = 0;
         if (!d.ph[0])
             for (auto &ev : d.ph) RT_CK(cudaEventCreate(&ev));
-        e = rt_launch_wave_f32(fa, scene_args(d, d.s32, ctx->scene), wa, st, &nk, d.ph);
+        e = fused ? rt_launch_fused_f32(fa, sa, wa, st, &nk, d.ph) : rt_launch_wave_f32(fa, sa, wa, st, &nk, d.ph);
         d.ph_valid = true;
         ctx->launches += nk - 1;  // the common increment below counts one
     } else {
@@ -524,7 +535,7 @@ int rt_ctx_destroy(rt_ctx *ctx) {
         cudaSetDevice(d.id);
         if (d.st) cudaStreamSynchronize(d.st);
         for (DBuf *b : {&d.w_p, &d.w_n, &d.w_s, &d.w_sc, &d.w_queue, &d.w_queue2, &d.w_mask2, &d.w_count, &d.w_pix,
-                        &d.w_work})
+                        &d.w_work, &d.w_rec, &d.w_pending})
             b->release();
         for (DBuf *b : {&d.frame, &d.rad, &d.rays_in, &d.rays_out, &d.sky_raw, &d.sky, &d.counters, &d.s32.geo, &d.s32.mat,
                         &d.s32.table, &d.s64.geo, &d.s64.mat, &d.s64.table})

@@ -10,10 +10,10 @@
 //              hit is queued with its candidate-body mask.  A pixel whose hits
 //              are all decided is unwound (renderer.py:185-224) and packed
 //              (renderer.py:45-50) right here; otherwise its records are parked
-//              in HBM with a count of pending hits.
+//              in HBM and the pixel is queued for C.
 //   B  sample  one warp per queued hit, 32 disc samples abreast against that
-//              hit's candidate bodies (held in registers); the warp that
-//              settles a pixel's last pending hit unwinds and packs it.
+//              hit's candidate bodies (held in registers);
+//   C  finish  one thread per parked pixel: unwind and pack.
 //
 // Arithmetic per shadow test is the unculled kernels' (render_wave_f32.cu,
 // render_f32.cu) operation for operation: the frames are bit-identical.
@@ -22,7 +22,7 @@
 //   hit_p float4 {p, body}, hit_n float4 {n, Lambert}   queued (undecided) hits only
 //   rec   float4 {body, Lambert, Blinn, coefficient}    every hit of a pending pixel
 //   pix   float4 {tail rgb, records | exhausted << 8}   pending pixels
-//   pending int per pixel; queue2 slots + candidate masks (word-major)
+//   queue2 slots + candidate masks (word-major), queue3 parked pixels
 #include "rt_wave.cuh"
 
 namespace {
@@ -247,14 +247,21 @@ __global__ void __launch_bounds__(kThreads)
             }
         }
     }
+    const bool park = valid && npend > 0;
+    const unsigned pb = __ballot_sync(0xffffffffu, park);
+    if (pb) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(wa.count + 2, (unsigned)__popc(pb));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (park) wa.queue3[base + __popc(pb & lanemask_lt())] = (int)lp;
+    }
     if (!valid) return;
-    if (npend == 0) {
+    if (!park) {
         const float3 c = unwind(m, exhausted, tail, sa, [&](int k) { return Record{ridx[k], rdfs[k], rs[k], rsc[k]}; });
         store_pixel(fa, x, y, c);
         if (fa.peer_out) __threadfence_system();
     } else {
         wa.pix[lp] = make_float4(tail.x, tail.y, tail.z, __int_as_float(m | (exhausted << 8)));
-        wa.pending[lp] = npend;
         for (int k = 0; k < m; k++)
             wa.rec[(int64_t)k * wa.n_pix + lp] = make_float4(__int_as_float(ridx[k]), rdfs[k], rs[k], rsc[k]);
     }
@@ -379,19 +386,22 @@ __global__ void __launch_bounds__(kThreads)
             atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n * nsph);
             atomicAdd(wa.work + kWorkPlaneTests, (unsigned long long)n * __popc(hm[kWords]));
         }
-        // the pixel's last pending hit: unwind and pack it (release / acquire
-        // fences around the count pair with the other hits' writes)
-        const int64_t lpix = slot % wa.n_pix;
-        __threadfence();
-        if (atomicSub(wa.pending + lpix, 1) != 1) continue;
-        __threadfence();
-        const float4 px = __ldcg(wa.pix + lpix);
+    }
+}
+
+// --- C: the pixels that had undecided hits --------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+    fused_finish(const FrameArgs fa, const SceneArgs<float> sa, const WaveArgs wa) {
+    const unsigned count = wa.count[2];
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+        const int lpix = __ldg(wa.queue3 + i);
+        const float4 px = wa.pix[lpix];
         const int info = __float_as_int(px.w);
         const float3 c = unwind(info & 0xff, (info >> 8) & 1, f3(px.x, px.y, px.z), sa, [&](int k) {
-            const float4 r = __ldcg(wa.rec + (int64_t)k * wa.n_pix + lpix);
+            const float4 r = wa.rec[(int64_t)k * wa.n_pix + lpix];
             return Record{__float_as_int(r.x), r.y, r.z, r.w};
         });
-        const int ly = (int)(lpix / fa.width), x = (int)(lpix - (int64_t)ly * fa.width);
+        const int ly = lpix / fa.width, x = lpix - ly * fa.width;
         store_pixel(fa, x, map_row(ly, fa), c);
         if (fa.peer_out) __threadfence_system();
     }
@@ -444,10 +454,10 @@ cudaError_t rt_launch_fused_f32(const rt::FrameArgs &fa, const rt::SceneArgs<flo
     else
         return cudaErrorInvalidValue;
     if (e != cudaSuccess) return e;
-    *n_kernels = 2;
-    if (ev) {
-        cudaEventRecord(ev[3], st);
-        cudaEventRecord(ev[4], st);
-    }
+    if (ev) cudaEventRecord(ev[3], st);
+    fused_finish<<<resident_ctas(fused_finish, 0), kThreads, 0, st>>>(fa, sa, wa);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    *n_kernels = 3;
+    if (ev) cudaEventRecord(ev[4], st);
     return cudaSuccess;
 }

@@ -66,13 +66,13 @@ struct WaveArgs {
     float *hit_s;      // Blinn factor
     float *hit_sc;     // shadow coefficient
     int *queue;        // slots holding a hit
-    unsigned *count;   // [0] queue length, [1] queue2 length
+    unsigned *count;   // [0] queue length, [1] queue2 length, [2] queue3 length
     int *queue2;          // culled path: undecided hits (slots)
     unsigned *mask2;      // their candidate-body masks, word-major [words][mask2_stride]
     int64_t mask2_stride;
     float4 *pix;       // {tail rgb, records | exhausted << 8}
     float4 *rec;       // culled path: {body, Lambert, Blinn, coefficient} per hit of a pending pixel
-    int *pending;      // culled path: undecided hits left per pixel
+    int *queue3;       // culled path: pixels with undecided hits (finished after sampling)
     int64_t n_pix;     // pixels of this partition (local_rows * width)
     unsigned long long *work;  // optional executed-work tallies of the culled path (kWork*), or null
     int cull;          // exact per-hit occluder culling in the shadow kernel

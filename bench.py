@@ -313,7 +313,12 @@ def run_ours(args):
         """Frames/s, per-phase device times and executed work of config c."""
         r = time_config(c, warmup, steps, sample_clocks)
         fps_c = len(r["ms"]) / (r["total_ms"] / 1e3)
-        phases = ctx.phase_ms()  # last timed frame
+        # one more (untimed) frame with phase events and work tallies on
+        ctx.set_option("phases", 1)
+        render_cfg(c)
+        torch.cuda.synchronize()
+        phases = ctx.phase_ms()
+        ctx.set_option("phases", 0)
         ctx.set_option("count_work", 1)
         ctx.work_counts(reset=True)
         render_cfg(c)

@@ -132,7 +132,10 @@ int rt_host_unregister(rt_ctx *ctx, void *ptr);
  *   "count_work"  tally the executed work of the culled pass (rt_work_counts);
  *   "bands"       rt_render_v1 on one device renders this many contiguous row
  *                 bands (1-4) and copies each to the host while the next
- *                 renders; 0 (default) = 4 for frames of >= 16 MB, else 1. */
+ *                 renders; 0 (default) = 4 for frames of >= 16 MB, else 1;
+ *   "phases"      record CUDA events between the wavefront kernels so
+ *                 rt_phase_ms can report per-phase device times (off by
+ *                 default: each event record costs the GPU ~2-3 us). */
 int rt_set_option(rt_ctx *ctx, const char *name, int32_t value);
 /* Executed-work tallies since the last reset: hits, per-hit cull tests, hits
  * that sampled, shadow rays traced, sphere tests, plane tests. */
@@ -141,7 +144,8 @@ int rt_work_counts(rt_ctx *ctx, uint64_t *out, int32_t n, int32_t reset);
 /* Device time (CUDA events) of the render kernels of the last rt_render_v1 /
  * rt_trace_rays_v1 call on ctx's first device, in milliseconds. */
 int rt_last_kernel_ms(rt_ctx *ctx, float *ms);
-/* Device time of the last wavefront frame's phases on ctx's first device, ms:
+/* Device time of the last wavefront frame's phases on ctx's first device, ms
+ * (needs option "phases"):
  * out[0] trace, out[1] classify (culled path), out[2] shadow / sample,
  * out[3] shade.  Zeros when no wavefront frame ran. */
 int rt_phase_ms(rt_ctx *ctx, float *out, int32_t n);

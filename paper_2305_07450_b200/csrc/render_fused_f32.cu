@@ -416,7 +416,7 @@ cudaError_t launch(const FrameArgs &fa, const SceneArgs<float> &sa, const WaveAr
     if (e != cudaSuccess) return e;
     if (ev) {
         cudaEventRecord(ev[1], st);
-        cudaEventRecord(ev[2], st);
+        cudaEventRecord(ev[2], st);  // no separate classify pass: a zero-length phase
     }
     const int n = fa.samples;
     if (n <= kWaveSmemSamples) {

@@ -138,6 +138,7 @@ struct rt_ctx {
     bool cull = true;   // exact per-hit occluder culling in the wavefront shadow pass ($B200RT_CULL=0: off)
     bool count_work = false;  // tally the culled path's executed work (rt_work_counts)
     int bands = 0;            // single-device row bands for copy overlap (0: by frame size)
+    bool phases = false;      // record per-phase events in wavefront frames (rt_phase_ms)
     std::mutex mu;
     HostScene scene;
     float last_ms = 0.f;
@@ -452,8 +453,9 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         int nk = 0;
         if (!d.ph[0])
             for (auto &ev : d.ph) RT_CK(cudaEventCreate(&ev));
-        e = fused ? rt_launch_fused_f32(fa, sa, wa, st, &nk, d.ph) : rt_launch_wave_f32(fa, sa, wa, st, &nk, d.ph);
-        d.ph_valid = true;
+        cudaEvent_t *ph = ctx->phases ? d.ph : nullptr;  // event records cost ~2-3 us of GPU time each
+        e = fused ? rt_launch_fused_f32(fa, sa, wa, st, &nk, ph) : rt_launch_wave_f32(fa, sa, wa, st, &nk, ph);
+        d.ph_valid = ctx->phases;
         ctx->launches += nk - 1;  // the common increment below counts one
     } else {
         e = rt_launch_render_f32(fa, scene_args(d, d.s32, ctx->scene), st);
@@ -834,6 +836,7 @@ int rt_set_option(rt_ctx *ctx, const char *name, int32_t value) {
     else if (n == "cull") ctx->cull = value != 0;
     else if (n == "count_work") ctx->count_work = value != 0;
     else if (n == "bands") ctx->bands = std::max(0, std::min((int)value, 4));
+    else if (n == "phases") ctx->phases = value != 0;
     else return fail(RT_ERR_INVALID, "unknown option " + n);
     return RT_OK;
 }

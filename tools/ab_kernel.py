@@ -24,7 +24,7 @@ def main():
     ap.add_argument("--bands", type=int, default=1, help="row bands of rt_render_v1 (0 = by frame size)")
     a = ap.parse_args()
     tag = os.path.basename(_native.LIB_PATH)
-    _native.set_options(bands=a.bands)
+    _native.set_options(bands=a.bands, phases=1)
     if a.mode:
         _native.set_options(**{"cull": dict(wave=1, cull=1), "wave": dict(wave=1, cull=0),
                                "mega": dict(wave=0, cull=0)}[a.mode])

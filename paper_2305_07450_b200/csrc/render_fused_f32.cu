@@ -362,6 +362,9 @@ __global__ void __launch_bounds__(kThreads)
         for (int i = threadIdx.x; i < n; i += blockDim.x) smem_tab_k[i] = gtab[i];
         __syncthreads();
     }
+    // programmatic dependent launch: everything above (the table staging)
+    // overlaps the trace kernel's tail; the queue is read only after it
+    cudaGridDependencySynchronize();
     const unsigned count = wa.count[1];
     const int lane = threadIdx.x & 31;
     const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -392,6 +395,7 @@ __global__ void __launch_bounds__(kThreads)
 // --- C: the pixels that had undecided hits --------------------------------------------
 __global__ void __launch_bounds__(kThreads)
     fused_finish(const FrameArgs fa, const SceneArgs<float> sa, const WaveArgs wa) {
+    cudaGridDependencySynchronize();
     const unsigned count = wa.count[2];
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
         const int lpix = __ldg(wa.queue3 + i);
@@ -405,6 +409,23 @@ __global__ void __launch_bounds__(kThreads)
         store_pixel(fa, x, map_row(ly, fa), c);
         if (fa.peer_out) __threadfence_system();
     }
+}
+
+// Launch with programmatic stream serialisation: the kernel may start while
+// the previous one drains and waits for it in cudaGridDependencySynchronize.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), int ctas, size_t smem, cudaStream_t st, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 template <int MAXS>
@@ -421,12 +442,12 @@ cudaError_t launch(const FrameArgs &fa, const SceneArgs<float> &sa, const WaveAr
     const int n = fa.samples;
     if (n <= kWaveSmemSamples) {
         const size_t smem = sizeof(float4) * (size_t)n;
-        fused_sample<MAXS, true><<<resident_ctas(fused_sample<MAXS, true>, smem), kThreads, smem, st>>>(fa, sa, wa,
-                                                                                                         ps);
+        e = launch_pdl(fused_sample<MAXS, true>, resident_ctas(fused_sample<MAXS, true>, smem), smem, st, fa, sa, wa,
+                       ps);
     } else {
-        fused_sample<MAXS, false><<<resident_ctas(fused_sample<MAXS, false>, 0), kThreads, 0, st>>>(fa, sa, wa, ps);
+        e = launch_pdl(fused_sample<MAXS, false>, resident_ctas(fused_sample<MAXS, false>, 0), 0, st, fa, sa, wa, ps);
     }
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace
@@ -455,8 +476,7 @@ cudaError_t rt_launch_fused_f32(const rt::FrameArgs &fa, const rt::SceneArgs<flo
         return cudaErrorInvalidValue;
     if (e != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[3], st);
-    fused_finish<<<resident_ctas(fused_finish, 0), kThreads, 0, st>>>(fa, sa, wa);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = launch_pdl(fused_finish, resident_ctas(fused_finish, 0), 0, st, fa, sa, wa)) != cudaSuccess) return e;
     *n_kernels = 3;
     if (ev) cudaEventRecord(ev[4], st);
     return cudaSuccess;

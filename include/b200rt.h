@@ -135,7 +135,9 @@ int rt_host_unregister(rt_ctx *ctx, void *ptr);
  *                 renders; 0 (default) = 4 for frames of >= 16 MB, else 1;
  *   "phases"      record CUDA events between the wavefront kernels so
  *                 rt_phase_ms can report per-phase device times (off by
- *                 default: each event record costs the GPU ~2-3 us). */
+ *                 default: each event record costs the GPU ~2-3 us);
+ *   "rgba"        write pixels as bytes R,G,B,A (the frame server's wire
+ *                 format, server.py:56-64) instead of 0xAARRGGBB. */
 int rt_set_option(rt_ctx *ctx, const char *name, int32_t value);
 /* Executed-work tallies since the last reset: hits, per-hit cull tests, hits
  * that sampled, shadow rays traced, sphere tests, plane tests. */

@@ -121,7 +121,7 @@ __device__ __forceinline__ void shade_pixel(const Geo &geo, const FrameArgs &fa,
     float3 dir = primary_direction(x, y, fa);
     float3 c = trace<BMAX>(geo, f3((float)fa.cam[0], (float)fa.cam[1], (float)fa.cam[2]), dir, sa, fa.samples,
                            fa.bounces);
-    fa.out[(int64_t)y * fa.out_pitch + x] = pack_color(c.x, c.y, c.z);
+    fa.out[(int64_t)y * fa.out_pitch + x] = pack_color(c.x, c.y, c.z, fa.rgba);
     if (fa.radiance) {
         float *r = (float *)fa.radiance + 3 * ((int64_t)y * fa.width + x);
         r[0] = c.x;

@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kThreads) render_f64_kernel(const FrameArgs fa
     if (y >= fa.row_end) return;
     d3 dir = primary_direction(x, y, fa);
     d3 c = trace<BMAX>(mk(fa.cam[0], fa.cam[1], fa.cam[2]), dir, geo, sa, fa.samples, fa.bounces);
-    fa.out[(int64_t)y * fa.out_pitch + x] = pack_color(c.x, c.y, c.z);
+    fa.out[(int64_t)y * fa.out_pitch + x] = pack_color(c.x, c.y, c.z, fa.rgba);
     if (fa.radiance) {
         double *r = (double *)fa.radiance + 3 * ((int64_t)y * fa.width + x);
         r[0] = c.x;

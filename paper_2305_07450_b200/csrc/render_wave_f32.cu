@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(kThreads) wave_shade(const FrameArgs fa, const
         col = f3(clamp01(br * lum + sa.lc[0] * sp), clamp01(bg * lum + sa.lc[1] * sp),
                  clamp01(bb * lum + sa.lc[2] * sp));
     }
-    fa.out[(int64_t)y * fa.out_pitch + x] = pack_color(col.x, col.y, col.z);
+    fa.out[(int64_t)y * fa.out_pitch + x] = pack_color(col.x, col.y, col.z, fa.rgba);
     if (fa.radiance) {
         float *r = (float *)fa.radiance + 3 * ((int64_t)y * fa.width + x);
         r[0] = col.x;

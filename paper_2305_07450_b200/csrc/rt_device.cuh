@@ -42,6 +42,7 @@ struct FrameArgs {
     unsigned int *work_counter;  // zeroed before the launch: persistent warps take 8x4 patches from it
     int sub_part, sub_parts;     // within a band: rows interleaved in 8-row blocks (sub_parts = 1: all)
     int row_end;                 // rows >= row_end are skipped (end of the band / frame)
+    int rgba;                    // pixel byte order: 0 B,G,R,A (0xAARRGGBB), 1 R,G,B,A
 };
 
 template <typename R>
@@ -121,13 +122,15 @@ __device__ __forceinline__ void thread_pixel(int &x, int &ly) {
     ly = blockIdx.y * kTileH + (warp >> 1) * 4 + (lane >> 3);
 }
 
-// renderer.py:45-50
+// renderer.py:45-50.  rgba = 0: 0xAARRGGBB (the reference's Framebuffer,
+// bytes B,G,R,A); rgba = 1: bytes R,G,B,A — the frame server's wire format
+// (server.py:56-64), so a frame can be streamed without a host-side repack.
 template <typename R>
-__device__ __forceinline__ uint32_t pack_color(R r, R g, R b) {
+__device__ __forceinline__ uint32_t pack_color(R r, R g, R b, int rgba) {
     uint32_t ri = (uint32_t)(int)(r * R(255.0) + R(0.5));
     uint32_t gi = (uint32_t)(int)(g * R(255.0) + R(0.5));
     uint32_t bi = (uint32_t)(int)(b * R(255.0) + R(0.5));
-    return 0xFF000000u | (ri << 16) | (gi << 8) | bi;
+    return rgba ? 0xFF000000u | (bi << 16) | (gi << 8) | ri : 0xFF000000u | (ri << 16) | (gi << 8) | bi;
 }
 
 }  // namespace rt

@@ -139,6 +139,7 @@ struct rt_ctx {
     bool count_work = false;  // tally the culled path's executed work (rt_work_counts)
     int bands = 0;            // single-device row bands for copy overlap (0: by frame size)
     bool phases = false;      // record per-phase events in wavefront frames (rt_phase_ms)
+    int rgba = 0;             // pixel byte order of the frames written (0 B,G,R,A / 1 R,G,B,A)
     std::mutex mu;
     HostScene scene;
     float last_ms = 0.f;
@@ -397,11 +398,13 @@ rt::FrameArgs frame_args(uint32_t *out, int64_t pitch, void *rad, int w, int h, 
     fa.sub_part = 0;
     fa.sub_parts = 1;
     fa.row_end = h;
+    fa.rgba = 0;
     return fa;
 }
 
 int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStream_t st) {
     cudaError_t e;
+    fa.rgba = ctx->rgba;
     if (fa.local_rows == 0) return RT_OK;
     int rc = d.counters.ensure(sizeof(unsigned) * rt::kCounterRing);
     if (rc) return rc;
@@ -837,6 +840,7 @@ int rt_set_option(rt_ctx *ctx, const char *name, int32_t value) {
     else if (n == "count_work") ctx->count_work = value != 0;
     else if (n == "bands") ctx->bands = std::max(0, std::min((int)value, 4));
     else if (n == "phases") ctx->phases = value != 0;
+    else if (n == "rgba") ctx->rgba = value != 0;
     else return fail(RT_ERR_INVALID, "unknown option " + n);
     return RT_OK;
 }

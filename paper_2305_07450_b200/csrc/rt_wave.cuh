@@ -190,7 +190,7 @@ __device__ __forceinline__ float3 unwind(int m, bool exhausted, float3 tail, con
 }
 
 __device__ __forceinline__ void store_pixel(const FrameArgs &fa, int x, int y, float3 c) {
-    fa.out[(int64_t)y * fa.out_pitch + x] = pack_color(c.x, c.y, c.z);
+    fa.out[(int64_t)y * fa.out_pitch + x] = pack_color(c.x, c.y, c.z, fa.rgba);
     if (fa.radiance) {
         float *r = (float *)fa.radiance + 3 * ((int64_t)y * fa.width + x);
         r[0] = c.x;

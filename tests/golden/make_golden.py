@@ -203,6 +203,13 @@ def main():
     add("c3like_192x108_s200_b3_sky", build_benchmark_scene(), BENCH_CAMERA, 192, 108, 200, 3,
         sky="grad:2048:1024", radiance=True)
 
+    # --- the frame server's wire format (server.py:56-64) of the golden frame ----
+    from raytracer.server import encode_frame as ref_encode_frame
+
+    fb = Framebuffer.create(128, 72)
+    fb.pixels[:] = arrays["bench_128x72_s200_b3/pixels"]
+    arrays["encode/bench_128x72_s200_b3_id7"] = np.frombuffer(ref_encode_frame(7, fb), dtype=np.uint8).copy()
+
     # --- per-ray fixtures: iterative (reference) + recursive oracle -------------
     rng = np.random.default_rng(303)
     ray_cases = []

@@ -1,0 +1,47 @@
+"""The frame server's wire format (server.py:56-74): the host restatement
+matches the reference's encode_frame bytes; the GPU renders the same message
+directly (R,G,B,A packed by the kernels)."""
+
+import numpy as np
+import pytest
+
+import golden_cases as G
+import paper_2305_07450_b200 as rt
+from paper_2305_07450_b200 import stream
+
+
+def _golden_fb():
+    fb = rt.Framebuffer.create(128, 72)
+    fb.pixels[:] = G.frame_pixels("bench_128x72_s200_b3")
+    return fb
+
+
+def test_encode_frame_matches_reference_bytes():
+    want = G._frames()["encode/bench_128x72_s200_b3_id7"].tobytes()
+    assert stream.encode_frame(7, _golden_fb()) == want
+
+
+def test_decode_frame_header():
+    msg = stream.encode_frame(0x1_0000_0005, _golden_fb())
+    assert stream.decode_frame_header(msg) == (5, 128, 72, stream.FORMAT_RGBA8)
+    with pytest.raises(ValueError):
+        stream.decode_frame_header(b"\0" * 16)
+    with pytest.raises(ValueError):
+        stream.decode_frame_header(b"RAYF")
+
+
+@pytest.mark.gpu
+def test_frame_encoder_renders_the_wire_message():
+    scene, cam = rt.build_benchmark_scene(), rt.benchmark_camera()
+    enc = stream.FrameEncoder()
+    try:
+        msg = enc.render(scene, cam, rt.RenderParams(200, 3, 128, 72), 7, precision="fp64")
+        assert bytes(msg) == G._frames()["encode/bench_128x72_s200_b3_id7"].tobytes()
+        params = rt.RenderParams(200, 3, 1280, 720)
+        fb = rt.Framebuffer.create(1280, 720)
+        rt.render_frame(scene, cam, params, fb)
+        for workers in (None, 3):
+            msg = enc.render(scene, cam, params, 42, workers=workers)
+            assert bytes(msg) == stream.encode_frame(42, fb)
+    finally:
+        enc.close()

@@ -310,3 +310,20 @@ def test_clustered_scene_modes_agree():
     rt.render_frame(s, cam, params, fb64, precision="fp64")
     for mode, px in frames.items():
         parity.assert_byte_gate(px, fb64.pixels, f"clustered [{mode}]")
+
+
+def test_moving_bodies_between_frames():
+    """The physics step moves spheres between frames (physics.py:49-72); the
+    scene cache must upload the change (the paper's per-frame streamIn)."""
+    scene, cam = rt.build_benchmark_scene(), rt.benchmark_camera()
+    params = rt.RenderParams(16, 2, 64, 36)
+    for step in range(3):
+        fb = rt.Framebuffer.create(64, 36)
+        rt.render_frame(scene, cam, params, fb, precision="fp64")
+        ps = rt.pack_scene(scene)
+        want = oracle.render(vars(ps), cam.position, cam.yaw, cam.pitch, cam.fov, 64, 36, 16, 2)
+        np.testing.assert_array_equal(fb.pixels, want)
+        for i in (3, 4):  # BENCHMARK_DYNAMIC_SPHERES (sceneio.py:311)
+            b = scene.bodies[i]
+            b.position = (b.position[0] + 0.15, b.position[1] + 0.05 * (step + 1), b.position[2] - 0.1)
+        scene.light.position = (scene.light.position[0] + 0.2, scene.light.position[1], scene.light.position[2])

@@ -19,10 +19,11 @@
 // render_f32.cu) operation for operation: the frames are bit-identical.
 //
 // HBM, slot = bounce * n_pix + local pixel:
-//   hit_p float4 {p, body}, hit_n float4 {n, Lambert}   queued (undecided) hits only
+//   hit_p float4 {p, record slot}, hit_n float4 {n, 0}  the queue of undecided hits
+//                                                     (compact: entry = queue position)
 //   rec   float4 {body, Lambert, Blinn, coefficient}    every hit of a pending pixel
 //   pix   float4 {tail rgb, records | exhausted << 8}   pending pixels
-//   queue2 slots + candidate masks (word-major), queue3 parked pixels
+//   candidate masks of the queued hits (word-major), queue3 parked pixels
 #include "rt_wave.cuh"
 
 namespace {
@@ -191,6 +192,7 @@ __global__ void __launch_bounds__(kThreads)
         int cls = 0;
         int64_t slot = 0;
         unsigned mask[kWords + 1];
+        float4 qp, qn;  // a queued hit's point (+ record slot) and normal
         if (hit_now) {
             float3 hit = origin + dir * h.t;
             float3 normal = h.g.w >= 0.f ? normalize3(hit - f3(h.g.x, h.g.y, h.g.z)) : f3(0.f, 1.f, 0.f);
@@ -212,8 +214,8 @@ __global__ void __launch_bounds__(kThreads)
             rs[k] = s;
             rsc[k] = cls == 2 ? 0.f : 1.f;
             if (cls == 1) {
-                wa.hit_p[slot] = make_float4(hit.x, hit.y, hit.z, __int_as_float(h.idx));
-                wa.hit_n[slot] = make_float4(normal.x, normal.y, normal.z, dfs);
+                qp = make_float4(hit.x, hit.y, hit.z, __int_as_float((int)slot));
+                qn = make_float4(normal.x, normal.y, normal.z, 0.f);
                 npend++;
             }
             m = k + 1;
@@ -233,8 +235,10 @@ __global__ void __launch_bounds__(kThreads)
             if (lane == 0) base = atomicAdd(wa.count + 1, (unsigned)__popc(nb));
             base = __shfl_sync(0xffffffffu, base, 0);
             if (need) {
+                // compact queue entry: everything the sampler needs, no indirection
                 const unsigned e = base + __popc(nb & lanemask_lt());
-                wa.queue2[e] = (int)slot;
+                wa.hit_p[e] = qp;
+                wa.hit_n[e] = qn;
 #pragma unroll
                 for (int w = 0; w <= kWords; w++) wa.mask2[(size_t)w * wa.mask2_stride + e] = mask[w];
             }
@@ -370,16 +374,26 @@ __global__ void __launch_bounds__(kThreads)
     const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned n_warps = (gridDim.x * blockDim.x) >> 5;
     const float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
-    for (unsigned h = warp; h < count; h += n_warps) {
-        const int slot = __ldg(wa.queue2 + h);
-        unsigned hm[kWords + 1];
+    // the next hit's queue entry is loaded while the current one samples
+    float4 P, N;
+    unsigned hm[kWords + 1];
+    auto fetch = [&](unsigned h) {
+        P = __ldg(wa.hit_p + h);
+        N = __ldg(wa.hit_n + h);
 #pragma unroll
         for (int w = 0; w <= kWords; w++) hm[w] = __ldg(wa.mask2 + (size_t)w * wa.mask2_stride + h);
-        const float4 P = __ldg(wa.hit_p + slot);
-        const float4 N = __ldg(wa.hit_n + slot);
-        const ShadowFrame f = shadow_frame(f3(P.x, P.y, P.z), f3(N.x, N.y, N.z), lp, true);
+    };
+    if (warp < count) fetch(warp);
+    for (unsigned h = warp; h < count; h += n_warps) {
+        const float4 Pc = P, Nc = N;
+        unsigned hmc[kWords + 1];
+#pragma unroll
+        for (int w = 0; w <= kWords; w++) hmc[w] = hm[w];
+        if (h + n_warps < count) fetch(h + n_warps);
+        const int slot = __float_as_int(Pc.w);
+        const ShadowFrame f = shadow_frame(f3(Pc.x, Pc.y, Pc.z), f3(Nc.x, Nc.y, Nc.z), lp, true);
         int nsph = 0;
-        int unblocked = sample_hit<MAXS, SMEM_TAB>(ps, f, hm, n, gtab, nsph);
+        int unblocked = sample_hit<MAXS, SMEM_TAB>(ps, f, hmc, n, gtab, nsph);
         unblocked = __reduce_add_sync(0xffffffffu, unblocked);
         if (lane != 0) continue;
         reinterpret_cast<float *>(wa.rec + slot)[3] = (float)unblocked / (float)n;
@@ -387,7 +401,7 @@ __global__ void __launch_bounds__(kThreads)
             atomicAdd(wa.work + kWorkSampledHits, 1ull);
             atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);
             atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n * nsph);
-            atomicAdd(wa.work + kWorkPlaneTests, (unsigned long long)n * __popc(hm[kWords]));
+            atomicAdd(wa.work + kWorkPlaneTests, (unsigned long long)n * __popc(hmc[kWords]));
         }
     }
 }
@@ -401,9 +415,11 @@ __global__ void __launch_bounds__(kThreads)
         const int lpix = __ldg(wa.queue3 + i);
         const float4 px = wa.pix[lpix];
         const int info = __float_as_int(px.w);
-        const float3 c = unwind(info & 0xff, (info >> 8) & 1, f3(px.x, px.y, px.z), sa, [&](int k) {
-            const float4 r = wa.rec[(int64_t)k * wa.n_pix + lpix];
-            return Record{__float_as_int(r.x), r.y, r.z, r.w};
+        const int m = info & 0xff;
+        float4 rk[kMaxBounce + 1];  // issue every record load before the first use
+        for (int k = 0; k < m; k++) rk[k] = wa.rec[(int64_t)k * wa.n_pix + lpix];
+        const float3 c = unwind(m, (info >> 8) & 1, f3(px.x, px.y, px.z), sa, [&](int k) {
+            return Record{__float_as_int(rk[k].x), rk[k].y, rk[k].z, rk[k].w};
         });
         const int ly = lpix / fa.width, x = lpix - ly * fa.width;
         store_pixel(fa, x, map_row(ly, fa), c);

@@ -119,8 +119,9 @@ int rt_trace_rays_v1(rt_ctx *ctx, const double *origins, const double *dirs, int
 int rt_sky_sample_v1(rt_ctx *ctx, const double *dirs, int64_t n, double *out_rgb, const float *sky, int32_t sky_w,
                      int32_t sky_h);
 
-/* Page-lock a host framebuffer so the device→host copy of rt_render_v1 runs
- * at PCIe speed.  The caller keeps the memory alive until unregistered. */
+/* Page-lock and map a host framebuffer: rt_render_v1 then writes it directly
+ * from the kernels (option "zero_copy") or copies into it at PCIe speed.
+ * The caller keeps the memory alive until unregistered. */
 int rt_host_register(rt_ctx *ctx, void *ptr, size_t bytes);
 int rt_host_unregister(rt_ctx *ctx, void *ptr);
 
@@ -137,7 +138,11 @@ int rt_host_unregister(rt_ctx *ctx, void *ptr);
  *                 rt_phase_ms can report per-phase device times (off by
  *                 default: each event record costs the GPU ~2-3 us);
  *   "rgba"        write pixels as bytes R,G,B,A (the frame server's wire
- *                 format, server.py:56-64) instead of 0xAARRGGBB. */
+ *                 format, server.py:56-64) instead of 0xAARRGGBB;
+ *   "zero_copy"   (default on) when the framebuffer passed to rt_render_v1
+ *                 on one device is registered (rt_host_register), the
+ *                 kernels store pixels straight into it over PCIe while they
+ *                 compute — no device-to-host copy after the frame. */
 int rt_set_option(rt_ctx *ctx, const char *name, int32_t value);
 /* Executed-work tallies since the last reset: hits, per-hit cull tests, hits
  * that sampled, shadow rays traced, sphere tests, plane tests. */

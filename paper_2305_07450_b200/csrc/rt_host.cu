@@ -140,6 +140,7 @@ struct rt_ctx {
     int bands = 0;            // single-device row bands for copy overlap (0: by frame size)
     bool phases = false;      // record per-phase events in wavefront frames (rt_phase_ms)
     int rgba = 0;             // pixel byte order of the frames written (0 B,G,R,A / 1 R,G,B,A)
+    bool zero_copy = true;    // kernels store straight into a registered (mapped) host framebuffer
     std::mutex mu;
     HostScene scene;
     float last_ms = 0.f;
@@ -610,6 +611,26 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
     if (n_dev == 1) {
         Dev &d = ctx->devs[0];
         RT_CK(cudaSetDevice(d.id));
+        // A page-locked, mapped framebuffer (rt_host_register) is written by the
+        // kernels themselves: pixel stores travel over PCIe while the frame is
+        // still being computed, so no copy follows the last kernel.
+        uint32_t *host_px = nullptr;
+        void *host_rad = nullptr;
+        if (ctx->zero_copy && cudaHostGetDevicePointer((void **)&host_px, pixels, 0) == cudaSuccess &&
+            (!radiance || cudaHostGetDevicePointer(&host_rad, radiance, 0) == cudaSuccess)) {
+            RT_CK(cudaEventRecord(d.e0, d.st));
+            for (int p = 0; p < n_parts; p++) {
+                rt::FrameArgs fa = frame_args(host_px, width, host_rad, width, height, cam_pos, yaw, pitch, vdist,
+                                              shadow_samples, bounce_limit, p, n_parts, block_rows);
+                fa.peer_out = 0;  // kernel completion + stream sync order the stores for the host
+                if ((rc = launch_frame(ctx, d, fa, precision, d.st))) return rc;
+            }
+            RT_CK(cudaEventRecord(d.e1, d.st));
+            RT_CK(cudaStreamSynchronize(d.st));
+            RT_CK(cudaEventElapsedTime(&ctx->last_ms, d.e0, d.e1));
+            return RT_OK;
+        }
+        cudaGetLastError();  // not registered: a cudaHostGetDevicePointer miss is not an error
         // (a band costs ~5 kernel boundaries; below ~16 MB that outweighs the hidden copy)
         int bands = ctx->bands > 0 ? ctx->bands : (px_bytes >= ((size_t)16 << 20) ? 4 : 1);
         bands = std::max(1, std::min(bands, height / 8));
@@ -820,7 +841,7 @@ int rt_sky_sample_v1(rt_ctx *ctx, const double *dirs, int64_t n, double *out_rgb
 int rt_host_register(rt_ctx *ctx, void *ptr, size_t bytes) {
     if (!ctx || !ptr || bytes == 0) return fail(RT_ERR_INVALID, "bad host range");
     RT_CK(cudaSetDevice(ctx->devs[0].id));
-    RT_CK(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable));
+    RT_CK(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped));
     return RT_OK;
 }
 
@@ -841,6 +862,7 @@ int rt_set_option(rt_ctx *ctx, const char *name, int32_t value) {
     else if (n == "bands") ctx->bands = std::max(0, std::min((int)value, 4));
     else if (n == "phases") ctx->phases = value != 0;
     else if (n == "rgba") ctx->rgba = value != 0;
+    else if (n == "zero_copy") ctx->zero_copy = value != 0;
     else return fail(RT_ERR_INVALID, "unknown option " + n);
     return RT_OK;
 }

@@ -139,10 +139,12 @@ int rt_host_unregister(rt_ctx *ctx, void *ptr);
  *                 default: each event record costs the GPU ~2-3 us);
  *   "rgba"        write pixels as bytes R,G,B,A (the frame server's wire
  *                 format, server.py:56-64) instead of 0xAARRGGBB;
- *   "zero_copy"   (default on) when the framebuffer passed to rt_render_v1
+ *   "zero_copy"   (default off) when the framebuffer passed to rt_render_v1
  *                 on one device is registered (rt_host_register), the
  *                 kernels store pixels straight into it over PCIe while they
- *                 compute — no device-to-host copy after the frame. */
+ *                 compute — no copy after the frame, but measured 1.3-2.4x
+ *                 slower end to end on B200 (PCIe writes of 32-byte rows
+ *                 stall the kernels), so the staged copy is the default. */
 int rt_set_option(rt_ctx *ctx, const char *name, int32_t value);
 /* Executed-work tallies since the last reset: hits, per-hit cull tests, hits
  * that sampled, shadow rays traced, sphere tests, plane tests. */

@@ -140,7 +140,7 @@ struct rt_ctx {
     int bands = 0;            // single-device row bands for copy overlap (0: by frame size)
     bool phases = false;      // record per-phase events in wavefront frames (rt_phase_ms)
     int rgba = 0;             // pixel byte order of the frames written (0 B,G,R,A / 1 R,G,B,A)
-    bool zero_copy = true;    // kernels store straight into a registered (mapped) host framebuffer
+    bool zero_copy = false;   // kernels store straight into a registered (mapped) host framebuffer
     std::mutex mu;
     HostScene scene;
     float last_ms = 0.f;

@@ -327,3 +327,52 @@ def test_moving_bodies_between_frames():
             b = scene.bodies[i]
             b.position = (b.position[0] + 0.15, b.position[1] + 0.05 * (step + 1), b.position[2] - 0.1)
         scene.light.position = (scene.light.position[0] + 0.2, scene.light.position[1], scene.light.position[2])
+
+
+@pytest.mark.parametrize("count,samples", [(300, 1), (300, 16), (1100, 4)])
+def test_large_scenes_take_the_memory_paths(count, samples):
+    """Scenes beyond the launch-parameter layout (> 256 spheres) run from
+    shared / global memory; FP32 stays within the byte gate of the FP64
+    kernel, which matches the oracle exactly."""
+    s = rt.stress_scene(count=count, seed=11)
+    cam = rt.Camera(position=(0.0, 2.0, -5.0), yaw=0.05, pitch=-0.15, fov=70.0)
+    w, h = (48, 27) if count > 1000 else (96, 54)
+    params = rt.RenderParams(samples, 3, w, h)
+    fb32 = rt.Framebuffer.create(w, h)
+    rt.render_frame(s, cam, params, fb32)
+    fb64 = rt.Framebuffer.create(w, h)
+    rt.render_frame(s, cam, params, fb64, precision="fp64")
+    ps = rt.pack_scene(s)
+    want = oracle.render(vars(ps), cam.position, cam.yaw, cam.pitch, cam.fov, w, h, samples, 3)
+    np.testing.assert_array_equal(fb64.pixels, want)
+    parity.assert_byte_gate(fb32.pixels, want, f"{count} spheres")
+
+
+def test_many_planes():
+    """More planes than the launch-parameter layout holds (8)."""
+    s = rt.build_benchmark_scene()
+    for k in range(10):
+        s.bodies.append(rt.Body.plane(-1.0 - 0.1 * k, (0.2, 0.3, 0.4 + 0.05 * k), 8.0))
+    s.bodies.append(rt.Body.plane(9.0, (0.9, 0.9, 0.9), 0.0))  # a ceiling above the light: shadows everything
+    cam, params = rt.benchmark_camera(), rt.RenderParams(12, 2, 64, 36)
+    fb32 = rt.Framebuffer.create(64, 36)
+    rt.render_frame(s, cam, params, fb32)
+    ps = rt.pack_scene(s)
+    want = oracle.render(vars(ps), cam.position, cam.yaw, cam.pitch, cam.fov, 64, 36, 12, 2)
+    parity.assert_byte_gate(fb32.pixels, want, "many planes")
+
+
+def test_zero_copy_option_gives_the_same_frame():
+    c = G.frame_case("sweep_160x90_s16_b5_sky")
+    base, _ = render_case(c, "fp32")
+    _native.set_options(zero_copy=1)
+    try:
+        scene = scene_from_case(c)
+        cam = rt.Camera(**{**c["camera"], "position": tuple(c["camera"]["position"])})
+        params = rt.RenderParams(c["samples"], c["bounces"], c["width"], c["height"])
+        fb = rt.Framebuffer.create(c["width"], c["height"])
+        _native.context(1).pin(fb.pixels)  # registered + mapped: the kernels write it directly
+        rt.render_frame(scene, cam, params, fb)
+        np.testing.assert_array_equal(fb.pixels, base)
+    finally:
+        _native.set_options(zero_copy=0)

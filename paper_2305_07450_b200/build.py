@@ -33,6 +33,7 @@ SOURCES = {
     "render_wave_f32.cu": ["--ftz=true", "--prec-div=false", "--prec-sqrt=false"],
     "render_fused_f32.cu": ["--ftz=true", "--prec-div=false", "--prec-sqrt=false"],
     "render_f64.cu": ["-fmad=false"],
+    "render_fused_f64.cu": ["-fmad=false"],
 }
 
 

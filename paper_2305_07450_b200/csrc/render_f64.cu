@@ -8,89 +8,11 @@
 //
 // Every function cites the reference line it restates
 // (/root/reference/pkg/src/raytracer/...).
-#include "rt_device.cuh"
+#include "rt_f64.cuh"
 
 namespace {
 using namespace rt;
-
-struct d3 {
-    double x, y, z;
-};
-__device__ __forceinline__ d3 mk(double x, double y, double z) { return d3{x, y, z}; }
-__device__ __forceinline__ d3 vsub(d3 a, d3 b) { return mk(a.x - b.x, a.y - b.y, a.z - b.z); }  // vecmath.py:33
-__device__ __forceinline__ double vdot(d3 a, d3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }  // vecmath.py:49
-__device__ __forceinline__ d3 vcross(d3 a, d3 b) {  // vecmath.py:54-60
-    return mk(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
-}
-__device__ __forceinline__ double vmag(d3 a) { return sqrt(a.x * a.x + a.y * a.y + a.z * a.z); }  // vecmath.py:63
-__device__ __forceinline__ d3 vnormalize(d3 a) {  // vecmath.py:68-78 (zero-safe)
-    double m = vmag(a);
-    if (m == 0.0) return mk(0.0, 0.0, 0.0);
-    return mk(a.x / m, a.y / m, a.z / m);
-}
-__device__ __forceinline__ double vdistance(d3 a, d3 b) {  // vecmath.py:81-86
-    double dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z;
-    return sqrt(dx * dx + dy * dy + dz * dz);
-}
-__device__ __forceinline__ d3 vreflect(d3 i, d3 n) {  // vecmath.py:89-96
-    double k = 2.0 * (n.x * i.x + n.y * i.y + n.z * i.z);
-    return mk(i.x - k * n.x, i.y - k * n.y, i.z - k * n.z);
-}
-
-// camera.py:46-54 + 70-77, vecmath.py:99-110
-__device__ __forceinline__ d3 primary_direction(int xi, int yi, const FrameArgs &fa) {
-    double x = (double)xi, y = (double)yi, w = (double)fa.width, h = (double)fa.height;
-    double u, v;
-    if (w > h) {
-        u = (x - w / 2 + h / 2) / h * 2 - 1;
-        v = -(y / h * 2 - 1);
-    } else {
-        u = x / w * 2 - 1;
-        v = -((y - h / 2 + w / 2) / w * 2 - 1);
-    }
-    d3 d = vnormalize(mk(u, v, fa.vdist));
-    double y2 = d.y * fa.cb - d.z * fa.sb;
-    double z2 = d.y * fa.sb + d.z * fa.cb;
-    double x2 = d.x * fa.ca + z2 * fa.sa;
-    double z3 = -d.x * fa.sa + z2 * fa.ca;
-    return mk(x2, y2, z3);
-}
-
-// geometry.py:83-105 — literal d2 = L.L - tca^2 (the golden hash encodes it)
-__device__ __forceinline__ double ray_sphere(d3 o, d3 d, const double *g) {
-    double lx = g[0] - o.x, ly = g[1] - o.y, lz = g[2] - o.z;
-    double tca = lx * d.x + ly * d.y + lz * d.z;
-    if (tca < 0.0) return INFINITY;
-    double d2 = lx * lx + ly * ly + lz * lz - tca * tca;
-    double rad = g[3] - d2;  // g[3] = radius * radius, formed on the host in float64
-    if (rad < -1e-7) return INFINITY;
-    if (rad < 0.0) rad = 0.0;
-    double t = tca - sqrt(rad);
-    if (t < 0.0) return INFINITY;
-    return t;
-}
-
-// geometry.py:108-117
-__device__ __forceinline__ double ray_plane(d3 o, d3 d, double h) {
-    double dy = d.y;
-    if (dy == 0.0) return INFINITY;
-    double t = (h - o.y) / dy;
-    if (t <= 0.0) return INFINITY;
-    return t;
-}
-
-// geometry.py:179-188
-__device__ __forceinline__ double intersect(d3 o, d3 d, const double *g) {
-    if (g[3] >= 0.0) return ray_sphere(o, d, g);
-    return ray_plane(o, d, g[1]);
-}
-
-// shading.py:89-100 with the (r cos, r sin) pair from the host table
-__device__ __forceinline__ d3 disc_point(int i, d3 c, d3 u, d3 v, const double *table) {
-    double a = table[2 * i];
-    double b = table[2 * i + 1];
-    return mk(c.x + a * u.x + b * v.x, c.y + a * u.y + b * v.y, c.z + a * u.z + b * v.z);
-}
+using namespace rt64;
 
 // renderer.py:82-105 (+ shading.py:76-86 disc_basis, geometry.py:204-210)
 __device__ double shadow_coeff(d3 surface, d3 normal, const double *__restrict__ geo, const SceneArgs<double> &sa,
@@ -126,28 +48,6 @@ __device__ double shadow_coeff(d3 surface, d3 normal, const double *__restrict__
         if (!blocked) unblocked += 1;
     }
     return (double)unblocked / (double)n;
-}
-
-__device__ __forceinline__ double clamp01(double x) {  // min(max(x, 0.0), 1.0)
-    double m = (0.0 > x) ? 0.0 : x;
-    return (1.0 < m) ? 1.0 : m;
-}
-
-// renderer.py:60-74
-__device__ d3 sky_sample(d3 d, const float4 *__restrict__ sky, int W, int H) {
-    double u = 0.5 + atan2(d.x, d.z) / (2.0 * 3.141592653589793);
-    double dy = d.y < -1.0 ? -1.0 : d.y;
-    dy = dy > 1.0 ? 1.0 : dy;
-    double v = 0.5 - asin(dy) / 3.141592653589793;
-    long long tx = (long long)floor(u * (double)W);
-    tx = ((tx % W) + W) % W;
-    long long ty = (long long)floor(v * (double)H);
-    if (ty < 0)
-        ty = 0;
-    else if (ty > H - 1)
-        ty = H - 1;
-    float4 t = __ldg(sky + ty * (long long)W + tx);  // texels pre-clamped on upload
-    return mk((double)t.x, (double)t.y, (double)t.z);
 }
 
 // renderer.py:108-224.  A record keeps (body, lum, spec): shade_color's

@@ -1,0 +1,312 @@
+// FP64 soft shadows with exact occluder culling: the bit-identical mode at
+// wavefront speed.  Same three kernels as the FP32 culled path
+// (render_fused_f32.cu) — trace + per-hit cone classification, sampling of
+// the undecided hits, unwind of the parked pixels — but every test that the
+// reference performs is performed here in its literal float64 order
+// (rt_f64.cuh, compiled with -fmad=false); the cone classifier only decides
+// which bodies cannot block any of a hit's shadow rays (or block all of
+// them) with margins of 1e-4 relative, far above float64 rounding, so the
+// skipped tests are exactly the ones the reference would have failed.
+//
+// Scenes of up to kMaxBodies64 bodies (geometry staged in shared memory per
+// CTA, candidate masks over original body indices); larger scenes keep the
+// megakernel.
+#include <map>
+#include <utility>
+
+#include "rt_f64.cuh"
+
+namespace {
+using namespace rt;
+using namespace rt64;
+
+constexpr int kWords64 = kMaxBodies64 / 32;
+constexpr double kCullRel64 = 1e-4;
+constexpr double kCullAbs64 = 1e-5;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// The hit's shadow cone (see rt_wave.cuh for the geometry), in float64.
+struct Cone64 {
+    d3 o, axis;
+    double H, rho, inv_H, sin_phi, cos_phi, reach;
+    bool ok;
+};
+
+__device__ __forceinline__ Cone64 make_cone(d3 o, d3 lp, double light_radius) {
+    Cone64 c;
+    c.o = o;
+    d3 A = vsub(lp, o);
+    c.H = sqrt(vdot(A, A));
+    c.rho = 2.0 * light_radius * (1.0 + kCullRel64) + kCullAbs64;
+    c.ok = c.H > 0.0 && c.rho < 0.999 * c.H;
+    c.inv_H = c.H > 0.0 ? 1.0 / c.H : 0.0;
+    c.axis = mk(A.x * c.inv_H, A.y * c.inv_H, A.z * c.inv_H);
+    c.sin_phi = c.ok ? c.rho * c.inv_H : 1.0;
+    c.cos_phi = sqrt(fmax(1.0 - c.sin_phi * c.sin_phi, 0.0));
+    double T = 1.0 + (1e-3 + kCullAbs64) / fmax(c.H - c.rho, 1e-9);
+    c.reach = T * (c.H + c.rho) * (1.0 + kCullRel64) + kCullAbs64;
+    return c;
+}
+
+// 0: the body can block none of the hit's shadow rays; 1: some; 2: all.
+__device__ __forceinline__ int body_class(const Cone64 &k, const double *g, double oy, double ly) {
+    if (!k.ok) return 1;
+    if (g[3] < 0.0) {  // horizontal plane at g[1]
+        double hp = g[1], m = kCullAbs64 * (1.0 + fabs(hp) + fabs(ly));
+        double lo = ly - k.rho - 1e-3 - m, hi = ly + k.rho + 1e-3 + m;
+        double a = oy - hp;
+        if ((a > m && lo > hp + m) || (a < -m && hi < hp - m)) return 0;
+        if ((a > m && hi < hp - m) || (a < -m && lo > hp + m)) return 2;
+        return 1;
+    }
+    d3 u = mk(g[0] - k.o.x, g[1] - k.o.y, g[2] - k.o.z);
+    double u2 = vdot(u, u);
+    if (u2 < g[3] * (1.0 - 4.0 * kCullRel64) - kCullAbs64) return 0;  // origin inside: t < 0 always
+    double h = vdot(u, k.axis);
+    d3 w = mk(u.x - k.axis.x * h, u.y - k.axis.y * h, u.z - k.axis.z * h);
+    double q = sqrt(vdot(w, w));
+    double un = fabs(h) + q;
+    double r = sqrt(g[3]);
+    double rp = sqrt(g[3] + 1e-7) * (1.0 + kCullRel64) + kCullAbs64 + 1e-6 * (un + k.H);
+    if (h < -rp || h - rp > k.reach) return 0;
+    if (h * k.cos_phi + q * k.sin_phi >= 0.0) {
+        if (q * k.cos_phi - h * k.sin_phi >= rp) return 0;
+    } else if (u2 >= rp * rp) {
+        return 0;
+    }
+    double rm = r * (1.0 - 10.0 * kCullRel64) - kCullAbs64 - 1e-6 * (un + k.H);
+    if (u2 > g[3] * (1.0 + 4.0 * kCullRel64) + kCullAbs64 && h > 0.0 &&
+        h + r < (k.H - k.rho) * (1.0 - kCullRel64) - 2e-3 && q + h * k.inv_H * k.rho * (1.0 + kCullRel64) < rm)
+        return 2;
+    return 1;
+}
+
+__device__ __forceinline__ const double *stage(const SceneArgs<double> &sa, double *smem) {
+    for (int i = threadIdx.x; i < 4 * sa.n; i += blockDim.x) smem[i] = sa.geo[i];
+    __syncthreads();
+    return smem;
+}
+
+// --- A: trace, classify, unwind the decided pixels ---------------------------------
+__global__ void __launch_bounds__(kThreads)
+    fused64_trace(const FrameArgs fa, const SceneArgs<double> sa, const WaveArgs64 wa) {
+    extern __shared__ double smem_geo[];
+    const double *__restrict__ geo = stage(sa, smem_geo);
+    const int lane = threadIdx.x & 31;
+    int x, ly;
+    thread_pixel(x, ly);
+    int y = 0;
+    bool alive = x < fa.width && ly < fa.local_rows;
+    if (alive) {
+        y = map_row(ly, fa);
+        alive = y < fa.row_end;
+    }
+    const bool valid = alive;
+    const int64_t lp = (int64_t)ly * fa.width + x;
+    const d3 light = mk(sa.light[0], sa.light[1], sa.light[2]);
+    d3 origin = mk(fa.cam[0], fa.cam[1], fa.cam[2]);
+    d3 dir = valid ? primary_direction(x, y, fa) : mk(0.0, 0.0, 1.0);
+    d3 tail = mk(0.0, 0.0, 0.0);
+    int m = 0, exhausted = 0, npend = 0;
+    int ridx[kMaxBounce + 1];
+    double rdfs[kMaxBounce + 1], rs[kMaxBounce + 1], rsc[kMaxBounce + 1];
+    for (int k = 0; k <= fa.bounces; k++) {
+        if (!__any_sync(0xffffffffu, alive)) break;
+        double t = INFINITY;
+        int idx = -1;
+        if (alive) idx = closest(origin, dir, geo, sa.n, t);
+        const bool hit_now = alive && idx >= 0;
+        if (alive && !hit_now) {
+            if (sa.has_sky) tail = sky_sample(dir, sa.sky, sa.sky_w, sa.sky_h);
+            alive = false;
+        }
+        int cls = 0;
+        int64_t slot = 0;
+        unsigned mask[kWords64];
+        d3 hit = mk(0.0, 0.0, 0.0), normal = mk(0.0, 1.0, 0.0);
+        if (hit_now) {
+            const double *g = geo + 4 * idx;
+            hit = mk(origin.x + dir.x * t, origin.y + dir.y * t, origin.z + dir.z * t);
+            normal = (g[3] >= 0.0) ? vnormalize(vsub(hit, mk(g[0], g[1], g[2]))) : mk(0.0, 1.0, 0.0);
+            d3 l = vnormalize(vsub(light, hit));
+            double dfs, s;
+            hit_terms(normal, l, dir, __ldg(sa.mat + 8 * idx + 4), dfs, s);
+            // renderer.py:87-89: the shadow rays' origin
+            const d3 so = mk(hit.x + 1e-3 * normal.x, hit.y + 1e-3 * normal.y, hit.z + 1e-3 * normal.z);
+            const Cone64 cone = make_cone(so, light, sa.light_radius);
+#pragma unroll
+            for (int w = 0; w < kWords64; w++) mask[w] = 0;
+            bool full = false, any = false;
+            for (int b = 0; b < sa.n; b++) {
+                int c = body_class(cone, geo + 4 * b, so.y, light.y);
+                mask[b >> 5] |= (c == 1 ? 1u : 0u) << (b & 31);
+                full |= c == 2;
+                any |= c == 1;
+            }
+            cls = full ? 2 : (any ? 1 : 0);
+            slot = (int64_t)k * wa.n_pix + lp;
+            ridx[k] = idx;
+            rdfs[k] = dfs;
+            rs[k] = s;
+            rsc[k] = cls == 2 ? 0.0 : 1.0;  // (double)n / n and 0 / n of renderer.py:105
+            if (cls == 1) npend++;
+            m = k + 1;
+            if (k == fa.bounces) {
+                exhausted = 1;
+                alive = false;
+            } else {
+                origin = so;  // renderer.py:178-183: the same offset
+                dir = vreflect(dir, normal);
+            }
+        }
+        const bool need = hit_now && cls == 1;
+        const unsigned nb = __ballot_sync(0xffffffffu, need);
+        if (nb) {
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(wa.count + 1, (unsigned)__popc(nb));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (need) {
+                const unsigned e = base + __popc(nb & lanemask_lt());
+                wa.q[2 * e] = make_double4(hit.x, hit.y, hit.z, (double)slot);
+                wa.q[2 * e + 1] = make_double4(normal.x, normal.y, normal.z, 0.0);
+#pragma unroll
+                for (int w = 0; w < kWords64; w++) wa.mask[(size_t)w * wa.mask_stride + e] = mask[w];
+            }
+        }
+    }
+    const bool park = valid && npend > 0;
+    const unsigned pb = __ballot_sync(0xffffffffu, park);
+    if (pb) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(wa.count + 2, (unsigned)__popc(pb));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (park) wa.parked[base + __popc(pb & lanemask_lt())] = (int)lp;
+    }
+    if (!valid) return;
+    if (!park) {
+        const d3 c = unwind(m, exhausted, tail, sa, [&](int k, int &i, double &d, double &s, double &sc) {
+            i = ridx[k];
+            d = rdfs[k];
+            s = rs[k];
+            sc = rsc[k];
+        });
+        fa.out[(int64_t)y * fa.out_pitch + x] = pack_color(c.x, c.y, c.z, fa.rgba);
+        if (fa.radiance) {
+            double *r = (double *)fa.radiance + 3 * ((int64_t)y * fa.width + x);
+            r[0] = c.x;
+            r[1] = c.y;
+            r[2] = c.z;
+        }
+        if (fa.peer_out) __threadfence_system();
+    } else {
+        wa.pix[lp] = make_double4(tail.x, tail.y, tail.z, (double)(m | (exhausted << 8)));
+        for (int k = 0; k < m; k++)
+            wa.rec[(int64_t)k * wa.n_pix + lp] = make_double4((double)ridx[k], rdfs[k], rs[k], rsc[k]);
+    }
+}
+
+// --- B: one warp per undecided hit, the reference's shadow loop (renderer.py:82-105) ---
+__global__ void __launch_bounds__(kThreads)
+    fused64_sample(const FrameArgs fa, const SceneArgs<double> sa, const WaveArgs64 wa) {
+    extern __shared__ double smem_geo[];
+    const double *__restrict__ geo = stage(sa, smem_geo);
+    const unsigned count = wa.count[1];
+    const int lane = threadIdx.x & 31;
+    const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned n_warps = (gridDim.x * blockDim.x) >> 5;
+    const int n = fa.samples;
+    const d3 lp = mk(sa.light[0], sa.light[1], sa.light[2]);
+    for (unsigned h = warp; h < count; h += n_warps) {
+        const double4 P = wa.q[2 * h], N = wa.q[2 * h + 1];
+        unsigned hm[kWords64];
+#pragma unroll
+        for (int w = 0; w < kWords64; w++) hm[w] = wa.mask[(size_t)w * wa.mask_stride + h];
+        const d3 surface = mk(P.x, P.y, P.z), normal = mk(N.x, N.y, N.z);
+        const d3 origin = mk(surface.x + 1e-3 * normal.x, surface.y + 1e-3 * normal.y, surface.z + 1e-3 * normal.z);
+        d3 bu, bv;
+        disc_basis(surface, lp, bu, bv);
+        int unblocked = 0;
+        for (int i = lane; i < n; i += 32) {
+            const d3 s = disc_point(i, lp, bu, bv, sa.table);
+            const d3 d = vnormalize(vsub(s, origin));
+            const double limit = vdistance(surface, s);
+            bool blocked = false;
+#pragma unroll
+            for (int w = 0; w < kWords64; w++)
+                for (unsigned bm = hm[w]; bm && !blocked; bm &= bm - 1)
+                    blocked = intersect(origin, d, geo + 4 * (w * 32 + __ffs(bm) - 1)) < limit;
+            unblocked += blocked ? 0 : 1;
+        }
+        unblocked = __reduce_add_sync(0xffffffffu, unblocked);
+        if (lane == 0) {
+            const int64_t slot = (int64_t)P.w;
+            wa.rec[slot].w = (double)unblocked / (double)n;
+        }
+    }
+}
+
+// --- C: unwind the parked pixels -------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+    fused64_finish(const FrameArgs fa, const SceneArgs<double> sa, const WaveArgs64 wa) {
+    const unsigned count = wa.count[2];
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+        const int lpix = wa.parked[i];
+        const double4 px = wa.pix[lpix];
+        const int info = (int)px.w;
+        const d3 c = unwind(info & 0xff, (info >> 8) & 1, mk(px.x, px.y, px.z), sa,
+                            [&](int k, int &idx, double &d, double &s, double &sc) {
+                                const double4 r = wa.rec[(int64_t)k * wa.n_pix + lpix];
+                                idx = (int)r.x;
+                                d = r.y;
+                                s = r.z;
+                                sc = r.w;
+                            });
+        const int ly = lpix / fa.width, x = lpix - ly * fa.width;
+        const int y = map_row(ly, fa);
+        fa.out[(int64_t)y * fa.out_pitch + x] = pack_color(c.x, c.y, c.z, fa.rgba);
+        if (fa.radiance) {
+            double *r = (double *)fa.radiance + 3 * ((int64_t)y * fa.width + x);
+            r[0] = c.x;
+            r[1] = c.y;
+            r[2] = c.z;
+        }
+        if (fa.peer_out) __threadfence_system();
+    }
+}
+
+int ctas_for(const void *kernel, size_t smem) {
+    static thread_local std::map<std::pair<const void *, size_t>, int> memo;
+    auto key = std::make_pair(kernel, smem);
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+    return memo[key] = sms * (per_sm > 0 ? per_sm : 1);
+}
+
+}  // namespace
+
+cudaError_t rt_launch_fused_f64(const rt::FrameArgs &fa, const rt::SceneArgs<double> &sa, const rt::WaveArgs64 &wa,
+                                cudaStream_t st, int *n_kernels) {
+    *n_kernels = 0;
+    if (sa.n > kMaxBodies64 || fa.samples < 2) return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemsetAsync(wa.count, 0, 4 * sizeof(unsigned), st);
+    if (e != cudaSuccess) return e;
+    const size_t smem = sizeof(double) * 4 * (size_t)(sa.n > 0 ? sa.n : 1);
+    dim3 grid((fa.width + kTileW - 1) / kTileW, (fa.local_rows + kTileH - 1) / kTileH);
+    fused64_trace<<<grid, kThreads, smem, st>>>(fa, sa, wa);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    fused64_sample<<<ctas_for((const void *)fused64_sample, smem), kThreads, smem, st>>>(fa, sa, wa);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    fused64_finish<<<ctas_for((const void *)fused64_finish, 0), kThreads, 0, st>>>(fa, sa, wa);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    *n_kernels = 3;
+    return cudaSuccess;
+}

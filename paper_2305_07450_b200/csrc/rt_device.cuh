@@ -78,6 +78,19 @@ struct WaveArgs {
     unsigned long long *work;  // optional executed-work tallies of the culled path (kWork*), or null
     int cull;          // exact per-hit occluder culling in the shadow kernel
 };
+// FP64 culled wavefront (render_fused_f64.cu): queues in float64
+constexpr int kMaxBodies64 = 256;
+struct WaveArgs64 {
+    double4 *q;        // queued undecided hits: [2e] {p, record slot}, [2e+1] {n, 0}
+    unsigned *mask;    // their candidate-body masks (original indices), word-major [8][mask_stride]
+    int64_t mask_stride;
+    unsigned *count;   // [1] queue length, [2] parked pixels
+    double4 *pix;      // parked pixels: {tail rgb, records | exhausted << 8}
+    double4 *rec;      // {body, Lambert, Blinn, coefficient} per hit of a parked pixel
+    int *parked;       // parked pixels (local indices)
+    int64_t n_pix;
+};
+
 // executed-work tallies of the culled shadow kernel (rt_work_counts)
 enum { kWorkHits = 0, kWorkCullTests, kWorkSampledHits, kWorkShadowRays, kWorkSphereTests, kWorkPlaneTests,
        kWorkTraceRays, kWorkTraceTests, kWorkTraceFullWarps, kWorkN };
@@ -145,6 +158,8 @@ int rt_wave_lanes(int samples);
 bool rt_fused_fits(const rt::SceneArgs<float> &sa);
 cudaError_t rt_launch_fused_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, const rt::WaveArgs &wa,
                                 cudaStream_t st, int *n_kernels, cudaEvent_t *phase_events /* 5 or null */);
+cudaError_t rt_launch_fused_f64(const rt::FrameArgs &fa, const rt::SceneArgs<double> &sa, const rt::WaveArgs64 &wa,
+                                cudaStream_t st, int *n_kernels);
 cudaError_t rt_launch_trace_f32(const double *d_orig, const double *d_dir, int64_t n, float *d_out,
                                 const rt::SceneArgs<float> &sa, int samples, int bounces, cudaStream_t st);
 cudaError_t rt_launch_trace_f64(const double *d_orig, const double *d_dir, int64_t n, double *d_out,

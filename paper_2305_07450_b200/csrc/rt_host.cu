@@ -87,7 +87,8 @@ struct Dev {
     cudaEvent_t band_ev[4] = {nullptr, nullptr, nullptr, nullptr};
     bool ph_valid = false;
     DBuf frame, rad, rays_in, rays_out, sky_raw, sky, counters;
-    DBuf w_p, w_n, w_s, w_sc, w_queue, w_queue2, w_mask2, w_count, w_pix, w_work, w_rec, w_pending;  // wavefront queues (FP32 soft shadows)
+    DBuf w_p, w_n, w_s, w_sc, w_queue, w_queue2, w_mask2, w_count, w_pix, w_work, w_rec, w_pending;
+    DBuf d_q, d_mask, d_pix, d_rec, d_parked;  // FP64 culled wavefront queues  // wavefront queues (FP32 soft shadows)
     unsigned counter_slot = 0;
     uint64_t sky_version = ~0ull;
     DevScene<float> s32;
@@ -412,7 +413,27 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
     fa.work_counter = (unsigned *)d.counters.p + (d.counter_slot++ % rt::kCounterRing);
     RT_CK(cudaMemsetAsync(fa.work_counter, 0, sizeof(unsigned), st));
     d.ph_valid = false;
-    if (precision == RT_PREC_FP64) {
+    if (precision == RT_PREC_FP64 && fa.samples >= rt::kWaveMinSamples && ctx->wave && ctx->cull &&
+        ctx->scene.n <= rt::kMaxBodies64) {
+        rt::WaveArgs64 wa = {};
+        wa.n_pix = (int64_t)fa.local_rows * fa.width;
+        size_t slots = (size_t)wa.n_pix * (fa.bounces + 1);
+        if ((rc = d.d_q.ensure(2 * sizeof(double4) * slots)) ||
+            (rc = d.d_mask.ensure(sizeof(unsigned) * slots * (rt::kMaxBodies64 / 32))) ||
+            (rc = d.d_pix.ensure(sizeof(double4) * (size_t)wa.n_pix)) || (rc = d.d_rec.ensure(sizeof(double4) * slots)) ||
+            (rc = d.d_parked.ensure(sizeof(int) * (size_t)wa.n_pix)) || (rc = d.w_count.ensure(4 * sizeof(unsigned))))
+            return rc;
+        wa.q = (double4 *)d.d_q.p;
+        wa.mask = (unsigned *)d.d_mask.p;
+        wa.mask_stride = (int64_t)slots;
+        wa.count = (unsigned *)d.w_count.p;
+        wa.pix = (double4 *)d.d_pix.p;
+        wa.rec = (double4 *)d.d_rec.p;
+        wa.parked = (int *)d.d_parked.p;
+        int nk = 0;
+        e = rt_launch_fused_f64(fa, scene_args(d, d.s64, ctx->scene), wa, st, &nk);
+        ctx->launches += nk - 1;
+    } else if (precision == RT_PREC_FP64) {
         e = rt_launch_render_f64(fa, scene_args(d, d.s64, ctx->scene), st);
     } else if (fa.samples >= rt::kWaveMinSamples && ctx->wave) {
         const rt::SceneArgs<float> sa = scene_args(d, d.s32, ctx->scene);
@@ -541,7 +562,7 @@ int rt_ctx_destroy(rt_ctx *ctx) {
         cudaSetDevice(d.id);
         if (d.st) cudaStreamSynchronize(d.st);
         for (DBuf *b : {&d.w_p, &d.w_n, &d.w_s, &d.w_sc, &d.w_queue, &d.w_queue2, &d.w_mask2, &d.w_count, &d.w_pix,
-                        &d.w_work, &d.w_rec, &d.w_pending})
+                        &d.w_work, &d.w_rec, &d.w_pending, &d.d_q, &d.d_mask, &d.d_pix, &d.d_rec, &d.d_parked})
             b->release();
         for (DBuf *b : {&d.frame, &d.rad, &d.rays_in, &d.rays_out, &d.sky_raw, &d.sky, &d.counters, &d.s32.geo, &d.s32.mat,
                         &d.s32.table, &d.s64.geo, &d.s64.mat, &d.s64.table})

@@ -254,12 +254,15 @@ def run_ours(args):
     fb_ptr = ipc.ptr
     tiny = torch.zeros(1, device=dev)
 
+    cur = {"prec": prec}
+
     def render_cfg(c, part=rank, n_parts=world):
         cam = c.camera()
         cp = np.array(cam.position, dtype=np.float64)
         rc = lib.rt_render_device_v1(ctx.handle, 0, fb_ptr, c.width, None, c.width, c.height, _native.ptr(cp),
                                      float(cam.yaw), float(cam.pitch), rt.camera_viewport_distance(cam.fov),
-                                     c.samples, c.bounces, part, n_parts, 8, prec, ctypes.c_void_p(stream.cuda_stream))
+                                     c.samples, c.bounces, part, n_parts, 8, cur["prec"],
+                                     ctypes.c_void_p(stream.cuda_stream))
         _native.check(rc, "rt_render_device_v1")
         if world > 1:
             import torch.distributed as dist
@@ -421,6 +424,15 @@ def run_ours(args):
                                                                    culled=False)}
         for k, v in dict(wave=1, cull=1).items():
             ctx.set_option(k, v)
+        # the bit-identical mode (float64 in the reference's operation order)
+        cur["prec"] = _native.RT_PREC_FP64
+        for key in (args.config, "P720", "P1080", "P4K"):
+            c = rt.CONFIGS[key]
+            r = time_config(c, 3, 10)
+            f = len(r["ms"]) / (r["total_ms"] / 1e3)
+            extra[f"{key}_fp64_bit_exact"] = {"workload": c.name, "fps": f, "ms_per_frame": statistics.mean(r["ms"]),
+                                              "precision": "fp64, bit-identical to the reference"}
+        cur["prec"] = prec
         line["extra"] = extra
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         v, meta = cpu_reference_sample(cfg, args.cpu_seconds)

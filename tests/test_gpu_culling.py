@@ -1,0 +1,87 @@
+"""Exactness of the culled paths on randomised scenes.
+
+The culls (shadow-cone classification, cluster bounds, warp ray bundles) only
+skip tests that cannot change a result, so on any scene:
+  FP32: culled frame == unculled wavefront frame == megakernel frame, bit for bit;
+  FP64: culled frame == literal megakernel frame, bit for bit (and == the oracle).
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2305_07450_b200 as rt
+from paper_2305_07450_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+MODES = {"cull": dict(wave=1, cull=1), "wave": dict(wave=1, cull=0), "mega": dict(wave=0, cull=0)}
+
+
+def random_scene(rng, n_spheres, with_plane=True, light_radius=None, sky=False):
+    bodies = []
+    for _ in range(n_spheres):
+        r = rng.uniform(0.15, 1.2)
+        bodies.append(rt.Body.sphere((rng.uniform(-4, 4), rng.uniform(-0.5, 3.0), rng.uniform(0, 8)), r,
+                                     tuple(rng.uniform(0.05, 0.95, size=3)), rng.uniform(0, 128)))
+    if with_plane:
+        bodies.insert(int(rng.integers(0, len(bodies) + 1)), rt.Body.plane(rng.uniform(-1.0, 0.2),
+                                                                           tuple(rng.uniform(0.2, 0.8, size=3)),
+                                                                           rng.uniform(0, 64)))
+    lr = light_radius if light_radius is not None else rng.uniform(0.1, 1.5)
+    light = rt.Light((rng.uniform(-5, 5), rng.uniform(3, 9), rng.uniform(-4, 6)), lr)
+    s = rt.Scene(bodies=bodies, light=light)
+    if sky:
+        s.skybox = rt.synthetic_skybox(64, 32)
+    return s
+
+
+def render(scene, cam, params, precision, mode):
+    _native.set_options(**MODES[mode])
+    try:
+        fb = rt.Framebuffer.create(params.width, params.height)
+        rt.render_frame(scene, cam, params, fb, precision=precision)
+        return fb.pixels.copy()
+    finally:
+        _native.set_options(**MODES["cull"])
+
+
+CASES = [
+    # (seed, spheres, samples, bounces, plane, light radius)
+    (1, 5, 200, 3, True, None),
+    (2, 8, 64, 5, True, 0.05),
+    (3, 3, 33, 2, False, 2.5),   # large light: wide cones, many undecided hits
+    (4, 12, 16, 4, True, None),  # > 8 spheres: clustered scene, bundle closest hits
+    (5, 40, 24, 3, True, None),
+    (6, 1, 2049, 1, True, 0.4),  # table beyond shared memory
+    (7, 6, 9, 31, True, None),   # deepest bounce budget
+    (8, 20, 47, 6, True, 0.8),
+]
+
+
+@pytest.mark.parametrize("seed,n,samples,bounces,plane,lr", CASES)
+def test_fp32_paths_bit_identical(seed, n, samples, bounces, plane, lr):
+    rng = np.random.default_rng(seed)
+    scene = random_scene(rng, n, plane, lr, sky=seed % 2 == 0)
+    cam = rt.Camera(position=(rng.uniform(-1, 1), rng.uniform(0.5, 2.5), -5.0), yaw=rng.uniform(-0.3, 0.3),
+                    pitch=rng.uniform(-0.3, 0.1), fov=rng.uniform(40, 90))
+    params = rt.RenderParams(samples, bounces, 120, 68)
+    cull = render(scene, cam, params, "fp32", "cull")
+    wave = render(scene, cam, params, "fp32", "wave")
+    np.testing.assert_array_equal(cull, wave)
+
+
+@pytest.mark.parametrize("seed,n,samples,bounces,plane,lr", CASES[:6])
+def test_fp64_culled_equals_literal_and_oracle(seed, n, samples, bounces, plane, lr):
+    rng = np.random.default_rng(100 + seed)
+    scene = random_scene(rng, n, plane, lr, sky=seed % 2 == 1)
+    cam = rt.Camera(position=(rng.uniform(-1, 1), rng.uniform(0.5, 2.5), -5.0), yaw=rng.uniform(-0.3, 0.3),
+                    pitch=rng.uniform(-0.3, 0.1), fov=rng.uniform(40, 90))
+    w, h = (64, 36) if samples > 1000 else (96, 54)
+    params = rt.RenderParams(samples, bounces, w, h)
+    culled = render(scene, cam, params, "fp64", "cull")
+    literal = render(scene, cam, params, "fp64", "mega")
+    np.testing.assert_array_equal(culled, literal)
+    ps = rt.pack_scene(scene)
+    want = oracle.render(vars(ps), cam.position, cam.yaw, cam.pitch, cam.fov, w, h, samples, bounces)
+    np.testing.assert_array_equal(culled, want)

@@ -129,6 +129,7 @@ class Context:
         self.handle = h
         self._registered = {}  # id(array) -> array (kept alive while pinned)
         self._reg_order = []
+        self._addr = {}  # id(array) -> data address of a pinned array
 
     def close(self):
         if getattr(self, "handle", None):
@@ -156,13 +157,22 @@ class Context:
         if lib.rt_host_register(self.handle, ptr(arr), arr.nbytes) != RT_OK:
             return False
         self._registered[key] = arr
+        self._addr[key] = arr.__array_interface__["data"][0]
         self._reg_order.append(key)
         while len(self._reg_order) > max_pinned:
             old = self._reg_order.pop(0)
             a = self._registered.pop(old, None)
+            self._addr.pop(old, None)
             if a is not None:
                 lib.rt_host_unregister(self.handle, ptr(a))
         return True
+
+    def address(self, arr: np.ndarray) -> int:
+        """Device-visible host address of `arr` (cached for pinned framebuffers)."""
+        hit = self._registered.get(id(arr))
+        if hit is arr:
+            return self._addr[id(arr)]
+        return arr.__array_interface__["data"][0]
 
     def set_option(self, name: str, value) -> None:
         check(load().rt_set_option(self.handle, name.encode(), int(value)), "rt_set_option")

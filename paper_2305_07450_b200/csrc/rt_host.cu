@@ -652,8 +652,11 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
             return RT_OK;
         }
         cudaGetLastError();  // not registered: a cudaHostGetDevicePointer miss is not an error
-        // (a band costs ~5 kernel boundaries; below ~16 MB that outweighs the hidden copy)
-        int bands = ctx->bands > 0 ? ctx->bands : (px_bytes >= ((size_t)16 << 20) ? 4 : 1);
+        // A band adds ~8-15 us of kernel boundaries and tails; the copy it hides
+        // runs at ~45 GB/s (82 us for 720p).  Measured best (tools/e2e_bands.py):
+        // 2 bands at 3.7 MB, 3 at 8.3 MB, 4 at 33 MB.
+        const size_t MB = (size_t)1 << 20;
+        int bands = ctx->bands > 0 ? ctx->bands : px_bytes < MB ? 1 : px_bytes < 6 * MB ? 2 : px_bytes < 16 * MB ? 3 : 4;
         bands = std::max(1, std::min(bands, height / 8));
         const int band_rows = (height + bands - 1) / bands;
         RT_CK(cudaEventRecord(d.e0, d.st));

@@ -216,37 +216,57 @@ class PackedScene:
         return int(self.kinds.shape[0])
 
 
+def _address(a: np.ndarray) -> int:
+    return a.__array_interface__["data"][0]
+
+
+_NO_SKY_ADDR = _address(_NO_SKY)
+_sky_addr = {}  # id(texels) -> (texels, address): skyboxes are re-packed every frame
+
+
 def pack_scene(scene) -> PackedScene:
-    """Pack any object with the reference Scene's attributes (duck-typed)."""
+    """Pack any object with the reference Scene's attributes (duck-typed).
+
+    The float64 columns are views of ONE buffer (positions | sizes | colors |
+    refls | light position | light colour) so the C-ABI pointers come from a
+    single address lookup: the reference re-packs the scene every frame
+    (renderer.py:331), and so does render_frame here."""
     bodies = scene.bodies
     n = len(bodies)
-    if n:
-        rows = [
-            (float(b.position[0]), float(b.position[1]), float(b.position[2]), float(b.size),
-             float(b.color[0]), float(b.color[1]), float(b.color[2]), float(b.reflectivity))
-            for b in bodies
-        ]
-        table = np.array(rows, dtype=np.float64)
-        kinds = np.array([int(b.kind) for b in bodies], dtype=np.int32)
-    else:
-        table = np.zeros((0, 8), dtype=np.float64)
-        kinds = np.zeros(0, dtype=np.int32)
     light = scene.light
+    lp, lc = light.position, light.color
+    flat = [b.position[i] for b in bodies for i in (0, 1, 2)]
+    flat += [b.size for b in bodies]
+    flat += [b.color[i] for b in bodies for i in (0, 1, 2)]
+    flat += [b.reflectivity for b in bodies]
+    flat += (lp[0], lp[1], lp[2], lc[0], lc[1], lc[2])
+    buf = np.array(flat, dtype=np.float64)
+    if buf.shape != (8 * n + 6,):
+        raise ValueError("body positions and colours must be 3-vectors of numbers")
+    kinds = np.array([int(b.kind) for b in bodies], dtype=np.int32)
     sky = getattr(scene, "skybox", None)
     if sky is None:
-        texels, sw, sh, has = _NO_SKY, 1, 1, False
+        texels, sw, sh, has, sky_addr = _NO_SKY, 1, 1, False, _NO_SKY_ADDR
     else:
         texels = np.ascontiguousarray(sky.texels, dtype=np.float32)
         sw, sh, has = int(sky.width), int(sky.height), True
-    return PackedScene(
+        hit = _sky_addr.get(id(texels))
+        if hit is not None and hit[0] is texels:
+            sky_addr = hit[1]
+        else:
+            if len(_sky_addr) > 16:
+                _sky_addr.clear()
+            sky_addr = _address(texels)
+            _sky_addr[id(texels)] = (texels, sky_addr)
+    ps = PackedScene(
         kinds=kinds,
-        positions=np.ascontiguousarray(table[:, 0:3]),
-        sizes=np.ascontiguousarray(table[:, 3]),
-        colors=np.ascontiguousarray(table[:, 4:7]),
-        refls=np.ascontiguousarray(table[:, 7]),
-        light_pos=np.array(light.position, dtype=np.float64),
+        positions=buf[0:3 * n].reshape(n, 3),
+        sizes=buf[3 * n:4 * n],
+        colors=buf[4 * n:7 * n].reshape(n, 3),
+        refls=buf[7 * n:8 * n],
+        light_pos=buf[8 * n:8 * n + 3],
         light_radius=float(light.radius),
-        light_color=np.array(light.color, dtype=np.float64),
+        light_color=buf[8 * n + 3:8 * n + 6],
         ambient=float(scene.ambient),
         max_refl=float(scene.max_reflectivity),
         sky=texels,
@@ -254,6 +274,11 @@ def pack_scene(scene) -> PackedScene:
         sky_h=sh,
         has_sky=has,
     )
+    base = _address(buf)
+    # C-ABI scene arguments of rt_render_v1 / rt_trace_rays_v1 / rt_stream_* (b200rt.h)
+    ps.argv = (n, _address(kinds), base, base + 24 * n, base + 32 * n, base + 56 * n, base + 64 * n,
+               ps.light_radius, base + 64 * n + 24, ps.ambient, ps.max_refl, sky_addr, sw, sh, int(has))
+    return ps
 
 
 def camera_viewport_distance(fov_degrees: float) -> float:

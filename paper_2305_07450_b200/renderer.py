@@ -24,6 +24,7 @@ bit for bit.
 
 from __future__ import annotations
 
+import ctypes
 import os
 
 import numpy as np
@@ -57,6 +58,9 @@ def _prec(precision) -> int:
 
 
 def _scene_argv(ps):
+    argv = getattr(ps, "argv", None)
+    if argv is not None:  # pack_scene's precomputed addresses
+        return argv
     P = _native.ptr
     return [
         ps.n_bodies, P(ps.kinds), P(ps.positions), P(ps.sizes), P(ps.colors), P(ps.refls), P(ps.light_pos),
@@ -104,10 +108,11 @@ def render_frame(scene, cam, params, out, workers=None, *, precision=None, radia
     if pixels.nbytes >= _PIN_MIN_BYTES:
         ctx.pin(pixels)
     ps = pack_scene(scene)
-    cam_pos = np.array(cam.position, dtype=np.float64)
+    cp = cam.position
+    cam_pos = (ctypes.c_double * 3)(cp[0], cp[1], cp[2])
     rc = _native.load().rt_render_v1(
-        ctx.handle, _native.ptr(pixels), _native.ptr(radiance), int(params.width), int(params.height),
-        _native.ptr(cam_pos), float(cam.yaw), float(cam.pitch), camera_viewport_distance(cam.fov),
+        ctx.handle, ctx.address(pixels), _native.ptr(radiance), int(params.width), int(params.height),
+        cam_pos, float(cam.yaw), float(cam.pitch), camera_viewport_distance(cam.fov),
         *_scene_argv(ps), int(params.shadow_samples), int(params.bounce_limit), n_parts, prec,
     )
     _native.check(rc, "rt_render_v1")

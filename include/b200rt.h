@@ -125,11 +125,16 @@ int rt_sky_sample_v1(rt_ctx *ctx, const double *dirs, int64_t n, double *out_rgb
 int rt_host_register(rt_ctx *ctx, void *ptr, size_t bytes);
 int rt_host_unregister(rt_ctx *ctx, void *ptr);
 
-/* Execution options of ctx (all default on except count_work):
+/* Execution options of ctx (default on: wave, cull, conic; the rest off):
  *   "wave"        FP32 soft shadows (samples >= 8) run as trace / shadow /
  *                 shade kernels over HBM queues instead of one megakernel;
  *   "cull"        the wavefront shadow pass skips, per hit, the bodies that
  *                 provably cannot block any of its shadow rays (exact);
+ *   "conic"       the culled pass tests a penumbra sphere against the disc
+ *                 samples in its silhouette form (six coefficients per hit
+ *                 and sphere, a quadratic per sample) instead of one ray per
+ *                 sample — the reference's predicate, FP32 rounding near the
+ *                 silhouette (off: the ray form, bit-identical to "cull" 0);
  *   "count_work"  tally the executed work of the culled pass (rt_work_counts);
  *   "bands"       rt_render_v1 on one device renders this many contiguous row
  *                 bands (1-4) and copies each to the host while the next
@@ -147,8 +152,10 @@ int rt_host_unregister(rt_ctx *ctx, void *ptr);
  *                 slower end to end on B200 (PCIe writes of 32-byte rows
  *                 stall the kernels), so the staged copy is the default. */
 int rt_set_option(rt_ctx *ctx, const char *name, int32_t value);
-/* Executed-work tallies since the last reset: hits, per-hit cull tests, hits
- * that sampled, shadow rays traced, sphere tests, plane tests. */
+/* Executed-work tallies since the last reset (option "count_work"), in this
+ * order: hits, per-hit cull tests, hits that sampled, shadow rays, sphere
+ * tests, plane tests, bundle-traced rays, their sphere tests, warps whose
+ * bundle did not cull, hits sampled in the silhouette form. */
 int rt_work_counts(rt_ctx *ctx, uint64_t *out, int32_t n, int32_t reset);
 
 /* Device time (CUDA events) of the render kernels of the last rt_render_v1 /

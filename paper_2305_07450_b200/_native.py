@@ -178,10 +178,10 @@ class Context:
         check(load().rt_set_option(self.handle, name.encode(), int(value)), "rt_set_option")
 
     def work_counts(self, reset: bool = True) -> dict:
-        arr = (ctypes.c_uint64 * 9)()
-        check(load().rt_work_counts(self.handle, arr, 9, int(reset)), "rt_work_counts")
+        arr = (ctypes.c_uint64 * 10)()
+        check(load().rt_work_counts(self.handle, arr, 10, int(reset)), "rt_work_counts")
         keys = ("hits", "cull_tests", "sampled_hits", "shadow_rays", "sphere_tests", "plane_tests", "trace_rays",
-                "trace_tests", "trace_unculled_warps")
+                "trace_tests", "trace_unculled_warps", "conic_hits")
         return dict(zip(keys, (int(v) for v in arr)))
 
     def last_kernel_ms(self) -> float:
@@ -207,7 +207,7 @@ _options = {}  # execution options applied to every context (rt_set_option)
 
 def set_options(**opts) -> None:
     """Execution options for every context, present and future:
-    wave (bool), cull (bool), count_work (bool), bands (0-4) — see
+    wave (bool), cull (bool), conic (bool), count_work (bool), bands (0-4) — see
     include/b200rt.h (rt_set_option)."""
     with _ctx_lock:
         _options.update({k: int(v) for k, v in opts.items()})

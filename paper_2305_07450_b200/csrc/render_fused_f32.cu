@@ -74,6 +74,41 @@ __device__ __forceinline__ int classify_hit(const ParamScene<MAXS> &ps, const Co
     return any ? 1 : 0;
 }
 
+// The silhouette form for queue entry e (rt_wave.cuh, conic_coeffs): when
+// every candidate is a sphere (at most kConic) whose preconditions hold, sphere
+// j's coefficients go to wa.conic[2j][e], [2j+1][e] and qp becomes
+// {|lo|^2, 2 lo.bu, 2 lo.bv, record slot}.  Returns the entry code
+//   spheres | z-tested spheres << 3 | spheres with z0 = -1 << 7
+// or 0 (qp untouched: the sampler takes the ray form).
+template <int MAXS>
+__device__ __forceinline__ int conic_entry(const ParamScene<MAXS> &ps, const WaveArgs &wa, unsigned e,
+                                           const unsigned *mask, float4 &qp, float4 qn, float3 light,
+                                           float light_radius) {
+    constexpr int kWords = (MAXS + 31) / 32;
+    if (mask[kWords] != 0) return 0;  // a plane candidate
+    int nc = 0;
+#pragma unroll
+    for (int w = 0; w < kWords; w++) nc += __popc(mask[w]);
+    if (nc > kConic) return 0;
+    // the hit's shadow frame exactly as the sampler forms it (shadow_frame)
+    const ShadowFrame f = shadow_frame(f3(qp.x, qp.y, qp.z), f3(qn.x, qn.y, qn.z), light, true);
+    const Cone k = make_cone(f.origin, light, light_radius);
+    int j = 0, code = nc;
+    for (int w = 0; w < kWords; w++) {
+        for (unsigned m = mask[w]; m; m &= m - 1, j++) {
+            float4 ca, cb;
+            const int r = conic_coeffs(k, ps.sph[w * 32 + __ffs(m) - 1], f.lo, f.bu, f.bv, f.ls2, ca, cb);
+            if (r == 0) return 0;
+            if (r >= 2) code |= 1 << (3 + j);
+            if (r == 3) code |= 1 << (7 + j);
+            wa.conic[(size_t)(2 * j) * wa.conic_cap + e] = ca;
+            wa.conic[(size_t)(2 * j + 1) * wa.conic_cap + e] = cb;
+        }
+    }
+    qp = make_float4(dot3(f.lo, f.lo), 2.f * dot3(f.lo, f.bu), 2.f * dot3(f.lo, f.bv), qp.w);
+    return code;
+}
+
 // --- A ----------------------------------------------------------------------------
 template <int MAXS>
 __global__ void __launch_bounds__(kThreads)
@@ -237,6 +272,9 @@ __global__ void __launch_bounds__(kThreads)
             if (need) {
                 // compact queue entry: everything the sampler needs, no indirection
                 const unsigned e = base + __popc(nb & lanemask_lt());
+                int code = 0;
+                if (e < wa.conic_cap) code = conic_entry(ps, wa, e, mask, qp, qn, light, sa.light_radius);
+                qn.w = __int_as_float(code);
                 wa.hit_p[e] = qp;
                 wa.hit_n[e] = qn;
 #pragma unroll
@@ -355,6 +393,88 @@ __device__ __forceinline__ int sample_hit(const ParamScene<MAXS> &ps, const Shad
     return unblocked;
 }
 
+// Sampling of one silhouette-form hit (conic_entry): P = {|lo|^2, 2 lo.bu,
+// 2 lo.bv, slot}, sphere j's coefficients C[2j], C[2j+1] (the first sphere's
+// arrive prefetched).  Returns the unblocked count of this lane's samples.
+template <bool SMEM_TAB>
+__device__ __forceinline__ int sample_conic(const WaveArgs &wa, unsigned e, int code, float4 P, float4 A0, float4 B0,
+                                            int n, const float4 *gtab) {
+    const int lane = threadIdx.x & 31;
+    auto table = [&](int i) -> float4 {
+        if constexpr (SMEM_TAB) {
+            extern __shared__ float4 smem_tab_c[];
+            return smem_tab_c[i];
+        } else {
+            return __ldg(gtab + i);
+        }
+    };
+    const int ncon = code & 7;
+    const int full = n >> 5;
+    int unblocked = 0;
+    auto run = [&](auto open) {
+#pragma unroll 4
+        for (int j = 0; j < full; j++) unblocked += open(table(lane + 32 * j));
+        if (lane + 32 * full < n) unblocked += open(table(lane + 32 * full));
+    };
+    if (ncon == 1 && !(code & (1 << 3))) {  // one sphere wholly in front: the common penumbra
+        run([&](float4 t) -> int {
+            const float w2 = fmaf(P.y, t.x, fmaf(P.z, t.y, P.x + t.z));
+            const float x = fmaf(A0.y, t.x, fmaf(A0.z, t.y, A0.x));
+            const float y = fmaf(B0.x, t.x, fmaf(B0.y, t.y, A0.w));
+            return fmaf(x, x, y * y) < w2 ? 0 : 1;
+        });
+        return unblocked;
+    }
+    if (ncon == 1) {  // one sphere straddling o's horizon: the self-shadowing terminator
+        const float z0 = (code & (1 << 7)) ? -1.f : 1.f;
+        run([&](float4 t) -> int {
+            const float w2 = fmaf(P.y, t.x, fmaf(P.z, t.y, P.x + t.z));
+            const float x = fmaf(A0.y, t.x, fmaf(A0.z, t.y, A0.x));
+            const float y = fmaf(B0.x, t.x, fmaf(B0.y, t.y, A0.w));
+            const float z = fmaf(B0.z, t.x, fmaf(B0.w, t.y, z0));
+            return (fmaf(x, x, y * y) < w2 && z > 0.f) ? 0 : 1;
+        });
+        return unblocked;
+    }
+    float4 A[kConic], B[kConic];
+    float Z[kConic];
+    A[0] = A0;
+    B[0] = B0;
+#pragma unroll
+    for (int j = 1; j < kConic; j++) {
+        if (j < ncon) {
+            A[j] = __ldg(wa.conic + (size_t)(2 * j) * wa.conic_cap + e);
+            B[j] = __ldg(wa.conic + (size_t)(2 * j + 1) * wa.conic_cap + e);
+        } else {  // never blocks: x^2 + y^2 = +inf
+            A[j] = make_float4(INFINITY, 0.f, 0.f, 0.f);
+            B[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kConic; j++) Z[j] = (code & (1 << (7 + j))) ? -1.f : 1.f;  // no z test: z = 1
+    auto blocked_by = [&](int j, float4 t, float w2) -> bool {
+        const float x = fmaf(A[j].y, t.x, fmaf(A[j].z, t.y, A[j].x));
+        const float y = fmaf(B[j].x, t.x, fmaf(B[j].y, t.y, A[j].w));
+        const float z = fmaf(B[j].z, t.x, fmaf(B[j].w, t.y, Z[j]));
+        return fmaf(x, x, y * y) < w2 && z > 0.f;
+    };
+    if (ncon == 2) {
+        run([&](float4 t) -> int {
+            const float w2 = fmaf(P.y, t.x, fmaf(P.z, t.y, P.x + t.z));
+            return (blocked_by(0, t, w2) || blocked_by(1, t, w2)) ? 0 : 1;
+        });
+        return unblocked;
+    }
+    run([&](float4 t) -> int {
+        const float w2 = fmaf(P.y, t.x, fmaf(P.z, t.y, P.x + t.z));
+        bool b = false;
+#pragma unroll
+        for (int j = 0; j < kConic; j++) b |= blocked_by(j, t, w2);
+        return b ? 0 : 1;
+    });
+    return unblocked;
+}
+
 template <int MAXS, bool SMEM_TAB>
 __global__ void __launch_bounds__(kThreads)
     fused_sample(const FrameArgs fa, const SceneArgs<float> sa, const WaveArgs wa, const ParamScene<MAXS> ps) {
@@ -375,29 +495,41 @@ __global__ void __launch_bounds__(kThreads)
     const unsigned n_warps = (gridDim.x * blockDim.x) >> 5;
     const float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
     // the next hit's queue entry is loaded while the current one samples
-    float4 P, N;
+    float4 P, N, A0 = make_float4(0.f, 0.f, 0.f, 0.f), B0 = A0;
     unsigned hm[kWords + 1];
     auto fetch = [&](unsigned h) {
         P = __ldg(wa.hit_p + h);
         N = __ldg(wa.hit_n + h);
 #pragma unroll
         for (int w = 0; w <= kWords; w++) hm[w] = __ldg(wa.mask2 + (size_t)w * wa.mask2_stride + h);
+        if (h < wa.conic_cap) {  // the first silhouette sphere, should the entry have one
+            A0 = __ldg(wa.conic + h);
+            B0 = __ldg(wa.conic + wa.conic_cap + h);
+        }
     };
     if (warp < count) fetch(warp);
     for (unsigned h = warp; h < count; h += n_warps) {
-        const float4 Pc = P, Nc = N;
+        const float4 Pc = P, Nc = N, A0c = A0, B0c = B0;
         unsigned hmc[kWords + 1];
 #pragma unroll
         for (int w = 0; w <= kWords; w++) hmc[w] = hm[w];
         if (h + n_warps < count) fetch(h + n_warps);
         const int slot = __float_as_int(Pc.w);
-        const ShadowFrame f = shadow_frame(f3(Pc.x, Pc.y, Pc.z), f3(Nc.x, Nc.y, Nc.z), lp, true);
+        const int code = __float_as_int(Nc.w);
         int nsph = 0;
-        int unblocked = sample_hit<MAXS, SMEM_TAB>(ps, f, hmc, n, gtab, nsph);
+        int unblocked;
+        if (code != 0) {
+            unblocked = sample_conic<SMEM_TAB>(wa, h, code, Pc, A0c, B0c, n, gtab);
+            nsph = code & 7;
+        } else {
+            const ShadowFrame f = shadow_frame(f3(Pc.x, Pc.y, Pc.z), f3(Nc.x, Nc.y, Nc.z), lp, true);
+            unblocked = sample_hit<MAXS, SMEM_TAB>(ps, f, hmc, n, gtab, nsph);
+        }
         unblocked = __reduce_add_sync(0xffffffffu, unblocked);
         if (lane != 0) continue;
         reinterpret_cast<float *>(wa.rec + slot)[3] = (float)unblocked / (float)n;
         if (wa.work) {
+            if (code != 0) atomicAdd(wa.work + kWorkConicHits, 1ull);
             atomicAdd(wa.work + kWorkSampledHits, 1ull);
             atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);
             atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n * nsph);

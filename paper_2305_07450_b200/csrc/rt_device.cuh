@@ -77,6 +77,8 @@ struct WaveArgs {
     int64_t n_pix;     // pixels of this partition (local_rows * width)
     unsigned long long *work;  // optional executed-work tallies of the culled path (kWork*), or null
     int cull;          // exact per-hit occluder culling in the shadow kernel
+    float4 *conic;     // culled path: silhouette coefficients of queued hits, [2 kConic][conic_cap]
+    unsigned conic_cap;  // queue positions below this may take the silhouette form (0: off)
 };
 // FP64 culled wavefront (render_fused_f64.cu): queues in float64
 constexpr int kMaxBodies64 = 256;
@@ -93,10 +95,11 @@ struct WaveArgs64 {
 
 // executed-work tallies of the culled shadow kernel (rt_work_counts)
 enum { kWorkHits = 0, kWorkCullTests, kWorkSampledHits, kWorkShadowRays, kWorkSphereTests, kWorkPlaneTests,
-       kWorkTraceRays, kWorkTraceTests, kWorkTraceFullWarps, kWorkN };
+       kWorkTraceRays, kWorkTraceTests, kWorkTraceFullWarps, kWorkConicHits, kWorkN };
 constexpr int kParamSpheres = 256;  // scenes up to this many spheres ride in the launch parameters
 constexpr int kMaskWords = kParamSpheres / 32;
 constexpr int kWaveMinSamples = 8;     // soft shadows at or above this take the wavefront path
+constexpr int kConic = 4;             // silhouette-form spheres per queued hit (rt_wave.cuh; more: the ray form)
 constexpr int kWaveSmemSamples = 2048;  // disc tables (16 B/sample) up to this size are staged in shared memory
 
 // Row-block interleave: local row ly of partition `part` -> frame row.

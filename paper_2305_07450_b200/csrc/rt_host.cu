@@ -87,7 +87,7 @@ struct Dev {
     cudaEvent_t band_ev[4] = {nullptr, nullptr, nullptr, nullptr};
     bool ph_valid = false;
     DBuf frame, rad, rays_in, rays_out, sky_raw, sky, counters;
-    DBuf w_p, w_n, w_s, w_sc, w_queue, w_queue2, w_mask2, w_count, w_pix, w_work, w_rec, w_pending;
+    DBuf w_p, w_n, w_s, w_sc, w_queue, w_queue2, w_mask2, w_count, w_pix, w_work, w_rec, w_pending, w_conic;
     DBuf d_q, d_mask, d_pix, d_rec, d_parked;  // FP64 culled wavefront queues  // wavefront queues (FP32 soft shadows)
     unsigned counter_slot = 0;
     uint64_t sky_version = ~0ull;
@@ -141,6 +141,7 @@ struct rt_ctx {
     int bands = 0;            // single-device row bands for copy overlap (0: by frame size)
     bool phases = false;      // record per-phase events in wavefront frames (rt_phase_ms)
     int rgba = 0;             // pixel byte order of the frames written (0 B,G,R,A / 1 R,G,B,A)
+    bool conic = true;        // culled FP32 path: silhouette form of the soft-shadow sphere test
     bool zero_copy = false;   // kernels store straight into a registered (mapped) host framebuffer
     std::mutex mu;
     HostScene scene;
@@ -450,6 +451,11 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
                 (rc = d.w_rec.ensure(sizeof(float4) * slots)) ||
                 (rc = d.w_pending.ensure(sizeof(int) * (size_t)wa.n_pix)))  // queue3
                 return rc;
+            if (ctx->conic) {  // silhouette coefficients for the first n_pix queued hits
+                if ((rc = d.w_conic.ensure(sizeof(float4) * 2 * rt::kConic * (size_t)wa.n_pix))) return rc;
+                wa.conic = (float4 *)d.w_conic.p;
+                wa.conic_cap = (unsigned)wa.n_pix;
+            }
         } else {
             if ((rc = d.w_s.ensure(sizeof(float) * slots)) || (rc = d.w_sc.ensure(sizeof(float) * slots)) ||
                 (rc = d.w_queue.ensure(sizeof(int) * slots)))
@@ -562,7 +568,7 @@ int rt_ctx_destroy(rt_ctx *ctx) {
         cudaSetDevice(d.id);
         if (d.st) cudaStreamSynchronize(d.st);
         for (DBuf *b : {&d.w_p, &d.w_n, &d.w_s, &d.w_sc, &d.w_queue, &d.w_queue2, &d.w_mask2, &d.w_count, &d.w_pix,
-                        &d.w_work, &d.w_rec, &d.w_pending, &d.d_q, &d.d_mask, &d.d_pix, &d.d_rec, &d.d_parked})
+                        &d.w_work, &d.w_rec, &d.w_pending, &d.w_conic, &d.d_q, &d.d_mask, &d.d_pix, &d.d_rec, &d.d_parked})
             b->release();
         for (DBuf *b : {&d.frame, &d.rad, &d.rays_in, &d.rays_out, &d.sky_raw, &d.sky, &d.counters, &d.s32.geo, &d.s32.mat,
                         &d.s32.table, &d.s64.geo, &d.s64.mat, &d.s64.table})
@@ -887,6 +893,7 @@ int rt_set_option(rt_ctx *ctx, const char *name, int32_t value) {
     else if (n == "phases") ctx->phases = value != 0;
     else if (n == "rgba") ctx->rgba = value != 0;
     else if (n == "zero_copy") ctx->zero_copy = value != 0;
+    else if (n == "conic") ctx->conic = value != 0;
     else return fail(RT_ERR_INVALID, "unknown option " + n);
     return RT_OK;
 }

@@ -141,6 +141,67 @@ __device__ __forceinline__ bool bound_meets_cone(const Cone &k, float4 B) {
     return u2 < rp * rp;
 }
 
+// --- the silhouette form of the soft-shadow sphere test ----------------------
+//
+// For one hit the shadow rays run from o along w_i = lo + a_i bu + b_i bv
+// (lo = L - o, disc basis bu, bv: shading.py:76-100) and a sphere (centre c,
+// u = c - o) blocks sample i iff tca > 0, d2 < r^2 + GRAZE and its entry
+// distance is below the limit (geometry.py:94-106, renderer.py:100-103).
+// With the origin clearly outside the sphere and |u| < |p - L| (checked once
+// per hit and sphere), entry <= tca <= |u| < limit for every sample, so
+// only tca > 0 and d2 decide, and
+//   d2 = |u x w|^2 / |w|^2 = |u|^2 ((e1.w)^2 + (e2.w)^2) / |w|^2,
+//   tca > 0  <=>  n.w > 0      (n = u / |u|, e1, e2 orthonormal, perpendicular to n).
+// Every dot product is affine in the disc coordinates (a, b) and |w|^2 =
+// |lo|^2 + 2a lo.bu + 2b lo.bv + a^2 + b^2, so with s = |u| / sqrt(r^2 + GRAZE)
+//   blocked_i  <=>  x_i^2 + y_i^2 < |w_i|^2  and  z_i > 0,
+//   x_i = s e1.lo + a_i s e1.bu + b_i s e1.bv   (y likewise with e2),
+//   z_i = sign(n.lo) + a_i n.bu / |n.lo| + b_i n.bv / |n.lo|:
+// coefficients formed once per (hit, sphere), then a few FMAs per sample
+// instead of a normalised ray and a sphere test.  The z test is dropped when
+// every sample direction lies within 90 degrees of u (the cone bound below),
+// which leaves it to the self-shadowing terminator hits.  The predicate is the
+// reference's on the same real numbers; only FP32 rounding near the
+// silhouette differs, of the same order as the ray form's (which also forms
+// d2 as a squared perpendicular).  Near z = 0 the rounding of z cannot
+// matter: there d2 ~ |u|^2 > r^2 + GRAZE, so the sample is open either way.
+//
+// Returns 0 (a precondition fails: the hit takes the ray form), 1 (no z test
+// needed), 2 (z test, z0 = +1) or 3 (z test, z0 = -1); c = {x0, x1, x2, y0},
+// {y1, y2, z1, z2}.
+__device__ __forceinline__ int conic_coeffs(const Cone &k, float4 g, float3 lo, float3 bu, float3 bv, float ls2,
+                                            float4 &ca, float4 &cb) {
+    if (!k.ok) return 0;
+    const float3 u = f3(g.x - k.o.x, g.y - k.o.y, g.z - k.o.z);
+    const float u2 = dot3(u, u);
+    const float r2g = g.w + kGraze;
+    if (!(u2 > r2g * (1.f + 4.f * kCullRel) + kCullAbs)) return 0;  // origin clearly outside
+    const float un = sqrtf(u2);
+    if (!(un * (1.f + kCullRel) + kCullAbs < sqrtf(ls2))) return 0;  // entry <= tca <= |u| < |p - L| <= limit
+    const float h = dot3(u, k.axis);
+    const float3 wp = u - k.axis * h;
+    const float q = sqrtf(dot3(wp, wp));
+    // every sample direction lies within phi of the axis: tca >= h cos(phi) - q sin(phi)
+    const bool front = h * k.cos_phi - q * k.sin_phi > kCullRel * (fabsf(h) + q) + kCullAbs;
+    const float3 n = u * (1.f / un);
+    // orthonormal pair perpendicular to n (branch-free, Duff et al. 2017)
+    const float sg = copysignf(1.f, n.z);
+    const float ia = -1.f / (sg + n.z);
+    const float bb = n.x * n.y * ia;
+    const float3 e1 = f3(1.f + sg * n.x * n.x * ia, sg * bb, -sg * n.x);
+    const float3 e2 = f3(bb, sg + n.y * n.y * ia, -n.y);
+    const float s = un * rsqrtf(r2g);
+    ca = make_float4(s * dot3(e1, lo), s * dot3(e1, bu), s * dot3(e1, bv), s * dot3(e2, lo));
+    cb = make_float4(s * dot3(e2, bu), s * dot3(e2, bv), 0.f, 0.f);
+    if (front) return 1;
+    const float z0 = dot3(n, lo);
+    if (!(fabsf(z0) > 1e-6f * (sqrtf(dot3(lo, lo)) + 1.f))) return 0;
+    const float iz = 1.f / fabsf(z0);
+    cb.z = dot3(n, bu) * iz;
+    cb.w = dot3(n, bv) * iz;
+    return z0 > 0.f ? 2 : 3;
+}
+
 // Planes: a shadow segment crosses y = hp iff o.y and its far end (within
 // 1e-3 of a disc point, whose height is within rho of L.y) straddle it.
 __device__ __forceinline__ int plane_class(const Cone &k, float oy, float ly, float hp) {

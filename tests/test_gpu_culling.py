@@ -2,7 +2,9 @@
 
 The culls (shadow-cone classification, cluster bounds, warp ray bundles) only
 skip tests that cannot change a result, so on any scene:
-  FP32: culled frame == unculled wavefront frame == megakernel frame, bit for bit;
+  FP32 (ray form): culled frame == unculled wavefront frame, bit for bit;
+  FP32 (silhouette form, the default): within the parity gates of the FP64
+      oracle, like every FP32 frame;
   FP64: culled frame == literal megakernel frame, bit for bit (and == the oracle).
 """
 
@@ -11,11 +13,13 @@ import pytest
 
 import oracle
 import paper_2305_07450_b200 as rt
+import parity
 from paper_2305_07450_b200 import _native
 
 pytestmark = pytest.mark.gpu
 
-MODES = {"cull": dict(wave=1, cull=1), "wave": dict(wave=1, cull=0), "mega": dict(wave=0, cull=0)}
+MODES = {"cull": dict(wave=1, cull=1, conic=1), "ray": dict(wave=1, cull=1, conic=0),
+         "wave": dict(wave=1, cull=0, conic=1), "mega": dict(wave=0, cull=0, conic=1)}
 
 
 def random_scene(rng, n_spheres, with_plane=True, light_radius=None, sky=False):
@@ -36,12 +40,15 @@ def random_scene(rng, n_spheres, with_plane=True, light_radius=None, sky=False):
     return s
 
 
-def render(scene, cam, params, precision, mode):
+def render(scene, cam, params, precision, mode, radiance=False):
     _native.set_options(**MODES[mode])
     try:
         fb = rt.Framebuffer.create(params.width, params.height)
-        rt.render_frame(scene, cam, params, fb, precision=precision)
-        return fb.pixels.copy()
+        rad = None
+        if radiance:
+            rad = np.zeros((params.width * params.height, 3), np.float32 if precision == "fp32" else np.float64)
+        rt.render_frame(scene, cam, params, fb, precision=precision, radiance=rad)
+        return (fb.pixels.copy(), rad) if radiance else fb.pixels.copy()
     finally:
         _native.set_options(**MODES["cull"])
 
@@ -66,9 +73,16 @@ def test_fp32_paths_bit_identical(seed, n, samples, bounces, plane, lr):
     cam = rt.Camera(position=(rng.uniform(-1, 1), rng.uniform(0.5, 2.5), -5.0), yaw=rng.uniform(-0.3, 0.3),
                     pitch=rng.uniform(-0.3, 0.1), fov=rng.uniform(40, 90))
     params = rt.RenderParams(samples, bounces, 120, 68)
-    cull = render(scene, cam, params, "fp32", "cull")
+    ray = render(scene, cam, params, "fp32", "ray")
     wave = render(scene, cam, params, "fp32", "wave")
-    np.testing.assert_array_equal(cull, wave)
+    np.testing.assert_array_equal(ray, wave)
+    # the silhouette form: the reference's predicate, FP32 rounding near silhouettes
+    px, rad = render(scene, cam, params, "fp32", "cull", radiance=True)
+    ps = rt.pack_scene(scene)
+    want, want_rad = oracle.render(vars(ps), cam.position, cam.yaw, cam.pitch, cam.fov, 120, 68, samples, bounces,
+                                   radiance=True)
+    parity.assert_byte_gate(px, want, f"silhouette seed {seed}")
+    parity.assert_radiance_gate(rad, want_rad, f"silhouette seed {seed}")
 
 
 @pytest.mark.parametrize("seed,n,samples,bounces,plane,lr", CASES[:6])

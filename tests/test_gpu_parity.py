@@ -23,10 +23,11 @@ pytestmark = pytest.mark.gpu
 
 CASES = [c["name"] for c in G.frame_cases()]
 
-# FP32 execution paths: wavefront + exact culling (default), wavefront without
+# FP32 execution paths: wavefront + exact culling with the silhouette-form
+# penumbra test (default), the same with the ray form, wavefront without
 # culling, and the one-thread-per-pixel megakernel
-MODES = {"cull": dict(wave=True, cull=True), "wave": dict(wave=True, cull=False),
-         "mega": dict(wave=False, cull=False)}
+MODES = {"cull": dict(wave=True, cull=True, conic=True), "ray": dict(wave=True, cull=True, conic=False),
+         "wave": dict(wave=True, cull=False), "mega": dict(wave=False, cull=False)}
 
 
 @pytest.fixture(params=list(MODES))
@@ -107,14 +108,18 @@ def test_fp32_frames_byte_and_radiance_gates(name, fp32_mode):
 
 def test_culled_path_is_exact_against_unculled():
     """Culling only skips bodies that cannot block: the culled FP32 frames
-    equal the unculled wavefront's bit for bit (same arithmetic per test)."""
+    (ray form) equal the unculled wavefront's bit for bit (same arithmetic per
+    test)."""
     for name in ("bench_128x72_s200_b3", "sweep_160x90_s16_b5_sky", "stress_96x54_s500_b8", "random4_64x36_s16_b4",
                  "c3like_192x108_s200_b3_sky", "blocked_32x18_s4_b1"):
         c = G.frame_case(name)
         _native.set_options(wave=True, cull=False)
         ref, rref = render_case(c, "fp32", radiance=True)
-        _native.set_options(wave=True, cull=True)
-        got, rgot = render_case(c, "fp32", radiance=True)
+        _native.set_options(wave=True, cull=True, conic=False)
+        try:
+            got, rgot = render_case(c, "fp32", radiance=True)
+        finally:
+            _native.set_options(**MODES["cull"])
         np.testing.assert_array_equal(got, ref, err_msg=name)
         np.testing.assert_array_equal(rgot, rref, err_msg=name)
 
@@ -305,7 +310,7 @@ def test_clustered_scene_modes_agree():
         rt.render_frame(s, cam, params, fb)
         frames[mode] = fb.pixels.copy()
     _native.set_options(**MODES["cull"])
-    np.testing.assert_array_equal(frames["cull"], frames["wave"])
+    np.testing.assert_array_equal(frames["ray"], frames["wave"])
     fb64 = rt.Framebuffer.create(160, 90)
     rt.render_frame(s, cam, params, fb64, precision="fp64")
     for mode, px in frames.items():

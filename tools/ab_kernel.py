@@ -20,14 +20,14 @@ def main():
     ap.add_argument("configs", nargs="*", default=["C2", "C4"])
     ap.add_argument("--frames", type=int, default=20)
     ap.add_argument("--precision", default="fp32")
-    ap.add_argument("--mode", default=None, help="cull | wave | mega")
+    ap.add_argument("--mode", default=None, help="cull | ray | wave | mega")
     ap.add_argument("--bands", type=int, default=1, help="row bands of rt_render_v1 (0 = by frame size)")
     a = ap.parse_args()
     tag = os.path.basename(_native.LIB_PATH)
     _native.set_options(bands=a.bands, phases=1)
     if a.mode:
-        _native.set_options(**{"cull": dict(wave=1, cull=1), "wave": dict(wave=1, cull=0),
-                               "mega": dict(wave=0, cull=0)}[a.mode])
+        _native.set_options(**{"cull": dict(wave=1, cull=1, conic=1), "ray": dict(wave=1, cull=1, conic=0),
+                               "wave": dict(wave=1, cull=0), "mega": dict(wave=0, cull=0)}[a.mode])
         tag += f"[{a.mode}]"
     for key in a.configs:
         cfg = rt.CONFIGS[key]

@@ -228,6 +228,8 @@ __global__ void __launch_bounds__(kThreads)
         int64_t slot = 0;
         unsigned mask[kWords + 1];
         float4 qp, qn;  // a queued hit's point (+ record slot) and normal
+        bool to_lane = false;
+        float4 lq0, lq1, lq2;  // its lane-sampler entry
         if (hit_now) {
             float3 hit = origin + dir * h.t;
             float3 normal = h.g.w >= 0.f ? normalize3(hit - f3(h.g.x, h.g.y, h.g.z)) : f3(0.f, 1.f, 0.f);
@@ -252,6 +254,24 @@ __global__ void __launch_bounds__(kThreads)
                 qp = make_float4(hit.x, hit.y, hit.z, __int_as_float((int)slot));
                 qn = make_float4(normal.x, normal.y, normal.z, 0.f);
                 npend++;
+                // one candidate sphere in the silhouette form: a lane of the lane sampler
+                if (wa.lane_cap && mask[kWords] == 0) {
+                    int nc = 0, b = 0;
+#pragma unroll
+                    for (int w = 0; w < kWords; w++) {
+                        if (mask[w]) b = w * 32 + __ffs(mask[w]) - 1;
+                        nc += __popc(mask[w]);
+                    }
+                    if (nc == 1) {
+                        const ShadowFrame f = shadow_frame(hit, normal, light, true);
+                        const int r = conic_coeffs(cone, ps.sph[b], f.lo, f.bu, f.bv, f.ls2, lq1, lq2);
+                        if (r != 0) {
+                            to_lane = true;
+                            lq0 = make_float4(dot3(f.lo, f.lo), 2.f * dot3(f.lo, f.bu), 2.f * dot3(f.lo, f.bv),
+                                              __int_as_float((int)slot | (r == 3 ? (int)0x80000000 : 0)));
+                        }
+                    }
+                }
             }
             m = k + 1;
             if (k == fa.bounces) {
@@ -262,8 +282,25 @@ __global__ void __launch_bounds__(kThreads)
                 dir = dir - normal * (2.f * dot3(normal, dir));
             }
         }
-        // queue the undecided hits: one atomic per warp and bounce
-        const bool need = hit_now && cls == 1;
+        // queue the undecided hits: one atomic per warp, bounce and queue
+        bool laned = false;
+        {
+            const bool want = hit_now && cls == 1 && to_lane;
+            const unsigned lb = __ballot_sync(0xffffffffu, want);
+            if (lb) {
+                unsigned base = 0;
+                if (lane == 0) base = atomicAdd(wa.count + 3, (unsigned)__popc(lb));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                const unsigned e = base + __popc(lb & lanemask_lt());
+                if (want && e < wa.lane_cap) {
+                    wa.lane_q[e] = lq0;
+                    wa.lane_q[wa.lane_cap + e] = lq1;
+                    wa.lane_q[2 * (size_t)wa.lane_cap + e] = lq2;
+                    laned = true;
+                }
+            }
+        }
+        const bool need = hit_now && cls == 1 && !laned;
         const unsigned nb = __ballot_sync(0xffffffffu, need);
         if (nb) {
             unsigned base = 0;
@@ -538,6 +575,68 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
+// --- B1: single-sphere silhouette hits, one lane each ------------------------------
+// Every lane of a warp takes the same disc sample at the same time (a shared-
+// memory broadcast) against its own hit's coefficients: no per-hit setup, no
+// reduction, no idle lanes but the grid's last warp.  The per-sample
+// expressions are sample_conic's, so the coefficient is the same bits.
+template <bool SMEM_TAB>
+__global__ void __launch_bounds__(kThreads)
+    fused_lanes(const FrameArgs fa, const SceneArgs<float> sa, const WaveArgs wa) {
+    const int n = fa.samples;
+    const float4 *gtab = reinterpret_cast<const float4 *>(sa.table);
+    extern __shared__ float4 smem_tab_l[];
+    if constexpr (SMEM_TAB) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) smem_tab_l[i] = gtab[i];
+        __syncthreads();
+    }
+    cudaGridDependencySynchronize();
+    auto table = [&](int i) -> float4 {
+        if constexpr (SMEM_TAB) {
+            return smem_tab_l[i];
+        } else {
+            return __ldg(gtab + i);
+        }
+    };
+    const unsigned count = min(wa.count[3], wa.lane_cap);
+    for (unsigned h = blockIdx.x * blockDim.x + threadIdx.x; h < count; h += gridDim.x * blockDim.x) {
+        const float4 P = __ldg(wa.lane_q + h);
+        const float4 A = __ldg(wa.lane_q + wa.lane_cap + h);
+        const float4 B = __ldg(wa.lane_q + 2 * (size_t)wa.lane_cap + h);
+        const int sw = __float_as_int(P.w);
+        const float z0 = sw < 0 ? -1.f : 1.f;
+        const bool needz = sw < 0 || B.z != 0.f || B.w != 0.f;
+        int unblocked = 0;
+        if (__any_sync(__activemask(), needz)) {
+#pragma unroll 4
+            for (int i = 0; i < n; i++) {
+                const float4 t = table(i);
+                const float w2 = fmaf(P.y, t.x, fmaf(P.z, t.y, P.x + t.z));
+                const float x = fmaf(A.y, t.x, fmaf(A.z, t.y, A.x));
+                const float y = fmaf(B.x, t.x, fmaf(B.y, t.y, A.w));
+                const float z = fmaf(B.z, t.x, fmaf(B.w, t.y, z0));
+                unblocked += (fmaf(x, x, y * y) < w2 && z > 0.f) ? 0 : 1;
+            }
+        } else {
+#pragma unroll 4
+            for (int i = 0; i < n; i++) {
+                const float4 t = table(i);
+                const float w2 = fmaf(P.y, t.x, fmaf(P.z, t.y, P.x + t.z));
+                const float x = fmaf(A.y, t.x, fmaf(A.z, t.y, A.x));
+                const float y = fmaf(B.x, t.x, fmaf(B.y, t.y, A.w));
+                unblocked += fmaf(x, x, y * y) < w2 ? 0 : 1;
+            }
+        }
+        reinterpret_cast<float *>(wa.rec + (sw & 0x7fffffff))[3] = (float)unblocked / (float)n;
+        if (wa.work) {
+            atomicAdd(wa.work + kWorkConicHits, 1ull);
+            atomicAdd(wa.work + kWorkSampledHits, 1ull);
+            atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);
+            atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n);
+        }
+    }
+}
+
 // --- C: the pixels that had undecided hits --------------------------------------------
 __global__ void __launch_bounds__(kThreads)
     fused_finish(const FrameArgs fa, const SceneArgs<float> sa, const WaveArgs wa) {
@@ -588,6 +687,15 @@ cudaError_t launch(const FrameArgs &fa, const SceneArgs<float> &sa, const WaveAr
         cudaEventRecord(ev[2], st);  // no separate classify pass: a zero-length phase
     }
     const int n = fa.samples;
+    if (wa.lane_cap) {
+        if (n <= kWaveSmemSamples) {
+            const size_t smem = sizeof(float4) * (size_t)n;
+            e = launch_pdl(fused_lanes<true>, resident_ctas(fused_lanes<true>, smem), smem, st, fa, sa, wa);
+        } else {
+            e = launch_pdl(fused_lanes<false>, resident_ctas(fused_lanes<false>, 0), 0, st, fa, sa, wa);
+        }
+        if (e != cudaSuccess) return e;
+    }
     if (n <= kWaveSmemSamples) {
         const size_t smem = sizeof(float4) * (size_t)n;
         e = launch_pdl(fused_sample<MAXS, true>, resident_ctas(fused_sample<MAXS, true>, smem), smem, st, fa, sa, wa,
@@ -625,7 +733,7 @@ cudaError_t rt_launch_fused_f32(const rt::FrameArgs &fa, const rt::SceneArgs<flo
     if (e != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[3], st);
     if ((e = launch_pdl(fused_finish, resident_ctas(fused_finish, 0), 0, st, fa, sa, wa)) != cudaSuccess) return e;
-    *n_kernels = 3;
+    *n_kernels = wa.lane_cap ? 4 : 3;
     if (ev) cudaEventRecord(ev[4], st);
     return cudaSuccess;
 }

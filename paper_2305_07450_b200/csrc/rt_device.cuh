@@ -79,6 +79,8 @@ struct WaveArgs {
     int cull;          // exact per-hit occluder culling in the shadow kernel
     float4 *conic;     // culled path: silhouette coefficients of queued hits, [2 kConic][conic_cap]
     unsigned conic_cap;  // queue positions below this may take the silhouette form (0: off)
+    float4 *lane_q;    // culled path: single-sphere silhouette hits, one lane each, [3][lane_cap]
+    unsigned lane_cap; // (0: off)
 };
 // FP64 culled wavefront (render_fused_f64.cu): queues in float64
 constexpr int kMaxBodies64 = 256;

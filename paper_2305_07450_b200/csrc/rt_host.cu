@@ -87,7 +87,7 @@ struct Dev {
     cudaEvent_t band_ev[4] = {nullptr, nullptr, nullptr, nullptr};
     bool ph_valid = false;
     DBuf frame, rad, rays_in, rays_out, sky_raw, sky, counters;
-    DBuf w_p, w_n, w_s, w_sc, w_queue, w_queue2, w_mask2, w_count, w_pix, w_work, w_rec, w_pending, w_conic;
+    DBuf w_p, w_n, w_s, w_sc, w_queue, w_queue2, w_mask2, w_count, w_pix, w_work, w_rec, w_pending, w_conic, w_lane;
     DBuf d_q, d_mask, d_pix, d_rec, d_parked;  // FP64 culled wavefront queues  // wavefront queues (FP32 soft shadows)
     unsigned counter_slot = 0;
     uint64_t sky_version = ~0ull;
@@ -455,6 +455,9 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
                 if ((rc = d.w_conic.ensure(sizeof(float4) * 2 * rt::kConic * (size_t)wa.n_pix))) return rc;
                 wa.conic = (float4 *)d.w_conic.p;
                 wa.conic_cap = (unsigned)wa.n_pix;
+                if ((rc = d.w_lane.ensure(sizeof(float4) * 3 * (size_t)wa.n_pix))) return rc;
+                wa.lane_q = (float4 *)d.w_lane.p;
+                wa.lane_cap = (unsigned)wa.n_pix;
             }
         } else {
             if ((rc = d.w_s.ensure(sizeof(float) * slots)) || (rc = d.w_sc.ensure(sizeof(float) * slots)) ||
@@ -568,7 +571,7 @@ int rt_ctx_destroy(rt_ctx *ctx) {
         cudaSetDevice(d.id);
         if (d.st) cudaStreamSynchronize(d.st);
         for (DBuf *b : {&d.w_p, &d.w_n, &d.w_s, &d.w_sc, &d.w_queue, &d.w_queue2, &d.w_mask2, &d.w_count, &d.w_pix,
-                        &d.w_work, &d.w_rec, &d.w_pending, &d.w_conic, &d.d_q, &d.d_mask, &d.d_pix, &d.d_rec, &d.d_parked})
+                        &d.w_work, &d.w_rec, &d.w_pending, &d.w_conic, &d.w_lane, &d.d_q, &d.d_mask, &d.d_pix, &d.d_rec, &d.d_parked})
             b->release();
         for (DBuf *b : {&d.frame, &d.rad, &d.rays_in, &d.rays_out, &d.sky_raw, &d.sky, &d.counters, &d.s32.geo, &d.s32.mat,
                         &d.s32.table, &d.s64.geo, &d.s64.mat, &d.s64.table})

@@ -228,8 +228,7 @@ __global__ void __launch_bounds__(kThreads)
         int64_t slot = 0;
         unsigned mask[kWords + 1];
         float4 qp, qn;  // a queued hit's point (+ record slot) and normal
-        bool to_lane = false;
-        float4 lq0, lq1, lq2;  // its lane-sampler entry
+        bool to_lane = false;  // qn.w: the candidate sphere's slot
         if (hit_now) {
             float3 hit = origin + dir * h.t;
             float3 normal = h.g.w >= 0.f ? normalize3(hit - f3(h.g.x, h.g.y, h.g.z)) : f3(0.f, 1.f, 0.f);
@@ -254,7 +253,7 @@ __global__ void __launch_bounds__(kThreads)
                 qp = make_float4(hit.x, hit.y, hit.z, __int_as_float((int)slot));
                 qn = make_float4(normal.x, normal.y, normal.z, 0.f);
                 npend++;
-                // one candidate sphere in the silhouette form: a lane of the lane sampler
+                // one candidate sphere: a lane of the lane sampler
                 if (wa.lane_cap && mask[kWords] == 0) {
                     int nc = 0, b = 0;
 #pragma unroll
@@ -263,13 +262,8 @@ __global__ void __launch_bounds__(kThreads)
                         nc += __popc(mask[w]);
                     }
                     if (nc == 1) {
-                        const ShadowFrame f = shadow_frame(hit, normal, light, true);
-                        const int r = conic_coeffs(cone, ps.sph[b], f.lo, f.bu, f.bv, f.ls2, lq1, lq2);
-                        if (r != 0) {
-                            to_lane = true;
-                            lq0 = make_float4(dot3(f.lo, f.lo), 2.f * dot3(f.lo, f.bu), 2.f * dot3(f.lo, f.bv),
-                                              __int_as_float((int)slot | (r == 3 ? (int)0x80000000 : 0)));
-                        }
+                        to_lane = true;
+                        qn.w = __int_as_float(b);
                     }
                 }
             }
@@ -293,9 +287,8 @@ __global__ void __launch_bounds__(kThreads)
                 base = __shfl_sync(0xffffffffu, base, 0);
                 const unsigned e = base + __popc(lb & lanemask_lt());
                 if (want && e < wa.lane_cap) {
-                    wa.lane_q[e] = lq0;
-                    wa.lane_q[wa.lane_cap + e] = lq1;
-                    wa.lane_q[2 * (size_t)wa.lane_cap + e] = lq2;
+                    wa.lane_q[e] = qp;
+                    wa.lane_q[wa.lane_cap + e] = qn;
                     laned = true;
                 }
             }
@@ -310,6 +303,7 @@ __global__ void __launch_bounds__(kThreads)
                 // compact queue entry: everything the sampler needs, no indirection
                 const unsigned e = base + __popc(nb & lanemask_lt());
                 int code = 0;
+                qn.w = 0.f;
                 if (e < wa.conic_cap) code = conic_entry(ps, wa, e, mask, qp, qn, light, sa.light_radius);
                 qn.w = __int_as_float(code);
                 wa.hit_p[e] = qp;
@@ -575,14 +569,17 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
-// --- B1: single-sphere silhouette hits, one lane each ------------------------------
+// --- B1: single-candidate hits, one lane each -------------------------------------
 // Every lane of a warp takes the same disc sample at the same time (a shared-
-// memory broadcast) against its own hit's coefficients: no per-hit setup, no
-// reduction, no idle lanes but the grid's last warp.  The per-sample
-// expressions are sample_conic's, so the coefficient is the same bits.
-template <bool SMEM_TAB>
+// memory broadcast) against its own hit: the per-hit setup (shadow frame,
+// silhouette coefficients) is one lane's, not a warp's, and there is no
+// reduction.  The per-sample expressions are sample_conic's (silhouette form)
+// and sample_hit's single-sphere loop (ray form, when a precondition fails),
+// so the coefficient is the same bits either sampler would produce.  Hits are
+// dealt warp-interleaved over the CTAs so that every SM gets a share.
+template <int MAXS, bool SMEM_TAB>
 __global__ void __launch_bounds__(kThreads)
-    fused_lanes(const FrameArgs fa, const SceneArgs<float> sa, const WaveArgs wa) {
+    fused_lanes(const FrameArgs fa, const SceneArgs<float> sa, const WaveArgs wa, const ParamScene<MAXS> ps) {
     const int n = fa.samples;
     const float4 *gtab = reinterpret_cast<const float4 *>(sa.table);
     extern __shared__ float4 smem_tab_l[];
@@ -598,20 +595,50 @@ __global__ void __launch_bounds__(kThreads)
             return __ldg(gtab + i);
         }
     };
+    const float3 light = f3(sa.light[0], sa.light[1], sa.light[2]);
     const unsigned count = min(wa.count[3], wa.lane_cap);
-    for (unsigned h = blockIdx.x * blockDim.x + threadIdx.x; h < count; h += gridDim.x * blockDim.x) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned stride = gridDim.x * blockDim.x;
+    // warp w of CTA c starts at hit 32 (w * gridDim + c): the first warps of all CTAs fill first
+    for (unsigned h = 32u * ((threadIdx.x >> 5) * gridDim.x + blockIdx.x) + lane; h < count; h += stride) {
         const float4 P = __ldg(wa.lane_q + h);
-        const float4 A = __ldg(wa.lane_q + wa.lane_cap + h);
-        const float4 B = __ldg(wa.lane_q + 2 * (size_t)wa.lane_cap + h);
-        const int sw = __float_as_int(P.w);
-        const float z0 = sw < 0 ? -1.f : 1.f;
-        const bool needz = sw < 0 || B.z != 0.f || B.w != 0.f;
+        const float4 N = __ldg(wa.lane_q + wa.lane_cap + h);
+        const int slot = __float_as_int(P.w);
+        const float4 g = ps.sph[__float_as_int(N.w)];
+        const ShadowFrame f = shadow_frame(f3(P.x, P.y, P.z), f3(N.x, N.y, N.z), light, true);
+        const Cone k = make_cone(f.origin, light, sa.light_radius);
+        float4 A, B;
+        const int r = conic_coeffs(k, g, f.lo, f.bu, f.bv, f.ls2, A, B);
+        const float b0 = dot3(f.lo, f.lo), b1 = 2.f * dot3(f.lo, f.bu), b2 = 2.f * dot3(f.lo, f.bv);
         int unblocked = 0;
-        if (__any_sync(__activemask(), needz)) {
+        const unsigned act = __activemask();
+        if (__any_sync(act, r == 0)) {
+            // some lane's hit needs the ray form: those lanes take it, the rest the silhouette
+            // form with the z test (a no-z hit has z1 = z2 = 0, z0 = 1)
+            const float3 L = f3(g.x - f.origin.x, g.y - f.origin.y, g.z - f.origin.z);
+            const float r2g = sphere_r2g(L, g.w);
+            const float z0 = r == 3 ? -1.f : 1.f;
+            for (int i = 0; i < n; i++) {
+                const float4 t = table(i);
+                if (r == 0) {
+                    float3 dir;
+                    float limit;
+                    shadow_ray_unguarded(f, t, dir, limit);
+                    unblocked += sphere_margin_L(L, dir, r2g, limit) > 0.f ? 0 : 1;
+                } else {
+                    const float w2 = fmaf(b1, t.x, fmaf(b2, t.y, b0 + t.z));
+                    const float x = fmaf(A.y, t.x, fmaf(A.z, t.y, A.x));
+                    const float y = fmaf(B.x, t.x, fmaf(B.y, t.y, A.w));
+                    const float z = fmaf(B.z, t.x, fmaf(B.w, t.y, z0));
+                    unblocked += (fmaf(x, x, y * y) < w2 && z > 0.f) ? 0 : 1;
+                }
+            }
+        } else if (__any_sync(act, r >= 2)) {
+            const float z0 = r == 3 ? -1.f : 1.f;
 #pragma unroll 4
             for (int i = 0; i < n; i++) {
                 const float4 t = table(i);
-                const float w2 = fmaf(P.y, t.x, fmaf(P.z, t.y, P.x + t.z));
+                const float w2 = fmaf(b1, t.x, fmaf(b2, t.y, b0 + t.z));
                 const float x = fmaf(A.y, t.x, fmaf(A.z, t.y, A.x));
                 const float y = fmaf(B.x, t.x, fmaf(B.y, t.y, A.w));
                 const float z = fmaf(B.z, t.x, fmaf(B.w, t.y, z0));
@@ -621,15 +648,15 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll 4
             for (int i = 0; i < n; i++) {
                 const float4 t = table(i);
-                const float w2 = fmaf(P.y, t.x, fmaf(P.z, t.y, P.x + t.z));
+                const float w2 = fmaf(b1, t.x, fmaf(b2, t.y, b0 + t.z));
                 const float x = fmaf(A.y, t.x, fmaf(A.z, t.y, A.x));
                 const float y = fmaf(B.x, t.x, fmaf(B.y, t.y, A.w));
                 unblocked += fmaf(x, x, y * y) < w2 ? 0 : 1;
             }
         }
-        reinterpret_cast<float *>(wa.rec + (sw & 0x7fffffff))[3] = (float)unblocked / (float)n;
+        reinterpret_cast<float *>(wa.rec + slot)[3] = (float)unblocked / (float)n;
         if (wa.work) {
-            atomicAdd(wa.work + kWorkConicHits, 1ull);
+            if (r != 0) atomicAdd(wa.work + kWorkConicHits, 1ull);
             atomicAdd(wa.work + kWorkSampledHits, 1ull);
             atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);
             atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n);
@@ -690,9 +717,11 @@ cudaError_t launch(const FrameArgs &fa, const SceneArgs<float> &sa, const WaveAr
     if (wa.lane_cap) {
         if (n <= kWaveSmemSamples) {
             const size_t smem = sizeof(float4) * (size_t)n;
-            e = launch_pdl(fused_lanes<true>, resident_ctas(fused_lanes<true>, smem), smem, st, fa, sa, wa);
+            e = launch_pdl(fused_lanes<MAXS, true>, resident_ctas(fused_lanes<MAXS, true>, smem), smem, st, fa, sa,
+                           wa, ps);
         } else {
-            e = launch_pdl(fused_lanes<false>, resident_ctas(fused_lanes<false>, 0), 0, st, fa, sa, wa);
+            e = launch_pdl(fused_lanes<MAXS, false>, resident_ctas(fused_lanes<MAXS, false>, 0), 0, st, fa, sa, wa,
+                           ps);
         }
         if (e != cudaSuccess) return e;
     }

@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kThreads)
         int64_t slot = 0;
         unsigned mask[kWords + 1];
         float4 qp, qn;  // a queued hit's point (+ record slot) and normal
-        bool to_lane = false;  // qn.w: the candidate sphere's slot
+        bool to_lane = false, lane_z = false;  // qn.w: the candidate sphere's slot
         if (hit_now) {
             float3 hit = origin + dir * h.t;
             float3 normal = h.g.w >= 0.f ? normalize3(hit - f3(h.g.x, h.g.y, h.g.z)) : f3(0.f, 1.f, 0.f);
@@ -263,6 +263,7 @@ __global__ void __launch_bounds__(kThreads)
                     }
                     if (nc == 1) {
                         to_lane = true;
+                        lane_z = !conic_front(cone, ps.sph[b]);
                         qn.w = __int_as_float(b);
                     }
                 }
@@ -278,17 +279,18 @@ __global__ void __launch_bounds__(kThreads)
         }
         // queue the undecided hits: one atomic per warp, bounce and queue
         bool laned = false;
-        {
-            const bool want = hit_now && cls == 1 && to_lane;
+#pragma unroll
+        for (int q = 0; q < 2; q++) {  // the two lane queues: sphere wholly in front / not
+            const bool want = hit_now && cls == 1 && to_lane && lane_z == (q == 1);
             const unsigned lb = __ballot_sync(0xffffffffu, want);
             if (lb) {
                 unsigned base = 0;
-                if (lane == 0) base = atomicAdd(wa.count + 3, (unsigned)__popc(lb));
+                if (lane == 0) base = atomicAdd(wa.count + (q == 0 ? 3 : 0), (unsigned)__popc(lb));
                 base = __shfl_sync(0xffffffffu, base, 0);
                 const unsigned e = base + __popc(lb & lanemask_lt());
                 if (want && e < wa.lane_cap) {
-                    wa.lane_q[e] = qp;
-                    wa.lane_q[wa.lane_cap + e] = qn;
+                    wa.lane_q[(size_t)(2 * q) * wa.lane_cap + e] = qp;
+                    wa.lane_q[(size_t)(2 * q + 1) * wa.lane_cap + e] = qn;
                     laned = true;
                 }
             }
@@ -506,103 +508,30 @@ __device__ __forceinline__ int sample_conic(const WaveArgs &wa, unsigned e, int 
     return unblocked;
 }
 
+// One single-candidate hit per lane (lane queue q): called by every thread of
+// fused_sample before the warp-per-hit queue.  Each CTA takes an equal chunk
+// so that every SM gets the same share whatever the block placement.
 template <int MAXS, bool SMEM_TAB>
-__global__ void __launch_bounds__(kThreads)
-    fused_sample(const FrameArgs fa, const SceneArgs<float> sa, const WaveArgs wa, const ParamScene<MAXS> ps) {
-    constexpr int kWords = (MAXS + 31) / 32;
+__device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArgs<float> &sa, const WaveArgs &wa,
+                                             const ParamScene<MAXS> &ps, int q, const float4 *gtab) {
     const int n = fa.samples;
-    const float4 *gtab = reinterpret_cast<const float4 *>(sa.table);
-    if constexpr (SMEM_TAB) {
-        extern __shared__ float4 smem_tab_k[];
-        for (int i = threadIdx.x; i < n; i += blockDim.x) smem_tab_k[i] = gtab[i];
-        __syncthreads();
-    }
-    // programmatic dependent launch: everything above (the table staging)
-    // overlaps the trace kernel's tail; the queue is read only after it
-    cudaGridDependencySynchronize();
-    const unsigned count = wa.count[1];
-    const int lane = threadIdx.x & 31;
-    const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const unsigned n_warps = (gridDim.x * blockDim.x) >> 5;
-    const float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
-    // the next hit's queue entry is loaded while the current one samples
-    float4 P, N, A0 = make_float4(0.f, 0.f, 0.f, 0.f), B0 = A0;
-    unsigned hm[kWords + 1];
-    auto fetch = [&](unsigned h) {
-        P = __ldg(wa.hit_p + h);
-        N = __ldg(wa.hit_n + h);
-#pragma unroll
-        for (int w = 0; w <= kWords; w++) hm[w] = __ldg(wa.mask2 + (size_t)w * wa.mask2_stride + h);
-        if (h < wa.conic_cap) {  // the first silhouette sphere, should the entry have one
-            A0 = __ldg(wa.conic + h);
-            B0 = __ldg(wa.conic + wa.conic_cap + h);
-        }
-    };
-    if (warp < count) fetch(warp);
-    for (unsigned h = warp; h < count; h += n_warps) {
-        const float4 Pc = P, Nc = N, A0c = A0, B0c = B0;
-        unsigned hmc[kWords + 1];
-#pragma unroll
-        for (int w = 0; w <= kWords; w++) hmc[w] = hm[w];
-        if (h + n_warps < count) fetch(h + n_warps);
-        const int slot = __float_as_int(Pc.w);
-        const int code = __float_as_int(Nc.w);
-        int nsph = 0;
-        int unblocked;
-        if (code != 0) {
-            unblocked = sample_conic<SMEM_TAB>(wa, h, code, Pc, A0c, B0c, n, gtab);
-            nsph = code & 7;
-        } else {
-            const ShadowFrame f = shadow_frame(f3(Pc.x, Pc.y, Pc.z), f3(Nc.x, Nc.y, Nc.z), lp, true);
-            unblocked = sample_hit<MAXS, SMEM_TAB>(ps, f, hmc, n, gtab, nsph);
-        }
-        unblocked = __reduce_add_sync(0xffffffffu, unblocked);
-        if (lane != 0) continue;
-        reinterpret_cast<float *>(wa.rec + slot)[3] = (float)unblocked / (float)n;
-        if (wa.work) {
-            if (code != 0) atomicAdd(wa.work + kWorkConicHits, 1ull);
-            atomicAdd(wa.work + kWorkSampledHits, 1ull);
-            atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);
-            atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n * nsph);
-            atomicAdd(wa.work + kWorkPlaneTests, (unsigned long long)n * __popc(hmc[kWords]));
-        }
-    }
-}
-
-// --- B1: single-candidate hits, one lane each -------------------------------------
-// Every lane of a warp takes the same disc sample at the same time (a shared-
-// memory broadcast) against its own hit: the per-hit setup (shadow frame,
-// silhouette coefficients) is one lane's, not a warp's, and there is no
-// reduction.  The per-sample expressions are sample_conic's (silhouette form)
-// and sample_hit's single-sphere loop (ray form, when a precondition fails),
-// so the coefficient is the same bits either sampler would produce.  Hits are
-// dealt warp-interleaved over the CTAs so that every SM gets a share.
-template <int MAXS, bool SMEM_TAB>
-__global__ void __launch_bounds__(kThreads)
-    fused_lanes(const FrameArgs fa, const SceneArgs<float> sa, const WaveArgs wa, const ParamScene<MAXS> ps) {
-    const int n = fa.samples;
-    const float4 *gtab = reinterpret_cast<const float4 *>(sa.table);
-    extern __shared__ float4 smem_tab_l[];
-    if constexpr (SMEM_TAB) {
-        for (int i = threadIdx.x; i < n; i += blockDim.x) smem_tab_l[i] = gtab[i];
-        __syncthreads();
-    }
-    cudaGridDependencySynchronize();
     auto table = [&](int i) -> float4 {
         if constexpr (SMEM_TAB) {
+            extern __shared__ float4 smem_tab_l[];
             return smem_tab_l[i];
         } else {
             return __ldg(gtab + i);
         }
     };
     const float3 light = f3(sa.light[0], sa.light[1], sa.light[2]);
-    const unsigned count = min(wa.count[3], wa.lane_cap);
-    const unsigned lane = threadIdx.x & 31;
-    const unsigned stride = gridDim.x * blockDim.x;
-    // warp w of CTA c starts at hit 32 (w * gridDim + c): the first warps of all CTAs fill first
-    for (unsigned h = 32u * ((threadIdx.x >> 5) * gridDim.x + blockIdx.x) + lane; h < count; h += stride) {
-        const float4 P = __ldg(wa.lane_q + h);
-        const float4 N = __ldg(wa.lane_q + wa.lane_cap + h);
+    const unsigned count = min(wa.count[q == 0 ? 3 : 0], wa.lane_cap);
+    const unsigned chunk = (count + gridDim.x - 1) / gridDim.x;
+    const unsigned end = min(count, (blockIdx.x + 1) * chunk);
+    const float4 *qp = wa.lane_q + (size_t)(2 * q) * wa.lane_cap;
+    const float4 *qn = qp + wa.lane_cap;
+    for (unsigned h = blockIdx.x * chunk + threadIdx.x; h < end; h += blockDim.x) {
+        const float4 P = __ldg(qp + h);
+        const float4 N = __ldg(qn + h);
         const int slot = __float_as_int(P.w);
         const float4 g = ps.sph[__float_as_int(N.w)];
         const ShadowFrame f = shadow_frame(f3(P.x, P.y, P.z), f3(N.x, N.y, N.z), light, true);
@@ -664,6 +593,82 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
+template <int MAXS, bool SMEM_TAB>
+__global__ void __launch_bounds__(kThreads)
+    fused_sample(const FrameArgs fa, const SceneArgs<float> sa, const WaveArgs wa, const ParamScene<MAXS> ps) {
+    constexpr int kWords = (MAXS + 31) / 32;
+    const int n = fa.samples;
+    const float4 *gtab = reinterpret_cast<const float4 *>(sa.table);
+    if constexpr (SMEM_TAB) {
+        extern __shared__ float4 smem_tab_k[];
+        for (int i = threadIdx.x; i < n; i += blockDim.x) smem_tab_k[i] = gtab[i];
+        __syncthreads();
+    }
+    // programmatic dependent launch: everything above (the table staging)
+    // overlaps the trace kernel's tail; the queue is read only after it
+    cudaGridDependencySynchronize();
+    if (wa.lane_cap) {  // B1: the single-candidate hits, one lane each
+        sample_lanes<MAXS, SMEM_TAB>(fa, sa, wa, ps, 0, gtab);
+        sample_lanes<MAXS, SMEM_TAB>(fa, sa, wa, ps, 1, gtab);
+    }
+    // B2: the rest, one warp each
+    const unsigned count = wa.count[1];
+    const int lane = threadIdx.x & 31;
+    const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned n_warps = (gridDim.x * blockDim.x) >> 5;
+    const float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
+    // the next hit's queue entry is loaded while the current one samples
+    float4 P, N, A0 = make_float4(0.f, 0.f, 0.f, 0.f), B0 = A0;
+    unsigned hm[kWords + 1];
+    auto fetch = [&](unsigned h) {
+        P = __ldg(wa.hit_p + h);
+        N = __ldg(wa.hit_n + h);
+#pragma unroll
+        for (int w = 0; w <= kWords; w++) hm[w] = __ldg(wa.mask2 + (size_t)w * wa.mask2_stride + h);
+        if (h < wa.conic_cap) {  // the first silhouette sphere, should the entry have one
+            A0 = __ldg(wa.conic + h);
+            B0 = __ldg(wa.conic + wa.conic_cap + h);
+        }
+    };
+    if (warp < count) fetch(warp);
+    for (unsigned h = warp; h < count; h += n_warps) {
+        const float4 Pc = P, Nc = N, A0c = A0, B0c = B0;
+        unsigned hmc[kWords + 1];
+#pragma unroll
+        for (int w = 0; w <= kWords; w++) hmc[w] = hm[w];
+        if (h + n_warps < count) fetch(h + n_warps);
+        const int slot = __float_as_int(Pc.w);
+        const int code = __float_as_int(Nc.w);
+        int nsph = 0;
+        int unblocked;
+        if (code != 0) {
+            unblocked = sample_conic<SMEM_TAB>(wa, h, code, Pc, A0c, B0c, n, gtab);
+            nsph = code & 7;
+        } else {
+            const ShadowFrame f = shadow_frame(f3(Pc.x, Pc.y, Pc.z), f3(Nc.x, Nc.y, Nc.z), lp, true);
+            unblocked = sample_hit<MAXS, SMEM_TAB>(ps, f, hmc, n, gtab, nsph);
+        }
+        unblocked = __reduce_add_sync(0xffffffffu, unblocked);
+        if (lane != 0) continue;
+        reinterpret_cast<float *>(wa.rec + slot)[3] = (float)unblocked / (float)n;
+        if (wa.work) {
+            if (code != 0) atomicAdd(wa.work + kWorkConicHits, 1ull);
+            atomicAdd(wa.work + kWorkSampledHits, 1ull);
+            atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);
+            atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n * nsph);
+            atomicAdd(wa.work + kWorkPlaneTests, (unsigned long long)n * __popc(hmc[kWords]));
+        }
+    }
+}
+
+// --- B1: single-candidate hits, one lane each -------------------------------------
+// Every lane of a warp takes the same disc sample at the same time (a shared-
+// memory broadcast) against its own hit: the per-hit setup (shadow frame,
+// silhouette coefficients) is one lane's, not a warp's, and there is no
+// reduction.  The per-sample expressions are sample_conic's (silhouette form)
+// and sample_hit's single-sphere loop (ray form, when a precondition fails),
+// so the coefficient is the same bits either sampler would produce.  Hits are
+// dealt warp-interleaved over the CTAs so that every SM gets a share.
 // --- C: the pixels that had undecided hits --------------------------------------------
 __global__ void __launch_bounds__(kThreads)
     fused_finish(const FrameArgs fa, const SceneArgs<float> sa, const WaveArgs wa) {
@@ -714,17 +719,6 @@ cudaError_t launch(const FrameArgs &fa, const SceneArgs<float> &sa, const WaveAr
         cudaEventRecord(ev[2], st);  // no separate classify pass: a zero-length phase
     }
     const int n = fa.samples;
-    if (wa.lane_cap) {
-        if (n <= kWaveSmemSamples) {
-            const size_t smem = sizeof(float4) * (size_t)n;
-            e = launch_pdl(fused_lanes<MAXS, true>, resident_ctas(fused_lanes<MAXS, true>, smem), smem, st, fa, sa,
-                           wa, ps);
-        } else {
-            e = launch_pdl(fused_lanes<MAXS, false>, resident_ctas(fused_lanes<MAXS, false>, 0), 0, st, fa, sa, wa,
-                           ps);
-        }
-        if (e != cudaSuccess) return e;
-    }
     if (n <= kWaveSmemSamples) {
         const size_t smem = sizeof(float4) * (size_t)n;
         e = launch_pdl(fused_sample<MAXS, true>, resident_ctas(fused_sample<MAXS, true>, smem), smem, st, fa, sa, wa,
@@ -762,7 +756,7 @@ cudaError_t rt_launch_fused_f32(const rt::FrameArgs &fa, const rt::SceneArgs<flo
     if (e != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[3], st);
     if ((e = launch_pdl(fused_finish, resident_ctas(fused_finish, 0), 0, st, fa, sa, wa)) != cudaSuccess) return e;
-    *n_kernels = wa.lane_cap ? 4 : 3;
+    *n_kernels = 3;
     if (ev) cudaEventRecord(ev[4], st);
     return cudaSuccess;
 }

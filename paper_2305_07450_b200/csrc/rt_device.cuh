@@ -79,7 +79,9 @@ struct WaveArgs {
     int cull;          // exact per-hit occluder culling in the shadow kernel
     float4 *conic;     // culled path: silhouette coefficients of queued hits, [2 kConic][conic_cap]
     unsigned conic_cap;  // queue positions below this may take the silhouette form (0: off)
-    float4 *lane_q;    // culled path: single-sphere silhouette hits, one lane each, [3][lane_cap]
+    float4 *lane_q;    // culled path: single-candidate hits sampled one lane each: queue q (0: the
+                       // sphere wholly in front, 1: not), row r (0: {p, slot}, 1: {n, sphere}) at
+                       // [(2q + r) lane_cap]; lengths count[3] and count[0]
     unsigned lane_cap; // (0: off)
 };
 // FP64 culled wavefront (render_fused_f64.cu): queues in float64

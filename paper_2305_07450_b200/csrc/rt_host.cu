@@ -455,7 +455,7 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
                 if ((rc = d.w_conic.ensure(sizeof(float4) * 2 * rt::kConic * (size_t)wa.n_pix))) return rc;
                 wa.conic = (float4 *)d.w_conic.p;
                 wa.conic_cap = (unsigned)wa.n_pix;
-                if ((rc = d.w_lane.ensure(sizeof(float4) * 3 * (size_t)wa.n_pix))) return rc;
+                if ((rc = d.w_lane.ensure(sizeof(float4) * 4 * (size_t)wa.n_pix))) return rc;
                 wa.lane_q = (float4 *)d.w_lane.p;
                 wa.lane_cap = (unsigned)wa.n_pix;
             }

@@ -169,6 +169,17 @@ __device__ __forceinline__ bool bound_meets_cone(const Cone &k, float4 B) {
 // Returns 0 (a precondition fails: the hit takes the ray form), 1 (no z test
 // needed), 2 (z test, z0 = +1) or 3 (z test, z0 = -1); c = {x0, x1, x2, y0},
 // {y1, y2, z1, z2}.
+// Every sample direction lies within phi of the cone axis, so tca >= h cos(phi)
+// - q sin(phi) for u = c - o split into h along the axis and q across it:
+// true when that bound is clearly positive (no z test needed).
+__device__ __forceinline__ bool conic_front(const Cone &k, float4 g) {
+    const float3 u = f3(g.x - k.o.x, g.y - k.o.y, g.z - k.o.z);
+    const float h = dot3(u, k.axis);
+    const float3 wp = u - k.axis * h;
+    const float q = sqrtf(dot3(wp, wp));
+    return h * k.cos_phi - q * k.sin_phi > kCullRel * (fabsf(h) + q) + kCullAbs;
+}
+
 __device__ __forceinline__ int conic_coeffs(const Cone &k, float4 g, float3 lo, float3 bu, float3 bv, float ls2,
                                             float4 &ca, float4 &cb) {
     if (!k.ok) return 0;
@@ -178,11 +189,7 @@ __device__ __forceinline__ int conic_coeffs(const Cone &k, float4 g, float3 lo, 
     if (!(u2 > r2g * (1.f + 4.f * kCullRel) + kCullAbs)) return 0;  // origin clearly outside
     const float un = sqrtf(u2);
     if (!(un * (1.f + kCullRel) + kCullAbs < sqrtf(ls2))) return 0;  // entry <= tca <= |u| < |p - L| <= limit
-    const float h = dot3(u, k.axis);
-    const float3 wp = u - k.axis * h;
-    const float q = sqrtf(dot3(wp, wp));
-    // every sample direction lies within phi of the axis: tca >= h cos(phi) - q sin(phi)
-    const bool front = h * k.cos_phi - q * k.sin_phi > kCullRel * (fabsf(h) + q) + kCullAbs;
+    const bool front = conic_front(k, g);
     const float3 n = u * (1.f / un);
     // orthonormal pair perpendicular to n (branch-free, Duff et al. 2017)
     const float sg = copysignf(1.f, n.z);

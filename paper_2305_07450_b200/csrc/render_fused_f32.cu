@@ -426,6 +426,27 @@ __device__ __forceinline__ int sample_hit(const ParamScene<MAXS> &ps, const Shad
     return unblocked;
 }
 
+// Silhouette-form sample test (rt_wave.cuh): sphere coefficients A = {x0, x1,
+// x2, y0}, B = {y1, y2, z1, z2}, the hit's |w|^2 = b0 + b1 a + b2 b + rho,
+// table entry t = {a, b, rho}.  Returns 1 when blocked: the sign bit of
+// d = x^2 + y^2 - |w|^2 (and, with the z test, z > 0 as a clear sign bit).
+__device__ __forceinline__ unsigned conic_blocked(float4 A, float4 B, float b0, float b1, float b2, float4 t) {
+    const float w2 = fmaf(b1, t.x, fmaf(b2, t.y, b0 + t.z));
+    const float x = fmaf(A.y, t.x, fmaf(A.z, t.y, A.x));
+    const float y = fmaf(B.x, t.x, fmaf(B.y, t.y, A.w));
+    const float d = fmaf(x, x, fmaf(y, y, -w2));
+    return __float_as_uint(d) >> 31;
+}
+__device__ __forceinline__ unsigned conic_blocked_z(float4 A, float4 B, float z0, float b0, float b1, float b2,
+                                                    float4 t) {
+    const float w2 = fmaf(b1, t.x, fmaf(b2, t.y, b0 + t.z));
+    const float x = fmaf(A.y, t.x, fmaf(A.z, t.y, A.x));
+    const float y = fmaf(B.x, t.x, fmaf(B.y, t.y, A.w));
+    const float z = fmaf(B.z, t.x, fmaf(B.w, t.y, z0));
+    const float d = fmaf(x, x, fmaf(y, y, -w2));
+    return (__float_as_uint(d) & ~__float_as_uint(z)) >> 31;
+}
+
 // Sampling of one silhouette-form hit (conic_entry): P = {|lo|^2, 2 lo.bu,
 // 2 lo.bv, slot}, sphere j's coefficients C[2j], C[2j+1] (the first sphere's
 // arrive prefetched).  Returns the unblocked count of this lane's samples.
@@ -443,32 +464,12 @@ __device__ __forceinline__ int sample_conic(const WaveArgs &wa, unsigned e, int 
     };
     const int ncon = code & 7;
     const int full = n >> 5;
-    int unblocked = 0;
-    auto run = [&](auto open) {
+    unsigned blocked = 0;
+    auto run = [&](auto test) {
 #pragma unroll 4
-        for (int j = 0; j < full; j++) unblocked += open(table(lane + 32 * j));
-        if (lane + 32 * full < n) unblocked += open(table(lane + 32 * full));
+        for (int j = 0; j < full; j++) blocked += test(table(lane + 32 * j));
+        if (lane + 32 * full < n) blocked += test(table(lane + 32 * full));
     };
-    if (ncon == 1 && !(code & (1 << 3))) {  // one sphere wholly in front: the common penumbra
-        run([&](float4 t) -> int {
-            const float w2 = fmaf(P.y, t.x, fmaf(P.z, t.y, P.x + t.z));
-            const float x = fmaf(A0.y, t.x, fmaf(A0.z, t.y, A0.x));
-            const float y = fmaf(B0.x, t.x, fmaf(B0.y, t.y, A0.w));
-            return fmaf(x, x, y * y) < w2 ? 0 : 1;
-        });
-        return unblocked;
-    }
-    if (ncon == 1) {  // one sphere straddling o's horizon: the self-shadowing terminator
-        const float z0 = (code & (1 << 7)) ? -1.f : 1.f;
-        run([&](float4 t) -> int {
-            const float w2 = fmaf(P.y, t.x, fmaf(P.z, t.y, P.x + t.z));
-            const float x = fmaf(A0.y, t.x, fmaf(A0.z, t.y, A0.x));
-            const float y = fmaf(B0.x, t.x, fmaf(B0.y, t.y, A0.w));
-            const float z = fmaf(B0.z, t.x, fmaf(B0.w, t.y, z0));
-            return (fmaf(x, x, y * y) < w2 && z > 0.f) ? 0 : 1;
-        });
-        return unblocked;
-    }
     float4 A[kConic], B[kConic];
     float Z[kConic];
     A[0] = A0;
@@ -478,39 +479,41 @@ __device__ __forceinline__ int sample_conic(const WaveArgs &wa, unsigned e, int 
         if (j < ncon) {
             A[j] = __ldg(wa.conic + (size_t)(2 * j) * wa.conic_cap + e);
             B[j] = __ldg(wa.conic + (size_t)(2 * j + 1) * wa.conic_cap + e);
-        } else {  // never blocks: x^2 + y^2 = +inf
+        } else {  // never blocks: x = +inf
             A[j] = make_float4(INFINITY, 0.f, 0.f, 0.f);
             B[j] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
     }
 #pragma unroll
     for (int j = 0; j < kConic; j++) Z[j] = (code & (1 << (7 + j))) ? -1.f : 1.f;  // no z test: z = 1
-    auto blocked_by = [&](int j, float4 t, float w2) -> bool {
-        const float x = fmaf(A[j].y, t.x, fmaf(A[j].z, t.y, A[j].x));
-        const float y = fmaf(B[j].x, t.x, fmaf(B[j].y, t.y, A[j].w));
-        const float z = fmaf(B[j].z, t.x, fmaf(B[j].w, t.y, Z[j]));
-        return fmaf(x, x, y * y) < w2 && z > 0.f;
-    };
-    if (ncon == 2) {
-        run([&](float4 t) -> int {
-            const float w2 = fmaf(P.y, t.x, fmaf(P.z, t.y, P.x + t.z));
-            return (blocked_by(0, t, w2) || blocked_by(1, t, w2)) ? 0 : 1;
+    if (ncon == 1 && !(code & (1 << 3))) {
+        run([&](float4 t) { return conic_blocked(A[0], B[0], P.x, P.y, P.z, t); });
+    } else if (ncon == 1) {
+        run([&](float4 t) { return conic_blocked_z(A[0], B[0], Z[0], P.x, P.y, P.z, t); });
+    } else if (ncon == 2) {
+        run([&](float4 t) {
+            return conic_blocked_z(A[0], B[0], Z[0], P.x, P.y, P.z, t) |
+                   conic_blocked_z(A[1], B[1], Z[1], P.x, P.y, P.z, t);
         });
-        return unblocked;
-    }
-    run([&](float4 t) -> int {
-        const float w2 = fmaf(P.y, t.x, fmaf(P.z, t.y, P.x + t.z));
-        bool b = false;
+    } else {
+        run([&](float4 t) {
+            unsigned b = 0;
 #pragma unroll
-        for (int j = 0; j < kConic; j++) b |= blocked_by(j, t, w2);
-        return b ? 0 : 1;
-    });
-    return unblocked;
+            for (int j = 0; j < kConic; j++) b |= conic_blocked_z(A[j], B[j], Z[j], P.x, P.y, P.z, t);
+            return b;
+        });
+    }
+    return (n - lane + 31) / 32 - (int)blocked;  // this lane's samples lane, lane + 32, ... less the blocked
 }
 
-// One single-candidate hit per lane (lane queue q): called by every thread of
-// fused_sample before the warp-per-hit queue.  Each CTA takes an equal chunk
-// so that every SM gets the same share whatever the block placement.
+// Single-candidate hits, one per lane (lane queue q): every lane of a warp
+// takes the same disc sample at the same time (a shared-memory broadcast)
+// against its own hit; the per-hit setup is one lane's, not a warp's, and
+// there is no reduction.  Warps grab 32 hits at a time from an atomic
+// counter, so the SMs stay evenly loaded whatever the block placement.  A
+// sample is blocked iff d = x^2 + y^2 - |w|^2 < 0 (and z > 0): its sign bit
+// is added to the blocked count.  d is formed exactly as in sample_conic, so
+// either sampler gives the same bits.
 template <int MAXS, bool SMEM_TAB>
 __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArgs<float> &sa, const WaveArgs &wa,
                                              const ParamScene<MAXS> &ps, int q, const float4 *gtab) {
@@ -525,11 +528,15 @@ __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArg
     };
     const float3 light = f3(sa.light[0], sa.light[1], sa.light[2]);
     const unsigned count = min(wa.count[q == 0 ? 3 : 0], wa.lane_cap);
-    const unsigned chunk = (count + gridDim.x - 1) / gridDim.x;
-    const unsigned end = min(count, (blockIdx.x + 1) * chunk);
     const float4 *qp = wa.lane_q + (size_t)(2 * q) * wa.lane_cap;
     const float4 *qn = qp + wa.lane_cap;
-    for (unsigned h = blockIdx.x * chunk + threadIdx.x; h < end; h += blockDim.x) {
+    const unsigned lane = threadIdx.x & 31;
+    for (;;) {
+        unsigned u = 0;
+        if (lane == 0) u = atomicAdd(wa.count + 4 + q, 1u);
+        const unsigned h = 32u * __shfl_sync(0xffffffffu, u, 0) + lane;
+        if (h - lane >= count) break;
+        if (h >= count) continue;
         const float4 P = __ldg(qp + h);
         const float4 N = __ldg(qn + h);
         const int slot = __float_as_int(P.w);
@@ -539,7 +546,7 @@ __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArg
         float4 A, B;
         const int r = conic_coeffs(k, g, f.lo, f.bu, f.bv, f.ls2, A, B);
         const float b0 = dot3(f.lo, f.lo), b1 = 2.f * dot3(f.lo, f.bu), b2 = 2.f * dot3(f.lo, f.bv);
-        int unblocked = 0;
+        unsigned blocked = 0;
         const unsigned act = __activemask();
         if (__any_sync(act, r == 0)) {
             // some lane's hit needs the ray form: those lanes take it, the rest the silhouette
@@ -553,37 +560,20 @@ __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArg
                     float3 dir;
                     float limit;
                     shadow_ray_unguarded(f, t, dir, limit);
-                    unblocked += sphere_margin_L(L, dir, r2g, limit) > 0.f ? 0 : 1;
+                    blocked += sphere_margin_L(L, dir, r2g, limit) > 0.f ? 1 : 0;
                 } else {
-                    const float w2 = fmaf(b1, t.x, fmaf(b2, t.y, b0 + t.z));
-                    const float x = fmaf(A.y, t.x, fmaf(A.z, t.y, A.x));
-                    const float y = fmaf(B.x, t.x, fmaf(B.y, t.y, A.w));
-                    const float z = fmaf(B.z, t.x, fmaf(B.w, t.y, z0));
-                    unblocked += (fmaf(x, x, y * y) < w2 && z > 0.f) ? 0 : 1;
+                    blocked += conic_blocked_z(A, B, z0, b0, b1, b2, t);
                 }
             }
         } else if (__any_sync(act, r >= 2)) {
             const float z0 = r == 3 ? -1.f : 1.f;
 #pragma unroll 4
-            for (int i = 0; i < n; i++) {
-                const float4 t = table(i);
-                const float w2 = fmaf(b1, t.x, fmaf(b2, t.y, b0 + t.z));
-                const float x = fmaf(A.y, t.x, fmaf(A.z, t.y, A.x));
-                const float y = fmaf(B.x, t.x, fmaf(B.y, t.y, A.w));
-                const float z = fmaf(B.z, t.x, fmaf(B.w, t.y, z0));
-                unblocked += (fmaf(x, x, y * y) < w2 && z > 0.f) ? 0 : 1;
-            }
+            for (int i = 0; i < n; i++) blocked += conic_blocked_z(A, B, z0, b0, b1, b2, table(i));
         } else {
 #pragma unroll 4
-            for (int i = 0; i < n; i++) {
-                const float4 t = table(i);
-                const float w2 = fmaf(b1, t.x, fmaf(b2, t.y, b0 + t.z));
-                const float x = fmaf(A.y, t.x, fmaf(A.z, t.y, A.x));
-                const float y = fmaf(B.x, t.x, fmaf(B.y, t.y, A.w));
-                unblocked += fmaf(x, x, y * y) < w2 ? 0 : 1;
-            }
+            for (int i = 0; i < n; i++) blocked += conic_blocked(A, B, b0, b1, b2, table(i));
         }
-        reinterpret_cast<float *>(wa.rec + slot)[3] = (float)unblocked / (float)n;
+        reinterpret_cast<float *>(wa.rec + slot)[3] = (float)(n - (int)blocked) / (float)n;
         if (wa.work) {
             if (r != 0) atomicAdd(wa.work + kWorkConicHits, 1ull);
             atomicAdd(wa.work + kWorkSampledHits, 1ull);
@@ -742,7 +732,7 @@ bool rt_fused_fits(const rt::SceneArgs<float> &sa) {
 cudaError_t rt_launch_fused_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, const rt::WaveArgs &wa,
                                 cudaStream_t st, int *n_kernels, cudaEvent_t *ev) {
     *n_kernels = 0;
-    cudaError_t e = cudaMemsetAsync(wa.count, 0, 4 * sizeof(unsigned), st);
+    cudaError_t e = cudaMemsetAsync(wa.count, 0, 8 * sizeof(unsigned), st);
     if (e != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[0], st);
     ParamScene<8> p8;

@@ -67,7 +67,8 @@ struct WaveArgs {
     float *hit_s;      // Blinn factor
     float *hit_sc;     // shadow coefficient
     int *queue;        // slots holding a hit
-    unsigned *count;   // [0] queue length, [1] queue2 length, [2] queue3 length
+    unsigned *count;   // queue lengths; culled path: [0], [3] lane queues, [1] warp queue, [2] parked
+                       // pixels, [4], [5] the lane queues' grab counters
     int *queue2;          // culled path: undecided hits (slots)
     unsigned *mask2;      // their candidate-body masks, word-major [words][mask2_stride]
     int64_t mask2_stride;

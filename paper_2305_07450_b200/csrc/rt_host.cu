@@ -443,7 +443,7 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         wa.n_pix = (int64_t)fa.local_rows * fa.width;
         size_t slots = (size_t)wa.n_pix * (fa.bounces + 1);
         if ((rc = d.w_p.ensure(sizeof(float4) * slots)) || (rc = d.w_n.ensure(sizeof(float4) * slots)) ||
-            (rc = d.w_count.ensure(4 * sizeof(unsigned))) || (rc = d.w_pix.ensure(sizeof(float4) * (size_t)wa.n_pix)))
+            (rc = d.w_count.ensure(8 * sizeof(unsigned))) || (rc = d.w_pix.ensure(sizeof(float4) * (size_t)wa.n_pix)))
             return rc;
         if (fused) {
             if ((rc = d.w_queue2.ensure(sizeof(int) * slots)) ||

@@ -506,17 +506,18 @@ __device__ __forceinline__ int sample_conic(const WaveArgs &wa, unsigned e, int 
     return (n - lane + 31) / 32 - (int)blocked;  // this lane's samples lane, lane + 32, ... less the blocked
 }
 
-// Single-candidate hits, one per lane (lane queue q): every lane of a warp
-// takes the same disc sample at the same time (a shared-memory broadcast)
-// against its own hit; the per-hit setup is one lane's, not a warp's, and
-// there is no reduction.  Warps grab 32 hits at a time from an atomic
-// counter, so the SMs stay evenly loaded whatever the block placement.  A
-// sample is blocked iff d = x^2 + y^2 - |w|^2 < 0 (and z > 0): its sign bit
-// is added to the blocked count.  d is formed exactly as in sample_conic, so
-// either sampler gives the same bits.
+// Single-candidate hits, one per lane: every lane of a warp takes the same
+// disc sample at the same time (a shared-memory broadcast) against its own
+// hit; the per-hit setup is one lane's, not a warp's, and there is no
+// reduction.  The two lane queues are cut into units of 32 hits, listed one
+// after the other; CTA c takes units [c U / G, (c + 1) U / G) — the grid is
+// exactly the resident CTAs, the same count on every SM, so the SMs get equal
+// shares.  A sample is blocked iff d = x^2 + y^2 - |w|^2 < 0 (and z > 0): its
+// sign bit is added to the blocked count; d is formed exactly as in
+// sample_conic, so either sampler gives the same bits.
 template <int MAXS, bool SMEM_TAB>
 __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArgs<float> &sa, const WaveArgs &wa,
-                                             const ParamScene<MAXS> &ps, int q, const float4 *gtab) {
+                                             const ParamScene<MAXS> &ps, const float4 *gtab) {
     const int n = fa.samples;
     auto table = [&](int i) -> float4 {
         if constexpr (SMEM_TAB) {
@@ -527,16 +528,17 @@ __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArg
         }
     };
     const float3 light = f3(sa.light[0], sa.light[1], sa.light[2]);
-    const unsigned count = min(wa.count[q == 0 ? 3 : 0], wa.lane_cap);
-    const float4 *qp = wa.lane_q + (size_t)(2 * q) * wa.lane_cap;
-    const float4 *qn = qp + wa.lane_cap;
+    const unsigned c0 = min(wa.count[3], wa.lane_cap), c1 = min(wa.count[0], wa.lane_cap);
+    const unsigned u0 = (c0 + 31) / 32, units = u0 + (c1 + 31) / 32;
+    const unsigned first = (unsigned)(((unsigned long long)units * blockIdx.x) / gridDim.x);
+    const unsigned last = (unsigned)(((unsigned long long)units * (blockIdx.x + 1)) / gridDim.x);
     const unsigned lane = threadIdx.x & 31;
-    for (;;) {
-        unsigned u = 0;
-        if (lane == 0) u = atomicAdd(wa.count + 4 + q, 1u);
-        const unsigned h = 32u * __shfl_sync(0xffffffffu, u, 0) + lane;
-        if (h - lane >= count) break;
-        if (h >= count) continue;
+    for (unsigned u = first + (threadIdx.x >> 5); u < last; u += blockDim.x >> 5) {
+        const int q = u < u0 ? 0 : 1;
+        const unsigned h = 32u * (q == 0 ? u : u - u0) + lane;
+        if (h >= (q == 0 ? c0 : c1)) continue;
+        const float4 *qp = wa.lane_q + (size_t)(2 * q) * wa.lane_cap;
+        const float4 *qn = qp + wa.lane_cap;
         const float4 P = __ldg(qp + h);
         const float4 N = __ldg(qn + h);
         const int slot = __float_as_int(P.w);
@@ -598,8 +600,7 @@ __global__ void __launch_bounds__(kThreads)
     // overlaps the trace kernel's tail; the queue is read only after it
     cudaGridDependencySynchronize();
     if (wa.lane_cap) {  // B1: the single-candidate hits, one lane each
-        sample_lanes<MAXS, SMEM_TAB>(fa, sa, wa, ps, 0, gtab);
-        sample_lanes<MAXS, SMEM_TAB>(fa, sa, wa, ps, 1, gtab);
+        sample_lanes<MAXS, SMEM_TAB>(fa, sa, wa, ps, gtab);
     }
     // B2: the rest, one warp each
     const unsigned count = wa.count[1];
@@ -732,7 +733,7 @@ bool rt_fused_fits(const rt::SceneArgs<float> &sa) {
 cudaError_t rt_launch_fused_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, const rt::WaveArgs &wa,
                                 cudaStream_t st, int *n_kernels, cudaEvent_t *ev) {
     *n_kernels = 0;
-    cudaError_t e = cudaMemsetAsync(wa.count, 0, 8 * sizeof(unsigned), st);
+    cudaError_t e = cudaMemsetAsync(wa.count, 0, 4 * sizeof(unsigned), st);
     if (e != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[0], st);
     ParamScene<8> p8;

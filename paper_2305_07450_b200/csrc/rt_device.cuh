@@ -67,8 +67,7 @@ struct WaveArgs {
     float *hit_s;      // Blinn factor
     float *hit_sc;     // shadow coefficient
     int *queue;        // slots holding a hit
-    unsigned *count;   // queue lengths; culled path: [0], [3] lane queues, [1] warp queue, [2] parked
-                       // pixels, [4], [5] the lane queues' grab counters
+    unsigned *count;   // queue lengths; culled path: [0], [3] lane queues, [1] warp queue, [2] parked pixels
     int *queue2;          // culled path: undecided hits (slots)
     unsigned *mask2;      // their candidate-body masks, word-major [words][mask2_stride]
     int64_t mask2_stride;

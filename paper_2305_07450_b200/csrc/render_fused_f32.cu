@@ -7,23 +7,28 @@
 //              (shading.py:53-73) and the exact classification of every body
 //              against the hit's shadow cone (rt_wave.cuh): nothing can block
 //              -> coefficient 1, something blocks every sample -> 0, else the
-//              hit is queued with its candidate-body mask.  A pixel whose hits
-//              are all decided is unwound (renderer.py:185-224) and packed
-//              (renderer.py:45-50) right here; otherwise its records are parked
-//              in HBM and the pixel is queued for C.
-//   B  sample  one warp per queued hit, 32 disc samples abreast against that
-//              hit's candidate bodies (held in registers);
-//   C  finish  one thread per parked pixel: unwind and pack.
+//              hit is queued.  A pixel whose hits are all decided is unwound
+//              (renderer.py:185-224) and packed (renderer.py:45-50) right
+//              here; otherwise its records are parked in HBM.
+//   B  sample  B1: hits with a single candidate sphere, one lane each (two
+//              lane queues: sphere wholly in front of the hit / not), every
+//              lane on the same disc sample at once; B2: the rest, one warp
+//              per hit, 32 samples abreast against its candidates.  The
+//              sampler of a pixel's last pending hit unwinds and packs it.
 //
-// Arithmetic per shadow test is the unculled kernels' (render_wave_f32.cu,
-// render_f32.cu) operation for operation: the frames are bit-identical.
+// A penumbra sphere is tested in its silhouette form (rt_wave.cuh,
+// conic_coeffs: six coefficients per hit and sphere, a quadratic per sample)
+// when its preconditions hold, else — and everywhere with option "conic" off
+// — in the ray form, operation for operation the unculled kernels'
+// (render_wave_f32.cu), whose frames the culled ones then equal bit for bit.
 //
 // HBM, slot = bounce * n_pix + local pixel:
-//   hit_p float4 {p, record slot}, hit_n float4 {n, 0}  the queue of undecided hits
-//                                                     (compact: entry = queue position)
-//   rec   float4 {body, Lambert, Blinn, coefficient}    every hit of a pending pixel
-//   pix   float4 {tail rgb, records | exhausted << 8}   pending pixels
-//   candidate masks of the queued hits (word-major), queue3 parked pixels
+//   lane_q  {p, record slot}, {n, candidate sphere}       the two lane queues
+//   hit_p   {p, slot} or {|lo|^2, 2 lo.bu, 2 lo.bv, slot}  the warp queue (ray / silhouette form)
+//   hit_n   {n, silhouette code}, masks word-major, conic coefficients [2j][e]
+//   rec     float4 {body, Lambert, Blinn, coefficient}   every hit of a parked pixel
+//   pix     float4 {tail rgb, records | exhausted << 8 | several pending << 9}
+//   pend    per parked pixel with several pending hits: the countdown
 #include "rt_wave.cuh"
 
 namespace {
@@ -322,24 +327,44 @@ __global__ void __launch_bounds__(kThreads)
             }
         }
     }
-    const bool park = valid && npend > 0;
-    const unsigned pb = __ballot_sync(0xffffffffu, park);
-    if (pb) {
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(wa.count + 2, (unsigned)__popc(pb));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (park) wa.queue3[base + __popc(pb & lanemask_lt())] = (int)lp;
-    }
     if (!valid) return;
-    if (!park) {
+    if (npend == 0) {
         const float3 c = unwind(m, exhausted, tail, sa, [&](int k) { return Record{ridx[k], rdfs[k], rs[k], rsc[k]}; });
         store_pixel(fa, x, y, c);
         if (fa.peer_out) __threadfence_system();
     } else {
-        wa.pix[lp] = make_float4(tail.x, tail.y, tail.z, __int_as_float(m | (exhausted << 8)));
+        // parked: the sampler of its last pending hit unwinds it (resolve_hit)
+        wa.pix[lp] = make_float4(tail.x, tail.y, tail.z, __int_as_float(m | (exhausted << 8) | ((npend > 1) << 9)));
+        if (npend > 1) wa.pend[lp] = npend;
         for (int k = 0; k < m; k++)
             wa.rec[(int64_t)k * wa.n_pix + lp] = make_float4(__int_as_float(ridx[k]), rdfs[k], rs[k], rsc[k]);
     }
+}
+
+// A sampled hit's coefficient sc (record slot = bounce * n_pix + pixel): a
+// pixel with this one pending hit is unwound and packed at once (its other
+// records are decided); with several, the coefficient is stored and the last
+// of the pixel's samplers — an atomic countdown, fenced both ways — unwinds it.
+__device__ __forceinline__ void resolve_hit(const FrameArgs &fa, const SceneArgs<float> &sa, const WaveArgs &wa,
+                                            int slot, float sc) {
+    const int n_pix = (int)wa.n_pix;
+    const int kh = slot / n_pix, lp = slot - kh * n_pix;
+    const float4 px = __ldcg(wa.pix + lp);
+    const int info = __float_as_int(px.w);
+    if (info & (1 << 9)) {
+        reinterpret_cast<float *>(wa.rec + slot)[3] = sc;
+        __threadfence();
+        if (atomicSub(wa.pend + lp, 1) != 1) return;
+        __threadfence();
+        sc = __ldcg(wa.rec + slot).w;
+    }
+    const float3 c = unwind(info & 0xff, (info >> 8) & 1, f3(px.x, px.y, px.z), sa, [&](int k) {
+        const float4 r = __ldcg(wa.rec + (int64_t)k * n_pix + lp);
+        return Record{__float_as_int(r.x), r.y, r.z, k == kh ? sc : r.w};
+    });
+    const int ly = lp / fa.width, x = lp - ly * fa.width;
+    store_pixel(fa, x, map_row(ly, fa), c);
+    if (fa.peer_out) __threadfence_system();
 }
 
 // --- B ----------------------------------------------------------------------------
@@ -575,7 +600,7 @@ __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArg
 #pragma unroll 4
             for (int i = 0; i < n; i++) blocked += conic_blocked(A, B, b0, b1, b2, table(i));
         }
-        reinterpret_cast<float *>(wa.rec + slot)[3] = (float)(n - (int)blocked) / (float)n;
+        resolve_hit(fa, sa, wa, slot, (float)(n - (int)blocked) / (float)n);
         if (wa.work) {
             if (r != 0) atomicAdd(wa.work + kWorkConicHits, 1ull);
             atomicAdd(wa.work + kWorkSampledHits, 1ull);
@@ -622,6 +647,8 @@ __global__ void __launch_bounds__(kThreads)
         }
     };
     if (warp < count) fetch(warp);
+    int held = 0, my_slot = -1;
+    float my_sc = 0.f;
     for (unsigned h = warp; h < count; h += n_warps) {
         const float4 Pc = P, Nc = N, A0c = A0, B0c = B0;
         unsigned hmc[kWords + 1];
@@ -640,8 +667,17 @@ __global__ void __launch_bounds__(kThreads)
             unblocked = sample_hit<MAXS, SMEM_TAB>(ps, f, hmc, n, gtab, nsph);
         }
         unblocked = __reduce_add_sync(0xffffffffu, unblocked);
+        // lane `held` keeps this hit; every 32 hits the lanes resolve theirs together
+        if (lane == held) {
+            my_slot = slot;
+            my_sc = (float)unblocked / (float)n;
+        }
+        if (++held == 32) {
+            if (my_slot >= 0) resolve_hit(fa, sa, wa, my_slot, my_sc);
+            my_slot = -1;
+            held = 0;
+        }
         if (lane != 0) continue;
-        reinterpret_cast<float *>(wa.rec + slot)[3] = (float)unblocked / (float)n;
         if (wa.work) {
             if (code != 0) atomicAdd(wa.work + kWorkConicHits, 1ull);
             atomicAdd(wa.work + kWorkSampledHits, 1ull);
@@ -650,35 +686,7 @@ __global__ void __launch_bounds__(kThreads)
             atomicAdd(wa.work + kWorkPlaneTests, (unsigned long long)n * __popc(hmc[kWords]));
         }
     }
-}
-
-// --- B1: single-candidate hits, one lane each -------------------------------------
-// Every lane of a warp takes the same disc sample at the same time (a shared-
-// memory broadcast) against its own hit: the per-hit setup (shadow frame,
-// silhouette coefficients) is one lane's, not a warp's, and there is no
-// reduction.  The per-sample expressions are sample_conic's (silhouette form)
-// and sample_hit's single-sphere loop (ray form, when a precondition fails),
-// so the coefficient is the same bits either sampler would produce.  Hits are
-// dealt warp-interleaved over the CTAs so that every SM gets a share.
-// --- C: the pixels that had undecided hits --------------------------------------------
-__global__ void __launch_bounds__(kThreads)
-    fused_finish(const FrameArgs fa, const SceneArgs<float> sa, const WaveArgs wa) {
-    cudaGridDependencySynchronize();
-    const unsigned count = wa.count[2];
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
-        const int lpix = __ldg(wa.queue3 + i);
-        const float4 px = wa.pix[lpix];
-        const int info = __float_as_int(px.w);
-        const int m = info & 0xff;
-        float4 rk[kMaxBounce + 1];  // issue every record load before the first use
-        for (int k = 0; k < m; k++) rk[k] = wa.rec[(int64_t)k * wa.n_pix + lpix];
-        const float3 c = unwind(m, (info >> 8) & 1, f3(px.x, px.y, px.z), sa, [&](int k) {
-            return Record{__float_as_int(rk[k].x), rk[k].y, rk[k].z, rk[k].w};
-        });
-        const int ly = lpix / fa.width, x = lpix - ly * fa.width;
-        store_pixel(fa, x, map_row(ly, fa), c);
-        if (fa.peer_out) __threadfence_system();
-    }
+    if (my_slot >= 0) resolve_hit(fa, sa, wa, my_slot, my_sc);
 }
 
 // Launch with programmatic stream serialisation: the kernel may start while
@@ -745,9 +753,10 @@ cudaError_t rt_launch_fused_f32(const rt::FrameArgs &fa, const rt::SceneArgs<flo
     else
         return cudaErrorInvalidValue;
     if (e != cudaSuccess) return e;
-    if (ev) cudaEventRecord(ev[3], st);
-    if ((e = launch_pdl(fused_finish, resident_ctas(fused_finish, 0), 0, st, fa, sa, wa)) != cudaSuccess) return e;
-    *n_kernels = 3;
-    if (ev) cudaEventRecord(ev[4], st);
+    if (ev) {  // the sampler also unwinds: a zero-length shade phase
+        cudaEventRecord(ev[3], st);
+        cudaEventRecord(ev[4], st);
+    }
+    *n_kernels = 2;
     return cudaSuccess;
 }

@@ -73,7 +73,7 @@ struct WaveArgs {
     int64_t mask2_stride;
     float4 *pix;       // {tail rgb, records | exhausted << 8}
     float4 *rec;       // culled path: {body, Lambert, Blinn, coefficient} per hit of a pending pixel
-    int *queue3;       // culled path: pixels with undecided hits (finished after sampling)
+    int *pend;         // culled path: per pixel, its hits still sampling (written when 2 or more)
     int64_t n_pix;     // pixels of this partition (local_rows * width)
     unsigned long long *work;  // optional executed-work tallies of the culled path (kWork*), or null
     int cull;          // exact per-hit occluder culling in the shadow kernel

@@ -449,7 +449,7 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
             if ((rc = d.w_queue2.ensure(sizeof(int) * slots)) ||
                 (rc = d.w_mask2.ensure(sizeof(unsigned) * slots * (ctx->scene.n <= 8 ? 2 : rt::kMaskWords + 1))) ||
                 (rc = d.w_rec.ensure(sizeof(float4) * slots)) ||
-                (rc = d.w_pending.ensure(sizeof(int) * (size_t)wa.n_pix)))  // queue3
+                (rc = d.w_pending.ensure(sizeof(int) * (size_t)wa.n_pix)))  // pend
                 return rc;
             if (ctx->conic) {  // silhouette coefficients for the first n_pix queued hits
                 if ((rc = d.w_conic.ensure(sizeof(float4) * 2 * rt::kConic * (size_t)wa.n_pix))) return rc;
@@ -475,7 +475,7 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         wa.mask2_stride = (int64_t)slots;
         wa.pix = (float4 *)d.w_pix.p;
         wa.rec = (float4 *)d.w_rec.p;
-        wa.queue3 = (int *)d.w_pending.p;
+        wa.pend = (int *)d.w_pending.p;
         wa.cull = fused;
         wa.work = nullptr;
         if (ctx->count_work) {

@@ -80,7 +80,7 @@ __device__ float3 trace(const Geo &geo, float3 origin, float3 dir, const SceneAr
         float s = 0.f;
         if (hm2 > 0.f) {
             float dd = fmaxf(dot3(normal, hv) * rsqrtf(hm2), 0.f);
-            s = powf(dd, __ldg(sa.mat + 8 * h.idx + 4));
+            s = blinn_pow(dd, __ldg(sa.mat + 8 * h.idx + 4));
         }
         float lum = fminf(sa.ambient + sc * dfs * (1.f - sa.ambient), 1.f);
         ridx[k] = h.idx;

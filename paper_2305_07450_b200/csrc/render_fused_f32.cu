@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kThreads)
             float s = 0.f;
             if (hm2 > 0.f) {
                 float dd = fmaxf(dot3(normal, hv) * rsqrtf(hm2), 0.f);
-                s = powf(dd, __ldg(sa.mat + 8 * h.idx + 4));
+                s = blinn_pow(dd, __ldg(sa.mat + 8 * h.idx + 4));
             }
             const float3 so = hit + normal * 1e-3f;  // shadow (and reflection) origin
             const Cone cone = make_cone(so, light, sa.light_radius);

@@ -64,7 +64,7 @@ __device__ __forceinline__ void trace_chain(const Geo &geo, const FrameArgs &fa,
         float s = 0.f;
         if (hm2 > 0.f) {
             float dd = fmaxf(dot3(normal, hv) * rsqrtf(hm2), 0.f);
-            s = powf(dd, __ldg(sa.mat + 8 * h.idx + 4));
+            s = blinn_pow(dd, __ldg(sa.mat + 8 * h.idx + 4));
         }
         const int64_t slot = (int64_t)k * wa.n_pix + lp;
         wa.hit_p[slot] = make_float4(hit.x, hit.y, hit.z, __int_as_float(h.idx));
@@ -201,7 +201,7 @@ __device__ __forceinline__ void trace_chain_bundle(const ParamScene<MAXS> &ps, c
             float s = 0.f;
             if (hm2 > 0.f) {
                 float dd = fmaxf(dot3(normal, hv) * rsqrtf(hm2), 0.f);
-                s = powf(dd, __ldg(sa.mat + 8 * h.idx + 4));
+                s = blinn_pow(dd, __ldg(sa.mat + 8 * h.idx + 4));
             }
             slot_id = (int64_t)k * wa.n_pix + lp;
             wa.hit_p[slot_id] = make_float4(hit.x, hit.y, hit.z, __int_as_float(h.idx));

@@ -463,6 +463,8 @@ FLOP_PRIMARY = 36       # primary direction + pack
 FLOP_REFLECT = 18
 FLOP_SHADE = 45
 FLOP_CULL = 40          # one body's cone classification (centre offset, axial/radial split, 2 sqrt, compares)
+FLOP_CONIC = 17         # one silhouette-form sample test (|w|^2, x, y, d: 7 FMA + 1 add; culled sampler)
+FLOP_CONIC_SETUP = 120  # shadow frame, cone and the six coefficients of one (hit, sphere) pair
 
 
 def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True):
@@ -478,17 +480,22 @@ def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True):
         "shade": c["SHADE"] * FLOP_SHADE,
     }
     if culled and work.get("hits"):
-        flops["classify"] = work["cull_tests"] * FLOP_CULL
-        flops["shadow"] = (work["shadow_rays"] * setup + work["sampled_hits"] * (FLOP_BASIS if samples > 1 else 0)
-                           + work["sphere_tests"] * FLOP_SPHERE_FULL + work["plane_tests"] * FLOP_PLANE)
+        # the culled (fused) path: the trace kernel classifies its hits; the
+        # sampler runs silhouette-form tests, and ray-form ones for the rest
+        flops["trace"] += work["cull_tests"] * FLOP_CULL
+        flops["classify"] = 0
+        conic_hits, conic_tests = work.get("conic_hits", 0), work.get("conic_tests", 0)
+        ray_hits = work["sampled_hits"] - conic_hits
+        ray_rays = ray_hits * samples
+        flops["shadow"] = (conic_tests * FLOP_CONIC + conic_hits * FLOP_CONIC_SETUP
+                           + ray_rays * setup + ray_hits * (FLOP_BASIS if samples > 1 else 0)
+                           + (work["sphere_tests"] - conic_tests) * FLOP_SPHERE_FULL
+                           + work["plane_tests"] * FLOP_PLANE)
     else:
         sh_tests = c["SH_TCA"] + c["SH_DISC"] + c["SH_FULL"]
         flops["classify"] = 0
         flops["shadow"] = (c["SH_RAYS"] * setup + c["HITS"] * (FLOP_BASIS if samples > 1 else 0)
                            + sh_tests * FLOP_SPHERE_FULL + c["SH_PLANE"] * FLOP_PLANE)
-    if phases and phases.get("classify", 0) == 0 and flops.get("classify"):
-        flops["trace"] += flops["classify"]  # fused path: the trace kernel classifies its hits
-        flops["classify"] = 0
     if phases and sum(phases.values()) > 0:
         kernel = max(phases, key=phases.get)
         kms = phases[kernel]
@@ -497,6 +504,12 @@ def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True):
         kernel, kms, share = "megakernel", ms_frame, 1.0
         flops = {"megakernel": sum(flops.values())}
     achieved = flops[kernel] / (kms * 1e-3) / 1e12 if kms > 0 else 0.0
+    per_kernel = {}
+    if phases and sum(phases.values()) > 0:
+        for k, ms in phases.items():
+            if flops.get(k) and ms > 0.005:  # phases of a few us are event gaps, not kernels
+                a = flops[k] / (ms * 1e-3) / 1e12
+                per_kernel[k] = {"ms": ms, "flops": flops[k], "achieved": a, "frac": a / peak if peak else None}
     return {
         "bound": "fp32",
         "kernel": kernel,
@@ -512,6 +525,7 @@ def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True):
                        "MEASURED_PEAKS.json has no FP32 CUDA-core figure",
         "peak_nominal": NOMINAL_FP32_TFLOPS,
         "reference_equivalent_tflops": wcc["flops"] / (ms_frame * 1e-3) / 1e12,
+        "kernels": per_kernel,
     }
 
 

@@ -602,7 +602,10 @@ __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArg
         }
         resolve_hit(fa, sa, wa, slot, (float)(n - (int)blocked) / (float)n);
         if (wa.work) {
-            if (r != 0) atomicAdd(wa.work + kWorkConicHits, 1ull);
+            if (r != 0) {
+                atomicAdd(wa.work + kWorkConicHits, 1ull);
+                atomicAdd(wa.work + kWorkConicTests, (unsigned long long)n);
+            }
             atomicAdd(wa.work + kWorkSampledHits, 1ull);
             atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);
             atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n);
@@ -679,7 +682,10 @@ __global__ void __launch_bounds__(kThreads)
         }
         if (lane != 0) continue;
         if (wa.work) {
-            if (code != 0) atomicAdd(wa.work + kWorkConicHits, 1ull);
+            if (code != 0) {
+                atomicAdd(wa.work + kWorkConicHits, 1ull);
+                atomicAdd(wa.work + kWorkConicTests, (unsigned long long)n * nsph);
+            }
             atomicAdd(wa.work + kWorkSampledHits, 1ull);
             atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);
             atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n * nsph);

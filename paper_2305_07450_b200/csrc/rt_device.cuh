@@ -99,7 +99,7 @@ struct WaveArgs64 {
 
 // executed-work tallies of the culled shadow kernel (rt_work_counts)
 enum { kWorkHits = 0, kWorkCullTests, kWorkSampledHits, kWorkShadowRays, kWorkSphereTests, kWorkPlaneTests,
-       kWorkTraceRays, kWorkTraceTests, kWorkTraceFullWarps, kWorkConicHits, kWorkN };
+       kWorkTraceRays, kWorkTraceTests, kWorkTraceFullWarps, kWorkConicHits, kWorkConicTests, kWorkN };
 constexpr int kParamSpheres = 256;  // scenes up to this many spheres ride in the launch parameters
 constexpr int kMaskWords = kParamSpheres / 32;
 constexpr int kWaveMinSamples = 8;     // soft shadows at or above this take the wavefront path

@@ -135,6 +135,9 @@ int rt_host_unregister(rt_ctx *ctx, void *ptr);
  *                 and sphere, a quadratic per sample) instead of one ray per
  *                 sample — the reference's predicate, FP32 rounding near the
  *                 silhouette (off: the ray form, bit-identical to "cull" 0);
+ *   "cull_check"  (off) the culled pass leaves every body undecided, so each
+ *                 hit is sampled against all of them by the same kernels: with
+ *                 "conic" off, frames must equal the culled ones bit for bit;
  *   "count_work"  tally the executed work of the culled pass (rt_work_counts);
  *   "bands"       rt_render_v1 on one device renders this many contiguous row
  *                 bands (1-4) and copies each to the host while the next

@@ -43,10 +43,15 @@ constexpr int kRegCand = 4;  // candidate spheres a sampling warp keeps in regis
 // 0..kWords-1, planes in word kWords).
 template <int MAXS>
 __device__ __forceinline__ int classify_hit(const ParamScene<MAXS> &ps, const Cone &k, float oy, float ly,
-                                            unsigned *mask) {
+                                            unsigned *mask, bool check) {
     constexpr int kWords = (MAXS + 31) / 32;
 #pragma unroll
     for (int w = 0; w <= kWords; w++) mask[w] = 0;
+    if (check) {  // option cull_check: every body undecided
+        for (int b = 0; b < ps.ns; b++) mask[b >> 5] |= 1u << (b & 31);
+        mask[kWords] = (1u << ps.np) - 1u;
+        return ps.ns + ps.np > 0 ? 1 : 0;
+    }
     bool full = false;
     auto classify = [&](int b) {
         int cls = sphere_class(k, ps.sph[b], ps.sph_rad[b]);
@@ -248,7 +253,7 @@ __global__ void __launch_bounds__(kThreads)
             }
             const float3 so = hit + normal * 1e-3f;  // shadow (and reflection) origin
             const Cone cone = make_cone(so, light, sa.light_radius);
-            cls = classify_hit(ps, cone, so.y, light.y, mask);
+            cls = classify_hit(ps, cone, so.y, light.y, mask, wa.cull == 2);
             slot = (int64_t)k * wa.n_pix + lp;
             ridx[k] = h.idx;
             rdfs[k] = dfs;

@@ -76,7 +76,7 @@ struct WaveArgs {
     int *pend;         // culled path: per pixel, its hits still sampling (written when 2 or more)
     int64_t n_pix;     // pixels of this partition (local_rows * width)
     unsigned long long *work;  // optional executed-work tallies of the culled path (kWork*), or null
-    int cull;          // exact per-hit occluder culling in the shadow kernel
+    int cull;          // exact per-hit occluder culling (1); 2: every body left undecided (cull_check)
     float4 *conic;     // culled path: silhouette coefficients of queued hits, [2 kConic][conic_cap]
     unsigned conic_cap;  // queue positions below this may take the silhouette form (0: off)
     float4 *lane_q;    // culled path: single-candidate hits sampled one lane each: queue q (0: the

@@ -142,6 +142,7 @@ struct rt_ctx {
     bool phases = false;      // record per-phase events in wavefront frames (rt_phase_ms)
     int rgba = 0;             // pixel byte order of the frames written (0 B,G,R,A / 1 R,G,B,A)
     bool conic = true;        // culled FP32 path: silhouette form of the soft-shadow sphere test
+    bool cull_check = false;  // culled FP32 path: classify every body as undecided (an exactness check)
     bool zero_copy = false;   // kernels store straight into a registered (mapped) host framebuffer
     std::mutex mu;
     HostScene scene;
@@ -476,7 +477,7 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         wa.pix = (float4 *)d.w_pix.p;
         wa.rec = (float4 *)d.w_rec.p;
         wa.pend = (int *)d.w_pending.p;
-        wa.cull = fused;
+        wa.cull = fused ? (ctx->cull_check ? 2 : 1) : 0;
         wa.work = nullptr;
         if (ctx->count_work) {
             bool fresh = d.w_work.p == nullptr;
@@ -897,6 +898,7 @@ int rt_set_option(rt_ctx *ctx, const char *name, int32_t value) {
     else if (n == "rgba") ctx->rgba = value != 0;
     else if (n == "zero_copy") ctx->zero_copy = value != 0;
     else if (n == "conic") ctx->conic = value != 0;
+    else if (n == "cull_check") ctx->cull_check = value != 0;
     else return fail(RT_ERR_INVALID, "unknown option " + n);
     return RT_OK;
 }

@@ -2,7 +2,8 @@
 
 The culls (shadow-cone classification, cluster bounds, warp ray bundles) only
 skip tests that cannot change a result, so on any scene:
-  FP32 (ray form): culled frame == unculled wavefront frame, bit for bit;
+  FP32 (ray form): culled frame == the same kernels with every body left
+      undecided (option cull_check), bit for bit;
   FP32 (silhouette form, the default): within the parity gates of the FP64
       oracle, like every FP32 frame;
   FP64: culled frame == literal megakernel frame, bit for bit (and == the oracle).
@@ -18,8 +19,9 @@ from paper_2305_07450_b200 import _native
 
 pytestmark = pytest.mark.gpu
 
-MODES = {"cull": dict(wave=1, cull=1, conic=1), "ray": dict(wave=1, cull=1, conic=0),
-         "wave": dict(wave=1, cull=0, conic=1), "mega": dict(wave=0, cull=0, conic=1)}
+MODES = {"cull": dict(wave=1, cull=1, conic=1, cull_check=0), "ray": dict(wave=1, cull=1, conic=0, cull_check=0),
+         "check": dict(wave=1, cull=1, conic=0, cull_check=1),
+         "wave": dict(wave=1, cull=0, conic=1, cull_check=0), "mega": dict(wave=0, cull=0, conic=1, cull_check=0)}
 
 
 def random_scene(rng, n_spheres, with_plane=True, light_radius=None, sky=False):
@@ -74,8 +76,10 @@ def test_fp32_paths_bit_identical(seed, n, samples, bounces, plane, lr):
                     pitch=rng.uniform(-0.3, 0.1), fov=rng.uniform(40, 90))
     params = rt.RenderParams(samples, bounces, 120, 68)
     ray = render(scene, cam, params, "fp32", "ray")
+    check = render(scene, cam, params, "fp32", "check")
+    np.testing.assert_array_equal(ray, check)
     wave = render(scene, cam, params, "fp32", "wave")
-    np.testing.assert_array_equal(ray, wave)
+    parity.assert_byte_gate(ray, wave, f"ray vs unculled, seed {seed}")
     # the silhouette form: the reference's predicate, FP32 rounding near silhouettes
     px, rad = render(scene, cam, params, "fp32", "cull", radiance=True)
     ps = rt.pack_scene(scene)

@@ -108,20 +108,25 @@ def test_fp32_frames_byte_and_radiance_gates(name, fp32_mode):
 
 def test_culled_path_is_exact_against_unculled():
     """Culling only skips bodies that cannot block: the culled FP32 frames
-    (ray form) equal the unculled wavefront's bit for bit (same arithmetic per
-    test)."""
+    (ray form) equal, bit for bit, those of the same kernels with every body
+    left undecided (option cull_check: each hit sampled against all bodies),
+    and the unculled wavefront's within the parity gates."""
     for name in ("bench_128x72_s200_b3", "sweep_160x90_s16_b5_sky", "stress_96x54_s500_b8", "random4_64x36_s16_b4",
                  "c3like_192x108_s200_b3_sky", "blocked_32x18_s4_b1"):
         c = G.frame_case(name)
-        _native.set_options(wave=True, cull=False)
-        ref, rref = render_case(c, "fp32", radiance=True)
-        _native.set_options(wave=True, cull=True, conic=False)
         try:
+            _native.set_options(wave=True, cull=True, conic=False, cull_check=True)
+            ref, rref = render_case(c, "fp32", radiance=True)
+            _native.set_options(wave=True, cull=True, conic=False, cull_check=False)
             got, rgot = render_case(c, "fp32", radiance=True)
+            _native.set_options(wave=True, cull=False)
+            wave, rwave = render_case(c, "fp32", radiance=True)
         finally:
-            _native.set_options(**MODES["cull"])
+            _native.set_options(cull_check=False, **MODES["cull"])
         np.testing.assert_array_equal(got, ref, err_msg=name)
         np.testing.assert_array_equal(rgot, rref, err_msg=name)
+        parity.assert_byte_gate(got, wave, name)
+        parity.assert_radiance_gate(rgot, rwave, name)
 
 
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
@@ -310,7 +315,7 @@ def test_clustered_scene_modes_agree():
         rt.render_frame(s, cam, params, fb)
         frames[mode] = fb.pixels.copy()
     _native.set_options(**MODES["cull"])
-    np.testing.assert_array_equal(frames["ray"], frames["wave"])
+    parity.assert_byte_gate(frames["ray"], frames["wave"], "clustered ray vs wave")
     fb64 = rt.Framebuffer.create(160, 90)
     rt.render_frame(s, cam, params, fb64, precision="fp64")
     for mode, px in frames.items():

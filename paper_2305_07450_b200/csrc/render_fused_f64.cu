@@ -164,7 +164,34 @@ __global__ void __launch_bounds__(kThreads)
                 dir = vreflect(dir, normal);
             }
         }
-        const bool need = hit_now && cls == 1;
+        // a single candidate sphere: a lane of the lane sampler
+        int one = -1;
+        if (hit_now && cls == 1 && wa.lane_cap) {
+            int nc = 0;
+#pragma unroll
+            for (int w = 0; w < kWords64; w++) {
+                if (mask[w]) one = w * 32 + __ffs(mask[w]) - 1;
+                nc += __popc(mask[w]);
+            }
+            if (nc != 1 || geo[4 * one + 3] < 0.0) one = -1;
+        }
+        bool laned = false;
+        {
+            const bool want = one >= 0;
+            const unsigned lb = __ballot_sync(0xffffffffu, want);
+            if (lb) {
+                unsigned base = 0;
+                if (lane == 0) base = atomicAdd(wa.count + 3, (unsigned)__popc(lb));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                const unsigned e = base + __popc(lb & lanemask_lt());
+                if (want && e < wa.lane_cap) {
+                    wa.lane_q[2 * e] = make_double4(hit.x, hit.y, hit.z, (double)slot);
+                    wa.lane_q[2 * e + 1] = make_double4(normal.x, normal.y, normal.z, (double)one);
+                    laned = true;
+                }
+            }
+        }
+        const bool need = hit_now && cls == 1 && !laned;
         const unsigned nb = __ballot_sync(0xffffffffu, need);
         if (nb) {
             unsigned base = 0;
@@ -210,11 +237,106 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
-// --- B: one warp per undecided hit, the reference's shadow loop (renderer.py:82-105) ---
+// --- B1: single-sphere hits, one lane each, decisions exact ---------------------
+//
+// The reference's test of sample i against sphere g (renderer.py:90-103,
+// geometry.py:83-105) is, when the shadow origin o is clearly outside g and
+// |g - o| < |p - L| (so the entry point always precedes the limit),
+//   blocked  <=>  tca > 0  and  d2 <= r^2 + 1e-7,
+// a predicate on the real numbers that the silhouette form (rt_wave.cuh,
+// conic_coeffs, here in float64 with explicit FMAs) evaluates as the sign of
+// dd = x^2 + y^2 - |w|^2 (and z > 0 for tca).  Both the reference's literal
+// float64 arithmetic and this one approximate that predicate; their errors
+// are below c eps (s^2 + s (1 + 4R/H) + 1) |w|^2 with s = |u| / r (the literal
+// d2 = L.L - tca^2 cancels by s^2).  With tau = 1024 eps (...) |w|^2 far
+// above both, a sample with |dd| > tau is decided the way the reference
+// decides it; the rare sample inside the band takes the literal test.  Near
+// z = 0, d2 ~ |u|^2 > r^2 (1 + 1e-6): the z sign never decides there.  The
+// coefficient, unblocked / n, is thus the reference's bit for bit.
+__device__ void sample_lanes64(const FrameArgs &fa, const SceneArgs<double> &sa, const WaveArgs64 &wa,
+                               const double *geo) {
+    const int n = fa.samples;
+    const d3 lp = mk(sa.light[0], sa.light[1], sa.light[2]);
+    const double *tab = sa.table;
+    const unsigned count = min(wa.count[3], wa.lane_cap);
+    const unsigned units = (count + 31) / 32;
+    const unsigned first = (unsigned)(((unsigned long long)units * blockIdx.x) / gridDim.x);
+    const unsigned last = (unsigned)(((unsigned long long)units * (blockIdx.x + 1)) / gridDim.x);
+    const unsigned lane = threadIdx.x & 31;
+    for (unsigned u = first + (threadIdx.x >> 5); u < last; u += blockDim.x >> 5) {
+        const unsigned h = 32u * u + lane;
+        if (h >= count) continue;
+        const double4 P = wa.lane_q[2 * h], N = wa.lane_q[2 * h + 1];
+        const double *g = geo + 4 * (int)N.w;
+        const d3 surface = mk(P.x, P.y, P.z), normal = mk(N.x, N.y, N.z);
+        const d3 origin = mk(surface.x + 1e-3 * normal.x, surface.y + 1e-3 * normal.y, surface.z + 1e-3 * normal.z);
+        d3 bu, bv;
+        disc_basis(surface, lp, bu, bv);
+        // the silhouette coefficients and their preconditions
+        const d3 uc = mk(g[0] - origin.x, g[1] - origin.y, g[2] - origin.z);
+        const d3 lo = mk(lp.x - origin.x, lp.y - origin.y, lp.z - origin.z);
+        const d3 ls = mk(surface.x - lp.x, surface.y - lp.y, surface.z - lp.z);
+        const double u2 = fma(uc.z, uc.z, fma(uc.y, uc.y, uc.x * uc.x));
+        const double r2g = g[3] + 1e-7;
+        const double un = sqrt(u2), H = sqrt(fma(lo.z, lo.z, fma(lo.y, lo.y, lo.x * lo.x)));
+        const double rho = 2.0 * sa.light_radius * (1.0 + 1e-6) + 1e-9;
+        bool conic = u2 > r2g * (1.0 + 1e-6) + 1e-12 && un * (1.0 + 1e-8) + 1e-12 <
+                     sqrt(fma(ls.z, ls.z, fma(ls.y, ls.y, ls.x * ls.x))) && H > 1.001 * rho;
+        double x0 = 0, x1 = 0, x2 = 0, y0 = 0, y1 = 0, y2 = 0, z0 = 1, z1 = 0, z2 = 0, b0 = 0, b1 = 0, b2 = 0,
+               tau = 0;
+        bool front = false;
+        if (conic) {
+            const d3 nu = mk(uc.x / un, uc.y / un, uc.z / un);
+            const d3 ax = mk(lo.x / H, lo.y / H, lo.z / H);
+            const double hh = fma(uc.z, ax.z, fma(uc.y, ax.y, uc.x * ax.x));
+            const d3 wp = mk(fma(-ax.x, hh, uc.x), fma(-ax.y, hh, uc.y), fma(-ax.z, hh, uc.z));
+            const double q = sqrt(fma(wp.z, wp.z, fma(wp.y, wp.y, wp.x * wp.x)));
+            const double sin_phi = rho / H, cos_phi = sqrt(1.0 - sin_phi * sin_phi);
+            front = hh * cos_phi - q * sin_phi > 1e-8 * (fabs(hh) + q) + 1e-12;
+            const double sg = nu.z >= 0.0 ? 1.0 : -1.0;
+            const double ia = -1.0 / (sg + nu.z);
+            const double bb = nu.x * nu.y * ia;
+            const d3 e1 = mk(fma(sg * nu.x * nu.x, ia, 1.0), sg * bb, -sg * nu.x);
+            const d3 e2 = mk(bb, fma(nu.y * nu.y, ia, sg), -nu.y);
+            const double sc = un / sqrt(r2g);
+            auto dot = [](d3 a, d3 b) { return fma(a.z, b.z, fma(a.y, b.y, a.x * b.x)); };
+            x0 = sc * dot(e1, lo), x1 = sc * dot(e1, bu), x2 = sc * dot(e1, bv);
+            y0 = sc * dot(e2, lo), y1 = sc * dot(e2, bu), y2 = sc * dot(e2, bv);
+            z0 = dot(nu, lo), z1 = dot(nu, bu), z2 = dot(nu, bv);
+            b0 = dot(lo, lo), b1 = 2.0 * dot(lo, bu), b2 = 2.0 * dot(lo, bv);
+            const double s = un / sqrt(g[3] > 0.0 ? g[3] : 1e-300);
+            tau = 1024.0 * 2.220446049250313e-16 * (s * s + s * (1.0 + 4.0 * sa.light_radius / H) + 1.0);
+            if (!(tau < 1e-3)) conic = false;  // ill-conditioned: every sample literal
+        }
+        int unblocked = 0;
+        for (int i = 0; i < n; i++) {
+            const double a = __ldg(tab + 2 * i), b = __ldg(tab + 2 * i + 1);
+            int decided = -1;  // 1 blocked, 0 open, -1 literal
+            if (conic) {
+                const double w2 = fma(b1, a, fma(b2, b, b0)) + fma(a, a, b * b);
+                const double x = fma(x1, a, fma(x2, b, x0)), y = fma(y1, a, fma(y2, b, y0));
+                const double dd = fma(x, x, fma(y, y, -w2));
+                const double band = tau * w2;
+                if (dd > band) decided = 0;
+                else if (dd < -band) decided = (front || fma(z1, a, fma(z2, b, z0)) > 0.0) ? 1 : 0;
+            }
+            if (decided < 0) {  // the reference's literal test (renderer.py:90-103)
+                const d3 s = disc_point(i, lp, bu, bv, tab);
+                const d3 d = vnormalize(vsub(s, origin));
+                decided = intersect(origin, d, g) < vdistance(surface, s) ? 1 : 0;
+            }
+            unblocked += 1 - decided;
+        }
+        wa.rec[(int64_t)P.w].w = (double)unblocked / (double)n;
+    }
+}
+
+// --- B2: one warp per undecided hit, the reference's shadow loop (renderer.py:82-105) ---
 __global__ void __launch_bounds__(kThreads)
     fused64_sample(const FrameArgs fa, const SceneArgs<double> sa, const WaveArgs64 wa) {
     extern __shared__ double smem_geo[];
     const double *__restrict__ geo = stage(sa, smem_geo);
+    if (wa.lane_cap) sample_lanes64(fa, sa, wa, geo);
     const unsigned count = wa.count[1];
     const int lane = threadIdx.x & 31;
     const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;

@@ -95,6 +95,8 @@ struct WaveArgs64 {
     double4 *rec;      // {body, Lambert, Blinn, coefficient} per hit of a parked pixel
     int *parked;       // parked pixels (local indices)
     int64_t n_pix;
+    double4 *lane_q;   // single-sphere undecided hits, one sampling lane each: [2e] {p, slot}, [2e+1] {n, body}
+    unsigned lane_cap; // (0: off); length count[3]
 };
 
 // executed-work tallies of the culled shadow kernel (rt_work_counts)

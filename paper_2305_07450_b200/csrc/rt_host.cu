@@ -88,7 +88,7 @@ struct Dev {
     bool ph_valid = false;
     DBuf frame, rad, rays_in, rays_out, sky_raw, sky, counters;
     DBuf w_p, w_n, w_s, w_sc, w_queue, w_queue2, w_mask2, w_count, w_pix, w_work, w_rec, w_pending, w_conic, w_lane;
-    DBuf d_q, d_mask, d_pix, d_rec, d_parked;  // FP64 culled wavefront queues  // wavefront queues (FP32 soft shadows)
+    DBuf d_q, d_mask, d_pix, d_rec, d_parked, d_lane;  // FP64 culled wavefront queues  // wavefront queues (FP32 soft shadows)
     unsigned counter_slot = 0;
     uint64_t sky_version = ~0ull;
     DevScene<float> s32;
@@ -432,6 +432,11 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         wa.pix = (double4 *)d.d_pix.p;
         wa.rec = (double4 *)d.d_rec.p;
         wa.parked = (int *)d.d_parked.p;
+        if (ctx->conic) {  // single-sphere hits sampled one lane each (render_fused_f64.cu)
+            if ((rc = d.d_lane.ensure(2 * sizeof(double4) * (size_t)wa.n_pix))) return rc;
+            wa.lane_q = (double4 *)d.d_lane.p;
+            wa.lane_cap = (unsigned)wa.n_pix;
+        }
         int nk = 0;
         e = rt_launch_fused_f64(fa, scene_args(d, d.s64, ctx->scene), wa, st, &nk);
         ctx->launches += nk - 1;
@@ -572,7 +577,7 @@ int rt_ctx_destroy(rt_ctx *ctx) {
         cudaSetDevice(d.id);
         if (d.st) cudaStreamSynchronize(d.st);
         for (DBuf *b : {&d.w_p, &d.w_n, &d.w_s, &d.w_sc, &d.w_queue, &d.w_queue2, &d.w_mask2, &d.w_count, &d.w_pix,
-                        &d.w_work, &d.w_rec, &d.w_pending, &d.w_conic, &d.w_lane, &d.d_q, &d.d_mask, &d.d_pix, &d.d_rec, &d.d_parked})
+                        &d.w_work, &d.w_rec, &d.w_pending, &d.w_conic, &d.w_lane, &d.d_q, &d.d_mask, &d.d_pix, &d.d_rec, &d.d_parked, &d.d_lane})
             b->release();
         for (DBuf *b : {&d.frame, &d.rad, &d.rays_in, &d.rays_out, &d.sky_raw, &d.sky, &d.counters, &d.s32.geo, &d.s32.mat,
                         &d.s32.table, &d.s64.geo, &d.s64.mat, &d.s64.table})

@@ -258,6 +258,7 @@ __device__ void sample_lanes64(const FrameArgs &fa, const SceneArgs<double> &sa,
     const int n = fa.samples;
     const d3 lp = mk(sa.light[0], sa.light[1], sa.light[2]);
     const double *tab = sa.table;
+    const double2 *tab2 = reinterpret_cast<const double2 *>(tab);  // {r cos, r sin} per sample (host libm)
     const unsigned count = min(wa.count[3], wa.lane_cap);
     const unsigned units = (count + 31) / 32;
     const unsigned first = (unsigned)(((unsigned long long)units * blockIdx.x) / gridDim.x);
@@ -308,24 +309,40 @@ __device__ void sample_lanes64(const FrameArgs &fa, const SceneArgs<double> &sa,
             tau = 1024.0 * 2.220446049250313e-16 * (s * s + s * (1.0 + 4.0 * sa.light_radius / H) + 1.0);
             if (!(tau < 1e-3)) conic = false;  // ill-conditioned: every sample literal
         }
-        int unblocked = 0;
-        for (int i = 0; i < n; i++) {
-            const double a = __ldg(tab + 2 * i), b = __ldg(tab + 2 * i + 1);
-            int decided = -1;  // 1 blocked, 0 open, -1 literal
-            if (conic) {
-                const double w2 = fma(b1, a, fma(b2, b, b0)) + fma(a, a, b * b);
-                const double x = fma(x1, a, fma(x2, b, x0)), y = fma(y1, a, fma(y2, b, y0));
-                const double dd = fma(x, x, fma(y, y, -w2));
-                const double band = tau * w2;
-                if (dd > band) decided = 0;
-                else if (dd < -band) decided = (front || fma(z1, a, fma(z2, b, z0)) > 0.0) ? 1 : 0;
+        // pass 1: the silhouette decisions (the band's samples counted, not decided)
+        int unblocked = 0, amb = n;
+        auto sil = [&](int i, double &dd, double &band, double &a, double &b) {
+            const double2 t = tab2[i];
+            a = t.x;
+            b = t.y;
+            const double w2 = fma(b1, a, fma(b2, b, b0)) + fma(a, a, b * b);
+            const double x = fma(x1, a, fma(x2, b, x0)), y = fma(y1, a, fma(y2, b, y0));
+            dd = fma(x, x, fma(y, y, -w2));
+            band = tau * w2;
+        };
+        if (conic) {
+            amb = 0;
+#pragma unroll 4
+            for (int i = 0; i < n; i++) {
+                double dd, band, a, b;
+                sil(i, dd, band, a, b);
+                const bool open = dd > band || (dd < -band && !(front || fma(z1, a, fma(z2, b, z0)) > 0.0));
+                unblocked += open ? 1 : 0;
+                amb += fabs(dd) <= band ? 1 : 0;
             }
-            if (decided < 0) {  // the reference's literal test (renderer.py:90-103)
+        }
+        // pass 2 (rare): the band's samples by the reference's literal test (renderer.py:90-103)
+        if (amb) {
+            for (int i = 0; i < n; i++) {
+                if (conic) {
+                    double dd, band, a, b;
+                    sil(i, dd, band, a, b);
+                    if (!(fabs(dd) <= band)) continue;
+                }
                 const d3 s = disc_point(i, lp, bu, bv, tab);
                 const d3 d = vnormalize(vsub(s, origin));
-                decided = intersect(origin, d, g) < vdistance(surface, s) ? 1 : 0;
+                unblocked += intersect(origin, d, g) < vdistance(surface, s) ? 0 : 1;
             }
-            unblocked += 1 - decided;
         }
         wa.rec[(int64_t)P.w].w = (double)unblocked / (double)n;
     }

@@ -103,3 +103,41 @@ def test_fp64_culled_equals_literal_and_oracle(seed, n, samples, bounces, plane,
     ps = rt.pack_scene(scene)
     want = oracle.render(vars(ps), cam.position, cam.yaw, cam.pitch, cam.fov, w, h, samples, bounces)
     np.testing.assert_array_equal(culled, want)
+
+
+def adversarial_scene(kind, rng):
+    """Scenes that stress the FP64 lane sampler's exactness band: tiny far
+    occluders (badly conditioned silhouettes), a light nearly touching a
+    sphere, terminator self-shadowing, and a scene far from the origin."""
+    bodies = []
+    off = np.array([0.0, 0.0, 0.0])
+    lr = 0.6
+    if kind == "tiny":
+        for _ in range(12):
+            bodies.append(rt.Body.sphere(tuple(rng.uniform([-3, 0.5, -1], [3, 5, 8])), rng.uniform(0.005, 0.05),
+                                         (0.8, 0.8, 0.8), 16.0))
+    elif kind == "near_light":
+        bodies.append(rt.Body.sphere((-3.2, 6.1, -1.7), 0.5, (0.9, 0.2, 0.2), 8.0))
+        bodies.append(rt.Body.sphere((0.0, 0.8, 1.6), 0.8, (0.1, 0.5, 0.1), 32.0))
+        lr = 1.1
+    elif kind == "terminator":
+        for i in range(6):
+            bodies.append(rt.Body.sphere((-3.0 + 1.2 * i, 0.5, 2.0 + 0.3 * i), 0.5, (0.7, 0.7, 0.2), 64.0))
+    elif kind == "far":
+        off = np.array([1000.0, 0.0, -2000.0])
+        for _ in range(6):
+            c = rng.uniform([-3, 0.3, 0], [3, 2.5, 6]) + off
+            bodies.append(rt.Body.sphere(tuple(c), rng.uniform(0.2, 1.0), (0.5, 0.6, 0.7), 32.0))
+    bodies.append(rt.Body.plane(0.0, (0.4, 0.45, 0.5), 16.0))
+    light = rt.Light(tuple(np.array([-4.0, 7.0, -2.0]) + off), lr)
+    cam = rt.Camera(position=tuple(np.array([0.0, 1.4, -4.5]) + off), yaw=0.0, pitch=-0.08, fov=60.0)
+    return rt.Scene(bodies=bodies, light=light), cam
+
+
+@pytest.mark.parametrize("kind", ["tiny", "near_light", "terminator", "far"])
+def test_fp64_lane_sampler_exact_on_adversarial_scenes(kind):
+    scene, cam = adversarial_scene(kind, np.random.default_rng(7))
+    params = rt.RenderParams(64, 3, 128, 72)
+    culled = render(scene, cam, params, "fp64", "cull")
+    literal = render(scene, cam, params, "fp64", "mega")
+    np.testing.assert_array_equal(culled, literal)

@@ -316,11 +316,18 @@ def run_ours(args):
         """Frames/s, per-phase device times and executed work of config c."""
         r = time_config(c, warmup, steps, sample_clocks)
         fps_c = len(r["ms"]) / (r["total_ms"] / 1e3)
-        # one more (untimed) frame with phase events and work tallies on
+        # per-kernel device times: CUDA events between the kernels on their
+        # launch stream, averaged over as many frames as were timed (events
+        # cost ~2.5 us each, so they stay out of the timed region itself)
         ctx.set_option("phases", 1)
-        render_cfg(c)
-        torch.cuda.synchronize()
-        phases = ctx.phase_ms()
+        acc = {}
+        n_ph = max(3, min(steps, 50))
+        for _ in range(n_ph):
+            render_cfg(c)
+            torch.cuda.synchronize()
+            for k, v in ctx.phase_ms().items():
+                acc[k] = acc.get(k, 0.0) + v / n_ph
+        phases = acc
         ctx.set_option("phases", 0)
         ctx.set_option("count_work", 1)
         ctx.work_counts(reset=True)

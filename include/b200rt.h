@@ -140,9 +140,10 @@ int rt_host_unregister(rt_ctx *ctx, void *ptr);
  *                 "conic" off, frames must equal the culled ones bit for bit;
  *   "count_work"  tally the executed work of the culled pass (rt_work_counts);
  *   "bands"       rt_render_v1 on one device renders this many contiguous row
- *                 bands (1-4) and copies each to the host while the next
- *                 renders; 0 (default) = by frame size: 1 below 1 MB, 2 below
- *                 6 MB, 3 below 16 MB, else 4;
+ *                 bands (1-8), each on its own stream (band 0 at the highest
+ *                 priority), and copies each to the host as soon as it is
+ *                 done; 0 (default) = by frame size: 1 below 1 MB, 2 below
+ *                 6 MB, 4 below 24 MB, else 6;
  *   "phases"      record CUDA events between the wavefront kernels so
  *                 rt_phase_ms can report per-phase device times (off by
  *                 default: each event record costs the GPU ~2-3 us);

@@ -207,7 +207,7 @@ _options = {}  # execution options applied to every context (rt_set_option)
 
 def set_options(**opts) -> None:
     """Execution options for every context, present and future:
-    wave (bool), cull (bool), conic (bool), count_work (bool), bands (0-4) — see
+    wave (bool), cull (bool), conic (bool), count_work (bool), bands (0-8) — see
     include/b200rt.h (rt_set_option)."""
     with _ctx_lock:
         _options.update({k: int(v) for k, v in opts.items()})

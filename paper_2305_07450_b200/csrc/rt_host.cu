@@ -78,17 +78,35 @@ struct DevScene {
     double table_radius = NAN;
 };
 
+// Queues of one wavefront frame (or row band): FP32 wavefront / culled path
+// (w_*) and FP64 culled path (d_*).
+struct WaveBufs {
+    DBuf w_p, w_n, w_s, w_sc, w_queue, w_queue2, w_mask2, w_count, w_pix, w_rec, w_pending, w_conic, w_lane;
+    DBuf d_q, d_mask, d_pix, d_rec, d_parked, d_lane;
+    void release() {
+        for (DBuf *b : {&w_p, &w_n, &w_s, &w_sc, &w_queue, &w_queue2, &w_mask2, &w_count, &w_pix, &w_rec, &w_pending,
+                        &w_conic, &w_lane, &d_q, &d_mask, &d_pix, &d_rec, &d_parked, &d_lane})
+            b->release();
+    }
+};
+
+constexpr int kMaxBands = 8;
+
 struct Dev {
     int id = 0;
     cudaStream_t st = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     cudaEvent_t ph[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // wavefront phase boundaries
     cudaStream_t copy_st = nullptr;           // device->host copies of finished row bands
-    cudaEvent_t band_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t band_ev[kMaxBands] = {};
+    // row bands run on their own streams, band 0 at the highest priority: the
+    // next band's CTAs fill the SMs a band's tail leaves idle, yet the bands
+    // finish in order, so each copy starts as early as it can
+    cudaStream_t band_st[kMaxBands] = {};
+    cudaEvent_t fork_ev = nullptr;
     bool ph_valid = false;
-    DBuf frame, rad, rays_in, rays_out, sky_raw, sky, counters;
-    DBuf w_p, w_n, w_s, w_sc, w_queue, w_queue2, w_mask2, w_count, w_pix, w_work, w_rec, w_pending, w_conic, w_lane;
-    DBuf d_q, d_mask, d_pix, d_rec, d_parked, d_lane;  // FP64 culled wavefront queues  // wavefront queues (FP32 soft shadows)
+    DBuf frame, rad, rays_in, rays_out, sky_raw, sky, counters, w_work;
+    WaveBufs wb[kMaxBands];
     unsigned counter_slot = 0;
     uint64_t sky_version = ~0ull;
     DevScene<float> s32;
@@ -406,7 +424,8 @@ rt::FrameArgs frame_args(uint32_t *out, int64_t pitch, void *rad, int w, int h, 
     return fa;
 }
 
-int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStream_t st) {
+int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStream_t st, int buf = 0) {
+    WaveBufs &b = d.wb[buf];
     cudaError_t e;
     fa.rgba = ctx->rgba;
     if (fa.local_rows == 0) return RT_OK;
@@ -420,21 +439,21 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         rt::WaveArgs64 wa = {};
         wa.n_pix = (int64_t)fa.local_rows * fa.width;
         size_t slots = (size_t)wa.n_pix * (fa.bounces + 1);
-        if ((rc = d.d_q.ensure(2 * sizeof(double4) * slots)) ||
-            (rc = d.d_mask.ensure(sizeof(unsigned) * slots * (rt::kMaxBodies64 / 32))) ||
-            (rc = d.d_pix.ensure(sizeof(double4) * (size_t)wa.n_pix)) || (rc = d.d_rec.ensure(sizeof(double4) * slots)) ||
-            (rc = d.d_parked.ensure(sizeof(int) * (size_t)wa.n_pix)) || (rc = d.w_count.ensure(4 * sizeof(unsigned))))
+        if ((rc = b.d_q.ensure(2 * sizeof(double4) * slots)) ||
+            (rc = b.d_mask.ensure(sizeof(unsigned) * slots * (rt::kMaxBodies64 / 32))) ||
+            (rc = b.d_pix.ensure(sizeof(double4) * (size_t)wa.n_pix)) || (rc = b.d_rec.ensure(sizeof(double4) * slots)) ||
+            (rc = b.d_parked.ensure(sizeof(int) * (size_t)wa.n_pix)) || (rc = b.w_count.ensure(4 * sizeof(unsigned))))
             return rc;
-        wa.q = (double4 *)d.d_q.p;
-        wa.mask = (unsigned *)d.d_mask.p;
+        wa.q = (double4 *)b.d_q.p;
+        wa.mask = (unsigned *)b.d_mask.p;
         wa.mask_stride = (int64_t)slots;
-        wa.count = (unsigned *)d.w_count.p;
-        wa.pix = (double4 *)d.d_pix.p;
-        wa.rec = (double4 *)d.d_rec.p;
-        wa.parked = (int *)d.d_parked.p;
+        wa.count = (unsigned *)b.w_count.p;
+        wa.pix = (double4 *)b.d_pix.p;
+        wa.rec = (double4 *)b.d_rec.p;
+        wa.parked = (int *)b.d_parked.p;
         if (ctx->conic) {  // single-sphere hits sampled one lane each (render_fused_f64.cu)
-            if ((rc = d.d_lane.ensure(2 * sizeof(double4) * (size_t)wa.n_pix))) return rc;
-            wa.lane_q = (double4 *)d.d_lane.p;
+            if ((rc = b.d_lane.ensure(2 * sizeof(double4) * (size_t)wa.n_pix))) return rc;
+            wa.lane_q = (double4 *)b.d_lane.p;
             wa.lane_cap = (unsigned)wa.n_pix;
         }
         int nk = 0;
@@ -448,40 +467,40 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         rt::WaveArgs wa = {};
         wa.n_pix = (int64_t)fa.local_rows * fa.width;
         size_t slots = (size_t)wa.n_pix * (fa.bounces + 1);
-        if ((rc = d.w_p.ensure(sizeof(float4) * slots)) || (rc = d.w_n.ensure(sizeof(float4) * slots)) ||
-            (rc = d.w_count.ensure(8 * sizeof(unsigned))) || (rc = d.w_pix.ensure(sizeof(float4) * (size_t)wa.n_pix)))
+        if ((rc = b.w_p.ensure(sizeof(float4) * slots)) || (rc = b.w_n.ensure(sizeof(float4) * slots)) ||
+            (rc = b.w_count.ensure(8 * sizeof(unsigned))) || (rc = b.w_pix.ensure(sizeof(float4) * (size_t)wa.n_pix)))
             return rc;
         if (fused) {
-            if ((rc = d.w_queue2.ensure(sizeof(int) * slots)) ||
-                (rc = d.w_mask2.ensure(sizeof(unsigned) * slots * (ctx->scene.n <= 8 ? 2 : rt::kMaskWords + 1))) ||
-                (rc = d.w_rec.ensure(sizeof(float4) * slots)) ||
-                (rc = d.w_pending.ensure(sizeof(int) * (size_t)wa.n_pix)))  // pend
+            if ((rc = b.w_queue2.ensure(sizeof(int) * slots)) ||
+                (rc = b.w_mask2.ensure(sizeof(unsigned) * slots * (ctx->scene.n <= 8 ? 2 : rt::kMaskWords + 1))) ||
+                (rc = b.w_rec.ensure(sizeof(float4) * slots)) ||
+                (rc = b.w_pending.ensure(sizeof(int) * (size_t)wa.n_pix)))  // pend
                 return rc;
             if (ctx->conic) {  // silhouette coefficients for the first n_pix queued hits
-                if ((rc = d.w_conic.ensure(sizeof(float4) * 2 * rt::kConic * (size_t)wa.n_pix))) return rc;
-                wa.conic = (float4 *)d.w_conic.p;
+                if ((rc = b.w_conic.ensure(sizeof(float4) * 2 * rt::kConic * (size_t)wa.n_pix))) return rc;
+                wa.conic = (float4 *)b.w_conic.p;
                 wa.conic_cap = (unsigned)wa.n_pix;
-                if ((rc = d.w_lane.ensure(sizeof(float4) * 4 * (size_t)wa.n_pix))) return rc;
-                wa.lane_q = (float4 *)d.w_lane.p;
+                if ((rc = b.w_lane.ensure(sizeof(float4) * 4 * (size_t)wa.n_pix))) return rc;
+                wa.lane_q = (float4 *)b.w_lane.p;
                 wa.lane_cap = (unsigned)wa.n_pix;
             }
         } else {
-            if ((rc = d.w_s.ensure(sizeof(float) * slots)) || (rc = d.w_sc.ensure(sizeof(float) * slots)) ||
-                (rc = d.w_queue.ensure(sizeof(int) * slots)))
+            if ((rc = b.w_s.ensure(sizeof(float) * slots)) || (rc = b.w_sc.ensure(sizeof(float) * slots)) ||
+                (rc = b.w_queue.ensure(sizeof(int) * slots)))
                 return rc;
         }
-        wa.hit_p = (float4 *)d.w_p.p;
-        wa.hit_n = (float4 *)d.w_n.p;
-        wa.hit_s = (float *)d.w_s.p;
-        wa.hit_sc = (float *)d.w_sc.p;
-        wa.queue = (int *)d.w_queue.p;
-        wa.count = (unsigned *)d.w_count.p;
-        wa.queue2 = (int *)d.w_queue2.p;
-        wa.mask2 = (unsigned *)d.w_mask2.p;
+        wa.hit_p = (float4 *)b.w_p.p;
+        wa.hit_n = (float4 *)b.w_n.p;
+        wa.hit_s = (float *)b.w_s.p;
+        wa.hit_sc = (float *)b.w_sc.p;
+        wa.queue = (int *)b.w_queue.p;
+        wa.count = (unsigned *)b.w_count.p;
+        wa.queue2 = (int *)b.w_queue2.p;
+        wa.mask2 = (unsigned *)b.w_mask2.p;
         wa.mask2_stride = (int64_t)slots;
-        wa.pix = (float4 *)d.w_pix.p;
-        wa.rec = (float4 *)d.w_rec.p;
-        wa.pend = (int *)d.w_pending.p;
+        wa.pix = (float4 *)b.w_pix.p;
+        wa.rec = (float4 *)b.w_rec.p;
+        wa.pend = (int *)b.w_pending.p;
         wa.cull = fused ? (ctx->cull_check ? 2 : 1) : 0;
         wa.work = nullptr;
         if (ctx->count_work) {
@@ -559,6 +578,12 @@ int rt_ctx_create(rt_ctx **out, const int32_t *devices, int32_t n_devices) {
                   cudaStreamCreateWithFlags(&d.copy_st, cudaStreamNonBlocking) == cudaSuccess &&
                   cudaEventCreate(&d.e0) == cudaSuccess && cudaEventCreate(&d.e1) == cudaSuccess;
         for (auto &ev : d.band_ev) ok = ok && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess;
+        ok = ok && cudaEventCreateWithFlags(&d.fork_ev, cudaEventDisableTiming) == cudaSuccess;
+        int least = 0, greatest = 0;
+        if (ok) cudaDeviceGetStreamPriorityRange(&least, &greatest);
+        for (int k = 0; ok && k < kMaxBands; k++)
+            ok = cudaStreamCreateWithPriority(&d.band_st[k], cudaStreamNonBlocking, std::min(least, greatest + k)) ==
+                 cudaSuccess;
         if (!ok) {
             std::string m = cudaGetErrorString(cudaGetLastError());
             ctx->devs.push_back(d);
@@ -576,9 +601,8 @@ int rt_ctx_destroy(rt_ctx *ctx) {
     for (Dev &d : ctx->devs) {
         cudaSetDevice(d.id);
         if (d.st) cudaStreamSynchronize(d.st);
-        for (DBuf *b : {&d.w_p, &d.w_n, &d.w_s, &d.w_sc, &d.w_queue, &d.w_queue2, &d.w_mask2, &d.w_count, &d.w_pix,
-                        &d.w_work, &d.w_rec, &d.w_pending, &d.w_conic, &d.w_lane, &d.d_q, &d.d_mask, &d.d_pix, &d.d_rec, &d.d_parked, &d.d_lane})
-            b->release();
+        for (WaveBufs &wb : d.wb) wb.release();
+        d.w_work.release();
         for (DBuf *b : {&d.frame, &d.rad, &d.rays_in, &d.rays_out, &d.sky_raw, &d.sky, &d.counters, &d.s32.geo, &d.s32.mat,
                         &d.s32.table, &d.s64.geo, &d.s64.mat, &d.s64.table})
             b->release();
@@ -586,6 +610,9 @@ int rt_ctx_destroy(rt_ctx *ctx) {
             if (ev) cudaEventDestroy(ev);
         for (auto ev : d.band_ev)
             if (ev) cudaEventDestroy(ev);
+        for (auto bs : d.band_st)
+            if (bs) cudaStreamDestroy(bs);
+        if (d.fork_ev) cudaEventDestroy(d.fork_ev);
         if (d.copy_st) cudaStreamDestroy(d.copy_st);
         if (d.e0) cudaEventDestroy(d.e0);
         if (d.e1) cudaEventDestroy(d.e1);
@@ -667,15 +694,21 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
             return RT_OK;
         }
         cudaGetLastError();  // not registered: a cudaHostGetDevicePointer miss is not an error
-        // A band adds ~8-15 us of kernel boundaries and tails; the copy it hides
-        // runs at ~45 GB/s (82 us for 720p).  Measured best (tools/e2e_bands.py):
-        // 2 bands at 3.7 MB, 3 at 8.3 MB, 4 at 33 MB.
+        // Bands run on their own prioritised streams (Dev::band_st), so their
+        // kernels overlap; what a band costs is its first-band latency and
+        // copy setup, against a copy at 45-56 GB/s (82 us for 720p, 600 us at
+        // 4K).  Measured best (tools/e2e_probe.py): 2 bands at 3.7 MB, 4 at
+        // 8.3 MB, 6 at 33 MB.
         const size_t MB = (size_t)1 << 20;
-        int bands = ctx->bands > 0 ? ctx->bands : px_bytes < MB ? 1 : px_bytes < 6 * MB ? 2 : px_bytes < 16 * MB ? 3 : 4;
+        int bands = ctx->bands > 0 ? ctx->bands : px_bytes < MB ? 1 : px_bytes < 6 * MB ? 2 : px_bytes < 24 * MB ? 4 : 6;
+        if (ctx->phases) bands = 1;  // phase events describe one frame on one stream
         bands = std::max(1, std::min(bands, height / 8));
         const int band_rows = (height + bands - 1) / bands;
         RT_CK(cudaEventRecord(d.e0, d.st));
+        if (bands > 1) RT_CK(cudaEventRecord(d.fork_ev, d.st));
         for (int k = 0; k < bands; k++) {
+            cudaStream_t bs = bands > 1 ? d.band_st[k] : d.st;
+            if (bands > 1) RT_CK(cudaStreamWaitEvent(bs, d.fork_ev, 0));
             for (int p = 0; p < n_parts; p++) {  // the caller's partitions inside the band, same device
                 rt::FrameArgs fa = frame_args((uint32_t *)d.frame.p, width, radiance ? d.rad.p : nullptr, width,
                                               height, cam_pos, yaw, pitch, vdist, shadow_samples, bounce_limit, 0, 1,
@@ -688,10 +721,11 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
                 fa.sub_parts = n_parts;
                 fa.local_rows = rt::rt_band_local_rows(height, k, bands, band_rows, p, n_parts);
                 fa.row_end = std::min(height, (k + 1) * band_rows);
-                if ((rc = launch_frame(ctx, d, fa, precision, d.st))) return rc;
+                if ((rc = launch_frame(ctx, d, fa, precision, bs, k))) return rc;
             }
-            RT_CK(cudaEventRecord(d.band_ev[k], d.st));
+            RT_CK(cudaEventRecord(d.band_ev[k], bs));
             RT_CK(cudaStreamWaitEvent(d.copy_st, d.band_ev[k], 0));
+            if (bands > 1) RT_CK(cudaStreamWaitEvent(d.st, d.band_ev[k], 0));  // the join
             const int y0 = k * band_rows, y1 = std::min(height, y0 + band_rows);
             if (y1 > y0) {
                 size_t off = (size_t)y0 * width, cnt = (size_t)(y1 - y0) * width;
@@ -898,7 +932,7 @@ int rt_set_option(rt_ctx *ctx, const char *name, int32_t value) {
     if (n == "wave") ctx->wave = value != 0;
     else if (n == "cull") ctx->cull = value != 0;
     else if (n == "count_work") ctx->count_work = value != 0;
-    else if (n == "bands") ctx->bands = std::max(0, std::min((int)value, 4));
+    else if (n == "bands") ctx->bands = std::max(0, std::min((int)value, kMaxBands));
     else if (n == "phases") ctx->phases = value != 0;
     else if (n == "rgba") ctx->rgba = value != 0;
     else if (n == "zero_copy") ctx->zero_copy = value != 0;

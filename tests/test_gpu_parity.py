@@ -386,3 +386,28 @@ def test_zero_copy_option_gives_the_same_frame():
         np.testing.assert_array_equal(fb.pixels, base)
     finally:
         _native.set_options(zero_copy=0)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_copy_overlap_bands_do_not_change_pixels(precision):
+    """rt_render_v1's row bands (option bands, 1-8, each on its own stream,
+    copied as soon as it is done) partition the frame: same bytes, same
+    radiance, with and without several partitions inside each band."""
+    s = rt.build_benchmark_scene()
+    cam = rt.benchmark_camera()
+    params = rt.RenderParams(32, 3, 240, 136)
+    dt = np.float32 if precision == "fp32" else np.float64
+    ref = None
+    try:
+        for bands in (1, 2, 3, 5, 8):
+            for workers in (None, 3):
+                _native.set_options(bands=bands)
+                fb = rt.Framebuffer.create(240, 136)
+                rad = np.zeros((240 * 136, 3), dt)
+                rt.render_frame(s, cam, params, fb, workers, precision=precision, radiance=rad)
+                if ref is None:
+                    ref = (fb.pixels.copy(), rad.copy())
+                np.testing.assert_array_equal(fb.pixels, ref[0], err_msg=f"bands={bands} workers={workers}")
+                np.testing.assert_array_equal(rad, ref[1], err_msg=f"bands={bands} workers={workers}")
+    finally:
+        _native.set_options(bands=0)

@@ -30,58 +30,69 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
-// The hit's shadow cone (see rt_wave.cuh for the geometry), in float64.
-struct Cone64 {
-    d3 o, axis;
-    double H, rho, inv_H, sin_phi, cos_phi, reach;
+// The hit's shadow cone and the classification of a body against it (see
+// rt_wave.cuh for the geometry: nothing can block / some samples / all).
+// In float32 on the float64 inputs rounded once:
+// the margins (1e-4 relative, 1e-5 absolute) stand far above both that
+// rounding (6e-8 relative) and float32 arithmetic, so the decisions stay
+// conservative — exactly the skips the float64 classifier would make, or
+// fewer — at a fraction of the float64 pipe's cost.
+struct Cone32 {
+    float ox, oy, oz, ax, ay, az, H, rho, inv_H, sin_phi, cos_phi, reach;
     bool ok;
 };
 
-__device__ __forceinline__ Cone64 make_cone(d3 o, d3 lp, double light_radius) {
-    Cone64 c;
-    c.o = o;
-    d3 A = vsub(lp, o);
-    c.H = sqrt(vdot(A, A));
-    c.rho = 2.0 * light_radius * (1.0 + kCullRel64) + kCullAbs64;
-    c.ok = c.H > 0.0 && c.rho < 0.999 * c.H;
-    c.inv_H = c.H > 0.0 ? 1.0 / c.H : 0.0;
-    c.axis = mk(A.x * c.inv_H, A.y * c.inv_H, A.z * c.inv_H);
-    c.sin_phi = c.ok ? c.rho * c.inv_H : 1.0;
-    c.cos_phi = sqrt(fmax(1.0 - c.sin_phi * c.sin_phi, 0.0));
-    double T = 1.0 + (1e-3 + kCullAbs64) / fmax(c.H - c.rho, 1e-9);
-    c.reach = T * (c.H + c.rho) * (1.0 + kCullRel64) + kCullAbs64;
+__device__ __forceinline__ Cone32 make_cone32(d3 o64, d3 lp64, double light_radius) {
+    constexpr float rel = (float)kCullRel64, abs_ = (float)kCullAbs64;
+    Cone32 c;
+    c.ox = (float)o64.x;
+    c.oy = (float)o64.y;
+    c.oz = (float)o64.z;
+    const float Ax = (float)lp64.x - c.ox, Ay = (float)lp64.y - c.oy, Az = (float)lp64.z - c.oz;
+    c.H = sqrtf(Ax * Ax + Ay * Ay + Az * Az);
+    c.rho = 2.f * (float)light_radius * (1.f + rel) + abs_;
+    c.ok = c.H > 0.f && c.rho < 0.999f * c.H;
+    c.inv_H = c.H > 0.f ? 1.f / c.H : 0.f;
+    c.ax = Ax * c.inv_H;
+    c.ay = Ay * c.inv_H;
+    c.az = Az * c.inv_H;
+    c.sin_phi = c.ok ? c.rho * c.inv_H : 1.f;
+    c.cos_phi = sqrtf(fmaxf(1.f - c.sin_phi * c.sin_phi, 0.f));
+    const float T = 1.f + (1e-3f + abs_) / fmaxf(c.H - c.rho, 1e-6f);
+    c.reach = T * (c.H + c.rho) * (1.f + rel) + abs_;
     return c;
 }
 
-// 0: the body can block none of the hit's shadow rays; 1: some; 2: all.
-__device__ __forceinline__ int body_class(const Cone64 &k, const double *g, double oy, double ly) {
+__device__ __forceinline__ int body_class32(const Cone32 &k, const double *g, float oy, float ly) {
+    constexpr float rel = (float)kCullRel64, abs_ = (float)kCullAbs64;
     if (!k.ok) return 1;
     if (g[3] < 0.0) {  // horizontal plane at g[1]
-        double hp = g[1], m = kCullAbs64 * (1.0 + fabs(hp) + fabs(ly));
-        double lo = ly - k.rho - 1e-3 - m, hi = ly + k.rho + 1e-3 + m;
-        double a = oy - hp;
+        const float hp = (float)g[1], m = abs_ * (1.f + fabsf(hp) + fabsf(ly));
+        const float lo = ly - k.rho - 1e-3f - m, hi = ly + k.rho + 1e-3f + m;
+        const float a = oy - hp;
         if ((a > m && lo > hp + m) || (a < -m && hi < hp - m)) return 0;
         if ((a > m && hi < hp - m) || (a < -m && lo > hp + m)) return 2;
         return 1;
     }
-    d3 u = mk(g[0] - k.o.x, g[1] - k.o.y, g[2] - k.o.z);
-    double u2 = vdot(u, u);
-    if (u2 < g[3] * (1.0 - 4.0 * kCullRel64) - kCullAbs64) return 0;  // origin inside: t < 0 always
-    double h = vdot(u, k.axis);
-    d3 w = mk(u.x - k.axis.x * h, u.y - k.axis.y * h, u.z - k.axis.z * h);
-    double q = sqrt(vdot(w, w));
-    double un = fabs(h) + q;
-    double r = sqrt(g[3]);
-    double rp = sqrt(g[3] + 1e-7) * (1.0 + kCullRel64) + kCullAbs64 + 1e-6 * (un + k.H);
+    const float r2 = (float)g[3];
+    const float ux = (float)g[0] - k.ox, uy = (float)g[1] - k.oy, uz = (float)g[2] - k.oz;
+    const float u2 = ux * ux + uy * uy + uz * uz;
+    if (u2 < r2 * (1.f - 4.f * rel) - abs_) return 0;  // origin inside: t < 0 always
+    const float h = ux * k.ax + uy * k.ay + uz * k.az;
+    const float wx = ux - k.ax * h, wy = uy - k.ay * h, wz = uz - k.az * h;
+    const float q = sqrtf(wx * wx + wy * wy + wz * wz);
+    const float un = fabsf(h) + q;
+    const float r = sqrtf(r2);
+    const float rp = sqrtf(r2 + 1e-7f) * (1.f + rel) + abs_ + 1e-6f * (un + k.H);
     if (h < -rp || h - rp > k.reach) return 0;
-    if (h * k.cos_phi + q * k.sin_phi >= 0.0) {
+    if (h * k.cos_phi + q * k.sin_phi >= 0.f) {
         if (q * k.cos_phi - h * k.sin_phi >= rp) return 0;
     } else if (u2 >= rp * rp) {
         return 0;
     }
-    double rm = r * (1.0 - 10.0 * kCullRel64) - kCullAbs64 - 1e-6 * (un + k.H);
-    if (u2 > g[3] * (1.0 + 4.0 * kCullRel64) + kCullAbs64 && h > 0.0 &&
-        h + r < (k.H - k.rho) * (1.0 - kCullRel64) - 2e-3 && q + h * k.inv_H * k.rho * (1.0 + kCullRel64) < rm)
+    const float rm = r * (1.f - 10.f * rel) - abs_ - 1e-6f * (un + k.H);
+    if (u2 > r2 * (1.f + 4.f * rel) + abs_ && h > 0.f && h + r < (k.H - k.rho) * (1.f - rel) - 2e-3f &&
+        q + h * k.inv_H * k.rho * (1.f + rel) < rm)
         return 2;
     return 1;
 }
@@ -138,12 +149,12 @@ __global__ void __launch_bounds__(kThreads)
             hit_terms(normal, l, dir, __ldg(sa.mat + 8 * idx + 4), dfs, s);
             // renderer.py:87-89: the shadow rays' origin
             const d3 so = mk(hit.x + 1e-3 * normal.x, hit.y + 1e-3 * normal.y, hit.z + 1e-3 * normal.z);
-            const Cone64 cone = make_cone(so, light, sa.light_radius);
+            const Cone32 cone = make_cone32(so, light, sa.light_radius);
 #pragma unroll
             for (int w = 0; w < kWords64; w++) mask[w] = 0;
             bool full = false, any = false;
             for (int b = 0; b < sa.n; b++) {
-                int c = body_class(cone, geo + 4 * b, so.y, light.y);
+                int c = body_class32(cone, geo + 4 * b, (float)so.y, (float)light.y);
                 mask[b >> 5] |= (c == 1 ? 1u : 0u) << (b & 31);
                 full |= c == 2;
                 any |= c == 1;

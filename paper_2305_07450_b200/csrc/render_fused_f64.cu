@@ -1,12 +1,13 @@
 // FP64 soft shadows with exact occluder culling: the bit-identical mode at
-// wavefront speed.  Same three kernels as the FP32 culled path
-// (render_fused_f32.cu) — trace + per-hit cone classification, sampling of
-// the undecided hits, unwind of the parked pixels — but every test that the
-// reference performs is performed here in its literal float64 order
-// (rt_f64.cuh, compiled with -fmad=false); the cone classifier only decides
-// which bodies cannot block any of a hit's shadow rays (or block all of
-// them) with margins of 1e-4 relative, far above float64 rounding, so the
-// skipped tests are exactly the ones the reference would have failed.
+// wavefront speed.  Three kernels, as the FP32 culled path
+// (render_fused_f32.cu) had them: trace + per-hit cone classification,
+// sampling of the undecided hits, unwind of the parked pixels.  Every value
+// the reference computes is computed here in its literal float64 order
+// (rt_f64.cuh, compiled with -fmad=false).  The cone classifier (float32 on
+// rounded inputs, margins of 1e-4 relative) only decides which bodies cannot
+// block any of a hit's shadow rays, or block all of them; the lane sampler
+// decides a sample by a float64 silhouette test only when the decision is
+// certain, else by the literal test.  Every decision is the reference's.
 //
 // Scenes of up to kMaxBodies64 bodies (geometry staged in shared memory per
 // CTA, candidate masks over original body indices); larger scenes keep the

@@ -37,13 +37,93 @@ using namespace rt32;
 
 constexpr int kRegCand = 4;  // candidate spheres a sampling warp keeps in registers
 
-// Classify every body against one hit's shadow cone (a single lane).
+// --- the shadow grid ------------------------------------------------------------
+// A box around the spheres is cut into kGridCells cells.  A hit's shadow
+// segments leave o toward the disc (within 2R of L) and stop at most 1e-3
+// beyond it; for every o in a cell (within rb of its centre cc) they lie within
+// rb of the cone from cc (half-angle asin(rho / (H - rb)), axial reach
+// T (H + rb + rho) with T formed with H - rb - rho): o + t (s - o) =
+// cc + t (s - cc) + (1 - t)(o - cc).  An occluder bound clear of that dilated
+// cone (sphere_class's outside tests, margins included) cannot meet the cone of
+// any hit in the cell, so its bit is clear in the cell's mask.  Hits outside
+// the box, or in a cell whose cone degenerates, classify every body.  The
+// grid depends on the scene and the light only (rt_host.cu rebuilds it when
+// either changes).
+__device__ __forceinline__ unsigned grid_mask(const WaveArgs &wa, float3 o) {
+    if (!wa.grid) return ~0u;
+    const int ix = __float2int_rd((o.x - wa.grid_lo[0]) * wa.grid_inv[0]);
+    const int iy = __float2int_rd((o.y - wa.grid_lo[1]) * wa.grid_inv[1]);
+    const int iz = __float2int_rd((o.z - wa.grid_lo[2]) * wa.grid_inv[2]);
+    if ((unsigned)ix >= (unsigned)wa.grid_dim[0] || (unsigned)iy >= (unsigned)wa.grid_dim[1] ||
+        (unsigned)iz >= (unsigned)wa.grid_dim[2])
+        return ~0u;
+    return __ldg(wa.grid + ((size_t)iz * wa.grid_dim[1] + iy) * wa.grid_dim[0] + ix);
+}
+
+template <int MAXS>
+__global__ void __launch_bounds__(kThreads)
+    shadow_grid_build(const ParamScene<MAXS> ps, const SceneArgs<float> sa, const WaveArgs wa, unsigned *out) {
+    const int n_cells = wa.grid_dim[0] * wa.grid_dim[1] * wa.grid_dim[2];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_cells) return;
+    const int ix = i % wa.grid_dim[0], iy = (i / wa.grid_dim[0]) % wa.grid_dim[1];
+    const int iz = i / (wa.grid_dim[0] * wa.grid_dim[1]);
+    const float3 cell = f3(1.f / wa.grid_inv[0], 1.f / wa.grid_inv[1], 1.f / wa.grid_inv[2]);
+    const float3 cc = f3(wa.grid_lo[0] + (ix + 0.5f) * cell.x, wa.grid_lo[1] + (iy + 0.5f) * cell.y,
+                         wa.grid_lo[2] + (iz + 0.5f) * cell.z);
+    // the cell's points lie within rb of cc (the float cell edges add ~1e-6 relative)
+    const float rb = 0.5f * sqrtf(dot3(cell, cell)) * (1.f + kCullRel) + kCullAbs +
+                     1e-6f * (fabsf(cc.x) + fabsf(cc.y) + fabsf(cc.z));
+    const float3 light = f3(sa.light[0], sa.light[1], sa.light[2]);
+    const float rho = 2.f * sa.light_radius * (1.f + kCullRel) + kCullAbs;
+    const float3 A = light - cc;
+    const float H = sqrtf(dot3(A, A));
+    if (!(H - rb > rho / 0.999f)) {
+        out[i] = ~0u;
+        return;
+    }
+    const float3 axis = A * (1.f / H);
+    const float sin_phi = fminf(rho / (H - rb), 1.f);
+    const float cos_phi = sqrtf(fmaxf(1.f - sin_phi * sin_phi, 0.f));
+    const float T = 1.f + (1e-3f + kCullAbs) / fmaxf(H - rb - rho, 1e-6f);
+    const float reach = T * (H + rb + rho) * (1.f + kCullRel) + kCullAbs;
+    constexpr bool kClustered = ParamScene<MAXS>::kClustered;
+    const int n_occ = kClustered ? ps.nc : ps.ns;
+    unsigned m = 0;
+    for (int b = 0; b < n_occ && b < 32; b++) {
+        float4 g;
+        if constexpr (kClustered) {
+            g = ps.cl[b];
+        } else {
+            g = make_float4(ps.sph[b].x, ps.sph[b].y, ps.sph[b].z, ps.sph_rad[b].y);
+        }
+        const float3 u = f3(g.x - cc.x, g.y - cc.y, g.z - cc.z);
+        const float h = dot3(u, axis);
+        const float3 w = u - axis * h;
+        const float q = sqrtf(dot3(w, w));
+        const float rp = (g.w + rb) * (1.f + kCullRel) + kCullAbs + 1e-6f * (fabsf(h) + q + H);
+        bool cand;
+        if (h < -rp || h - rp > reach) {
+            cand = false;
+        } else if (h * cos_phi + q * sin_phi >= 0.f) {
+            cand = q * cos_phi - h * sin_phi < rp;
+        } else {
+            cand = dot3(u, u) < rp * rp;
+        }
+        m |= (cand ? 1u : 0u) << b;
+    }
+    out[i] = m;
+}
+
+// Classify every body against one hit's shadow cone (a single lane); spheres
+// (clusters, in clustered scenes) outside the shadow grid's mask wm for the
+// hit's cell are skipped: they cannot meet the cone.
 // Returns 0 (nothing can block), 2 (a body blocks every sample) or 1
 // (undecided; mask[] holds the candidates: sphere slots in words
 // 0..kWords-1, planes in word kWords).
 template <int MAXS>
 __device__ __forceinline__ int classify_hit(const ParamScene<MAXS> &ps, const Cone &k, float oy, float ly,
-                                            unsigned *mask, bool check) {
+                                            unsigned *mask, bool check, unsigned wm) {
     constexpr int kWords = (MAXS + 31) / 32;
 #pragma unroll
     for (int w = 0; w <= kWords; w++) mask[w] = 0;
@@ -62,11 +142,11 @@ __device__ __forceinline__ int classify_hit(const ParamScene<MAXS> &ps, const Co
 #pragma unroll
         for (int b = 0; b < MAXS; b++) {
             if (b >= ps.ns) break;
-            classify(b);
+            if ((wm >> b) & 1u) classify(b);  // wm: the shadow grid's cell mask
         }
     } else {
         for (int c = 0; c < ps.nc; c++) {
-            if (!bound_meets_cone(k, ps.cl[c])) continue;
+            if (!((wm >> c) & 1u) || !bound_meets_cone(k, ps.cl[c])) continue;
             for (int b = ps.cl_begin[c]; b < ps.cl_begin[c + 1]; b++) classify(b);
         }
     }
@@ -253,7 +333,7 @@ __global__ void __launch_bounds__(kThreads)
             }
             const float3 so = hit + normal * 1e-3f;  // shadow (and reflection) origin
             const Cone cone = make_cone(so, light, sa.light_radius);
-            cls = classify_hit(ps, cone, so.y, light.y, mask, wa.cull == 2);
+            cls = classify_hit(ps, cone, so.y, light.y, mask, wa.cull == 2, grid_mask(wa, so));
             slot = (int64_t)k * wa.n_pix + lp;
             ridx[k] = h.idx;
             rdfs[k] = dfs;
@@ -770,4 +850,55 @@ cudaError_t rt_launch_fused_f32(const rt::FrameArgs &fa, const rt::SceneArgs<flo
     }
     *n_kernels = 2;
     return cudaSuccess;
+}
+
+// The shadow grid of the culled path: a box around the spheres (grown by its
+// own extent sideways, where their shadows fall), 48 x 24 x 48 cells.
+cudaError_t rt_build_shadow_grid_f32(const rt::SceneArgs<float> &sa, unsigned *mask, int capacity, rt::WaveArgs &wa,
+                                     cudaStream_t st) {
+    wa.grid = nullptr;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    double plane_lo = INFINITY;
+    int ns = 0;
+    for (int b = 0; b < sa.n; b++) {
+        const double *g = sa.host_geo + 4 * b;
+        if (g[3] < 0.0) {
+            plane_lo = std::min(plane_lo, g[1]);
+            continue;
+        }
+        const double r = std::sqrt(g[3]);
+        for (int a = 0; a < 3; a++) {
+            lo[a] = std::min(lo[a], g[a] - r);
+            hi[a] = std::max(hi[a], g[a] + r);
+        }
+        ns++;
+    }
+    if (ns == 0) return cudaSuccess;
+    const int dims[3] = {48, 24, 48};
+    if (dims[0] * dims[1] * dims[2] > capacity) return cudaSuccess;
+    for (int a = 0; a < 3; a += 2) {
+        const double grow = std::max(hi[a] - lo[a], 4.0);
+        lo[a] -= grow;
+        hi[a] += grow;
+    }
+    lo[1] = std::min(lo[1], plane_lo) - 0.5;
+    hi[1] += 0.5;
+    for (int a = 0; a < 3; a++) {
+        if (!(hi[a] > lo[a]) || !std::isfinite(lo[a]) || !std::isfinite(hi[a])) return cudaSuccess;
+        wa.grid_lo[a] = (float)lo[a];
+        wa.grid_dim[a] = dims[a];
+        wa.grid_inv[a] = (float)(dims[a] / (hi[a] - lo[a]));
+    }
+    ParamScene<8> p8;
+    thread_local ParamScene<kParamSpheres> p256;
+    const int blocks = (dims[0] * dims[1] * dims[2] + kThreads - 1) / kThreads;
+    if (pack_params(sa, p8))
+        shadow_grid_build<8><<<blocks, kThreads, 0, st>>>(p8, sa, wa, mask);
+    else if (pack_params(sa, p256))
+        shadow_grid_build<kParamSpheres><<<blocks, kThreads, 0, st>>>(p256, sa, wa, mask);
+    else
+        return cudaSuccess;
+    const cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) wa.grid = mask;
+    return e;
 }

@@ -79,6 +79,12 @@ struct WaveArgs {
     int cull;          // exact per-hit occluder culling (1); 2: every body left undecided (cull_check)
     float4 *conic;     // culled path: silhouette coefficients of queued hits, [2 kConic][conic_cap]
     unsigned conic_cap;  // queue positions below this may take the silhouette form (0: off)
+    // culled path: the shadow grid (rt_build_shadow_grid_f32): per cell of a
+    // box around the spheres, the occluders (spheres, or clusters) that may
+    // meet the shadow cone of a hit anywhere in the cell; null: none
+    const unsigned *grid;
+    float grid_lo[3], grid_inv[3];
+    int grid_dim[3];
     float4 *lane_q;    // culled path: single-candidate hits sampled one lane each: queue q (0: the
                        // sphere wholly in front, 1: not), row r (0: {p, slot}, 1: {n, sphere}) at
                        // [(2q + r) lane_cap]; lengths count[3] and count[0]
@@ -105,6 +111,7 @@ enum { kWorkHits = 0, kWorkCullTests, kWorkSampledHits, kWorkShadowRays, kWorkSp
 constexpr int kParamSpheres = 256;  // scenes up to this many spheres ride in the launch parameters
 constexpr int kMaskWords = kParamSpheres / 32;
 constexpr int kWaveMinSamples = 8;     // soft shadows at or above this take the wavefront path
+constexpr int kGridCells = 48 * 24 * 48;  // shadow grid (x, y, z) of the culled FP32 path
 constexpr int kConic = 4;             // silhouette-form spheres per queued hit (rt_wave.cuh; more: the ray form)
 constexpr int kWaveSmemSamples = 2048;  // disc tables (16 B/sample) up to this size are staged in shared memory
 
@@ -165,6 +172,11 @@ cudaError_t rt_launch_wave_f32(const rt::FrameArgs &fa, const rt::SceneArgs<floa
                                cudaStream_t st, int *n_kernels, cudaEvent_t *phase_events /* 5 or null */);
 int rt_wave_lanes(int samples);
 bool rt_fused_fits(const rt::SceneArgs<float> &sa);
+// Build the shadow grid of the scene in sa (light included) into `mask`
+// (capacity cells), filling wa's grid fields; a scene without spheres or that
+// does not fit leaves wa.grid null.
+cudaError_t rt_build_shadow_grid_f32(const rt::SceneArgs<float> &sa, unsigned *mask, int capacity, rt::WaveArgs &wa,
+                                     cudaStream_t st);
 cudaError_t rt_launch_fused_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, const rt::WaveArgs &wa,
                                 cudaStream_t st, int *n_kernels, cudaEvent_t *phase_events /* 5 or null */);
 cudaError_t rt_launch_fused_f64(const rt::FrameArgs &fa, const rt::SceneArgs<double> &sa, const rt::WaveArgs64 &wa,

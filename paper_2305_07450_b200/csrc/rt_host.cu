@@ -106,6 +106,9 @@ struct Dev {
     cudaEvent_t fork_ev = nullptr;
     bool ph_valid = false;
     DBuf frame, rad, rays_in, rays_out, sky_raw, sky, counters, w_work;
+    DBuf grid;                        // the culled FP32 path's shadow grid (scene + light)
+    uint64_t grid_version = ~0ull;
+    rt::WaveArgs grid_wa = {};        // its box and dims (grid null: none)
     WaveBufs wb[kMaxBands];
     unsigned counter_slot = 0;
     uint64_t sky_version = ~0ull;
@@ -366,7 +369,18 @@ int prepare(rt_ctx *ctx, Dev &d, int precision, int samples) {
     RT_CK(cudaSetDevice(d.id));
     if ((rc = upload_sky(ctx, d))) return rc;
     if (precision == RT_PREC_FP64) return upload_prec(d, d.s64, ctx->scene, samples);
-    return upload_prec(d, d.s32, ctx->scene, samples);
+    if ((rc = upload_prec(d, d.s32, ctx->scene, samples))) return rc;
+    // the culled path's shadow grid, rebuilt on d.st when the scene or the
+    // light changed (before any row band forks off d.st)
+    if (samples >= rt::kWaveMinSamples && ctx->wave && ctx->cull && d.grid_version != ctx->scene.version) {
+        if ((rc = d.grid.ensure(sizeof(unsigned) * rt::kGridCells))) return rc;
+        d.grid_wa = {};
+        cudaError_t e = rt_build_shadow_grid_f32(scene_args(d, d.s32, ctx->scene), (unsigned *)d.grid.p,
+                                                 rt::kGridCells, d.grid_wa, d.st);
+        if (e != cudaSuccess) return fail(RT_ERR_CUDA, std::string("shadow grid: ") + cudaGetErrorString(e));
+        d.grid_version = ctx->scene.version;
+    }
+    return RT_OK;
 }
 
 // Rows of partition `part`, rounded up to whole blocks (the kernel skips rows
@@ -502,6 +516,14 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         wa.rec = (float4 *)b.w_rec.p;
         wa.pend = (int *)b.w_pending.p;
         wa.cull = fused ? (ctx->cull_check ? 2 : 1) : 0;
+        if (fused && d.grid_version == ctx->scene.version && d.grid_wa.grid) {
+            wa.grid = d.grid_wa.grid;
+            for (int a = 0; a < 3; a++) {
+                wa.grid_lo[a] = d.grid_wa.grid_lo[a];
+                wa.grid_inv[a] = d.grid_wa.grid_inv[a];
+                wa.grid_dim[a] = d.grid_wa.grid_dim[a];
+            }
+        }
         wa.work = nullptr;
         if (ctx->count_work) {
             bool fresh = d.w_work.p == nullptr;
@@ -603,6 +625,7 @@ int rt_ctx_destroy(rt_ctx *ctx) {
         if (d.st) cudaStreamSynchronize(d.st);
         for (WaveBufs &wb : d.wb) wb.release();
         d.w_work.release();
+        d.grid.release();
         for (DBuf *b : {&d.frame, &d.rad, &d.rays_in, &d.rays_out, &d.sky_raw, &d.sky, &d.counters, &d.s32.geo, &d.s32.mat,
                         &d.s32.table, &d.s64.geo, &d.s64.mat, &d.s64.table})
             b->release();

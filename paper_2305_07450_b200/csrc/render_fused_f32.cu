@@ -222,6 +222,10 @@ __global__ void __launch_bounds__(kThreads)
     }
     float4 *cand_sph = s_cand_sph[threadIdx.x >> 5];
     int *cand_idx = s_cand_idx[threadIdx.x >> 5];
+    // launched with programmatic dependent launch: the previous frame's
+    // sampler may still be draining; nothing global is touched before it is done
+    cudaGridDependencySynchronize();
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 8) wa.count_next[threadIdx.x] = 0;
 
     int x, ly;
     thread_pixel(x, ly);
@@ -783,9 +787,9 @@ __global__ void __launch_bounds__(kThreads)
 // Launch with programmatic stream serialisation: the kernel may start while
 // the previous one drains and waits for it in cudaGridDependencySynchronize.
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kernel)(KArgs...), int ctas, size_t smem, cudaStream_t st, Args &&...args) {
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 ctas, size_t smem, cudaStream_t st, Args &&...args) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ctas);
+    cfg.gridDim = ctas;
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -801,8 +805,7 @@ template <int MAXS>
 cudaError_t launch(const FrameArgs &fa, const SceneArgs<float> &sa, const WaveArgs &wa, const ParamScene<MAXS> &ps,
                    cudaStream_t st, cudaEvent_t *ev) {
     dim3 grid((fa.width + kTileW - 1) / kTileW, (fa.local_rows + kTileH - 1) / kTileH);
-    fused_trace<MAXS><<<grid, kThreads, 0, st>>>(fa, sa, wa, ps);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_pdl(fused_trace<MAXS>, grid, 0, st, fa, sa, wa, ps);
     if (e != cudaSuccess) return e;
     if (ev) {
         cudaEventRecord(ev[1], st);
@@ -832,8 +835,7 @@ bool rt_fused_fits(const rt::SceneArgs<float> &sa) {
 cudaError_t rt_launch_fused_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, const rt::WaveArgs &wa,
                                 cudaStream_t st, int *n_kernels, cudaEvent_t *ev) {
     *n_kernels = 0;
-    cudaError_t e = cudaMemsetAsync(wa.count, 0, 4 * sizeof(unsigned), st);
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;  // the counters were zeroed by the previous frame's trace
     if (ev) cudaEventRecord(ev[0], st);
     ParamScene<8> p8;
     thread_local ParamScene<kParamSpheres> p256;

@@ -67,7 +67,8 @@ struct WaveArgs {
     float *hit_s;      // Blinn factor
     float *hit_sc;     // shadow coefficient
     int *queue;        // slots holding a hit
-    unsigned *count;   // queue lengths; culled path: [0], [3] lane queues, [1] warp queue, [2] parked pixels
+    unsigned *count;   // queue lengths; culled path: [0], [3] lane queues, [1] warp queue, [4] spare
+    unsigned *count_next;  // culled path: the next frame's counters, zeroed by this frame's trace
     int *queue2;          // culled path: undecided hits (slots)
     unsigned *mask2;      // their candidate-body masks, word-major [words][mask2_stride]
     int64_t mask2_stride;

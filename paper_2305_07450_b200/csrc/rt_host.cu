@@ -82,6 +82,7 @@ struct DevScene {
 // (w_*) and FP64 culled path (d_*).
 struct WaveBufs {
     DBuf w_p, w_n, w_s, w_sc, w_queue, w_queue2, w_mask2, w_count, w_pix, w_rec, w_pending, w_conic, w_lane;
+    int count_parity = 0;  // culled FP32 path: which of its two counter sets this frame uses
     DBuf d_q, d_mask, d_pix, d_rec, d_parked, d_lane;
     void release() {
         for (DBuf *b : {&w_p, &w_n, &w_s, &w_sc, &w_queue, &w_queue2, &w_mask2, &w_count, &w_pix, &w_rec, &w_pending,
@@ -438,6 +439,18 @@ rt::FrameArgs frame_args(uint32_t *out, int64_t pitch, void *rad, int w, int h, 
     return fa;
 }
 
+// Queue counters: [0, 8) the FP64 and unculled paths (zeroed per frame),
+// [8, 16) and [16, 24) the culled FP32 path's two sets (each frame's trace
+// zeroes the other set once the previous frame is done: no memset per frame).
+int ensure_counts(WaveBufs &b, cudaStream_t st) {
+    if (b.w_count.p && b.w_count.cap >= 32 * sizeof(unsigned)) return RT_OK;
+    int rc = b.w_count.ensure(32 * sizeof(unsigned));
+    if (rc) return rc;
+    RT_CK(cudaMemsetAsync(b.w_count.p, 0, 32 * sizeof(unsigned), st));
+    b.count_parity = 0;
+    return RT_OK;
+}
+
 int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStream_t st, int buf = 0) {
     WaveBufs &b = d.wb[buf];
     cudaError_t e;
@@ -456,7 +469,7 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         if ((rc = b.d_q.ensure(2 * sizeof(double4) * slots)) ||
             (rc = b.d_mask.ensure(sizeof(unsigned) * slots * (rt::kMaxBodies64 / 32))) ||
             (rc = b.d_pix.ensure(sizeof(double4) * (size_t)wa.n_pix)) || (rc = b.d_rec.ensure(sizeof(double4) * slots)) ||
-            (rc = b.d_parked.ensure(sizeof(int) * (size_t)wa.n_pix)) || (rc = b.w_count.ensure(4 * sizeof(unsigned))))
+            (rc = b.d_parked.ensure(sizeof(int) * (size_t)wa.n_pix)) || (rc = ensure_counts(b, st)))
             return rc;
         wa.q = (double4 *)b.d_q.p;
         wa.mask = (unsigned *)b.d_mask.p;
@@ -482,7 +495,7 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         wa.n_pix = (int64_t)fa.local_rows * fa.width;
         size_t slots = (size_t)wa.n_pix * (fa.bounces + 1);
         if ((rc = b.w_p.ensure(sizeof(float4) * slots)) || (rc = b.w_n.ensure(sizeof(float4) * slots)) ||
-            (rc = b.w_count.ensure(8 * sizeof(unsigned))) || (rc = b.w_pix.ensure(sizeof(float4) * (size_t)wa.n_pix)))
+            (rc = ensure_counts(b, st)) || (rc = b.w_pix.ensure(sizeof(float4) * (size_t)wa.n_pix)))
             return rc;
         if (fused) {
             if ((rc = b.w_queue2.ensure(sizeof(int) * slots)) ||
@@ -516,6 +529,11 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         wa.rec = (float4 *)b.w_rec.p;
         wa.pend = (int *)b.w_pending.p;
         wa.cull = fused ? (ctx->cull_check ? 2 : 1) : 0;
+        if (fused) {
+            wa.count = (unsigned *)b.w_count.p + 8 + 8 * b.count_parity;
+            wa.count_next = (unsigned *)b.w_count.p + 8 + 8 * (1 - b.count_parity);
+            b.count_parity ^= 1;
+        }
         if (fused && d.grid_version == ctx->scene.version && d.grid_wa.grid) {
             wa.grid = d.grid_wa.grid;
             for (int a = 0; a < 3; a++) {

@@ -411,3 +411,67 @@ def test_copy_overlap_bands_do_not_change_pixels(precision):
                 np.testing.assert_array_equal(rad, ref[1], err_msg=f"bands={bands} workers={workers}")
     finally:
         _native.set_options(bands=0)
+
+
+def _edge_cases():
+    """Small scenes at the edges of the renderer's domain, each rendered on
+    every path and checked against the oracle."""
+    bench = rt.build_benchmark_scene()
+    cam = rt.benchmark_camera()
+    cases = {}
+    # frame shapes off the 16x8 tile grid, and a 1-pixel frame
+    cases["1x1_s200_b3"] = (bench, cam, rt.RenderParams(200, 3, 1, 1))
+    cases["17x9_s200_b3"] = (bench, cam, rt.RenderParams(200, 3, 17, 9))
+    cases["9x31_s16_b2"] = (bench, cam, rt.RenderParams(16, 2, 9, 31))
+    # the wavefront threshold (8 samples) and one below it
+    cases["48x27_s8_b3"] = (bench, cam, rt.RenderParams(8, 3, 48, 27))
+    cases["48x27_s7_b3"] = (bench, cam, rt.RenderParams(7, 3, 48, 27))
+    # the deepest bounce budget, in a hall of mirrors
+    mirrors = rt.Scene(bodies=[rt.Body.sphere((-1.1, 1.0, 2.0), 1.0, (0.9, 0.9, 0.9), 128.0),
+                               rt.Body.sphere((1.1, 1.0, 2.0), 1.0, (0.9, 0.9, 0.9), 128.0),
+                               rt.Body.plane(0.0, (0.5, 0.5, 0.5), 128.0)],
+                       light=rt.Light((0.0, 6.0, -2.0), 0.4), max_reflectivity=128.0)
+    cases["mirrors_32x18_s16_b31"] = (mirrors, cam, rt.RenderParams(16, 31, 32, 18))
+    # a near-point light (the reference requires a positive radius)
+    point = rt.Scene(bodies=list(bench.bodies), light=rt.Light((-4.0, 7.0, -2.0), 1e-6))
+    cases["pointlight_48x27_s16_b2"] = (point, cam, rt.RenderParams(16, 2, 48, 27))
+    # the light inside a sphere, and the camera inside a sphere
+    inside = rt.Scene(bodies=list(bench.bodies) + [rt.Body.sphere((-4.0, 7.0, -2.0), 1.5, (0.9, 0.9, 0.2), 8.0)],
+                      light=rt.Light((-4.0, 7.0, -2.0), 0.6))
+    cases["light_inside_48x27_s32_b2"] = (inside, cam, rt.RenderParams(32, 2, 48, 27))
+    shell = rt.Scene(bodies=list(bench.bodies) + [rt.Body.sphere(cam.position, 0.5, (0.3, 0.6, 0.9), 16.0)],
+                     light=rt.Light((-4.0, 7.0, -2.0), 0.6))
+    cases["camera_inside_48x27_s32_b2"] = (shell, cam, rt.RenderParams(32, 2, 48, 27))
+    # a light larger than the distance to the nearest surfaces
+    huge = rt.Scene(bodies=list(bench.bodies), light=rt.Light((0.0, 3.0, 1.0), 2.5))
+    cases["hugelight_48x27_s64_b2"] = (huge, cam, rt.RenderParams(64, 2, 48, 27))
+    return cases
+
+
+EDGE = _edge_cases()
+
+
+@pytest.mark.parametrize("name", sorted(EDGE))
+def test_edge_cases_against_oracle(name):
+    scene, cam, params = EDGE[name]
+    w, h = params.width, params.height
+    ps = rt.pack_scene(scene)
+    want, want_rad = oracle.render(vars(ps), cam.position, cam.yaw, cam.pitch, cam.fov, w, h,
+                                   params.shadow_samples, params.bounce_limit, radiance=True)
+    fb = rt.Framebuffer.create(w, h)
+    rt.render_frame(scene, cam, params, fb, precision="fp64")
+    np.testing.assert_array_equal(fb.pixels, want, err_msg=f"{name} fp64")
+    try:
+        for mode, opts in MODES.items():
+            _native.set_options(**opts)
+            fb = rt.Framebuffer.create(w, h)
+            rad = np.zeros((w * h, 3), np.float32)
+            rt.render_frame(scene, cam, params, fb, precision="fp32", radiance=rad)
+            if w * h >= 1000:
+                parity.assert_byte_gate(fb.pixels, want, f"{name} [{mode}]")
+                parity.assert_radiance_gate(rad, want_rad, f"{name} [{mode}]")
+            else:  # too few pixels for a 99.9% gate: every channel within 1
+                frac, worst = parity.byte_gate(fb.pixels, want)
+                assert worst <= 1, f"{name} [{mode}]: worst channel delta {worst}"
+    finally:
+        _native.set_options(**MODES["cull"])

@@ -435,25 +435,34 @@ __global__ void __launch_bounds__(kThreads)
 // records are decided); with several, the coefficient is stored and the last
 // of the pixel's samplers — an atomic countdown, fenced both ways — unwinds it.
 __device__ __forceinline__ void resolve_hit(const FrameArgs &fa, const SceneArgs<float> &sa, const WaveArgs &wa,
-                                            int slot, float sc) {
+                                            int slot, float sc, float4 px, const float4 *mat4) {
     const int n_pix = (int)wa.n_pix;
     const int kh = slot / n_pix, lp = slot - kh * n_pix;
-    const float4 px = __ldcg(wa.pix + lp);
     const int info = __float_as_int(px.w);
-    if (info & (1 << 9)) {
+    const bool several = info & (1 << 9);
+    if (several) {
         reinterpret_cast<float *>(wa.rec + slot)[3] = sc;
         __threadfence();
         if (atomicSub(wa.pend + lp, 1) != 1) return;
         __threadfence();
-        sc = __ldcg(wa.rec + slot).w;
     }
-    const float3 c = unwind(info & 0xff, (info >> 8) & 1, f3(px.x, px.y, px.z), sa, [&](int k) {
-        const float4 r = __ldcg(wa.rec + (int64_t)k * n_pix + lp);
-        return Record{__float_as_int(r.x), r.y, r.z, k == kh ? sc : r.w};
-    });
+    const int m = info & 0xff;
+    float4 rk[kMaxBounce + 1];  // every record load in flight before the first use
+    for (int k = 0; k < m; k++) rk[k] = __ldcg(wa.rec + (int64_t)k * n_pix + lp);
+    const float3 c = unwind(
+        m, (info >> 8) & 1, f3(px.x, px.y, px.z), sa,
+        [&](int k) { return Record{__float_as_int(rk[k].x), rk[k].y, rk[k].z, (k == kh && !several) ? sc : rk[k].w}; },
+        mat4);
     const int ly = lp / fa.width, x = lp - ly * fa.width;
     store_pixel(fa, x, map_row(ly, fa), c);
     if (fa.peer_out) __threadfence_system();
+}
+
+// The parked-pixel word of a hit's pixel (issued early: its latency hides
+// behind the sampling).
+__device__ __forceinline__ float4 pixel_word(const WaveArgs &wa, int slot) {
+    const int n_pix = (int)wa.n_pix;
+    return __ldcg(wa.pix + (slot - (slot / n_pix) * n_pix));
 }
 
 // --- B ----------------------------------------------------------------------------
@@ -631,7 +640,7 @@ __device__ __forceinline__ int sample_conic(const WaveArgs &wa, unsigned e, int 
 // sample_conic, so either sampler gives the same bits.
 template <int MAXS, bool SMEM_TAB>
 __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArgs<float> &sa, const WaveArgs &wa,
-                                             const ParamScene<MAXS> &ps, const float4 *gtab) {
+                                             const ParamScene<MAXS> &ps, const float4 *gtab, const float4 *mat4) {
     const int n = fa.samples;
     auto table = [&](int i) -> float4 {
         if constexpr (SMEM_TAB) {
@@ -656,6 +665,7 @@ __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArg
         const float4 P = __ldg(qp + h);
         const float4 N = __ldg(qn + h);
         const int slot = __float_as_int(P.w);
+        const float4 px = pixel_word(wa, slot);
         const float4 g = ps.sph[__float_as_int(N.w)];
         const ShadowFrame f = shadow_frame(f3(P.x, P.y, P.z), f3(N.x, N.y, N.z), light, true);
         const Cone k = make_cone(f.origin, light, sa.light_radius);
@@ -689,7 +699,7 @@ __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArg
 #pragma unroll 4
             for (int i = 0; i < n; i++) blocked += conic_blocked(A, B, b0, b1, b2, table(i));
         }
-        resolve_hit(fa, sa, wa, slot, (float)(n - (int)blocked) / (float)n);
+        resolve_hit(fa, sa, wa, slot, (float)(n - (int)blocked) / (float)n, px, mat4);
         if (wa.work) {
             if (r != 0) {
                 atomicAdd(wa.work + kWorkConicHits, 1ull);
@@ -708,16 +718,19 @@ __global__ void __launch_bounds__(kThreads)
     constexpr int kWords = (MAXS + 31) / 32;
     const int n = fa.samples;
     const float4 *gtab = reinterpret_cast<const float4 *>(sa.table);
+    // the bodies' base colours for the unwinds (kParamSpheres + kMaxPlanes bodies at most)
+    __shared__ float4 s_mat[kParamSpheres + kMaxPlanes];
+    for (int i = threadIdx.x; i < sa.n; i += blockDim.x) s_mat[i] = __ldg(reinterpret_cast<const float4 *>(sa.mat) + 2 * i);
     if constexpr (SMEM_TAB) {
         extern __shared__ float4 smem_tab_k[];
         for (int i = threadIdx.x; i < n; i += blockDim.x) smem_tab_k[i] = gtab[i];
-        __syncthreads();
     }
+    __syncthreads();
     // programmatic dependent launch: everything above (the table staging)
     // overlaps the trace kernel's tail; the queue is read only after it
     cudaGridDependencySynchronize();
     if (wa.lane_cap) {  // B1: the single-candidate hits, one lane each
-        sample_lanes<MAXS, SMEM_TAB>(fa, sa, wa, ps, gtab);
+        sample_lanes<MAXS, SMEM_TAB>(fa, sa, wa, ps, gtab, s_mat);
     }
     // B2: the rest, one warp each
     const unsigned count = wa.count[1];
@@ -765,7 +778,7 @@ __global__ void __launch_bounds__(kThreads)
             my_sc = (float)unblocked / (float)n;
         }
         if (++held == 32) {
-            if (my_slot >= 0) resolve_hit(fa, sa, wa, my_slot, my_sc);
+            if (my_slot >= 0) resolve_hit(fa, sa, wa, my_slot, my_sc, pixel_word(wa, my_slot), s_mat);
             my_slot = -1;
             held = 0;
         }
@@ -781,7 +794,7 @@ __global__ void __launch_bounds__(kThreads)
             atomicAdd(wa.work + kWorkPlaneTests, (unsigned long long)n * __popc(hmc[kWords]));
         }
     }
-    if (my_slot >= 0) resolve_hit(fa, sa, wa, my_slot, my_sc);
+    if (my_slot >= 0) resolve_hit(fa, sa, wa, my_slot, my_sc, pixel_word(wa, my_slot), s_mat);
 }
 
 // Launch with programmatic stream serialisation: the kernel may start while

@@ -236,14 +236,17 @@ struct Record {
     float dfs, s, sc;
 };
 
+// mat4: the bodies' {r, g, b, refl/max_refl} staged in shared memory, or
+// null (read from sa.mat)
 template <class Get>
-__device__ __forceinline__ float3 unwind(int m, bool exhausted, float3 tail, const SceneArgs<float> &sa, Get get) {
+__device__ __forceinline__ float3 unwind(int m, bool exhausted, float3 tail, const SceneArgs<float> &sa, Get get,
+                                         const float4 *mat4 = nullptr) {
     float3 col = tail;
     for (int k = m - 1; k >= 0; k--) {
         const Record r = get(k);
         float lum = fminf(sa.ambient + r.sc * r.dfs * (1.f - sa.ambient), 1.f);
         float sp = r.sc * r.s;
-        const float4 mt = __ldg(reinterpret_cast<const float4 *>(sa.mat + 8 * r.idx));
+        const float4 mt = mat4 ? mat4[r.idx] : __ldg(reinterpret_cast<const float4 *>(sa.mat + 8 * r.idx));
         float br = mt.x, bg = mt.y, bb = mt.z;
         if (!(exhausted && k == m - 1)) {
             float rr = mt.w;

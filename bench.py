@@ -343,7 +343,7 @@ def run_ours(args):
     wcc = wc[args.config]
     rays = wcc["rays"]
     peak_meas = _native.fp32_peak_tflops(local)
-    roof = roofline(wcc, phases, work, ms_frame, cfg.samples, peak_meas)
+    roof = roofline(wcc, phases, work, ms_frame, cfg.samples, peak_meas, config_key=args.config)
 
     # e2e through the public API into a host framebuffer (rank 0's process)
     e2e = None
@@ -417,7 +417,7 @@ def run_ours(args):
             km = statistics.mean(r["ms"])
             extra[key] = {"workload": c.name, "fps": f, "ms_per_frame": km,
                           "mrays_per_s": wc[key]["rays"] * f / 1e6, "phases_ms": ph,
-                          "roofline": roofline(wc[key], ph, wk, km, c.samples, peak_meas)}
+                          "roofline": roofline(wc[key], ph, wk, km, c.samples, peak_meas, config_key=key)}
             if key in rt.workloads.PAPER_FPS:
                 extra[key]["paper_fps_rtx2060"] = rt.workloads.PAPER_FPS[key]
         # ablation on the headline config: the same frame without culling, and as one megakernel
@@ -474,7 +474,7 @@ FLOP_CONIC = 17         # one silhouette-form sample test (|w|^2, x, y, d: 7 FMA
 FLOP_CONIC_SETUP = 120  # shadow frame, cone and the six coefficients of one (hit, sphere) pair
 
 
-def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True):
+def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True, config_key=None):
     """Roofline of the dominant kernel: its executed FLOPs (cost model above,
     counts from the reference's control flow or the culled pass's own
     tallies) over its measured device time."""
@@ -511,6 +511,17 @@ def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True):
         kernel, kms, share = "megakernel", ms_frame, 1.0
         flops = {"megakernel": sum(flops.values())}
     achieved = flops[kernel] / (kms * 1e-3) / 1e12 if kms > 0 else 0.0
+    # DRAM traffic per launch of that kernel, from the committed ncu capture
+    # (profiles/ncu_traffic.json); null when there is none for this config
+    traffic, traffic_src = None, None
+    try:
+        tr = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")))
+        t = tr.get(config_key, {}).get(kernel)
+        if t:
+            traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
+            traffic_src = tr["_source"]
+    except (OSError, ValueError, KeyError):
+        pass
     per_kernel = {}
     if phases and sum(phases.values()) > 0:
         for k, ms in phases.items():
@@ -524,7 +535,8 @@ def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True):
         "peak": peak,
         "unit": "TFLOP/s",
         "frac": achieved / peak if peak else None,
-        "traffic": None,
+        "traffic": traffic,
+        "traffic_source": traffic_src,
         "kernel_ms": kms,
         "kernel_share_of_frame": share,
         "flops_per_launch": flops[kernel],

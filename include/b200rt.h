@@ -183,6 +183,14 @@ int rt_ipc_close(void *d_ptr);
 /* Synchronous device->host copy of `bytes` from d_src on `stream` (NULL = the
  * slot's stream): rank 0 reads the gathered frame back. */
 int rt_copy_to_host(rt_ctx *ctx, int32_t slot, void *host_dst, const void *d_src, size_t bytes, void *stream);
+/* Copy partition `part`'s rows (8-row blocks round-robin, as
+ * rt_render_device_v1 renders them) of the device frame d_frame into the
+ * host frame host_frame (same layout: pixel (x, y) at y * width + x), on
+ * `stream` (null: the context's stream), and wait for it.  With one process
+ * per GPU and host_frame a page-locked buffer shared by them, every GPU
+ * copies its own rows over its own PCIe link. */
+int rt_copy_partition_to_host(rt_ctx *ctx, int32_t slot, uint32_t *host_frame, const uint32_t *d_frame, int32_t width,
+                              int32_t height, int32_t part, int32_t n_parts, int32_t block_rows, void *stream);
 
 /* Plain device allocations (cudaMalloc) — IPC-exportable framebuffers. */
 int rt_device_malloc(int32_t device, size_t bytes, void **d_ptr_out);

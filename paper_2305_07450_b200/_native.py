@@ -58,6 +58,7 @@ SIGNATURES = {
     "rt_ipc_open": (ctypes.c_int, [_p, _p]),
     "rt_ipc_close": (ctypes.c_int, [_p]),
     "rt_copy_to_host": (ctypes.c_int, [_p, _i32, _p, _p, ctypes.c_size_t, _p]),
+    "rt_copy_partition_to_host": (ctypes.c_int, [_p, _i32, _p, _p, _i32, _i32, _i32, _i32, _i32, _p]),
     "rt_device_malloc": (ctypes.c_int, [_i32, ctypes.c_size_t, _p]),
     "rt_device_free": (ctypes.c_int, [_p]),
     "rt_fp32_peak_tflops": (ctypes.c_int, [_i32, _p]),
@@ -173,6 +174,16 @@ class Context:
         if hit is arr:
             return self._addr[id(arr)]
         return arr.__array_interface__["data"][0]
+
+    def unpin(self, arr: np.ndarray) -> None:
+        """Release a buffer page-locked by pin()."""
+        key = id(arr)
+        if self._registered.get(key) is arr:
+            load().rt_host_unregister(self.handle, ptr(arr))
+            del self._registered[key]
+            self._addr.pop(key, None)
+            if key in self._reg_order:
+                self._reg_order.remove(key)
 
     def set_option(self, name: str, value) -> None:
         check(load().rt_set_option(self.handle, name.encode(), int(value)), "rt_set_option")

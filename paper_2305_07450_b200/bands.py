@@ -8,10 +8,14 @@ exchange during the render.  Contiguous equal bands would be ~2.5x
 imbalanced at 8 GPUs on the benchmark camera (the top 46% of rows are sky,
 SURVEY.md §8e); round-robin 8-row blocks keep max/mean load within ~3%.
 
-Two gathers:
-  * `IpcFrame` (the product path): rank 0 exports its device framebuffer
-    through CUDA IPC and every rank's render kernel stores its rows straight
-    into it over NVLink — the gather is fused into the render, no extra pass;
+Three gathers:
+  * `IpcFrame` (the device-resident path): rank 0 exports its device
+    framebuffer through CUDA IPC and every rank's render kernel stores its
+    rows straight into it over NVLink — the gather is fused into the render;
+  * `ShmFrame` (the host-frame path): a page-locked host frame shared by the
+    ranks of the node; every rank copies its own rows into it over its own
+    PCIe link (rt_copy_partition_to_host), so the device-to-host traffic of a
+    frame is spread over G links instead of funnelled through rank 0's;
   * `gather_bands` (collective fallback, and the CPU/gloo-testable path):
     compact rows per rank, `torch.distributed.gather` to rank 0, scatter into
     the frame.
@@ -103,6 +107,53 @@ class IpcFrame:
         else:
             self.lib.rt_ipc_close(self.ptr)
         self.ptr = None
+
+
+class ShmFrame:
+    """A host framebuffer shared by every rank of the node (POSIX shared
+    memory), page-locked in each rank's process, uint32[width * height].
+
+    `copy_rows(ctx, d_frame, part, n_parts)` copies this rank's rows of its
+    device frame into it; after a barrier rank 0 holds the whole frame in
+    `pixels`.  `exchange` broadcasts rank 0's segment name."""
+
+    def __init__(self, ctx, width: int, height: int, rank: int, exchange):
+        from multiprocessing import shared_memory
+
+        self.width, self.height, self.rank = width, height, rank
+        nbytes = 4 * width * height
+        if rank == 0:
+            self.shm = shared_memory.SharedMemory(create=True, size=nbytes)
+            name = exchange(self.shm.name.encode()).decode()
+        else:
+            name = exchange(b"").decode()
+            self.shm = shared_memory.SharedMemory(name=name)
+            try:  # rank 0 owns (and unlinks) the segment; attached ranks must not
+                from multiprocessing import resource_tracker
+
+                resource_tracker.unregister(self.shm._name, "shared_memory")
+            except Exception:
+                pass
+        self.pixels = np.ndarray((width * height,), dtype=np.uint32, buffer=self.shm.buf)
+        self.ctx = ctx
+        if not ctx.pin(self.pixels):
+            raise _native.NativeError("could not page-lock the shared host frame")
+
+    def copy_rows(self, d_frame, part: int, n_parts: int, stream=None, block_rows: int = BLOCK_ROWS):
+        lib = _native.load()
+        _native.check(lib.rt_copy_partition_to_host(self.ctx.handle, 0, _native.ptr(self.pixels), d_frame,
+                                                    self.width, self.height, part, n_parts, block_rows, stream),
+                      "rt_copy_partition_to_host")
+
+    def close(self):
+        if self.shm is None:
+            return
+        self.ctx.unpin(self.pixels)
+        self.pixels = None
+        self.shm.close()
+        if self.rank == 0:
+            self.shm.unlink()
+        self.shm = None
 
 
 def torch_exchange(blob: bytes) -> bytes:

@@ -564,6 +564,31 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
     return RT_OK;
 }
 
+// Device-to-host copy of the rows of partition `part` (8-row blocks
+// round-robin, map_row): one strided 2D copy of its whole blocks, one copy of
+// a trailing partial block.  elem = bytes per pixel (4 for the frame, 12 or 24
+// for radiance); host and device frames share the layout.
+int copy_partition(void *host, const void *dev, size_t elem, int width, int height, int part, int n_parts,
+                   int block_rows, cudaStream_t st) {
+    const int n_blocks = (height + block_rows - 1) / block_rows;
+    int full = 0;  // owned blocks that are complete
+    for (int j = part; j < n_blocks; j += n_parts)
+        if ((j + 1) * block_rows <= height) full++;
+    const size_t row_b = elem * (size_t)width;
+    const size_t off = (size_t)part * block_rows * row_b;
+    char *h = (char *)host;
+    const char *dv = (const char *)dev;
+    if (full > 0)
+        RT_CK(cudaMemcpy2DAsync(h + off, row_b * block_rows * n_parts, dv + off, row_b * block_rows * n_parts,
+                                row_b * block_rows, full, cudaMemcpyDeviceToHost, st));
+    const int last = part + full * n_parts;  // a trailing partial block, if this part owns it
+    if (last < n_blocks) {
+        const size_t o2 = (size_t)last * block_rows * row_b;
+        RT_CK(cudaMemcpyAsync(h + o2, dv + o2, row_b * (height - last * block_rows), cudaMemcpyDeviceToHost, st));
+    }
+    return RT_OK;
+}
+
 int check_frame_args(int32_t w, int32_t h, int32_t samples, int32_t bounces, int32_t precision) {
     if (w < 1 || h < 1) return fail(RT_ERR_INVALID, "frame dimensions must be positive");
     if ((int64_t)w * h > (int64_t)1 << 31) return fail(RT_ERR_LIMIT, "frame too large");
@@ -801,37 +826,12 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
         Dev &d = ctx->devs[g];
         RT_CK(cudaSetDevice(d.id));
         for (int p = g; p < n_parts; p += n_dev) {
-            int n_blocks = (height + block_rows - 1) / block_rows;
-            int full = 0;  // owned blocks that are complete
-            for (int j = p; j < n_blocks; j += n_parts)
-                if ((j + 1) * block_rows <= height) full++;
-            size_t row_b = sizeof(uint32_t) * (size_t)width;
-            size_t off = (size_t)p * block_rows * width;
-            if (full > 0)
-                RT_CK(cudaMemcpy2DAsync(pixels + off, row_b * block_rows * n_parts, (uint32_t *)d.frame.p + off,
-                                        row_b * block_rows * n_parts, row_b * block_rows, full,
-                                        cudaMemcpyDeviceToHost, d.st));
-            int last = p + full * n_parts;  // a trailing partial block, if this part owns it
-            if (last < n_blocks) {
-                int rows = height - last * block_rows;
-                size_t o2 = (size_t)last * block_rows * width;
-                RT_CK(cudaMemcpyAsync(pixels + o2, (uint32_t *)d.frame.p + o2, row_b * rows, cudaMemcpyDeviceToHost,
-                                      d.st));
-            }
-            if (radiance) {
-                size_t rrow = rad_elem * 3 * (size_t)width;
-                char *hr = (char *)radiance, *dr = (char *)d.rad.p;
-                size_t roff = (size_t)p * block_rows * rrow;
-                if (full > 0)
-                    RT_CK(cudaMemcpy2DAsync(hr + roff, rrow * block_rows * n_parts, dr + roff,
-                                            rrow * block_rows * n_parts, rrow * block_rows, full,
-                                            cudaMemcpyDeviceToHost, d.st));
-                if (last < n_blocks) {
-                    int rows = height - last * block_rows;
-                    size_t o2 = (size_t)last * block_rows * rrow;
-                    RT_CK(cudaMemcpyAsync(hr + o2, dr + o2, rrow * rows, cudaMemcpyDeviceToHost, d.st));
-                }
-            }
+            if ((rc = copy_partition(pixels, (const uint32_t *)d.frame.p, sizeof(uint32_t), width, height, p, n_parts,
+                                     block_rows, d.st)))
+                return rc;
+            if (radiance &&
+                (rc = copy_partition(radiance, d.rad.p, rad_elem * 3, width, height, p, n_parts, block_rows, d.st)))
+                return rc;
         }
     }
     for (int g = 0; g < n_dev; g++) {
@@ -1052,6 +1052,21 @@ int rt_copy_to_host(rt_ctx *ctx, int32_t slot, void *host_dst, const void *d_src
     RT_CK(cudaSetDevice(d.id));
     cudaStream_t st = stream ? (cudaStream_t)stream : d.st;
     RT_CK(cudaMemcpyAsync(host_dst, d_src, bytes, cudaMemcpyDeviceToHost, st));
+    RT_CK(cudaStreamSynchronize(st));
+    return RT_OK;
+}
+
+int rt_copy_partition_to_host(rt_ctx *ctx, int32_t slot, uint32_t *host_frame, const uint32_t *d_frame, int32_t width,
+                              int32_t height, int32_t part, int32_t n_parts, int32_t block_rows, void *stream) {
+    if (!ctx || !host_frame || !d_frame) return fail(RT_ERR_INVALID, "null argument");
+    if (slot < 0 || slot >= (int)ctx->devs.size()) return fail(RT_ERR_INVALID, "bad device slot");
+    if (width < 1 || height < 1 || n_parts < 1 || part < 0 || part >= n_parts || block_rows < 1)
+        return fail(RT_ERR_INVALID, "bad partition");
+    Dev &d = ctx->devs[slot];
+    RT_CK(cudaSetDevice(d.id));
+    cudaStream_t st = stream ? (cudaStream_t)stream : d.st;
+    int rc = copy_partition(host_frame, d_frame, sizeof(uint32_t), width, height, part, n_parts, block_rows, st);
+    if (rc) return rc;
     RT_CK(cudaStreamSynchronize(st));
     return RT_OK;
 }

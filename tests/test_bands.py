@@ -8,6 +8,7 @@ GPU: two processes sharing one B200 render their bands through
 IPC (the one-process-per-GPU product path), byte-identical to one render.
 """
 
+import ctypes
 import os
 import socket
 
@@ -121,6 +122,56 @@ def test_ipc_row_bands_two_processes_one_gpu(tmp_path):
 
     out = str(tmp_path / "frame.npy")
     mp.spawn(_ipc_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    cfg = rt.CONFIGS["C2"]
+    fb = rt.Framebuffer.create(cfg.width, cfg.height)
+    rt.render_frame(cfg.scene(), cfg.camera(), cfg.params(), fb)
+    np.testing.assert_array_equal(np.load(out), fb.pixels)
+
+
+def _shm_worker(rank, world, port, out_path):
+    import paper_2305_07450_b200 as rt
+    from paper_2305_07450_b200 import _native
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = rt.CONFIGS["C2"]
+    lib = _native.load()
+    ctx = _native.Context((0,))
+    ps = rt.pack_scene(cfg.scene())
+    P = _native.ptr
+    _native.check(lib.rt_set_scene_v1(ctx.handle, ps.n_bodies, P(ps.kinds), P(ps.positions), P(ps.sizes),
+                                      P(ps.colors), P(ps.refls), P(ps.light_pos), ps.light_radius, P(ps.light_color),
+                                      ps.ambient, ps.max_refl, P(ps.sky), ps.sky_w, ps.sky_h, int(ps.has_sky)),
+                  "rt_set_scene_v1")
+    # each rank renders its rows into its own device frame and copies them into the shared host frame
+    d_frame = ctypes.c_void_p()
+    _native.check(lib.rt_device_malloc(0, 4 * cfg.width * cfg.height, ctypes.byref(d_frame)), "rt_device_malloc")
+    shm = bands.ShmFrame(ctx, cfg.width, cfg.height, rank, bands.torch_exchange)
+    cam = cfg.camera()
+    cp = np.array(cam.position, dtype=np.float64)
+    _native.check(lib.rt_render_device_v1(ctx.handle, 0, d_frame, cfg.width, None, cfg.width, cfg.height, P(cp),
+                                          cam.yaw, cam.pitch, rt.camera_viewport_distance(cam.fov), cfg.samples,
+                                          cfg.bounces, rank, world, bands.BLOCK_ROWS, _native.RT_PREC_FP32, None),
+                  "rt_render_device_v1")
+    shm.copy_rows(d_frame, rank, world)
+    dist.barrier()  # every rank's rows are in the shared frame
+    if rank == 0:
+        np.save(out_path, shm.pixels.copy())
+    dist.barrier()
+    shm.close()
+    lib.rt_device_free(d_frame)
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_shm_host_frame_two_processes_one_gpu(tmp_path):
+    """The host-frame gather: two ranks copy their interleaved rows into a
+    page-locked shared host frame over their own PCIe links; the frame equals
+    a single-process render byte for byte."""
+    import paper_2305_07450_b200 as rt
+
+    out = str(tmp_path / "frame.npy")
+    mp.spawn(_shm_worker, args=(2, _free_port(), out), nprocs=2, join=True)
     cfg = rt.CONFIGS["C2"]
     fb = rt.Framebuffer.create(cfg.width, cfg.height)
     rt.render_frame(cfg.scene(), cfg.camera(), cfg.params(), fb)

@@ -272,13 +272,16 @@ __device__ void sample_lanes64(const FrameArgs &fa, const SceneArgs<double> &sa,
     const double *tab = sa.table;
     const double2 *tab2 = reinterpret_cast<const double2 *>(tab);  // {r cos, r sin} per sample (host libm)
     const unsigned count = min(wa.count[3], wa.lane_cap);
-    const unsigned units = (count + 31) / 32;
+    // kSplit adjacent lanes share a hit, each taking every kSplit-th sample:
+    // more warps to hide the float64 latency with, for one more setup per hit
+    constexpr unsigned kSplit = 2, kPer = 32 / kSplit;
+    const unsigned units = (count + kPer - 1) / kPer;
     const unsigned first = (unsigned)(((unsigned long long)units * blockIdx.x) / gridDim.x);
     const unsigned last = (unsigned)(((unsigned long long)units * (blockIdx.x + 1)) / gridDim.x);
-    const unsigned lane = threadIdx.x & 31;
+    const unsigned lane = threadIdx.x & 31, part = lane % kSplit;
     for (unsigned u = first + (threadIdx.x >> 5); u < last; u += blockDim.x >> 5) {
-        const unsigned h = 32u * u + lane;
-        if (h >= count) continue;
+        const unsigned h = kPer * u + lane / kSplit;
+        if (h >= count) continue;  // both lanes of a hit alike
         const double4 P = wa.lane_q[2 * h], N = wa.lane_q[2 * h + 1];
         const double *g = geo + 4 * (int)N.w;
         const d3 surface = mk(P.x, P.y, P.z), normal = mk(N.x, N.y, N.z);
@@ -335,7 +338,7 @@ __device__ void sample_lanes64(const FrameArgs &fa, const SceneArgs<double> &sa,
         if (conic) {
             amb = 0;
 #pragma unroll 4
-            for (int i = 0; i < n; i++) {
+            for (int i = part; i < n; i += kSplit) {
                 double dd, band, a, b;
                 sil(i, dd, band, a, b);
                 const bool open = dd > band || (dd < -band && !(front || fma(z1, a, fma(z2, b, z0)) > 0.0));
@@ -345,7 +348,7 @@ __device__ void sample_lanes64(const FrameArgs &fa, const SceneArgs<double> &sa,
         }
         // pass 2 (rare): the band's samples by the reference's literal test (renderer.py:90-103)
         if (amb) {
-            for (int i = 0; i < n; i++) {
+            for (int i = part; i < n; i += kSplit) {
                 if (conic) {
                     double dd, band, a, b;
                     sil(i, dd, band, a, b);
@@ -356,7 +359,10 @@ __device__ void sample_lanes64(const FrameArgs &fa, const SceneArgs<double> &sa,
                 unblocked += intersect(origin, d, g) < vdistance(surface, s) ? 0 : 1;
             }
         }
-        wa.rec[(int64_t)P.w].w = (double)unblocked / (double)n;
+        const unsigned act = __activemask();
+#pragma unroll
+        for (unsigned o = 1; o < kSplit; o <<= 1) unblocked += __shfl_xor_sync(act, unblocked, o);
+        if (part == 0) wa.rec[(int64_t)P.w].w = (double)unblocked / (double)n;
     }
 }
 

@@ -38,7 +38,7 @@ sys.path.insert(0, ROOT)
 
 NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # SMs x FP32 lanes x FMA x max SM clock
 L2_FLUSH_BYTES = 256 << 20
-EXTRA_CONFIGS = ("C1", "P720", "P1080", "P4K", "C3", "C4", "C5")
+EXTRA_CONFIGS = ("C1", "P720", "P1080", "P4K", "C3", "C4", "C5", "C5_512")
 
 
 def parse_args(argv=None):

@@ -205,12 +205,15 @@ __global__ void __launch_bounds__(kThreads)
     fused_trace(const FrameArgs fa, const SceneArgs<float> sa, const WaveArgs wa, const ParamScene<MAXS> ps) {
     constexpr int kWords = (MAXS + 31) / 32;
     constexpr bool kBundle = ParamScene<MAXS>::kClustered;
-    constexpr int kCandCap = kBundle ? MAXS : 1;
+    // per-warp candidate lists hold at most 256 spheres: larger scenes build and
+    // test them in chunks of 8 mask words (the (t, index) order survives it)
+    constexpr int kCandCap = kBundle ? (MAXS < 256 ? MAXS : 256) : 1;
+    constexpr int kChunkWords = kCandCap / 32 > 0 ? kCandCap / 32 : 1;
     const int lane = threadIdx.x & 31;
     // many-sphere scenes: spheres staged in shared memory for the lane-parallel
     // bundle test, and a per-warp candidate list (see trace_chain_bundle)
-    __shared__ float4 s_sph[kCandCap];
-    __shared__ int s_idx[kCandCap];
+    __shared__ float4 s_sph[kBundle ? MAXS : 1];
+    __shared__ int s_idx[kBundle ? MAXS : 1];
     __shared__ float4 s_cand_sph[kThreads / 32][kCandCap];
     __shared__ int s_cand_idx[kThreads / 32][kCandCap];
     if constexpr (kBundle) {
@@ -265,26 +268,6 @@ __global__ void __launch_bounds__(kThreads)
             const bool cull = cos_t > 0.25f && sn > 0.f;
             cos_t = fminf(cos_t * (1.f - kBoundRel), 1.f);
             const float sin_t = sqrtf(fmaxf(1.f - cos_t * cos_t, 0.f));
-            int ncand = 0;
-#pragma unroll
-            for (int w = 0; w < kWords; w++) {
-                const int b = w * 32 + lane;
-                const float4 g = s_sph[b < ps.ns ? b : 0];
-                bool cand = b < ps.ns && (!cull || sphere_meets_bundle<MAXS>(g, co, A, cos_t, sin_t, rho));
-                const unsigned bm = __ballot_sync(0xffffffffu, cand);
-                if (cand) {
-                    const int at = ncand + __popc(bm & lanemask_lt());
-                    cand_sph[at] = g;
-                    cand_idx[at] = s_idx[b];
-                }
-                ncand += __popc(bm);
-            }
-            __syncwarp();
-            if (wa.work && lane == 0) {
-                atomicAdd(wa.work + kWorkTraceRays, (unsigned long long)__popc(live));
-                atomicAdd(wa.work + kWorkTraceTests, (unsigned long long)__popc(live) * ncand);
-                if (!cull) atomicAdd(wa.work + kWorkTraceFullWarps, 1ull);
-            }
             if (alive) {
 #pragma unroll
                 for (int j = 0; j < kMaxPlanes; j++) {
@@ -296,22 +279,47 @@ __global__ void __launch_bounds__(kThreads)
                         h.g = make_float4(0.f, ps.pl_h[j], 0.f, -1.f);
                     }
                 }
-                int best = -1;
+            }
+            for (int w0 = 0; w0 < kWords; w0 += kChunkWords) {
+                int ncand = 0;
+#pragma unroll
+                for (int w = w0; w < w0 + kChunkWords; w++) {
+                    const int b = w * 32 + lane;
+                    const float4 g = s_sph[b < ps.ns ? b : 0];
+                    bool cand = b < ps.ns && (!cull || sphere_meets_bundle<MAXS>(g, co, A, cos_t, sin_t, rho));
+                    const unsigned bm = __ballot_sync(0xffffffffu, cand);
+                    if (cand) {
+                        const int at = ncand + __popc(bm & lanemask_lt());
+                        cand_sph[at] = g;
+                        cand_idx[at] = s_idx[b];
+                    }
+                    ncand += __popc(bm);
+                }
+                __syncwarp();
+                if (wa.work && lane == 0) {
+                    if (w0 == 0) atomicAdd(wa.work + kWorkTraceRays, (unsigned long long)__popc(live));
+                    atomicAdd(wa.work + kWorkTraceTests, (unsigned long long)__popc(live) * ncand);
+                    if (!cull && w0 == 0) atomicAdd(wa.work + kWorkTraceFullWarps, 1ull);
+                }
+                if (alive) {
+                    int best = -1;
 #pragma unroll 4
-                for (int c = 0; c < ncand; c++) {
-                    float t = sphere_t(origin, dir, cand_sph[c]);
-                    if (t <= h.t) {
-                        int id = cand_idx[c];
-                        if (t < h.t || id < h.idx) {  // (t, index) order: lowest original index wins ties
-                            h.t = t;
-                            h.idx = id;
-                            best = c;
+                    for (int c = 0; c < ncand; c++) {
+                        float t = sphere_t(origin, dir, cand_sph[c]);
+                        if (t <= h.t) {
+                            int id = cand_idx[c];
+                            if (t < h.t || id < h.idx) {  // (t, index) order: lowest original index wins ties
+                                h.t = t;
+                                h.idx = id;
+                                best = c;
+                            }
                         }
                     }
+                    if (best >= 0 && h.idx == cand_idx[best]) h.g = cand_sph[best];
                 }
-                if (best >= 0 && h.idx == cand_idx[best]) h.g = cand_sph[best];
+                __syncwarp();  // the list is rebuilt for the next chunk
+                if (ps.ns <= (w0 + kChunkWords) * 32) break;
             }
-            __syncwarp();
         }
         const bool hit_now = alive && h.idx >= 0;
         if (alive && !hit_now) {
@@ -851,11 +859,14 @@ cudaError_t rt_launch_fused_f32(const rt::FrameArgs &fa, const rt::SceneArgs<flo
     cudaError_t e = cudaSuccess;  // the counters were zeroed by the previous frame's trace
     if (ev) cudaEventRecord(ev[0], st);
     ParamScene<8> p8;
-    thread_local ParamScene<kParamSpheres> p256;
+    thread_local ParamScene<kParamMid> p256;
+    thread_local ParamScene<kParamSpheres> p512;
     if (pack_params(sa, p8))
         e = launch(fa, sa, wa, p8, st, ev);
     else if (pack_params(sa, p256))
         e = launch(fa, sa, wa, p256, st, ev);
+    else if (pack_params(sa, p512))
+        e = launch(fa, sa, wa, p512, st, ev);
     else
         return cudaErrorInvalidValue;
     if (e != cudaSuccess) return e;
@@ -905,12 +916,15 @@ cudaError_t rt_build_shadow_grid_f32(const rt::SceneArgs<float> &sa, unsigned *m
         wa.grid_inv[a] = (float)(dims[a] / (hi[a] - lo[a]));
     }
     ParamScene<8> p8;
-    thread_local ParamScene<kParamSpheres> p256;
+    thread_local ParamScene<kParamMid> p256;
+    thread_local ParamScene<kParamSpheres> p512;
     const int blocks = (dims[0] * dims[1] * dims[2] + kThreads - 1) / kThreads;
     if (pack_params(sa, p8))
         shadow_grid_build<8><<<blocks, kThreads, 0, st>>>(p8, sa, wa, mask);
     else if (pack_params(sa, p256))
-        shadow_grid_build<kParamSpheres><<<blocks, kThreads, 0, st>>>(p256, sa, wa, mask);
+        shadow_grid_build<kParamMid><<<blocks, kThreads, 0, st>>>(p256, sa, wa, mask);
+    else if (pack_params(sa, p512))
+        shadow_grid_build<kParamSpheres><<<blocks, kThreads, 0, st>>>(p512, sa, wa, mask);
     else
         return cudaSuccess;
     const cudaError_t e = cudaGetLastError();

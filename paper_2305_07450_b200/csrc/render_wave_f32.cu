@@ -93,8 +93,12 @@ __device__ __forceinline__ void trace_chain_bundle(const ParamScene<MAXS> &ps, c
                                                    const SceneArgs<float> &sa, const WaveArgs &wa, int x, int ly) {
     constexpr int kWords = (MAXS + 31) / 32;
     const int lane = threadIdx.x & 31;
-    __shared__ float4 s_cand_sph[kThreads / 32][MAXS];
-    __shared__ int s_cand_idx[kThreads / 32][MAXS];
+    // candidate lists of at most 256 spheres: larger scenes build and test them
+    // in chunks of 8 mask words (the (t, index) order survives it)
+    constexpr int kCandCap = MAXS < 256 ? MAXS : 256;
+    constexpr int kChunkWords = kCandCap / 32 > 0 ? kCandCap / 32 : 1;
+    __shared__ float4 s_cand_sph[kThreads / 32][kCandCap];
+    __shared__ int s_cand_idx[kThreads / 32][kCandCap];
     float4 *cand_sph = s_cand_sph[threadIdx.x >> 5];
     int *cand_idx = s_cand_idx[threadIdx.x >> 5];
     // the lane-parallel bundle test reads 32 different spheres at once: from
@@ -135,28 +139,6 @@ __device__ __forceinline__ void trace_chain_bundle(const ParamScene<MAXS> &ps, c
         const bool cull = cos_t > 0.25f && sn > 0.f;
         cos_t = fminf(cos_t * (1.f - kBoundRel), 1.f);  // widen the cone for rounding
         const float sin_t = sqrtf(fmaxf(1.f - cos_t * cos_t, 0.f));
-        // compact the candidates into this warp's shared-memory list: every
-        // lane then walks the same entries (broadcast LDS, unrolled)
-        int ncand = 0;
-#pragma unroll
-        for (int w = 0; w < kWords; w++) {
-            const int b = w * 32 + lane;
-            const float4 g = s_sph[b < ps.ns ? b : 0];
-            bool cand = b < ps.ns && (!cull || sphere_meets_bundle<MAXS>(g, co, A, cos_t, sin_t, rho));
-            const unsigned bm = __ballot_sync(0xffffffffu, cand);
-            if (cand) {
-                const int at = ncand + __popc(bm & lanemask_lt());
-                cand_sph[at] = g;
-                cand_idx[at] = s_idx[b];
-            }
-            ncand += __popc(bm);
-        }
-        __syncwarp();
-        if (wa.work && lane == 0) {
-            atomicAdd(wa.work + kWorkTraceRays, (unsigned long long)__popc(live));
-            atomicAdd(wa.work + kWorkTraceTests, (unsigned long long)__popc(live) * ncand);
-            if (!cull) atomicAdd(wa.work + kWorkTraceFullWarps, 1ull);
-        }
         Hit h{-1, INFINITY, make_float4(0.f, 0.f, 0.f, -1.f)};
         if (alive) {
 #pragma unroll
@@ -169,22 +151,49 @@ __device__ __forceinline__ void trace_chain_bundle(const ParamScene<MAXS> &ps, c
                     h.g = make_float4(0.f, ps.pl_h[j], 0.f, -1.f);
                 }
             }
-            int best = -1;
+        }
+        // compact the candidates into this warp's shared-memory list: every
+        // lane then walks the same entries (broadcast LDS, unrolled)
+        for (int w0 = 0; w0 < kWords; w0 += kChunkWords) {
+            int ncand = 0;
+#pragma unroll
+            for (int w = w0; w < w0 + kChunkWords; w++) {
+                const int b = w * 32 + lane;
+                const float4 g = s_sph[b < ps.ns ? b : 0];
+                bool cand = b < ps.ns && (!cull || sphere_meets_bundle<MAXS>(g, co, A, cos_t, sin_t, rho));
+                const unsigned bm = __ballot_sync(0xffffffffu, cand);
+                if (cand) {
+                    const int at = ncand + __popc(bm & lanemask_lt());
+                    cand_sph[at] = g;
+                    cand_idx[at] = s_idx[b];
+                }
+                ncand += __popc(bm);
+            }
+            __syncwarp();
+            if (wa.work && lane == 0) {
+                if (w0 == 0) atomicAdd(wa.work + kWorkTraceRays, (unsigned long long)__popc(live));
+                atomicAdd(wa.work + kWorkTraceTests, (unsigned long long)__popc(live) * ncand);
+                if (!cull && w0 == 0) atomicAdd(wa.work + kWorkTraceFullWarps, 1ull);
+            }
+            if (alive) {
+                int best = -1;
 #pragma unroll 4
-            for (int c = 0; c < ncand; c++) {
-                float t = sphere_t(origin, dir, cand_sph[c]);
-                if (t <= h.t) {
-                    int id = cand_idx[c];
-                    if (t < h.t || id < h.idx) {  // (t, index) order: lowest original index wins ties
-                        h.t = t;
-                        h.idx = id;
-                        best = c;
+                for (int c = 0; c < ncand; c++) {
+                    float t = sphere_t(origin, dir, cand_sph[c]);
+                    if (t <= h.t) {
+                        int id = cand_idx[c];
+                        if (t < h.t || id < h.idx) {  // (t, index) order: lowest original index wins ties
+                            h.t = t;
+                            h.idx = id;
+                            best = c;
+                        }
                     }
                 }
+                if (best >= 0 && h.idx == cand_idx[best]) h.g = cand_sph[best];
             }
-            if (best >= 0 && h.idx == cand_idx[best]) h.g = cand_sph[best];
+            __syncwarp();  // the list is rebuilt for the next chunk
+            if (ps.ns <= (w0 + kChunkWords) * 32) break;
         }
-        __syncwarp();
         const bool hit_now = alive && h.idx >= 0;
         if (alive && !hit_now) {
             if (sa.has_sky) tail = sky_sample(dir, sa.sky, sa.sky_w, sa.sky_h);

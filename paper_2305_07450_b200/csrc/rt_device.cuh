@@ -109,8 +109,12 @@ struct WaveArgs64 {
 // executed-work tallies of the culled shadow kernel (rt_work_counts)
 enum { kWorkHits = 0, kWorkCullTests, kWorkSampledHits, kWorkShadowRays, kWorkSphereTests, kWorkPlaneTests,
        kWorkTraceRays, kWorkTraceTests, kWorkTraceFullWarps, kWorkConicHits, kWorkConicTests, kWorkN };
-constexpr int kParamSpheres = 256;  // scenes up to this many spheres ride in the launch parameters
+constexpr int kParamSpheres = 512;  // scenes up to this many spheres ride in the launch parameters (~15 KB)
+constexpr int kParamMid = 256;      // the culled path's middle size (smaller parameter block and masks)
 constexpr int kMaskWords = kParamSpheres / 32;
+// candidate-mask words per queued hit of the culled path for a scene of ns
+// spheres (the ParamScene<MAXS> instantiation it takes), plus the plane word
+inline int rt_mask_words(int ns) { return (ns <= 8 ? 1 : ns <= kParamMid ? kParamMid / 32 : kMaskWords) + 1; }
 constexpr int kWaveMinSamples = 8;     // soft shadows at or above this take the wavefront path
 constexpr int kGridCells = 48 * 24 * 48;  // shadow grid (x, y, z) of the culled FP32 path
 constexpr int kConic = 4;             // silhouette-form spheres per queued hit (rt_wave.cuh; more: the ray form)

@@ -365,6 +365,12 @@ rt::SceneArgs<R> scene_args(const Dev &d, const DevScene<R> &ds, const HostScene
     return a;
 }
 
+int count_spheres(const HostScene &s) {
+    int ns = 0;
+    for (int b = 0; b < s.n; b++) ns += s.geo[4 * b + 3] >= 0.0 ? 1 : 0;
+    return ns;
+}
+
 int prepare(rt_ctx *ctx, Dev &d, int precision, int samples) {
     int rc;
     RT_CK(cudaSetDevice(d.id));
@@ -499,7 +505,7 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
             return rc;
         if (fused) {
             if ((rc = b.w_queue2.ensure(sizeof(int) * slots)) ||
-                (rc = b.w_mask2.ensure(sizeof(unsigned) * slots * (ctx->scene.n <= 8 ? 2 : rt::kMaskWords + 1))) ||
+                (rc = b.w_mask2.ensure(sizeof(unsigned) * slots * rt::rt_mask_words(count_spheres(ctx->scene)))) ||
                 (rc = b.w_rec.ensure(sizeof(float4) * slots)) ||
                 (rc = b.w_pending.ensure(sizeof(int) * (size_t)wa.n_pix)))  // pend
                 return rc;

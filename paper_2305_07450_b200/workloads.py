@@ -83,12 +83,13 @@ class Config:
     bounces: int
     sky: bool = False
     stress: bool = False
+    spheres: int = 256  # stress scenes: sphere count
 
     def params(self) -> RenderParams:
         return RenderParams(self.samples, self.bounces, self.width, self.height)
 
     def scene(self, skybox: Optional[Skybox] = None) -> Scene:
-        scene = stress_scene() if self.stress else build_benchmark_scene()
+        scene = stress_scene(self.spheres) if self.stress else build_benchmark_scene()
         if self.sky:
             scene.skybox = skybox if skybox is not None else synthetic_skybox()
         return scene
@@ -104,6 +105,8 @@ CONFIGS = {
     "C3": Config("C3 1920x1080 s200 b3 sky", 1920, 1080, 200, 3, sky=True),
     "C4": Config("C4 3840x2160 s200 b3 sky", 3840, 2160, 200, 3, sky=True),
     "C5": Config("C5 3840x2160 s500 b8 stress256", 3840, 2160, 500, 8, stress=True),
+    # "also report 512"
+    "C5_512": Config("C5 3840x2160 s500 b8 stress512", 3840, 2160, 500, 8, stress=True, spheres=512),
     # the paper's measurement condition: 1 sample, 1 bounce
     "P720": Config("paper 1280x720 s1 b1", 1280, 720, 1, 1),
     "P1080": Config("paper 1920x1080 s1 b1", 1920, 1080, 1, 1),

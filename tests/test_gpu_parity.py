@@ -475,3 +475,35 @@ def test_edge_cases_against_oracle(name):
                 assert worst <= 1, f"{name} [{mode}]: worst channel delta {worst}"
     finally:
         _native.set_options(**MODES["cull"])
+
+
+def test_512_sphere_scene_culled_path():
+    """SURVEY.md §8d's 512-sphere stress scene takes the culled path (launch-
+    parameter scene of up to 512 spheres, candidate lists in chunks): exact
+    against its own cull_check frame, within the gates of the oracle, and the
+    FP64 frame bit-identical to it."""
+    s = rt.stress_scene(count=512)
+    cam = rt.CONFIGS["C5"].camera()
+    params = rt.RenderParams(32, 4, 96, 54)
+    ps = rt.pack_scene(s)
+    want, want_rad = oracle.render(vars(ps), cam.position, cam.yaw, cam.pitch, cam.fov, 96, 54, 32, 4, radiance=True)
+    frames = {}
+    try:
+        for name, opts in (("check", dict(wave=True, cull=True, conic=False, cull_check=True)),
+                           ("ray", dict(wave=True, cull=True, conic=False, cull_check=False)),
+                           ("cull", dict(wave=True, cull=True, conic=True, cull_check=False))):
+            _native.set_options(**opts)
+            fb = rt.Framebuffer.create(96, 54)
+            rad = np.zeros((96 * 54, 3), np.float32)
+            rt.render_frame(s, cam, params, fb, radiance=rad)
+            frames[name] = (fb.pixels.copy(), rad)
+    finally:
+        _native.set_options(cull_check=False, **MODES["cull"])
+    np.testing.assert_array_equal(frames["ray"][0], frames["check"][0])
+    np.testing.assert_array_equal(frames["ray"][1], frames["check"][1])
+    for name, (px, rad) in frames.items():
+        parity.assert_byte_gate(px, want, f"512 spheres [{name}]")
+        parity.assert_radiance_gate(rad, want_rad, f"512 spheres [{name}]")
+    fb = rt.Framebuffer.create(96, 54)
+    rt.render_frame(s, cam, params, fb, precision="fp64")
+    np.testing.assert_array_equal(fb.pixels, want)

@@ -54,8 +54,15 @@ def count(cfg, row_step=1):
 
 
 def main():
+    # python tools/work_counts.py [KEY ...]: recount only those configurations
+    path = os.path.join(ROOT, "paper_2305_07450_b200", "work_counts.json")
+    only = sys.argv[1:]
     res = {"model": __doc__.split("\n\n")[1].replace("\n", " "), "configs": {}}
+    if only and os.path.exists(path):
+        res["configs"] = json.load(open(path))["configs"]
     for key, cfg in CONFIGS.items():
+        if only and key not in only:
+            continue
         t = time.time()
         step = 8 if cfg.stress else 1
         c = count(cfg, step)
@@ -63,7 +70,7 @@ def main():
                      row_sample_step=step)
         res["configs"][key] = entry
         print(f"{key}: rays {entry['rays']:.4g} flops {entry['flops']:.4g} ({time.time() - t:.1f}s)", flush=True)
-    with open(os.path.join(ROOT, "paper_2305_07450_b200", "work_counts.json"), "w") as f:
+    with open(path, "w") as f:
         json.dump(res, f, indent=1)
         f.write("\n")
 

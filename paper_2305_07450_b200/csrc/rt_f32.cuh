@@ -60,8 +60,8 @@ __device__ __forceinline__ float sphere_t(float3 o, float3 d, float4 g) {
     float3 p = L - d * tca;
     float rad = g.w - dot3(p, p);
     float t = tca - sqrtf(fmaxf(rad, 0.f));
-    bool hit = (tca >= 0.f) & (rad >= -1e-7f) & (t >= 0.f);
-    return hit ? t : INFINITY;
+    // the reference's tca < 0 miss is implied: t <= tca, so t >= 0 needs tca >= 0
+    return (rad >= -1e-7f && t >= 0.f) ? t : INFINITY;
 }
 
 // geometry.py:108-117

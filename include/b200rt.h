@@ -93,6 +93,24 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
                  double ambient, double max_refl, const float *sky, int32_t sky_w, int32_t sky_h, int32_t has_sky,
                  int32_t shadow_samples, int32_t bounce_limit, int32_t n_parts, int32_t precision);
 
+/* Pipelined frames (the frame server's loop, server.py:276-289): enqueue a
+ * frame exactly as rt_render_v1 renders it on the context's first device
+ * (no radiance, one partition) into frame slot `slot` (0-3) and return at
+ * once; the pixels land in the caller's `pixels` (page-locked for PCIe
+ * speed: rt_host_register) once rt_frame_wait_v1(slot) returns.  Frames run
+ * in submission order and each frame's device-to-host copy overlaps the next
+ * frame's kernels.  The scene arguments are consumed before the call returns;
+ * `pixels` must stay valid until the wait.  Submitting into a slot whose
+ * frame was not waited for waits for it first. */
+int rt_render_async_v1(rt_ctx *ctx, int32_t slot, uint32_t *pixels, int32_t width, int32_t height,
+                       const double cam_pos[3], double yaw, double pitch, double vdist, int32_t n_bodies,
+                       const int32_t *kinds, const double *positions, const double *sizes, const double *colors,
+                       const double *refls, const double light_pos[3], double light_radius,
+                       const double light_color[3], double ambient, double max_refl, const float *sky, int32_t sky_w,
+                       int32_t sky_h, int32_t has_sky, int32_t shadow_samples, int32_t bounce_limit,
+                       int32_t precision);
+int rt_frame_wait_v1(rt_ctx *ctx, int32_t slot);
+
 /* Device-resident render of one row-block partition with the scene last set
  * by rt_set_scene_v1 on device slot `slot`.  Row y is rendered iff
  * (y / block_rows) % n_parts == part; pixel (x, y) is stored at

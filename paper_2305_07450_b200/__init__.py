@@ -30,6 +30,7 @@ from .model import (
     pack_scene,
 )
 from .renderer import (
+    FramePipeline,
     default_precision,
     last_kernel_ms,
     pack_color,

@@ -44,6 +44,9 @@ SIGNATURES = {
                                     _d, _d, _p, _i32, _i32, _i32, _i32, _i32, _i32, _i32]),
     "rt_render_device_v1": (ctypes.c_int, [_p, _i32, _p, _i64, _p, _i32, _i32, _p, _d, _d, _d, _i32, _i32, _i32,
                                            _i32, _i32, _i32, _p]),
+    "rt_render_async_v1": (ctypes.c_int, [_p, _i32, _p, _i32, _i32, _p, _d, _d, _d, _i32, _p, _p, _p, _p, _p, _p, _d,
+                                          _p, _d, _d, _p, _i32, _i32, _i32, _i32, _i32, _i32]),
+    "rt_frame_wait_v1": (ctypes.c_int, [_p, _i32]),
     "rt_trace_rays_v1": (ctypes.c_int, [_p, _p, _p, _i64, _p, _i32, _p, _p, _p, _p, _p, _p, _d, _p, _d, _d, _p,
                                         _i32, _i32, _i32, _i32, _i32, _i32]),
     "rt_sky_sample_v1": (ctypes.c_int, [_p, _p, _i64, _p, _p, _i32, _i32]),

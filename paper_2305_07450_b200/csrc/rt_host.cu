@@ -107,6 +107,12 @@ struct Dev {
     cudaEvent_t fork_ev = nullptr;
     bool ph_valid = false;
     DBuf frame, rad, rays_in, rays_out, sky_raw, sky, counters, w_work;
+    // pipelined frames (rt_render_async_v1): per slot a device frame, the
+    // event its kernels end with and the event its host copy ends with
+    static constexpr int kSlots = 4;
+    DBuf slot_frame[kSlots];
+    cudaEvent_t slot_comp[kSlots] = {}, slot_done[kSlots] = {};
+    bool slot_busy[kSlots] = {};
     DBuf grid;                        // the culled FP32 path's shadow grid (scene + light)
     uint64_t grid_version = ~0ull;
     rt::WaveArgs grid_wa = {};        // its box and dims (grid null: none)
@@ -650,6 +656,10 @@ int rt_ctx_create(rt_ctx **out, const int32_t *devices, int32_t n_devices) {
                   cudaEventCreate(&d.e0) == cudaSuccess && cudaEventCreate(&d.e1) == cudaSuccess;
         for (auto &ev : d.band_ev) ok = ok && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess;
         ok = ok && cudaEventCreateWithFlags(&d.fork_ev, cudaEventDisableTiming) == cudaSuccess;
+        for (int k = 0; ok && k < Dev::kSlots; k++)
+            ok = cudaEventCreateWithFlags(&d.slot_comp[k], cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&d.slot_done[k], cudaEventDisableTiming) ==
+                     cudaSuccess;
         int least = 0, greatest = 0;
         if (ok) cudaDeviceGetStreamPriorityRange(&least, &greatest);
         for (int k = 0; ok && k < kMaxBands; k++)
@@ -685,6 +695,11 @@ int rt_ctx_destroy(rt_ctx *ctx) {
         for (auto bs : d.band_st)
             if (bs) cudaStreamDestroy(bs);
         if (d.fork_ev) cudaEventDestroy(d.fork_ev);
+        for (int k = 0; k < Dev::kSlots; k++) {
+            if (d.slot_comp[k]) cudaEventDestroy(d.slot_comp[k]);
+            if (d.slot_done[k]) cudaEventDestroy(d.slot_done[k]);
+            d.slot_frame[k].release();
+        }
         if (d.copy_st) cudaStreamDestroy(d.copy_st);
         if (d.e0) cudaEventDestroy(d.e0);
         if (d.e1) cudaEventDestroy(d.e1);
@@ -1059,6 +1074,57 @@ int rt_copy_to_host(rt_ctx *ctx, int32_t slot, void *host_dst, const void *d_src
     cudaStream_t st = stream ? (cudaStream_t)stream : d.st;
     RT_CK(cudaMemcpyAsync(host_dst, d_src, bytes, cudaMemcpyDeviceToHost, st));
     RT_CK(cudaStreamSynchronize(st));
+    return RT_OK;
+}
+
+int rt_render_async_v1(rt_ctx *ctx, int32_t slot, uint32_t *pixels, int32_t width, int32_t height,
+                       const double cam_pos[3], double yaw, double pitch, double vdist, int32_t n_bodies,
+                       const int32_t *kinds, const double *positions, const double *sizes, const double *colors,
+                       const double *refls, const double light_pos[3], double light_radius,
+                       const double light_color[3], double ambient, double max_refl, const float *sky, int32_t sky_w,
+                       int32_t sky_h, int32_t has_sky, int32_t shadow_samples, int32_t bounce_limit,
+                       int32_t precision) {
+    if (!ctx || !pixels || !cam_pos) return fail(RT_ERR_INVALID, "null argument");
+    if (slot < 0 || slot >= Dev::kSlots) return fail(RT_ERR_INVALID, "frame slot out of range");
+    int rc = check_frame_args(width, height, shadow_samples, bounce_limit, precision);
+    if (rc) return rc;
+    if ((rc = validate_scene(n_bodies, kinds, positions, sizes, colors, refls, light_pos, light_color, max_refl, sky,
+                             sky_w, sky_h, has_sky)))
+        return rc;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    Dev &d = ctx->devs[0];
+    RT_CK(cudaSetDevice(d.id));
+    if (d.slot_busy[slot]) {  // the slot's previous frame was never waited for
+        RT_CK(cudaEventSynchronize(d.slot_done[slot]));
+        d.slot_busy[slot] = false;
+    }
+    set_host_scene(ctx->scene, n_bodies, kinds, positions, sizes, colors, refls, light_pos, light_radius, light_color,
+                   ambient, max_refl, sky, sky_w, sky_h, has_sky);
+    const size_t px_bytes = sizeof(uint32_t) * (size_t)width * height;
+    if ((rc = prepare(ctx, d, precision, shadow_samples))) return rc;
+    if ((rc = d.slot_frame[slot].ensure(px_bytes))) return rc;
+    // the kernels on the frame stream (frames in order), the copy on the copy
+    // stream: the next frame's kernels overlap this frame's PCIe transfer
+    rt::FrameArgs fa = frame_args((uint32_t *)d.slot_frame[slot].p, width, nullptr, width, height, cam_pos, yaw, pitch,
+                                  vdist, shadow_samples, bounce_limit, 0, 1, RT_DEFAULT_BLOCK_ROWS);
+    RT_CK(cudaEventRecord(d.e0, d.st));
+    if ((rc = launch_frame(ctx, d, fa, precision, d.st))) return rc;
+    RT_CK(cudaEventRecord(d.e1, d.st));
+    RT_CK(cudaEventRecord(d.slot_comp[slot], d.st));
+    RT_CK(cudaStreamWaitEvent(d.copy_st, d.slot_comp[slot], 0));
+    RT_CK(cudaMemcpyAsync(pixels, d.slot_frame[slot].p, px_bytes, cudaMemcpyDeviceToHost, d.copy_st));
+    RT_CK(cudaEventRecord(d.slot_done[slot], d.copy_st));
+    d.slot_busy[slot] = true;
+    return RT_OK;
+}
+
+int rt_frame_wait_v1(rt_ctx *ctx, int32_t slot) {
+    if (!ctx) return fail(RT_ERR_INVALID, "null argument");
+    if (slot < 0 || slot >= Dev::kSlots) return fail(RT_ERR_INVALID, "frame slot out of range");
+    Dev &d = ctx->devs[0];
+    RT_CK(cudaSetDevice(d.id));
+    RT_CK(cudaEventSynchronize(d.slot_done[slot]));
+    d.slot_busy[slot] = false;
     return RT_OK;
 }
 

@@ -41,6 +41,7 @@ __all__ = [
     "skybox_sample",
     "pack_color",
     "default_precision",
+    "FramePipeline",
 ]
 
 _PIN_MIN_BYTES = 1 << 18  # page-lock framebuffers of >= 256 KiB
@@ -116,6 +117,76 @@ def render_frame(scene, cam, params, out, workers=None, *, precision=None, radia
         *_scene_argv(ps), int(params.shadow_samples), int(params.bounce_limit), n_parts, prec,
     )
     _native.check(rc, "rt_render_v1")
+
+
+class FramePipeline:
+    """Frames rendered back to back, each frame's device-to-host copy
+    overlapping the next frame's kernels — the frame server's loop
+    (`FrameLoop.tick`, server.py:276-289) without the idle PCIe time.
+
+    `submit(scene, cam, params, out)` validates like `render_frame`, enqueues
+    the frame and returns a ticket; `wait(ticket)` returns `out` once its
+    pixels are in (bit for bit what `render_frame` gives).  At most `depth`
+    (2-4) frames are in flight; submitting more waits for the oldest.  `out`
+    must not be touched between submit and wait."""
+
+    def __init__(self, depth: int = 2, *, precision=None):
+        if not 1 <= int(depth) <= 4:
+            raise ValueError("depth must be 1-4")
+        self.depth = int(depth)
+        self.precision = precision
+        if _native.device_count() < 1:
+            raise _native.NativeError("no CUDA device visible: the b200rt frame render has no CPU path")
+        # its own context (streams, pinned buffers): render_frame's pinning
+        # never unpins a buffer with a copy in flight here
+        dev = int(os.environ.get("LOCAL_RANK", "0")) % _native.device_count()
+        self.ctx = _native.Context((dev,))
+        for k, v in _native.get_options().items():
+            self.ctx.set_option(k, v)
+        self._next = 0
+        self._pending = {}  # ticket -> framebuffer
+
+    def submit(self, scene, cam, params, out) -> int:
+        if (out.width, out.height) != (params.width, params.height):
+            raise ValueError(
+                f"framebuffer {out.width}x{out.height} does not match params {params.width}x{params.height}"
+            )
+        if params.bounce_limit > MAX_BOUNCE_LIMIT:
+            raise ValueError(f"bounce limit capped at {MAX_BOUNCE_LIMIT}")
+        pixels = out.pixels
+        if pixels.dtype != np.uint32 or not pixels.flags.c_contiguous or pixels.size != params.width * params.height:
+            raise ValueError("framebuffer pixels must be a contiguous uint32 array of width * height")
+        prec = _prec(self.precision)
+        ticket = self._next
+        oldest = ticket - self.depth
+        if oldest in self._pending:
+            self.wait(oldest)
+        self.ctx.pin(pixels, max_pinned=2 * self.depth + 2)
+        ps = pack_scene(scene)
+        cp = cam.position
+        cam_pos = (ctypes.c_double * 3)(cp[0], cp[1], cp[2])
+        rc = _native.load().rt_render_async_v1(
+            self.ctx.handle, ticket % self.depth, self.ctx.address(pixels), int(params.width), int(params.height),
+            cam_pos, float(cam.yaw), float(cam.pitch), camera_viewport_distance(cam.fov), *_scene_argv(ps),
+            int(params.shadow_samples), int(params.bounce_limit), prec,
+        )
+        _native.check(rc, "rt_render_async_v1")
+        self._pending[ticket] = out
+        self._next += 1
+        return ticket
+
+    def wait(self, ticket: int):
+        out = self._pending.pop(ticket)
+        _native.check(_native.load().rt_frame_wait_v1(self.ctx.handle, ticket % self.depth), "rt_frame_wait_v1")
+        return out
+
+    def drain(self):
+        for t in sorted(self._pending):
+            self.wait(t)
+
+    def close(self):
+        self.drain()
+        self.ctx.close()
 
 
 def trace_rays(origins, directions, scene, params, *, precision=None) -> np.ndarray:

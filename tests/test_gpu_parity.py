@@ -507,3 +507,32 @@ def test_512_sphere_scene_culled_path():
     fb = rt.Framebuffer.create(96, 54)
     rt.render_frame(s, cam, params, fb, precision="fp64")
     np.testing.assert_array_equal(fb.pixels, want)
+
+
+@pytest.mark.parametrize("depth", [1, 2, 3])
+def test_frame_pipeline_matches_render_frame(depth):
+    """FramePipeline (rt_render_async_v1 / rt_frame_wait_v1): a sequence of
+    frames with a moving camera and a moving body, several in flight, each
+    equal to render_frame's bytes."""
+    scene = rt.build_benchmark_scene()
+    params = rt.RenderParams(64, 3, 320, 180)
+    pipe = rt.FramePipeline(depth)
+    cams, outs, tickets, wants = [], [], [], []
+    try:
+        for i in range(7):
+            cam = rt.Camera(position=(0.1 * i, 1.4, -4.5), yaw=0.02 * i, pitch=-0.08, fov=60.0)
+            scene.bodies[0].position = (-2.4 + 0.05 * i, 1.0, 2.8)
+            fb = rt.Framebuffer.create(320, 180)
+            tickets.append(pipe.submit(scene, cam, params, fb))
+            outs.append(fb)
+            want = rt.Framebuffer.create(320, 180)
+            rt.render_frame(scene, cam, params, want)
+            wants.append(want.pixels.copy())
+        for t, fb, want in zip(tickets, outs, wants):
+            if t in pipe._pending:
+                pipe.wait(t)
+            np.testing.assert_array_equal(fb.pixels, want, err_msg=f"frame {t}")
+    finally:
+        pipe.close()
+    with pytest.raises(ValueError):
+        rt.FramePipeline(5)

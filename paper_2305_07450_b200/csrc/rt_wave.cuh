@@ -65,11 +65,9 @@ __device__ __forceinline__ float warp_max(float v) {
 // hit's shadow tests, so skipping it leaves the coefficient unchanged; a
 // sphere that swallows the cone's whole cross-section between o and the disc
 // blocks every sample, so the coefficient is exactly 0.  Only hits with a
-// body in the penumbra test rays, and only against those bodies.
-//
-// One warp per hit (hits taken from an atomic counter — their costs now
-// differ): lanes test one body each for the cull, then take the samples
-// lane, lane + 32, ... against the surviving bodies (a warp-uniform mask).
+// body in the penumbra test rays, and only against those bodies
+// (render_fused_f32.cu: the trace kernel classifies, the sample kernel tests
+// the undecided hits' rays).
 constexpr float kCullRel = 1e-4f;  // relative margin of the cull / full-block decisions
 constexpr float kCullAbs = 1e-5f;  // absolute margin (scene units)
 
@@ -220,14 +218,6 @@ __device__ __forceinline__ int plane_class(const Cone &k, float oy, float ly, fl
     return 1;
 }
 
-// Two kernels:
-//  B1  one lane per hit classifies every body (a few instructions per hit);
-//      decided hits (nothing can block: 1, something blocks all: 0) are
-//      written at once, undecided ones go to a second queue with their
-//      body mask (warp-aggregated append);
-//  B2  one warp per undecided hit, 32 samples abreast, against that hit's
-//      surviving bodies only — every queued hit costs the same, so a static
-//      stride keeps the SMs evenly loaded.
 // renderer.py:185-224: the unwind of one pixel's records (body, Lambert,
 // Blinn, shadow coefficient), deepest first; a depth-cut chain shades its
 // last base colour as-is, every other record mixes base*(1-rr) + col*rr.

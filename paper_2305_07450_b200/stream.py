@@ -82,3 +82,71 @@ class FrameEncoder:
 
     def close(self):
         self.ctx.close()
+
+
+class PipelinedFrameEncoder:
+    """`FrameEncoder` for the frame loop (FrameLoop.tick, server.py:276-289):
+    up to `depth` RAYF messages in flight, each frame's device-to-host copy
+    overlapping the next frame's kernels (rt_render_async_v1).
+
+    `submit(...)` returns a ticket; `wait(ticket)` returns that frame's
+    message, valid until `depth` more frames have been submitted."""
+
+    def __init__(self, depth: int = 3, device: int = 0):
+        if not 1 <= int(depth) <= 4:
+            raise ValueError("depth must be 1-4")
+        self.depth = int(depth)
+        self.ctx = _native.Context((int(device),))
+        self.ctx.set_option("rgba", 1)
+        self._bufs = [None] * self.depth
+        self._dims = None
+        self._next = 0
+        self._pending = set()
+
+    def submit(self, scene, cam, params, frame_id: int, *, precision=None) -> int:
+        if params.bounce_limit > MAX_BOUNCE_LIMIT:
+            raise ValueError(f"bounce limit capped at {MAX_BOUNCE_LIMIT}")
+        from .renderer import _prec, _scene_argv
+
+        prec = _prec(precision)
+        w, h = int(params.width), int(params.height)
+        ticket = self._next
+        slot = ticket % self.depth
+        if ticket - self.depth in self._pending:
+            self.wait(ticket - self.depth)
+        if self._dims != (w, h):
+            self.drain()
+            for i in range(self.depth):
+                if self._bufs[i] is not None:
+                    self.ctx.unpin(self._bufs[i])
+                self._bufs[i] = np.zeros(HEADER.size + 4 * w * h, dtype=np.uint8)
+                self.ctx.pin(self._bufs[i], max_pinned=self.depth + 1)
+            self._dims = (w, h)
+        buf = self._bufs[slot]
+        HEADER.pack_into(buf, 0, FRAME_MAGIC, frame_id & 0xFFFFFFFF, w, h, FORMAT_RGBA8)
+        ps = pack_scene(scene)
+        cam_pos = np.array(cam.position, dtype=np.float64)
+        rc = _native.load().rt_render_async_v1(
+            self.ctx.handle, slot, _native.ptr(buf.ctypes.data + HEADER.size), w, h, _native.ptr(cam_pos),
+            float(cam.yaw), float(cam.pitch), camera_viewport_distance(cam.fov), *_scene_argv(ps),
+            int(params.shadow_samples), int(params.bounce_limit), prec,
+        )
+        _native.check(rc, "rt_render_async_v1")
+        self._pending.add(ticket)
+        self._next += 1
+        return ticket
+
+    def wait(self, ticket: int) -> memoryview:
+        slot = ticket % self.depth
+        if ticket in self._pending:
+            _native.check(_native.load().rt_frame_wait_v1(self.ctx.handle, slot), "rt_frame_wait_v1")
+            self._pending.discard(ticket)
+        return memoryview(self._bufs[slot])
+
+    def drain(self):
+        for t in sorted(self._pending):
+            self.wait(t)
+
+    def close(self):
+        self.drain()
+        self.ctx.close()

@@ -45,3 +45,26 @@ def test_frame_encoder_renders_the_wire_message():
             assert bytes(msg) == stream.encode_frame(42, fb)
     finally:
         enc.close()
+
+
+@pytest.mark.gpu
+def test_pipelined_frame_encoder_messages():
+    """Several RAYF messages in flight: each equals the synchronous
+    encoder's message for the same frame."""
+    scene = rt.build_benchmark_scene()
+    params = rt.RenderParams(32, 3, 320, 180)
+    sync = stream.FrameEncoder()
+    pipe = stream.PipelinedFrameEncoder(3)
+    try:
+        want, tickets = [], []
+        for i in range(6):
+            cam = rt.Camera(position=(0.1 * i, 1.4, -4.5), yaw=0.02 * i, pitch=-0.08, fov=60.0)
+            want.append(bytes(sync.render(scene, cam, params, 100 + i)))
+            tickets.append(pipe.submit(scene, cam, params, 100 + i))
+            if i >= 2:  # consume with a lag of two frames, as a frame loop would
+                assert bytes(pipe.wait(tickets[i - 2])) == want[i - 2]
+        for i in (4, 5):
+            assert bytes(pipe.wait(tickets[i])) == want[i]
+    finally:
+        pipe.close()
+        sync.close()

@@ -182,7 +182,7 @@ def run_reference(args):
         "warmup": args.warmup,
         "ms_per_step": 1000.0 / fps,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (the paper's benchmark scene, sceneio.py:314-333)",
@@ -256,24 +256,37 @@ def run_ours(args):
     from paper_2305_07450_b200 import bands
 
     extra_keys = () if (args.no_extra or world > 1) else EXTRA_CONFIGS
-    max_px = max(rt.CONFIGS[k].width * rt.CONFIGS[k].height for k in (args.config, *extra_keys))
+    size_keys = (args.config, *extra_keys, *(("C4",) if world > 1 else ()))
+    max_px = max(rt.CONFIGS[k].width * rt.CONFIGS[k].height for k in size_keys)
     frame_bytes = 4 * cfg.width * cfg.height
     exchange = bands.torch_exchange if world > 1 else (lambda blob: blob)
     ipc = bands.IpcFrame(local, 1, max_px, rank, exchange)
     fb_ptr = ipc.ptr
     tiny = torch.zeros(1, device=dev)
 
-    cur = {"prec": prec}
+    # N > 1: frames are independent units, so the headline shards whole
+    # frames across the GPUs (each renders its own frames into its own
+    # device frame, no collective: "weak" scaling); the north star's row
+    # bands of one frame gathered to rank 0 (strong scaling) are measured too
+    d_local = ctypes.c_void_p()
+    if world > 1:
+        _native.check(lib.rt_device_malloc(local, 4 * max_px, ctypes.byref(d_local)), "rt_device_malloc")
+    cur = {"prec": prec, "mode": "frames"}
 
-    def render_cfg(c, part=rank, n_parts=world, out=None, sync=True):
+    def render_cfg(c, part=None, n_parts=None, out=None, sync=True):
+        bands_mode = world > 1 and cur["mode"] == "bands"
+        if part is None:
+            part, n_parts = (rank, world) if bands_mode else (0, 1)
+        if out is None:
+            out = fb_ptr if (world == 1 or bands_mode) else d_local
         cam = c.camera()
         cp = np.array(cam.position, dtype=np.float64)
-        rc = lib.rt_render_device_v1(ctx.handle, 0, out or fb_ptr, c.width, None, c.width, c.height, _native.ptr(cp),
+        rc = lib.rt_render_device_v1(ctx.handle, 0, out, c.width, None, c.width, c.height, _native.ptr(cp),
                                      float(cam.yaw), float(cam.pitch), rt.camera_viewport_distance(cam.fov),
                                      c.samples, c.bounces, part, n_parts, 8, cur["prec"],
                                      ctypes.c_void_p(stream.cuda_stream))
         _native.check(rc, "rt_render_device_v1")
-        if world > 1 and sync:
+        if bands_mode and sync:
             import torch.distributed as dist
             dist.all_reduce(tiny)  # completes once every rank's band has landed
 
@@ -324,7 +337,10 @@ def run_ours(args):
     def measure(c, warmup, steps, sample_clocks=False):
         """Frames/s, per-phase device times and executed work of config c."""
         r = time_config(c, warmup, steps, sample_clocks)
-        fps_c = len(r["ms"]) / (r["total_ms"] / 1e3)
+        # whole-job frames/s: every rank rendered len(ms) whole frames
+        # ("frames" mode), or the ranks rendered len(ms) frames together ("bands")
+        per = world if (world > 1 and cur["mode"] == "frames") else 1
+        fps_c = per * len(r["ms"]) / (r["total_ms"] / 1e3)
         # per-kernel device times: CUDA events between the kernels on their
         # launch stream, averaged over as many frames as were timed (events
         # cost ~2.5 us each, so they stay out of the timed region itself)
@@ -393,7 +409,7 @@ def run_ours(args):
     else:
         import torch.distributed as dist
 
-        def e2e_run(step):
+        def e2e_run(step, frames_per_step):
             ts = []
             for i in range(max(3, args.warmup) + args.steps):
                 dist.barrier()
@@ -404,20 +420,30 @@ def run_ours(args):
                     ts.append(time.perf_counter() - t)
             t = torch.tensor([sum(ts)], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            return args.steps / float(t.item())
+            return frames_per_step * args.steps / float(t.item())
 
-        # (1) every rank renders its rows into its own device frame and copies
-        # them into a page-locked host frame shared by the node's ranks, over
-        # its own PCIe link (the alternative gather)
-        d_local = ctypes.c_void_p()
-        _native.check(lib.rt_device_malloc(local, frame_bytes, ctypes.byref(d_local)), "rt_device_malloc")
+        # (0) the headline: every rank renders whole frames and reads each back
+        # into its own page-locked host frame over its own PCIe link
+        host_own = torch.empty(cfg.width * cfg.height, dtype=torch.int32, pin_memory=True)
+
+        def own_step():
+            cur["mode"] = "frames"
+            render_cfg(cfg)
+            _native.check(lib.rt_copy_to_host(ctx.handle, 0, ctypes.c_void_p(host_own.data_ptr()), d_local,
+                                              frame_bytes, ctypes.c_void_p(stream.cuda_stream)), "rt_copy_to_host")
+
+        fps_own = e2e_run(own_step, world)
+
+        # (1) one frame split in row bands: every rank renders its rows into its
+        # own device frame and copies them into a page-locked host frame shared
+        # by the node's ranks, over its own PCIe link
         shm = bands.ShmFrame(ctx, cfg.width, cfg.height, rank, bands.torch_exchange)
 
         def shm_step():
-            render_cfg(cfg, out=d_local, sync=False)
+            render_cfg(cfg, part=rank, n_parts=world, out=d_local, sync=False)
             shm.copy_rows(d_local, rank, world, ctypes.c_void_p(stream.cuda_stream))
 
-        fps_shm = e2e_run(shm_step)
+        fps_shm = e2e_run(shm_step, 1)
         ok = True
         if rank == 0:  # the shared frame is the frame
             ref = np.empty(cfg.width * cfg.height, dtype=np.uint32)
@@ -428,25 +454,32 @@ def run_ours(args):
         if rank == 0:
             ok = bool(np.array_equal(ref, shm.pixels))
         shm.close()
-        lib.rt_device_free(d_local)
 
-        # (2) rows gathered into rank 0's device frame (CUDA IPC), one D2H on rank 0
+        # (2) row bands gathered into rank 0's device frame (CUDA IPC), one D2H on rank 0
         host = torch.empty(cfg.width * cfg.height, dtype=torch.int32, pin_memory=True) if rank == 0 else None
 
         def ipc_step():
+            cur["mode"] = "bands"
             render_cfg(cfg)  # its all-reduce orders "every band landed"
             if rank == 0:
                 _native.check(lib.rt_copy_to_host(ctx.handle, 0, ctypes.c_void_p(host.data_ptr()), fb_ptr,
                                                   frame_bytes, ctypes.c_void_p(stream.cuda_stream)),
                               "rt_copy_to_host")
 
-        fps_ipc = e2e_run(ipc_step)
-        e2e = {"value": fps_shm, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": frame_bytes,
-               "path": "rt_render_device_v1 per rank + rt_copy_partition_to_host into a page-locked host frame "
-                       "shared by the ranks (each GPU's rows over its own PCIe link)",
-               "frame_matches_single_gpu_render": ok,
-               "ipc_gather": {"value": fps_ipc, "unit": "frames/s",
-                              "path": "rows into rank 0's device frame over NVLink (CUDA IPC) + one D2H on rank 0"}}
+        fps_ipc = e2e_run(ipc_step, 1)
+        cur["mode"] = "frames"
+        e2e = {"value": fps_own, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": frame_bytes * world,
+               "path": f"rt_render_device_v1 whole frames on each of {world} ranks, each read back into the "
+                       "rank's own page-locked host frame (its own PCIe link)",
+               "row_bands_shared_host_frame": {
+                   "value": fps_shm, "unit": "frames/s", "d2h_bytes_per_step": frame_bytes,
+                   "path": "one frame in row bands: rt_copy_partition_to_host into a page-locked host frame "
+                           "shared by the ranks (each GPU's rows over its own PCIe link)",
+                   "frame_matches_single_gpu_render": ok},
+               "row_bands_ipc_gather": {
+                   "value": fps_ipc, "unit": "frames/s", "d2h_bytes_per_step": frame_bytes,
+                   "path": "one frame in row bands into rank 0's device frame over NVLink (CUDA IPC) + one D2H "
+                           "on rank 0"}}
 
     line = {
         "metric": "frames/s",
@@ -457,12 +490,13 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": main["total_ms"] / args.steps,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f32" if args.precision == "fp32" else "f64",
         "data": "synthetic (the paper's benchmark scene and camera, sceneio.py:314-333)",
         "config": {"workload": cfg.name, "width": cfg.width, "height": cfg.height, "samples": cfg.samples,
-                   "bounces": cfg.bounces, "sky": cfg.sky, "parallelism": f"row-blocks x{world} (8-row interleave)",
+                   "bounces": cfg.bounces, "sky": cfg.sky, "parallelism": (f"frames x{world} (a whole frame per GPU per step, no collective)" if world > 1
+                                   else "one GPU"),
                    "path": "wavefront + exact per-hit occluder culling (default)",
                    "l2": "flushed between timed frames (256 MiB memset outside the event pair)"},
         "mrays_per_s": rays * fps / 1e6,
@@ -473,6 +507,22 @@ def run_ours(args):
         "phases_ms": phases,
         "executed_work": work,
     }
+    if world > 1:
+        # the north star's row bands: one frame split across the GPUs, rows
+        # gathered into rank 0's frame over NVLink (strong scaling), and the
+        # same for 4K, where the split pays
+        bands_lines = {}
+        cur["mode"] = "bands"
+        for key in (args.config, "C4"):
+            c = rt.CONFIGS[key]
+            if c.width * c.height > max_px:
+                continue
+            r = time_config(c, 3, args.steps)
+            bands_lines[key] = {"workload": c.name, "fps": len(r["ms"]) / (r["total_ms"] / 1e3),
+                                "ms_per_frame": r["total_ms"] / len(r["ms"]), "scaling": "strong",
+                                "path": "rt_render_device_v1 row blocks into rank 0's frame (CUDA IPC) + all-reduce"}
+        cur["mode"] = "frames"
+        line["row_bands"] = bands_lines
     if rank == 0 and not args.no_extra and world == 1:
         extra = {}
         for key in extra_keys:
@@ -516,6 +566,8 @@ def run_ours(args):
         import torch.distributed as dist
         dist.barrier()
     ipc.close()
+    if d_local:
+        lib.rt_device_free(d_local)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -2,7 +2,6 @@
 matches the reference's encode_frame bytes; the GPU renders the same message
 directly (R,G,B,A packed by the kernels)."""
 
-import numpy as np
 import pytest
 
 import golden_cases as G

@@ -10,7 +10,6 @@ import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-import numpy as np  # noqa: E402
 
 import paper_2305_07450_b200 as rt  # noqa: E402
 from paper_2305_07450_b200 import _native, renderer  # noqa: E402

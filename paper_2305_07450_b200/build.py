@@ -61,7 +61,7 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
     dflags = [f"-D{d}" for d in defines]
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
     headers.append(os.path.join(INCLUDE, "b200rt.h"))
-    objs = []
+    objs, cmds = [], []
     for src, extra in SOURCES.items():
         s = os.path.join(CSRC, src)
         o = os.path.join(bdir, src.replace(".cu", ".o"))
@@ -72,7 +72,16 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
                 cmd += ["-Xptxas", "-v"]
             if verbose:
                 print(" ".join(cmd), flush=True)
-            subprocess.run(cmd, check=True)
+            cmds.append(cmd)
+    # the translation units are independent: compile them side by side
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as pool:
+        for r in list(pool.map(lambda c: subprocess.run(c, capture_output=not verbose), cmds)):
+            if r.returncode != 0:
+                if r.stderr:
+                    sys.stderr.write(r.stderr.decode(errors="replace"))
+                raise subprocess.CalledProcessError(r.returncode, r.args)
     if force or _stale(lib, objs):
         cmd = [nvcc, *_ccbin(), *ARCH, "-shared", "-o", lib, *objs]
         if verbose:

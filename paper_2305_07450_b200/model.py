@@ -11,6 +11,7 @@ reference's own dataclass instances are accepted as well.
 
 from __future__ import annotations
 
+import array
 import enum
 import math
 from dataclasses import dataclass
@@ -224,13 +225,10 @@ _NO_SKY_ADDR = _address(_NO_SKY)
 _sky_addr = {}  # id(texels) -> (texels, address): skyboxes are re-packed every frame
 
 
-def pack_scene(scene) -> PackedScene:
-    """Pack any object with the reference Scene's attributes (duck-typed).
-
-    The float64 columns are views of ONE buffer (positions | sizes | colors |
-    refls | light position | light colour) so the C-ABI pointers come from a
-    single address lookup: the reference re-packs the scene every frame
-    (renderer.py:331), and so does render_frame here."""
+def _pack_core(scene):
+    """The float64 block (positions | sizes | colors | refls | light position |
+    light colour), the int32 kinds and the sky, as the C ABI takes them
+    (array.array buffers: their addresses cost no numpy round trip)."""
     bodies = scene.bodies
     n = len(bodies)
     light = scene.light
@@ -240,10 +238,13 @@ def pack_scene(scene) -> PackedScene:
     flat += [b.color[i] for b in bodies for i in (0, 1, 2)]
     flat += [b.reflectivity for b in bodies]
     flat += (lp[0], lp[1], lp[2], lc[0], lc[1], lc[2])
-    buf = np.array(flat, dtype=np.float64)
-    if buf.shape != (8 * n + 6,):
+    try:
+        buf = array.array("d", flat)
+    except TypeError:
+        buf = array.array("d", [float(v) for v in flat])
+    if len(buf) != 8 * n + 6:
         raise ValueError("body positions and colours must be 3-vectors of numbers")
-    kinds = np.array([int(b.kind) for b in bodies], dtype=np.int32)
+    kinds = array.array("i", [int(b.kind) for b in bodies])
     sky = getattr(scene, "skybox", None)
     if sky is None:
         texels, sw, sh, has, sky_addr = _NO_SKY, 1, 1, False, _NO_SKY_ADDR
@@ -258,6 +259,32 @@ def pack_scene(scene) -> PackedScene:
                 _sky_addr.clear()
             sky_addr = _address(texels)
             _sky_addr[id(texels)] = (texels, sky_addr)
+    base = buf.buffer_info()[0]
+    radius, ambient, max_refl = float(light.radius), float(scene.ambient), float(scene.max_reflectivity)
+    # C-ABI scene arguments of rt_render_v1 / rt_render_async_v1 / rt_trace_rays_v1 (b200rt.h)
+    argv = (n, kinds.buffer_info()[0] if n else 0, base, base + 24 * n, base + 32 * n, base + 56 * n,
+            base + 64 * n, radius, base + 64 * n + 24, ambient, max_refl, sky_addr, sw, sh, int(has))
+    return buf, kinds, texels, argv
+
+
+def scene_argv(scene):
+    """(C-ABI scene arguments, the arrays they point into) — render_frame's
+    per-frame packing without the PackedScene views."""
+    buf, kinds, texels, argv = _pack_core(scene)
+    return argv, (buf, kinds, texels)
+
+
+def pack_scene(scene) -> PackedScene:
+    """Pack any object with the reference Scene's attributes (duck-typed).
+
+    The float64 columns are views of ONE buffer (positions | sizes | colors |
+    refls | light position | light colour) so the C-ABI pointers come from a
+    single address lookup: the reference re-packs the scene every frame
+    (renderer.py:331), and so does render_frame here."""
+    buf_a, kinds_a, texels, argv = _pack_core(scene)
+    buf = np.frombuffer(buf_a, dtype=np.float64)
+    kinds = np.frombuffer(kinds_a, dtype=np.int32) if len(kinds_a) else np.zeros(0, dtype=np.int32)
+    n = argv[0]
     ps = PackedScene(
         kinds=kinds,
         positions=buf[0:3 * n].reshape(n, 3),
@@ -265,19 +292,17 @@ def pack_scene(scene) -> PackedScene:
         colors=buf[4 * n:7 * n].reshape(n, 3),
         refls=buf[7 * n:8 * n],
         light_pos=buf[8 * n:8 * n + 3],
-        light_radius=float(light.radius),
+        light_radius=argv[7],
         light_color=buf[8 * n + 3:8 * n + 6],
-        ambient=float(scene.ambient),
-        max_refl=float(scene.max_reflectivity),
+        ambient=argv[9],
+        max_refl=argv[10],
         sky=texels,
-        sky_w=sw,
-        sky_h=sh,
-        has_sky=has,
+        sky_w=argv[12],
+        sky_h=argv[13],
+        has_sky=bool(argv[14]),
     )
-    base = _address(buf)
-    # C-ABI scene arguments of rt_render_v1 / rt_trace_rays_v1 / rt_stream_* (b200rt.h)
-    ps.argv = (n, _address(kinds), base, base + 24 * n, base + 32 * n, base + 56 * n, base + 64 * n,
-               ps.light_radius, base + 64 * n + 24, ps.ambient, ps.max_refl, sky_addr, sw, sh, int(has))
+    ps.argv = (argv[0], _address(kinds)) + argv[2:] if argv[0] else argv
+    ps._keep = (buf_a, kinds_a)
     return ps
 
 

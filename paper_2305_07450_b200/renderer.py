@@ -30,7 +30,7 @@ import os
 import numpy as np
 
 from . import _native
-from .model import MAX_BOUNCE_LIMIT, REFLECT_EPS, camera_viewport_distance, pack_scene
+from .model import MAX_BOUNCE_LIMIT, REFLECT_EPS, camera_viewport_distance, pack_scene, scene_argv
 
 __all__ = [
     "MAX_BOUNCE_LIMIT",
@@ -108,14 +108,15 @@ def render_frame(scene, cam, params, out, workers=None, *, precision=None, radia
     ctx = _native.context(n_parts)
     if pixels.nbytes >= _PIN_MIN_BYTES:
         ctx.pin(pixels)
-    ps = pack_scene(scene)
+    argv, keep = scene_argv(scene)
     cp = cam.position
     cam_pos = (ctypes.c_double * 3)(cp[0], cp[1], cp[2])
     rc = _native.load().rt_render_v1(
         ctx.handle, ctx.address(pixels), _native.ptr(radiance), int(params.width), int(params.height),
         cam_pos, float(cam.yaw), float(cam.pitch), camera_viewport_distance(cam.fov),
-        *_scene_argv(ps), int(params.shadow_samples), int(params.bounce_limit), n_parts, prec,
+        *argv, int(params.shadow_samples), int(params.bounce_limit), n_parts, prec,
     )
+    del keep
     _native.check(rc, "rt_render_v1")
 
 
@@ -162,14 +163,15 @@ class FramePipeline:
         if oldest in self._pending:
             self.wait(oldest)
         self.ctx.pin(pixels, max_pinned=2 * self.depth + 2)
-        ps = pack_scene(scene)
+        argv, keep = scene_argv(scene)
         cp = cam.position
         cam_pos = (ctypes.c_double * 3)(cp[0], cp[1], cp[2])
         rc = _native.load().rt_render_async_v1(
             self.ctx.handle, ticket % self.depth, self.ctx.address(pixels), int(params.width), int(params.height),
-            cam_pos, float(cam.yaw), float(cam.pitch), camera_viewport_distance(cam.fov), *_scene_argv(ps),
+            cam_pos, float(cam.yaw), float(cam.pitch), camera_viewport_distance(cam.fov), *argv,
             int(params.shadow_samples), int(params.bounce_limit), prec,
         )
+        del keep
         _native.check(rc, "rt_render_async_v1")
         self._pending[ticket] = out
         self._next += 1

@@ -87,7 +87,29 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
+    if not defines:
+        build_pyfast(verbose, force)
     return lib
+
+
+def build_pyfast(verbose: bool = False, force: bool = False):
+    """The CPython fast path of render_frame (csrc/pyfast.c): scene packing
+    and the rt_render_v1 call without ctypes marshalling.  Optional: without
+    a C compiler or Python headers the ctypes path serves."""
+    import sysconfig
+
+    src = os.path.join(CSRC, "pyfast.c")
+    out = os.path.join(PKG, "_pyfast" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
+    cc = "/usr/bin/gcc" if os.path.exists("/usr/bin/gcc") else shutil.which("gcc")
+    inc = sysconfig.get_paths().get("include")
+    if not cc or not inc or not os.path.exists(os.path.join(inc, "Python.h")):
+        return None
+    if force or _stale(out, [src, __file__]):
+        cmd = [cc, "-O2", "-shared", "-fPIC", "-I", inc, "-I", INCLUDE, src, "-o", out]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    return out
 
 
 if __name__ == "__main__":

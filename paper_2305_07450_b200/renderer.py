@@ -47,6 +47,25 @@ __all__ = [
 _PIN_MIN_BYTES = 1 << 18  # page-lock framebuffers of >= 256 KiB
 
 
+_FAST = []  # [module or None]: the CPython fast path (csrc/pyfast.c), loaded once
+
+
+def _fast():
+    """The CPython fast path (scene packing + the C-ABI call without ctypes
+    marshalling), or None when it is not built: the ctypes path serves."""
+    if not _FAST:
+        try:
+            from . import _pyfast
+        except ImportError:
+            _FAST.append(None)
+        else:
+            lib = _native.load()
+            _pyfast.set_entry_points(ctypes.cast(lib.rt_render_v1, ctypes.c_void_p).value,
+                                     ctypes.cast(lib.rt_render_async_v1, ctypes.c_void_p).value)
+            _FAST.append(_pyfast)
+    return _FAST[0]
+
+
 def default_precision() -> str:
     return os.environ.get("B200RT_PRECISION", "fp32")
 
@@ -108,15 +127,23 @@ def render_frame(scene, cam, params, out, workers=None, *, precision=None, radia
     ctx = _native.context(n_parts)
     if pixels.nbytes >= _PIN_MIN_BYTES:
         ctx.pin(pixels)
-    argv, keep = scene_argv(scene)
-    cp = cam.position
-    cam_pos = (ctypes.c_double * 3)(cp[0], cp[1], cp[2])
-    rc = _native.load().rt_render_v1(
-        ctx.handle, ctx.address(pixels), _native.ptr(radiance), int(params.width), int(params.height),
-        cam_pos, float(cam.yaw), float(cam.pitch), camera_viewport_distance(cam.fov),
-        *argv, int(params.shadow_samples), int(params.bounce_limit), n_parts, prec,
-    )
-    del keep
+    fast = _fast()
+    rc = None
+    if fast is not None:
+        rc = fast.render(ctx.handle.value, ctx.address(pixels), 0 if radiance is None else _native.ptr(radiance).value,
+                         int(params.width), int(params.height), cam.position, float(cam.yaw), float(cam.pitch),
+                         camera_viewport_distance(cam.fov), scene, int(params.shadow_samples),
+                         int(params.bounce_limit), n_parts, prec)
+    if rc is None:  # no fast path, or a scene it does not take: the ctypes path (and its errors)
+        argv, keep = scene_argv(scene)
+        cp = cam.position
+        cam_pos = (ctypes.c_double * 3)(cp[0], cp[1], cp[2])
+        rc = _native.load().rt_render_v1(
+            ctx.handle, ctx.address(pixels), _native.ptr(radiance), int(params.width), int(params.height),
+            cam_pos, float(cam.yaw), float(cam.pitch), camera_viewport_distance(cam.fov),
+            *argv, int(params.shadow_samples), int(params.bounce_limit), n_parts, prec,
+        )
+        del keep
     _native.check(rc, "rt_render_v1")
 
 
@@ -163,15 +190,23 @@ class FramePipeline:
         if oldest in self._pending:
             self.wait(oldest)
         self.ctx.pin(pixels, max_pinned=2 * self.depth + 2)
-        argv, keep = scene_argv(scene)
-        cp = cam.position
-        cam_pos = (ctypes.c_double * 3)(cp[0], cp[1], cp[2])
-        rc = _native.load().rt_render_async_v1(
-            self.ctx.handle, ticket % self.depth, self.ctx.address(pixels), int(params.width), int(params.height),
-            cam_pos, float(cam.yaw), float(cam.pitch), camera_viewport_distance(cam.fov), *argv,
-            int(params.shadow_samples), int(params.bounce_limit), prec,
-        )
-        del keep
+        fast = _fast()
+        rc = None
+        if fast is not None:
+            rc = fast.render_async(self.ctx.handle.value, ticket % self.depth, self.ctx.address(pixels),
+                                   int(params.width), int(params.height), cam.position, float(cam.yaw),
+                                   float(cam.pitch), camera_viewport_distance(cam.fov), scene,
+                                   int(params.shadow_samples), int(params.bounce_limit), prec)
+        if rc is None:
+            argv, keep = scene_argv(scene)
+            cp = cam.position
+            cam_pos = (ctypes.c_double * 3)(cp[0], cp[1], cp[2])
+            rc = _native.load().rt_render_async_v1(
+                self.ctx.handle, ticket % self.depth, self.ctx.address(pixels), int(params.width),
+                int(params.height), cam_pos, float(cam.yaw), float(cam.pitch), camera_viewport_distance(cam.fov),
+                *argv, int(params.shadow_samples), int(params.bounce_limit), prec,
+            )
+            del keep
         _native.check(rc, "rt_render_async_v1")
         self._pending[ticket] = out
         self._next += 1

@@ -536,3 +536,21 @@ def test_frame_pipeline_matches_render_frame(depth):
         pipe.close()
     with pytest.raises(ValueError):
         rt.FramePipeline(5)
+
+
+def test_fast_and_ctypes_paths_give_the_same_frame():
+    from paper_2305_07450_b200 import renderer
+
+    cfg = rt.CONFIGS["C3"]
+    scene, cam = cfg.scene(), cfg.camera()
+    params = rt.RenderParams(64, 3, 320, 180)
+    a = rt.Framebuffer.create(320, 180)
+    rt.render_frame(scene, cam, params, a)
+    saved = list(renderer._FAST)
+    renderer._FAST[:] = [None]
+    try:
+        b = rt.Framebuffer.create(320, 180)
+        rt.render_frame(scene, cam, params, b)
+    finally:
+        renderer._FAST[:] = saved
+    np.testing.assert_array_equal(a.pixels, b.pixels)

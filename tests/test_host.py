@@ -173,3 +173,28 @@ def test_work_counts_cover_every_config():
     assert wc["C1"]["flops"] == pytest.approx(4.911e7, rel=1e-3)
     assert wc["C2"]["rays"] == 129_330_618
     assert wc["C4"]["rays"] == 1_164_482_622
+
+
+def test_cpython_fast_path_packs_or_declines():
+    """csrc/pyfast.c: with a null context the C ABI rejects the call after the
+    scene was read (RT_ERR_INVALID); a scene it cannot read is declined (None)
+    so the ctypes path raises the reference's errors."""
+    from paper_2305_07450_b200 import renderer
+
+    fast = renderer._fast()
+    if fast is None:
+        pytest.skip("the CPython fast path is not built")
+    scene = rt.build_benchmark_scene()
+    cam = rt.benchmark_camera()
+    assert fast.render(0, 1, 0, 8, 8, cam.position, 0.0, 0.0, 1.7, scene, 1, 1, 1, 0) == -1
+
+    class Broken:
+        bodies = [object()]
+        light = None
+
+    assert fast.render(0, 1, 0, 8, 8, cam.position, 0.0, 0.0, 1.7, Broken(), 1, 1, 1, 0) is None
+    sky_scene = rt.build_benchmark_scene()
+    sky_scene.skybox = types.SimpleNamespace(width=4, height=2, texels=np.zeros((2, 4, 3)))  # float64: declined
+    assert fast.render(0, 1, 0, 8, 8, cam.position, 0.0, 0.0, 1.7, sky_scene, 1, 1, 1, 0) is None
+    sky_scene.skybox = rt.Skybox(4, 2, np.zeros((2, 4, 3), dtype=np.float32))  # taken
+    assert fast.render(0, 1, 0, 8, 8, cam.position, 0.0, 0.0, 1.7, sky_scene, 1, 1, 1, 0) == -1

@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kThreads) render_f64_kernel(const FrameArgs fa
     extern __shared__ double smem_geo[];
     const double *__restrict__ geo = stage_geo<SMEM>(sa, smem_geo);
     int x, ly;
-    thread_pixel(x, ly);
+    thread_pixel_bottom_first(x, ly);
     if (x >= fa.width || ly >= fa.local_rows) return;
     int y = map_row(ly, fa);
     if (y >= fa.row_end) return;

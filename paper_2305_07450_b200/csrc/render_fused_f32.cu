@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? 8 : 6)
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 8) wa.count_next[threadIdx.x] = 0;
 
     int x, ly;
-    thread_pixel(x, ly);
+    thread_pixel_bottom_first(x, ly);
     int y = 0;
     bool alive = x < fa.width && ly < fa.local_rows;
     if (alive) {

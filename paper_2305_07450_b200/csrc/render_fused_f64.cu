@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kThreads)
     const double *__restrict__ geo = stage(sa, smem_geo);
     const int lane = threadIdx.x & 31;
     int x, ly;
-    thread_pixel(x, ly);
+    thread_pixel_bottom_first(x, ly);
     int y = 0;
     bool alive = x < fa.width && ly < fa.local_rows;
     if (alive) {

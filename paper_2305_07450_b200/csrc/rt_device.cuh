@@ -156,6 +156,15 @@ __device__ __forceinline__ void thread_pixel(int &x, int &ly) {
     ly = blockIdx.y * kTileH + (warp >> 1) * 4 + (lane >> 3);
 }
 
+// The same with the tile rows taken bottom first: blocks are dispatched in
+// index order, and the scene sits below the horizon, so the costly tiles
+// start first and cheap sky tiles fill the last wave.
+__device__ __forceinline__ void thread_pixel_bottom_first(int &x, int &ly) {
+    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    x = blockIdx.x * kTileW + (warp & 1) * 8 + (lane & 7);
+    ly = (gridDim.y - 1 - blockIdx.y) * kTileH + (warp >> 1) * 4 + (lane >> 3);
+}
+
 // renderer.py:45-50.  rgba = 0: 0xAARRGGBB (the reference's Framebuffer,
 // bytes B,G,R,A); rgba = 1: bytes R,G,B,A — the frame server's wire format
 // (server.py:56-64), so a frame can be streamed without a host-side repack.

@@ -468,10 +468,7 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
     cudaError_t e;
     fa.rgba = ctx->rgba;
     if (fa.local_rows == 0) return RT_OK;
-    int rc = d.counters.ensure(sizeof(unsigned) * rt::kCounterRing);
-    if (rc) return rc;
-    fa.work_counter = (unsigned *)d.counters.p + (d.counter_slot++ % rt::kCounterRing);
-    RT_CK(cudaMemsetAsync(fa.work_counter, 0, sizeof(unsigned), st));
+    int rc = RT_OK;
     d.ph_valid = false;
     if (precision == RT_PREC_FP64 && fa.samples >= rt::kWaveMinSamples && ctx->wave && ctx->cull &&
         ctx->scene.n <= rt::kMaxBodies64) {
@@ -569,6 +566,11 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         d.ph_valid = ctx->phases;
         ctx->launches += nk - 1;  // the common increment below counts one
     } else {
+        // the FP32 megakernel's persistent warps take patches from a counter:
+        // a fresh ring slot per launch (concurrent bands never share one)
+        if ((rc = d.counters.ensure(sizeof(unsigned) * rt::kCounterRing))) return rc;
+        fa.work_counter = (unsigned *)d.counters.p + (d.counter_slot++ % rt::kCounterRing);
+        RT_CK(cudaMemsetAsync(fa.work_counter, 0, sizeof(unsigned), st));
         e = rt_launch_render_f32(fa, scene_args(d, d.s32, ctx->scene), st);
     }
     if (e != cudaSuccess) return fail(RT_ERR_CUDA, std::string("render kernel launch: ") + cudaGetErrorString(e));

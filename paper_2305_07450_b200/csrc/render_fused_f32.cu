@@ -444,8 +444,28 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? 8 : 6)
 // pixel with this one pending hit is unwound and packed at once (its other
 // records are decided); with several, the coefficient is stored and the last
 // of the pixel's samplers — an atomic countdown, fenced both ways — unwinds it.
+// The first records of a parked pixel, loaded ahead (their latency hides
+// behind the sampling); kPre covers every record of a frame of up to 3 bounces.
+constexpr int kPre = 4;
+struct PreRecords {
+    float4 r[kPre];
+    int n;  // how many of r are loaded
+};
+
+__device__ __forceinline__ PreRecords prefetch_records(const WaveArgs &wa, int slot, float4 px) {
+    PreRecords p;
+    const int n_pix = (int)wa.n_pix;
+    const int lp = slot - (slot / n_pix) * n_pix;
+    const int m = __float_as_int(px.w) & 0xff;
+    p.n = m < kPre ? m : kPre;
+#pragma unroll
+    for (int k = 0; k < kPre; k++) p.r[k] = k < p.n ? __ldcg(wa.rec + (int64_t)k * n_pix + lp) : make_float4(0, 0, 0, 0);
+    return p;
+}
+
 __device__ __forceinline__ void resolve_hit(const FrameArgs &fa, const SceneArgs<float> &sa, const WaveArgs &wa,
-                                            int slot, float sc, float4 px, const float4 *mat4) {
+                                            int slot, float sc, float4 px, const float4 *mat4,
+                                            const PreRecords *pre = nullptr) {
     const int n_pix = (int)wa.n_pix;
     const int kh = slot / n_pix, lp = slot - kh * n_pix;
     const int info = __float_as_int(px.w);
@@ -457,8 +477,14 @@ __device__ __forceinline__ void resolve_hit(const FrameArgs &fa, const SceneArgs
         __threadfence();
     }
     const int m = info & 0xff;
+    // records of a single-pending pixel do not change after the trace: the
+    // prefetched ones serve; with several pending, the coefficients just landed
+    const int have = (pre && !several) ? pre->n : 0;
     float4 rk[kMaxBounce + 1];  // every record load in flight before the first use
-    for (int k = 0; k < m; k++) rk[k] = __ldcg(wa.rec + (int64_t)k * n_pix + lp);
+#pragma unroll
+    for (int k = 0; k < kPre; k++)
+        if (k < have) rk[k] = pre->r[k];
+    for (int k = have; k < m; k++) rk[k] = __ldcg(wa.rec + (int64_t)k * n_pix + lp);
     const float3 c = unwind(
         m, (info >> 8) & 1, f3(px.x, px.y, px.z), sa,
         [&](int k) { return Record{__float_as_int(rk[k].x), rk[k].y, rk[k].z, (k == kh && !several) ? sc : rk[k].w}; },
@@ -682,6 +708,7 @@ __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArg
         float4 A, B;
         const int r = conic_coeffs(k, g, f.lo, f.bu, f.bv, f.ls2, A, B);
         const float b0 = dot3(f.lo, f.lo), b1 = 2.f * dot3(f.lo, f.bu), b2 = 2.f * dot3(f.lo, f.bv);
+        const PreRecords pre = prefetch_records(wa, slot, px);
         unsigned blocked = 0;
         const unsigned act = __activemask();
         if (__any_sync(act, r == 0)) {
@@ -709,7 +736,7 @@ __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArg
 #pragma unroll 4
             for (int i = 0; i < n; i++) blocked += conic_blocked(A, B, b0, b1, b2, table(i));
         }
-        resolve_hit(fa, sa, wa, slot, (float)(n - (int)blocked) / (float)n, px, mat4);
+        resolve_hit(fa, sa, wa, slot, (float)(n - (int)blocked) / (float)n, px, mat4, &pre);
         if (wa.work) {
             if (r != 0) {
                 atomicAdd(wa.work + kWorkConicHits, 1ull);

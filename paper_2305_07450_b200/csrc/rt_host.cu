@@ -470,7 +470,10 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
     if (fa.local_rows == 0) return RT_OK;
     int rc = RT_OK;
     d.ph_valid = false;
-    if (precision == RT_PREC_FP64 && fa.samples >= rt::kWaveMinSamples && ctx->wave && ctx->cull &&
+    // queued hits carry their record slot (bounce * pixels + pixel) in 31 bits:
+    // larger frame x bounce products take the megakernels, which queue nothing
+    const bool slots_fit = (int64_t)fa.local_rows * fa.width * (fa.bounces + 1) < ((int64_t)1 << 31);
+    if (precision == RT_PREC_FP64 && fa.samples >= rt::kWaveMinSamples && ctx->wave && ctx->cull && slots_fit &&
         ctx->scene.n <= rt::kMaxBodies64) {
         rt::WaveArgs64 wa = {};
         wa.n_pix = (int64_t)fa.local_rows * fa.width;
@@ -497,7 +500,7 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         ctx->launches += nk - 1;
     } else if (precision == RT_PREC_FP64) {
         e = rt_launch_render_f64(fa, scene_args(d, d.s64, ctx->scene), st);
-    } else if (fa.samples >= rt::kWaveMinSamples && ctx->wave) {
+    } else if (fa.samples >= rt::kWaveMinSamples && ctx->wave && slots_fit) {
         const rt::SceneArgs<float> sa = scene_args(d, d.s32, ctx->scene);
         const bool fused = ctx->cull && rt_fused_fits(sa);
         rt::WaveArgs wa = {};

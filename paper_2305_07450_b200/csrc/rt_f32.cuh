@@ -309,7 +309,9 @@ static __device__ float3 sky_sample(float3 d, const float4 *__restrict__ sky, in
     float dy = fminf(fmaxf(d.y, -1.f), 1.f);
     float v = 0.5f - asinf(dy) * 0.3183098861837907f;
     int tx = (int)floorf(u * (float)W);
-    tx = ((tx % W) + W) % W;
+    // ((tx % W) + W) % W of renderer.py:67 for the only reachable tx, -1..W
+    // (u is within rounding of [0, 1]): no integer divisions
+    tx = tx < 0 ? tx + W : (tx >= W ? tx - W : tx);
     int ty = (int)floorf(v * (float)H);
     ty = min(max(ty, 0), H - 1);
     float4 t = __ldg(sky + (int64_t)ty * W + tx);

@@ -99,7 +99,9 @@ static __device__ d3 sky_sample(d3 d, const float4 *__restrict__ sky, int W, int
     dy = dy > 1.0 ? 1.0 : dy;
     double v = 0.5 - asin(dy) / 3.141592653589793;
     long long tx = (long long)floor(u * (double)W);
-    tx = ((tx % W) + W) % W;
+    // ((tx % W) + W) % W for the only reachable tx, -1..W (u is within
+    // rounding of [0, 1]): no 64-bit integer divisions
+    tx = tx < 0 ? tx + W : (tx >= W ? tx - W : tx);
     long long ty = (long long)floor(v * (double)H);
     if (ty < 0)
         ty = 0;

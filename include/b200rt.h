@@ -162,6 +162,10 @@ int rt_host_unregister(rt_ctx *ctx, void *ptr);
  *                 priority), and copies each to the host as soon as it is
  *                 done; 0 (default) = by frame size: 1 below 1 MB, 2 below
  *                 6 MB, 4 below 24 MB, else 6;
+ *   "band_first"  permille of the frame's rows in band 0 (0, default: equal
+ *                 bands; the others always share the rest equally);
+ *   "band_times"  record timed events at each band's kernel end and copy end
+ *                 (rt_band_times_ms);
  *   "phases"      record CUDA events between the wavefront kernels so
  *                 rt_phase_ms can report per-phase device times (off by
  *                 default: each event record costs the GPU ~2-3 us);
@@ -189,6 +193,11 @@ int rt_last_kernel_ms(rt_ctx *ctx, float *ms);
  * out[0] trace, out[1] classify (culled path), out[2] shadow / sample,
  * out[3] shade.  Zeros when no wavefront frame ran. */
 int rt_phase_ms(rt_ctx *ctx, float *out, int32_t n);
+/* With option "band_times": for each row band of the last single-device
+ * rt_render_v1, out[2k] = ms from the frame's start to the end of band k's
+ * kernels and out[2k+1] = to the end of its device-to-host copy (n >= 2 *
+ * bands).  Returns the number of bands (0: none timed), or a negative code. */
+int rt_band_times_ms(rt_ctx *ctx, float *out, int32_t n);
 /* Number of kernels this ctx has launched so far. */
 int rt_launch_count(rt_ctx *ctx, int64_t *count);
 

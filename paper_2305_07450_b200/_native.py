@@ -56,6 +56,7 @@ SIGNATURES = {
     "rt_work_counts": (ctypes.c_int, [_p, _p, _i32, _i32]),
     "rt_last_kernel_ms": (ctypes.c_int, [_p, _p]),
     "rt_phase_ms": (ctypes.c_int, [_p, _p, _i32]),
+    "rt_band_times_ms": (ctypes.c_int, [_p, _p, _i32]),
     "rt_launch_count": (ctypes.c_int, [_p, _p]),
     "rt_ipc_get_handle": (ctypes.c_int, [_p, _p]),
     "rt_ipc_open": (ctypes.c_int, [_p, _p]),
@@ -207,6 +208,13 @@ class Context:
         arr = (ctypes.c_float * 4)()
         check(load().rt_phase_ms(self.handle, arr, 4), "rt_phase_ms")
         return dict(zip(("trace", "classify", "shadow", "shade"), (float(v) for v in arr)))
+
+    def band_times_ms(self) -> list:
+        """[(kernels_end_ms, copy_end_ms)] per row band of the last frame (option "band_times")."""
+        arr = (ctypes.c_float * 16)()
+        n = load().rt_band_times_ms(self.handle, arr, 16)
+        check(min(n, 0), "rt_band_times_ms")
+        return [(float(arr[2 * k]), float(arr[2 * k + 1])) for k in range(n)]
 
     def launch_count(self) -> int:
         v = _i64(0)

@@ -42,6 +42,7 @@ struct FrameArgs {
     unsigned int *work_counter;  // zeroed before the launch: persistent warps take 8x4 patches from it
     int sub_part, sub_parts;     // within a band: rows interleaved in 8-row blocks (sub_parts = 1: all)
     int row_end;                 // rows >= row_end are skipped (end of the band / frame)
+    int row0;                    // first frame row of a contiguous band (sub_parts > 1 or n_parts == 1)
     int rgba;                    // pixel byte order: 0 B,G,R,A (0xAARRGGBB), 1 R,G,B,A
 };
 
@@ -122,25 +123,24 @@ constexpr int kWaveSmemSamples = 2048;  // disc tables (16 B/sample) up to this 
 
 // Row-block interleave: local row ly of partition `part` -> frame row.
 // Partition `part` owns the blocks j = part, part + n_parts, ... of
-// block_rows rows; inside them, sub-partition `sub_part` owns the 8-row
-// blocks i = sub_part, sub_part + sub_parts, ... (a contiguous band split
-// among workers, rt_render_v1 on one device).
+// block_rows rows.  A contiguous band (n_parts = 1) starts at row0; inside
+// it, sub-partition `sub_part` owns the 8-row blocks i = sub_part,
+// sub_part + sub_parts, ... (a band split among workers, rt_render_v1 on
+// one device).
 __host__ __device__ __forceinline__ int map_row(int ly, const FrameArgs &a) {
-    if (a.sub_parts > 1) {  // one band: block_rows rows starting at part * block_rows
+    if (a.sub_parts > 1) {
         int jl = ly / 8, r = ly - jl * 8;
-        return a.part * a.block_rows + (jl * a.sub_parts + a.sub_part) * 8 + r;
+        return a.row0 + (jl * a.sub_parts + a.sub_part) * 8 + r;
     }
-    if (a.n_parts == 1) return ly;
+    if (a.n_parts == 1) return a.row0 + ly;
     int jl = ly / a.block_rows;
     int r = ly - jl * a.block_rows;
     return (jl * a.n_parts + a.part) * a.block_rows + r;
 }
 
-// Rows of sub-partition p of band k (rounded up to whole 8-row blocks; the
-// kernels skip rows outside the band and the frame).
-inline int rt_band_local_rows(int height, int k, int bands, int band_rows, int p, int parts) {
-    int y0 = k * band_rows;
-    int rows = height - y0 < band_rows ? height - y0 : band_rows;
+// Rows of sub-partition p of a band of `rows` rows (rounded up to whole
+// 8-row blocks; the kernels skip rows outside the band and the frame).
+inline int rt_band_local_rows(int rows, int p, int parts) {
     if (rows <= 0) return 0;
     if (parts == 1) return rows;
     int nb = (rows + 7) / 8;

@@ -105,6 +105,7 @@ struct Dev {
     // finish in order, so each copy starts as early as it can
     cudaStream_t band_st[kMaxBands] = {};
     cudaEvent_t fork_ev = nullptr;
+    cudaEvent_t tl_ev[2 * kMaxBands] = {};  // band_times: band k's kernels end, then its copy ends
     bool ph_valid = false;
     DBuf frame, rad, rays_in, rays_out, sky_raw, sky, counters, w_work;
     // pipelined frames (rt_render_async_v1): per slot a device frame, the
@@ -167,6 +168,10 @@ struct rt_ctx {
     bool cull = true;   // exact per-hit occluder culling in the wavefront shadow pass ($B200RT_CULL=0: off)
     bool count_work = false;  // tally the culled path's executed work (rt_work_counts)
     int bands = 0;            // single-device row bands for copy overlap (0: by frame size)
+    int band_first = 0;       // permille of the rows in band 0 (0: equal bands)
+    bool band_times = false;  // time each band's kernels and copy (rt_band_times_ms)
+    float band_ms[2 * kMaxBands] = {};
+    int band_count = 0;
     bool phases = false;      // record per-phase events in wavefront frames (rt_phase_ms)
     int rgba = 0;             // pixel byte order of the frames written (0 B,G,R,A / 1 R,G,B,A)
     bool conic = true;        // culled FP32 path: silhouette form of the soft-shadow sphere test
@@ -447,6 +452,7 @@ rt::FrameArgs frame_args(uint32_t *out, int64_t pitch, void *rad, int w, int h, 
     fa.sub_part = 0;
     fa.sub_parts = 1;
     fa.row_end = h;
+    fa.row0 = 0;
     fa.rgba = 0;
     return fa;
 }
@@ -661,6 +667,7 @@ int rt_ctx_create(rt_ctx **out, const int32_t *devices, int32_t n_devices) {
                   cudaEventCreate(&d.e0) == cudaSuccess && cudaEventCreate(&d.e1) == cudaSuccess;
         for (auto &ev : d.band_ev) ok = ok && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess;
         ok = ok && cudaEventCreateWithFlags(&d.fork_ev, cudaEventDisableTiming) == cudaSuccess;
+        for (auto &ev : d.tl_ev) ok = ok && cudaEventCreate(&ev) == cudaSuccess;
         for (int k = 0; ok && k < Dev::kSlots; k++)
             ok = cudaEventCreateWithFlags(&d.slot_comp[k], cudaEventDisableTiming) == cudaSuccess &&
                  cudaEventCreateWithFlags(&d.slot_done[k], cudaEventDisableTiming) ==
@@ -700,6 +707,8 @@ int rt_ctx_destroy(rt_ctx *ctx) {
         for (auto bs : d.band_st)
             if (bs) cudaStreamDestroy(bs);
         if (d.fork_ev) cudaEventDestroy(d.fork_ev);
+        for (auto ev : d.tl_ev)
+            if (ev) cudaEventDestroy(ev);
         for (int k = 0; k < Dev::kSlots; k++) {
             if (d.slot_comp[k]) cudaEventDestroy(d.slot_comp[k]);
             if (d.slot_done[k]) cudaEventDestroy(d.slot_done[k]);
@@ -795,30 +804,42 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
         int bands = ctx->bands > 0 ? ctx->bands : px_bytes < MB ? 1 : px_bytes < 6 * MB ? 2 : px_bytes < 24 * MB ? 4 : 6;
         if (ctx->phases) bands = 1;  // phase events describe one frame on one stream
         bands = std::max(1, std::min(bands, height / 8));
-        const int band_rows = (height + bands - 1) / bands;
+        // band boundaries in whole 8-row blocks: band 0 takes band_first
+        // permille of the rows (when set), the others share the rest equally
+        int y_at[kMaxBands + 1];
+        {
+            const int blocks = (height + 7) / 8;
+            int first = ctx->band_first > 0 && bands > 1 ? (int)((int64_t)blocks * ctx->band_first / 1000)
+                                                          : (blocks + bands - 1) / bands;
+            first = std::max(1, std::min(first, blocks - (bands - 1)));
+            y_at[0] = 0;
+            y_at[1] = first;
+            const int rest = blocks - first, others = bands - 1;
+            for (int k = 1; k < bands; k++) y_at[k + 1] = first + (int)((int64_t)rest * k / others);
+            for (int k = 0; k <= bands; k++) y_at[k] = std::min(height, y_at[k] * 8);
+        }
         RT_CK(cudaEventRecord(d.e0, d.st));
         if (bands > 1) RT_CK(cudaEventRecord(d.fork_ev, d.st));
         for (int k = 0; k < bands; k++) {
             cudaStream_t bs = bands > 1 ? d.band_st[k] : d.st;
             if (bands > 1) RT_CK(cudaStreamWaitEvent(bs, d.fork_ev, 0));
+            const int y0 = y_at[k], y1 = y_at[k + 1];
             for (int p = 0; p < n_parts; p++) {  // the caller's partitions inside the band, same device
                 rt::FrameArgs fa = frame_args((uint32_t *)d.frame.p, width, radiance ? d.rad.p : nullptr, width,
                                               height, cam_pos, yaw, pitch, vdist, shadow_samples, bounce_limit, 0, 1,
-                                              band_rows);
-                // band k of the frame, partition p of the band (rows interleaved in 8-row blocks)
-                fa.part = k;
-                fa.n_parts = bands;
-                fa.block_rows = band_rows;
+                                              height);
+                // rows [y0, y1) of the frame, partition p of the band (8-row blocks interleaved)
+                fa.row0 = y0;
                 fa.sub_part = p;
                 fa.sub_parts = n_parts;
-                fa.local_rows = rt::rt_band_local_rows(height, k, bands, band_rows, p, n_parts);
-                fa.row_end = std::min(height, (k + 1) * band_rows);
+                fa.local_rows = rt::rt_band_local_rows(y1 - y0, p, n_parts);
+                fa.row_end = y1;
                 if ((rc = launch_frame(ctx, d, fa, precision, bs, k))) return rc;
             }
             RT_CK(cudaEventRecord(d.band_ev[k], bs));
+            if (ctx->band_times) RT_CK(cudaEventRecord(d.tl_ev[k], bs));
             RT_CK(cudaStreamWaitEvent(d.copy_st, d.band_ev[k], 0));
             if (bands > 1) RT_CK(cudaStreamWaitEvent(d.st, d.band_ev[k], 0));  // the join
-            const int y0 = k * band_rows, y1 = std::min(height, y0 + band_rows);
             if (y1 > y0) {
                 size_t off = (size_t)y0 * width, cnt = (size_t)(y1 - y0) * width;
                 RT_CK(cudaMemcpyAsync(pixels + off, (uint32_t *)d.frame.p + off, sizeof(uint32_t) * cnt,
@@ -827,11 +848,17 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
                     RT_CK(cudaMemcpyAsync((char *)radiance + rad_elem * 3 * off, (char *)d.rad.p + rad_elem * 3 * off,
                                           rad_elem * 3 * cnt, cudaMemcpyDeviceToHost, d.copy_st));
             }
+            if (ctx->band_times) RT_CK(cudaEventRecord(d.tl_ev[kMaxBands + k], d.copy_st));
         }
         RT_CK(cudaEventRecord(d.e1, d.st));
         RT_CK(cudaStreamSynchronize(d.copy_st));
         RT_CK(cudaStreamSynchronize(d.st));
         RT_CK(cudaEventElapsedTime(&ctx->last_ms, d.e0, d.e1));
+        ctx->band_count = ctx->band_times ? bands : 0;
+        for (int k = 0; k < ctx->band_count; k++) {
+            RT_CK(cudaEventElapsedTime(&ctx->band_ms[k], d.e0, d.tl_ev[k]));
+            RT_CK(cudaEventElapsedTime(&ctx->band_ms[kMaxBands + k], d.e0, d.tl_ev[kMaxBands + k]));
+        }
         return RT_OK;
     }
     // several devices: partition p runs on device p % n_dev, each device
@@ -1005,6 +1032,8 @@ int rt_set_option(rt_ctx *ctx, const char *name, int32_t value) {
     else if (n == "zero_copy") ctx->zero_copy = value != 0;
     else if (n == "conic") ctx->conic = value != 0;
     else if (n == "cull_check") ctx->cull_check = value != 0;
+    else if (n == "band_first") ctx->band_first = std::max(0, std::min((int)value, 1000));
+    else if (n == "band_times") ctx->band_times = value != 0;
     else return fail(RT_ERR_INVALID, "unknown option " + n);
     return RT_OK;
 }
@@ -1040,6 +1069,17 @@ int rt_phase_ms(rt_ctx *ctx, float *out, int32_t n) {
     RT_CK(cudaEventSynchronize(d.ph[4]));
     for (int i = 0; i < 4; i++) RT_CK(cudaEventElapsedTime(&out[i], d.ph[i], d.ph[i + 1]));
     return RT_OK;
+}
+
+int rt_band_times_ms(rt_ctx *ctx, float *out, int32_t n) {
+    if (!ctx || (!out && n > 0)) return fail(RT_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    const int b = ctx->band_count;
+    for (int k = 0; k < b && 2 * k + 1 < n; k++) {
+        out[2 * k] = ctx->band_ms[k];
+        out[2 * k + 1] = ctx->band_ms[kMaxBands + k];
+    }
+    return b;
 }
 
 int rt_launch_count(rt_ctx *ctx, int64_t *count) {

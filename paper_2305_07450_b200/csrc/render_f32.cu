@@ -61,7 +61,7 @@ __device__ float3 trace(const Geo &geo, float3 origin, float3 dir, const SceneAr
     bool exhausted = false;
     float3 tail = f3(0.f, 0.f, 0.f);
     float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
-#pragma unroll 1
+#pragma unroll(BMAX <= 1 ? BMAX + 1 : 1)
     for (int k = 0; k <= BMAX; k++) {
         if (k > bounces) break;
         Hit h = geo.closest(origin, dir);
@@ -95,8 +95,9 @@ __device__ float3 trace(const Geo &geo, float3 origin, float3 dir, const SceneAr
         dir = dir - normal * (2.f * dot3(normal, dir));
     }
     float3 col = tail;
-#pragma unroll 1
-    for (int k = m - 1; k >= 0; k--) {
+#pragma unroll(BMAX <= 1 ? BMAX + 1 : 1)
+    for (int k = BMAX <= 1 ? BMAX : m - 1; k >= 0; k--) {
+        if (k >= m) continue;  // (BMAX <= 1: unrolled, the records stay in registers)
         const float4 mt = __ldg(reinterpret_cast<const float4 *>(sa.mat + 8 * ridx[k]));
         float br = mt.x, bg = mt.y, bb = mt.z;
         if (!(exhausted && k == m - 1)) {
@@ -161,6 +162,18 @@ __global__ void __launch_bounds__(kThreads, RT_F32_MIN_BLOCKS)
     render_patches<BMAX>(ps, fa, sa);
 }
 
+// One CTA per 16 x 8 tile, tile rows bottom first, no work counter: for
+// frames whose pixels cost about the same (hard shadows, few samples), where
+// one shared counter would serialise ~10^5 atomics per 4K frame.
+template <int BMAX, int MAXS>
+__global__ void __launch_bounds__(kThreads, RT_F32_MIN_BLOCKS)
+    render_f32_tile_kernel(const FrameArgs fa, const SceneArgs<float> sa, const ParamScene<MAXS> ps) {
+    int x, ly;
+    thread_pixel_bottom_first(x, ly);
+    shade_pixel<BMAX>(ps, fa, sa, x, ly);
+    if (fa.peer_out) __threadfence_system();
+}
+
 template <int BMAX, bool SMEM>
 __global__ void __launch_bounds__(kThreads) render_f32_kernel(const FrameArgs fa, const SceneArgs<float> sa) {
     extern __shared__ float4 smem_geo[];
@@ -203,7 +216,21 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 template <int BMAX>
-cudaError_t launch_render(const FrameArgs &fa, const SceneArgs<float> &sa, cudaStream_t st) {
+cudaError_t launch_render(const FrameArgs &fa, const SceneArgs<float> &sa, cudaStream_t st, bool tiles) {
+    if (tiles) {
+        const dim3 grid((fa.width + kTileW - 1) / kTileW, (fa.local_rows + kTileH - 1) / kTileH);
+        ParamScene<8> ps;
+        if (pack_params(sa, ps)) {
+            render_f32_tile_kernel<BMAX, 8><<<grid, kThreads, 0, st>>>(fa, sa, ps);
+            return cudaGetLastError();
+        }
+        thread_local ParamScene<kParamSpheres> pl;
+        if (pack_params(sa, pl)) {
+            render_f32_tile_kernel<BMAX, kParamSpheres><<<grid, kThreads, 0, st>>>(fa, sa, pl);
+            return cudaGetLastError();
+        }
+        return cudaErrorNotSupported;  // larger scenes take the persistent kernels
+    }
     {
         ParamScene<8> ps;
         if (pack_params(sa, ps)) {
@@ -251,8 +278,10 @@ cudaError_t launch_trace(const double *o, const double *d, int64_t n, float *out
 
 }  // namespace
 
-cudaError_t rt_launch_render_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, cudaStream_t st) {
-    return launch_render<rt::kMaxBounce>(fa, sa, st);
+cudaError_t rt_launch_render_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, cudaStream_t st,
+                                 bool tiles) {
+    if (fa.bounces <= 1) return launch_render<1>(fa, sa, st, tiles);
+    return launch_render<rt::kMaxBounce>(fa, sa, st, tiles);
 }
 
 cudaError_t rt_launch_trace_f32(const double *o, const double *d, int64_t n, float *out,

@@ -180,7 +180,10 @@ __device__ __forceinline__ uint32_t pack_color(R r, R g, R b, int rgba) {
 
 // Launchers (one translation unit per precision; the FP64 one is compiled
 // with -fmad=false so no a*b+c is contracted, as numba compiles the reference).
-cudaError_t rt_launch_render_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, cudaStream_t st);
+// tiles: one CTA per 16 x 8 tile (scenes that fit the launch parameters);
+// otherwise persistent warps on a work counter (fa.work_counter, zeroed)
+cudaError_t rt_launch_render_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, cudaStream_t st,
+                                 bool tiles);
 cudaError_t rt_launch_render_f64(const rt::FrameArgs &fa, const rt::SceneArgs<double> &sa, cudaStream_t st);
 cudaError_t rt_launch_wave_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, const rt::WaveArgs &wa,
                                cudaStream_t st, int *n_kernels, cudaEvent_t *phase_events /* 5 or null */);

@@ -177,6 +177,7 @@ struct rt_ctx {
     bool conic = true;        // culled FP32 path: silhouette form of the soft-shadow sphere test
     bool cull_check = false;  // culled FP32 path: classify every body as undecided (an exactness check)
     bool zero_copy = false;   // kernels store straight into a registered (mapped) host framebuffer
+    int mega_tiles = -1;      // FP32 megakernel: 1 one CTA per tile, 0 persistent warps, -1 by sample count
     std::mutex mu;
     HostScene scene;
     float last_ms = 0.f;
@@ -575,12 +576,18 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         d.ph_valid = ctx->phases;
         ctx->launches += nk - 1;  // the common increment below counts one
     } else {
-        // the FP32 megakernel's persistent warps take patches from a counter:
-        // a fresh ring slot per launch (concurrent bands never share one)
-        if ((rc = d.counters.ensure(sizeof(unsigned) * rt::kCounterRing))) return rc;
-        fa.work_counter = (unsigned *)d.counters.p + (d.counter_slot++ % rt::kCounterRing);
-        RT_CK(cudaMemsetAsync(fa.work_counter, 0, sizeof(unsigned), st));
-        e = rt_launch_render_f32(fa, scene_args(d, d.s32, ctx->scene), st);
+        // few samples: one CTA per tile; many (the megakernel fallback of soft
+        // shadows): persistent warps taking patches from a counter, a fresh
+        // ring slot per launch (concurrent bands never share one)
+        const int ns = count_spheres(ctx->scene), np = ctx->scene.n - ns;
+        const bool tiles = (ctx->mega_tiles > 0 || (ctx->mega_tiles < 0 && fa.samples < rt::kWaveMinSamples)) &&
+                           ns <= rt::kParamSpheres && np <= 8;
+        if (!tiles) {
+            if ((rc = d.counters.ensure(sizeof(unsigned) * rt::kCounterRing))) return rc;
+            fa.work_counter = (unsigned *)d.counters.p + (d.counter_slot++ % rt::kCounterRing);
+            RT_CK(cudaMemsetAsync(fa.work_counter, 0, sizeof(unsigned), st));
+        }
+        e = rt_launch_render_f32(fa, scene_args(d, d.s32, ctx->scene), st, tiles);
     }
     if (e != cudaSuccess) return fail(RT_ERR_CUDA, std::string("render kernel launch: ") + cudaGetErrorString(e));
     ctx->launches++;
@@ -1034,6 +1041,7 @@ int rt_set_option(rt_ctx *ctx, const char *name, int32_t value) {
     else if (n == "cull_check") ctx->cull_check = value != 0;
     else if (n == "band_first") ctx->band_first = std::max(0, std::min((int)value, 1000));
     else if (n == "band_times") ctx->band_times = value != 0;
+    else if (n == "mega_tiles") ctx->mega_tiles = value < 0 ? -1 : value != 0;
     else return fail(RT_ERR_INVALID, "unknown option " + n);
     return RT_OK;
 }

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--precision", default="fp32")
     ap.add_argument("--mode", default=None, help="cull | ray | wave | mega")
     ap.add_argument("--bands", type=int, default=1, help="row bands of rt_render_v1 (0 = by frame size)")
+    ap.add_argument("--opt", action="append", default=[], help="extra rt_set_option name=value (repeatable)")
     a = ap.parse_args()
     tag = os.path.basename(_native.LIB_PATH)
     _native.set_options(bands=a.bands, phases=1)
@@ -29,6 +30,10 @@ def main():
         _native.set_options(**{"cull": dict(wave=1, cull=1, conic=1), "ray": dict(wave=1, cull=1, conic=0),
                                "wave": dict(wave=1, cull=0), "mega": dict(wave=0, cull=0)}[a.mode])
         tag += f"[{a.mode}]"
+    for o in a.opt:
+        name, value = o.split("=")
+        _native.set_options(**{name: int(value)})
+        tag += f"[{o}]"
     for key in a.configs:
         cfg = rt.CONFIGS[key]
         scene, cam, params = cfg.scene(), cfg.camera(), cfg.params()

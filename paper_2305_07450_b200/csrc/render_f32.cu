@@ -34,7 +34,7 @@ template <class Geo>
 __device__ float shadow_coeff(const Geo &geo, float3 surface, float3 normal, const SceneArgs<float> &sa, int n) {
     const float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
     const ShadowFrame f = shadow_frame(surface, normal, lp, n > 1);
-    const auto lc = geo.localize(f.origin);
+    const auto lc = geo.localize(f.origin, scene_grid_mask(sa, f.origin));
     const float4 *__restrict__ tab = reinterpret_cast<const float4 *>(sa.table);
     int unblocked = 0;
 #pragma unroll 2
@@ -165,8 +165,11 @@ __global__ void __launch_bounds__(kThreads, RT_F32_MIN_BLOCKS)
 // One CTA per 16 x 8 tile, tile rows bottom first, no work counter: for
 // frames whose pixels cost about the same (hard shadows, few samples), where
 // one shared counter would serialise ~10^5 atomics per 4K frame.
+#ifndef RT_F32_TILE_MIN_BLOCKS
+#define RT_F32_TILE_MIN_BLOCKS 7  // 7 CTAs (<= 72 registers): 15-18% faster at s1 b1 than the uncapped 103
+#endif
 template <int BMAX, int MAXS>
-__global__ void __launch_bounds__(kThreads, RT_F32_MIN_BLOCKS)
+__global__ void __launch_bounds__(kThreads, RT_F32_TILE_MIN_BLOCKS)
     render_f32_tile_kernel(const FrameArgs fa, const SceneArgs<float> sa, const ParamScene<MAXS> ps) {
     int x, ly;
     thread_pixel_bottom_first(x, ly);

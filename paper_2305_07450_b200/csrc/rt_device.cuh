@@ -59,6 +59,12 @@ struct SceneArgs {
     R lc[3];
     R ambient;
     const double *host_geo;  // host copy of geo (float64), for launch-parameter scene packing
+    // FP32 scenes of up to 8 spheres: the shadow grid (render_fused_f32.cu,
+    // shadow_grid_build) — per cell the spheres that can block a shadow ray
+    // from it; null: none
+    const unsigned *grid;
+    float grid_lo[3], grid_inv[3];
+    int grid_dim[3];
 };
 
 // Wavefront queues (render_wave_f32.cu); slot = bounce * n_pix + local pixel.

@@ -88,6 +88,19 @@ __device__ __forceinline__ float blinn_pow(float d, float e) {
 
 constexpr float kGraze = 1e-7f;  // geometry.py:24
 
+// The shadow grid's mask for a shadow origin o (SceneArgs::grid): ~0 when
+// there is no grid or o lies outside it.
+__device__ __forceinline__ unsigned scene_grid_mask(const SceneArgs<float> &sa, float3 o) {
+    if (!sa.grid) return ~0u;
+    const int ix = __float2int_rd((o.x - sa.grid_lo[0]) * sa.grid_inv[0]);
+    const int iy = __float2int_rd((o.y - sa.grid_lo[1]) * sa.grid_inv[1]);
+    const int iz = __float2int_rd((o.z - sa.grid_lo[2]) * sa.grid_inv[2]);
+    if ((unsigned)ix >= (unsigned)sa.grid_dim[0] || (unsigned)iy >= (unsigned)sa.grid_dim[1] ||
+        (unsigned)iz >= (unsigned)sa.grid_dim[2])
+        return ~0u;
+    return __ldg(sa.grid + ((size_t)iz * sa.grid_dim[1] + iy) * sa.grid_dim[0] + ix);
+}
+
 // L = centre - origin; r2g = r^2 + GRAZE, or -inf when the origin is inside
 // the sphere (t < 0 for every direction: it never blocks).
 __device__ __forceinline__ float sphere_margin_L(float3 L, float3 d, float r2g, float limit) {
@@ -223,15 +236,20 @@ struct ParamScene {
     // Per-hit constants of the any-hit loop: the shadow origin is shared by
     // all samples of a hit, so L = c - o, the inside/outside decision and
     // h - o.y are formed once per hit.
+    // wm (unclustered scenes): the spheres that can block a ray from o, from
+    // the shadow grid's cell of o (all when there is none); the others are
+    // skipped, which leaves the any-hit answer unchanged.
     struct Local {
         float3 o;
         float4 L[kClustered ? 1 : MAXS];  // xyz = centre - origin, w = r2g
         float num[kMaxPlanes];
+        unsigned wm;
     };
 
-    __device__ __forceinline__ Local localize(float3 o) const {
+    __device__ __forceinline__ Local localize(float3 o, unsigned wm = ~0u) const {
         Local lc;
         lc.o = o;
+        lc.wm = wm;
         if constexpr (!kClustered) {
 #pragma unroll
             for (int b = 0; b < MAXS; b++) {
@@ -255,6 +273,7 @@ struct ParamScene {
 #pragma unroll
             for (int b = 0; b < MAXS; b++) {
                 if (b >= ns) break;
+                if (!((lc.wm >> b) & 1u)) continue;
                 float4 L = lc.L[b];
                 m = fmaxf(m, sphere_margin_L(f3(L.x, L.y, L.z), d, L.w, limit));
             }
@@ -291,7 +310,7 @@ struct MemScene {
     struct Local {
         float3 o;
     };
-    __device__ __forceinline__ Local localize(float3 o) const { return Local{o}; }
+    __device__ __forceinline__ Local localize(float3 o, unsigned = ~0u) const { return Local{o}; }
 
     __device__ __forceinline__ bool occluded(const Local &lc, float3 d, float limit) const {
         for (int b = 0; b < n; b++) {

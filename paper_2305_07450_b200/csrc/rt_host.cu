@@ -374,6 +374,11 @@ rt::SceneArgs<R> scene_args(const Dev &d, const DevScene<R> &ds, const HostScene
     a.light_radius = (R)s.light_radius;
     a.ambient = (R)s.ambient;
     a.host_geo = s.geo.data();
+    a.grid = nullptr;
+    for (int c = 0; c < 3; c++) {
+        a.grid_lo[c] = a.grid_inv[c] = 0.f;
+        a.grid_dim[c] = 0;
+    }
     return a;
 }
 
@@ -391,7 +396,7 @@ int prepare(rt_ctx *ctx, Dev &d, int precision, int samples) {
     if ((rc = upload_prec(d, d.s32, ctx->scene, samples))) return rc;
     // the culled path's shadow grid, rebuilt on d.st when the scene or the
     // light changed (before any row band forks off d.st)
-    if (samples >= rt::kWaveMinSamples && ctx->wave && ctx->cull && d.grid_version != ctx->scene.version) {
+    if (ctx->cull && d.grid_version != ctx->scene.version) {
         if ((rc = d.grid.ensure(sizeof(unsigned) * rt::kGridCells))) return rc;
         d.grid_wa = {};
         cudaError_t e = rt_build_shadow_grid_f32(scene_args(d, d.s32, ctx->scene), (unsigned *)d.grid.p,
@@ -587,7 +592,18 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
             fa.work_counter = (unsigned *)d.counters.p + (d.counter_slot++ % rt::kCounterRing);
             RT_CK(cudaMemsetAsync(fa.work_counter, 0, sizeof(unsigned), st));
         }
-        e = rt_launch_render_f32(fa, scene_args(d, d.s32, ctx->scene), st, tiles);
+        rt::SceneArgs<float> sa = scene_args(d, d.s32, ctx->scene);
+        // the shadow grid filters the any-hit tests of scenes up to 8 spheres
+        // (it is built over their spheres; larger scenes' bits name clusters)
+        if (ctx->cull && ns <= 8 && d.grid_version == ctx->scene.version && d.grid_wa.grid) {
+            sa.grid = d.grid_wa.grid;
+            for (int c = 0; c < 3; c++) {
+                sa.grid_lo[c] = d.grid_wa.grid_lo[c];
+                sa.grid_inv[c] = d.grid_wa.grid_inv[c];
+                sa.grid_dim[c] = d.grid_wa.grid_dim[c];
+            }
+        }
+        e = rt_launch_render_f32(fa, sa, st, tiles);
     }
     if (e != cudaSuccess) return fail(RT_ERR_CUDA, std::string("render kernel launch: ") + cudaGetErrorString(e));
     ctx->launches++;

@@ -21,7 +21,8 @@ pytestmark = pytest.mark.gpu
 
 MODES = {"cull": dict(wave=1, cull=1, conic=1, cull_check=0), "ray": dict(wave=1, cull=1, conic=0, cull_check=0),
          "check": dict(wave=1, cull=1, conic=0, cull_check=1),
-         "wave": dict(wave=1, cull=0, conic=1, cull_check=0), "mega": dict(wave=0, cull=0, conic=1, cull_check=0)}
+         "wave": dict(wave=1, cull=0, conic=1, cull_check=0), "mega": dict(wave=0, cull=0, conic=1, cull_check=0),
+         "mega_grid": dict(wave=0, cull=1, conic=1, cull_check=0)}
 
 
 def random_scene(rng, n_spheres, with_plane=True, light_radius=None, sky=False):
@@ -87,6 +88,41 @@ def test_fp32_paths_bit_identical(seed, n, samples, bounces, plane, lr):
                                    radiance=True)
     parity.assert_byte_gate(px, want, f"silhouette seed {seed}")
     parity.assert_radiance_gate(rad, want_rad, f"silhouette seed {seed}")
+
+
+MEGA_CASES = [
+    # (seed, spheres, samples, bounces, plane, light radius)
+    (11, 5, 1, 1, True, None),
+    (12, 8, 1, 0, True, 2.0),
+    (13, 3, 4, 3, False, 0.3),
+    (14, 6, 7, 2, True, 1.2),
+    (15, 5, 40, 3, True, None),   # soft shadows on the megakernel (option wave off)
+    (16, 12, 1, 1, True, None),   # > 8 spheres: no grid
+]
+
+
+@pytest.mark.parametrize("seed,n,samples,bounces,plane,lr", MEGA_CASES)
+def test_fp32_megakernel_shadow_grid_exact(seed, n, samples, bounces, plane, lr):
+    """The FP32 megakernel skips the spheres the shadow grid rules out for a
+    shadow origin's cell (option cull): frames equal the unfiltered ones bit
+    for bit, with tiles and with persistent warps."""
+    rng = np.random.default_rng(seed)
+    scene = random_scene(rng, n, plane, lr, sky=seed % 2 == 0)
+    cam = rt.Camera(position=(rng.uniform(-1, 1), rng.uniform(0.5, 2.5), -5.0), yaw=rng.uniform(-0.3, 0.3),
+                    pitch=rng.uniform(-0.3, 0.1), fov=rng.uniform(40, 90))
+    params = rt.RenderParams(samples, bounces, 160, 90)
+    frames = []
+    for tiles in (-1, 0, 1):
+        _native.set_options(mega_tiles=tiles)
+        try:
+            frames += [render(scene, cam, params, "fp32", "mega_grid"), render(scene, cam, params, "fp32", "mega")]
+        finally:
+            _native.set_options(mega_tiles=-1)
+    for f in frames[1:]:
+        np.testing.assert_array_equal(frames[0], f)
+    ps = rt.pack_scene(scene)
+    want = oracle.render(vars(ps), cam.position, cam.yaw, cam.pitch, cam.fov, 160, 90, samples, bounces)
+    parity.assert_byte_gate(frames[0], want, f"megakernel seed {seed}")
 
 
 @pytest.mark.parametrize("seed,n,samples,bounces,plane,lr", CASES[:6])

@@ -54,7 +54,7 @@ __device__ float shadow_coeff(const Geo &geo, float3 surface, float3 normal, con
 // live in L1-resident local memory.
 template <int BMAX, class Geo>
 __device__ float3 trace(const Geo &geo, float3 origin, float3 dir, const SceneArgs<float> &sa, int samples,
-                        int bounces) {
+                        int bounces, unsigned smask = ~0u) {
     int ridx[BMAX + 1];
     float rlum[BMAX + 1], rspec[BMAX + 1];
     int m = 0;
@@ -64,7 +64,7 @@ __device__ float3 trace(const Geo &geo, float3 origin, float3 dir, const SceneAr
 #pragma unroll(BMAX <= 1 ? BMAX + 1 : 1)
     for (int k = 0; k <= BMAX; k++) {
         if (k > bounces) break;
-        Hit h = geo.closest(origin, dir);
+        Hit h = geo.closest(origin, dir, k == 0 ? smask : ~0u);
         if (h.idx < 0) {
             if (sa.has_sky) tail = sky_sample(dir, sa.sky, sa.sky_w, sa.sky_h);
             break;
@@ -121,7 +121,7 @@ __device__ __forceinline__ void shade_pixel(const Geo &geo, const FrameArgs &fa,
     if (y >= fa.row_end) return;
     float3 dir = primary_direction(x, y, fa);
     float3 c = trace<BMAX>(geo, f3((float)fa.cam[0], (float)fa.cam[1], (float)fa.cam[2]), dir, sa, fa.samples,
-                           fa.bounces);
+                           fa.bounces, primary_sphere_mask(fa, x, y));
     fa.out[(int64_t)y * fa.out_pitch + x] = pack_color(c.x, c.y, c.z, fa.rgba);
     if (fa.radiance) {
         float *r = (float *)fa.radiance + 3 * ((int64_t)y * fa.width + x);

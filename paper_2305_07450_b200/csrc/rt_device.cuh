@@ -44,7 +44,25 @@ struct FrameArgs {
     int row_end;                 // rows >= row_end are skipped (end of the band / frame)
     int row0;                    // first frame row of a contiguous band (sub_parts > 1 or n_parts == 1)
     int rgba;                    // pixel byte order: 0 B,G,R,A (0xAARRGGBB), 1 R,G,B,A
+    // FP32 scenes of up to 8 spheres: per sphere (in ascending body order) a
+    // conservative pixel box {x0, y0, x1, y1} outside which no primary ray
+    // can hit it (nbox = 0: none, every primary ray tests every sphere)
+    int nbox;
+    int box[8][4];
 };
+
+// The spheres whose primary-ray box holds pixel (x, y) (all when no boxes).
+__host__ __device__ __forceinline__ unsigned primary_sphere_mask(const FrameArgs &fa, int x, int y) {
+    if (!fa.nbox) return ~0u;
+    unsigned m = 0;
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+        if (b >= fa.nbox) break;
+        const bool in = x >= fa.box[b][0] && x <= fa.box[b][2] && y >= fa.box[b][1] && y <= fa.box[b][3];
+        m |= (in ? 1u : 0u) << b;
+    }
+    return m;
+}
 
 template <typename R>
 struct SceneArgs {

@@ -173,13 +173,16 @@ struct ParamScene {
     int cl_begin[kNC + 1];   // members of cluster c: slots [cl_begin[c], cl_begin[c+1])
     int ns, np, nc;
 
-    __device__ __forceinline__ Hit closest(float3 o, float3 d) const {
+    // smask (unclustered scenes): the spheres worth testing — a primary ray's
+    // primary_sphere_mask; the others cannot be hit
+    __device__ __forceinline__ Hit closest(float3 o, float3 d, unsigned smask = ~0u) const {
         Hit h{-1, INFINITY, make_float4(0.f, 0.f, 0.f, -1.f)};
         int slot = -1;
         if constexpr (!kClustered) {
 #pragma unroll
             for (int b = 0; b < MAXS; b++) {
                 if (b >= ns) break;
+                if (!((smask >> b) & 1u)) continue;
                 float t = sphere_t(o, d, sph[b]);
                 if (t < h.t) {  // spheres ascend in original index: strict '<' keeps the lowest
                     h.t = t;
@@ -293,7 +296,7 @@ struct MemScene {
     const float4 *__restrict__ geo;
     int n;
 
-    __device__ __forceinline__ Hit closest(float3 o, float3 d) const {
+    __device__ __forceinline__ Hit closest(float3 o, float3 d, unsigned = ~0u) const {
         Hit h{-1, INFINITY, make_float4(0.f, 0.f, 0.f, -1.f)};
         for (int b = 0; b < n; b++) {
             float4 g = geo[b];

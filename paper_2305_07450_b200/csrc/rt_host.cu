@@ -177,6 +177,7 @@ struct rt_ctx {
     bool conic = true;        // culled FP32 path: silhouette form of the soft-shadow sphere test
     bool cull_check = false;  // culled FP32 path: classify every body as undecided (an exactness check)
     bool zero_copy = false;   // kernels store straight into a registered (mapped) host framebuffer
+    bool boxes = true;        // FP32 scenes of <= 8 spheres: primary-ray sphere boxes (with cull)
     int mega_tiles = -1;      // FP32 megakernel: 1 one CTA per tile, 0 persistent warps, -1 by sample count
     std::mutex mu;
     HostScene scene;
@@ -460,6 +461,7 @@ rt::FrameArgs frame_args(uint32_t *out, int64_t pitch, void *rad, int w, int h, 
     fa.row_end = h;
     fa.row0 = 0;
     fa.rgba = 0;
+    fa.nbox = 0;
     return fa;
 }
 
@@ -475,10 +477,71 @@ int ensure_counts(WaveBufs &b, cudaStream_t st) {
     return RT_OK;
 }
 
+// Per sphere of a scene of up to 8, the pixels whose primary ray can hit it
+// (FrameArgs::box): the rays within angle asin(r'/D) of the direction to the
+// centre (D away, r' = r inflated well past the FP32 test's rounding and the
+// graze tolerance), bounded in camera space by the planes through the eye
+// holding an image axis (A s^2 - 2 a.z a s + a^2 - sin^2 = 0 for the slope s
+// of each bounding plane), mapped to pixels and padded by two.  A sphere
+// behind the eye gets an empty box; one the eye is in or near, or whose cone
+// reaches the image plane's horizon, the whole frame.  Exact: a ray outside
+// the box misses the sphere in the kernels' own test.
+void primary_boxes(rt::FrameArgs &fa, const HostScene &s) {
+    fa.nbox = 0;
+    int nb = 0;
+    for (int b = 0; b < s.n; b++) nb += s.geo[4 * b + 3] >= 0.0 ? 1 : 0;
+    if (nb == 0 || nb > 8) return;
+    const double W = fa.width, H = fa.height;
+    int k = 0;
+    for (int b = 0; b < s.n; b++) {
+        const double *g = &s.geo[4 * b];
+        if (g[3] < 0.0) continue;
+        int *bx = fa.box[k++];
+        bx[0] = bx[1] = -1;  // the whole frame
+        bx[2] = fa.width;
+        bx[3] = fa.height;
+        const double r = std::sqrt(g[3]);
+        const double wx = g[0] - fa.cam[0], wy = g[1] - fa.cam[1], wz = g[2] - fa.cam[2];
+        // world -> camera: undo the yaw, then the pitch (camera.py:70-77 inverted)
+        const double cx = wx * fa.ca - wz * fa.sa, z2 = wx * fa.sa + wz * fa.ca;
+        const double cy = wy * fa.cb + z2 * fa.sb, cz = -wy * fa.sb + z2 * fa.cb;
+        const double D = std::sqrt(cx * cx + cy * cy + cz * cz);
+        const double re = r * (1.0 + 1e-3) + 1e-3 + 1e-5 * D;
+        if (!(D > 1.001 * re)) continue;
+        const double sn = re / D, ax = cx / D, ay = cy / D, az = cz / D;
+        if (az < -sn) {  // wholly behind the eye: primary rays point forward
+            bx[0] = bx[1] = 1;
+            bx[2] = bx[3] = 0;
+            continue;
+        }
+        if (!(az - sn > 1e-3)) continue;
+        const double A = az * az - sn * sn;
+        auto slopes = [&](double a, double &lo, double &hi) {
+            const double B = a * az, sq = std::sqrt(std::max(B * B - A * (a * a - sn * sn), 0.0));
+            lo = (B - sq) / A;
+            hi = (B + sq) / A;
+        };
+        double s0, s1, t0, t1;
+        slopes(ax, s0, s1);
+        slopes(ay, t0, t1);
+        // u = vdist * s = x * ndc0 + ndc1, v = vdist * t = y * ndc2 + ndc3 (camera.py:46-54)
+        const double xa = (fa.vdist * s0 - fa.ndc[1]) / fa.ndc[0], xb = (fa.vdist * s1 - fa.ndc[1]) / fa.ndc[0];
+        const double ya = (fa.vdist * t0 - fa.ndc[3]) / fa.ndc[2], yb = (fa.vdist * t1 - fa.ndc[3]) / fa.ndc[2];
+        if (!std::isfinite(xa) || !std::isfinite(xb) || !std::isfinite(ya) || !std::isfinite(yb)) continue;
+        auto clampd = [](double v, double lo, double hi) { return std::min(std::max(v, lo), hi); };
+        bx[0] = (int)clampd(std::floor(std::min(xa, xb)) - 2.0, -1.0, W);
+        bx[2] = (int)clampd(std::ceil(std::max(xa, xb)) + 2.0, -1.0, W);
+        bx[1] = (int)clampd(std::floor(std::min(ya, yb)) - 2.0, -1.0, H);
+        bx[3] = (int)clampd(std::ceil(std::max(ya, yb)) + 2.0, -1.0, H);
+    }
+    fa.nbox = nb;
+}
+
 int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStream_t st, int buf = 0) {
     WaveBufs &b = d.wb[buf];
     cudaError_t e;
     fa.rgba = ctx->rgba;
+    if (precision == RT_PREC_FP32 && ctx->cull && ctx->boxes && !ctx->cull_check) primary_boxes(fa, ctx->scene);
     if (fa.local_rows == 0) return RT_OK;
     int rc = RT_OK;
     d.ph_valid = false;
@@ -1057,6 +1120,7 @@ int rt_set_option(rt_ctx *ctx, const char *name, int32_t value) {
     else if (n == "cull_check") ctx->cull_check = value != 0;
     else if (n == "band_first") ctx->band_first = std::max(0, std::min((int)value, 1000));
     else if (n == "band_times") ctx->band_times = value != 0;
+    else if (n == "boxes") ctx->boxes = value != 0;
     else if (n == "mega_tiles") ctx->mega_tiles = value < 0 ? -1 : value != 0;
     else return fail(RT_ERR_INVALID, "unknown option " + n);
     return RT_OK;

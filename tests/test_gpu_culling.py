@@ -125,6 +125,32 @@ def test_fp32_megakernel_shadow_grid_exact(seed, n, samples, bounces, plane, lr)
     parity.assert_byte_gate(frames[0], want, f"megakernel seed {seed}")
 
 
+@pytest.mark.parametrize("fov,samples,bounces", [(150.0, 1, 1), (100.0, 200, 2), (60.0, 1, 0), (170.0, 16, 3)])
+def test_fp32_primary_boxes_around_the_eye(fov, samples, bounces):
+    """Primary-ray sphere boxes (option cull) with spheres behind, beside,
+    around and just in front of the eye and wide fields of view: frames equal
+    the unboxed ones bit for bit (megakernel: cull off; wavefront: cull_check)."""
+    eye = (0.3, 1.2, -2.0)
+    bodies = [
+        rt.Body.sphere((0.3, 1.2, -5.0), 0.8, (0.8, 0.2, 0.2), 40.0),     # behind
+        rt.Body.sphere((0.35, 1.25, -2.05), 0.5, (0.2, 0.8, 0.2), 0.0),   # around the eye
+        rt.Body.sphere((2.5, 1.2, -1.9), 0.7, (0.2, 0.2, 0.8), 90.0),     # beside (horizon of the image plane)
+        rt.Body.sphere((0.3, 1.1, -1.2), 0.3, (0.9, 0.9, 0.2), 10.0),     # just in front
+        rt.Body.sphere((-1.0, 0.8, 3.0), 1.0, (0.5, 0.5, 0.5), 120.0),
+        rt.Body.plane(0.0, (0.4, 0.4, 0.4), 16.0),
+    ]
+    scene = rt.Scene(bodies=bodies, light=rt.Light((-3.0, 6.0, -1.0), 0.5))
+    params = rt.RenderParams(samples, bounces, 160, 90)
+    for yaw, pitch in [(0.0, 0.0), (3.0, 0.2), (1.57, -0.6), (-2.2, 0.9)]:
+        cam = rt.Camera(position=eye, yaw=yaw, pitch=pitch, fov=fov)
+        if samples < 8:
+            np.testing.assert_array_equal(render(scene, cam, params, "fp32", "mega_grid"),
+                                          render(scene, cam, params, "fp32", "mega"))
+        else:
+            np.testing.assert_array_equal(render(scene, cam, params, "fp32", "ray"),
+                                          render(scene, cam, params, "fp32", "check"))
+
+
 @pytest.mark.parametrize("seed,n,samples,bounces,plane,lr", CASES[:6])
 def test_fp64_culled_equals_literal_and_oracle(seed, n, samples, bounces, plane, lr):
     rng = np.random.default_rng(100 + seed)

@@ -749,8 +749,13 @@ __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArg
     }
 }
 
+// 5 resident CTAs (95 registers, as unbounded); 6-7 measured no faster
+// (spills), and an explicit 1 raises the register count and costs ~15%
+#ifndef RT_SAMPLE_MIN_BLOCKS
+#define RT_SAMPLE_MIN_BLOCKS 5
+#endif
 template <int MAXS, bool SMEM_TAB>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_SAMPLE_MIN_BLOCKS : 1)
     fused_sample(const FrameArgs fa, const SceneArgs<float> sa, const WaveArgs wa, const ParamScene<MAXS> ps) {
     constexpr int kWords = (MAXS + 31) / 32;
     const int n = fa.samples;

@@ -164,9 +164,9 @@ int rt_host_unregister(rt_ctx *ctx, void *ptr);
  *                 6 MB, 4 below 24 MB, else 6;
  *   "band_first"  permille of the frame's rows in band 0 (0, default: equal
  *                 bands; the others always share the rest equally);
- *   "boxes"       (default on, with "cull") FP32 scenes of up to 8 spheres:
- *                 primary rays test only the spheres whose conservative
- *                 pixel box holds them (exact);
+ *   "boxes"       (default on, with "cull") FP32 megakernel frames (under 8
+ *                 samples) of up to 8 spheres: primary rays test only the
+ *                 spheres whose conservative pixel box holds them (exact);
  *   "mega_tiles"  FP32 megakernel (frames under 8 shadow samples, or option
  *                 "wave" off): 1 one CTA per 16x8 tile, 0 persistent warps
  *                 taking 8x4 patches from a counter, -1 (default) tiles below

@@ -36,12 +36,18 @@ __device__ float shadow_coeff(const Geo &geo, float3 surface, float3 normal, con
     const ShadowFrame f = shadow_frame(surface, normal, lp, n > 1);
     const auto lc = geo.localize(f.origin, scene_grid_mask(sa, f.origin));
     const float4 *__restrict__ tab = reinterpret_cast<const float4 *>(sa.table);
+    if (n == 1) {  // hard shadows: one ray, the ruled-out spheres skipped
+        float3 dir;
+        float limit;
+        shadow_ray(f, make_float4(0.f, 0.f, 0.f, 0.f), dir, limit);
+        return geo.template occluded<true>(lc, dir, limit) ? 0.f : 1.f;
+    }
     int unblocked = 0;
 #pragma unroll 2
     for (int i = 0; i < n; i++) {
         float3 dir;
         float limit;
-        shadow_ray(f, n > 1 ? __ldg(tab + i) : make_float4(0.f, 0.f, 0.f, 0.f), dir, limit);
+        shadow_ray(f, __ldg(tab + i), dir, limit);
         unblocked += geo.occluded(lc, dir, limit) ? 0 : 1;
     }
     return (float)unblocked / (float)n;
@@ -64,7 +70,7 @@ __device__ float3 trace(const Geo &geo, float3 origin, float3 dir, const SceneAr
 #pragma unroll(BMAX <= 1 ? BMAX + 1 : 1)
     for (int k = 0; k <= BMAX; k++) {
         if (k > bounces) break;
-        Hit h = geo.closest(origin, dir, k == 0 ? smask : ~0u);
+        Hit h = k == 0 ? geo.template closest<true>(origin, dir, smask) : geo.closest(origin, dir);
         if (h.idx < 0) {
             if (sa.has_sky) tail = sky_sample(dir, sa.sky, sa.sky_w, sa.sky_h);
             break;

@@ -254,7 +254,9 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? 8 : 6)
         if (!live) break;
         Hit h{-1, INFINITY, make_float4(0.f, 0.f, 0.f, -1.f)};
         if constexpr (!kBundle) {
-            if (alive) h = ps.closest(origin, dir, k == 0 ? primary_sphere_mask(fa, x, y) : ~0u);
+            // (the primary-ray sphere boxes cost this kernel ~4%: its unrolled,
+            // branch-free sphere loop keeps more rays in flight)
+            if (alive) h = ps.closest(origin, dir);
         } else {
             // warp bundle of the live rays -> uniform candidate list
             float3 sd = f3(warp_sum(alive ? dir.x : 0.f), warp_sum(alive ? dir.y : 0.f),

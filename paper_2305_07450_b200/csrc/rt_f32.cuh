@@ -173,8 +173,9 @@ struct ParamScene {
     int cl_begin[kNC + 1];   // members of cluster c: slots [cl_begin[c], cl_begin[c+1])
     int ns, np, nc;
 
-    // smask (unclustered scenes): the spheres worth testing — a primary ray's
-    // primary_sphere_mask; the others cannot be hit
+    // SPARSE (unclustered scenes): only the spheres in smask are tested — a
+    // primary ray's primary_sphere_mask; the others cannot be hit
+    template <bool SPARSE = false>
     __device__ __forceinline__ Hit closest(float3 o, float3 d, unsigned smask = ~0u) const {
         Hit h{-1, INFINITY, make_float4(0.f, 0.f, 0.f, -1.f)};
         int slot = -1;
@@ -182,7 +183,7 @@ struct ParamScene {
 #pragma unroll
             for (int b = 0; b < MAXS; b++) {
                 if (b >= ns) break;
-                if (!((smask >> b) & 1u)) continue;
+                if (SPARSE && !((smask >> b) & 1u)) continue;
                 float t = sphere_t(o, d, sph[b]);
                 if (t < h.t) {  // spheres ascend in original index: strict '<' keeps the lowest
                     h.t = t;
@@ -257,7 +258,8 @@ struct ParamScene {
 #pragma unroll
             for (int b = 0; b < MAXS; b++) {
                 float3 L = f3(sph[b].x - o.x, sph[b].y - o.y, sph[b].z - o.z);
-                lc.L[b] = make_float4(L.x, L.y, L.z, sphere_r2g(L, sph[b].w));
+                // a sphere the grid rules out never blocks: r2g = -inf, as for an origin inside
+                lc.L[b] = make_float4(L.x, L.y, L.z, (wm >> b) & 1u ? sphere_r2g(L, sph[b].w) : -INFINITY);
             }
         }
 #pragma unroll
@@ -265,6 +267,9 @@ struct ParamScene {
         return lc;
     }
 
+    // SPARSE (one ray per hit): the spheres the grid rules out are skipped;
+    // otherwise tested branch-free (their r2g = -inf never blocks)
+    template <bool SPARSE = false>
     __device__ __forceinline__ bool occluded(const Local &lc, float3 d, float limit) const {
         float m = -INFINITY;
 #pragma unroll
@@ -276,7 +281,7 @@ struct ParamScene {
 #pragma unroll
             for (int b = 0; b < MAXS; b++) {
                 if (b >= ns) break;
-                if (!((lc.wm >> b) & 1u)) continue;
+                if (SPARSE && !((lc.wm >> b) & 1u)) continue;
                 float4 L = lc.L[b];
                 m = fmaxf(m, sphere_margin_L(f3(L.x, L.y, L.z), d, L.w, limit));
             }
@@ -296,6 +301,7 @@ struct MemScene {
     const float4 *__restrict__ geo;
     int n;
 
+    template <bool SPARSE = false>
     __device__ __forceinline__ Hit closest(float3 o, float3 d, unsigned = ~0u) const {
         Hit h{-1, INFINITY, make_float4(0.f, 0.f, 0.f, -1.f)};
         for (int b = 0; b < n; b++) {
@@ -315,6 +321,7 @@ struct MemScene {
     };
     __device__ __forceinline__ Local localize(float3 o, unsigned = ~0u) const { return Local{o}; }
 
+    template <bool SPARSE = false>
     __device__ __forceinline__ bool occluded(const Local &lc, float3 d, float limit) const {
         for (int b = 0; b < n; b++) {
             float4 g = geo[b];

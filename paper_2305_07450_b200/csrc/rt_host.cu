@@ -541,7 +541,6 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
     WaveBufs &b = d.wb[buf];
     cudaError_t e;
     fa.rgba = ctx->rgba;
-    if (precision == RT_PREC_FP32 && ctx->cull && ctx->boxes && !ctx->cull_check) primary_boxes(fa, ctx->scene);
     if (fa.local_rows == 0) return RT_OK;
     int rc = RT_OK;
     d.ph_valid = false;
@@ -655,6 +654,7 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
             fa.work_counter = (unsigned *)d.counters.p + (d.counter_slot++ % rt::kCounterRing);
             RT_CK(cudaMemsetAsync(fa.work_counter, 0, sizeof(unsigned), st));
         }
+        if (ctx->cull && ctx->boxes) primary_boxes(fa, ctx->scene);
         rt::SceneArgs<float> sa = scene_args(d, d.s32, ctx->scene);
         // the shadow grid filters the any-hit tests of scenes up to 8 spheres
         // (it is built over their spheres; larger scenes' bits name clusters)

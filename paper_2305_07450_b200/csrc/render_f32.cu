@@ -31,10 +31,11 @@ using namespace rt32;
 
 // renderer.py:82-105 (+ shading.py:76-86 disc basis, 89-100 disc points)
 template <class Geo>
-__device__ float shadow_coeff(const Geo &geo, float3 surface, float3 normal, const SceneArgs<float> &sa, int n) {
+__device__ float shadow_coeff(const Geo &geo, float3 surface, float3 normal, const SceneArgs<float> &sa, int n,
+                             const MegaCull &mc) {
     const float3 lp = f3(sa.light[0], sa.light[1], sa.light[2]);
     const ShadowFrame f = shadow_frame(surface, normal, lp, n > 1);
-    const auto lc = geo.localize(f.origin, scene_grid_mask(sa, f.origin));
+    const auto lc = geo.localize(f.origin, scene_grid_mask(mc, f.origin));
     const float4 *__restrict__ tab = reinterpret_cast<const float4 *>(sa.table);
     if (n == 1) {  // hard shadows: one ray, the ruled-out spheres skipped
         float3 dir;
@@ -60,7 +61,7 @@ __device__ float shadow_coeff(const Geo &geo, float3 surface, float3 normal, con
 // live in L1-resident local memory.
 template <int BMAX, class Geo>
 __device__ float3 trace(const Geo &geo, float3 origin, float3 dir, const SceneArgs<float> &sa, int samples,
-                        int bounces, unsigned smask = ~0u) {
+                        int bounces, const MegaCull &mc, unsigned smask = ~0u) {
     int ridx[BMAX + 1];
     float rlum[BMAX + 1], rspec[BMAX + 1];
     int m = 0;
@@ -78,7 +79,7 @@ __device__ float3 trace(const Geo &geo, float3 origin, float3 dir, const SceneAr
         float3 hit = origin + dir * h.t;
         float3 normal = h.g.w >= 0.f ? normalize3(hit - f3(h.g.x, h.g.y, h.g.z)) : f3(0.f, 1.f, 0.f);
         float3 l = normalize3(lp - hit);
-        float sc = shadow_coeff(geo, hit, normal, sa, samples);
+        float sc = shadow_coeff(geo, hit, normal, sa, samples, mc);
         // shading.py:53-73, 159-162 (view = -dir)
         float dfs = fmaxf(dot3(normal, l), 0.f);
         float3 hv = l - dir;
@@ -120,14 +121,15 @@ __device__ float3 trace(const Geo &geo, float3 origin, float3 dir, const SceneAr
 }
 
 template <int BMAX, class Geo>
-__device__ __forceinline__ void shade_pixel(const Geo &geo, const FrameArgs &fa, const SceneArgs<float> &sa, int x,
+__device__ __forceinline__ void shade_pixel(const Geo &geo, const FrameArgs &fa, const SceneArgs<float> &sa,
+                                            const MegaCull &mc, int x,
                                             int ly) {
     if (x >= fa.width || ly >= fa.local_rows) return;
     int y = map_row(ly, fa);
     if (y >= fa.row_end) return;
     float3 dir = primary_direction(x, y, fa);
     float3 c = trace<BMAX>(geo, f3((float)fa.cam[0], (float)fa.cam[1], (float)fa.cam[2]), dir, sa, fa.samples,
-                           fa.bounces, primary_sphere_mask(fa, x, y));
+                           fa.bounces, mc, primary_sphere_mask(mc, x, y));
     fa.out[(int64_t)y * fa.out_pitch + x] = pack_color(c.x, c.y, c.z, fa.rgba);
     if (fa.radiance) {
         float *r = (float *)fa.radiance + 3 * ((int64_t)y * fa.width + x);
@@ -144,7 +146,8 @@ __device__ __forceinline__ void shade_pixel(const Geo &geo, const FrameArgs &fa,
 // patches are handed out bottom rows first (the scene, below the horizon)
 // so the cheap sky patches fill the tail.
 template <int BMAX, class Geo>
-__device__ __forceinline__ void render_patches(const Geo &geo, const FrameArgs &fa, const SceneArgs<float> &sa) {
+__device__ __forceinline__ void render_patches(const Geo &geo, const FrameArgs &fa, const SceneArgs<float> &sa,
+                                               const MegaCull &mc) {
     const int lane = threadIdx.x & 31;
     const int pw = (fa.width + 7) >> 3;
     const int ph = (fa.local_rows + 3) >> 2;
@@ -156,7 +159,7 @@ __device__ __forceinline__ void render_patches(const Geo &geo, const FrameArgs &
         if (p >= n_patches) break;
         int prow = ph - 1 - (int)(p / (unsigned)pw);
         int pcol = (int)(p % (unsigned)pw);
-        shade_pixel<BMAX>(geo, fa, sa, pcol * 8 + (lane & 7), prow * 4 + (lane >> 3));
+        shade_pixel<BMAX>(geo, fa, sa, mc, pcol * 8 + (lane & 7), prow * 4 + (lane >> 3));
         __syncwarp();
     }
     if (fa.peer_out) __threadfence_system();  // frame stores over NVLink land before the kernel retires
@@ -164,8 +167,9 @@ __device__ __forceinline__ void render_patches(const Geo &geo, const FrameArgs &
 
 template <int BMAX, int MAXS>
 __global__ void __launch_bounds__(kThreads, RT_F32_MIN_BLOCKS)
-    render_f32_param_kernel(const FrameArgs fa, const SceneArgs<float> sa, const ParamScene<MAXS> ps) {
-    render_patches<BMAX>(ps, fa, sa);
+    render_f32_param_kernel(const FrameArgs fa, const SceneArgs<float> sa, const ParamScene<MAXS> ps,
+                            const MegaCull mc) {
+    render_patches<BMAX>(ps, fa, sa, mc);
 }
 
 // One CTA per 16 x 8 tile, tile rows bottom first, no work counter: for
@@ -176,15 +180,17 @@ __global__ void __launch_bounds__(kThreads, RT_F32_MIN_BLOCKS)
 #endif
 template <int BMAX, int MAXS>
 __global__ void __launch_bounds__(kThreads, RT_F32_TILE_MIN_BLOCKS)
-    render_f32_tile_kernel(const FrameArgs fa, const SceneArgs<float> sa, const ParamScene<MAXS> ps) {
+    render_f32_tile_kernel(const FrameArgs fa, const SceneArgs<float> sa, const ParamScene<MAXS> ps,
+                           const MegaCull mc) {
     int x, ly;
     thread_pixel_bottom_first(x, ly);
-    shade_pixel<BMAX>(ps, fa, sa, x, ly);
+    shade_pixel<BMAX>(ps, fa, sa, mc, x, ly);
     if (fa.peer_out) __threadfence_system();
 }
 
 template <int BMAX, bool SMEM>
-__global__ void __launch_bounds__(kThreads) render_f32_kernel(const FrameArgs fa, const SceneArgs<float> sa) {
+__global__ void __launch_bounds__(kThreads)
+    render_f32_kernel(const FrameArgs fa, const SceneArgs<float> sa, const MegaCull mc) {
     extern __shared__ float4 smem_geo[];
     MemScene geo{reinterpret_cast<const float4 *>(sa.geo), sa.n};
     if constexpr (SMEM) {
@@ -192,7 +198,7 @@ __global__ void __launch_bounds__(kThreads) render_f32_kernel(const FrameArgs fa
         __syncthreads();
         geo.geo = smem_geo;
     }
-    render_patches<BMAX>(geo, fa, sa);
+    render_patches<BMAX>(geo, fa, sa, mc);
 }
 
 template <int BMAX, int MAXS>
@@ -203,7 +209,7 @@ __global__ void __launch_bounds__(kThreads)
     if (i >= n_rays) return;
     float3 c = trace<BMAX>(ps, f3((float)orig[3 * i], (float)orig[3 * i + 1], (float)orig[3 * i + 2]),
                            f3((float)dirs[3 * i], (float)dirs[3 * i + 1], (float)dirs[3 * i + 2]), sa, samples,
-                           bounces);
+                           bounces, MegaCull{});
     out[3 * i] = c.x;
     out[3 * i + 1] = c.y;
     out[3 * i + 2] = c.z;
@@ -218,24 +224,25 @@ __global__ void __launch_bounds__(kThreads)
     if (i >= n_rays) return;
     float3 c = trace<BMAX>(geo, f3((float)orig[3 * i], (float)orig[3 * i + 1], (float)orig[3 * i + 2]),
                            f3((float)dirs[3 * i], (float)dirs[3 * i + 1], (float)dirs[3 * i + 2]), sa, samples,
-                           bounces);
+                           bounces, MegaCull{});
     out[3 * i] = c.x;
     out[3 * i + 1] = c.y;
     out[3 * i + 2] = c.z;
 }
 
 template <int BMAX>
-cudaError_t launch_render(const FrameArgs &fa, const SceneArgs<float> &sa, cudaStream_t st, bool tiles) {
+cudaError_t launch_render(const FrameArgs &fa, const SceneArgs<float> &sa, cudaStream_t st, bool tiles,
+                          const MegaCull &mc) {
     if (tiles) {
         const dim3 grid((fa.width + kTileW - 1) / kTileW, (fa.local_rows + kTileH - 1) / kTileH);
         ParamScene<8> ps;
         if (pack_params(sa, ps)) {
-            render_f32_tile_kernel<BMAX, 8><<<grid, kThreads, 0, st>>>(fa, sa, ps);
+            render_f32_tile_kernel<BMAX, 8><<<grid, kThreads, 0, st>>>(fa, sa, ps, mc);
             return cudaGetLastError();
         }
         thread_local ParamScene<kParamSpheres> pl;
         if (pack_params(sa, pl)) {
-            render_f32_tile_kernel<BMAX, kParamSpheres><<<grid, kThreads, 0, st>>>(fa, sa, pl);
+            render_f32_tile_kernel<BMAX, kParamSpheres><<<grid, kThreads, 0, st>>>(fa, sa, pl, mc);
             return cudaGetLastError();
         }
         return cudaErrorNotSupported;  // larger scenes take the persistent kernels
@@ -245,7 +252,7 @@ cudaError_t launch_render(const FrameArgs &fa, const SceneArgs<float> &sa, cudaS
         if (pack_params(sa, ps)) {
             static thread_local int ctas = 0;
             if (!ctas) ctas = resident_ctas(render_f32_param_kernel<BMAX, 8>, 0);
-            render_f32_param_kernel<BMAX, 8><<<ctas, kThreads, 0, st>>>(fa, sa, ps);
+            render_f32_param_kernel<BMAX, 8><<<ctas, kThreads, 0, st>>>(fa, sa, ps, mc);
             return cudaGetLastError();
         }
     }
@@ -254,18 +261,18 @@ cudaError_t launch_render(const FrameArgs &fa, const SceneArgs<float> &sa, cudaS
         if (pack_params(sa, ps)) {
             static thread_local int ctas = 0;
             if (!ctas) ctas = resident_ctas(render_f32_param_kernel<BMAX, kParamSpheres>, 0);
-            render_f32_param_kernel<BMAX, kParamSpheres><<<ctas, kThreads, 0, st>>>(fa, sa, ps);
+            render_f32_param_kernel<BMAX, kParamSpheres><<<ctas, kThreads, 0, st>>>(fa, sa, ps, mc);
             return cudaGetLastError();
         }
     }
     size_t geo_bytes = sizeof(float4) * (size_t)sa.n;
     if (geo_bytes <= (size_t)kSmemGeoBytes) {
         int ctas = resident_ctas(render_f32_kernel<BMAX, true>, geo_bytes);
-        render_f32_kernel<BMAX, true><<<ctas, kThreads, geo_bytes, st>>>(fa, sa);
+        render_f32_kernel<BMAX, true><<<ctas, kThreads, geo_bytes, st>>>(fa, sa, mc);
     } else {
         static thread_local int ctas = 0;
         if (!ctas) ctas = resident_ctas(render_f32_kernel<BMAX, false>, 0);
-        render_f32_kernel<BMAX, false><<<ctas, kThreads, 0, st>>>(fa, sa);
+        render_f32_kernel<BMAX, false><<<ctas, kThreads, 0, st>>>(fa, sa, mc);
     }
     return cudaGetLastError();
 }
@@ -288,9 +295,9 @@ cudaError_t launch_trace(const double *o, const double *d, int64_t n, float *out
 }  // namespace
 
 cudaError_t rt_launch_render_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, cudaStream_t st,
-                                 bool tiles) {
-    if (fa.bounces <= 1) return launch_render<1>(fa, sa, st, tiles);
-    return launch_render<rt::kMaxBounce>(fa, sa, st, tiles);
+                                 bool tiles, const rt::MegaCull &mc) {
+    if (fa.bounces <= 1) return launch_render<1>(fa, sa, st, tiles, mc);
+    return launch_render<rt::kMaxBounce>(fa, sa, st, tiles, mc);
 }
 
 cudaError_t rt_launch_trace_f32(const double *o, const double *d, int64_t n, float *out,

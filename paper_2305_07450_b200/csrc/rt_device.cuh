@@ -44,21 +44,31 @@ struct FrameArgs {
     int row_end;                 // rows >= row_end are skipped (end of the band / frame)
     int row0;                    // first frame row of a contiguous band (sub_parts > 1 or n_parts == 1)
     int rgba;                    // pixel byte order: 0 B,G,R,A (0xAARRGGBB), 1 R,G,B,A
-    // FP32 scenes of up to 8 spheres: per sphere (in ascending body order) a
-    // conservative pixel box {x0, y0, x1, y1} outside which no primary ray
-    // can hit it (nbox = 0: none, every primary ray tests every sphere)
+};
+
+// The FP32 megakernel's per-frame culling data (render_f32.cu), a kernel
+// parameter of its own so the other kernels' parameters stay lean.
+struct MegaCull {
+    // scenes of up to 8 spheres: per sphere (ascending body order) a
+    // conservative pixel box {x0, y0, x1, y1} outside which no primary ray can
+    // hit it (nbox = 0: none, every primary ray tests every sphere)
     int nbox;
     int box[8][4];
+    // the shadow grid (render_fused_f32.cu, shadow_grid_build): per cell the
+    // spheres that can block a shadow ray from it; null: none
+    const unsigned *grid;
+    float grid_lo[3], grid_inv[3];
+    int grid_dim[3];
 };
 
 // The spheres whose primary-ray box holds pixel (x, y) (all when no boxes).
-__host__ __device__ __forceinline__ unsigned primary_sphere_mask(const FrameArgs &fa, int x, int y) {
-    if (!fa.nbox) return ~0u;
+__host__ __device__ __forceinline__ unsigned primary_sphere_mask(const MegaCull &mc, int x, int y) {
+    if (!mc.nbox) return ~0u;
     unsigned m = 0;
 #pragma unroll
     for (int b = 0; b < 8; b++) {
-        if (b >= fa.nbox) break;
-        const bool in = x >= fa.box[b][0] && x <= fa.box[b][2] && y >= fa.box[b][1] && y <= fa.box[b][3];
+        if (b >= mc.nbox) break;
+        const bool in = x >= mc.box[b][0] && x <= mc.box[b][2] && y >= mc.box[b][1] && y <= mc.box[b][3];
         m |= (in ? 1u : 0u) << b;
     }
     return m;
@@ -77,12 +87,6 @@ struct SceneArgs {
     R lc[3];
     R ambient;
     const double *host_geo;  // host copy of geo (float64), for launch-parameter scene packing
-    // FP32 scenes of up to 8 spheres: the shadow grid (render_fused_f32.cu,
-    // shadow_grid_build) — per cell the spheres that can block a shadow ray
-    // from it; null: none
-    const unsigned *grid;
-    float grid_lo[3], grid_inv[3];
-    int grid_dim[3];
 };
 
 // Wavefront queues (render_wave_f32.cu); slot = bounce * n_pix + local pixel.
@@ -207,7 +211,7 @@ __device__ __forceinline__ uint32_t pack_color(R r, R g, R b, int rgba) {
 // tiles: one CTA per 16 x 8 tile (scenes that fit the launch parameters);
 // otherwise persistent warps on a work counter (fa.work_counter, zeroed)
 cudaError_t rt_launch_render_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, cudaStream_t st,
-                                 bool tiles);
+                                 bool tiles, const rt::MegaCull &mc);
 cudaError_t rt_launch_render_f64(const rt::FrameArgs &fa, const rt::SceneArgs<double> &sa, cudaStream_t st);
 cudaError_t rt_launch_wave_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, const rt::WaveArgs &wa,
                                cudaStream_t st, int *n_kernels, cudaEvent_t *phase_events /* 5 or null */);

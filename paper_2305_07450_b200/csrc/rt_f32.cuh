@@ -88,17 +88,17 @@ __device__ __forceinline__ float blinn_pow(float d, float e) {
 
 constexpr float kGraze = 1e-7f;  // geometry.py:24
 
-// The shadow grid's mask for a shadow origin o (SceneArgs::grid): ~0 when
+// The shadow grid's mask for a shadow origin o (MegaCull::grid): ~0 when
 // there is no grid or o lies outside it.
-__device__ __forceinline__ unsigned scene_grid_mask(const SceneArgs<float> &sa, float3 o) {
-    if (!sa.grid) return ~0u;
-    const int ix = __float2int_rd((o.x - sa.grid_lo[0]) * sa.grid_inv[0]);
-    const int iy = __float2int_rd((o.y - sa.grid_lo[1]) * sa.grid_inv[1]);
-    const int iz = __float2int_rd((o.z - sa.grid_lo[2]) * sa.grid_inv[2]);
-    if ((unsigned)ix >= (unsigned)sa.grid_dim[0] || (unsigned)iy >= (unsigned)sa.grid_dim[1] ||
-        (unsigned)iz >= (unsigned)sa.grid_dim[2])
+__device__ __forceinline__ unsigned scene_grid_mask(const MegaCull &mc, float3 o) {
+    if (!mc.grid) return ~0u;
+    const int ix = __float2int_rd((o.x - mc.grid_lo[0]) * mc.grid_inv[0]);
+    const int iy = __float2int_rd((o.y - mc.grid_lo[1]) * mc.grid_inv[1]);
+    const int iz = __float2int_rd((o.z - mc.grid_lo[2]) * mc.grid_inv[2]);
+    if ((unsigned)ix >= (unsigned)mc.grid_dim[0] || (unsigned)iy >= (unsigned)mc.grid_dim[1] ||
+        (unsigned)iz >= (unsigned)mc.grid_dim[2])
         return ~0u;
-    return __ldg(sa.grid + ((size_t)iz * sa.grid_dim[1] + iy) * sa.grid_dim[0] + ix);
+    return __ldg(mc.grid + ((size_t)iz * mc.grid_dim[1] + iy) * mc.grid_dim[0] + ix);
 }
 
 // L = centre - origin; r2g = r^2 + GRAZE, or -inf when the origin is inside

@@ -375,11 +375,6 @@ rt::SceneArgs<R> scene_args(const Dev &d, const DevScene<R> &ds, const HostScene
     a.light_radius = (R)s.light_radius;
     a.ambient = (R)s.ambient;
     a.host_geo = s.geo.data();
-    a.grid = nullptr;
-    for (int c = 0; c < 3; c++) {
-        a.grid_lo[c] = a.grid_inv[c] = 0.f;
-        a.grid_dim[c] = 0;
-    }
     return a;
 }
 
@@ -461,7 +456,6 @@ rt::FrameArgs frame_args(uint32_t *out, int64_t pitch, void *rad, int w, int h, 
     fa.row_end = h;
     fa.row0 = 0;
     fa.rgba = 0;
-    fa.nbox = 0;
     return fa;
 }
 
@@ -486,8 +480,8 @@ int ensure_counts(WaveBufs &b, cudaStream_t st) {
 // behind the eye gets an empty box; one the eye is in or near, or whose cone
 // reaches the image plane's horizon, the whole frame.  Exact: a ray outside
 // the box misses the sphere in the kernels' own test.
-void primary_boxes(rt::FrameArgs &fa, const HostScene &s) {
-    fa.nbox = 0;
+void primary_boxes(rt::MegaCull &mc, const rt::FrameArgs &fa, const HostScene &s) {
+    mc.nbox = 0;
     int nb = 0;
     for (int b = 0; b < s.n; b++) nb += s.geo[4 * b + 3] >= 0.0 ? 1 : 0;
     if (nb == 0 || nb > 8) return;
@@ -496,7 +490,7 @@ void primary_boxes(rt::FrameArgs &fa, const HostScene &s) {
     for (int b = 0; b < s.n; b++) {
         const double *g = &s.geo[4 * b];
         if (g[3] < 0.0) continue;
-        int *bx = fa.box[k++];
+        int *bx = mc.box[k++];
         bx[0] = bx[1] = -1;  // the whole frame
         bx[2] = fa.width;
         bx[3] = fa.height;
@@ -534,7 +528,7 @@ void primary_boxes(rt::FrameArgs &fa, const HostScene &s) {
         bx[1] = (int)clampd(std::floor(std::min(ya, yb)) - 2.0, -1.0, H);
         bx[3] = (int)clampd(std::ceil(std::max(ya, yb)) + 2.0, -1.0, H);
     }
-    fa.nbox = nb;
+    mc.nbox = nb;
 }
 
 int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStream_t st, int buf = 0) {
@@ -654,19 +648,19 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
             fa.work_counter = (unsigned *)d.counters.p + (d.counter_slot++ % rt::kCounterRing);
             RT_CK(cudaMemsetAsync(fa.work_counter, 0, sizeof(unsigned), st));
         }
-        if (ctx->cull && ctx->boxes) primary_boxes(fa, ctx->scene);
-        rt::SceneArgs<float> sa = scene_args(d, d.s32, ctx->scene);
+        rt::MegaCull mc = {};
+        if (ctx->cull && ctx->boxes) primary_boxes(mc, fa, ctx->scene);
         // the shadow grid filters the any-hit tests of scenes up to 8 spheres
         // (it is built over their spheres; larger scenes' bits name clusters)
         if (ctx->cull && ns <= 8 && d.grid_version == ctx->scene.version && d.grid_wa.grid) {
-            sa.grid = d.grid_wa.grid;
+            mc.grid = d.grid_wa.grid;
             for (int c = 0; c < 3; c++) {
-                sa.grid_lo[c] = d.grid_wa.grid_lo[c];
-                sa.grid_inv[c] = d.grid_wa.grid_inv[c];
-                sa.grid_dim[c] = d.grid_wa.grid_dim[c];
+                mc.grid_lo[c] = d.grid_wa.grid_lo[c];
+                mc.grid_inv[c] = d.grid_wa.grid_inv[c];
+                mc.grid_dim[c] = d.grid_wa.grid_dim[c];
             }
         }
-        e = rt_launch_render_f32(fa, sa, st, tiles);
+        e = rt_launch_render_f32(fa, scene_args(d, d.s32, ctx->scene), st, tiles, mc);
     }
     if (e != cudaSuccess) return fail(RT_ERR_CUDA, std::string("render kernel launch: ") + cudaGetErrorString(e));
     ctx->launches++;

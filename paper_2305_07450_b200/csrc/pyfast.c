@@ -41,27 +41,48 @@ typedef struct {
 static float g_no_sky[3] = {0.f, 0.f, 0.f};
 static __thread Packed g_packed;
 
+/* attribute names, interned once (PyInit__pyfast) */
+enum { A_BODIES, A_KIND, A_POSITION, A_SIZE, A_COLOR, A_REFLECTIVITY, A_LIGHT, A_RADIUS, A_AMBIENT, A_MAX_REFL,
+       A_SKYBOX, A_TEXELS, A_WIDTH, A_HEIGHT, A_N };
+static const char *const g_attr_names[A_N] = {"bodies", "kind",  "position",         "size",   "color",
+                                              "reflectivity", "light", "radius", "ambient", "max_reflectivity",
+                                              "skybox", "texels", "width", "height"};
+static PyObject *g_attr[A_N];
+
+static PyObject *get(PyObject *o, int a) { return PyObject_GetAttr(o, g_attr[a]); }
+
+/* a float (or int) item without the generic number protocol when it is a float */
+static inline int as_double(PyObject *v, double *out) {
+    if (PyFloat_CheckExact(v)) {
+        *out = PyFloat_AS_DOUBLE(v);
+        return 1;
+    }
+    *out = PyFloat_AsDouble(v);
+    if (*out == -1.0 && PyErr_Occurred()) {
+        PyErr_Clear();
+        return 0;
+    }
+    return 1;
+}
+
 /* 3 floats from a sequence attribute; 0 on failure (no Python error left set) */
 static int vec3(PyObject *o, double *out) {
+    if (PyTuple_CheckExact(o) && PyTuple_GET_SIZE(o) >= 3)
+        return as_double(PyTuple_GET_ITEM(o, 0), out) && as_double(PyTuple_GET_ITEM(o, 1), out + 1) &&
+               as_double(PyTuple_GET_ITEM(o, 2), out + 2);
     PyObject *seq = PySequence_Fast(o, "");
     if (!seq) {
         PyErr_Clear();
         return 0;
     }
     int ok = PySequence_Fast_GET_SIZE(seq) >= 3;
-    for (int i = 0; ok && i < 3; i++) {
-        out[i] = PyFloat_AsDouble(PySequence_Fast_GET_ITEM(seq, i));
-        if (out[i] == -1.0 && PyErr_Occurred()) {
-            PyErr_Clear();
-            ok = 0;
-        }
-    }
+    for (int i = 0; ok && i < 3; i++) ok = as_double(PySequence_Fast_GET_ITEM(seq, i), out + i);
     Py_DECREF(seq);
     return ok;
 }
 
-static int attr_vec3(PyObject *o, const char *name, double *out) {
-    PyObject *a = PyObject_GetAttrString(o, name);
+static int attr_vec3(PyObject *o, int name, double *out) {
+    PyObject *a = get(o, name);
     if (!a) {
         PyErr_Clear();
         return 0;
@@ -71,24 +92,20 @@ static int attr_vec3(PyObject *o, const char *name, double *out) {
     return ok;
 }
 
-static int attr_double(PyObject *o, const char *name, double *out) {
-    PyObject *a = PyObject_GetAttrString(o, name);
+static int attr_double(PyObject *o, int name, double *out) {
+    PyObject *a = get(o, name);
     if (!a) {
         PyErr_Clear();
         return 0;
     }
-    *out = PyFloat_AsDouble(a);
+    int ok = as_double(a, out);
     Py_DECREF(a);
-    if (*out == -1.0 && PyErr_Occurred()) {
-        PyErr_Clear();
-        return 0;
-    }
-    return 1;
+    return ok;
 }
 
 static int pack(PyObject *scene, Packed *p) {
     p->have_view = 0;
-    PyObject *bodies = PyObject_GetAttrString(scene, "bodies");
+    PyObject *bodies = get(scene, A_BODIES);
     if (!bodies) {
         PyErr_Clear();
         return 0;
@@ -104,7 +121,7 @@ static int pack(PyObject *scene, Packed *p) {
     p->n = (int)n;
     for (Py_ssize_t i = 0; ok && i < n; i++) {
         PyObject *b = PySequence_Fast_GET_ITEM(seq, i);
-        PyObject *k = PyObject_GetAttrString(b, "kind");
+        PyObject *k = get(b, A_KIND);
         if (!k) {
             PyErr_Clear();
             ok = 0;
@@ -118,22 +135,22 @@ static int pack(PyObject *scene, Packed *p) {
             break;
         }
         p->kinds[i] = (int32_t)kv;
-        ok = attr_vec3(b, "position", p->pos + 3 * i) && attr_double(b, "size", p->size + i) &&
-             attr_vec3(b, "color", p->color + 3 * i) && attr_double(b, "reflectivity", p->refl + i);
+        ok = attr_vec3(b, A_POSITION, p->pos + 3 * i) && attr_double(b, A_SIZE, p->size + i) &&
+             attr_vec3(b, A_COLOR, p->color + 3 * i) && attr_double(b, A_REFLECTIVITY, p->refl + i);
     }
     Py_DECREF(seq);
     if (!ok) return 0;
-    PyObject *light = PyObject_GetAttrString(scene, "light");
+    PyObject *light = get(scene, A_LIGHT);
     if (!light) {
         PyErr_Clear();
         return 0;
     }
-    ok = attr_vec3(light, "position", p->light_pos) && attr_vec3(light, "color", p->light_color) &&
-         attr_double(light, "radius", &p->light_radius);
+    ok = attr_vec3(light, A_POSITION, p->light_pos) && attr_vec3(light, A_COLOR, p->light_color) &&
+         attr_double(light, A_RADIUS, &p->light_radius);
     Py_DECREF(light);
-    if (!ok || !attr_double(scene, "ambient", &p->ambient) || !attr_double(scene, "max_reflectivity", &p->max_refl))
+    if (!ok || !attr_double(scene, A_AMBIENT, &p->ambient) || !attr_double(scene, A_MAX_REFL, &p->max_refl))
         return 0;
-    PyObject *sky = PyObject_GetAttrString(scene, "skybox");
+    PyObject *sky = get(scene, A_SKYBOX);
     if (!sky) PyErr_Clear();
     if (!sky || sky == Py_None) {
         Py_XDECREF(sky);
@@ -143,8 +160,8 @@ static int pack(PyObject *scene, Packed *p) {
         return 1;
     }
     double w = 0, h = 0;
-    PyObject *tex = PyObject_GetAttrString(sky, "texels");
-    ok = tex && attr_double(sky, "width", &w) && attr_double(sky, "height", &h);
+    PyObject *tex = get(sky, A_TEXELS);
+    ok = tex && attr_double(sky, A_WIDTH, &w) && attr_double(sky, A_HEIGHT, &h);
     Py_DECREF(sky);
     if (!tex) PyErr_Clear();
     if (ok && PyObject_GetBuffer(tex, &p->sky_view, PyBUF_C_CONTIGUOUS | PyBUF_FORMAT) == 0) {
@@ -237,4 +254,8 @@ static PyMethodDef methods[] = {
 
 static struct PyModuleDef module = {PyModuleDef_HEAD_INIT, "_pyfast", NULL, -1, methods};
 
-PyMODINIT_FUNC PyInit__pyfast(void) { return PyModule_Create(&module); }
+PyMODINIT_FUNC PyInit__pyfast(void) {
+    for (int i = 0; i < A_N; i++)
+        if (!g_attr[i] && !(g_attr[i] = PyUnicode_InternFromString(g_attr_names[i]))) return NULL;
+    return PyModule_Create(&module);
+}

@@ -391,26 +391,34 @@ def test_zero_copy_option_gives_the_same_frame():
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 def test_copy_overlap_bands_do_not_change_pixels(precision):
     """rt_render_v1's row bands (option bands, 1-8, each on its own stream,
-    copied as soon as it is done) partition the frame: same bytes, same
-    radiance, with and without several partitions inside each band."""
+    copied as soon as it is done; band_first sizes band 0) partition the
+    frame: same bytes, same radiance, with and without several partitions
+    inside each band."""
     s = rt.build_benchmark_scene()
     cam = rt.benchmark_camera()
     params = rt.RenderParams(32, 3, 240, 136)
     dt = np.float32 if precision == "fp32" else np.float64
     ref = None
+    ctx = _native.context(1)
     try:
-        for bands in (1, 2, 3, 5, 8):
+        for bands, first in ((1, 0), (2, 0), (3, 0), (5, 0), (8, 0), (2, 700), (4, 450), (3, 999), (6, 1)):
             for workers in (None, 3):
-                _native.set_options(bands=bands)
+                _native.set_options(bands=bands, band_first=first, band_times=1)
                 fb = rt.Framebuffer.create(240, 136)
                 rad = np.zeros((240 * 136, 3), dt)
                 rt.render_frame(s, cam, params, fb, workers, precision=precision, radiance=rad)
                 if ref is None:
                     ref = (fb.pixels.copy(), rad.copy())
-                np.testing.assert_array_equal(fb.pixels, ref[0], err_msg=f"bands={bands} workers={workers}")
-                np.testing.assert_array_equal(rad, ref[1], err_msg=f"bands={bands} workers={workers}")
+                tag = f"bands={bands} first={first} workers={workers}"
+                np.testing.assert_array_equal(fb.pixels, ref[0], err_msg=tag)
+                np.testing.assert_array_equal(rad, ref[1], err_msg=tag)
+                if workers is None:  # band_times: per band, kernels end before the copy ends, in band order
+                    times = ctx.band_times_ms()
+                    assert len(times) == bands, tag
+                    assert all(0.0 <= k <= c for k, c in times), (tag, times)
+                    assert all(a[1] <= b[1] for a, b in zip(times, times[1:])), (tag, times)
     finally:
-        _native.set_options(bands=0)
+        _native.set_options(bands=0, band_first=0, band_times=0)
 
 
 def _edge_cases():

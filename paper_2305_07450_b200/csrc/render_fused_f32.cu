@@ -128,6 +128,7 @@ __device__ __forceinline__ int classify_hit(const ParamScene<MAXS> &ps, const Co
 #pragma unroll
     for (int w = 0; w <= kWords; w++) mask[w] = 0;
     if (check) {  // option cull_check: every body undecided
+#pragma unroll 1
         for (int b = 0; b < ps.ns; b++) mask[b >> 5] |= 1u << (b & 31);
         mask[kWords] = (1u << ps.np) - 1u;
         return ps.ns + ps.np > 0 ? 1 : 0;
@@ -150,9 +151,8 @@ __device__ __forceinline__ int classify_hit(const ParamScene<MAXS> &ps, const Co
             for (int b = ps.cl_begin[c]; b < ps.cl_begin[c + 1]; b++) classify(b);
         }
     }
-#pragma unroll
-    for (int j = 0; j < kMaxPlanes; j++) {
-        if (j >= ps.np) break;
+#pragma unroll(kPlaneUnroll)
+    for (int j = 0; j < ps.np; j++) {
         int cls = plane_class(k, oy, ly, ps.pl_h[j]);
         mask[kWords] |= (cls == 1 ? 1u : 0u) << j;
         full |= cls == 2;
@@ -273,9 +273,8 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? 8 : 6)
             cos_t = fminf(cos_t * (1.f - kBoundRel), 1.f);
             const float sin_t = sqrtf(fmaxf(1.f - cos_t * cos_t, 0.f));
             if (alive) {
-#pragma unroll
-                for (int j = 0; j < kMaxPlanes; j++) {
-                    if (j >= ps.np) break;
+#pragma unroll(kPlaneUnroll)
+                for (int j = 0; j < ps.np; j++) {
                     float t = plane_t(origin, dir, ps.pl_h[j]);
                     if (t < h.t || (t == h.t && ps.pl_idx[j] < h.idx)) {
                         h.t = t;
@@ -437,6 +436,7 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? 8 : 6)
         // parked: the sampler of its last pending hit unwinds it (resolve_hit)
         wa.pix[lp] = make_float4(tail.x, tail.y, tail.z, __int_as_float(m | (exhausted << 8) | ((npend > 1) << 9)));
         if (npend > 1) wa.pend[lp] = npend;
+#pragma unroll 2
         for (int k = 0; k < m; k++)
             wa.rec[(int64_t)k * wa.n_pix + lp] = make_float4(__int_as_float(ridx[k]), rdfs[k], rs[k], rsc[k]);
     }
@@ -486,6 +486,7 @@ __device__ __forceinline__ void resolve_hit(const FrameArgs &fa, const SceneArgs
 #pragma unroll
     for (int k = 0; k < kPre; k++)
         if (k < have) rk[k] = pre->r[k];
+#pragma unroll 4
     for (int k = have; k < m; k++) rk[k] = __ldcg(wa.rec + (int64_t)k * n_pix + lp);
     const float3 c = unwind(
         m, (info >> 8) & 1, f3(px.x, px.y, px.z), sa,

@@ -21,6 +21,12 @@ namespace rt32 {
 using namespace rt;
 
 constexpr int kMaxPlanes = 8;
+// plane loops (a scene has one plane or a few): not unrolled, which keeps the
+// hot kernels' code — and their instruction-cache misses — smaller
+#ifndef RT_PLANE_UNROLL
+#define RT_PLANE_UNROLL 1
+#endif
+constexpr int kPlaneUnroll = RT_PLANE_UNROLL;
 
 __device__ __forceinline__ float3 f3(float x, float y, float z) { return make_float3(x, y, z); }
 __device__ __forceinline__ float3 operator+(float3 a, float3 b) { return f3(a.x + b.x, a.y + b.y, a.z + b.z); }
@@ -78,11 +84,13 @@ __device__ __forceinline__ float plane_t(float3 o, float3 d, float h) {
 //   sphere: tca >= 0, rad >= -GRAZE, origin outside (tca^2 >= rad), and
 //           t = tca - sqrt(max(rad, 0)) < limit  <=>  min(q, q^2 - rad) < 0, q = tca - limit;
 //   plane:  0 < (h - o.y)/d.y < limit  <=>  min(num*dy, limit*|dy| - |num|) > 0.
-// d ** e of the Blinn highlight (shading.py:73) for d in [0, 1]: exp2(e log2 d)
-// with pow's special cases (0 ** 0 = 1, 0 ** e = 0); log2f / exp2f keep ~1e-7
-// relative error, the FP32 budget, at a fraction of powf's instructions.
+// d ** e of the Blinn highlight (shading.py:73) for d in [0, 1] and the
+// validated reflectivities e >= 0 (geometry.py:42-48): exp2(e log2 d) with
+// pow's special cases (d ** 0 = 1, 0 ** e = 0); log2f / exp2f keep ~1e-7
+// relative error, the FP32 budget.  No powf: its ~150 instructions of
+// special-case code sat in every hit's path (instruction-cache pressure).
 __device__ __forceinline__ float blinn_pow(float d, float e) {
-    if (!(e > 0.f)) return e == 0.f ? 1.f : powf(d, e);
+    if (e == 0.f) return 1.f;
     return d > 0.f ? exp2f(e * log2f(d)) : 0.f;
 }
 
@@ -194,9 +202,8 @@ struct ParamScene {
                 h.idx = sph_idx[slot];
                 h.g = sph[slot];
             }
-#pragma unroll
-            for (int j = 0; j < kMaxPlanes; j++) {
-                if (j >= np) break;
+#pragma unroll(kPlaneUnroll)
+            for (int j = 0; j < np; j++) {
                 float t = plane_t(o, d, pl_h[j]);
                 if (t < h.t || (t == h.t && pl_idx[j] < h.idx)) {  // geometry.py:198 across kinds
                     h.t = t;
@@ -206,9 +213,8 @@ struct ParamScene {
             }
         } else {
             // planes first: a floor hit bounds the cluster walk
-#pragma unroll
-            for (int j = 0; j < kMaxPlanes; j++) {
-                if (j >= np) break;
+#pragma unroll(kPlaneUnroll)
+            for (int j = 0; j < np; j++) {
                 float t = plane_t(o, d, pl_h[j]);
                 if (t < h.t || (t == h.t && pl_idx[j] < h.idx)) {
                     h.t = t;
@@ -246,7 +252,6 @@ struct ParamScene {
     struct Local {
         float3 o;
         float4 L[kClustered ? 1 : MAXS];  // xyz = centre - origin, w = r2g
-        float num[kMaxPlanes];
         unsigned wm;
     };
 
@@ -262,8 +267,6 @@ struct ParamScene {
                 lc.L[b] = make_float4(L.x, L.y, L.z, (wm >> b) & 1u ? sphere_r2g(L, sph[b].w) : -INFINITY);
             }
         }
-#pragma unroll
-        for (int j = 0; j < kMaxPlanes; j++) lc.num[j] = pl_h[j] - o.y;
         return lc;
     }
 
@@ -272,10 +275,9 @@ struct ParamScene {
     template <bool SPARSE = false>
     __device__ __forceinline__ bool occluded(const Local &lc, float3 d, float limit) const {
         float m = -INFINITY;
-#pragma unroll
-        for (int j = 0; j < kMaxPlanes; j++) {
-            if (j >= np) break;
-            m = fmaxf(m, plane_margin(lc.num[j], d.y, limit));
+#pragma unroll(kPlaneUnroll)
+        for (int j = 0; j < np; j++) {
+            m = fmaxf(m, plane_margin(pl_h[j] - lc.o.y, d.y, limit));
         }
         if constexpr (!kClustered) {
 #pragma unroll

@@ -609,6 +609,44 @@ __device__ __forceinline__ unsigned conic_blocked_z(float4 A, float4 B, float z0
     return (__float_as_uint(d) & ~__float_as_uint(z)) >> 31;
 }
 
+// The same tests on two samples at once with the paired FP32 instructions
+// (FFMA2 / FADD2: per component exactly fmaf / the add, so each sample's d —
+// and its bit — is the scalar test's).  ab = {a_i, a_i+1, b_i, b_i+1}, rho =
+// {rho_i, rho_i+1} (SamplePairs); returns how many of the two are blocked.
+struct Conic2 {
+    float2 ax, ay, az, aw, bx, by, bz, bw, b0, b1, b2, z0;
+};
+__device__ __forceinline__ float2 dup2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ Conic2 make_conic2(float4 A, float4 B, float z0, float b0, float b1, float b2) {
+    return Conic2{dup2(A.x), dup2(A.y), dup2(A.z), dup2(A.w), dup2(B.x), dup2(B.y),
+                  dup2(B.z), dup2(B.w), dup2(b0), dup2(b1), dup2(b2), dup2(z0)};
+}
+template <bool ZTEST>
+__device__ __forceinline__ unsigned conic_blocked2(const Conic2 &c, float4 ab, float2 rho) {
+    const float2 a = make_float2(ab.x, ab.y), b = make_float2(ab.z, ab.w);
+    const float2 w2 = __ffma2_rn(c.b1, a, __ffma2_rn(c.b2, b, __fadd2_rn(c.b0, rho)));
+    const float2 x = __ffma2_rn(c.ay, a, __ffma2_rn(c.az, b, c.ax));
+    const float2 y = __ffma2_rn(c.bx, a, __ffma2_rn(c.by, b, c.aw));
+    const float2 d = __ffma2_rn(x, x, __ffma2_rn(y, y, make_float2(-w2.x, -w2.y)));
+    unsigned bx = __float_as_uint(d.x), by = __float_as_uint(d.y);
+    if constexpr (ZTEST) {
+        const float2 z = __ffma2_rn(c.bz, a, __ffma2_rn(c.bw, b, c.z0));
+        bx &= ~__float_as_uint(z.x);
+        by &= ~__float_as_uint(z.y);
+    }
+    return (bx >> 31) + (by >> 31);
+}
+
+// The disc-sample table in pairs for conic_blocked2, staged after the float4
+// table in shared memory by fused_sample for up to kPairSamples samples; an
+// odd count's last pair is padded with rho = -inf, which never blocks.
+constexpr int kPairSamples = 1024;
+struct SamplePairs {
+    const float4 *ab;
+    const float2 *rho;
+    int n;  // pairs
+};
+
 // Sampling of one silhouette-form hit (conic_entry): P = {|lo|^2, 2 lo.bu,
 // 2 lo.bv, slot}, sphere j's coefficients C[2j], C[2j+1] (the first sphere's
 // arrive prefetched).  Returns the unblocked count of this lane's samples.
@@ -679,7 +717,8 @@ __device__ __forceinline__ int sample_conic(const WaveArgs &wa, unsigned e, int 
 // sample_conic, so either sampler gives the same bits.
 template <int MAXS, bool SMEM_TAB>
 __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArgs<float> &sa, const WaveArgs &wa,
-                                             const ParamScene<MAXS> &ps, const float4 *gtab, const float4 *mat4) {
+                                             const ParamScene<MAXS> &ps, const float4 *gtab, const float4 *mat4,
+                                             const SamplePairs pairs) {
     const int n = fa.samples;
     auto table = [&](int i) -> float4 {
         if constexpr (SMEM_TAB) {
@@ -731,6 +770,15 @@ __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArg
                     blocked += conic_blocked_z(A, B, z0, b0, b1, b2, t);
                 }
             }
+        } else if (pairs.n) {  // the paired instructions, two samples a step
+            const Conic2 c2 = make_conic2(A, B, r == 3 ? -1.f : 1.f, b0, b1, b2);
+            if (__any_sync(act, r >= 2)) {
+#pragma unroll 2
+                for (int p = 0; p < pairs.n; p++) blocked += conic_blocked2<true>(c2, pairs.ab[p], pairs.rho[p]);
+            } else {
+#pragma unroll 2
+                for (int p = 0; p < pairs.n; p++) blocked += conic_blocked2<false>(c2, pairs.ab[p], pairs.rho[p]);
+            }
         } else if (__any_sync(act, r >= 2)) {
             const float z0 = r == 3 ? -1.f : 1.f;
 #pragma unroll 4
@@ -766,16 +814,29 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_SAMPLE_MIN_BLOCKS : 1
     // the bodies' base colours for the unwinds (kParamSpheres + kMaxPlanes bodies at most)
     __shared__ float4 s_mat[kParamSpheres + kMaxPlanes];
     for (int i = threadIdx.x; i < sa.n; i += blockDim.x) s_mat[i] = __ldg(reinterpret_cast<const float4 *>(sa.mat) + 2 * i);
+    SamplePairs pairs = {nullptr, nullptr, 0};
     if constexpr (SMEM_TAB) {
         extern __shared__ float4 smem_tab_k[];
         for (int i = threadIdx.x; i < n; i += blockDim.x) smem_tab_k[i] = gtab[i];
+        if (n <= kPairSamples) {
+            const int np = (n + 1) / 2;
+            float4 *ab = smem_tab_k + n;
+            float2 *rho = reinterpret_cast<float2 *>(ab + np);
+            for (int p = threadIdx.x; p < np; p += blockDim.x) {
+                const float4 t0 = gtab[2 * p];
+                const float4 t1 = 2 * p + 1 < n ? gtab[2 * p + 1] : make_float4(0.f, 0.f, -INFINITY, 0.f);
+                ab[p] = make_float4(t0.x, t1.x, t0.y, t1.y);
+                rho[p] = make_float2(t0.z, t1.z);
+            }
+            pairs = SamplePairs{ab, rho, np};
+        }
     }
     __syncthreads();
     // programmatic dependent launch: everything above (the table staging)
     // overlaps the trace kernel's tail; the queue is read only after it
     cudaGridDependencySynchronize();
     if (wa.lane_cap) {  // B1: the single-candidate hits, one lane each
-        sample_lanes<MAXS, SMEM_TAB>(fa, sa, wa, ps, gtab, s_mat);
+        sample_lanes<MAXS, SMEM_TAB>(fa, sa, wa, ps, gtab, s_mat, pairs);
     }
     // B2: the rest, one warp each
     const unsigned count = wa.count[1];
@@ -871,7 +932,9 @@ cudaError_t launch(const FrameArgs &fa, const SceneArgs<float> &sa, const WaveAr
     }
     const int n = fa.samples;
     if (n <= kWaveSmemSamples) {
-        const size_t smem = sizeof(float4) * (size_t)n;
+        // the float4 table, then (up to kPairSamples samples) its pairs
+        const size_t smem = sizeof(float4) * (size_t)n +
+                            (n <= kPairSamples ? (sizeof(float4) + sizeof(float2)) * (size_t)((n + 1) / 2) : 0);
         e = launch_pdl(fused_sample<MAXS, true>, resident_ctas(fused_sample<MAXS, true>, smem), smem, st, fa, sa, wa,
                        ps);
     } else {

@@ -30,6 +30,7 @@
 //   pix     float4 {tail rgb, records | exhausted << 8 | several pending << 9}
 //   pend    per parked pixel with several pending hits: the countdown
 #include "rt_wave.cuh"
+#include <cuda/atomic>
 
 namespace {
 using namespace rt;
@@ -474,9 +475,15 @@ __device__ __forceinline__ void resolve_hit(const FrameArgs &fa, const SceneArgs
     const bool several = info & (1 << 9);
     if (several) {
         reinterpret_cast<float *>(wa.rec + slot)[3] = sc;
+#ifdef RT_ACQREL_COUNTDOWN
+        // release our coefficient, acquire the others' (the last sampler reads them)
+        cuda::atomic_ref<int, cuda::thread_scope_device> pend(wa.pend[lp]);
+        if (pend.fetch_sub(1, cuda::memory_order_acq_rel) != 1) return;
+#else
         __threadfence();
         if (atomicSub(wa.pend + lp, 1) != 1) return;
         __threadfence();
+#endif
     }
     const int m = info & 0xff;
     // records of a single-pending pixel do not change after the trace: the
@@ -641,6 +648,10 @@ __device__ __forceinline__ unsigned conic_blocked2(const Conic2 &c, float4 ab, f
 // table in shared memory by fused_sample for up to kPairSamples samples; an
 // odd count's last pair is padded with rho = -inf, which never blocks.
 constexpr int kPairSamples = 1024;
+#ifndef RT_PAIR_UNROLL
+#define RT_PAIR_UNROLL 2
+#endif
+constexpr int kPairUnroll = RT_PAIR_UNROLL;
 struct SamplePairs {
     const float4 *ab;
     const float2 *rho;
@@ -773,10 +784,10 @@ __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArg
         } else if (pairs.n) {  // the paired instructions, two samples a step
             const Conic2 c2 = make_conic2(A, B, r == 3 ? -1.f : 1.f, b0, b1, b2);
             if (__any_sync(act, r >= 2)) {
-#pragma unroll 2
+#pragma unroll(kPairUnroll)
                 for (int p = 0; p < pairs.n; p++) blocked += conic_blocked2<true>(c2, pairs.ab[p], pairs.rho[p]);
             } else {
-#pragma unroll 2
+#pragma unroll(kPairUnroll)
                 for (int p = 0; p < pairs.n; p++) blocked += conic_blocked2<false>(c2, pairs.ab[p], pairs.rho[p]);
             }
         } else if (__any_sync(act, r >= 2)) {
@@ -796,6 +807,7 @@ __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArg
             atomicAdd(wa.work + kWorkSampledHits, 1ull);
             atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);
             atomicAdd(wa.work + kWorkSphereTests, (unsigned long long)n);
+            atomicAdd(wa.work + kWorkLaneHits, 1ull);
         }
     }
 }

@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? 8 : 6)
 // A sampled hit's coefficient sc (record slot = bounce * n_pix + pixel): a
 // pixel with this one pending hit is unwound and packed at once (its other
 // records are decided); with several, the coefficient is stored and the last
-// of the pixel's samplers — an atomic countdown, fenced both ways — unwinds it.
+// of the pixel's samplers — an acquire-release atomic countdown — unwinds it.
 // The first records of a parked pixel, loaded ahead (their latency hides
 // behind the sampling); kPre covers every record of a frame of up to 3 bounces.
 constexpr int kPre = 4;
@@ -475,15 +475,11 @@ __device__ __forceinline__ void resolve_hit(const FrameArgs &fa, const SceneArgs
     const bool several = info & (1 << 9);
     if (several) {
         reinterpret_cast<float *>(wa.rec + slot)[3] = sc;
-#ifdef RT_ACQREL_COUNTDOWN
-        // release our coefficient, acquire the others' (the last sampler reads them)
+        // release our coefficient, acquire the others' (the last sampler reads
+        // them): one acq_rel countdown instead of two sequentially consistent
+        // fences around a relaxed one (C2 2.5% faster)
         cuda::atomic_ref<int, cuda::thread_scope_device> pend(wa.pend[lp]);
         if (pend.fetch_sub(1, cuda::memory_order_acq_rel) != 1) return;
-#else
-        __threadfence();
-        if (atomicSub(wa.pend + lp, 1) != 1) return;
-        __threadfence();
-#endif
     }
     const int m = info & 0xff;
     // records of a single-pending pixel do not change after the trace: the
@@ -648,10 +644,7 @@ __device__ __forceinline__ unsigned conic_blocked2(const Conic2 &c, float4 ab, f
 // table in shared memory by fused_sample for up to kPairSamples samples; an
 // odd count's last pair is padded with rho = -inf, which never blocks.
 constexpr int kPairSamples = 1024;
-#ifndef RT_PAIR_UNROLL
-#define RT_PAIR_UNROLL 2
-#endif
-constexpr int kPairUnroll = RT_PAIR_UNROLL;
+constexpr int kPairUnroll = 4;  // (2: C2 2.5% slower)
 struct SamplePairs {
     const float4 *ab;
     const float2 *rho;

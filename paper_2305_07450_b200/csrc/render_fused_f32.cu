@@ -203,8 +203,11 @@ __device__ __forceinline__ int conic_entry(const ParamScene<MAXS> &ps, const Wav
 // --- A ----------------------------------------------------------------------------
 // 8 resident CTAs (64 registers) for unclustered scenes: 1.5-3.5% faster at
 // C2-C4; the clustered variant needs its registers (6 CTAs; 8 costs C5 10%)
+#ifndef RT_TRACE_MIN_BLOCKS
+#define RT_TRACE_MIN_BLOCKS 8  // 7 (72 registers): 2-3% slower; 9 (56, spills): equal
+#endif
 template <int MAXS>
-__global__ void __launch_bounds__(kThreads, MAXS <= 8 ? 8 : 6)
+__global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_TRACE_MIN_BLOCKS : 6)
     fused_trace(const FrameArgs fa, const SceneArgs<float> sa, const WaveArgs wa, const ParamScene<MAXS> ps) {
     constexpr int kWords = (MAXS + 31) / 32;
     constexpr bool kBundle = ParamScene<MAXS>::kClustered;

@@ -139,7 +139,12 @@ int rt_sky_sample_v1(rt_ctx *ctx, const double *dirs, int64_t n, double *out_rgb
 
 /* Page-lock and map a host framebuffer: rt_render_v1 then writes it directly
  * from the kernels (option "zero_copy") or copies into it at PCIe speed.
- * The caller keeps the memory alive until unregistered. */
+ * The caller keeps the memory alive until unregistered.  Returns
+ * RT_ALREADY_REGISTERED (> 0, not an error) when the range is already
+ * page-locked by someone else — the caller then must not unregister it.  A
+ * failed registration leaves no CUDA error pending.  ctx may be NULL (the
+ * registration is process-wide: portable + mapped). */
+#define RT_ALREADY_REGISTERED 1
 int rt_host_register(rt_ctx *ctx, void *ptr, size_t bytes);
 int rt_host_unregister(rt_ctx *ctx, void *ptr);
 

@@ -42,6 +42,18 @@ static _Thread_local long long *g_cnt;
 #define GRAZE_EPS 1e-7
 #define MAX_BOUNCE_LIMIT 31
 
+/* Precision probe build (-DRTO_ROUND=mask, tools/precision_probe.py only; the
+ * pinned oracle never defines it): round chosen intermediates to float32 to
+ * measure how sensitive the frame is to each — 1 primary direction, 2 hit
+ * point and normal, 4 shadow origin and sample directions, 8 reflected
+ * direction and origin, 16 shadow origin only, 32 the shading vectors. */
+#ifdef RTO_ROUND
+static inline double rf(double x) { return (double)(float)x; }
+#define RND(bit, v) ((RTO_ROUND & (bit)) ? (v3){rf((v).x), rf((v).y), rf((v).z)} : (v))
+#else
+#define RND(bit, v) (v)
+#endif
+
 static double golden_angle(void) { return M_PI * (3.0 - sqrt(5.0)); } /* shading.py:29 */
 
 static inline v3 mk(double x, double y, double z) { v3 r = {x, y, z}; return r; }
@@ -183,6 +195,7 @@ static double shadow_coeff(const scene_t *s, v3 surface, v3 normal) {
     int n = s->samples;
     v3 origin = mk(surface.x + SHADOW_EPS * normal.x, surface.y + SHADOW_EPS * normal.y,
                    surface.z + SHADOW_EPS * normal.z);
+    origin = RND(4 | 16, origin);
     v3 bu, bv;
     if (n > 1) {
         v3 axis = vnormalize(vsub(surface, s->light_pos));
@@ -194,7 +207,7 @@ static double shadow_coeff(const scene_t *s, v3 surface, v3 normal) {
     int unblocked = 0;
     for (int i = 0; i < n; i++) {
         v3 sp = (n == 1) ? s->light_pos : disc_point(i, n, s->light_pos, s->light_radius, bu, bv, s->ga);
-        v3 dir = vnormalize(vsub(sp, origin));
+        v3 dir = RND(4, vnormalize(vsub(sp, origin)));
         double limit = vdistance(surface, sp);
         CNT(C_SH_RAYS);
         if (!occluded(s, origin, dir, limit)) unblocked += 1;
@@ -274,21 +287,25 @@ static v3 trace(const scene_t *s, v3 origin, v3 dir) {
             normal = vnormalize(vsub(hit, mk(s->pos[3 * idx], s->pos[3 * idx + 1], s->pos[3 * idx + 2])));
         else
             normal = mk(0.0, 1.0, 0.0);
+        hit = RND(2, hit);
+        normal = RND(2, normal);
         v3 view = mk(-dir.x, -dir.y, -dir.z);
         v3 to_light = vnormalize(vsub(s->light_pos, hit));
         double sc = shadow_coeff(s, hit, normal);
         rec_t *r = &stack[m++];
         r->base = mk(s->col[3 * idx], s->col[3 * idx + 1], s->col[3 * idx + 2]);
         r->rr = s->refl[idx] / s->max_refl;
-        r->n = normal;
-        r->view = view;
-        r->l = to_light;
+        r->n = RND(32, normal);
+        r->view = RND(32, view);
+        r->l = RND(32, to_light);
         r->sc = sc;
         r->refl = s->refl[idx];
         if (k == s->bounces) { exhausted = 1; break; }
         CNT(C_REFL);
         origin = mk(hit.x + REFLECT_EPS * normal.x, hit.y + REFLECT_EPS * normal.y, hit.z + REFLECT_EPS * normal.z);
         dir = vreflect(dir, normal);
+        origin = RND(8, origin);
+        dir = RND(8, dir);
     }
     if (m == 0) return tail;
     v3 col;
@@ -371,7 +388,7 @@ int rto_render(uint32_t *pixels, double *radiance, int w, int h, const double *c
     for (int ri = 0; ri < nrows; ri++) {
         int y = row0 + ri * row_step;
         for (int x = 0; x < w; x++) {
-            v3 d = primary_direction((double)x, (double)y, (double)w, (double)h, cb, sb, ca, sa, vdist);
+            v3 d = RND(1, primary_direction((double)x, (double)y, (double)w, (double)h, cb, sb, ca, sa, vdist));
             CNT(C_PIX);
             v3 c = trace(&s, cam, d);
             size_t idx = (size_t)x + (size_t)y * (size_t)w;

@@ -11,6 +11,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
+import weakref
 
 import numpy as np
 
@@ -23,6 +24,7 @@ RT_ERR_CUDA = -2
 RT_ERR_NO_DEVICE = -3
 RT_ERR_NOMEM = -4
 RT_ERR_LIMIT = -5
+RT_ALREADY_REGISTERED = 1
 RT_PREC_FP32 = 0
 RT_PREC_FP64 = 1
 PRECISIONS = {"fp32": RT_PREC_FP32, "fp64": RT_PREC_FP64}
@@ -132,17 +134,10 @@ class Context:
         arr = (_i32 * len(self.devices))(*self.devices)
         check(lib.rt_ctx_create(ctypes.byref(h), arr, len(self.devices)), "rt_ctx_create")
         self.handle = h
-        self._registered = {}  # id(array) -> array (kept alive while pinned)
-        self._reg_order = []
-        self._addr = {}  # id(array) -> data address of a pinned array
 
     def close(self):
         if getattr(self, "handle", None):
-            lib = load()
-            for a in list(self._registered.values()):
-                lib.rt_host_unregister(self.handle, ptr(a))
-            self._registered.clear()
-            lib.rt_ctx_destroy(self.handle)
+            load().rt_ctx_destroy(self.handle)
             self.handle = None
 
     def __del__(self):
@@ -151,43 +146,18 @@ class Context:
         except Exception:
             pass
 
-    # -- pinned host framebuffers ------------------------------------------------
+    # -- pinned host framebuffers (the process-wide registry, _PINS) ------------
     def pin(self, arr: np.ndarray, max_pinned: int = 4) -> bool:
-        """Page-lock `arr` (kept alive while pinned) so the frame copy runs at
-        PCIe speed; the oldest pinned buffer is released beyond `max_pinned`."""
-        key = id(arr)
-        if key in self._registered and self._registered[key] is arr:
-            return True
-        lib = load()
-        if lib.rt_host_register(self.handle, ptr(arr), arr.nbytes) != RT_OK:
-            return False
-        self._registered[key] = arr
-        self._addr[key] = arr.__array_interface__["data"][0]
-        self._reg_order.append(key)
-        while len(self._reg_order) > max_pinned:
-            old = self._reg_order.pop(0)
-            a = self._registered.pop(old, None)
-            self._addr.pop(old, None)
-            if a is not None:
-                lib.rt_host_unregister(self.handle, ptr(a))
-        return True
+        """Page-lock `arr` so the frame copy runs at PCIe speed (see _Pins)."""
+        return _PINS.pin(arr, max_pinned)
 
     def address(self, arr: np.ndarray) -> int:
-        """Device-visible host address of `arr` (cached for pinned framebuffers)."""
-        hit = self._registered.get(id(arr))
-        if hit is arr:
-            return self._addr[id(arr)]
+        """Device-visible host address of `arr` (mapped: the host address)."""
         return arr.__array_interface__["data"][0]
 
     def unpin(self, arr: np.ndarray) -> None:
         """Release a buffer page-locked by pin()."""
-        key = id(arr)
-        if self._registered.get(key) is arr:
-            load().rt_host_unregister(self.handle, ptr(arr))
-            del self._registered[key]
-            self._addr.pop(key, None)
-            if key in self._reg_order:
-                self._reg_order.remove(key)
+        _PINS.unpin(arr)
 
     def set_option(self, name: str, value) -> None:
         check(load().rt_set_option(self.handle, name.encode(), int(value)), "rt_set_option")
@@ -221,6 +191,101 @@ class Context:
         check(load().rt_launch_count(self.handle, ctypes.byref(v)), "rt_launch_count")
         return int(v.value)
 
+
+class _Pins:
+    """Process-wide registry of page-locked host framebuffers.
+
+    A registration (cudaHostRegister, portable + mapped) belongs to the
+    process, not to a context, so one registry serves render_frame,
+    FramePipeline and the frame encoders alike:
+
+    * it holds only a weak reference: when the caller drops a framebuffer its
+      pages are unlocked (weakref callback, before numpy frees the memory) —
+      nothing is retained;
+    * at most `max_pinned` live buffers stay locked, least recently used
+      first out — but never one that is `hold()`-ed (a device-to-host copy
+      into it is in flight: FramePipeline / PipelinedFrameEncoder);
+    * a range some other code already page-locked (RT_ALREADY_REGISTERED) is
+      used as is and never unregistered here.
+    """
+
+    def __init__(self):
+        self._lock = threading.RLock()
+        self._entries = {}  # address -> [weakref, nbytes, holds, owned]
+        self._order = []    # addresses, least recently used first
+
+    def _drop(self, addr):
+        e = self._entries.pop(addr, None)
+        if addr in self._order:
+            self._order.remove(addr)
+        if e is not None and e[3]:
+            load().rt_host_unregister(None, ctypes.c_void_p(addr))
+
+    def _finalize(self, addr, ref):
+        with self._lock:
+            e = self._entries.get(addr)
+            if e is not None and e[0] is ref:
+                self._drop(addr)
+
+    def pin(self, arr: np.ndarray, max_pinned: int = 4) -> bool:
+        addr = arr.__array_interface__["data"][0]
+        with self._lock:
+            e = self._entries.get(addr)
+            if e is not None:
+                if e[0]() is arr and e[1] >= arr.nbytes:
+                    self._order.remove(addr)
+                    self._order.append(addr)
+                    return True
+                if e[2] == 0:
+                    self._drop(addr)  # a different or larger array now lives here
+                else:
+                    return False
+            rc = load().rt_host_register(None, ptr(arr), arr.nbytes)
+            if rc < 0:
+                return False
+            ref = weakref.ref(arr, lambda r, a=addr: self._finalize(a, r))
+            self._entries[addr] = [ref, arr.nbytes, 0, rc == RT_OK]
+            self._order.append(addr)
+            for old in list(self._order):
+                if len(self._order) <= max_pinned:
+                    break
+                if old != addr and self._entries[old][2] == 0:
+                    self._drop(old)
+            return True
+
+    def unpin(self, arr: np.ndarray) -> None:
+        addr = arr.__array_interface__["data"][0]
+        with self._lock:
+            e = self._entries.get(addr)
+            if e is not None and e[0]() is arr:
+                if e[2] > 0:
+                    raise RuntimeError("framebuffer has a copy in flight: wait for it before unpinning")
+                self._drop(addr)
+
+    def hold(self, arr: np.ndarray) -> None:
+        """Mark a copy into `arr` in flight: it is not evicted until release()."""
+        with self._lock:
+            e = self._entries.get(arr.__array_interface__["data"][0])
+            if e is not None:
+                e[2] += 1
+
+    def release(self, arr: np.ndarray) -> None:
+        with self._lock:
+            e = self._entries.get(arr.__array_interface__["data"][0])
+            if e is not None and e[2] > 0:
+                e[2] -= 1
+
+    def pinned(self, arr: np.ndarray) -> bool:
+        with self._lock:
+            e = self._entries.get(arr.__array_interface__["data"][0])
+            return e is not None and e[0]() is arr
+
+    def count(self) -> int:
+        with self._lock:
+            return len(self._entries)
+
+
+_PINS = _Pins()
 
 _contexts = {}
 _ctx_lock = threading.Lock()

@@ -138,6 +138,7 @@ class ShmFrame:
         self.ctx = ctx
         if not ctx.pin(self.pixels):
             raise _native.NativeError("could not page-lock the shared host frame")
+        _native._PINS.hold(self.pixels)  # every rank copies into it: never evicted
 
     def copy_rows(self, d_frame, part: int, n_parts: int, stream=None, block_rows: int = BLOCK_ROWS):
         lib = _native.load()
@@ -148,6 +149,7 @@ class ShmFrame:
     def close(self):
         if self.shm is None:
             return
+        _native._PINS.release(self.pixels)
         self.ctx.unpin(self.pixels)
         self.pixels = None
         self.shm.close()

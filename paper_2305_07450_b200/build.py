@@ -26,7 +26,8 @@ COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", 
 HOST_CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else None
 
 SOURCES = {
-    "rt_host.cu": [],
+    # host side: the skybox check splits its compare over OpenMP threads
+    "rt_host.cu": ["-Xcompiler", "-fopenmp"],
     # FP32 product path: flush denormals, approximate sqrt/div (powf, atan2f
     # and asinf stay full precision: no --use_fast_math)
     "render_f32.cu": ["--ftz=true", "--prec-div=false", "--prec-sqrt=false"],
@@ -48,21 +49,26 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = False, defines=(), out=None) -> str:
+def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = False, defines=(), out=None,
+          f32_flags=None) -> str:
     """Compile (incrementally) and link libb200rt.so.  `defines` (e.g.
-    ["RT_F32_MIN_BLOCKS=6"]) and `out` build an experimental variant into a
-    separate object directory."""
+    ["RT_F32_MIN_BLOCKS=6"]), `f32_flags` (replacing the FP32 sources' own
+    flags) and `out` build an experimental variant into a separate object
+    directory."""
     if not os.path.exists(NVCC) and shutil.which("nvcc") is None:
         raise RuntimeError("nvcc not found: cannot build libb200rt.so")
     nvcc = NVCC if os.path.exists(NVCC) else shutil.which("nvcc")
     lib = out or LIB
-    bdir = BUILD if not defines else os.path.join(BUILD, "v_" + "_".join(d.replace("=", "") for d in defines))
+    tag = [d.replace("=", "") for d in defines] + [f.strip("-").replace("=", "") for f in (f32_flags or [])]
+    bdir = BUILD if not tag else os.path.join(BUILD, "v_" + "_".join(tag))
     os.makedirs(bdir, exist_ok=True)
     dflags = [f"-D{d}" for d in defines]
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
     headers.append(os.path.join(INCLUDE, "b200rt.h"))
     objs, cmds = [], []
     for src, extra in SOURCES.items():
+        if f32_flags is not None and "f32" in src:
+            extra = list(f32_flags)
         s = os.path.join(CSRC, src)
         o = os.path.join(bdir, src.replace(".cu", ".o"))
         objs.append(o)
@@ -83,11 +89,11 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
                     sys.stderr.write(r.stderr.decode(errors="replace"))
                 raise subprocess.CalledProcessError(r.returncode, r.args)
     if force or _stale(lib, objs):
-        cmd = [nvcc, *_ccbin(), *ARCH, "-shared", "-o", lib, *objs]
+        cmd = [nvcc, *_ccbin(), *ARCH, "-shared", "-o", lib, *objs, "-lgomp"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-    if not defines:
+    if not tag:
         build_pyfast(verbose, force)
     return lib
 
@@ -115,5 +121,6 @@ def build_pyfast(verbose: bool = False, force: bool = False):
 if __name__ == "__main__":
     defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
     outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    f32 = [a[6:] for a in sys.argv[1:] if a.startswith("--f32=")]
     print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, ptxas_verbose="--ptxas" in sys.argv,
-                defines=defs, out=outs[0] if outs else None))
+                defines=defs, out=outs[0] if outs else None, f32_flags=f32[0].split() if f32 else None))

@@ -13,6 +13,8 @@
 #include <string>
 #include <vector>
 
+#include <omp.h>
+
 #include "b200rt.h"
 #include "rt_device.cuh"
 
@@ -63,10 +65,10 @@ struct HostScene {
     double light[3] = {0, 0, 0}, light_radius = 1, lc[3] = {1, 1, 1}, ambient = 0.15, max_refl = 128;
     std::vector<char> key;  // bytes compared to detect a changed scene
     uint64_t version = 0;
-    // skybox identity
+    // skybox: the caller's array and the copy of its texels last uploaded
     const float *sky_ptr = nullptr;
     int sky_w = 1, sky_h = 1, has_sky = 0;
-    uint64_t sky_sig = 0;
+    std::vector<float> sky_shadow;
     uint64_t sky_version = 0;
 };
 
@@ -114,6 +116,10 @@ struct Dev {
     DBuf slot_frame[kSlots];
     cudaEvent_t slot_comp[kSlots] = {}, slot_done[kSlots] = {};
     bool slot_busy[kSlots] = {};
+    // rt_render_device_v1 on caller streams: the end of the last call's
+    // kernels, and the end of this call's uploads
+    cudaEvent_t dev_call_ev = nullptr, dev_prep_ev = nullptr;
+    bool dev_call_pending = false;
     DBuf grid;                        // the culled FP32 path's shadow grid (scene + light)
     uint64_t grid_version = ~0ull;
     rt::WaveArgs grid_wa = {};        // its box and dims (grid null: none)
@@ -172,6 +178,7 @@ struct rt_ctx {
     bool band_times = false;  // time each band's kernels and copy (rt_band_times_ms)
     float band_ms[2 * kMaxBands] = {};
     int band_count = 0;
+    int band_pending = 0;     // bands of the frame enqueued by enqueue_frame (0: one stream)
     bool phases = false;      // record per-phase events in wavefront frames (rt_phase_ms)
     int rgba = 0;             // pixel byte order of the frames written (0 B,G,R,A / 1 R,G,B,A)
     bool conic = true;        // culled FP32 path: silhouette form of the soft-shadow sphere test
@@ -202,24 +209,56 @@ std::vector<double> disc_table(int n, double radius) {
     return t;
 }
 
-uint64_t fnv1a(const void *data, size_t n, uint64_t h = 1469598103934665603ull) {
-    const unsigned char *p = (const unsigned char *)data;
-    for (size_t i = 0; i < n; i++) h = (h ^ p[i]) * 1099511628211ull;
-    return h;
+// The skybox is read by the reference on every frame (renderer.py:282-300),
+// so an in-place edit of its texels must show in the next frame.  The
+// library keeps a host copy of the texels it uploaded (`sky_shadow`) and
+// compares the caller's array with it in full, bit for bit, on every frame
+// that reuses the same array: exact, and split over up to kSkyThreads host
+// threads (25 MB: ~0.2-0.35 ms on 8 cores of the B200 host,
+// tools/micro/host_compare.c).  rt_render_v1 runs the compare while the
+// frame's kernels execute (the frame is rendered with the device copy); a
+// difference re-uploads the sky and renders the frame again before the call
+// returns.
+int sky_threads() {
+    static int t = [] {
+        if (const char *e = std::getenv("B200RT_SKY_THREADS")) return std::max(1, std::atoi(e));
+        return std::max(1, std::min(8, omp_get_num_procs() / 2));
+    }();
+    return t;
 }
 
-// Cheap identity of a skybox: dimensions, first/last rows and a strided
-// sample of texels (a full hash of a 25 MB panorama would cost ~10 ms/frame).
-uint64_t sky_signature(const float *sky, int w, int h) {
-    size_t n = (size_t)w * h * 3;
-    uint64_t s = fnv1a(&w, sizeof w);
-    s = fnv1a(&h, sizeof h, s);
-    size_t row = (size_t)w * 3;
-    s = fnv1a(sky, sizeof(float) * std::min(row, n), s);
-    s = fnv1a(sky + (n - std::min(row, n)), sizeof(float) * std::min(row, n), s);
-    size_t stride = std::max<size_t>(1, n / 4099);
-    for (size_t i = 0; i < n; i += stride) s = fnv1a(sky + i, sizeof(float), s);
-    return s;
+// true when a and b differ anywhere (n floats, bitwise)
+bool texels_differ(const float *a, const float *b, size_t n) {
+    const size_t bytes = sizeof(float) * n;
+    const int chunks = 4 * sky_threads();
+    int diff = 0;
+#pragma omp parallel for num_threads(sky_threads()) schedule(static) reduction(| : diff)
+    for (int k = 0; k < chunks; k++) {
+        const size_t lo = bytes * k / chunks, hi = bytes * (k + 1) / chunks;
+        diff |= std::memcmp((const char *)a + lo, (const char *)b + lo, hi - lo) != 0;
+    }
+    return diff != 0;
+}
+
+void copy_texels(float *dst, const float *src, size_t n) {
+    const size_t bytes = sizeof(float) * n;
+    const int chunks = 4 * sky_threads();
+#pragma omp parallel for num_threads(sky_threads()) schedule(static)
+    for (int k = 0; k < chunks; k++) {
+        const size_t lo = bytes * k / chunks, hi = bytes * (k + 1) / chunks;
+        std::memcpy((char *)dst + lo, (const char *)src + lo, hi - lo);
+    }
+}
+
+// The caller's texels (same array as the last frame's) against the uploaded
+// copy; on a difference the copy is refreshed and the sky version bumped.
+bool sky_content_changed(HostScene &s) {
+    if (!s.has_sky || !s.sky_ptr) return false;
+    const size_t n = (size_t)s.sky_w * s.sky_h * 3;
+    if (!texels_differ(s.sky_ptr, s.sky_shadow.data(), n)) return false;
+    copy_texels(s.sky_shadow.data(), s.sky_ptr, n);
+    s.sky_version++;
+    return true;
 }
 
 int validate_scene(int32_t n_bodies, const int32_t *kinds, const double *positions, const double *sizes,
@@ -238,7 +277,9 @@ int validate_scene(int32_t n_bodies, const int32_t *kinds, const double *positio
     return RT_OK;
 }
 
-void set_host_scene(HostScene &s, int32_t n, const int32_t *kinds, const double *positions, const double *sizes,
+// Returns true when the frame reuses the last frame's sky array, whose
+// content the caller must still compare (sky_content_changed).
+bool set_host_scene(HostScene &s, int32_t n, const int32_t *kinds, const double *positions, const double *sizes,
                     const double *colors, const double *refls, const double *light_pos, double light_radius,
                     const double *light_color, double ambient, double max_refl, const float *sky, int32_t sky_w,
                     int32_t sky_h, int32_t has_sky) {
@@ -290,15 +331,25 @@ void set_host_scene(HostScene &s, int32_t n, const int32_t *kinds, const double 
         s.max_refl = max_refl;
         s.version++;
     }
-    uint64_t sig = has_sky ? sky_signature(sky, sky_w, sky_h) : 0;
-    if (has_sky != s.has_sky || sky != s.sky_ptr || sky_w != s.sky_w || sky_h != s.sky_h || sig != s.sky_sig) {
+    // a different array (or none): a new sky, uploaded from a fresh copy;
+    // the same array: its content is compared in full (sky_content_changed)
+    if (has_sky != s.has_sky || (has_sky && (sky != s.sky_ptr || sky_w != s.sky_w || sky_h != s.sky_h))) {
         s.has_sky = has_sky;
         s.sky_ptr = has_sky ? sky : nullptr;
         s.sky_w = has_sky ? sky_w : 1;
         s.sky_h = has_sky ? sky_h : 1;
-        s.sky_sig = sig;
+        if (has_sky) {
+            const size_t n = (size_t)sky_w * sky_h * 3;
+            s.sky_shadow.resize(n);
+            copy_texels(s.sky_shadow.data(), sky, n);
+        } else {
+            s.sky_shadow.clear();
+            s.sky_shadow.shrink_to_fit();
+        }
         s.sky_version++;
+        return false;
     }
+    return has_sky != 0;
 }
 
 template <typename R>
@@ -342,7 +393,7 @@ int upload_sky(rt_ctx *ctx, Dev &d) {
     if (s.has_sky) {
         int64_t n = (int64_t)s.sky_w * s.sky_h;
         if ((rc = d.sky_raw.ensure(sizeof(float) * 3 * n)) || (rc = d.sky.ensure(sizeof(float4) * n))) return rc;
-        RT_CK(cudaMemcpyAsync(d.sky_raw.p, s.sky_ptr, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, d.st));
+        RT_CK(cudaMemcpyAsync(d.sky_raw.p, s.sky_shadow.data(), sizeof(float) * 3 * n, cudaMemcpyHostToDevice, d.st));
         sky_to_float4<<<(unsigned)((n + 255) / 256), 256, 0, d.st>>>((const float *)d.sky_raw.p, (float4 *)d.sky.p,
                                                                    n);
         RT_CK(cudaGetLastError());
@@ -747,6 +798,8 @@ int rt_ctx_create(rt_ctx **out, const int32_t *devices, int32_t n_devices) {
                   cudaEventCreate(&d.e0) == cudaSuccess && cudaEventCreate(&d.e1) == cudaSuccess;
         for (auto &ev : d.band_ev) ok = ok && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess;
         ok = ok && cudaEventCreateWithFlags(&d.fork_ev, cudaEventDisableTiming) == cudaSuccess;
+        ok = ok && cudaEventCreateWithFlags(&d.dev_call_ev, cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&d.dev_prep_ev, cudaEventDisableTiming) == cudaSuccess;
         for (auto &ev : d.tl_ev) ok = ok && cudaEventCreate(&ev) == cudaSuccess;
         for (int k = 0; ok && k < Dev::kSlots; k++)
             ok = cudaEventCreateWithFlags(&d.slot_comp[k], cudaEventDisableTiming) == cudaSuccess &&
@@ -787,6 +840,8 @@ int rt_ctx_destroy(rt_ctx *ctx) {
         for (auto bs : d.band_st)
             if (bs) cudaStreamDestroy(bs);
         if (d.fork_ev) cudaEventDestroy(d.fork_ev);
+        if (d.dev_call_ev) cudaEventDestroy(d.dev_call_ev);
+        if (d.dev_prep_ev) cudaEventDestroy(d.dev_prep_ev);
         for (auto ev : d.tl_ev)
             if (ev) cudaEventDestroy(ev);
         for (int k = 0; k < Dev::kSlots; k++) {
@@ -812,8 +867,9 @@ int rt_set_scene_v1(rt_ctx *ctx, int32_t n_bodies, const int32_t *kinds, const d
                             sky_w, sky_h, has_sky);
     if (rc) return rc;
     std::lock_guard<std::mutex> lk(ctx->mu);
-    set_host_scene(ctx->scene, n_bodies, kinds, positions, sizes, colors, refls, light_pos, light_radius, light_color,
-                   ambient, max_refl, sky, sky_w, sky_h, has_sky);
+    if (set_host_scene(ctx->scene, n_bodies, kinds, positions, sizes, colors, refls, light_pos, light_radius,
+                       light_color, ambient, max_refl, sky, sky_w, sky_h, has_sky))
+        sky_content_changed(ctx->scene);
     for (Dev &d : ctx->devs) {
         RT_CK(cudaSetDevice(d.id));
         if ((rc = upload_sky(ctx, d))) return rc;
@@ -821,23 +877,15 @@ int rt_set_scene_v1(rt_ctx *ctx, int32_t n_bodies, const int32_t *kinds, const d
     return RT_OK;
 }
 
-int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, int32_t height,
-                 const double cam_pos[3], double yaw, double pitch, double vdist, int32_t n_bodies,
-                 const int32_t *kinds, const double *positions, const double *sizes, const double *colors,
-                 const double *refls, const double light_pos[3], double light_radius, const double light_color[3],
-                 double ambient, double max_refl, const float *sky, int32_t sky_w, int32_t sky_h, int32_t has_sky,
-                 int32_t shadow_samples, int32_t bounce_limit, int32_t n_parts, int32_t precision) {
-    if (!ctx || !pixels || !cam_pos) return fail(RT_ERR_INVALID, "null argument");
-    int rc = check_frame_args(width, height, shadow_samples, bounce_limit, precision);
-    if (rc) return rc;
-    if ((rc = validate_scene(n_bodies, kinds, positions, sizes, colors, refls, light_pos, light_color, max_refl, sky,
-                             sky_w, sky_h, has_sky)))
-        return rc;
-    if (n_parts < 1) n_parts = 1;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    set_host_scene(ctx->scene, n_bodies, kinds, positions, sizes, colors, refls, light_pos, light_radius, light_color,
-                   ambient, max_refl, sky, sky_w, sky_h, has_sky);
-    const int n_dev = std::min<int>((int)ctx->devs.size(), n_parts);
+}  // extern "C"
+
+namespace {
+
+// Enqueue one frame of rt_render_v1 on n_dev devices (no wait).
+int enqueue_frame(rt_ctx *ctx, int n_dev, uint32_t *pixels, void *radiance, int32_t width, int32_t height,
+                  const double cam_pos[3], double yaw, double pitch, double vdist, int32_t shadow_samples,
+                  int32_t bounce_limit, int32_t n_parts, int32_t precision) {
+    int rc;
     const int block_rows = RT_DEFAULT_BLOCK_ROWS;
     const size_t px_bytes = sizeof(uint32_t) * (size_t)width * height;
     const size_t rad_elem = precision == RT_PREC_FP64 ? sizeof(double) : sizeof(float);
@@ -870,8 +918,7 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
                 if ((rc = launch_frame(ctx, d, fa, precision, d.st))) return rc;
             }
             RT_CK(cudaEventRecord(d.e1, d.st));
-            RT_CK(cudaStreamSynchronize(d.st));
-            RT_CK(cudaEventElapsedTime(&ctx->last_ms, d.e0, d.e1));
+            ctx->band_pending = 0;
             return RT_OK;
         }
         cudaGetLastError();  // not registered: a cudaHostGetDevicePointer miss is not an error
@@ -931,14 +978,7 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
             if (ctx->band_times) RT_CK(cudaEventRecord(d.tl_ev[kMaxBands + k], d.copy_st));
         }
         RT_CK(cudaEventRecord(d.e1, d.st));
-        RT_CK(cudaStreamSynchronize(d.copy_st));
-        RT_CK(cudaStreamSynchronize(d.st));
-        RT_CK(cudaEventElapsedTime(&ctx->last_ms, d.e0, d.e1));
-        ctx->band_count = ctx->band_times ? bands : 0;
-        for (int k = 0; k < ctx->band_count; k++) {
-            RT_CK(cudaEventElapsedTime(&ctx->band_ms[k], d.e0, d.tl_ev[k]));
-            RT_CK(cudaEventElapsedTime(&ctx->band_ms[kMaxBands + k], d.e0, d.tl_ev[kMaxBands + k]));
-        }
+        ctx->band_pending = bands;
         return RT_OK;
     }
     // several devices: partition p runs on device p % n_dev, each device
@@ -967,14 +1007,63 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
                 return rc;
         }
     }
+    ctx->band_pending = 0;
+    return RT_OK;
+}
+
+
+// Wait for the frame enqueued by enqueue_frame; its device time and band times.
+int finish_frame(rt_ctx *ctx, int n_dev) {
     for (int g = 0; g < n_dev; g++) {
         Dev &d = ctx->devs[g];
         RT_CK(cudaSetDevice(d.id));
+        if (n_dev == 1) RT_CK(cudaStreamSynchronize(d.copy_st));
         RT_CK(cudaStreamSynchronize(d.st));
     }
-    RT_CK(cudaSetDevice(ctx->devs[0].id));
-    RT_CK(cudaEventElapsedTime(&ctx->last_ms, ctx->devs[0].e0, ctx->devs[0].e1));
+    Dev &d = ctx->devs[0];
+    RT_CK(cudaSetDevice(d.id));
+    RT_CK(cudaEventElapsedTime(&ctx->last_ms, d.e0, d.e1));
+    ctx->band_count = (n_dev == 1 && ctx->band_times) ? ctx->band_pending : 0;
+    for (int k = 0; k < ctx->band_count; k++) {
+        RT_CK(cudaEventElapsedTime(&ctx->band_ms[k], d.e0, d.tl_ev[k]));
+        RT_CK(cudaEventElapsedTime(&ctx->band_ms[kMaxBands + k], d.e0, d.tl_ev[kMaxBands + k]));
+    }
     return RT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, int32_t height,
+                 const double cam_pos[3], double yaw, double pitch, double vdist, int32_t n_bodies,
+                 const int32_t *kinds, const double *positions, const double *sizes, const double *colors,
+                 const double *refls, const double light_pos[3], double light_radius, const double light_color[3],
+                 double ambient, double max_refl, const float *sky, int32_t sky_w, int32_t sky_h, int32_t has_sky,
+                 int32_t shadow_samples, int32_t bounce_limit, int32_t n_parts, int32_t precision) {
+    if (!ctx || !pixels || !cam_pos) return fail(RT_ERR_INVALID, "null argument");
+    int rc = check_frame_args(width, height, shadow_samples, bounce_limit, precision);
+    if (rc) return rc;
+    if ((rc = validate_scene(n_bodies, kinds, positions, sizes, colors, refls, light_pos, light_color, max_refl, sky,
+                             sky_w, sky_h, has_sky)))
+        return rc;
+    if (n_parts < 1) n_parts = 1;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    const bool verify_sky = set_host_scene(ctx->scene, n_bodies, kinds, positions, sizes, colors, refls, light_pos,
+                                           light_radius, light_color, ambient, max_refl, sky, sky_w, sky_h, has_sky);
+    const int n_dev = std::min<int>((int)ctx->devs.size(), n_parts);
+    // The frame is enqueued with the device's copy of the sky; when the
+    // caller passed the same sky array as before, its texels are compared in
+    // full with that copy while the kernels run, and on a difference the sky
+    // is uploaded again and the frame rendered again.
+    for (int attempt = 0;; attempt++) {
+        if ((rc = enqueue_frame(ctx, n_dev, pixels, radiance, width, height, cam_pos, yaw, pitch, vdist,
+                                shadow_samples, bounce_limit, n_parts, precision)))
+            return rc;
+        if (attempt > 0 || !verify_sky || !sky_content_changed(ctx->scene)) break;
+        if ((rc = finish_frame(ctx, n_dev))) return rc;  // the stale frame ends before the sky is replaced
+    }
+    return finish_frame(ctx, n_dev);
 }
 
 int rt_render_device_v1(rt_ctx *ctx, int32_t slot, uint32_t *d_out, int64_t out_pitch, void *d_radiance,
@@ -990,8 +1079,19 @@ int rt_render_device_v1(rt_ctx *ctx, int32_t slot, uint32_t *d_out, int64_t out_
     if (out_pitch < width) return fail(RT_ERR_INVALID, "out_pitch < width");
     std::lock_guard<std::mutex> lk(ctx->mu);
     Dev &d = ctx->devs[slot];
-    if ((rc = prepare(ctx, d, precision, shadow_samples))) return rc;
+    RT_CK(cudaSetDevice(d.id));
     cudaStream_t st = stream ? (cudaStream_t)stream : d.st;
+    // Order this call after the previous one on the device whatever stream
+    // either used: the scene / grid uploads of prepare() (on d.st) must not
+    // overwrite buffers a previous frame's kernels still read, this frame's
+    // kernels must see them complete, and two frames never share the queues
+    // of wb[0] at the same time.
+    if (d.dev_call_pending) RT_CK(cudaStreamWaitEvent(d.st, d.dev_call_ev, 0));
+    if ((rc = prepare(ctx, d, precision, shadow_samples))) return rc;
+    if (st != d.st) {
+        RT_CK(cudaEventRecord(d.dev_prep_ev, d.st));
+        RT_CK(cudaStreamWaitEvent(st, d.dev_prep_ev, 0));
+    }
     rt::FrameArgs fa = frame_args(d_out, out_pitch, d_radiance, width, height, cam_pos, yaw, pitch, vdist,
                                   shadow_samples, bounce_limit, part, n_parts, block_rows);
     cudaPointerAttributes attr;
@@ -1001,7 +1101,10 @@ int rt_render_device_v1(rt_ctx *ctx, int32_t slot, uint32_t *d_out, int64_t out_
     } else {
         fa.peer_out = (attr.type != cudaMemoryTypeDevice || attr.device != d.id) ? 1 : 0;
     }
-    return launch_frame(ctx, d, fa, precision, st);
+    if ((rc = launch_frame(ctx, d, fa, precision, st))) return rc;
+    RT_CK(cudaEventRecord(d.dev_call_ev, st));
+    d.dev_call_pending = true;
+    return RT_OK;
 }
 
 int rt_trace_rays_v1(rt_ctx *ctx, const double *origins, const double *dirs, int64_t n_rays, void *out_rgb,
@@ -1018,8 +1121,9 @@ int rt_trace_rays_v1(rt_ctx *ctx, const double *origins, const double *dirs, int
                              sky_w, sky_h, has_sky)))
         return rc;
     std::lock_guard<std::mutex> lk(ctx->mu);
-    set_host_scene(ctx->scene, n_bodies, kinds, positions, sizes, colors, refls, light_pos, light_radius, light_color,
-                   ambient, max_refl, sky, sky_w, sky_h, has_sky);
+    if (set_host_scene(ctx->scene, n_bodies, kinds, positions, sizes, colors, refls, light_pos, light_radius,
+                       light_color, ambient, max_refl, sky, sky_w, sky_h, has_sky))
+        sky_content_changed(ctx->scene);
     if (n_rays == 0) return RT_OK;
     Dev &d = ctx->devs[0];
     if ((rc = prepare(ctx, d, precision, shadow_samples))) return rc;
@@ -1086,17 +1190,22 @@ int rt_sky_sample_v1(rt_ctx *ctx, const double *dirs, int64_t n, double *out_rgb
 }
 
 int rt_host_register(rt_ctx *ctx, void *ptr, size_t bytes) {
-    if (!ctx || !ptr || bytes == 0) return fail(RT_ERR_INVALID, "bad host range");
-    RT_CK(cudaSetDevice(ctx->devs[0].id));
-    RT_CK(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped));
-    return RT_OK;
+    if (!ptr || bytes == 0) return fail(RT_ERR_INVALID, "bad host range");
+    if (ctx) RT_CK(cudaSetDevice(ctx->devs[0].id));
+    cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped);
+    if (e == cudaSuccess) return RT_OK;
+    cudaGetLastError();  // leave no sticky error for the next launch check to report
+    if (e == cudaErrorHostMemoryAlreadyRegistered) return RT_ALREADY_REGISTERED;
+    return fail(RT_ERR_CUDA, std::string("cudaHostRegister: ") + cudaGetErrorString(e));
 }
 
 int rt_host_unregister(rt_ctx *ctx, void *ptr) {
-    if (!ctx || !ptr) return fail(RT_ERR_INVALID, "bad host pointer");
-    RT_CK(cudaSetDevice(ctx->devs[0].id));
-    RT_CK(cudaHostUnregister(ptr));
-    return RT_OK;
+    if (!ptr) return fail(RT_ERR_INVALID, "bad host pointer");
+    if (ctx) RT_CK(cudaSetDevice(ctx->devs[0].id));
+    cudaError_t e = cudaHostUnregister(ptr);
+    if (e == cudaSuccess) return RT_OK;
+    cudaGetLastError();
+    return fail(RT_ERR_CUDA, std::string("cudaHostUnregister: ") + cudaGetErrorString(e));
 }
 
 int rt_set_option(rt_ctx *ctx, const char *name, int32_t value) {
@@ -1225,22 +1334,28 @@ int rt_render_async_v1(rt_ctx *ctx, int32_t slot, uint32_t *pixels, int32_t widt
         RT_CK(cudaEventSynchronize(d.slot_done[slot]));
         d.slot_busy[slot] = false;
     }
-    set_host_scene(ctx->scene, n_bodies, kinds, positions, sizes, colors, refls, light_pos, light_radius, light_color,
-                   ambient, max_refl, sky, sky_w, sky_h, has_sky);
+    const bool verify_sky = set_host_scene(ctx->scene, n_bodies, kinds, positions, sizes, colors, refls, light_pos,
+                                           light_radius, light_color, ambient, max_refl, sky, sky_w, sky_h, has_sky);
     const size_t px_bytes = sizeof(uint32_t) * (size_t)width * height;
-    if ((rc = prepare(ctx, d, precision, shadow_samples))) return rc;
-    if ((rc = d.slot_frame[slot].ensure(px_bytes))) return rc;
     // the kernels on the frame stream (frames in order), the copy on the copy
-    // stream: the next frame's kernels overlap this frame's PCIe transfer
-    rt::FrameArgs fa = frame_args((uint32_t *)d.slot_frame[slot].p, width, nullptr, width, height, cam_pos, yaw, pitch,
-                                  vdist, shadow_samples, bounce_limit, 0, 1, RT_DEFAULT_BLOCK_ROWS);
-    RT_CK(cudaEventRecord(d.e0, d.st));
-    if ((rc = launch_frame(ctx, d, fa, precision, d.st))) return rc;
-    RT_CK(cudaEventRecord(d.e1, d.st));
-    RT_CK(cudaEventRecord(d.slot_comp[slot], d.st));
-    RT_CK(cudaStreamWaitEvent(d.copy_st, d.slot_comp[slot], 0));
-    RT_CK(cudaMemcpyAsync(pixels, d.slot_frame[slot].p, px_bytes, cudaMemcpyDeviceToHost, d.copy_st));
-    RT_CK(cudaEventRecord(d.slot_done[slot], d.copy_st));
+    // stream: the next frame's kernels overlap this frame's PCIe transfer.
+    // The sky is verified while the frame runs (as in rt_render_v1): on a
+    // difference the frame is enqueued again after the upload.
+    for (int attempt = 0;; attempt++) {
+        if ((rc = prepare(ctx, d, precision, shadow_samples))) return rc;
+        if ((rc = d.slot_frame[slot].ensure(px_bytes))) return rc;
+        rt::FrameArgs fa = frame_args((uint32_t *)d.slot_frame[slot].p, width, nullptr, width, height, cam_pos, yaw,
+                                      pitch, vdist, shadow_samples, bounce_limit, 0, 1, RT_DEFAULT_BLOCK_ROWS);
+        RT_CK(cudaEventRecord(d.e0, d.st));
+        if ((rc = launch_frame(ctx, d, fa, precision, d.st))) return rc;
+        RT_CK(cudaEventRecord(d.e1, d.st));
+        RT_CK(cudaEventRecord(d.slot_comp[slot], d.st));
+        RT_CK(cudaStreamWaitEvent(d.copy_st, d.slot_comp[slot], 0));
+        RT_CK(cudaMemcpyAsync(pixels, d.slot_frame[slot].p, px_bytes, cudaMemcpyDeviceToHost, d.copy_st));
+        RT_CK(cudaEventRecord(d.slot_done[slot], d.copy_st));
+        if (attempt > 0 || !verify_sky || !sky_content_changed(ctx->scene)) break;
+        RT_CK(cudaEventSynchronize(d.slot_done[slot]));  // the stale frame ends before the sky is replaced
+    }
     d.slot_busy[slot] = true;
     return RT_OK;
 }

@@ -165,8 +165,9 @@ class FramePipeline:
         self.precision = precision
         if _native.device_count() < 1:
             raise _native.NativeError("no CUDA device visible: the b200rt frame render has no CPU path")
-        # its own context (streams, pinned buffers): render_frame's pinning
-        # never unpins a buffer with a copy in flight here
+        # its own context (streams, frame slots); its framebuffers are held in
+        # the pin registry while their copies are in flight, so no other
+        # caller's pinning evicts them (_native._Pins)
         dev = int(os.environ.get("LOCAL_RANK", "0")) % _native.device_count()
         self.ctx = _native.Context((dev,))
         for k, v in _native.get_options().items():
@@ -208,13 +209,17 @@ class FramePipeline:
             )
             del keep
         _native.check(rc, "rt_render_async_v1")
+        _native._PINS.hold(pixels)
         self._pending[ticket] = out
         self._next += 1
         return ticket
 
     def wait(self, ticket: int):
         out = self._pending.pop(ticket)
-        _native.check(_native.load().rt_frame_wait_v1(self.ctx.handle, ticket % self.depth), "rt_frame_wait_v1")
+        try:
+            _native.check(_native.load().rt_frame_wait_v1(self.ctx.handle, ticket % self.depth), "rt_frame_wait_v1")
+        finally:
+            _native._PINS.release(out.pixels)
         return out
 
     def drain(self):

@@ -118,9 +118,11 @@ class PipelinedFrameEncoder:
             self.drain()
             for i in range(self.depth):
                 if self._bufs[i] is not None:
+                    _native._PINS.release(self._bufs[i])
                     self.ctx.unpin(self._bufs[i])
                 self._bufs[i] = np.zeros(HEADER.size + 4 * w * h, dtype=np.uint8)
                 self.ctx.pin(self._bufs[i], max_pinned=self.depth + 1)
+                _native._PINS.hold(self._bufs[i])  # copies land here while frames are in flight
             self._dims = (w, h)
         buf = self._bufs[slot]
         HEADER.pack_into(buf, 0, FRAME_MAGIC, frame_id & 0xFFFFFFFF, w, h, FORMAT_RGBA8)
@@ -149,4 +151,7 @@ class PipelinedFrameEncoder:
 
     def close(self):
         self.drain()
+        for b in self._bufs:
+            if b is not None:
+                _native._PINS.release(b)
         self.ctx.close()

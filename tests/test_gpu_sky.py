@@ -1,0 +1,90 @@
+"""The skybox is read by the reference on every frame (renderer.py:282-300):
+an in-place edit of `Skybox.texels` between two frames must show in the
+second frame.  The library compares the caller's array with its uploaded copy
+in full on every frame (rt_host.cu: sky_content_changed)."""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import parity
+import paper_2305_07450_b200 as rt
+from paper_2305_07450_b200 import FramePipeline
+
+pytestmark = pytest.mark.gpu
+
+W, H = 96, 54
+
+
+def _texel_of(d, sw, sh):
+    """renderer.py:60-74: the texel a unit direction samples."""
+    u = 0.5 + math.atan2(d[0], d[2]) / (2 * math.pi)
+    v = 0.5 - math.asin(max(-1.0, min(1.0, d[1]))) / math.pi
+    tx = int(math.floor(u * sw)) % sw
+    ty = min(max(int(math.floor(v * sh)), 0), sh - 1)
+    return tx, ty
+
+
+def _setup():
+    cfg = rt.CONFIGS["C3"]
+    scene, cam = cfg.scene(), cfg.camera()
+    sky = scene.skybox
+    # a sky pixel of the top row and the texel it samples, chosen so that its
+    # float index is not on the old sampled signature's stride (n / 4099)
+    n = sky.texels.size
+    stride = max(1, n // 4099)
+    xs = np.arange(W, dtype=np.int32)
+    dirs = oracle.primary_directions(xs, np.zeros(W, np.int32), W, H, cam.yaw, cam.pitch, cam.fov)
+    for x, d in zip(xs, dirs):
+        tx, ty = _texel_of(d, sky.width, sky.height)
+        i = (ty * sky.width + tx) * 3
+        if 0 < ty < sky.height - 1 and all((i + c) % stride for c in range(3)):
+            return scene, cam, rt.RenderParams(8, 2, W, H), int(x), tx, ty
+    raise AssertionError("no suitable sky pixel")
+
+
+def _want(scene, cam, params):
+    return oracle.render(vars(rt.pack_scene(scene)), cam.position, cam.yaw, cam.pitch, cam.fov, W, H,
+                         params.shadow_samples, params.bounce_limit)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_in_place_texel_edit_is_rendered(precision):
+    scene, cam, params, px, tx, ty = _setup()
+    sky = scene.skybox
+    fb = rt.Framebuffer.create(W, H)
+    rt.render_frame(scene, cam, params, fb, precision=precision)
+    before = fb.pixels.copy()
+    sky.texels[ty, tx] = (0.9, 0.05, 0.6)  # one texel, in place (same array)
+    want = _want(scene, cam, params)
+    assert want[px] != before[px], "the edited texel is visible at the chosen pixel"
+    rt.render_frame(scene, cam, params, fb, precision=precision)
+    if precision == "fp64":
+        np.testing.assert_array_equal(fb.pixels, want)
+    else:
+        parity.assert_byte_gate(fb.pixels, want, "sky edit")
+        assert fb.pixels[px] == want[px]
+    # and back: the original texel returns
+    sky.texels[ty, tx] = (tx / sky.width, ty / sky.height, 0.25)
+    rt.render_frame(scene, cam, params, fb, precision=precision)
+    np.testing.assert_array_equal(fb.pixels[px], before[px])
+
+
+def test_in_place_texel_edit_pipelined():
+    scene, cam, params, px, tx, ty = _setup()
+    sky = scene.skybox
+    pipe = FramePipeline(2)
+    try:
+        a, b = rt.Framebuffer.create(W, H), rt.Framebuffer.create(W, H)
+        ta = pipe.submit(scene, cam, params, a)
+        pipe.wait(ta)
+        sky.texels[ty, tx] = (0.05, 0.95, 0.1)
+        tb = pipe.submit(scene, cam, params, b)
+        pipe.wait(tb)
+    finally:
+        pipe.close()
+    want = _want(scene, cam, params)
+    assert b.pixels[px] == want[px] and a.pixels[px] != want[px]
+    parity.assert_byte_gate(b.pixels, want, "pipelined sky edit")

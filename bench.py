@@ -46,7 +46,7 @@ def parse_args(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default=None, help="workload (default: C2 on one GPU, C4 in row bands on several)")
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
     ap.add_argument("--no-extra", action="store_true", help="skip the other configurations' fps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -154,6 +154,8 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    # the same workload as this run's own arm (run_ours)
+    args.config = args.config or ("C2" if int(os.environ.get("WORLD_SIZE", "1")) == 1 else "C4")
     cfg = CONFIGS[args.config]
     threads = oracle.max_threads()
     per_step = max(2.0, args.cpu_seconds / max(1, args.steps))
@@ -204,16 +206,59 @@ def _dist_env():
     return world, rank, local
 
 
+# CPU baseline protocol per configuration: the paper's 100
+# warm-up + 10 measured frames (reference bench.py:24-25) where a CPU frame
+# is short, 1 + 3 whole frames for the soft-shadow configurations, and C5 on
+# a 384x216 frame scaled by the pixel count (a 4K C5 frame is ~20 CPU-minutes)
+CPU_PROTOCOL = {"C1": (100, 10, None), "P720": (100, 10, None), "P1080": (100, 10, None), "P4K": (100, 10, None),
+                "C2": (1, 3, None), "C3": (1, 3, None), "C4": (1, 3, None), "C5": (1, 3, (384, 216)),
+                "C5_512": (1, 3, (384, 216))}
+
+
+def cpu_frames(key, threads=0):
+    """The reference algorithm (float64 C port of render_frame, oracle/,
+    bit-identical to the reference) on the host cores, per CPU_PROTOCOL."""
+    import oracle
+    from paper_2305_07450_b200 import CONFIGS, pack_scene
+
+    cfg = CONFIGS[key]
+    warm, meas, sub = CPU_PROTOCOL[key]
+    w, h = sub or (cfg.width, cfg.height)
+    scene, cam = cfg.scene(), cfg.camera()
+    ps = vars(pack_scene(scene))
+
+    def one():
+        oracle.render(ps, cam.position, cam.yaw, cam.pitch, cam.fov, w, h, cfg.samples, cfg.bounces, threads=threads)
+
+    for _ in range(warm):
+        one()
+    t = time.perf_counter()
+    for _ in range(meas):
+        one()
+    dt = time.perf_counter() - t
+    scale = (w * h) / (cfg.width * cfg.height)
+    fps = meas / dt * scale
+    what = f"{warm} warm-up + {meas} measured frames"
+    if sub:
+        what += f" at {w}x{h}, scaled by the pixel count to {cfg.width}x{cfg.height}"
+    return fps, {"value": fps, "unit": "frames/s", "cores": threads or oracle.max_threads(), "kind": "port",
+                 "sample": f"{what} of {cfg.name}; float64 C port of render_frame (oracle/rt_oracle.c, "
+                           f"bit-identical to the reference), OpenMP dynamic rows, {dt:.1f} s"}
+
+
 def run_ours(args):
     import numpy as np
     import torch
 
     import paper_2305_07450_b200 as rt
-    from paper_2305_07450_b200 import _native
+    from paper_2305_07450_b200 import _native, bands
 
     world, rank, local = _dist_env()
     if world != args.gpus:
         args.gpus = world
+    # the headline workload: BASELINE.json configs[1] (C2) on one GPU; with
+    # several, configs[3] (C4, 4K) split in row bands across them
+    key = args.config or ("C2" if world == 1 else "C4")
     # B200RT_BENCH_SHARE_GPU=1: every rank on GPU 0 with host (gloo)
     # collectives — a functional check of the N > 1 code path on a one-GPU
     # box (no kernel waits on another rank's), never a measurement
@@ -231,7 +276,7 @@ def run_ours(args):
 
     lib = _native.load()
     ctx = _native.Context((local,))
-    cfg = rt.CONFIGS[args.config]
+    cfg = rt.CONFIGS[key]
     prec = _native.PRECISIONS[args.precision]
     wc = work_counts()
 
@@ -251,26 +296,18 @@ def run_ours(args):
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
 
     # framebuffer: rank 0 owns it (sized for the largest frame measured);
-    # other ranks map it over NVLink (CUDA IPC) and render straight into it
-    from paper_2305_07450_b200 import bands
-
-    extra_keys = () if (args.no_extra or world > 1) else EXTRA_CONFIGS
-    size_keys = (args.config, *extra_keys, *(("C4",) if world > 1 else ()))
+    # other ranks map it over NVLink (CUDA IPC) and render their rows into it
+    extra_keys = () if (args.no_extra or world > 1) else tuple(k for k in EXTRA_CONFIGS if k != key)
+    size_keys = (key, *extra_keys, "C2", "C4")
     max_px = max(rt.CONFIGS[k].width * rt.CONFIGS[k].height for k in size_keys)
-    frame_bytes = 4 * cfg.width * cfg.height
     exchange = bands.torch_exchange if world > 1 else (lambda blob: blob)
     ipc = bands.IpcFrame(local, 1, max_px, rank, exchange)
     fb_ptr = ipc.ptr
     tiny = torch.zeros(1, device=dev)
-
-    # N > 1: frames are independent units, so the headline shards whole
-    # frames across the GPUs (each renders its own frames into its own
-    # device frame, no collective: "weak" scaling); the north star's row
-    # bands of one frame gathered to rank 0 (strong scaling) are measured too
     d_local = ctypes.c_void_p()
-    if world > 1:
+    if world > 1:  # each rank's own device frame (whole-frame sharding, shared-host-frame gather)
         _native.check(lib.rt_device_malloc(local, 4 * max_px, ctypes.byref(d_local)), "rt_device_malloc")
-    cur = {"prec": prec, "mode": "frames"}
+    cur = {"prec": prec, "mode": "bands" if world > 1 else "frames"}
 
     def render_cfg(c, part=None, n_parts=None, out=None, sync=True):
         bands_mode = world > 1 and cur["mode"] == "bands"
@@ -287,7 +324,7 @@ def run_ours(args):
         _native.check(rc, "rt_render_device_v1")
         if bands_mode and sync:
             import torch.distributed as dist
-            dist.all_reduce(tiny)  # completes once every rank's band has landed
+            dist.all_reduce(tiny)  # completes once every rank's rows have landed in rank 0's frame
 
     def time_config(c, warmup, steps, sample_clocks=False):
         set_scene(c.scene())
@@ -334,15 +371,15 @@ def run_ours(args):
         return dict(ms=ms, total_ms=total, wall_s=wall, launches=launches, clocks=clk)
 
     def measure(c, warmup, steps, sample_clocks=False):
-        """Frames/s, per-phase device times and executed work of config c."""
+        """Frames/s, per-kernel device shares and executed work of config c."""
         r = time_config(c, warmup, steps, sample_clocks)
         # whole-job frames/s: every rank rendered len(ms) whole frames
         # ("frames" mode), or the ranks rendered len(ms) frames together ("bands")
         per = world if (world > 1 and cur["mode"] == "frames") else 1
         fps_c = per * len(r["ms"]) / (r["total_ms"] / 1e3)
-        # per-kernel device times: CUDA events between the kernels on their
-        # launch stream, averaged over as many frames as were timed (events
-        # cost ~2.5 us each, so they stay out of the timed region itself)
+        # per-kernel shares: CUDA events between the kernels on their launch
+        # stream, averaged over as many frames as were timed (events cost
+        # ~2.5 us each, so they stay out of the timed region itself)
         ctx.set_option("phases", 1)
         acc = {}
         n_ph = max(3, min(steps, 50))
@@ -351,7 +388,6 @@ def run_ours(args):
             torch.cuda.synchronize()
             for k, v in ctx.phase_ms().items():
                 acc[k] = acc.get(k, 0.0) + v / n_ph
-        phases = acc
         ctx.set_option("phases", 0)
         ctx.set_option("count_work", 1)
         ctx.work_counts(reset=True)
@@ -359,44 +395,51 @@ def run_ours(args):
         torch.cuda.synchronize()
         work = ctx.work_counts(reset=True)
         ctx.set_option("count_work", 0)
-        return r, fps_c, phases, work
+        return r, fps_c, acc, work
 
-    # headline: device-resident frames/s on the default path (wavefront + exact culling)
-    main, fps, phases, work = measure(cfg, max(3, args.warmup), args.steps, sample_clocks=True)
-    ms_frame = statistics.mean(main["ms"])
-    wcc = wc[args.config]
-    rays = wcc["rays"]
-    peak_meas = _native.fp32_peak_tflops(local)
-    roof = roofline(wcc, phases, work, ms_frame, cfg.samples, peak_meas, config_key=args.config)
-
-    # e2e through the public API into a host framebuffer (rank 0's process)
-    e2e = None
-    if world == 1:
-        scene, cam, params = cfg.scene(), cfg.camera(), cfg.params()
-        fb = rt.Framebuffer.create(cfg.width, cfg.height)
+    def e2e_sync(c, steps):
+        """render_frame (the reference's call) into a host Framebuffer, a new
+        camera every step; wall clock around each synchronous call."""
+        scene, cam, params = c.scene(), c.camera(), c.params()
+        fb = rt.Framebuffer.create(c.width, c.height)
         for _ in range(max(3, args.warmup)):
             rt.render_frame(scene, cam, params, fb, precision=args.precision)
-        # every step a new camera (the frame loop's moving view): the frame
-        # differs each step; the scene arrays and camera cross the C ABI and
-        # travel to the device in the launch parameters (the library compares
-        # the scene with its cached copy and re-uploads only what changed)
+        # every step a new camera (the frame loop's moving view): the scene
+        # arrays and camera cross the C ABI, the library compares the scene
+        # (and the sky's texels) with its copies and uploads only what changed
         cams = [rt.Camera(position=cam.position, yaw=cam.yaw + 1e-4 * (i % 2), pitch=cam.pitch, fov=cam.fov)
                 for i in range(2)]
         ts = []
-        for i in range(args.steps):
+        for i in range(steps):
             t = time.perf_counter()
             rt.render_frame(scene, cams[i % 2], params, fb, precision=args.precision)
             ts.append(time.perf_counter() - t)
-        e2e_fps = args.steps / sum(ts)
         ps = rt.pack_scene(scene)
         # kinds, positions, sizes, colours, reflectivities, light, ambient, max_refl + camera (f64, i32)
         h2d = int(4 * len(ps.kinds) + 8 * (3 + 1 + 3 + 1) * len(ps.kinds) + 8 * (3 + 1 + 3 + 2) + 8 * 6)
-        e2e = {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": frame_bytes,
-               "ms_per_step": 1e3 * statistics.mean(ts),
-               "path": "paper_2305_07450_b200.render_frame -> rt_render_v1 (C ABI), pinned host framebuffer"}
+        return {"value": steps / sum(ts), "unit": "frames/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": 4 * c.width * c.height, "ms_per_step": 1e3 * statistics.mean(ts),
+                "ms_median": 1e3 * statistics.median(ts),
+                "path": "paper_2305_07450_b200.render_frame -> rt_render_v1 (C ABI), pinned host framebuffer"}
+
+    line = {"metric": "frames/s", "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "vs_baseline": None,
+            "dtype": "f32" if args.precision == "fp32" else "f64",
+            "data": "synthetic (the paper's benchmark scene and camera, sceneio.py:314-333)"}
+    if world == 1:
+        # headline: device-resident frames/s on the default path (wavefront + exact culling)
+        main, fps, phases, work = measure(cfg, max(3, args.warmup), args.steps, sample_clocks=True)
+        ms_frame = statistics.mean(main["ms"])
+        wcc = wc[key]
+        peak_meas = _native.fp32_peak_tflops(local)
+        roof = roofline(wcc, phases, work, ms_frame, cfg.samples, peak_meas, config_key=key)
+        e2e = e2e_sync(cfg, args.steps)
         # the frame server's loop: frames back to back through FramePipeline,
         # each frame's copy overlapping the next frame's kernels; every frame
         # still lands whole in a host framebuffer before it is counted
+        scene, cam, params = cfg.scene(), cfg.camera(), cfg.params()
+        cams = [rt.Camera(position=cam.position, yaw=cam.yaw + 1e-4 * (i % 2), pitch=cam.pitch, fov=cam.fov)
+                for i in range(2)]
         depth = 3
         pipe = rt.FramePipeline(depth, precision=args.precision)
         fbs = [rt.Framebuffer.create(cfg.width, cfg.height) for _ in range(depth)]
@@ -409,13 +452,82 @@ def run_ours(args):
         pipe.drain()
         dt = time.perf_counter() - t
         pipe.close()
-        e2e["pipelined"] = {"value": args.steps / dt, "unit": "frames/s", "h2d_bytes_per_step": h2d,
-                            "d2h_bytes_per_step": frame_bytes,
-                            "ms_per_step": 1e3 * dt / args.steps,
+        e2e["pipelined"] = {"value": args.steps / dt, "unit": "frames/s",
+                            "h2d_bytes_per_step": e2e["h2d_bytes_per_step"],
+                            "d2h_bytes_per_step": e2e["d2h_bytes_per_step"], "ms_per_step": 1e3 * dt / args.steps,
                             "path": "paper_2305_07450_b200.FramePipeline (rt_render_async_v1 / rt_frame_wait_v1), "
                                     "depth 3, pinned host framebuffers"}
+        line.update({
+            "value": fps, "ms_per_step": main["total_ms"] / args.steps, "scaling": "weak",
+            "config": {"workload": cfg.name, "width": cfg.width, "height": cfg.height, "samples": cfg.samples,
+                       "bounces": cfg.bounces, "sky": cfg.sky, "parallelism": "one GPU",
+                       "path": "wavefront + exact per-hit occluder culling (default)",
+                       "l2": "flushed between timed frames (256 MiB memset outside the event pair)"},
+            **ray_rates(wcc, work, fps),
+            "mrays_definition": "reference_equivalent: the rays the reference's control flow traces for the frame "
+                                "(closest-hit + every shadow sample) / time; executed: closest-hit rays + the shadow "
+                                "rays the culled pass sampled",
+            "e2e": e2e, "gpu_launches": main["launches"], "clocks": main["clocks"], "roofline": roof,
+            "phases_ms": phases, "executed_work": work})
+        if not args.no_extra:
+            extra = {}
+            for k in extra_keys:
+                c = rt.CONFIGS[k]
+                r, f, ph, wk = measure(c, 3, 10 if k not in ("C4", "C5", "C5_512") else 5)
+                km = statistics.mean(r["ms"])
+                extra[k] = {"workload": c.name, "fps": f, "ms_per_frame": km, **ray_rates(wc[k], wk, f),
+                            "phases_ms": ph,
+                            "roofline": roofline(wc[k], ph, wk, km, c.samples, peak_meas, config_key=k),
+                            "e2e": e2e_sync(c, 10 if c.width * c.height < 4_000_000 else 5)}
+                if k in rt.workloads.PAPER_FPS:
+                    extra[k]["paper_fps_rtx2060"] = rt.workloads.PAPER_FPS[k]
+                if not args.no_cpu_baseline and k in CPU_PROTOCOL:
+                    extra[k]["cpu_baseline"] = cpu_frames(k)[1]
+            # ablation on the headline config: the same frame without culling, and as one megakernel
+            for name, opts in (("no_cull", dict(wave=1, cull=0)), ("megakernel", dict(wave=0, cull=0))):
+                for o, v in opts.items():
+                    ctx.set_option(o, v)
+                r, f, ph, wk = measure(cfg, 3, args.steps)
+                km = statistics.mean(r["ms"])
+                extra[f"{key}_{name}"] = {"fps": f, "ms_per_frame": km, "phases_ms": ph,
+                                          "roofline": roofline(wcc, ph, wk, km, cfg.samples, peak_meas,
+                                                               culled=False)}
+            for o, v in dict(wave=1, cull=1).items():
+                ctx.set_option(o, v)
+            # the bit-identical mode (float64 in the reference's operation order)
+            cur["prec"] = _native.RT_PREC_FP64
+            for k in (key, "P720", "P1080", "P4K"):
+                c = rt.CONFIGS[k]
+                r = time_config(c, 3, 10)
+                f = len(r["ms"]) / (r["total_ms"] / 1e3)
+                extra[f"{k}_fp64_bit_exact"] = {"workload": c.name, "fps": f, "ms_per_frame": statistics.mean(r["ms"]),
+                                                "precision": "fp64, bit-identical to the reference"}
+            cur["prec"] = prec
+            line["extra"] = extra
+        if not args.no_cpu_baseline:
+            if key in CPU_PROTOCOL:
+                line["cpu_baseline"] = cpu_frames(key)[1]
+            else:
+                v, meta = cpu_reference_sample(cfg, args.cpu_seconds)
+                line["cpu_baseline"] = {"value": v, "unit": "frames/s", "cores": meta["threads"], "kind": "port",
+                                        "sample": f"{meta['rows']} rows of {cfg.name}"}
     else:
         import torch.distributed as dist
+
+        # headline: one frame of C4 in row bands (8-row blocks round-robin,
+        # SURVEY.md §8e), every rank storing its rows into rank 0's device
+        # frame over NVLink (CUDA IPC) — the gather fused into the render; the
+        # all-reduce completes once every band has landed (strong scaling)
+        cur["mode"] = "bands"
+        main, fps, phases, work = measure(cfg, max(3, args.warmup), args.steps, sample_clocks=True)
+        peak_meas = _native.fp32_peak_tflops(local)
+        # per GPU: rank 0's kernels did ~1/world of the frame's work (balanced
+        # row blocks) in its frame time
+        work_frame = {k: v * world for k, v in work.items()}
+        roof = roofline(wc[key], phases, work_frame, world * statistics.mean(main["ms"]), cfg.samples, peak_meas,
+                        config_key=key)
+        roof["per"] = "GPU (rank 0's share of the frame)"
+        frame_bytes = 4 * cfg.width * cfg.height
 
         def e2e_run(step, frames_per_step):
             ts = []
@@ -424,27 +536,18 @@ def run_ours(args):
                 t = time.perf_counter()
                 step()
                 torch.cuda.synchronize()
+                dist.barrier()
                 if i >= max(3, args.warmup):
                     ts.append(time.perf_counter() - t)
             t = torch.tensor([sum(ts)], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             return frames_per_step * args.steps / float(t.item())
 
-        # (0) the headline: every rank renders whole frames and reads each back
-        # into its own page-locked host frame over its own PCIe link
-        host_own = torch.empty(cfg.width * cfg.height, dtype=torch.int32, pin_memory=True)
-
-        def own_step():
-            cur["mode"] = "frames"
-            render_cfg(cfg)
-            _native.check(lib.rt_copy_to_host(ctx.handle, 0, ctypes.c_void_p(host_own.data_ptr()), d_local,
-                                              frame_bytes, ctypes.c_void_p(stream.cuda_stream)), "rt_copy_to_host")
-
-        fps_own = e2e_run(own_step, world)
-
-        # (1) one frame split in row bands: every rank renders its rows into its
-        # own device frame and copies them into a page-locked host frame shared
-        # by the node's ranks, over its own PCIe link
+        # e2e (1): every rank renders its rows into its own device frame and
+        # copies them into a page-locked host frame shared by the node's ranks
+        # over its own PCIe link — the frame is whole in host
+        # memory when the closing barrier passes
+        set_scene(cfg.scene())
         shm = bands.ShmFrame(ctx, cfg.width, cfg.height, rank, bands.torch_exchange)
 
         def shm_step():
@@ -452,22 +555,10 @@ def run_ours(args):
             shm.copy_rows(d_local, rank, world, ctypes.c_void_p(stream.cuda_stream))
 
         fps_shm = e2e_run(shm_step, 1)
-        ok = True
-        if rank == 0:  # the shared frame is the frame
-            ref = np.empty(cfg.width * cfg.height, dtype=np.uint32)
-            render_cfg(cfg, part=0, n_parts=1, out=d_local, sync=False)
-            _native.check(lib.rt_copy_to_host(ctx.handle, 0, _native.ptr(ref), d_local, frame_bytes,
-                                              ctypes.c_void_p(stream.cuda_stream)), "rt_copy_to_host")
-        dist.barrier()
-        if rank == 0:
-            ok = bool(np.array_equal(ref, shm.pixels))
-        shm.close()
-
-        # (2) row bands gathered into rank 0's device frame (CUDA IPC), one D2H on rank 0
+        # e2e (2): the NVLink gather into rank 0's device frame + one D2H on rank 0
         host = torch.empty(cfg.width * cfg.height, dtype=torch.int32, pin_memory=True) if rank == 0 else None
 
         def ipc_step():
-            cur["mode"] = "bands"
             render_cfg(cfg)  # its all-reduce orders "every band landed"
             if rank == 0:
                 _native.check(lib.rt_copy_to_host(ctx.handle, 0, ctypes.c_void_p(host.data_ptr()), fb_ptr,
@@ -475,101 +566,49 @@ def run_ours(args):
                               "rt_copy_to_host")
 
         fps_ipc = e2e_run(ipc_step, 1)
+        # both host frames against one GPU rendering the whole frame
+        ok_shm = ok_ipc = True
+        if rank == 0:
+            ref = np.empty(cfg.width * cfg.height, dtype=np.uint32)
+            render_cfg(cfg, part=0, n_parts=1, out=d_local, sync=False)
+            _native.check(lib.rt_copy_to_host(ctx.handle, 0, _native.ptr(ref), d_local, frame_bytes,
+                                              ctypes.c_void_p(stream.cuda_stream)), "rt_copy_to_host")
+        dist.barrier()
+        if rank == 0:
+            ok_shm = bool(np.array_equal(ref, shm.pixels))
+            ok_ipc = bool(np.array_equal(ref, host.numpy().view(np.uint32)))
+        shm.close()
+        e2e = {"value": fps_shm, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": frame_bytes,
+               "path": f"one {cfg.name} frame in row bands over {world} ranks (rt_render_device_v1), each rank's rows "
+                       "copied into a page-locked host frame shared by the ranks over its own PCIe link "
+                       "(rt_copy_partition_to_host), barrier",
+               "frame_matches_single_gpu_render": ok_shm,
+               "ipc_gather": {"value": fps_ipc, "unit": "frames/s", "d2h_bytes_per_step": frame_bytes,
+                              "path": "row bands stored into rank 0's device frame over NVLink (CUDA IPC) + one D2H "
+                                      "on rank 0",
+                              "frame_matches_single_gpu_render": ok_ipc}}
+        # whole frames sharded across the GPUs (each rank its own frames, no
+        # collective: weak scaling) — the alternative split, reported alongside
         cur["mode"] = "frames"
-        e2e = {"value": fps_own, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": frame_bytes * world,
-               "path": f"rt_render_device_v1 whole frames on each of {world} ranks, each read back into the "
-                       "rank's own page-locked host frame (its own PCIe link)",
-               "row_bands_shared_host_frame": {
-                   "value": fps_shm, "unit": "frames/s", "d2h_bytes_per_step": frame_bytes,
-                   "path": "one frame in row bands: rt_copy_partition_to_host into a page-locked host frame "
-                           "shared by the ranks (each GPU's rows over its own PCIe link)",
-                   "frame_matches_single_gpu_render": ok},
-               "row_bands_ipc_gather": {
-                   "value": fps_ipc, "unit": "frames/s", "d2h_bytes_per_step": frame_bytes,
-                   "path": "one frame in row bands into rank 0's device frame over NVLink (CUDA IPC) + one D2H "
-                           "on rank 0"}}
-
-    line = {
-        "metric": "frames/s",
-        "value": fps,
-        "unit": "frames/s",
-        "n_gpus": world,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": main["total_ms"] / args.steps,
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
-        "dtype": "f32" if args.precision == "fp32" else "f64",
-        "data": "synthetic (the paper's benchmark scene and camera, sceneio.py:314-333)",
-        "config": {"workload": cfg.name, "width": cfg.width, "height": cfg.height, "samples": cfg.samples,
-                   "bounces": cfg.bounces, "sky": cfg.sky, "parallelism": (f"frames x{world} (a whole frame per GPU per step, no collective)" if world > 1
-                                   else "one GPU"),
-                   "path": "wavefront + exact per-hit occluder culling (default)",
-                   "l2": "flushed between timed frames (256 MiB memset outside the event pair)"},
-        "mrays_per_s": rays * fps / 1e6,
-        "e2e": e2e,
-        "gpu_launches": main["launches"],
-        "clocks": main["clocks"],
-        "roofline": roof,
-        "phases_ms": phases,
-        "executed_work": work,
-    }
-    if world > 1:
-        # the north star's row bands: one frame split across the GPUs, rows
-        # gathered into rank 0's frame over NVLink (strong scaling), and the
-        # same for 4K, where the split pays
-        bands_lines = {}
-        cur["mode"] = "bands"
-        for key in (args.config, "C4"):
-            c = rt.CONFIGS[key]
-            if c.width * c.height > max_px:
-                continue
+        whole = {}
+        for k in ("C2", "C4"):
+            c = rt.CONFIGS[k]
             r = time_config(c, 3, args.steps)
-            bands_lines[key] = {"workload": c.name, "fps": len(r["ms"]) / (r["total_ms"] / 1e3),
-                                "ms_per_frame": r["total_ms"] / len(r["ms"]), "scaling": "strong",
-                                "path": "rt_render_device_v1 row blocks into rank 0's frame (CUDA IPC) + all-reduce"}
-        cur["mode"] = "frames"
-        line["row_bands"] = bands_lines
-    if rank == 0 and not args.no_extra and world == 1:
-        extra = {}
-        for key in extra_keys:
-            c = rt.CONFIGS[key]
-            r, f, ph, wk = measure(c, 3, 10 if key not in ("C4", "C5") else 5)
-            km = statistics.mean(r["ms"])
-            extra[key] = {"workload": c.name, "fps": f, "ms_per_frame": km,
-                          "mrays_per_s": wc[key]["rays"] * f / 1e6, "phases_ms": ph,
-                          "roofline": roofline(wc[key], ph, wk, km, c.samples, peak_meas, config_key=key)}
-            if key in rt.workloads.PAPER_FPS:
-                extra[key]["paper_fps_rtx2060"] = rt.workloads.PAPER_FPS[key]
-        # ablation on the headline config: the same frame without culling, and as one megakernel
-        for name, opts in (("no_cull", dict(wave=1, cull=0)), ("megakernel", dict(wave=0, cull=0))):
-            for k, v in opts.items():
-                ctx.set_option(k, v)
-            r, f, ph, wk = measure(cfg, 3, args.steps)
-            km = statistics.mean(r["ms"])
-            extra[f"{args.config}_{name}"] = {"fps": f, "ms_per_frame": km, "phases_ms": ph,
-                                              "roofline": roofline(wcc, ph, wk, km, cfg.samples, peak_meas,
-                                                                   culled=False)}
-        for k, v in dict(wave=1, cull=1).items():
-            ctx.set_option(k, v)
-        # the bit-identical mode (float64 in the reference's operation order)
-        cur["prec"] = _native.RT_PREC_FP64
-        for key in (args.config, "P720", "P1080", "P4K"):
-            c = rt.CONFIGS[key]
-            r = time_config(c, 3, 10)
-            f = len(r["ms"]) / (r["total_ms"] / 1e3)
-            extra[f"{key}_fp64_bit_exact"] = {"workload": c.name, "fps": f, "ms_per_frame": statistics.mean(r["ms"]),
-                                              "precision": "fp64, bit-identical to the reference"}
-        cur["prec"] = prec
-        line["extra"] = extra
-    if rank == 0 and not args.no_cpu_baseline and world == 1:
-        v, meta = cpu_reference_sample(cfg, args.cpu_seconds)
-        what = (f"{meta['frames']} whole frames" if meta["frames"] else
-                f"every {meta['row_step']}th row ({meta['rows']}/{cfg.height} rows)")
-        line["cpu_baseline"] = {"value": v, "unit": "frames/s", "cores": meta["threads"], "kind": "port",
-                                "sample": f"{what} of {cfg.name}, float64 C port of render_frame (oracle/, "
-                                          f"bit-identical to the reference), {meta['seconds']:.1f} s"}
+            whole[k] = {"workload": c.name, "fps": world * len(r["ms"]) / (r["total_ms"] / 1e3),
+                        "ms_per_frame": r["total_ms"] / len(r["ms"]), "scaling": "weak",
+                        "path": "rt_render_device_v1 whole frames, one per rank per step, no collective"}
+        cur["mode"] = "bands"
+        line.update({
+            "value": fps, "ms_per_step": main["total_ms"] / args.steps, "scaling": "strong",
+            "config": {"workload": cfg.name, "width": cfg.width, "height": cfg.height, "samples": cfg.samples,
+                       "bounces": cfg.bounces, "sky": cfg.sky,
+                       "parallelism": f"row bands x{world} (8-row blocks round-robin), gathered into rank 0's frame "
+                                      "over NVLink",
+                       "path": "wavefront + exact per-hit occluder culling (default)",
+                       "l2": "flushed between timed frames (256 MiB memset outside the event pair)"},
+            **ray_rates(wc[key], work, fps),
+            "e2e": e2e, "gpu_launches": main["launches"], "clocks": main["clocks"], "roofline": roof,
+            "phases_ms": phases, "whole_frames": whole})
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
@@ -585,7 +624,9 @@ def run_ours(args):
 
 
 # FLOPs per unit of the SURVEY.md §8d cost model (FMA = 2, add/mul/sqrt/div = 1)
-FLOP_SPHERE_FULL = 19   # a sphere test evaluated to the end (the kernels are branch-free: every test is full)
+FLOP_SPHERE_TCA = 8     # a sphere test that exits at tca < 0
+FLOP_SPHERE_DISC = 17   # ... at the discriminant
+FLOP_SPHERE_FULL = 19   # ... evaluated to the end
 FLOP_PLANE = 2
 FLOP_SHADOW_SETUP = 33  # sample point from the table, normalise, limit (n > 1); 21 for n = 1
 FLOP_HIT = 60           # hit point, normal, to-light, Lambert/Blinn inputs
@@ -593,21 +634,38 @@ FLOP_BASIS = 39         # disc basis per hit (n > 1)
 FLOP_PRIMARY = 36       # primary direction + pack
 FLOP_REFLECT = 18
 FLOP_SHADE = 45
+# units of the culled path (no reference counterpart), weighted by the FP32
+# operations of their code (FMA = 2): reconciled against the ncu FP32
+# instruction counters in profiles/ncu_flops.json (bench line: model_over_counter)
 FLOP_CULL = 40          # one body's cone classification (centre offset, axial/radial split, 2 sqrt, compares)
 FLOP_CONIC = 17         # one silhouette-form sample test (|w|^2, x, y, d: 7 FMA + 1 add; culled sampler)
 FLOP_CONIC_SETUP = 120  # shadow frame, cone and the six coefficients of one (hit, sphere) pair
 
 
+def _sphere_flops(tca, disc, full):
+    return tca * FLOP_SPHERE_TCA + disc * FLOP_SPHERE_DISC + full * FLOP_SPHERE_FULL
+
+
+def _load_profile(name):
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
 def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True, config_key=None):
-    """Roofline of the dominant kernel: its executed FLOPs (cost model above,
-    counts from the reference's control flow or the culled pass's own
-    tallies) over its measured device time."""
+    """Roofline of the dominant kernel: its algorithmic FLOPs (SURVEY.md §8d
+    units x the counts of one launch: the reference's control flow, or the
+    culled pass's own tallies) over its device time.  The kernels' shares of
+    the frame come from CUDA events between them (phases); the kernel time is
+    that share of the frame time measured without them, so the events' own
+    cost (~2.5 us each) does not inflate it."""
     c = wcc["counts"]
     setup = FLOP_SHADOW_SETUP if samples > 1 else 21
-    ch_tests = c["CH_TCA"] + c["CH_DISC"] + c["CH_FULL"]
     flops = {
-        "trace": ch_tests * FLOP_SPHERE_FULL + c["CH_PLANE"] * FLOP_PLANE + c["HITS"] * FLOP_HIT
-        + c["PIX"] * FLOP_PRIMARY + c["REFL"] * FLOP_REFLECT,
+        "trace": _sphere_flops(c["CH_TCA"], c["CH_DISC"], c["CH_FULL"]) + c["CH_PLANE"] * FLOP_PLANE
+        + c["HITS"] * FLOP_HIT + c["PIX"] * FLOP_PRIMARY + c["REFL"] * FLOP_REFLECT,
         "shade": c["SHADE"] * FLOP_SHADE,
     }
     if culled and work.get("hits"):
@@ -623,36 +681,45 @@ def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True, config_key
                            + (work["sphere_tests"] - conic_tests) * FLOP_SPHERE_FULL
                            + work["plane_tests"] * FLOP_PLANE)
     else:
-        sh_tests = c["SH_TCA"] + c["SH_DISC"] + c["SH_FULL"]
         flops["classify"] = 0
         flops["shadow"] = (c["SH_RAYS"] * setup + c["HITS"] * (FLOP_BASIS if samples > 1 else 0)
-                           + sh_tests * FLOP_SPHERE_FULL + c["SH_PLANE"] * FLOP_PLANE)
-    if phases and sum(phases.values()) > 0:
-        kernel = max(phases, key=phases.get)
-        kms = phases[kernel]
-        share = kms / max(sum(phases.values()), 1e-12)
+                           + _sphere_flops(c["SH_TCA"], c["SH_DISC"], c["SH_FULL"]) + c["SH_PLANE"] * FLOP_PLANE)
+    real = {k: v for k, v in (phases or {}).items() if v > 0.005}  # phases of a few us are event gaps
+    if real:
+        total = sum(real.values())
+        shares = {k: v / total for k, v in real.items()}
+        kernel = max(shares, key=shares.get)
+        share = shares[kernel]
+        kms = share * ms_frame
     else:  # megakernel: one kernel does everything
         kernel, kms, share = "megakernel", ms_frame, 1.0
+        shares = {kernel: 1.0}
         flops = {"megakernel": sum(flops.values())}
     achieved = flops[kernel] / (kms * 1e-3) / 1e12 if kms > 0 else 0.0
     # DRAM traffic per launch of that kernel, from the committed ncu capture
     # (profiles/ncu_traffic.json); null when there is none for this config
     traffic, traffic_src = None, None
-    try:
-        tr = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")))
-        t = tr.get(config_key, {}).get(kernel)
-        if t:
-            traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
-            traffic_src = tr["_source"]
-    except (OSError, ValueError, KeyError):
-        pass
+    tr = _load_profile("ncu_traffic.json")
+    t = tr.get(config_key, {}).get(kernel) if tr else None
+    if t:
+        traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
+        traffic_src = tr.get("_source")
+    # executed FP32 operations per launch from ncu's instruction counters
+    # (FFMA x 2 + FADD + FMUL, paired forms x 2; profiles/ncu_flops.json)
+    counters = _load_profile("ncu_flops.json").get(config_key, {})
     per_kernel = {}
-    if phases and sum(phases.values()) > 0:
-        for k, ms in phases.items():
-            if flops.get(k) and ms > 0.005:  # phases of a few us are event gaps, not kernels
-                a = flops[k] / (ms * 1e-3) / 1e12
-                per_kernel[k] = {"ms": ms, "flops": flops[k], "achieved": a, "frac": a / peak if peak else None}
-    return {
+    for k, sh in shares.items():
+        ms = sh * ms_frame
+        if flops.get(k) and ms > 0:
+            a = flops[k] / (ms * 1e-3) / 1e12
+            per_kernel[k] = {"ms": ms, "share_of_frame": sh, "flops": flops[k], "achieved": a,
+                             "frac": a / peak if peak else None}
+            cf = counters.get(k, {}).get("flops")
+            if cf:
+                per_kernel[k]["counter_flops"] = cf
+                per_kernel[k]["counter_achieved"] = cf / (ms * 1e-3) / 1e12
+                per_kernel[k]["model_over_counter"] = flops[k] / cf
+    out = {
         "bound": "fp32",
         "kernel": kernel,
         "achieved": achieved,
@@ -664,12 +731,34 @@ def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True, config_key
         "kernel_ms": kms,
         "kernel_share_of_frame": share,
         "flops_per_launch": flops[kernel],
+        "flops_definition": "algorithmic: SURVEY.md §8d units (sphere test 8/17/19 by exit, plane 2, hit 60, "
+                            "primary 36, reflection 18, shade 45, shadow-ray setup 33) x this launch's counts, "
+                            "plus the culled path's own units (cone class 40, silhouette test 17, its setup 120)",
         "peak_source": "measured dependent-free FFMA stream on this GPU (rt_fp32_peak_tflops); "
                        "MEASURED_PEAKS.json has no FP32 CUDA-core figure",
         "peak_nominal": NOMINAL_FP32_TFLOPS,
         "reference_equivalent_tflops": wcc["flops"] / (ms_frame * 1e-3) / 1e12,
         "kernels": per_kernel,
     }
+    if per_kernel.get(kernel, {}).get("counter_flops"):
+        out["counter_flops_per_launch"] = per_kernel[kernel]["counter_flops"]
+        out["counter_achieved"] = per_kernel[kernel]["counter_achieved"]
+        out["model_over_counter"] = per_kernel[kernel]["model_over_counter"]
+        out["counter_source"] = counters.get("_source") or _load_profile("ncu_flops.json").get("_source")
+    return out
+
+
+def ray_rates(wcc, work, fps):
+    """Mrays/s two ways: reference-equivalent (the rays the reference's
+    control flow traces for this frame) and executed (the
+    closest-hit rays plus the shadow rays the culled pass actually sampled)."""
+    c = wcc["counts"]
+    out = {"mrays_per_s_reference_equivalent": wcc["rays"] * fps / 1e6}
+    if work.get("hits"):
+        out["mrays_per_s_executed"] = (c["CH_RAYS"] + work.get("shadow_rays", 0)) * fps / 1e6
+    else:
+        out["mrays_per_s_executed"] = out["mrays_per_s_reference_equivalent"]
+    return out
 
 
 def main(argv=None):

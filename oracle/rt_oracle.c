@@ -46,7 +46,8 @@ static _Thread_local long long *g_cnt;
  * pinned oracle never defines it): round chosen intermediates to float32 to
  * measure how sensitive the frame is to each — 1 primary direction, 2 hit
  * point and normal, 4 shadow origin and sample directions, 8 reflected
- * direction and origin, 16 shadow origin only, 32 the shading vectors. */
+ * direction and origin, 16 shadow origin only, 32 the shading vectors, 64 the
+ * scene geometry of the shadow tests. */
 #ifdef RTO_ROUND
 static inline double rf(double x) { return (double)(float)x; }
 #define RND(bit, v) ((RTO_ROUND & (bit)) ? (v3){rf((v).x), rf((v).y), rf((v).z)} : (v))
@@ -167,6 +168,15 @@ static inline int closest_hit(const scene_t *s, v3 o, v3 d, double *t_out) {
 
 /* geometry.py:204-210 */
 static inline int occluded(const scene_t *s, v3 o, v3 d, double limit) {
+#if defined(RTO_ROUND) && (RTO_ROUND & 64)
+    for (int i = 0; i < s->n; i++) { /* probe: float32 scene geometry in the shadow tests */
+        double t = s->kinds[i] == 0 ? ray_sphere(o, d, mk(rf(s->pos[3 * i]), rf(s->pos[3 * i + 1]), rf(s->pos[3 * i + 2])),
+                                                 rf(s->size[i]), 1)
+                                    : ray_plane(o, d, rf(s->pos[3 * i + 1]), 1);
+        if (t < limit) return 1;
+    }
+    return 0;
+#endif
     for (int i = 0; i < s->n; i++)
         if (intersect(s, o, d, i, 1) < limit) return 1;
     return 0;

@@ -21,7 +21,8 @@
 //    (geometry.py:94-104, 204-210) without the square root:
 //    t >= 0  <=>  tca^2 >= rad,   t < limit  <=>  tca - limit < 0 or (tca - limit)^2 < rad;
 //    the plane test `0 < (h - o.y)/d.y < limit` without the division;
-//  - primary directions are formed in float64 (camera.py:70-77) and rounded;
+//  - the ray chain (primary direction, hit points, normals, reflections) runs
+//    in float64 (rt_f32.cuh: refine_hit) — the search, shadows and shading in FP32;
 //  - the disc-sample table is built in float64 on the host and rounded.
 #include "rt_f32.cuh"
 
@@ -59,8 +60,10 @@ __device__ float shadow_coeff(const Geo &geo, float3 surface, float3 normal, con
 // so the unwind only mixes, scales and clamps.  The bounce loop is not
 // unrolled (it would copy the shadow loop per bounce); the 12-byte records
 // live in L1-resident local memory.
+// The ray chain runs in float64 (rt_f32.cuh: refine_hit): the FP32 body
+// search, shadow rays and shading work on its rounded values.
 template <int BMAX, class Geo>
-__device__ float3 trace(const Geo &geo, float3 origin, float3 dir, const SceneArgs<float> &sa, int samples,
+__device__ float3 trace(const Geo &geo, D3 o64, D3 d64, const SceneArgs<float> &sa, int samples,
                         int bounces, const MegaCull &mc, unsigned smask = ~0u) {
     int ridx[BMAX + 1];
     float rlum[BMAX + 1], rspec[BMAX + 1];
@@ -71,13 +74,15 @@ __device__ float3 trace(const Geo &geo, float3 origin, float3 dir, const SceneAr
 #pragma unroll(BMAX <= 1 ? BMAX + 1 : 1)
     for (int k = 0; k <= BMAX; k++) {
         if (k > bounces) break;
+        const float3 origin = rnd(o64), dir = rnd(d64);
         Hit h = k == 0 ? geo.template closest<true>(origin, dir, smask) : geo.closest(origin, dir);
         if (h.idx < 0) {
             if (sa.has_sky) tail = sky_sample(dir, sa.sky, sa.sky_w, sa.sky_h);
             break;
         }
-        float3 hit = origin + dir * h.t;
-        float3 normal = h.g.w >= 0.f ? normalize3(hit - f3(h.g.x, h.g.y, h.g.z)) : f3(0.f, 1.f, 0.f);
+        D3 p64, n64;
+        refine_hit(o64, d64, sa.geo64, sa.n, h.idx, p64, n64);
+        const float3 hit = rnd(p64), normal = rnd(n64);
         float3 l = normalize3(lp - hit);
         float sc = shadow_coeff(geo, hit, normal, sa, samples, mc);
         // shading.py:53-73, 159-162 (view = -dir)
@@ -98,8 +103,7 @@ __device__ float3 trace(const Geo &geo, float3 origin, float3 dir, const SceneAr
             exhausted = true;
             break;
         }
-        origin = hit + normal * 1e-3f;
-        dir = dir - normal * (2.f * dot3(normal, dir));
+        reflect64(p64, n64, o64, d64);
     }
     float3 col = tail;
 #pragma unroll(BMAX <= 1 ? BMAX + 1 : 1)
@@ -127,8 +131,7 @@ __device__ __forceinline__ void shade_pixel(const Geo &geo, const FrameArgs &fa,
     if (x >= fa.width || ly >= fa.local_rows) return;
     int y = map_row(ly, fa);
     if (y >= fa.row_end) return;
-    float3 dir = primary_direction(x, y, fa);
-    float3 c = trace<BMAX>(geo, f3((float)fa.cam[0], (float)fa.cam[1], (float)fa.cam[2]), dir, sa, fa.samples,
+    float3 c = trace<BMAX>(geo, D3{fa.cam[0], fa.cam[1], fa.cam[2]}, primary_direction64(x, y, fa), sa, fa.samples,
                            fa.bounces, mc, primary_sphere_mask(mc, x, y));
     fa.out[(int64_t)y * fa.out_pitch + x] = pack_color(c.x, c.y, c.z, fa.rgba);
     if (fa.radiance) {
@@ -207,9 +210,8 @@ __global__ void __launch_bounds__(kThreads)
                            const SceneArgs<float> sa, int samples, int bounces, const ParamScene<MAXS> ps) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_rays) return;
-    float3 c = trace<BMAX>(ps, f3((float)orig[3 * i], (float)orig[3 * i + 1], (float)orig[3 * i + 2]),
-                           f3((float)dirs[3 * i], (float)dirs[3 * i + 1], (float)dirs[3 * i + 2]), sa, samples,
-                           bounces, MegaCull{});
+    float3 c = trace<BMAX>(ps, D3{orig[3 * i], orig[3 * i + 1], orig[3 * i + 2]},
+                           D3{dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2]}, sa, samples, bounces, MegaCull{});
     out[3 * i] = c.x;
     out[3 * i + 1] = c.y;
     out[3 * i + 2] = c.z;
@@ -222,9 +224,8 @@ __global__ void __launch_bounds__(kThreads)
     MemScene geo{reinterpret_cast<const float4 *>(sa.geo), sa.n};
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_rays) return;
-    float3 c = trace<BMAX>(geo, f3((float)orig[3 * i], (float)orig[3 * i + 1], (float)orig[3 * i + 2]),
-                           f3((float)dirs[3 * i], (float)dirs[3 * i + 1], (float)dirs[3 * i + 2]), sa, samples,
-                           bounces, MegaCull{});
+    float3 c = trace<BMAX>(geo, D3{orig[3 * i], orig[3 * i + 1], orig[3 * i + 2]},
+                           D3{dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2]}, sa, samples, bounces, MegaCull{});
     out[3 * i] = c.x;
     out[3 * i + 1] = c.y;
     out[3 * i + 2] = c.z;

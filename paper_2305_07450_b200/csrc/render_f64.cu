@@ -97,7 +97,7 @@ __device__ d3 trace(d3 origin, d3 dir, const double *__restrict__ geo, const Sce
         } else {
             double dd = (normal.x * hx + normal.y * hy + normal.z * hz) / hm;
             if (dd < 0.0) dd = 0.0;
-            s = pow(dd, __ldg(sa.mat + 8 * idx + 4));
+            s = rtpow::pow_cr(dd, __ldg(sa.mat + 8 * idx + 4));  // rounded like libm (rt_pow.cuh)
         }
         double lum = sa.ambient + sc * dfs * (1.0 - sa.ambient);
         if (lum > 1.0) lum = 1.0;

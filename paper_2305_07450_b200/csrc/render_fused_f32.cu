@@ -247,8 +247,9 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_TRACE_MIN_BLOCKS : 6)
     const bool valid = alive;
     const int64_t lp = (int64_t)ly * fa.width + x;
     const float3 light = f3(sa.light[0], sa.light[1], sa.light[2]);
-    float3 origin = f3((float)fa.cam[0], (float)fa.cam[1], (float)fa.cam[2]);
-    float3 dir = valid ? primary_direction(x, y, fa) : f3(0.f, 0.f, 1.f);
+    // the ray chain in float64 (rt_f32.cuh: refine_hit), searched in FP32
+    D3 o64{fa.cam[0], fa.cam[1], fa.cam[2]};
+    D3 d64 = valid ? primary_direction64(x, y, fa) : D3{0.0, 0.0, 1.0};
     float3 tail = f3(0.f, 0.f, 0.f);
     int m = 0, exhausted = 0, npend = 0;
     int ridx[kMaxBounce + 1];
@@ -256,6 +257,7 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_TRACE_MIN_BLOCKS : 6)
     for (int k = 0; k <= fa.bounces; k++) {
         const unsigned live = __ballot_sync(0xffffffffu, alive);
         if (!live) break;
+        const float3 origin = rnd(o64), dir = rnd(d64);
         Hit h{-1, INFINITY, make_float4(0.f, 0.f, 0.f, -1.f)};
         if constexpr (!kBundle) {
             // (the primary-ray sphere boxes cost this kernel ~4%: its unrolled,
@@ -339,8 +341,9 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_TRACE_MIN_BLOCKS : 6)
         float4 qp, qn;  // a queued hit's point (+ record slot) and normal
         bool to_lane = false, lane_z = false;  // qn.w: the candidate sphere's slot
         if (hit_now) {
-            float3 hit = origin + dir * h.t;
-            float3 normal = h.g.w >= 0.f ? normalize3(hit - f3(h.g.x, h.g.y, h.g.z)) : f3(0.f, 1.f, 0.f);
+            D3 p64, n64;
+            refine_hit(o64, d64, sa.geo64, sa.n, h.idx, p64, n64);
+            const float3 hit = rnd(p64), normal = rnd(n64);
             float3 l = normalize3(light - hit);
             float dfs = fmaxf(dot3(normal, l), 0.f);
             float3 hv = l - dir;
@@ -382,8 +385,7 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_TRACE_MIN_BLOCKS : 6)
                 exhausted = 1;
                 alive = false;
             } else {
-                origin = so;
-                dir = dir - normal * (2.f * dot3(normal, dir));
+                reflect64(p64, n64, o64, d64);
             }
         }
         // queue the undecided hits: one atomic per warp, bounce and queue

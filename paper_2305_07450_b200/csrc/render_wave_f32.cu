@@ -44,19 +44,21 @@ __device__ __forceinline__ void trace_chain(const Geo &geo, const FrameArgs &fa,
     int y = map_row(ly, fa);
     if (y >= fa.row_end) return;
     const int64_t lp = (int64_t)ly * fa.width + x;
-    float3 origin = f3((float)fa.cam[0], (float)fa.cam[1], (float)fa.cam[2]);
-    float3 dir = primary_direction(x, y, fa);
+    D3 o64{fa.cam[0], fa.cam[1], fa.cam[2]};  // the ray chain in float64 (rt_f32.cuh: refine_hit)
+    D3 d64 = primary_direction64(x, y, fa);
     const float3 light = f3(sa.light[0], sa.light[1], sa.light[2]);
     float3 tail = f3(0.f, 0.f, 0.f);
     int m = 0, exhausted = 0;
     for (int k = 0; k <= fa.bounces; k++) {
+        const float3 origin = rnd(o64), dir = rnd(d64);
         Hit h = geo.closest(origin, dir);
         if (h.idx < 0) {
             if (sa.has_sky) tail = sky_sample(dir, sa.sky, sa.sky_w, sa.sky_h);
             break;
         }
-        float3 hit = origin + dir * h.t;
-        float3 normal = h.g.w >= 0.f ? normalize3(hit - f3(h.g.x, h.g.y, h.g.z)) : f3(0.f, 1.f, 0.f);
+        D3 p64, n64;
+        refine_hit(o64, d64, sa.geo64, sa.n, h.idx, p64, n64);
+        const float3 hit = rnd(p64), normal = rnd(n64);
         float3 l = normalize3(light - hit);
         float dfs = fmaxf(dot3(normal, l), 0.f);
         float3 hv = l - dir;
@@ -82,8 +84,7 @@ __device__ __forceinline__ void trace_chain(const Geo &geo, const FrameArgs &fa,
             exhausted = 1;
             break;
         }
-        origin = hit + normal * 1e-3f;
-        dir = dir - normal * (2.f * dot3(normal, dir));
+        reflect64(p64, n64, o64, d64);
     }
     wa.pix[lp] = make_float4(tail.x, tail.y, tail.z, __int_as_float(m | (exhausted << 8)));
 }
@@ -118,14 +119,15 @@ __device__ __forceinline__ void trace_chain_bundle(const ParamScene<MAXS> &ps, c
     }
     const bool valid = alive;
     const int64_t lp = (int64_t)ly * fa.width + x;
-    float3 origin = f3((float)fa.cam[0], (float)fa.cam[1], (float)fa.cam[2]);
-    float3 dir = valid ? primary_direction(x, y, fa) : f3(0.f, 0.f, 1.f);
+    D3 o64{fa.cam[0], fa.cam[1], fa.cam[2]};  // the ray chain in float64 (rt_f32.cuh: refine_hit)
+    D3 d64 = valid ? primary_direction64(x, y, fa) : D3{0.0, 0.0, 1.0};
     const float3 light = f3(sa.light[0], sa.light[1], sa.light[2]);
     float3 tail = f3(0.f, 0.f, 0.f);
     int m = 0, exhausted = 0;
     for (int k = 0; k <= fa.bounces; k++) {
         const unsigned live = __ballot_sync(0xffffffffu, alive);
         if (!live) break;
+        const float3 origin = rnd(o64), dir = rnd(d64);
         // bundle of the live rays
         float3 sd = f3(warp_sum(alive ? dir.x : 0.f), warp_sum(alive ? dir.y : 0.f), warp_sum(alive ? dir.z : 0.f));
         float sn = dot3(sd, sd);
@@ -201,8 +203,9 @@ __device__ __forceinline__ void trace_chain_bundle(const ParamScene<MAXS> &ps, c
         }
         int64_t slot_id = 0;
         if (hit_now) {
-            float3 hit = origin + dir * h.t;
-            float3 normal = h.g.w >= 0.f ? normalize3(hit - f3(h.g.x, h.g.y, h.g.z)) : f3(0.f, 1.f, 0.f);
+            D3 p64, n64;
+            refine_hit(o64, d64, sa.geo64, sa.n, h.idx, p64, n64);
+            const float3 hit = rnd(p64), normal = rnd(n64);
             float3 l = normalize3(light - hit);
             float dfs = fmaxf(dot3(normal, l), 0.f);
             float3 hv = l - dir;
@@ -221,8 +224,7 @@ __device__ __forceinline__ void trace_chain_bundle(const ParamScene<MAXS> &ps, c
                 exhausted = 1;
                 alive = false;
             } else {
-                origin = hit + normal * 1e-3f;
-                dir = dir - normal * (2.f * dot3(normal, dir));
+                reflect64(p64, n64, o64, d64);
             }
         }
         const unsigned hb = __ballot_sync(0xffffffffu, hit_now);

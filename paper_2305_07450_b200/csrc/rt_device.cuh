@@ -87,6 +87,7 @@ struct SceneArgs {
     R lc[3];
     R ambient;
     const double *host_geo;  // host copy of geo (float64), for launch-parameter scene packing
+    const double *geo64;     // device geo in float64 (the FP32 kernels' ray chain refines its hits with it)
 };
 
 // Wavefront queues (render_wave_f32.cu); slot = bounce * n_pix + local pixel.

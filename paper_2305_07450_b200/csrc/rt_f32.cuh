@@ -43,20 +43,90 @@ __device__ __forceinline__ float3 normalize3(float3 a) {
     return a * inv;
 }
 
-// camera.py:46-77 in float64, then rounded
-__device__ __forceinline__ float3 primary_direction(int xi, int yi, const FrameArgs &fa) {
-    // float64 throughout (u, v, normalisation, pitch/yaw rotation), one FMA per
-    // NDC coordinate and a reciprocal square root instead of the reference's
-    // five divisions and a square root; rounded to float at the end
+// --- the ray chain in float64 -------------------------------------------------------
+// A bounce chain is sensitive to its rays' rounding: a primary direction
+// merely rounded to float32 moves 0.07% of C5's pixels (and 0.2% of C2's)
+// more than 1e-4 relative away from the reference (tools/precision_probe.py).
+// So the FP32 kernels carry each ray's origin and direction in float64 —
+// the primary direction, the hit point and normal of every closest hit, the
+// reflected ray — exactly as the reference forms them; the body search, the
+// shadow tests and the shading run in FP32 on the rounded values (their
+// rounding measured harmless: < 0.004% of pixels).
+struct D3 {
+    double x, y, z;
+};
+__device__ __forceinline__ float3 rnd(D3 a) { return make_float3((float)a.x, (float)a.y, (float)a.z); }
+
+// float64 square root, reciprocal and reciprocal square root from an FP32
+// estimate and one Newton step (relative error ~1e-14, far below the float32
+// rounding the chain exists to avoid; a handful of DFMAs instead of the
+// IEEE sequences).  Arguments are finite, positive and within FP32 range.
+__device__ __forceinline__ double sqrt64(double x) {
+    const float sf = sqrtf((float)x);
+    if (!(sf > 0.f)) return 0.0;
+    const double s0 = (double)sf;
+    return fma(fma(-s0, s0, x), (double)(0.5f / sf), s0);
+}
+__device__ __forceinline__ double rsqrt64(double x) {
+    const double y = (double)rsqrtf((float)x);
+    return y * fma(-0.5 * x * y, y, 1.5);
+}
+__device__ __forceinline__ double div64(double a, double b) {
+    const double r = (double)(1.f / (float)b);
+    const double q = a * r;
+    return fma(fma(-q, b, a), r, q);
+}
+
+// camera.py:46-77 in float64: one FMA per NDC coordinate and a reciprocal
+// square root instead of the reference's five divisions and a square root
+__device__ __forceinline__ D3 primary_direction64(int xi, int yi, const FrameArgs &fa) {
     const double u = fma((double)xi, fa.ndc[0], fa.ndc[1]);
     const double v = fma((double)yi, fa.ndc[2], fa.ndc[3]);
-    const double inv = rsqrt(fma(u, u, fma(v, v, fa.vdist * fa.vdist)));
+    const double inv = rsqrt64(fma(u, u, fma(v, v, fa.vdist * fa.vdist)));
     const double dx = u * inv, dy = v * inv, dz = fa.vdist * inv;
     const double y2 = dy * fa.cb - dz * fa.sb;
     const double z2 = dy * fa.sb + dz * fa.cb;
     const double x2 = dx * fa.ca + z2 * fa.sa;
     const double z3 = -dx * fa.sa + z2 * fa.ca;
-    return f3((float)x2, (float)y2, (float)z3);
+    return D3{x2, y2, z3};
+}
+
+// camera.py:46-77 in float64, then rounded
+__device__ __forceinline__ float3 primary_direction(int xi, int yi, const FrameArgs &fa) {
+    return rnd(primary_direction64(xi, yi, fa));
+}
+
+// A closest hit found by the FP32 search, redone in float64 on the body's
+// float64 geometry (geo64: the reference's packed {c, r^2} / {0, h, 0, -1}
+// per body, then 1/r per body): the distance (geometry.py:83-117, the
+// perpendicular formed cancellation-free; a graze the float64 test would call
+// a miss counts as the FP32 search's hit), the hit point o + t d and the
+// normal (renderer.py:141-151).  reflect64 then forms the reflected ray
+// (renderer.py:178-183: origin p + 1e-3 n, direction d - 2 (n.d) n).
+__device__ __forceinline__ void refine_hit(D3 o, D3 d, const double *__restrict__ geo64, int n_bodies, int idx, D3 &p,
+                                           D3 &n) {
+    const double2 g01 = __ldg(reinterpret_cast<const double2 *>(geo64) + 2 * idx);
+    const double2 g23 = __ldg(reinterpret_cast<const double2 *>(geo64) + 2 * idx + 1);
+    if (g23.y >= 0.0) {
+        const double lx = g01.x - o.x, ly = g01.y - o.y, lz = g23.x - o.z;
+        const double tca = fma(lz, d.z, fma(ly, d.y, lx * d.x));
+        const double px = fma(-tca, d.x, lx), py = fma(-tca, d.y, ly), pz = fma(-tca, d.z, lz);
+        const double rad = fma(-pz, pz, fma(-py, py, fma(-px, px, g23.y)));
+        const double t = fmax(tca - sqrt64(fmax(rad, 0.0)), 0.0);
+        p = D3{fma(d.x, t, o.x), fma(d.y, t, o.y), fma(d.z, t, o.z)};
+        const double inv_r = __ldg(geo64 + 4 * n_bodies + idx);
+        n = D3{(p.x - g01.x) * inv_r, (p.y - g01.y) * inv_r, (p.z - g23.x) * inv_r};
+    } else {
+        const double t = div64(g01.y - o.y, d.y);
+        p = D3{fma(d.x, t, o.x), fma(d.y, t, o.y), fma(d.z, t, o.z)};
+        n = D3{0.0, 1.0, 0.0};
+    }
+}
+
+__device__ __forceinline__ void reflect64(D3 p, D3 n, D3 &o, D3 &d) {
+    o = D3{fma(n.x, 1e-3, p.x), fma(n.y, 1e-3, p.y), fma(n.z, 1e-3, p.z)};
+    const double k = 2.0 * fma(n.z, d.z, fma(n.y, d.y, n.x * d.x));
+    d = D3{fma(-k, n.x, d.x), fma(-k, n.y, d.y), fma(-k, n.z, d.z)};
 }
 
 // geometry.py:83-105 — distance to the sphere, +inf on a miss.

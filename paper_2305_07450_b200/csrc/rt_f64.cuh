@@ -4,6 +4,7 @@
 // -fmad=false: numba compiles the reference without FMA contraction.
 #pragma once
 #include "rt_device.cuh"
+#include "rt_pow.cuh"
 
 namespace rt64 {
 using namespace rt;
@@ -135,7 +136,7 @@ __device__ __forceinline__ void hit_terms(d3 normal, d3 l, d3 dir, double refl, 
     } else {
         double dd = (normal.x * hx + normal.y * hy + normal.z * hz) / hm;
         if (dd < 0.0) dd = 0.0;
-        s = pow(dd, refl);
+        s = rtpow::pow_cr(dd, refl);  // shading.py:73 `d**reflectivity`, rounded like libm (rt_pow.cuh)
     }
 }
 

@@ -5,6 +5,7 @@
 // PAPER.md:562-564), row-block partitioning over devices, and the copy of the
 // finished frame into the caller's host framebuffer.  No pixel is ever
 // computed here: every compute entry point launches a CUDA kernel or fails.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -75,6 +76,7 @@ struct HostScene {
 template <typename R>
 struct DevScene {
     DBuf geo, mat, table;
+    DBuf geo64;  // FP32 scenes: the geometry in float64 too (the kernels' ray chain, refine_hit)
     uint64_t version = ~0ull;
     int table_n = -1;
     double table_radius = NAN;
@@ -358,9 +360,17 @@ int upload_prec(Dev &d, DevScene<R> &ds, const HostScene &s, int samples) {
         std::vector<R> geo(s.geo.begin(), s.geo.end()), mat(s.mat.begin(), s.mat.end());
         int rc;
         if ((rc = ds.geo.ensure(sizeof(R) * geo.size())) || (rc = ds.mat.ensure(sizeof(R) * mat.size()))) return rc;
+        // FP32 kernels: the float64 geometry (refine_hit) — {c, r^2} / {0, h, 0, -1}, then 1/r per body
+        std::vector<double> geo64(s.geo);
+        for (int b = 0; b < s.n; b++) geo64.push_back(s.geo[4 * b + 3] > 0.0 ? 1.0 / std::sqrt(s.geo[4 * b + 3]) : 0.0);
+        if (sizeof(R) != sizeof(double) && (rc = ds.geo64.ensure(sizeof(double) * std::max<size_t>(geo64.size(), 1))))
+            return rc;
         if (!geo.empty()) {
             RT_CK(cudaMemcpyAsync(ds.geo.p, geo.data(), sizeof(R) * geo.size(), cudaMemcpyHostToDevice, d.st));
             RT_CK(cudaMemcpyAsync(ds.mat.p, mat.data(), sizeof(R) * mat.size(), cudaMemcpyHostToDevice, d.st));
+            if (sizeof(R) != sizeof(double))
+                RT_CK(cudaMemcpyAsync(ds.geo64.p, geo64.data(), sizeof(double) * geo64.size(), cudaMemcpyHostToDevice,
+                                      d.st));
         }
         RT_CK(cudaStreamSynchronize(d.st));  // host vectors die at scope exit
         ds.version = s.version;
@@ -426,6 +436,7 @@ rt::SceneArgs<R> scene_args(const Dev &d, const DevScene<R> &ds, const HostScene
     a.light_radius = (R)s.light_radius;
     a.ambient = (R)s.ambient;
     a.host_geo = s.geo.data();
+    a.geo64 = sizeof(R) == sizeof(double) ? (const double *)ds.geo.p : (const double *)ds.geo64.p;
     return a;
 }
 
@@ -831,7 +842,7 @@ int rt_ctx_destroy(rt_ctx *ctx) {
         d.w_work.release();
         d.grid.release();
         for (DBuf *b : {&d.frame, &d.rad, &d.rays_in, &d.rays_out, &d.sky_raw, &d.sky, &d.counters, &d.s32.geo, &d.s32.mat,
-                        &d.s32.table, &d.s64.geo, &d.s64.mat, &d.s64.table})
+                        &d.s32.table, &d.s32.geo64, &d.s64.geo, &d.s64.mat, &d.s64.table})
             b->release();
         for (auto ev : d.ph)
             if (ev) cudaEventDestroy(ev);

@@ -76,5 +76,9 @@ def test_fp64_full_frame_bit_exact(key):
     want_px, want_rad = _want(key)
     px, rad = _render(key, "fp64")
     np.testing.assert_array_equal(px, want_px, err_msg=key)
-    # device pow/atan2/asin may differ from glibc in the last ulp
+    # the Blinn pow is rounded like glibc's (csrc/rt_pow.cuh) except where
+    # glibc misrounds (~1e-3 of calls); device atan2/asin (sky texel index)
+    # may differ from glibc in the last ulp
     np.testing.assert_allclose(rad, want_rad, rtol=0, atol=1e-12, err_msg=key)
+    same = float(np.mean(np.all(rad == want_rad, axis=-1)))
+    print(f"\n{key} fp64: radiance bit-identical on {same:.6%} of pixels")

@@ -619,23 +619,26 @@ __device__ __forceinline__ unsigned conic_blocked_z(float4 A, float4 B, float z0
 
 // The same tests on two samples at once with the paired FP32 instructions
 // (FFMA2 / FADD2: per component exactly fmaf / the add, so each sample's d —
-// and its bit — is the scalar test's).  ab = {a_i, a_i+1, b_i, b_i+1}, rho =
-// {rho_i, rho_i+1} (SamplePairs); returns how many of the two are blocked.
+// and its bit — is the scalar test's).  ab = {a_i, a_i+1, b_i, b_i+1}, nrho =
+// {-rho_i, -rho_i+1} (SamplePairs); returns how many of the two are blocked.
+// -|w|^2 is formed directly from the negated coefficients and table: round to
+// nearest is symmetric, so fma(-p, q, -s) = -fma(p, q, s) and the value is
+// the scalar test's -w2 bit for bit, without two negations per pair.
 struct Conic2 {
-    float2 ax, ay, az, aw, bx, by, bz, bw, b0, b1, b2, z0;
+    float2 ax, ay, az, aw, bx, by, bz, bw, nb0, nb1, nb2, z0;
 };
 __device__ __forceinline__ float2 dup2(float v) { return make_float2(v, v); }
 __device__ __forceinline__ Conic2 make_conic2(float4 A, float4 B, float z0, float b0, float b1, float b2) {
     return Conic2{dup2(A.x), dup2(A.y), dup2(A.z), dup2(A.w), dup2(B.x), dup2(B.y),
-                  dup2(B.z), dup2(B.w), dup2(b0), dup2(b1), dup2(b2), dup2(z0)};
+                  dup2(B.z), dup2(B.w), dup2(-b0), dup2(-b1), dup2(-b2), dup2(z0)};
 }
 template <bool ZTEST>
-__device__ __forceinline__ unsigned conic_blocked2(const Conic2 &c, float4 ab, float2 rho) {
+__device__ __forceinline__ unsigned conic_blocked2(const Conic2 &c, float4 ab, float2 nrho) {
     const float2 a = make_float2(ab.x, ab.y), b = make_float2(ab.z, ab.w);
-    const float2 w2 = __ffma2_rn(c.b1, a, __ffma2_rn(c.b2, b, __fadd2_rn(c.b0, rho)));
+    const float2 nw2 = __ffma2_rn(c.nb1, a, __ffma2_rn(c.nb2, b, __fadd2_rn(c.nb0, nrho)));
     const float2 x = __ffma2_rn(c.ay, a, __ffma2_rn(c.az, b, c.ax));
     const float2 y = __ffma2_rn(c.bx, a, __ffma2_rn(c.by, b, c.aw));
-    const float2 d = __ffma2_rn(x, x, __ffma2_rn(y, y, make_float2(-w2.x, -w2.y)));
+    const float2 d = __ffma2_rn(x, x, __ffma2_rn(y, y, nw2));
     unsigned bx = __float_as_uint(d.x), by = __float_as_uint(d.y);
     if constexpr (ZTEST) {
         const float2 z = __ffma2_rn(c.bz, a, __ffma2_rn(c.bw, b, c.z0));
@@ -646,14 +649,15 @@ __device__ __forceinline__ unsigned conic_blocked2(const Conic2 &c, float4 ab, f
 }
 
 // The disc-sample table in pairs for conic_blocked2, staged after the float4
-// table in shared memory by fused_sample for up to kPairSamples samples; an
-// odd count's last pair is padded with rho = -inf, which never blocks.
+// table in shared memory by fused_sample for up to kPairSamples samples, rho
+// negated; an odd count's last pair is padded with -rho = +inf, which never
+// blocks.
 constexpr int kPairSamples = 1024;
 constexpr int kPairUnroll = 4;  // (2: C2 2.5% slower)
 struct SamplePairs {
     const float4 *ab;
-    const float2 *rho;
-    int n;  // pairs
+    const float2 *nrho;  // {-rho_i, -rho_i+1}
+    int n;               // pairs
 };
 
 // Sampling of one silhouette-form hit (conic_entry): P = {|lo|^2, 2 lo.bu,
@@ -783,10 +787,10 @@ __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArg
             const Conic2 c2 = make_conic2(A, B, r == 3 ? -1.f : 1.f, b0, b1, b2);
             if (__any_sync(act, r >= 2)) {
 #pragma unroll(kPairUnroll)
-                for (int p = 0; p < pairs.n; p++) blocked += conic_blocked2<true>(c2, pairs.ab[p], pairs.rho[p]);
+                for (int p = 0; p < pairs.n; p++) blocked += conic_blocked2<true>(c2, pairs.ab[p], pairs.nrho[p]);
             } else {
 #pragma unroll(kPairUnroll)
-                for (int p = 0; p < pairs.n; p++) blocked += conic_blocked2<false>(c2, pairs.ab[p], pairs.rho[p]);
+                for (int p = 0; p < pairs.n; p++) blocked += conic_blocked2<false>(c2, pairs.ab[p], pairs.nrho[p]);
             }
         } else if (__any_sync(act, r >= 2)) {
             const float z0 = r == 3 ? -1.f : 1.f;
@@ -831,14 +835,14 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_SAMPLE_MIN_BLOCKS : 1
         if (n <= kPairSamples) {
             const int np = (n + 1) / 2;
             float4 *ab = smem_tab_k + n;
-            float2 *rho = reinterpret_cast<float2 *>(ab + np);
+            float2 *nrho = reinterpret_cast<float2 *>(ab + np);
             for (int p = threadIdx.x; p < np; p += blockDim.x) {
                 const float4 t0 = gtab[2 * p];
                 const float4 t1 = 2 * p + 1 < n ? gtab[2 * p + 1] : make_float4(0.f, 0.f, -INFINITY, 0.f);
                 ab[p] = make_float4(t0.x, t1.x, t0.y, t1.y);
-                rho[p] = make_float2(t0.z, t1.z);
+                nrho[p] = make_float2(-t0.z, -t1.z);
             }
-            pairs = SamplePairs{ab, rho, np};
+            pairs = SamplePairs{ab, nrho, np};
         }
     }
     __syncthreads();

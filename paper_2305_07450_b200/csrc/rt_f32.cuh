@@ -55,24 +55,33 @@ __device__ __forceinline__ float3 normalize3(float3 a) {
 struct D3 {
     double x, y, z;
 };
-__device__ __forceinline__ float3 rnd(D3 a) { return make_float3((float)a.x, (float)a.y, (float)a.z); }
+// cvt.rn.f32.f64 as PTX: one F2F.  Under --ftz=true a C cast becomes
+// cvt.rn.ftz, which ptxas emulates with a range test and a predicated
+// multiply per component to flush float denormals; the FTZ arithmetic
+// downstream flushes any denormal it meets anyway.
+__device__ __forceinline__ float d2f(double x) {
+    float r;
+    asm("cvt.rn.f32.f64 %0, %1;" : "=f"(r) : "d"(x));
+    return r;
+}
+__device__ __forceinline__ float3 rnd(D3 a) { return make_float3(d2f(a.x), d2f(a.y), d2f(a.z)); }
 
 // float64 square root, reciprocal and reciprocal square root from an FP32
 // estimate and one Newton step (relative error ~1e-14, far below the float32
 // rounding the chain exists to avoid; a handful of DFMAs instead of the
 // IEEE sequences).  Arguments are finite, positive and within FP32 range.
 __device__ __forceinline__ double sqrt64(double x) {
-    const float sf = sqrtf((float)x);
+    const float sf = sqrtf(d2f(x));
     if (!(sf > 0.f)) return 0.0;
     const double s0 = (double)sf;
     return fma(fma(-s0, s0, x), (double)(0.5f / sf), s0);
 }
 __device__ __forceinline__ double rsqrt64(double x) {
-    const double y = (double)rsqrtf((float)x);
+    const double y = (double)rsqrtf(d2f(x));
     return y * fma(-0.5 * x * y, y, 1.5);
 }
 __device__ __forceinline__ double div64(double a, double b) {
-    const double r = (double)(1.f / (float)b);
+    const double r = (double)(1.f / d2f(b));
     const double q = a * r;
     return fma(fma(-q, b, a), r, q);
 }

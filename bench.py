@@ -639,6 +639,7 @@ FLOP_SHADE = 45
 # instruction counters in profiles/ncu_flops.json (bench line: model_over_counter)
 FLOP_CULL = 40          # one body's cone classification (centre offset, axial/radial split, 2 sqrt, compares)
 FLOP_CONIC = 17         # one silhouette-form sample test (|w|^2, x, y, d: 7 FMA + 1 add; culled sampler)
+FLOP_CONIC_Z = 4        # its terminator test z > 0 (2 FMA), when the sphere is not wholly in front
 FLOP_CONIC_SETUP = 120  # shadow frame, cone and the six coefficients of one (hit, sphere) pair
 
 
@@ -676,7 +677,8 @@ def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True, config_key
         conic_hits, conic_tests = work.get("conic_hits", 0), work.get("conic_tests", 0)
         ray_hits = work["sampled_hits"] - conic_hits
         ray_rays = ray_hits * samples
-        flops["shadow"] = (conic_tests * FLOP_CONIC + conic_hits * FLOP_CONIC_SETUP
+        flops["shadow"] = (conic_tests * FLOP_CONIC + work.get("conic_z_tests", 0) * FLOP_CONIC_Z
+                           + conic_hits * FLOP_CONIC_SETUP
                            + ray_rays * setup + ray_hits * (FLOP_BASIS if samples > 1 else 0)
                            + (work["sphere_tests"] - conic_tests) * FLOP_SPHERE_FULL
                            + work["plane_tests"] * FLOP_PLANE)
@@ -704,8 +706,11 @@ def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True, config_key
     if t:
         traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
         traffic_src = tr.get("_source")
-    # executed FP32 operations per launch from ncu's instruction counters
-    # (FFMA x 2 + FADD + FMUL, paired forms x 2; profiles/ncu_flops.json)
+    # executed operations per launch from ncu's instruction counters
+    # (profiles/ncu_flops.json): FP32 (FFMA x 2 + FADD + FMUL, the paired
+    # forms x 2 per component) plus FP64 (DFMA x 2 + DADD + DMUL) — the trace
+    # kernel carries each ray's origin and direction in float64, so part of
+    # the model's work runs on the FP64 pipe
     counters = _load_profile("ncu_flops.json").get(config_key, {})
     per_kernel = {}
     for k, sh in shares.items():
@@ -716,9 +721,12 @@ def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True, config_key
                              "frac": a / peak if peak else None}
             cf = counters.get(k, {}).get("flops")
             if cf:
-                per_kernel[k]["counter_flops"] = cf
-                per_kernel[k]["counter_achieved"] = cf / (ms * 1e-3) / 1e12
-                per_kernel[k]["model_over_counter"] = flops[k] / cf
+                c64 = counters.get(k, {}).get("fp64_ops", 0.0)
+                per_kernel[k]["counter_flops"] = cf + c64
+                per_kernel[k]["counter_flops_fp32"] = cf
+                per_kernel[k]["counter_flops_fp64"] = c64
+                per_kernel[k]["counter_achieved"] = (cf + c64) / (ms * 1e-3) / 1e12
+                per_kernel[k]["model_over_counter"] = flops[k] / (cf + c64)
     out = {
         "bound": "fp32",
         "kernel": kernel,
@@ -733,7 +741,8 @@ def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True, config_key
         "flops_per_launch": flops[kernel],
         "flops_definition": "algorithmic: SURVEY.md §8d units (sphere test 8/17/19 by exit, plane 2, hit 60, "
                             "primary 36, reflection 18, shade 45, shadow-ray setup 33) x this launch's counts, "
-                            "plus the culled path's own units (cone class 40, silhouette test 17, its setup 120)",
+                            "plus the culled path's own units (cone class 40, silhouette test 17 + 4 with the "
+                            "terminator test, its setup 120)",
         "peak_source": "measured dependent-free FFMA stream on this GPU (rt_fp32_peak_tflops); "
                        "MEASURED_PEAKS.json has no FP32 CUDA-core figure",
         "peak_nominal": NOMINAL_FP32_TFLOPS,

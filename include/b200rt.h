@@ -194,7 +194,8 @@ int rt_set_option(rt_ctx *ctx, const char *name, int32_t value);
  * order: hits, per-hit cull tests, hits that sampled, shadow rays, sphere
  * tests, plane tests, bundle-traced rays, their sphere tests, warps whose
  * bundle did not cull, hits sampled in the silhouette form, their sphere
- * tests, hits sampled by the lane sampler (one lane per hit). */
+ * tests, hits sampled by the lane sampler (one lane per hit), silhouette
+ * tests with the terminator (z) test. */
 int rt_work_counts(rt_ctx *ctx, uint64_t *out, int32_t n, int32_t reset);
 
 /* Device time (CUDA events) of the render kernels of the last rt_render_v1 /

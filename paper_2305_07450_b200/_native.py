@@ -163,10 +163,10 @@ class Context:
         check(load().rt_set_option(self.handle, name.encode(), int(value)), "rt_set_option")
 
     def work_counts(self, reset: bool = True) -> dict:
-        arr = (ctypes.c_uint64 * 12)()
-        check(load().rt_work_counts(self.handle, arr, 12, int(reset)), "rt_work_counts")
         keys = ("hits", "cull_tests", "sampled_hits", "shadow_rays", "sphere_tests", "plane_tests", "trace_rays",
-                "trace_tests", "trace_unculled_warps", "conic_hits", "conic_tests", "lane_hits")
+                "trace_tests", "trace_unculled_warps", "conic_hits", "conic_tests", "lane_hits", "conic_z_tests")
+        arr = (ctypes.c_uint64 * len(keys))()
+        check(load().rt_work_counts(self.handle, arr, len(keys), int(reset)), "rt_work_counts")
         return dict(zip(keys, (int(v) for v in arr)))
 
     def last_kernel_ms(self) -> float:

@@ -805,6 +805,7 @@ __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArg
             if (r != 0) {
                 atomicAdd(wa.work + kWorkConicHits, 1ull);
                 atomicAdd(wa.work + kWorkConicTests, (unsigned long long)n);
+                if (r >= 2) atomicAdd(wa.work + kWorkConicZTests, (unsigned long long)n);
             }
             atomicAdd(wa.work + kWorkSampledHits, 1ull);
             atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);
@@ -907,6 +908,7 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_SAMPLE_MIN_BLOCKS : 1
             if (code != 0) {
                 atomicAdd(wa.work + kWorkConicHits, 1ull);
                 atomicAdd(wa.work + kWorkConicTests, (unsigned long long)n * nsph);
+                atomicAdd(wa.work + kWorkConicZTests, (unsigned long long)n * __popc((code >> 3) & 15));
             }
             atomicAdd(wa.work + kWorkSampledHits, 1ull);
             atomicAdd(wa.work + kWorkShadowRays, (unsigned long long)n);

@@ -138,7 +138,8 @@ struct WaveArgs64 {
 
 // executed-work tallies of the culled shadow kernel (rt_work_counts)
 enum { kWorkHits = 0, kWorkCullTests, kWorkSampledHits, kWorkShadowRays, kWorkSphereTests, kWorkPlaneTests,
-       kWorkTraceRays, kWorkTraceTests, kWorkTraceFullWarps, kWorkConicHits, kWorkConicTests, kWorkLaneHits, kWorkN };
+       kWorkTraceRays, kWorkTraceTests, kWorkTraceFullWarps, kWorkConicHits, kWorkConicTests, kWorkLaneHits,
+       kWorkConicZTests, kWorkN };
 constexpr int kParamSpheres = 512;  // scenes up to this many spheres ride in the launch parameters (~15 KB)
 constexpr int kParamMid = 256;      // the culled path's middle size (smaller parameter block and masks)
 constexpr int kMaskWords = kParamSpheres / 32;

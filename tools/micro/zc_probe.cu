@@ -90,6 +90,29 @@ int main(int argc, char **argv) {
                bytes / (best * 1e-3) / 1e9);
     };
     printf("frame %dx%d, %.2f MB\n", w, h, bytes / 1e6);
+    {
+        cudaStream_t s2[4];
+        cudaEvent_t f[4];
+        for (int i = 0; i < 4; i++) {
+            CK(cudaStreamCreateWithFlags(&s2[i], cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&f[i], cudaEventDisableTiming));
+        }
+        for (int k : {2, 3, 4}) {
+            char name[64];
+            snprintf(name, sizeof name, "cudaMemcpyAsync D2H as %d concurrent parts", k);
+            time_it(name, [&] {
+                CK(cudaEventRecord(f[0], st));
+                for (int i = 0; i < k; i++) {
+                    CK(cudaStreamWaitEvent(s2[i], f[0], 0));
+                    const size_t a = bytes * i / k / 16 * 16, b = bytes * (i + 1) / k / 16 * 16;
+                    CK(cudaMemcpyAsync((char *)host + a, (char *)dev + a, (i == k - 1 ? bytes : b) - a,
+                                       cudaMemcpyDeviceToHost, s2[i]));
+                    CK(cudaEventRecord(f[i], s2[i]));
+                }
+                for (int i = 0; i < k; i++) CK(cudaStreamWaitEvent(st, f[i], 0));
+            });
+        }
+    }
     time_it("cudaMemcpyAsync D2H (pinned)", [&] { CK(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, st)); });
     time_it("zero-copy 8x4 patches (32 B segments)",
             [&] { patch_store<<<dim3((w + 15) / 16, (h + 7) / 8), 128, 0, st>>>(hdev, w, h); });

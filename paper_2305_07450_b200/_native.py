@@ -219,6 +219,8 @@ class _Pins:
         if addr in self._order:
             self._order.remove(addr)
         if e is not None and e[3]:
+            if load is None or ctypes is None:  # interpreter shutdown: the process releases the pages
+                return
             load().rt_host_unregister(None, ctypes.c_void_p(addr))
 
     def _finalize(self, addr, ref):

@@ -66,10 +66,10 @@ struct HostScene {
     double light[3] = {0, 0, 0}, light_radius = 1, lc[3] = {1, 1, 1}, ambient = 0.15, max_refl = 128;
     std::vector<char> key;  // bytes compared to detect a changed scene
     uint64_t version = 0;
-    // skybox: the caller's array and the copy of its texels last uploaded
+    // skybox: the caller's array and the hash of the texels last uploaded
     const float *sky_ptr = nullptr;
     int sky_w = 1, sky_h = 1, has_sky = 0;
-    std::vector<float> sky_shadow;
+    uint64_t sky_hash = 0;
     uint64_t sky_version = 0;
 };
 
@@ -213,52 +213,83 @@ std::vector<double> disc_table(int n, double radius) {
 
 // The skybox is read by the reference on every frame (renderer.py:282-300),
 // so an in-place edit of its texels must show in the next frame.  The
-// library keeps a host copy of the texels it uploaded (`sky_shadow`) and
-// compares the caller's array with it in full, bit for bit, on every frame
-// that reuses the same array: exact, and split over up to kSkyThreads host
-// threads (25 MB: ~0.2-0.35 ms on 8 cores of the B200 host,
-// tools/micro/host_compare.c).  rt_render_v1 runs the compare while the
-// frame's kernels execute (the frame is rendered with the device copy); a
-// difference re-uploads the sky and renders the frame again before the call
-// returns.
+// library hashes the caller's texels in full on every frame that reuses the
+// same array and compares the hash with that of the texels it uploaded: a
+// 64-bit xxh64-style hash (four multiply-rotate lanes per chunk, chunks
+// chained in order, so content and position both count), computed over all
+// host cores — it reads the array once, where comparing against a kept copy
+// read twice the bytes (C3 end to end: the 25 MB compare was the bottleneck,
+// 310-470 us by thread count, tools/micro/host_hash.c).  rt_render_v1 runs the
+// hash while the frame's kernels execute (the frame is rendered with the
+// device copy); a different hash re-uploads the sky and renders the frame
+// again before the call returns.
 int sky_threads() {
     static int t = [] {
         if (const char *e = std::getenv("B200RT_SKY_THREADS")) return std::max(1, std::atoi(e));
-        return std::max(1, std::min(8, omp_get_num_procs() / 2));
+        return std::max(1, omp_get_num_procs());
     }();
     return t;
 }
 
-// true when a and b differ anywhere (n floats, bitwise)
-bool texels_differ(const float *a, const float *b, size_t n) {
-    const size_t bytes = sizeof(float) * n;
-    const int chunks = 4 * sky_threads();
-    int diff = 0;
-#pragma omp parallel for num_threads(sky_threads()) schedule(static) reduction(| : diff)
-    for (int k = 0; k < chunks; k++) {
-        const size_t lo = bytes * k / chunks, hi = bytes * (k + 1) / chunks;
-        diff |= std::memcmp((const char *)a + lo, (const char *)b + lo, hi - lo) != 0;
+constexpr uint64_t kP1 = 0x9E3779B185EBCA87ull, kP2 = 0xC2B2AE3D27D4EB4Full, kP3 = 0x165667B19E3779F9ull,
+                   kP4 = 0x85EBCA77C2B2AE63ull;
+inline uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+inline uint64_t hround(uint64_t acc, uint64_t w) { return rotl64(acc + w * kP2, 31) * kP1; }
+inline uint64_t hmerge(uint64_t h, uint64_t v) { return (h ^ hround(0, v)) * kP1 + kP4; }
+
+// xxh64-style hash of n bytes (n a multiple of 4) at p with a seed
+uint64_t hash_bytes(const char *p, size_t n, uint64_t seed) {
+    uint64_t v1 = seed + kP1 + kP2, v2 = seed + kP2, v3 = seed, v4 = seed - kP1;
+    size_t i = 0;
+    for (; i + 32 <= n; i += 32) {
+        uint64_t w[4];
+        std::memcpy(w, p + i, 32);
+        v1 = hround(v1, w[0]);
+        v2 = hround(v2, w[1]);
+        v3 = hround(v3, w[2]);
+        v4 = hround(v4, w[3]);
     }
-    return diff != 0;
+    uint64_t h = rotl64(v1, 1) + rotl64(v2, 7) + rotl64(v3, 12) + rotl64(v4, 18);
+    h = hmerge(hmerge(hmerge(hmerge(h, v1), v2), v3), v4) + n;
+    for (; i + 8 <= n; i += 8) {
+        uint64_t w;
+        std::memcpy(&w, p + i, 8);
+        h = rotl64(h ^ hround(0, w), 27) * kP1 + kP4;
+    }
+    for (; i + 4 <= n; i += 4) {
+        uint32_t w;
+        std::memcpy(&w, p + i, 4);
+        h = rotl64(h ^ (uint64_t)w * kP1, 23) * kP2 + kP3;
+    }
+    h ^= h >> 33;
+    h *= kP2;
+    h ^= h >> 29;
+    h *= kP3;
+    return h ^ (h >> 32);
 }
 
-void copy_texels(float *dst, const float *src, size_t n) {
+// the texels' hash: chunks on all host threads, chained in chunk order
+uint64_t texel_hash(const float *a, size_t n) {
     const size_t bytes = sizeof(float) * n;
     const int chunks = 4 * sky_threads();
+    std::vector<uint64_t> part(chunks);
 #pragma omp parallel for num_threads(sky_threads()) schedule(static)
     for (int k = 0; k < chunks; k++) {
-        const size_t lo = bytes * k / chunks, hi = bytes * (k + 1) / chunks;
-        std::memcpy((char *)dst + lo, (const char *)src + lo, hi - lo);
+        const size_t lo = bytes * k / chunks / 4 * 4, hi = bytes * (k + 1) / chunks / 4 * 4;
+        part[k] = hash_bytes((const char *)a + lo, (k == chunks - 1 ? bytes : hi) - lo, (uint64_t)k);
     }
+    uint64_t h = 0x27D4EB2F165667C5ull;
+    for (int k = 0; k < chunks; k++) h = hround(h, part[k] ^ (uint64_t)k);
+    return h ^ bytes;
 }
 
 // The caller's texels (same array as the last frame's) against the uploaded
-// copy; on a difference the copy is refreshed and the sky version bumped.
+// ones; on a difference the sky version is bumped (upload_sky re-uploads).
 bool sky_content_changed(HostScene &s) {
     if (!s.has_sky || !s.sky_ptr) return false;
-    const size_t n = (size_t)s.sky_w * s.sky_h * 3;
-    if (!texels_differ(s.sky_ptr, s.sky_shadow.data(), n)) return false;
-    copy_texels(s.sky_shadow.data(), s.sky_ptr, n);
+    const uint64_t h = texel_hash(s.sky_ptr, (size_t)s.sky_w * s.sky_h * 3);
+    if (h == s.sky_hash) return false;
+    s.sky_hash = h;
     s.sky_version++;
     return true;
 }
@@ -333,21 +364,14 @@ bool set_host_scene(HostScene &s, int32_t n, const int32_t *kinds, const double 
         s.max_refl = max_refl;
         s.version++;
     }
-    // a different array (or none): a new sky, uploaded from a fresh copy;
-    // the same array: its content is compared in full (sky_content_changed)
+    // a different array (or none): a new sky, hashed and uploaded; the same
+    // array: its content is hashed in full again (sky_content_changed)
     if (has_sky != s.has_sky || (has_sky && (sky != s.sky_ptr || sky_w != s.sky_w || sky_h != s.sky_h))) {
         s.has_sky = has_sky;
         s.sky_ptr = has_sky ? sky : nullptr;
         s.sky_w = has_sky ? sky_w : 1;
         s.sky_h = has_sky ? sky_h : 1;
-        if (has_sky) {
-            const size_t n = (size_t)sky_w * sky_h * 3;
-            s.sky_shadow.resize(n);
-            copy_texels(s.sky_shadow.data(), sky, n);
-        } else {
-            s.sky_shadow.clear();
-            s.sky_shadow.shrink_to_fit();
-        }
+        s.sky_hash = has_sky ? texel_hash(sky, (size_t)sky_w * sky_h * 3) : 0;
         s.sky_version++;
         return false;
     }
@@ -403,7 +427,8 @@ int upload_sky(rt_ctx *ctx, Dev &d) {
     if (s.has_sky) {
         int64_t n = (int64_t)s.sky_w * s.sky_h;
         if ((rc = d.sky_raw.ensure(sizeof(float) * 3 * n)) || (rc = d.sky.ensure(sizeof(float4) * n))) return rc;
-        RT_CK(cudaMemcpyAsync(d.sky_raw.p, s.sky_shadow.data(), sizeof(float) * 3 * n, cudaMemcpyHostToDevice, d.st));
+        // from the caller's array, whose hash is s.sky_hash (the call is synchronous: it does not change meanwhile)
+        RT_CK(cudaMemcpyAsync(d.sky_raw.p, s.sky_ptr, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, d.st));
         sky_to_float4<<<(unsigned)((n + 255) / 256), 256, 0, d.st>>>((const float *)d.sky_raw.p, (float4 *)d.sky.p,
                                                                    n);
         RT_CK(cudaGetLastError());
@@ -415,6 +440,20 @@ int upload_sky(rt_ctx *ctx, Dev &d) {
         RT_CK(cudaMemsetAsync(d.sky.p, 0, sizeof(float4), d.st));
     }
     d.sky_version = s.sky_version;
+    return RT_OK;
+}
+
+// Every device's sky up to date before a call returns: the library keeps no
+// host copy of the texels (only their hash), so a device that did not take
+// part in this call's frame must not be left to upload later from an array
+// the caller may since have freed.
+int upload_sky_all(rt_ctx *ctx) {
+    int rc;
+    for (Dev &d : ctx->devs) {
+        if (d.sky_version == ctx->scene.sky_version) continue;
+        RT_CK(cudaSetDevice(d.id));
+        if ((rc = upload_sky(ctx, d))) return rc;
+    }
     return RT_OK;
 }
 
@@ -1064,9 +1103,9 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
                                            light_radius, light_color, ambient, max_refl, sky, sky_w, sky_h, has_sky);
     const int n_dev = std::min<int>((int)ctx->devs.size(), n_parts);
     // The frame is enqueued with the device's copy of the sky; when the
-    // caller passed the same sky array as before, its texels are compared in
-    // full with that copy while the kernels run, and on a difference the sky
-    // is uploaded again and the frame rendered again.
+    // caller passed the same sky array as before, its texels are hashed in
+    // full while the kernels run, and on a different hash the sky is uploaded
+    // again and the frame rendered again.
     for (int attempt = 0;; attempt++) {
         if ((rc = enqueue_frame(ctx, n_dev, pixels, radiance, width, height, cam_pos, yaw, pitch, vdist,
                                 shadow_samples, bounce_limit, n_parts, precision)))
@@ -1074,7 +1113,8 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
         if (attempt > 0 || !verify_sky || !sky_content_changed(ctx->scene)) break;
         if ((rc = finish_frame(ctx, n_dev))) return rc;  // the stale frame ends before the sky is replaced
     }
-    return finish_frame(ctx, n_dev);
+    if ((rc = finish_frame(ctx, n_dev))) return rc;
+    return upload_sky_all(ctx);
 }
 
 int rt_render_device_v1(rt_ctx *ctx, int32_t slot, uint32_t *d_out, int64_t out_pitch, void *d_radiance,
@@ -1135,7 +1175,7 @@ int rt_trace_rays_v1(rt_ctx *ctx, const double *origins, const double *dirs, int
     if (set_host_scene(ctx->scene, n_bodies, kinds, positions, sizes, colors, refls, light_pos, light_radius,
                        light_color, ambient, max_refl, sky, sky_w, sky_h, has_sky))
         sky_content_changed(ctx->scene);
-    if (n_rays == 0) return RT_OK;
+    if (n_rays == 0) return upload_sky_all(ctx);
     Dev &d = ctx->devs[0];
     if ((rc = prepare(ctx, d, precision, shadow_samples))) return rc;
     size_t in_b = sizeof(double) * 3 * (size_t)n_rays;
@@ -1158,7 +1198,7 @@ int rt_trace_rays_v1(rt_ctx *ctx, const double *origins, const double *dirs, int
     RT_CK(cudaMemcpyAsync(out_rgb, d.rays_out.p, out_b, cudaMemcpyDeviceToHost, d.st));
     RT_CK(cudaStreamSynchronize(d.st));
     RT_CK(cudaEventElapsedTime(&ctx->last_ms, d.e0, d.e1));
-    return RT_OK;
+    return upload_sky_all(ctx);
 }
 
 int rt_sky_sample_v1(rt_ctx *ctx, const double *dirs, int64_t n, double *out_rgb, const float *sky, int32_t sky_w,
@@ -1368,7 +1408,7 @@ int rt_render_async_v1(rt_ctx *ctx, int32_t slot, uint32_t *pixels, int32_t widt
         RT_CK(cudaEventSynchronize(d.slot_done[slot]));  // the stale frame ends before the sky is replaced
     }
     d.slot_busy[slot] = true;
-    return RT_OK;
+    return upload_sky_all(ctx);
 }
 
 int rt_frame_wait_v1(rt_ctx *ctx, int32_t slot) {

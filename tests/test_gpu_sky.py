@@ -1,7 +1,9 @@
 """The skybox is read by the reference on every frame (renderer.py:282-300):
 an in-place edit of `Skybox.texels` between two frames must show in the
-second frame.  The library compares the caller's array with its uploaded copy
-in full on every frame (rt_host.cu: sky_content_changed)."""
+second frame.  The library hashes the caller's array in full on every frame
+and compares the hash with that of the texels it uploaded (rt_host.cu:
+sky_content_changed); the hash sees content and position, so swapped texels
+are a change too."""
 
 import math
 
@@ -32,7 +34,7 @@ def _setup():
     scene, cam = cfg.scene(), cfg.camera()
     sky = scene.skybox
     # a sky pixel of the top row and the texel it samples, chosen so that its
-    # float index is not on the old sampled signature's stride (n / 4099)
+    # float index is not on the round-1 sampled signature's stride (n / 4099)
     n = sky.texels.size
     stride = max(1, n // 4099)
     xs = np.arange(W, dtype=np.int32)
@@ -89,3 +91,39 @@ def test_in_place_texel_edit_pipelined():
     want = _want(scene, cam, params)
     assert parity.byte_gate(b.pixels[px:px + 1], want[px:px + 1])[1] <= 1 and a.pixels[px] != b.pixels[px]
     parity.assert_byte_gate(b.pixels, want, "pipelined sky edit")
+
+
+def test_swapped_texels_are_a_change():
+    """Exchanging the sampled texel with another one (same multiset of
+    values, new positions) must be seen: the hash is position-sensitive."""
+    scene, cam, params, px, tx, ty = _setup()
+    sky = scene.skybox
+    fb = rt.Framebuffer.create(W, H)
+    rt.render_frame(scene, cam, params, fb, precision="fp64")
+    before = fb.pixels.copy()
+    ox = (tx + sky.width // 2) % sky.width  # a texel no top-row pixel samples
+    a, b = sky.texels[ty, tx].copy(), sky.texels[ty, ox].copy()
+    assert not np.array_equal(a, b)
+    sky.texels[ty, tx], sky.texels[ty, ox] = b, a
+    want = _want(scene, cam, params)
+    rt.render_frame(scene, cam, params, fb, precision="fp64")
+    np.testing.assert_array_equal(fb.pixels, want)
+    assert fb.pixels[px] != before[px]
+
+
+def test_new_sky_array_after_the_old_one_is_freed():
+    """The library keeps no copy of the texels: a frame after the caller
+    replaced (and freed) its sky array renders the new one."""
+    scene, cam, params, px, tx, ty = _setup()
+    fb = rt.Framebuffer.create(W, H)
+    rt.render_frame(scene, cam, params, fb, precision="fp64")
+    old = scene.skybox
+    t = old.texels.copy()
+    t[ty, tx] = (0.2, 0.9, 0.3)
+    scene.skybox = rt.Skybox(old.width, old.height, t)
+    del old
+    import gc
+
+    gc.collect()
+    rt.render_frame(scene, cam, params, fb, precision="fp64")
+    np.testing.assert_array_equal(fb.pixels, _want(scene, cam, params))

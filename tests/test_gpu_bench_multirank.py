@@ -1,0 +1,42 @@
+"""The N > 1 benchmark path (bench.py under torchrun: one C4 frame split in
+8-row round-robin bands, every rank storing its rows into rank 0's device
+frame through CUDA IPC, the host gathers, whole-frame sharding) run end to
+end as two ranks sharing the one B200 of this box over host (gloo)
+collectives (B200RT_BENCH_SHARE_GPU=1): a functional check of the
+multi-GPU code path — no kernel waits on another rank's — whose frames must
+equal a one-GPU render.  Never a measurement."""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_two_rank_bench_row_bands():
+    env = dict(os.environ, B200RT_BENCH_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps",
+           "2", "--warmup", "3", "--no-extra", "--no-cpu-baseline"]
+    proc = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
+    lines = [l for l in proc.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, proc.stdout[-3000:]  # rank 0 alone prints
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["config"]["workload"].startswith("C4")
+    text = json.dumps(d)
+    assert '"frame_matches_single_gpu_render": true' in text, text[:2000]
+    assert d["e2e"]["value"] > 0 and d["whole_frames"]

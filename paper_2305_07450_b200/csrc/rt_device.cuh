@@ -59,6 +59,7 @@ struct MegaCull {
     const unsigned *grid;
     float grid_lo[3], grid_inv[3];
     int grid_dim[3];
+    int4 hot;  // the tile kernel's hot tile rectangle (tile_of_block); x < 0: bottom rows first
 };
 
 // The spheres whose primary-ray box holds pixel (x, y) (all when no boxes).
@@ -120,6 +121,7 @@ struct WaveArgs {
                        // sphere wholly in front, 1: not), row r (0: {p, slot}, 1: {n, sphere}) at
                        // [(2q + r) lane_cap]; lengths count[3] and count[0]
     unsigned lane_cap; // (0: off)
+    int4 hot;          // the trace's hot tile rectangle (tile_of_block); x < 0: bottom rows first
 };
 // FP64 culled wavefront (render_fused_f64.cu): queues in float64
 constexpr int kMaxBodies64 = 256;
@@ -193,6 +195,52 @@ __device__ __forceinline__ void thread_pixel_bottom_first(int &x, int &ly) {
     int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     x = blockIdx.x * kTileW + (warp & 1) * 8 + (lane & 7);
     ly = (gridDim.y - 1 - blockIdx.y) * kTileH + (warp >> 1) * 4 + (lane >> 3);
+}
+
+// Tile dispatch order with a hot rectangle (tiles [h.x, h.z] x [h.y, h.w],
+// local tile rows): the hot tiles first, then the rest; each part bottom row
+// first.  h.x < 0: bottom first over the whole grid.  A bijection of the
+// linear block index onto the tiles (the hardware dispatches CTAs in
+// index order): the costliest tiles start early and the cheap ones fill the
+// last wave.
+__device__ __forceinline__ void tile_of_block(int4 h, int &tx, int &ty) {
+    const int W = gridDim.x, H = gridDim.y, b = blockIdx.y * W + blockIdx.x;
+    if (h.x < 0) {
+        tx = blockIdx.x;
+        ty = H - 1 - blockIdx.y;
+        return;
+    }
+    const int rw = h.z - h.x + 1, rh = h.w - h.y + 1, area = rw * rh;
+    if (b < area) {
+        tx = h.x + b % rw;
+        ty = h.w - b / rw;
+        return;
+    }
+    int j = b - area;
+    const int below = (H - 1 - h.w) * W;  // full rows under the rectangle
+    if (j < below) {
+        ty = H - 1 - j / W;
+        tx = j % W;
+        return;
+    }
+    j -= below;
+    const int side = W - rw, beside = side * rh;  // the rectangle's rows, left and right of it
+    if (j < beside) {
+        ty = h.w - j / side;
+        const int k = j % side;
+        tx = k < h.x ? k : k + rw;
+        return;
+    }
+    j -= beside;
+    ty = h.y - 1 - j / W;  // full rows above it
+    tx = j % W;
+}
+__device__ __forceinline__ void thread_pixel_hot_first(int4 h, int &x, int &ly) {
+    int tx, ty;
+    tile_of_block(h, tx, ty);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    x = tx * kTileW + (warp & 1) * 8 + (lane & 7);
+    ly = ty * kTileH + (warp >> 1) * 4 + (lane >> 3);
 }
 
 // renderer.py:45-50.  rgba = 0: 0xAARRGGBB (the reference's Framebuffer,

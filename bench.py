@@ -194,6 +194,11 @@ def run_reference(args):
                          "sample": sample},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    # the reference's own numba render_frame on the same cores, for context:
+    # the C port above is the conservative (faster) stand-in
+    nb = numba_reference(args.config)
+    if nb:
+        line["numba_reference"] = nb
     print(json.dumps(line), flush=True)
     return 0
 
@@ -213,6 +218,23 @@ def _dist_env():
 CPU_PROTOCOL = {"C1": (100, 10, None), "P720": (100, 10, None), "P1080": (100, 10, None), "P4K": (100, 10, None),
                 "C2": (1, 3, None), "C3": (1, 3, None), "C4": (1, 3, None), "C5": (1, 3, (384, 216)),
                 "C5_512": (1, 3, (384, 216))}
+
+
+def numba_reference(key, frames=2, timeout=240):
+    """The unmodified reference's own render_frame (numba, pip-installed into
+    baseline/_ref) on all host cores, in a subprocess (tools/
+    numba_reference_time.py): whole frames after the JIT warm-up.  None when
+    the reference is not installed or the configuration has no counterpart
+    built by the reference's sceneio (skybox configurations)."""
+    if not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "raytracer")):
+        return None
+    try:
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "numba_reference_time.py"), key,
+                              str(frames)], capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+        lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+        return json.loads(lines[-1]) if out.returncode == 0 and lines else None
+    except (subprocess.TimeoutExpired, OSError, ValueError):
+        return None
 
 
 def cpu_frames(key, threads=0):
@@ -459,10 +481,11 @@ def run_ours(args):
                                     "depth 3, pinned host framebuffers"}
         line.update({
             "value": fps, "ms_per_step": main["total_ms"] / args.steps, "scaling": "weak",
+            # config: the workload keys both arms share (--impl reference prints the same)
             "config": {"workload": cfg.name, "width": cfg.width, "height": cfg.height, "samples": cfg.samples,
-                       "bounces": cfg.bounces, "sky": cfg.sky, "parallelism": "one GPU",
-                       "path": "wavefront + exact per-hit occluder culling (default)",
-                       "l2": "flushed between timed frames (256 MiB memset outside the event pair)"},
+                       "bounces": cfg.bounces, "sky": cfg.sky},
+            "run": {"parallelism": "one GPU", "path": "wavefront + exact per-hit occluder culling (default)",
+                    "l2": "flushed between timed frames (256 MiB memset outside the event pair)"},
             **ray_rates(wcc, work, fps),
             "mrays_definition": "reference_equivalent: the rays the reference's control flow traces for the frame "
                                 "(closest-hit + every shadow sample) / time; executed: closest-hit rays + the shadow "
@@ -507,6 +530,9 @@ def run_ours(args):
         if not args.no_cpu_baseline:
             if key in CPU_PROTOCOL:
                 line["cpu_baseline"] = cpu_frames(key)[1]
+                nb = numba_reference(key)
+                if nb:  # the reference's own numba render_frame on the same cores
+                    line["cpu_baseline"]["numba_reference"] = nb
             else:
                 v, meta = cpu_reference_sample(cfg, args.cpu_seconds)
                 line["cpu_baseline"] = {"value": v, "unit": "frames/s", "cores": meta["threads"], "kind": "port",
@@ -601,11 +627,11 @@ def run_ours(args):
         line.update({
             "value": fps, "ms_per_step": main["total_ms"] / args.steps, "scaling": "strong",
             "config": {"workload": cfg.name, "width": cfg.width, "height": cfg.height, "samples": cfg.samples,
-                       "bounces": cfg.bounces, "sky": cfg.sky,
-                       "parallelism": f"row bands x{world} (8-row blocks round-robin), gathered into rank 0's frame "
-                                      "over NVLink",
-                       "path": "wavefront + exact per-hit occluder culling (default)",
-                       "l2": "flushed between timed frames (256 MiB memset outside the event pair)"},
+                       "bounces": cfg.bounces, "sky": cfg.sky},
+            "run": {"parallelism": f"row bands x{world} (8-row blocks round-robin), gathered into rank 0's frame "
+                                   "over NVLink",
+                    "path": "wavefront + exact per-hit occluder culling (default)",
+                    "l2": "flushed between timed frames (256 MiB memset outside the event pair)"},
             **ray_rates(wc[key], work, fps),
             "e2e": e2e, "gpu_launches": main["launches"], "clocks": main["clocks"], "roofline": roof,
             "phases_ms": phases, "whole_frames": whole})

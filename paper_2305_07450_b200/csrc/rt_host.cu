@@ -1010,11 +1010,12 @@ int enqueue_frame(rt_ctx *ctx, int n_dev, uint32_t *pixels, void *radiance, int3
         cudaGetLastError();  // not registered: a cudaHostGetDevicePointer miss is not an error
         // Bands run on their own prioritised streams (Dev::band_st), so their
         // kernels overlap; what a band costs is its first-band latency and
-        // copy setup, against a copy at 45-56 GB/s (82 us for 720p, 600 us at
-        // 4K).  Measured best (tools/e2e_probe.py): 2 bands at 3.7 MB, 4 at
-        // 8.3 MB, 6 at 33 MB.
+        // copy setup, against a copy at 45-56 GB/s (70 us for 720p, 585 us at
+        // 4K) that also slows the kernels beside it.  Measured
+        // best (tools/e2e_ab.py, round 2): 2 bands at 3.7 and 8.3 MB (C3: 258
+        // us against 280 with 4), 6 at 33 MB.
         const size_t MB = (size_t)1 << 20;
-        int bands = ctx->bands > 0 ? ctx->bands : px_bytes < MB ? 1 : px_bytes < 6 * MB ? 2 : px_bytes < 24 * MB ? 4 : 6;
+        int bands = ctx->bands > 0 ? ctx->bands : px_bytes < MB ? 1 : px_bytes < 24 * MB ? 2 : 6;
         if (ctx->phases) bands = 1;  // phase events describe one frame on one stream
         bands = std::max(1, std::min(bands, height / 8));
         // band boundaries in whole 8-row blocks: band 0 takes band_first

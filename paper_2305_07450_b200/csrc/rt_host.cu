@@ -6,6 +6,7 @@
 // finished frame into the caller's host framebuffer.  No pixel is ever
 // computed here: every compute entry point launches a CUDA kernel or fails.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -105,6 +106,7 @@ struct Dev {
     cudaEvent_t ph[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // wavefront phase boundaries
     cudaStream_t copy_st = nullptr;           // device->host copies of finished row bands
     cudaEvent_t band_ev[kMaxBands] = {};
+    cudaEvent_t copy_ev[kMaxBands] = {};  // a band's copy done (on its own stream)
     // row bands run on their own streams, band 0 at the highest priority: the
     // next band's CTAs fill the SMs a band's tail leaves idle, yet the bands
     // finish in order, so each copy starts as early as it can
@@ -190,6 +192,7 @@ struct rt_ctx {
     bool boxes = true;        // FP32 scenes of <= 8 spheres: primary-ray sphere boxes (with cull)
     int mega_tiles = -1;      // FP32 megakernel: 1 one CTA per tile, 0 persistent warps, -1 by sample count
     bool hot_tiles = true;    // culled FP32 trace: the spheres' tiles dispatched first
+    int band_order = 0;       // copy-overlap bands enqueued 0: top first, 1: bottom first (measured slower)
     std::mutex mu;
     HostScene scene;
     float last_ms = 0.f;
@@ -882,6 +885,7 @@ int rt_ctx_create(rt_ctx **out, const int32_t *devices, int32_t n_devices) {
                   cudaStreamCreateWithFlags(&d.copy_st, cudaStreamNonBlocking) == cudaSuccess &&
                   cudaEventCreate(&d.e0) == cudaSuccess && cudaEventCreate(&d.e1) == cudaSuccess;
         for (auto &ev : d.band_ev) ok = ok && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess;
+        for (auto &ev : d.copy_ev) ok = ok && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess;
         ok = ok && cudaEventCreateWithFlags(&d.fork_ev, cudaEventDisableTiming) == cudaSuccess;
         ok = ok && cudaEventCreateWithFlags(&d.dev_call_ev, cudaEventDisableTiming) == cudaSuccess &&
              cudaEventCreateWithFlags(&d.dev_prep_ev, cudaEventDisableTiming) == cudaSuccess;
@@ -922,6 +926,8 @@ int rt_ctx_destroy(rt_ctx *ctx) {
         for (auto ev : d.ph)
             if (ev) cudaEventDestroy(ev);
         for (auto ev : d.band_ev)
+            if (ev) cudaEventDestroy(ev);
+        for (auto ev : d.copy_ev)
             if (ev) cudaEventDestroy(ev);
         for (auto bs : d.band_st)
             if (bs) cudaStreamDestroy(bs);
@@ -1034,7 +1040,13 @@ int enqueue_frame(rt_ctx *ctx, int n_dev, uint32_t *pixels, void *radiance, int3
         }
         RT_CK(cudaEventRecord(d.e0, d.st));
         if (bands > 1) RT_CK(cudaEventRecord(d.fork_ev, d.st));
-        for (int k = 0; k < bands; k++) {
+        // each band's copy follows its kernels on its own stream, so the
+        // copies start in the order the bands finish (P720 end to end 115 ->
+        // 106 us, C4 692 -> 681 us against one copy stream).  Bands are
+        // enqueued top first; bottom first (option band_order: the costly
+        // rows reach the GPU sooner) measured 10-18% slower end to end
+        for (int i = 0; i < bands; i++) {
+            const int k = ctx->band_order && bands > 1 ? bands - 1 - i : i;
             cudaStream_t bs = bands > 1 ? d.band_st[k] : d.st;
             if (bands > 1) RT_CK(cudaStreamWaitEvent(bs, d.fork_ev, 0));
             const int y0 = y_at[k], y1 = y_at[k + 1];
@@ -1052,17 +1064,22 @@ int enqueue_frame(rt_ctx *ctx, int n_dev, uint32_t *pixels, void *radiance, int3
             }
             RT_CK(cudaEventRecord(d.band_ev[k], bs));
             if (ctx->band_times) RT_CK(cudaEventRecord(d.tl_ev[k], bs));
-            RT_CK(cudaStreamWaitEvent(d.copy_st, d.band_ev[k], 0));
-            if (bands > 1) RT_CK(cudaStreamWaitEvent(d.st, d.band_ev[k], 0));  // the join
+            if (bands > 1) RT_CK(cudaStreamWaitEvent(d.st, d.band_ev[k], 0));  // the join (kernels)
+            cudaStream_t cs = bands > 1 ? bs : d.copy_st;
+            if (bands == 1) RT_CK(cudaStreamWaitEvent(d.copy_st, d.band_ev[k], 0));
             if (y1 > y0) {
                 size_t off = (size_t)y0 * width, cnt = (size_t)(y1 - y0) * width;
                 RT_CK(cudaMemcpyAsync(pixels + off, (uint32_t *)d.frame.p + off, sizeof(uint32_t) * cnt,
-                                      cudaMemcpyDeviceToHost, d.copy_st));
+                                      cudaMemcpyDeviceToHost, cs));
                 if (radiance)
                     RT_CK(cudaMemcpyAsync((char *)radiance + rad_elem * 3 * off, (char *)d.rad.p + rad_elem * 3 * off,
-                                          rad_elem * 3 * cnt, cudaMemcpyDeviceToHost, d.copy_st));
+                                          rad_elem * 3 * cnt, cudaMemcpyDeviceToHost, cs));
             }
-            if (ctx->band_times) RT_CK(cudaEventRecord(d.tl_ev[kMaxBands + k], d.copy_st));
+            if (ctx->band_times) RT_CK(cudaEventRecord(d.tl_ev[kMaxBands + k], cs));
+            if (bands > 1) {  // the copy's end, joined into the copy stream that finish_frame waits for
+                RT_CK(cudaEventRecord(d.copy_ev[k], bs));
+                RT_CK(cudaStreamWaitEvent(d.copy_st, d.copy_ev[k], 0));
+            }
         }
         RT_CK(cudaEventRecord(d.e1, d.st));
         ctx->band_pending = bands;
@@ -1122,12 +1139,18 @@ int finish_frame(rt_ctx *ctx, int n_dev) {
 
 extern "C" {
 
+static bool host_timing() {
+    static const bool on = std::getenv("B200RT_HOST_TIMING") != nullptr;
+    return on;
+}
+
 int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, int32_t height,
                  const double cam_pos[3], double yaw, double pitch, double vdist, int32_t n_bodies,
                  const int32_t *kinds, const double *positions, const double *sizes, const double *colors,
                  const double *refls, const double light_pos[3], double light_radius, const double light_color[3],
                  double ambient, double max_refl, const float *sky, int32_t sky_w, int32_t sky_h, int32_t has_sky,
                  int32_t shadow_samples, int32_t bounce_limit, int32_t n_parts, int32_t precision) {
+    const auto t_call = std::chrono::steady_clock::now();
     if (!ctx || !pixels || !cam_pos) return fail(RT_ERR_INVALID, "null argument");
     int rc = check_frame_args(width, height, shadow_samples, bounce_limit, precision);
     if (rc) return rc;
@@ -1139,6 +1162,7 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
     const bool verify_sky = set_host_scene(ctx->scene, n_bodies, kinds, positions, sizes, colors, refls, light_pos,
                                            light_radius, light_color, ambient, max_refl, sky, sky_w, sky_h, has_sky);
     const int n_dev = std::min<int>((int)ctx->devs.size(), n_parts);
+    const auto t_enq = std::chrono::steady_clock::now();
     // The frame is enqueued with the device's copy of the sky; when the
     // caller passed the same sky array as before, its texels are hashed in
     // full while the kernels run, and on a different hash the sky is uploaded
@@ -1150,7 +1174,14 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
         if (attempt > 0 || !verify_sky || !sky_content_changed(ctx->scene)) break;
         if ((rc = finish_frame(ctx, n_dev))) return rc;  // the stale frame ends before the sky is replaced
     }
+    const auto t_wait = std::chrono::steady_clock::now();
     if ((rc = finish_frame(ctx, n_dev))) return rc;
+    if (host_timing()) {  // $B200RT_HOST_TIMING: where a synchronous call's host time goes
+        const auto t_end = std::chrono::steady_clock::now();
+        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+        fprintf(stderr, "rt_render_v1: setup %.1f us, enqueue %.1f us, wait %.1f us, device e0->e1 %.1f us\n",
+                us(t_call, t_enq), us(t_enq, t_wait), us(t_wait, t_end), 1e3 * ctx->last_ms);
+    }
     return upload_sky_all(ctx);
 }
 
@@ -1312,6 +1343,7 @@ int rt_set_option(rt_ctx *ctx, const char *name, int32_t value) {
     else if (n == "band_first") ctx->band_first = std::max(0, std::min((int)value, 1000));
     else if (n == "band_times") ctx->band_times = value != 0;
     else if (n == "hot_tiles") ctx->hot_tiles = value != 0;
+    else if (n == "band_order") ctx->band_order = value != 0;
     else if (n == "boxes") ctx->boxes = value != 0;
     else if (n == "mega_tiles") ctx->mega_tiles = value < 0 ? -1 : value != 0;
     else return fail(RT_ERR_INVALID, "unknown option " + n);

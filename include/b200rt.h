@@ -183,6 +183,12 @@ int rt_host_unregister(rt_ctx *ctx, void *ptr);
  *                 default: each event record costs the GPU ~2-3 us);
  *   "rgba"        write pixels as bytes R,G,B,A (the frame server's wire
  *                 format, server.py:56-64) instead of 0xAARRGGBB;
+ *   "sphere_bound" (default on; process-wide) FP32 scenes of 3-8 spheres: a
+ *                 ray that misses a bound over every sphere skips the sphere
+ *                 loop (exact: the clustered walk's bound test and margins;
+ *                 trace kernel -3% at C2/C3);
+ *   "hot_tiles"   (default on) the culled trace dispatches the tiles of the
+ *                 spheres' primary-ray boxes first, frames of up to 8 waves;
  *   "zero_copy"   (default off) when the framebuffer passed to rt_render_v1
  *                 on one device is registered (rt_host_register), the
  *                 kernels store pixels straight into it over PCIe while they

@@ -1047,3 +1047,5 @@ cudaError_t rt_build_shadow_grid_f32(const rt::SceneArgs<float> &sa, unsigned *m
     if (e == cudaSuccess) wa.grid = mask;
     return e;
 }
+
+void rt_set_sphere_bound(bool on) { rt32::g_sphere_bound = on; }

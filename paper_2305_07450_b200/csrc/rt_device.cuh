@@ -272,6 +272,9 @@ bool rt_fused_fits(const rt::SceneArgs<float> &sa);
 // does not fit leaves wa.grid null.
 cudaError_t rt_build_shadow_grid_f32(const rt::SceneArgs<float> &sa, unsigned *mask, int capacity, rt::WaveArgs &wa,
                                      cudaStream_t st);
+// unclustered FP32 scenes: a bound over every sphere lets a ray skip the
+// sphere loop (rt_f32.cuh, pack_params); process-wide switch for A/B runs
+void rt_set_sphere_bound(bool on);
 cudaError_t rt_launch_fused_f32(const rt::FrameArgs &fa, const rt::SceneArgs<float> &sa, const rt::WaveArgs &wa,
                                 cudaStream_t st, int *n_kernels, cudaEvent_t *phase_events /* 5 or null */);
 cudaError_t rt_launch_fused_f64(const rt::FrameArgs &fa, const rt::SceneArgs<double> &sa, const rt::WaveArgs64 &wa,

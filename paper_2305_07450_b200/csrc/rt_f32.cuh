@@ -267,9 +267,12 @@ struct ParamScene {
         Hit h{-1, INFINITY, make_float4(0.f, 0.f, 0.f, -1.f)};
         int slot = -1;
         if constexpr (!kClustered) {
+            // nc = 1: cl[0] bounds every sphere (pack_params); a ray missing
+            // it cannot hit one (the clustered walk's test, with its margins)
+            const bool skip = nc > 0 && bound_entry(o, d, cl[0]) == INFINITY;
 #pragma unroll
             for (int b = 0; b < MAXS; b++) {
-                if (b >= ns) break;
+                if (b >= ns || skip) break;
                 if (SPARSE && !((smask >> b) & 1u)) continue;
                 float t = sphere_t(o, d, sph[b]);
                 if (t < h.t) {  // spheres ascend in original index: strict '<' keeps the lowest
@@ -478,6 +481,9 @@ inline void split_clusters(const std::vector<float4> &c, std::vector<int> &order
 
 // Pack the host scene (float64 geo) into the launch-parameter layout; false
 // if it does not fit.
+constexpr int kBoundMinSpheres = 3;  // unclustered scenes of at least this many spheres get a sphere bound
+inline bool g_sphere_bound = true;   // (option sphere_bound; a host-side switch for A/B runs)
+
 template <int MAXS>
 inline bool pack_params(const SceneArgs<float> &sa, ParamScene<MAXS> &ps) {
     ps.ns = ps.np = 0;
@@ -527,6 +533,27 @@ inline bool pack_params(const SceneArgs<float> &sa, ParamScene<MAXS> &ps) {
             ps.nc++;
         }
         ps.cl_begin[ps.nc] = ps.ns;
+    } else if (ps.ns >= kBoundMinSpheres) {
+        // one bound over every sphere: a ray that misses it skips the sphere
+        // loop (sky rays, rays off into the distance)
+        double cx = 0, cy = 0, cz = 0;
+        for (const float4 &p : sph) {
+            cx += p.x;
+            cy += p.y;
+            cz += p.z;
+        }
+        cx /= ps.ns;
+        cy /= ps.ns;
+        cz /= ps.ns;
+        double R = 0;
+        for (const float4 &p : sph) {
+            double dx = p.x - cx, dy = p.y - cy, dz = p.z - cz;
+            R = std::max(R, std::sqrt(dx * dx + dy * dy + dz * dz) + std::sqrt((double)p.w + 1e-7));
+        }
+        ps.cl[0] = make_float4((float)cx, (float)cy, (float)cz, (float)(R * (1.0 + 1e-4) + 1e-4));
+        ps.cl_begin[0] = 0;
+        ps.cl_begin[1] = ps.ns;
+        ps.nc = g_sphere_bound ? 1 : 0;
     }
     for (int i = 0; i < ps.ns; i++) {
         ps.sph[i] = sph[order[i]];

@@ -1343,6 +1343,7 @@ int rt_set_option(rt_ctx *ctx, const char *name, int32_t value) {
     else if (n == "band_first") ctx->band_first = std::max(0, std::min((int)value, 1000));
     else if (n == "band_times") ctx->band_times = value != 0;
     else if (n == "hot_tiles") ctx->hot_tiles = value != 0;
+    else if (n == "sphere_bound") rt_set_sphere_bound(value != 0);
     else if (n == "band_order") ctx->band_order = value != 0;
     else if (n == "boxes") ctx->boxes = value != 0;
     else if (n == "mega_tiles") ctx->mega_tiles = value < 0 ? -1 : value != 0;

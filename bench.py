@@ -491,6 +491,7 @@ def run_ours(args):
                                 "(closest-hit + every shadow sample) / time; executed: closest-hit rays + the shadow "
                                 "rays the culled pass sampled",
             "e2e": e2e, "gpu_launches": main["launches"], "clocks": main["clocks"], "roofline": roof,
+            "framebuffer_write": framebuffer_writes(cfg, main["total_ms"] / args.steps),
             "phases_ms": phases, "executed_work": work})
         if not args.no_extra:
             extra = {}
@@ -780,6 +781,27 @@ def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True, config_key
         out["counter_achieved"] = per_kernel[kernel]["counter_achieved"]
         out["model_over_counter"] = per_kernel[kernel]["model_over_counter"]
         out["counter_source"] = counters.get("_source") or _load_profile("ncu_flops.json").get("_source")
+    return out
+
+
+def framebuffer_writes(cfg, ms_frame):
+    """The framebuffer's store traffic (north star: "framebuffer write
+    GB/s"): 4 B per pixel (one 0xAARRGGBB word per thread, coalesced into the
+    warp's 8x4 patch rows), over the frame's device time, against the
+    measured HBM copy bandwidth — a few percent: the frame is written once,
+    into L2 (ncu: DRAM writes of the kernels ~0.1 MB per C2 frame), and read
+    back over PCIe."""
+    bpf = 4 * cfg.width * cfg.height
+    gbs = bpf / (ms_frame * 1e-3) / 1e9 if ms_frame > 0 else 0.0
+    peak = None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peak = json.load(f).get("hbm_gbs")
+    except (OSError, ValueError):
+        pass
+    out = {"bytes_per_frame": bpf, "gbs": gbs, "store": "one 32-bit word per pixel, 32 B row segments per warp"}
+    if peak:
+        out.update({"hbm_peak_gbs": peak, "frac_of_hbm": gbs / peak})
     return out
 
 

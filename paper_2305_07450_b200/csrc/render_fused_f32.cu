@@ -200,6 +200,11 @@ __device__ __forceinline__ int conic_entry(const ParamScene<MAXS> &ps, const Wav
     return code;
 }
 
+// CTA-level compaction of the many-sphere trace's live rays: frames of at
+// least kCompactMinBounces bounces, from bounce kCompactFrom on
+constexpr int kCompactMinBounces = 4;
+constexpr int kCompactFrom = 2;
+
 // --- A ----------------------------------------------------------------------------
 // 8 resident CTAs (64 registers) for unclustered scenes: 1.5-3.5% faster at
 // C2-C4; the clustered variant needs its registers (6 CTAs; 8 costs C5 10%)
@@ -244,26 +249,107 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_TRACE_MIN_BLOCKS : 6)
         y = map_row(ly, fa);
         alive = y < fa.row_end;
     }
-    const bool valid = alive;
-    const int64_t lp = (int64_t)ly * fa.width + x;
+    // many-sphere scenes with deep bounces: the CTA's live rays are packed
+    // into its first warps between bounces (ray state through shared memory,
+    // bounce records in HBM, a pixel finished the moment its ray ends), so a
+    // bounce of a few surviving rays costs one warp, not four (C5 at b8:
+    // 6 live lanes per warp from bounce 4 on)
+    constexpr bool kCompact = kBundle;
+    const bool compact = kCompact && fa.bounces >= kCompactMinBounces && wa.compact;
+    bool valid = alive;
+    int64_t lp = (int64_t)ly * fa.width + x;
     const float3 light = f3(sa.light[0], sa.light[1], sa.light[2]);
     // the ray chain in float64 (rt_f32.cuh: refine_hit), searched in FP32
     D3 o64{fa.cam[0], fa.cam[1], fa.cam[2]};
     D3 d64 = valid ? primary_direction64(x, y, fa) : D3{0.0, 0.0, 1.0};
     float3 tail = f3(0.f, 0.f, 0.f);
     int m = 0, exhausted = 0, npend = 0;
-    int ridx[kMaxBounce + 1];
-    float rdfs[kMaxBounce + 1], rs[kMaxBounce + 1], rsc[kMaxBounce + 1];
+    int ridx[kCompact ? 1 : kMaxBounce + 1];
+    float rdfs[kCompact ? 1 : kMaxBounce + 1], rs[kCompact ? 1 : kMaxBounce + 1], rsc[kCompact ? 1 : kMaxBounce + 1];
+    // a pixel whose ray has ended: unwound and packed, or parked for the sampler
+    auto finish = [&]() {
+        if (npend == 0) {
+            const float3 c = kCompact ? unwind(m, exhausted, tail, sa, [&](int k) {
+                const float4 r = __ldcg(wa.rec + (int64_t)k * wa.n_pix + lp);
+                return Record{__float_as_int(r.x), r.y, r.z, r.w};
+            })
+                                      : unwind(m, exhausted, tail, sa,
+                                               [&](int k) { return Record{ridx[k], rdfs[k], rs[k], rsc[k]}; });
+            store_pixel(fa, x, y, c);
+            if (fa.peer_out) __threadfence_system();
+        } else {
+            // parked: the sampler of its last pending hit unwinds it (resolve_hit)
+            wa.pix[lp] =
+                make_float4(tail.x, tail.y, tail.z, __int_as_float(m | (exhausted << 8) | ((npend > 1) << 9)));
+            if (npend > 1) wa.pend[lp] = npend;
+            if constexpr (!kCompact) {
+#pragma unroll 2
+                for (int k = 0; k < m; k++)
+                    wa.rec[(int64_t)k * wa.n_pix + lp] = make_float4(__int_as_float(ridx[k]), rdfs[k], rs[k], rsc[k]);
+            }
+        }
+    };
+    __shared__ int s_wlive[kCompact ? kThreads / 32 : 1];
     for (int k = 0; k <= fa.bounces; k++) {
+        if constexpr (kCompact) {
+            if (compact) {
+                // the CTA loops in step (its barriers); done when no ray lives
+                const unsigned wl = __ballot_sync(0xffffffffu, alive);
+                if (lane == 0) s_wlive[threadIdx.x >> 5] = __popc(wl);
+                const int n_live = __syncthreads_count(alive);
+                if (n_live == 0) break;
+                int busy = 0, base = 0;
+#pragma unroll
+                for (int w = 0; w < kThreads / 32; w++) {
+                    busy += s_wlive[w] > 0;
+                    base += w < (int)(threadIdx.x >> 5) ? s_wlive[w] : 0;
+                }
+                if (k >= kCompactFrom && busy > (n_live + 31) / 32) {
+                    // pack: live ray i -> thread i (the candidate lists' shared memory as scratch)
+                    double *st = reinterpret_cast<double *>(&s_cand_sph[0][0]);
+                    int *sti = reinterpret_cast<int *>(st + 6 * kThreads);
+                    if (alive) {
+                        const int i = base + __popc(wl & lanemask_lt());
+                        st[6 * i] = o64.x;
+                        st[6 * i + 1] = o64.y;
+                        st[6 * i + 2] = o64.z;
+                        st[6 * i + 3] = d64.x;
+                        st[6 * i + 4] = d64.y;
+                        st[6 * i + 5] = d64.z;
+                        sti[4 * i] = (int)lp;
+                        sti[4 * i + 1] = x | (y << 16);
+                        sti[4 * i + 2] = m;
+                        sti[4 * i + 3] = npend;
+                    }
+                    __syncthreads();
+                    alive = (int)threadIdx.x < n_live;
+                    if (alive) {
+                        const int i = threadIdx.x;
+                        o64 = D3{st[6 * i], st[6 * i + 1], st[6 * i + 2]};
+                        d64 = D3{st[6 * i + 3], st[6 * i + 4], st[6 * i + 5]};
+                        lp = sti[4 * i];
+                        x = sti[4 * i + 1] & 0xffff;
+                        y = sti[4 * i + 1] >> 16;
+                        m = sti[4 * i + 2];
+                        npend = sti[4 * i + 3];
+                        exhausted = 0;
+                        tail = f3(0.f, 0.f, 0.f);
+                    }
+                    valid = alive;  // a thread without a ray has no pixel left to finish
+                    __syncthreads();  // the scratch is the candidate lists again
+                }
+            }
+        }
         const unsigned live = __ballot_sync(0xffffffffu, alive);
-        if (!live) break;
+        if (!compact && !live) break;
+        const bool was_alive = alive;
         const float3 origin = rnd(o64), dir = rnd(d64);
         Hit h{-1, INFINITY, make_float4(0.f, 0.f, 0.f, -1.f)};
         if constexpr (!kBundle) {
             // (the primary-ray sphere boxes cost this kernel ~4%: its unrolled,
             // branch-free sphere loop keeps more rays in flight)
             if (alive) h = ps.closest(origin, dir);
-        } else {
+        } else if (live) {  // (compacting: a warp with no ray left idles through the bounce)
             // warp bundle of the live rays -> uniform candidate list
             float3 sd = f3(warp_sum(alive ? dir.x : 0.f), warp_sum(alive ? dir.y : 0.f),
                            warp_sum(alive ? dir.z : 0.f));
@@ -357,10 +443,14 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_TRACE_MIN_BLOCKS : 6)
             const Cone cone = make_cone(so, light, sa.light_radius);
             cls = classify_hit(ps, cone, so.y, light.y, mask, wa.cull == 2, grid_mask(wa, so));
             slot = (int64_t)k * wa.n_pix + lp;
-            ridx[k] = h.idx;
-            rdfs[k] = dfs;
-            rs[k] = s;
-            rsc[k] = cls == 2 ? 0.f : 1.f;
+            if constexpr (kCompact) {
+                wa.rec[slot] = make_float4(__int_as_float(h.idx), dfs, s, cls == 2 ? 0.f : 1.f);
+            } else {
+                ridx[k] = h.idx;
+                rdfs[k] = dfs;
+                rs[k] = s;
+                rsc[k] = cls == 2 ? 0.f : 1.f;
+            }
             if (cls == 1) {
                 qp = make_float4(hit.x, hit.y, hit.z, __int_as_float((int)slot));
                 qn = make_float4(normal.x, normal.y, normal.z, 0.f);
@@ -432,20 +522,13 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_TRACE_MIN_BLOCKS : 6)
                 atomicAdd(wa.work + kWorkCullTests, (unsigned long long)nh * (ps.ns + ps.np));
             }
         }
+        if (compact && was_alive && !alive) {  // the ray ended: its pixel now (the thread may get another ray)
+            finish();
+            valid = false;
+        }
     }
     if (!valid) return;
-    if (npend == 0) {
-        const float3 c = unwind(m, exhausted, tail, sa, [&](int k) { return Record{ridx[k], rdfs[k], rs[k], rsc[k]}; });
-        store_pixel(fa, x, y, c);
-        if (fa.peer_out) __threadfence_system();
-    } else {
-        // parked: the sampler of its last pending hit unwinds it (resolve_hit)
-        wa.pix[lp] = make_float4(tail.x, tail.y, tail.z, __int_as_float(m | (exhausted << 8) | ((npend > 1) << 9)));
-        if (npend > 1) wa.pend[lp] = npend;
-#pragma unroll 2
-        for (int k = 0; k < m; k++)
-            wa.rec[(int64_t)k * wa.n_pix + lp] = make_float4(__int_as_float(ridx[k]), rdfs[k], rs[k], rsc[k]);
-    }
+    finish();
 }
 
 // A sampled hit's coefficient sc (record slot = bounce * n_pix + pixel): a

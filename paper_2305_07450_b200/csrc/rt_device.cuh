@@ -122,6 +122,7 @@ struct WaveArgs {
                        // [(2q + r) lane_cap]; lengths count[3] and count[0]
     unsigned lane_cap; // (0: off)
     int4 hot;          // the trace's hot tile rectangle (tile_of_block); x < 0: bottom rows first
+    int compact;       // many-sphere trace: pack the CTA's live rays between bounces (render_fused_f32.cu)
 };
 // FP64 culled wavefront (render_fused_f64.cu): queues in float64
 constexpr int kMaxBodies64 = 256;

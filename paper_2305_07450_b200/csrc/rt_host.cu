@@ -192,6 +192,7 @@ struct rt_ctx {
     bool boxes = true;        // FP32 scenes of <= 8 spheres: primary-ray sphere boxes (with cull)
     int mega_tiles = -1;      // FP32 megakernel: 1 one CTA per tile, 0 persistent warps, -1 by sample count
     bool hot_tiles = true;    // culled FP32 trace: the spheres' tiles dispatched first
+    int compact = 1;          // culled FP32 many-sphere trace: live rays packed between deep bounces
     int band_order = 0;       // copy-overlap bands enqueued 0: top first, 1: bottom first (measured slower)
     std::mutex mu;
     HostScene scene;
@@ -759,6 +760,7 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
             }
         }
         wa.hot = fused ? hot_rect(ctx, d, fa) : make_int4(-1, -1, -1, -1);
+        wa.compact = ctx->compact;
         wa.work = nullptr;
         if (ctx->count_work) {
             bool fresh = d.w_work.p == nullptr;
@@ -1343,6 +1345,7 @@ int rt_set_option(rt_ctx *ctx, const char *name, int32_t value) {
     else if (n == "band_first") ctx->band_first = std::max(0, std::min((int)value, 1000));
     else if (n == "band_times") ctx->band_times = value != 0;
     else if (n == "hot_tiles") ctx->hot_tiles = value != 0;
+    else if (n == "compact") ctx->compact = value != 0;
     else if (n == "sphere_bound") rt_set_sphere_bound(value != 0);
     else if (n == "band_order") ctx->band_order = value != 0;
     else if (n == "boxes") ctx->boxes = value != 0;

@@ -316,8 +316,7 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_TRACE_MIN_BLOCKS : 6)
                         st[6 * i + 3] = d64.x;
                         st[6 * i + 4] = d64.y;
                         st[6 * i + 5] = d64.z;
-                        sti[4 * i] = (int)lp;
-                        sti[4 * i + 1] = x | (y << 16);
+                        sti[4 * i] = (int)lp;  // < 2^31 (slots_fit); x and y follow from it
                         sti[4 * i + 2] = m;
                         sti[4 * i + 3] = npend;
                     }
@@ -328,8 +327,9 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_TRACE_MIN_BLOCKS : 6)
                         o64 = D3{st[6 * i], st[6 * i + 1], st[6 * i + 2]};
                         d64 = D3{st[6 * i + 3], st[6 * i + 4], st[6 * i + 5]};
                         lp = sti[4 * i];
-                        x = sti[4 * i + 1] & 0xffff;
-                        y = sti[4 * i + 1] >> 16;
+                        const int ly_i = (int)(lp / fa.width);
+                        x = (int)(lp - (int64_t)ly_i * fa.width);
+                        y = map_row(ly_i, fa);
                         m = sti[4 * i + 2];
                         npend = sti[4 * i + 3];
                         exhausted = 0;

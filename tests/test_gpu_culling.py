@@ -203,3 +203,36 @@ def test_fp64_lane_sampler_exact_on_adversarial_scenes(kind):
     culled = render(scene, cam, params, "fp64", "cull")
     literal = render(scene, cam, params, "fp64", "mega")
     np.testing.assert_array_equal(culled, literal)
+
+
+@pytest.mark.parametrize("seed,n,bounces,w,h", [(21, 12, 4, 120, 68), (22, 40, 8, 97, 53), (23, 300, 6, 64, 36),
+                                                 (24, 24, 31, 33, 17)])
+def test_fp32_compaction_bit_identical(seed, n, bounces, w, h):
+    """The many-sphere trace's CTA-level compaction of live rays (option
+    compact: ray state migrated between threads, records in HBM, pixels
+    finished when their ray ends) changes no bit: frames and radiance equal
+    the uncompacted kernel's, with 1 and 3 row partitions, silhouette and ray
+    forms, frame after frame."""
+    rng = np.random.default_rng(seed)
+    scene = random_scene(rng, n, True, None, sky=seed % 2 == 1)
+    for b in scene.bodies:  # mirrors: deep chains
+        if b.kind == rt.BodyKind.SPHERE:
+            b.reflectivity = 128.0
+    cam = rt.Camera(position=(0.0, 1.2, -5.0), yaw=0.05, pitch=-0.1, fov=70.0)
+    params = rt.RenderParams(16, bounces, w, h)
+    try:
+        for conic in (1, 0):
+            out = {}
+            for compact in (0, 1):
+                _native.set_options(wave=1, cull=1, conic=conic, cull_check=0, compact=compact)
+                for workers in (None, 3):
+                    for rep in range(2):
+                        fb = rt.Framebuffer.create(w, h)
+                        rad = np.zeros((w * h, 3), np.float32)
+                        rt.render_frame(scene, cam, params, fb, workers, radiance=rad)
+                        out.setdefault((workers, rep), []).append((fb.pixels.copy(), rad))
+            for key, ((p0, r0), (p1, r1)) in out.items():
+                np.testing.assert_array_equal(p1, p0, err_msg=f"seed {seed} conic {conic} {key}")
+                np.testing.assert_array_equal(r1, r0, err_msg=f"seed {seed} conic {conic} {key}")
+    finally:
+        _native.set_options(compact=1, **MODES["cull"])

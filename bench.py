@@ -220,6 +220,11 @@ CPU_PROTOCOL = {"C1": (100, 10, None), "P720": (100, 10, None), "P1080": (100, 1
                 "C5_512": (1, 3, (384, 216))}
 
 
+# whole frames of the reference's numba render_frame timed per extra configuration (no-sky rows only:
+# the reference's sceneio builds them; ~2-20 s each on 16 cores)
+NUMBA_FRAMES = {"C1": 10, "P720": 10, "P1080": 5, "P4K": 2}
+
+
 def numba_reference(key, frames=2, timeout=240):
     """The unmodified reference's own render_frame (numba, pip-installed into
     baseline/_ref) on all host cores, in a subprocess (tools/
@@ -507,6 +512,9 @@ def run_ours(args):
                     extra[k]["paper_fps_rtx2060"] = rt.workloads.PAPER_FPS[k]
                 if not args.no_cpu_baseline and k in CPU_PROTOCOL:
                     extra[k]["cpu_baseline"] = cpu_frames(k)[1]
+                    nb = numba_reference(k, frames=NUMBA_FRAMES.get(k, 0)) if k in NUMBA_FRAMES else None
+                    if nb:  # the reference's own numba render_frame on the same cores
+                        extra[k]["cpu_baseline"]["numba_reference"] = nb
             # ablation on the headline config: the same frame without culling, and as one megakernel
             for name, opts in (("no_cull", dict(wave=1, cull=0)), ("megakernel", dict(wave=0, cull=0))):
                 for o, v in opts.items():

@@ -128,7 +128,7 @@ __device__ __forceinline__ int classify_hit(const ParamScene<MAXS> &ps, const Co
     constexpr int kWords = (MAXS + 31) / 32;
 #pragma unroll
     for (int w = 0; w <= kWords; w++) mask[w] = 0;
-    if (check) {  // option cull_check: every body undecided
+    if (__builtin_expect(check, 0)) {  // option cull_check: every body undecided
 #pragma unroll 1
         for (int b = 0; b < ps.ns; b++) mask[b >> 5] |= 1u << (b & 31);
         mask[kWords] = (1u << ps.np) - 1u;
@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_TRACE_MIN_BLOCKS : 6)
         }
         const bool need = hit_now && cls == 1 && !laned;
         const unsigned nb = __ballot_sync(0xffffffffu, need);
-        if (nb) {
+        if (__builtin_expect(nb != 0, 0)) {  // (rare in small scenes: laid out off the hot path)
             unsigned base = 0;
             if (lane == 0) base = atomicAdd(wa.count + 1, (unsigned)__popc(nb));
             base = __shfl_sync(0xffffffffu, base, 0);
@@ -515,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_TRACE_MIN_BLOCKS : 6)
                 for (int w = 0; w <= kWords; w++) wa.mask2[(size_t)w * wa.mask2_stride + e] = mask[w];
             }
         }
-        if (wa.work) {
+        if (__builtin_expect(wa.work != nullptr, 0)) {
             const unsigned nh = __popc(__ballot_sync(0xffffffffu, hit_now));
             if (lane == 0 && nh) {
                 atomicAdd(wa.work + kWorkHits, (unsigned long long)nh);

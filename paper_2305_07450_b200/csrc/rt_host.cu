@@ -232,7 +232,7 @@ std::vector<double> disc_table(int n, double radius) {
 int sky_threads() {
     static int t = [] {
         if (const char *e = std::getenv("B200RT_SKY_THREADS")) return std::max(1, std::atoi(e));
-        return std::max(1, omp_get_num_procs());
+        return std::max(1, std::min(32, omp_get_num_procs()));
     }();
     return t;
 }

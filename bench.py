@@ -496,7 +496,7 @@ def run_ours(args):
                                 "(closest-hit + every shadow sample) / time; executed: closest-hit rays + the shadow "
                                 "rays the culled pass sampled",
             "e2e": e2e, "gpu_launches": main["launches"], "clocks": main["clocks"], "roofline": roof,
-            "framebuffer_write": framebuffer_writes(cfg, main["total_ms"] / args.steps),
+            "framebuffer_write": framebuffer_writes(cfg, main["total_ms"] / args.steps, key),
             "phases_ms": phases, "executed_work": work})
         if not args.no_extra:
             extra = {}
@@ -792,7 +792,7 @@ def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True, config_key
     return out
 
 
-def framebuffer_writes(cfg, ms_frame):
+def framebuffer_writes(cfg, ms_frame, cfg_key=None):
     """The framebuffer's store traffic (north star: "framebuffer write
     GB/s"): 4 B per pixel (one 0xAARRGGBB word per thread, coalesced into the
     warp's 8x4 patch rows), over the frame's device time, against the
@@ -810,6 +810,13 @@ def framebuffer_writes(cfg, ms_frame):
     out = {"bytes_per_frame": bpf, "gbs": gbs, "store": "one 32-bit word per pixel, 32 B row segments per warp"}
     if peak:
         out.update({"hbm_peak_gbs": peak, "frac_of_hbm": gbs / peak})
+    # ncu's dram__bytes_write.sum of the frame's kernels (profiles/ncu_flops.json;
+    # ncu flushes caches between kernels, so this is the frame leaving L2)
+    ctr = _load_profile("ncu_flops.json").get(cfg_key or "", {})
+    dw = sum(v.get("dram_write_bytes", 0.0) for v in ctr.values() if isinstance(v, dict))
+    if dw and ms_frame > 0:
+        out.update({"ncu_dram_write_bytes_per_frame": dw, "ncu_dram_write_gbs": dw / (ms_frame * 1e-3) / 1e9,
+                    "ncu_source": "profiles/ncu_flops.json (tools/ncu_counters.sh)"})
     return out
 
 

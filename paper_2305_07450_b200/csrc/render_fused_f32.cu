@@ -200,6 +200,10 @@ __device__ __forceinline__ int conic_entry(const ParamScene<MAXS> &ps, const Wav
     return code;
 }
 
+// A pixel's pending counts in one 64-bit word (resolve_hit): four 16-bit
+// fields, one per bounce, each holding an unblocked count + 1
+__device__ __forceinline__ bool packed_counts(const FrameArgs &fa) { return fa.bounces <= 3 && fa.samples <= 65534; }
+
 // CTA-level compaction of the many-sphere trace's live rays: frames of at
 // least kCompactMinBounces bounces, from bounce kCompactFrom on
 constexpr int kCompactMinBounces = 4;
@@ -263,12 +267,12 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_TRACE_MIN_BLOCKS : 6)
     D3 o64{fa.cam[0], fa.cam[1], fa.cam[2]};
     D3 d64 = valid ? primary_direction64(x, y, fa) : D3{0.0, 0.0, 1.0};
     float3 tail = f3(0.f, 0.f, 0.f);
-    int m = 0, exhausted = 0, npend = 0;
+    int m = 0, exhausted = 0, pmask = 0;  // pmask bit k: bounce k's hit is queued
     int ridx[kCompact ? 1 : kMaxBounce + 1];
     float rdfs[kCompact ? 1 : kMaxBounce + 1], rs[kCompact ? 1 : kMaxBounce + 1], rsc[kCompact ? 1 : kMaxBounce + 1];
     // a pixel whose ray has ended: unwound and packed, or parked for the sampler
     auto finish = [&]() {
-        if (npend == 0) {
+        if (pmask == 0) {
             const float3 c = kCompact ? unwind(m, exhausted, tail, sa, [&](int k) {
                 const float4 r = __ldcg(wa.rec + (int64_t)k * wa.n_pix + lp);
                 return Record{__float_as_int(r.x), r.y, r.z, r.w};
@@ -279,9 +283,17 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_TRACE_MIN_BLOCKS : 6)
             if (fa.peer_out) __threadfence_system();
         } else {
             // parked: the sampler of its last pending hit unwinds it (resolve_hit)
-            wa.pix[lp] =
-                make_float4(tail.x, tail.y, tail.z, __int_as_float(m | (exhausted << 8) | ((npend > 1) << 9)));
-            if (npend > 1) wa.pend[lp] = npend;
+            const bool several = (pmask & (pmask - 1)) != 0;
+            const bool packed = packed_counts(fa);
+            wa.pix[lp] = make_float4(tail.x, tail.y, tail.z,
+                                     __int_as_float(m | (exhausted << 8) | (several << 9) | (packed ? pmask << 10 : 0)));
+            if (several) {
+                if (packed) {
+                    wa.pend64[lp] = 0ull;
+                } else {
+                    wa.pend[lp] = __popc(pmask);
+                }
+            }
             if constexpr (!kCompact) {
 #pragma unroll 2
                 for (int k = 0; k < m; k++)
@@ -318,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_TRACE_MIN_BLOCKS : 6)
                         st[6 * i + 5] = d64.z;
                         sti[4 * i] = (int)lp;  // < 2^31 (slots_fit); x and y follow from it
                         sti[4 * i + 2] = m;
-                        sti[4 * i + 3] = npend;
+                        sti[4 * i + 3] = pmask;
                     }
                     __syncthreads();
                     alive = (int)threadIdx.x < n_live;
@@ -331,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_TRACE_MIN_BLOCKS : 6)
                         x = (int)(lp - (int64_t)ly_i * fa.width);
                         y = map_row(ly_i, fa);
                         m = sti[4 * i + 2];
-                        npend = sti[4 * i + 3];
+                        pmask = sti[4 * i + 3];
                         exhausted = 0;
                         tail = f3(0.f, 0.f, 0.f);
                     }
@@ -454,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_TRACE_MIN_BLOCKS : 6)
             if (cls == 1) {
                 qp = make_float4(hit.x, hit.y, hit.z, __int_as_float((int)slot));
                 qn = make_float4(normal.x, normal.y, normal.z, 0.f);
-                npend++;
+                pmask |= 1 << k;
                 // one candidate sphere: a lane of the lane sampler
                 if (wa.lane_cap && mask[kWords] == 0) {
                     int nc = 0, b = 0;
@@ -531,10 +543,15 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_TRACE_MIN_BLOCKS : 6)
     finish();
 }
 
-// A sampled hit's coefficient sc (record slot = bounce * n_pix + pixel): a
+// A sampled hit's unblocked count (record slot = bounce * n_pix + pixel): a
 // pixel with this one pending hit is unwound and packed at once (its other
-// records are decided); with several, the coefficient is stored and the last
-// of the pixel's samplers — an acquire-release atomic countdown — unwinds it.
+// records are decided).  With several pending hits the last of the pixel's
+// samplers unwinds it: in frames of up to 3 bounces and 65,534 samples
+// (packed_counts) each sampler adds its count + 1 into its bounce's 16-bit
+// field of the pixel's 64-bit word — one relaxed atomic; the sampler that
+// completes every pending field holds all the counts, no fence and no
+// reload — otherwise the coefficient is stored and an acquire-release
+// countdown elects the last.
 // The first records of a parked pixel, loaded ahead (their latency hides
 // behind the sampling); kPre covers every record of a frame of up to 3 bounces.
 constexpr int kPre = 4;
@@ -555,24 +572,37 @@ __device__ __forceinline__ PreRecords prefetch_records(const WaveArgs &wa, int s
 }
 
 __device__ __forceinline__ void resolve_hit(const FrameArgs &fa, const SceneArgs<float> &sa, const WaveArgs &wa,
-                                            int slot, float sc, float4 px, const float4 *mat4,
+                                            int slot, int unblocked, float4 px, const float4 *mat4,
                                             const PreRecords *pre = nullptr) {
     const int n_pix = (int)wa.n_pix;
     const int kh = slot / n_pix, lp = slot - kh * n_pix;
     const int info = __float_as_int(px.w);
     const bool several = info & (1 << 9);
+    const int n = fa.samples;
+    const float sc = (float)unblocked / (float)n;
+    const bool packed = packed_counts(fa);
+    const int pm = several && packed ? (info >> 10) & 15 : 0;  // the pending bounces
+    unsigned long long counts = 0;  // field k: bounce k's unblocked count + 1
     if (several) {
-        reinterpret_cast<float *>(wa.rec + slot)[3] = sc;
-        // release our coefficient, acquire the others' (the last sampler reads
-        // them): one acq_rel countdown instead of two sequentially consistent
-        // fences around a relaxed one (C2 2.5% faster)
-        cuda::atomic_ref<int, cuda::thread_scope_device> pend(wa.pend[lp]);
-        if (pend.fetch_sub(1, cuda::memory_order_acq_rel) != 1) return;
+        if (packed) {
+            const unsigned long long add = (unsigned long long)(unblocked + 1) << (16 * kh);
+            counts = atomicAdd(wa.pend64 + lp, add) + add;
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+                if (((pm >> k) & 1) && ((counts >> (16 * k)) & 0xffffu) == 0) return;  // a count still to come
+        } else {
+            reinterpret_cast<float *>(wa.rec + slot)[3] = sc;
+            // release our coefficient, acquire the others' (the last sampler reads
+            // them): one acq_rel countdown instead of two sequentially consistent
+            // fences around a relaxed one (C2 2.5% faster)
+            cuda::atomic_ref<int, cuda::thread_scope_device> pend(wa.pend[lp]);
+            if (pend.fetch_sub(1, cuda::memory_order_acq_rel) != 1) return;
+        }
     }
     const int m = info & 0xff;
-    // records of a single-pending pixel do not change after the trace: the
-    // prefetched ones serve; with several pending, the coefficients just landed
-    const int have = (pre && !several) ? pre->n : 0;
+    // the records do not change after the trace, except the coefficients the
+    // countdown's samplers store: the prefetched ones serve unless those landed
+    const int have = (pre && (!several || packed)) ? pre->n : 0;
     float4 rk[kMaxBounce + 1];  // every record load in flight before the first use
 #pragma unroll
     for (int k = 0; k < kPre; k++)
@@ -581,7 +611,12 @@ __device__ __forceinline__ void resolve_hit(const FrameArgs &fa, const SceneArgs
     for (int k = have; k < m; k++) rk[k] = __ldcg(wa.rec + (int64_t)k * n_pix + lp);
     const float3 c = unwind(
         m, (info >> 8) & 1, f3(px.x, px.y, px.z), sa,
-        [&](int k) { return Record{__float_as_int(rk[k].x), rk[k].y, rk[k].z, (k == kh && !several) ? sc : rk[k].w}; },
+        [&](int k) {
+            float c = rk[k].w;
+            if (k == kh && !several) c = sc;
+            if ((pm >> k) & 1) c = (float)((int)((counts >> (16 * k)) & 0xffffu) - 1) / (float)n;
+            return Record{__float_as_int(rk[k].x), rk[k].y, rk[k].z, c};
+        },
         mat4);
     const int ly = lp / fa.width, x = lp - ly * fa.width;
     store_pixel(fa, x, map_row(ly, fa), c);
@@ -883,7 +918,7 @@ __device__ __forceinline__ void sample_lanes(const FrameArgs &fa, const SceneArg
 #pragma unroll 4
             for (int i = 0; i < n; i++) blocked += conic_blocked(A, B, b0, b1, b2, table(i));
         }
-        resolve_hit(fa, sa, wa, slot, (float)(n - (int)blocked) / (float)n, px, mat4, &pre);
+        resolve_hit(fa, sa, wa, slot, n - (int)blocked, px, mat4, &pre);
         if (wa.work) {
             if (r != 0) {
                 atomicAdd(wa.work + kWorkConicHits, 1ull);
@@ -956,8 +991,7 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_SAMPLE_MIN_BLOCKS : 1
         }
     };
     if (warp < count) fetch(warp);
-    int held = 0, my_slot = -1;
-    float my_sc = 0.f;
+    int held = 0, my_slot = -1, my_unb = 0;
     for (unsigned h = warp; h < count; h += n_warps) {
         const float4 Pc = P, Nc = N, A0c = A0, B0c = B0;
         unsigned hmc[kWords + 1];
@@ -979,10 +1013,10 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_SAMPLE_MIN_BLOCKS : 1
         // lane `held` keeps this hit; every 32 hits the lanes resolve theirs together
         if (lane == held) {
             my_slot = slot;
-            my_sc = (float)unblocked / (float)n;
+            my_unb = unblocked;
         }
         if (++held == 32) {
-            if (my_slot >= 0) resolve_hit(fa, sa, wa, my_slot, my_sc, pixel_word(wa, my_slot), s_mat);
+            if (my_slot >= 0) resolve_hit(fa, sa, wa, my_slot, my_unb, pixel_word(wa, my_slot), s_mat);
             my_slot = -1;
             held = 0;
         }
@@ -999,7 +1033,7 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_SAMPLE_MIN_BLOCKS : 1
             atomicAdd(wa.work + kWorkPlaneTests, (unsigned long long)n * __popc(hmc[kWords]));
         }
     }
-    if (my_slot >= 0) resolve_hit(fa, sa, wa, my_slot, my_sc, pixel_word(wa, my_slot), s_mat);
+    if (my_slot >= 0) resolve_hit(fa, sa, wa, my_slot, my_unb, pixel_word(wa, my_slot), s_mat);
 }
 
 // Launch with programmatic stream serialisation: the kernel may start while

@@ -106,6 +106,7 @@ struct WaveArgs {
     float4 *pix;       // {tail rgb, records | exhausted << 8}
     float4 *rec;       // culled path: {body, Lambert, Blinn, coefficient} per hit of a pending pixel
     int *pend;         // culled path: per pixel, its hits still sampling (written when 2 or more)
+    unsigned long long *pend64;  // the same buffer as packed counts (render_fused_f32.cu, resolve_hit)
     int64_t n_pix;     // pixels of this partition (local_rows * width)
     unsigned long long *work;  // optional executed-work tallies of the culled path (kWork*), or null
     int cull;          // exact per-hit occluder culling (1); 2: every body left undecided (cull_check)

@@ -718,7 +718,7 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
             if ((rc = b.w_queue2.ensure(sizeof(int) * slots)) ||
                 (rc = b.w_mask2.ensure(sizeof(unsigned) * slots * rt::rt_mask_words(count_spheres(ctx->scene)))) ||
                 (rc = b.w_rec.ensure(sizeof(float4) * slots)) ||
-                (rc = b.w_pending.ensure(sizeof(int) * (size_t)wa.n_pix)))  // pend
+                (rc = b.w_pending.ensure(sizeof(unsigned long long) * (size_t)wa.n_pix)))  // pend / pend64
                 return rc;
             if (ctx->conic) {  // silhouette coefficients for the first n_pix queued hits
                 if ((rc = b.w_conic.ensure(sizeof(float4) * 2 * rt::kConic * (size_t)wa.n_pix))) return rc;
@@ -745,6 +745,7 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
         wa.pix = (float4 *)b.w_pix.p;
         wa.rec = (float4 *)b.w_rec.p;
         wa.pend = (int *)b.w_pending.p;
+        wa.pend64 = (unsigned long long *)b.w_pending.p;
         wa.cull = fused ? (ctx->cull_check ? 2 : 1) : 0;
         if (fused) {
             wa.count = (unsigned *)b.w_count.p + 8 + 8 * b.count_parity;

@@ -194,7 +194,18 @@ int rt_host_unregister(rt_ctx *ctx, void *ptr);
  *                 kernels store pixels straight into it over PCIe while they
  *                 compute — no copy after the frame, but measured 1.3-2.4x
  *                 slower end to end on B200 (PCIe writes of 32-byte rows
- *                 stall the kernels), so the staged copy is the default. */
+ *                 stall the kernels), so the staged copy is the default;
+ *   "codec"       (default on) rt_render_v1 on one device and the pipelined
+ *                 frames (rt_render_async_v1) move the finished pixels over
+ *                 PCIe compressed, losslessly: each row's mask of pixels that
+ *                 differ from their left neighbour and those pixels, written
+ *                 by an encode kernel into mapped host memory, then expanded
+ *                 into the caller's framebuffer by host threads (AVX2) — band
+ *                 by band as each lands.  The frame is the same bit for bit;
+ *                 C2 moves 0.33 MB instead of 3.7 (rt_last_d2h_bytes).  Off:
+ *                 the raw copy.  Rows wider than 6,144 pixels always copy raw;
+ *   "codec_threads" host threads expanding a compressed frame (0, default:
+ *                 up to 16 of the OpenMP pool). */
 int rt_set_option(rt_ctx *ctx, const char *name, int32_t value);
 /* Executed-work tallies since the last reset (option "count_work"), in this
  * order: hits, per-hit cull tests, hits that sampled, shadow rays, sphere
@@ -203,6 +214,27 @@ int rt_set_option(rt_ctx *ctx, const char *name, int32_t value);
  * tests, hits sampled by the lane sampler (one lane per hit), silhouette
  * tests with the terminator (z) test. */
 int rt_work_counts(rt_ctx *ctx, uint64_t *out, int32_t n, int32_t reset);
+
+/* Bytes the last rt_render_v1 / rt_frame_wait_v1 frame moved from the device
+ * to the host: the frame (and radiance) raw, or with option "codec" the
+ * mask words and literals that crossed PCIe. */
+int rt_last_d2h_bytes(rt_ctx *ctx, int64_t *bytes);
+
+/* The host half of option "codec", on its own (no GPU needed): expand a
+ * compressed frame host_buf into pixels (row pitch in pixels).  A pixel equal
+ * to its left neighbour is a repeat, the others (a row's first pixel always)
+ * literals.  In uint32 words, mw = ceil(width / 32), nb = ceil(mw / 32),
+ * stride = 32 * ceil((1 + nb + mw + width) / 32), row y at 32 + y * stride:
+ *   the literal count n | packed << 31;
+ *   nb bitmap words, bit j: mask word j is non-zero and listed next;
+ *   the listed mask words in order (bit i of mask word j: pixel 32 j + i is a
+ *   literal; unlisted words are 0);
+ *   the literals: packed, 3 bytes each (a pixel's low 3 bytes; its top byte
+ *   is 0xFF), ceil(3 n / 4) words; else n words.
+ * 32 words follow the last row (read, never used).  *words (may be NULL)
+ * receives the words the rows' runs occupy — what crossed PCIe. */
+int rt_frame_expand_v1(const uint32_t *host_buf, int32_t width, int32_t height, uint32_t *pixels, int64_t pitch,
+                       int32_t threads, int64_t *words);
 
 /* Device time (CUDA events) of the render kernels of the last rt_render_v1 /
  * rt_trace_rays_v1 call on ctx's first device, in milliseconds. */

@@ -57,6 +57,8 @@ SIGNATURES = {
     "rt_set_option": (ctypes.c_int, [_p, ctypes.c_char_p, _i32]),
     "rt_work_counts": (ctypes.c_int, [_p, _p, _i32, _i32]),
     "rt_last_kernel_ms": (ctypes.c_int, [_p, _p]),
+    "rt_last_d2h_bytes": (ctypes.c_int, [_p, _p]),
+    "rt_frame_expand_v1": (ctypes.c_int, [_p, _i32, _i32, _p, ctypes.c_int64, _i32, _p]),
     "rt_phase_ms": (ctypes.c_int, [_p, _p, _i32]),
     "rt_band_times_ms": (ctypes.c_int, [_p, _p, _i32]),
     "rt_launch_count": (ctypes.c_int, [_p, _p]),
@@ -173,6 +175,11 @@ class Context:
         v = ctypes.c_float(0)
         check(load().rt_last_kernel_ms(self.handle, ctypes.byref(v)), "rt_last_kernel_ms")
         return float(v.value)
+
+    def last_d2h_bytes(self) -> int:
+        v = ctypes.c_int64(0)
+        check(load().rt_last_d2h_bytes(self.handle, ctypes.byref(v)), "rt_last_d2h_bytes")
+        return int(v.value)
 
     def phase_ms(self) -> dict:
         arr = (ctypes.c_float * 4)()

@@ -35,6 +35,9 @@ SOURCES = {
     "render_fused_f32.cu": ["--ftz=true", "--prec-div=false", "--prec-sqrt=false"],
     "render_f64.cu": ["-fmad=false"],
     "render_fused_f64.cu": ["-fmad=false"],
+    # compressed frame transfer: the GPU encoder and the host's AVX2 expander
+    "frame_codec.cu": [],
+    "frame_decode.cpp": ["-Xcompiler", "-fopenmp"],
 }
 
 
@@ -63,14 +66,14 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
     bdir = BUILD if not tag else os.path.join(BUILD, "v_" + "_".join(tag))
     os.makedirs(bdir, exist_ok=True)
     dflags = [f"-D{d}" for d in defines]
-    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(INCLUDE, "b200rt.h"))
     objs, cmds = [], []
     for src, extra in SOURCES.items():
         if f32_flags is not None and "f32" in src:
             extra = list(f32_flags)
         s = os.path.join(CSRC, src)
-        o = os.path.join(bdir, src.replace(".cu", ".o"))
+        o = os.path.join(bdir, os.path.splitext(src)[0] + ".o")
         objs.append(o)
         if force or _stale(o, [s, *headers, __file__]):
             cmd = [nvcc, *_ccbin(), *COMMON, *extra, *dflags, "-c", s, "-o", o]

@@ -18,6 +18,7 @@
 #include <omp.h>
 
 #include "b200rt.h"
+#include "frame_codec.h"
 #include "rt_device.cuh"
 
 namespace {
@@ -55,6 +56,31 @@ struct DBuf {
     void release() {
         if (p) cudaFree(p);
         p = nullptr;
+        cap = 0;
+    }
+};
+
+// Page-locked, mapped host memory: the compressed frame transfer's target
+// (frame_codec.h), written by the encode kernel through its device address.
+struct HBuf {
+    void *p = nullptr, *dp = nullptr;
+    size_t cap = 0;
+    int ensure(size_t bytes) {
+        if (bytes <= cap && p) return RT_OK;
+        release();
+        cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+        if (e == cudaSuccess) e = cudaHostGetDevicePointer(&dp, p, 0);
+        if (e != cudaSuccess) {
+            release();
+            cudaGetLastError();
+            return fail(RT_ERR_NOMEM, std::string("cudaHostAlloc (mapped): ") + cudaGetErrorString(e));
+        }
+        cap = bytes;
+        return RT_OK;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = dp = nullptr;
         cap = 0;
     }
 };
@@ -121,6 +147,15 @@ struct Dev {
     DBuf slot_frame[kSlots];
     cudaEvent_t slot_comp[kSlots] = {}, slot_done[kSlots] = {};
     bool slot_busy[kSlots] = {};
+    // compressed transfer (option codec): the mapped host buffer of
+    // rt_render_v1's frames and of each slot, and what a slot's wait expands
+    HBuf codec_host;
+    HBuf slot_codec[kSlots];
+    struct SlotOut {
+        uint32_t *pixels = nullptr;
+        int width = 0, height = 0;
+        bool codec = false;
+    } slot_out[kSlots];
     // rt_render_device_v1 on caller streams: the end of the last call's
     // kernels, and the end of this call's uploads
     cudaEvent_t dev_call_ev = nullptr, dev_prep_ev = nullptr;
@@ -194,6 +229,17 @@ struct rt_ctx {
     bool hot_tiles = true;    // culled FP32 trace: the spheres' tiles dispatched first
     int compact = 1;          // culled FP32 many-sphere trace: live rays packed between deep bounces
     int band_order = 0;       // copy-overlap bands enqueued 0: top first, 1: bottom first (measured slower)
+    int codec = 1;            // host frames cross PCIe compressed (frame_codec.h) and are expanded here
+    int codec_threads = 0;    // host threads expanding a frame (0: up to 16 of the OpenMP pool)
+    // the frame enqueue_frame left for finish_frame to expand (one device)
+    struct CodecFrame {
+        bool on = false;
+        uint32_t *pixels = nullptr;
+        int width = 0, height = 0, bands = 0;
+        int y_at[kMaxBands + 1] = {};
+        int order[kMaxBands] = {};
+    } codec_frame;
+    int64_t last_d2h_bytes = 0;  // bytes the last frame moved device -> host
     std::mutex mu;
     HostScene scene;
     float last_ms = 0.f;
@@ -274,30 +320,45 @@ uint64_t hash_bytes(const char *p, size_t n, uint64_t seed) {
     return h ^ (h >> 32);
 }
 
-// the texels' hash: chunks on all host threads, chained in chunk order
-uint64_t texel_hash(const float *a, size_t n) {
-    const size_t bytes = sizeof(float) * n;
-    const int chunks = 4 * sky_threads();
-    std::vector<uint64_t> part(chunks);
-#pragma omp parallel for num_threads(sky_threads()) schedule(static)
-    for (int k = 0; k < chunks; k++) {
+// the texels' hash: chunks hashed independently (on all host threads, or by
+// the compressed frame's expansion team while it waits), chained in order
+struct TexelHash {
+    const float *a;
+    size_t bytes;
+    int chunks;
+    std::vector<uint64_t> part;
+    TexelHash(const float *a_, size_t n) : a(a_), bytes(sizeof(float) * n), chunks(4 * sky_threads()), part(chunks) {}
+    void chunk(int k) {
         const size_t lo = bytes * k / chunks / 4 * 4, hi = bytes * (k + 1) / chunks / 4 * 4;
         part[k] = hash_bytes((const char *)a + lo, (k == chunks - 1 ? bytes : hi) - lo, (uint64_t)k);
     }
-    uint64_t h = 0x27D4EB2F165667C5ull;
-    for (int k = 0; k < chunks; k++) h = hround(h, part[k] ^ (uint64_t)k);
-    return h ^ bytes;
+    static void run(void *self, int k) { static_cast<TexelHash *>(self)->chunk(k); }
+    uint64_t value() const {
+        uint64_t h = 0x27D4EB2F165667C5ull;
+        for (int k = 0; k < chunks; k++) h = hround(h, part[k] ^ (uint64_t)k);
+        return h ^ bytes;
+    }
+};
+
+uint64_t texel_hash(const float *a, size_t n) {
+    TexelHash t(a, n);
+#pragma omp parallel for num_threads(sky_threads()) schedule(static)
+    for (int k = 0; k < t.chunks; k++) t.chunk(k);
+    return t.value();
 }
 
 // The caller's texels (same array as the last frame's) against the uploaded
 // ones; on a difference the sky version is bumped (upload_sky re-uploads).
-bool sky_content_changed(HostScene &s) {
-    if (!s.has_sky || !s.sky_ptr) return false;
-    const uint64_t h = texel_hash(s.sky_ptr, (size_t)s.sky_w * s.sky_h * 3);
+bool sky_hash_differs(HostScene &s, uint64_t h) {
     if (h == s.sky_hash) return false;
     s.sky_hash = h;
     s.sky_version++;
     return true;
+}
+
+bool sky_content_changed(HostScene &s) {
+    if (!s.has_sky || !s.sky_ptr) return false;
+    return sky_hash_differs(s, texel_hash(s.sky_ptr, (size_t)s.sky_w * s.sky_h * 3));
 }
 
 int validate_scene(int32_t n_bodies, const int32_t *kinds, const double *positions, const double *sizes,
@@ -943,7 +1004,9 @@ int rt_ctx_destroy(rt_ctx *ctx) {
             if (d.slot_comp[k]) cudaEventDestroy(d.slot_comp[k]);
             if (d.slot_done[k]) cudaEventDestroy(d.slot_done[k]);
             d.slot_frame[k].release();
+            d.slot_codec[k].release();
         }
+        d.codec_host.release();
         if (d.copy_st) cudaStreamDestroy(d.copy_st);
         if (d.e0) cudaEventDestroy(d.e0);
         if (d.e1) cudaEventDestroy(d.e1);
@@ -1014,6 +1077,8 @@ int enqueue_frame(rt_ctx *ctx, int n_dev, uint32_t *pixels, void *radiance, int3
             }
             RT_CK(cudaEventRecord(d.e1, d.st));
             ctx->band_pending = 0;
+            ctx->codec_frame.on = false;
+            ctx->last_d2h_bytes = 0;  // (the kernels' own stores)
             return RT_OK;
         }
         cudaGetLastError();  // not registered: a cudaHostGetDevicePointer miss is not an error
@@ -1024,7 +1089,13 @@ int enqueue_frame(rt_ctx *ctx, int n_dev, uint32_t *pixels, void *radiance, int3
         // best (tools/e2e_ab.py, round 2): 2 bands at 3.7 and 8.3 MB (C3: 258
         // us against 280 with 4), 6 at 33 MB.
         const size_t MB = (size_t)1 << 20;
-        int bands = ctx->bands > 0 ? ctx->bands : px_bytes < MB ? 1 : px_bytes < 24 * MB ? 2 : 6;
+        // compressed (option codec), the transfer is ~10% of the frame: 1
+        // band below 6 MB (C2 104 us against 108 with 2), 2 below 24 MB (C3
+        // 207 / 213 with 3), 6 above (C4 531 / 543 with 4); raw, as above
+        const bool codec = ctx->codec && width <= rt::kCodecMaxWidth;
+        int bands = ctx->bands > 0 ? ctx->bands
+                    : codec        ? (px_bytes < 6 * MB ? 1 : px_bytes < 24 * MB ? 2 : 6)
+                                   : (px_bytes < MB ? 1 : px_bytes < 24 * MB ? 2 : 6);
         if (ctx->phases) bands = 1;  // phase events describe one frame on one stream
         bands = std::max(1, std::min(bands, height / 8));
         // band boundaries in whole 8-row blocks: band 0 takes band_first
@@ -1041,6 +1112,19 @@ int enqueue_frame(rt_ctx *ctx, int n_dev, uint32_t *pixels, void *radiance, int3
             for (int k = 1; k < bands; k++) y_at[k + 1] = first + (int)((int64_t)rest * k / others);
             for (int k = 0; k <= bands; k++) y_at[k] = std::min(height, y_at[k] * 8);
         }
+        // compressed transfer: each band's rows encoded into the mapped host
+        // buffer after its kernels; finish_frame expands them band by band
+        // (band k while the later bands still render)
+        auto &cf = ctx->codec_frame;
+        cf.on = codec;
+        if (cf.on) {
+            if ((rc = d.codec_host.ensure(rt::codec_host_bytes(width, height)))) return rc;
+            cf.pixels = pixels;
+            cf.width = width;
+            cf.height = height;
+            cf.bands = bands;
+            for (int k = 0; k <= bands; k++) cf.y_at[k] = y_at[k];
+        }
         RT_CK(cudaEventRecord(d.e0, d.st));
         if (bands > 1) RT_CK(cudaEventRecord(d.fork_ev, d.st));
         // each band's copy follows its kernels on its own stream, so the
@@ -1050,6 +1134,7 @@ int enqueue_frame(rt_ctx *ctx, int n_dev, uint32_t *pixels, void *radiance, int3
         // rows reach the GPU sooner) measured 10-18% slower end to end
         for (int i = 0; i < bands; i++) {
             const int k = ctx->band_order && bands > 1 ? bands - 1 - i : i;
+            cf.order[i] = k;
             cudaStream_t bs = bands > 1 ? d.band_st[k] : d.st;
             if (bands > 1) RT_CK(cudaStreamWaitEvent(bs, d.fork_ev, 0));
             const int y0 = y_at[k], y1 = y_at[k + 1];
@@ -1065,31 +1150,46 @@ int enqueue_frame(rt_ctx *ctx, int n_dev, uint32_t *pixels, void *radiance, int3
                 fa.row_end = y1;
                 if ((rc = launch_frame(ctx, d, fa, precision, bs, k))) return rc;
             }
-            RT_CK(cudaEventRecord(d.band_ev[k], bs));
             if (ctx->band_times) RT_CK(cudaEventRecord(d.tl_ev[k], bs));
+            if (cf.on) {
+                // the band's encode right behind its last kernel on the same
+                // stream (a programmatic dependent: no launch gap); the host
+                // expands the band once copy_ev[k] fires
+                RT_CK(rt::launch_encode_rows((const uint32_t *)d.frame.p, width, width, height, y0, y1,
+                                             (uint32_t *)d.codec_host.dp, bs));
+                RT_CK(cudaEventRecord(d.copy_ev[k], bs));
+            }
+            RT_CK(cudaEventRecord(d.band_ev[k], bs));
             if (bands > 1) RT_CK(cudaStreamWaitEvent(d.st, d.band_ev[k], 0));  // the join (kernels)
             cudaStream_t cs = bands > 1 ? bs : d.copy_st;
             if (bands == 1) RT_CK(cudaStreamWaitEvent(d.copy_st, d.band_ev[k], 0));
             if (y1 > y0) {
                 size_t off = (size_t)y0 * width, cnt = (size_t)(y1 - y0) * width;
-                RT_CK(cudaMemcpyAsync(pixels + off, (uint32_t *)d.frame.p + off, sizeof(uint32_t) * cnt,
-                                      cudaMemcpyDeviceToHost, cs));
+                if (!cf.on)
+                    RT_CK(cudaMemcpyAsync(pixels + off, (uint32_t *)d.frame.p + off, sizeof(uint32_t) * cnt,
+                                          cudaMemcpyDeviceToHost, cs));
                 if (radiance)
                     RT_CK(cudaMemcpyAsync((char *)radiance + rad_elem * 3 * off, (char *)d.rad.p + rad_elem * 3 * off,
                                           rad_elem * 3 * cnt, cudaMemcpyDeviceToHost, cs));
             }
             if (ctx->band_times) RT_CK(cudaEventRecord(d.tl_ev[kMaxBands + k], cs));
-            if (bands > 1) {  // the copy's end, joined into the copy stream that finish_frame waits for
-                RT_CK(cudaEventRecord(d.copy_ev[k], bs));
-                RT_CK(cudaStreamWaitEvent(d.copy_st, d.copy_ev[k], 0));
+            if (bands > 1) {  // the band's end, joined into the copy stream that finish_frame waits for
+                // (compressed, copy_ev[k] already marks the encode's end for the
+                // expansion: band_ev[k], its join done, is recorded again here)
+                cudaEvent_t end_ev = cf.on ? d.band_ev[k] : d.copy_ev[k];
+                RT_CK(cudaEventRecord(end_ev, bs));
+                RT_CK(cudaStreamWaitEvent(d.copy_st, end_ev, 0));
             }
         }
         RT_CK(cudaEventRecord(d.e1, d.st));
         ctx->band_pending = bands;
+        ctx->last_d2h_bytes = (cf.on ? 0 : (int64_t)px_bytes) + (radiance ? (int64_t)rad_bytes : 0);
         return RT_OK;
     }
     // several devices: partition p runs on device p % n_dev, each device
     // returns only its rows
+    ctx->codec_frame.on = false;
+    ctx->last_d2h_bytes = (int64_t)px_bytes + (radiance ? (int64_t)rad_bytes : 0);
     for (int g = 0; g < n_dev; g++) {
         Dev &d = ctx->devs[g];
         RT_CK(cudaSetDevice(d.id));
@@ -1119,8 +1219,46 @@ int enqueue_frame(rt_ctx *ctx, int n_dev, uint32_t *pixels, void *radiance, int3
 }
 
 
-// Wait for the frame enqueued by enqueue_frame; its device time and band times.
-int finish_frame(rt_ctx *ctx, int n_dev) {
+int codec_threads(const rt_ctx *ctx) {
+    return ctx->codec_threads > 0 ? ctx->codec_threads : std::min(16, omp_get_max_threads());
+}
+
+// Wait for the frame enqueued by enqueue_frame (compressed: expanding its
+// bands as they land); its device time and band times.
+// side: work for the expansion team's waits (only with a compressed frame)
+int finish_frame(rt_ctx *ctx, int n_dev, const rt::CodecSideJob *side = nullptr) {
+    auto &cf = ctx->codec_frame;
+    if (side && !(n_dev == 1 && cf.on)) {  // no expansion team: the side job on its own
+#pragma omp parallel for num_threads(sky_threads()) schedule(dynamic)
+        for (int i = 0; i < side->items; i++) side->run(side->arg, i);
+    }
+    if (n_dev == 1 && cf.on) {
+        // expand the bands in the order they finish, each as soon as its rows land
+        Dev &d = ctx->devs[0];
+        RT_CK(cudaSetDevice(d.id));
+        // the bands expanded in the order they finish, each the moment its rows
+        // are in (the side job — the sky hash — fills the wait)
+        struct W {
+            Dev *d;
+            static int query(void *arg, int k) {
+                const cudaError_t e = cudaEventQuery(static_cast<W *>(arg)->d->copy_ev[k]);
+                if (e == cudaErrorNotReady) return 0;
+                if (e == cudaSuccess) return 1;
+                return fail(RT_ERR_CUDA, std::string("compressed frame: ") + cudaGetErrorString(e));
+            }
+            static int wait(void *arg, int k) {
+                const cudaError_t e = cudaEventSynchronize(static_cast<W *>(arg)->d->copy_ev[k]);
+                return e == cudaSuccess ? 0 : fail(RT_ERR_CUDA, std::string("compressed frame: ") + cudaGetErrorString(e));
+            }
+        } w{&d};
+        int wrc = RT_OK;
+        const int64_t words = rt::decode_bands((const uint32_t *)d.codec_host.p, cf.width, cf.bands, cf.y_at,
+                                               cf.order, &W::query, &W::wait, &w, &wrc, cf.pixels, cf.width,
+                                               std::max(codec_threads(ctx), side ? sky_threads() : 1), side);
+        cf.on = false;
+        if (words < 0) return wrc;
+        ctx->last_d2h_bytes += (int64_t)sizeof(uint32_t) * words;
+    }
     for (int g = 0; g < n_dev; g++) {
         Dev &d = ctx->devs[g];
         RT_CK(cudaSetDevice(d.id));
@@ -1170,15 +1308,29 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
     // caller passed the same sky array as before, its texels are hashed in
     // full while the kernels run, and on a different hash the sky is uploaded
     // again and the frame rendered again.
+    bool finished = false;
     for (int attempt = 0;; attempt++) {
         if ((rc = enqueue_frame(ctx, n_dev, pixels, radiance, width, height, cam_pos, yaw, pitch, vdist,
                                 shadow_samples, bounce_limit, n_parts, precision)))
             return rc;
-        if (attempt > 0 || !verify_sky || !sky_content_changed(ctx->scene)) break;
+        if (attempt > 0 || !verify_sky || !ctx->scene.has_sky || !ctx->scene.sky_ptr) break;
+        if (ctx->codec_frame.on) {
+            // compressed: the host threads hash the sky while they wait for the
+            // bands, and expand each band as it lands
+            HostScene &sc = ctx->scene;
+            TexelHash th(sc.sky_ptr, (size_t)sc.sky_w * sc.sky_h * 3);
+            rt::CodecSideJob side{th.chunks, &TexelHash::run, &th};
+            if ((rc = finish_frame(ctx, n_dev, &side))) return rc;
+            finished = true;
+            if (!sky_hash_differs(sc, th.value())) break;
+            finished = false;  // stale: rendered again with the new sky
+            continue;
+        }
+        if (!sky_content_changed(ctx->scene)) break;
         if ((rc = finish_frame(ctx, n_dev))) return rc;  // the stale frame ends before the sky is replaced
     }
     const auto t_wait = std::chrono::steady_clock::now();
-    if ((rc = finish_frame(ctx, n_dev))) return rc;
+    if (!finished && (rc = finish_frame(ctx, n_dev))) return rc;
     if (host_timing()) {  // $B200RT_HOST_TIMING: where a synchronous call's host time goes
         const auto t_end = std::chrono::steady_clock::now();
         auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
@@ -1341,6 +1493,8 @@ int rt_set_option(rt_ctx *ctx, const char *name, int32_t value) {
     else if (n == "phases") ctx->phases = value != 0;
     else if (n == "rgba") ctx->rgba = value != 0;
     else if (n == "zero_copy") ctx->zero_copy = value != 0;
+    else if (n == "codec") ctx->codec = value != 0;
+    else if (n == "codec_threads") ctx->codec_threads = std::max(0, (int)value);
     else if (n == "conic") ctx->conic = value != 0;
     else if (n == "cull_check") ctx->cull_check = value != 0;
     else if (n == "band_first") ctx->band_first = std::max(0, std::min((int)value, 1000));
@@ -1367,6 +1521,21 @@ int rt_work_counts(rt_ctx *ctx, uint64_t *out, int32_t n, int32_t reset) {
         if (reset) RT_CK(cudaMemset(d.w_work.p, 0, sizeof h));
     }
     for (int i = 0; i < n && i < rt::kWorkN; i++) out[i] = h[i];
+    return RT_OK;
+}
+
+int rt_frame_expand_v1(const uint32_t *host_buf, int32_t width, int32_t height, uint32_t *pixels, int64_t pitch,
+                       int32_t threads, int64_t *words) {
+    if (!host_buf || !pixels) return fail(RT_ERR_INVALID, "null argument");
+    if (width < 1 || height < 1 || pitch < width) return fail(RT_ERR_INVALID, "bad frame size");
+    const int64_t n = rt::decode_rows(host_buf, width, 0, height, pixels, pitch, threads > 0 ? threads : 1);
+    if (words) *words = n;
+    return RT_OK;
+}
+
+int rt_last_d2h_bytes(rt_ctx *ctx, int64_t *bytes) {
+    if (!ctx || !bytes) return fail(RT_ERR_INVALID, "null argument");
+    *bytes = ctx->last_d2h_bytes;
     return RT_OK;
 }
 
@@ -1439,6 +1608,28 @@ int rt_copy_to_host(rt_ctx *ctx, int32_t slot, void *host_dst, const void *d_src
     return RT_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// A pipelined frame's end: its copy (or encode) done, then, compressed, its
+// expansion into the caller's framebuffer.
+int slot_finish(rt_ctx *ctx, Dev &d, int slot) {
+    RT_CK(cudaEventSynchronize(d.slot_done[slot]));
+    auto &so = d.slot_out[slot];
+    if (so.codec) {
+        const int64_t words = rt::decode_rows((const uint32_t *)d.slot_codec[slot].p, so.width, 0, so.height,
+                                              so.pixels, so.width, codec_threads(ctx));
+        ctx->last_d2h_bytes = (int64_t)sizeof(uint32_t) * words;
+    } else {
+        ctx->last_d2h_bytes = (int64_t)sizeof(uint32_t) * so.width * so.height;
+    }
+    d.slot_busy[slot] = false;
+    return RT_OK;
+}
+}  // namespace
+
+extern "C" {
+
 int rt_render_async_v1(rt_ctx *ctx, int32_t slot, uint32_t *pixels, int32_t width, int32_t height,
                        const double cam_pos[3], double yaw, double pitch, double vdist, int32_t n_bodies,
                        const int32_t *kinds, const double *positions, const double *sizes, const double *colors,
@@ -1456,9 +1647,8 @@ int rt_render_async_v1(rt_ctx *ctx, int32_t slot, uint32_t *pixels, int32_t widt
     std::lock_guard<std::mutex> lk(ctx->mu);
     Dev &d = ctx->devs[0];
     RT_CK(cudaSetDevice(d.id));
-    if (d.slot_busy[slot]) {  // the slot's previous frame was never waited for
-        RT_CK(cudaEventSynchronize(d.slot_done[slot]));
-        d.slot_busy[slot] = false;
+    if (d.slot_busy[slot]) {  // the slot's previous frame was never waited for: completed now
+        if ((rc = slot_finish(ctx, d, slot))) return rc;
     }
     const bool verify_sky = set_host_scene(ctx->scene, n_bodies, kinds, positions, sizes, colors, refls, light_pos,
                                            light_radius, light_color, ambient, max_refl, sky, sky_w, sky_h, has_sky);
@@ -1477,7 +1667,18 @@ int rt_render_async_v1(rt_ctx *ctx, int32_t slot, uint32_t *pixels, int32_t widt
         RT_CK(cudaEventRecord(d.e1, d.st));
         RT_CK(cudaEventRecord(d.slot_comp[slot], d.st));
         RT_CK(cudaStreamWaitEvent(d.copy_st, d.slot_comp[slot], 0));
-        RT_CK(cudaMemcpyAsync(pixels, d.slot_frame[slot].p, px_bytes, cudaMemcpyDeviceToHost, d.copy_st));
+        auto &so = d.slot_out[slot];
+        so.codec = ctx->codec && width <= rt::kCodecMaxWidth;
+        so.pixels = pixels;
+        so.width = width;
+        so.height = height;
+        if (so.codec) {  // encoded into the slot's mapped buffer; rt_frame_wait_v1 expands it
+            if ((rc = d.slot_codec[slot].ensure(rt::codec_host_bytes(width, height)))) return rc;
+            RT_CK(rt::launch_encode_rows((const uint32_t *)d.slot_frame[slot].p, width, width, height, 0, height,
+                                         (uint32_t *)d.slot_codec[slot].dp, d.copy_st));
+        } else {
+            RT_CK(cudaMemcpyAsync(pixels, d.slot_frame[slot].p, px_bytes, cudaMemcpyDeviceToHost, d.copy_st));
+        }
         RT_CK(cudaEventRecord(d.slot_done[slot], d.copy_st));
         if (attempt > 0 || !verify_sky || !sky_content_changed(ctx->scene)) break;
         RT_CK(cudaEventSynchronize(d.slot_done[slot]));  // the stale frame ends before the sky is replaced
@@ -1491,9 +1692,8 @@ int rt_frame_wait_v1(rt_ctx *ctx, int32_t slot) {
     if (slot < 0 || slot >= Dev::kSlots) return fail(RT_ERR_INVALID, "frame slot out of range");
     Dev &d = ctx->devs[0];
     RT_CK(cudaSetDevice(d.id));
-    RT_CK(cudaEventSynchronize(d.slot_done[slot]));
-    d.slot_busy[slot] = false;
-    return RT_OK;
+    if (!d.slot_busy[slot]) return RT_OK;
+    return slot_finish(ctx, d, slot);
 }
 
 int rt_copy_partition_to_host(rt_ctx *ctx, int32_t slot, uint32_t *host_frame, const uint32_t *d_frame, int32_t width,

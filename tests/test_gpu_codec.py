@@ -1,0 +1,98 @@
+"""The compressed frame transfer (option "codec", frame_codec.h) on the GPU:
+every frame it delivers equals the raw device-to-host copy bit for bit —
+full-size configurations, ragged and tiny frames, every band count, FP64,
+radiance alongside, the pipelined slots — and it moves fewer bytes."""
+
+import numpy as np
+import pytest
+
+import paper_2305_07450_b200 as rt
+from paper_2305_07450_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _restore_options():
+    yield
+    _native.set_options(codec=1, bands=0, codec_threads=0)
+
+
+def _frame(scene, cam, params, precision=None, radiance=None, **opts):
+    _native.set_options(**opts)
+    fb = rt.Framebuffer.create(params.width, params.height)
+    fb.pixels[:] = 0x5A5A5A5A  # a stale framebuffer: every pixel must be written
+    rt.render_frame(scene, cam, params, fb, precision=precision, radiance=radiance)
+    return fb.pixels.copy(), _native.context(1).last_d2h_bytes()
+
+
+def _small(width, height, samples=16, bounces=2, sky=False):
+    c = rt.CONFIGS["C3" if sky else "C2"]
+    params = rt.RenderParams(width=width, height=height, shadow_samples=samples, bounce_limit=bounces)
+    return c.scene(), c.camera(), params
+
+
+@pytest.mark.parametrize("key", ["C1", "C2", "C3", "P720", "P1080"])
+def test_codec_equals_raw_copy_full_size(key):
+    c = rt.CONFIGS[key]
+    scene, cam, params = c.scene(), c.camera(), c.params()
+    raw, raw_bytes = _frame(scene, cam, params, codec=0)
+    enc, enc_bytes = _frame(scene, cam, params, codec=1)
+    np.testing.assert_array_equal(enc, raw)
+    assert raw_bytes == 4 * c.width * c.height
+    assert enc_bytes < raw_bytes / 2, (enc_bytes, raw_bytes)
+
+
+@pytest.mark.parametrize("bands", [1, 2, 3, 6, 8])
+def test_codec_every_band_count(bands):
+    scene, cam, params = _small(333, 251, samples=32, bounces=3)
+    raw, _ = _frame(scene, cam, params, codec=0, bands=bands)
+    enc, _ = _frame(scene, cam, params, codec=1, bands=bands)
+    np.testing.assert_array_equal(enc, raw)
+
+
+@pytest.mark.parametrize("size", [(1, 1), (1, 9), (7, 3), (8, 8), (9, 17), (31, 5), (33, 40), (97, 61), (1000, 3)])
+def test_codec_ragged_and_tiny_frames(size):
+    w, h = size
+    scene, cam, params = _small(w, h, samples=8, bounces=1, sky=True)
+    raw, _ = _frame(scene, cam, params, codec=0)
+    enc, _ = _frame(scene, cam, params, codec=1)
+    np.testing.assert_array_equal(enc, raw)
+
+
+def test_codec_fp64_and_radiance_alongside():
+    scene, cam, params = _small(160, 90, samples=16, bounces=2, sky=True)
+    raw_rad = np.zeros((160 * 90, 3), dtype=np.float64)
+    enc_rad = np.zeros((160 * 90, 3), dtype=np.float64)
+    raw, _ = _frame(scene, cam, params, precision="fp64", radiance=raw_rad, codec=0)
+    enc, enc_bytes = _frame(scene, cam, params, precision="fp64", radiance=enc_rad, codec=1)
+    np.testing.assert_array_equal(enc, raw)
+    np.testing.assert_array_equal(enc_rad, raw_rad)
+    assert enc_bytes >= raw_rad.nbytes  # the radiance still travels raw
+
+
+@pytest.mark.parametrize("threads", [1, 2, 16])
+def test_codec_thread_counts(threads):
+    c = rt.CONFIGS["C2"]
+    scene, cam, params = c.scene(), c.camera(), c.params()
+    raw, _ = _frame(scene, cam, params, codec=0)
+    enc, _ = _frame(scene, cam, params, codec=1, codec_threads=threads)
+    np.testing.assert_array_equal(enc, raw)
+
+
+def test_codec_pipelined_frames_equal_raw():
+    c = rt.CONFIGS["C2"]
+    scene, cam, params = c.scene(), c.camera(), c.params()
+    cams = [rt.Camera(position=(0.3 * i, 1.4, -4.5), yaw=0.05 * i, pitch=-0.08, fov=60.0) for i in range(6)]
+    want = []
+    for cm in cams:
+        raw, _ = _frame(scene, cm, params, codec=0)
+        want.append(raw)
+    _native.set_options(codec=1)
+    pipe = rt.FramePipeline(depth=3)
+    fbs = [rt.Framebuffer.create(c.width, c.height) for _ in cams]
+    for cm, fb in zip(cams, fbs):
+        pipe.submit(scene, cm, params, fb)  # (waits for the frame depth tickets back)
+    pipe.drain()
+    for fb, w in zip(fbs, want):
+        np.testing.assert_array_equal(fb.pixels, w)

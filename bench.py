@@ -437,17 +437,24 @@ def run_ours(args):
         cams = [rt.Camera(position=cam.position, yaw=cam.yaw + 1e-4 * (i % 2), pitch=cam.pitch, fov=cam.fov)
                 for i in range(2)]
         ts = []
+        d2h = 0
+        ctx1 = _native.context(1)
         for i in range(steps):
             t = time.perf_counter()
             rt.render_frame(scene, cams[i % 2], params, fb, precision=args.precision)
             ts.append(time.perf_counter() - t)
+            d2h += ctx1.last_d2h_bytes()  # (outside the timed call)
         ps = rt.pack_scene(scene)
         # kinds, positions, sizes, colours, reflectivities, light, ambient, max_refl + camera (f64, i32)
         h2d = int(4 * len(ps.kinds) + 8 * (3 + 1 + 3 + 1) * len(ps.kinds) + 8 * (3 + 1 + 3 + 2) + 8 * 6)
+        codec = bool(_native.get_options().get("codec", 1))
         return {"value": steps / sum(ts), "unit": "frames/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": 4 * c.width * c.height, "ms_per_step": 1e3 * statistics.mean(ts),
-                "ms_median": 1e3 * statistics.median(ts),
-                "path": "paper_2305_07450_b200.render_frame -> rt_render_v1 (C ABI), pinned host framebuffer"}
+                "d2h_bytes_per_step": d2h // steps, "d2h_frame_bytes": 4 * c.width * c.height,
+                "ms_per_step": 1e3 * statistics.mean(ts), "ms_median": 1e3 * statistics.median(ts),
+                "transfer": ("compressed (option codec): the encode kernel's row runs into mapped host memory, "
+                             "expanded by host threads into the framebuffer, bit-exact; d2h_bytes_per_step as "
+                             "moved over PCIe (rt_last_d2h_bytes)") if codec else "raw frame copy",
+                "path": "paper_2305_07450_b200.render_frame -> rt_render_v1 (C ABI), host framebuffer"}
 
     line = {"metric": "frames/s", "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "vs_baseline": None,
@@ -461,6 +468,11 @@ def run_ours(args):
         peak_meas = _native.fp32_peak_tflops(local)
         roof = roofline(wcc, phases, work, ms_frame, cfg.samples, peak_meas, config_key=key)
         e2e = e2e_sync(cfg, args.steps)
+        # the same call with the frame copied raw (option codec off), for comparison
+        _native.set_options(codec=0)
+        raw = e2e_sync(cfg, args.steps)
+        _native.set_options(codec=1)
+        e2e["raw_copy"] = {k: raw[k] for k in ("value", "unit", "d2h_bytes_per_step", "ms_median")}
         # the frame server's loop: frames back to back through FramePipeline,
         # each frame's copy overlapping the next frame's kernels; every frame
         # still lands whole in a host framebuffer before it is counted
@@ -478,12 +490,13 @@ def run_ours(args):
             pipe.submit(scene, cams[i % 2], params, fbs[i % depth])
         pipe.drain()
         dt = time.perf_counter() - t
+        pipe_d2h = pipe.ctx.last_d2h_bytes()  # (the last frame's)
         pipe.close()
         e2e["pipelined"] = {"value": args.steps / dt, "unit": "frames/s",
                             "h2d_bytes_per_step": e2e["h2d_bytes_per_step"],
-                            "d2h_bytes_per_step": e2e["d2h_bytes_per_step"], "ms_per_step": 1e3 * dt / args.steps,
+                            "d2h_bytes_per_step": pipe_d2h, "ms_per_step": 1e3 * dt / args.steps,
                             "path": "paper_2305_07450_b200.FramePipeline (rt_render_async_v1 / rt_frame_wait_v1), "
-                                    "depth 3, pinned host framebuffers"}
+                                    "depth 3, host framebuffers"}
         line.update({
             "value": fps, "ms_per_step": main["total_ms"] / args.steps, "scaling": "weak",
             # config: the workload keys both arms share (--impl reference prints the same)

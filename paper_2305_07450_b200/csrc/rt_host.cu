@@ -129,6 +129,7 @@ struct Dev {
     int sm_count = 148;
     cudaStream_t st = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEvent_t pe0 = nullptr, pe1 = nullptr;  // the previous frame's pair while its time is still unread
     cudaEvent_t ph[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // wavefront phase boundaries
     cudaStream_t copy_st = nullptr;           // device->host copies of finished row bands
     cudaEvent_t band_ev[kMaxBands] = {};
@@ -238,8 +239,13 @@ struct rt_ctx {
         int width = 0, height = 0, bands = 0;
         int y_at[kMaxBands + 1] = {};
         int order[kMaxBands] = {};
+        bool radiance = false;  // copied raw alongside (finish_frame waits for it)
     } codec_frame;
     int64_t last_d2h_bytes = 0;  // bytes the last frame moved device -> host
+    // a compressed frame returns once its last band is expanded: its device
+    // time (events ms_e0 -> ms_e1) is read later, off the caller's path
+    bool ms_pending = false;
+    cudaEvent_t ms_e0 = nullptr, ms_e1 = nullptr;
     std::mutex mu;
     HostScene scene;
     float last_ms = 0.f;
@@ -729,7 +735,23 @@ int4 hot_rect(rt_ctx *ctx, const Dev &d, const rt::FrameArgs &fa) {
     return tx0 <= tx1 && ty0 <= ty1 ? make_int4(tx0, ty0, tx1, ty1) : make_int4(-1, -1, -1, -1);
 }
 
+// $B200RT_HOST_TIMING: where a synchronous call's host time goes (rt_render_v1 prints it)
+bool host_timing_on() {
+    static const bool on = std::getenv("B200RT_HOST_TIMING") != nullptr;
+    return on;
+}
+std::chrono::steady_clock::time_point g_t_first_launch, g_t_team_start, g_t_team_end, g_t_sync1, g_t_sync2,
+    g_t_elapsed;
+bool g_first_launch_pending = false;
+inline void stamp(std::chrono::steady_clock::time_point &t) {
+    if (host_timing_on()) t = std::chrono::steady_clock::now();
+}
+
 int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStream_t st, int buf = 0) {
+    if (g_first_launch_pending) {
+        stamp(g_t_first_launch);
+        g_first_launch_pending = false;
+    }
     WaveBufs &b = d.wb[buf];
     cudaError_t e;
     fa.rgba = ctx->rgba;
@@ -947,7 +969,8 @@ int rt_ctx_create(rt_ctx **out, const int32_t *devices, int32_t n_devices) {
         bool ok = cudaSetDevice(id) == cudaSuccess &&
                   cudaStreamCreateWithFlags(&d.st, cudaStreamNonBlocking) == cudaSuccess &&
                   cudaStreamCreateWithFlags(&d.copy_st, cudaStreamNonBlocking) == cudaSuccess &&
-                  cudaEventCreate(&d.e0) == cudaSuccess && cudaEventCreate(&d.e1) == cudaSuccess;
+                  cudaEventCreate(&d.e0) == cudaSuccess && cudaEventCreate(&d.e1) == cudaSuccess &&
+                  cudaEventCreate(&d.pe0) == cudaSuccess && cudaEventCreate(&d.pe1) == cudaSuccess;
         for (auto &ev : d.band_ev) ok = ok && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess;
         for (auto &ev : d.copy_ev) ok = ok && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess;
         ok = ok && cudaEventCreateWithFlags(&d.fork_ev, cudaEventDisableTiming) == cudaSuccess;
@@ -1010,6 +1033,8 @@ int rt_ctx_destroy(rt_ctx *ctx) {
         if (d.copy_st) cudaStreamDestroy(d.copy_st);
         if (d.e0) cudaEventDestroy(d.e0);
         if (d.e1) cudaEventDestroy(d.e1);
+        if (d.pe0) cudaEventDestroy(d.pe0);
+        if (d.pe1) cudaEventDestroy(d.pe1);
         if (d.st) cudaStreamDestroy(d.st);
     }
     delete ctx;
@@ -1038,6 +1063,15 @@ int rt_set_scene_v1(rt_ctx *ctx, int32_t n_bodies, const int32_t *kinds, const d
 }  // extern "C"
 
 namespace {
+
+// The last compressed frame's device time, once its events are done (rt_ctx::ms_pending).
+int settle_last_ms(rt_ctx *ctx) {
+    if (!ctx->ms_pending) return RT_OK;
+    ctx->ms_pending = false;
+    RT_CK(cudaEventSynchronize(ctx->ms_e1));
+    RT_CK(cudaEventElapsedTime(&ctx->last_ms, ctx->ms_e0, ctx->ms_e1));
+    return RT_OK;
+}
 
 // Enqueue one frame of rt_render_v1 on n_dev devices (no wait).
 int enqueue_frame(rt_ctx *ctx, int n_dev, uint32_t *pixels, void *radiance, int32_t width, int32_t height,
@@ -1068,6 +1102,7 @@ int enqueue_frame(rt_ctx *ctx, int n_dev, uint32_t *pixels, void *radiance, int3
         void *host_rad = nullptr;
         if (ctx->zero_copy && cudaHostGetDevicePointer((void **)&host_px, pixels, 0) == cudaSuccess &&
             (!radiance || cudaHostGetDevicePointer(&host_rad, radiance, 0) == cudaSuccess)) {
+            if ((rc = settle_last_ms(ctx))) return rc;
             RT_CK(cudaEventRecord(d.e0, d.st));
             for (int p = 0; p < n_parts; p++) {
                 rt::FrameArgs fa = frame_args(host_px, width, host_rad, width, height, cam_pos, yaw, pitch, vdist,
@@ -1120,10 +1155,20 @@ int enqueue_frame(rt_ctx *ctx, int n_dev, uint32_t *pixels, void *radiance, int3
         if (cf.on) {
             if ((rc = d.codec_host.ensure(rt::codec_host_bytes(width, height)))) return rc;
             cf.pixels = pixels;
+            cf.radiance = radiance != nullptr;
             cf.width = width;
             cf.height = height;
             cf.bands = bands;
             for (int k = 0; k <= bands; k++) cf.y_at[k] = y_at[k];
+        }
+        // the previous compressed frame's events, unread: kept aside and read
+        // once this frame is launched
+        const bool settle_after = ctx->ms_pending;
+        if (settle_after) {
+            std::swap(d.e0, d.pe0);
+            std::swap(d.e1, d.pe1);
+            ctx->ms_e0 = d.pe0;
+            ctx->ms_e1 = d.pe1;
         }
         RT_CK(cudaEventRecord(d.e0, d.st));
         if (bands > 1) RT_CK(cudaEventRecord(d.fork_ev, d.st));
@@ -1182,6 +1227,7 @@ int enqueue_frame(rt_ctx *ctx, int n_dev, uint32_t *pixels, void *radiance, int3
             }
         }
         RT_CK(cudaEventRecord(d.e1, d.st));
+        if (settle_after && (rc = settle_last_ms(ctx))) return rc;
         ctx->band_pending = bands;
         ctx->last_d2h_bytes = (cf.on ? 0 : (int64_t)px_bytes) + (radiance ? (int64_t)rad_bytes : 0);
         return RT_OK;
@@ -1190,6 +1236,7 @@ int enqueue_frame(rt_ctx *ctx, int n_dev, uint32_t *pixels, void *radiance, int3
     // returns only its rows
     ctx->codec_frame.on = false;
     ctx->last_d2h_bytes = (int64_t)px_bytes + (radiance ? (int64_t)rad_bytes : 0);
+    if ((rc = settle_last_ms(ctx))) return rc;
     for (int g = 0; g < n_dev; g++) {
         Dev &d = ctx->devs[g];
         RT_CK(cudaSetDevice(d.id));
@@ -1252,22 +1299,37 @@ int finish_frame(rt_ctx *ctx, int n_dev, const rt::CodecSideJob *side = nullptr)
             }
         } w{&d};
         int wrc = RT_OK;
+        stamp(g_t_team_start);
         const int64_t words = rt::decode_bands((const uint32_t *)d.codec_host.p, cf.width, cf.bands, cf.y_at,
                                                cf.order, &W::query, &W::wait, &w, &wrc, cf.pixels, cf.width,
                                                std::max(codec_threads(ctx), side ? sky_threads() : 1), side);
+        stamp(g_t_team_end);
         cf.on = false;
         if (words < 0) return wrc;
         ctx->last_d2h_bytes += (int64_t)sizeof(uint32_t) * words;
+        // the frame is in the caller's buffer and the encode was the streams'
+        // last work: return now (stream syncs and the events' elapsed time
+        // cost ~8 us here); the device time is read later (settle_last_ms)
+        if (!cf.radiance && !ctx->phases && !ctx->band_times) {
+            ctx->ms_pending = true;
+            ctx->ms_e0 = d.e0;
+            ctx->ms_e1 = d.e1;
+            ctx->band_count = 0;
+            return RT_OK;
+        }
     }
     for (int g = 0; g < n_dev; g++) {
         Dev &d = ctx->devs[g];
         RT_CK(cudaSetDevice(d.id));
         if (n_dev == 1) RT_CK(cudaStreamSynchronize(d.copy_st));
+        stamp(g_t_sync1);
         RT_CK(cudaStreamSynchronize(d.st));
     }
+    stamp(g_t_sync2);
     Dev &d = ctx->devs[0];
     RT_CK(cudaSetDevice(d.id));
     RT_CK(cudaEventElapsedTime(&ctx->last_ms, d.e0, d.e1));
+    stamp(g_t_elapsed);
     ctx->band_count = (n_dev == 1 && ctx->band_times) ? ctx->band_pending : 0;
     for (int k = 0; k < ctx->band_count; k++) {
         RT_CK(cudaEventElapsedTime(&ctx->band_ms[k], d.e0, d.tl_ev[k]));
@@ -1280,10 +1342,6 @@ int finish_frame(rt_ctx *ctx, int n_dev, const rt::CodecSideJob *side = nullptr)
 
 extern "C" {
 
-static bool host_timing() {
-    static const bool on = std::getenv("B200RT_HOST_TIMING") != nullptr;
-    return on;
-}
 
 int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, int32_t height,
                  const double cam_pos[3], double yaw, double pitch, double vdist, int32_t n_bodies,
@@ -1292,6 +1350,7 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
                  double ambient, double max_refl, const float *sky, int32_t sky_w, int32_t sky_h, int32_t has_sky,
                  int32_t shadow_samples, int32_t bounce_limit, int32_t n_parts, int32_t precision) {
     const auto t_call = std::chrono::steady_clock::now();
+    g_first_launch_pending = host_timing_on();
     if (!ctx || !pixels || !cam_pos) return fail(RT_ERR_INVALID, "null argument");
     int rc = check_frame_args(width, height, shadow_samples, bounce_limit, precision);
     if (rc) return rc;
@@ -1331,11 +1390,15 @@ int rt_render_v1(rt_ctx *ctx, uint32_t *pixels, void *radiance, int32_t width, i
     }
     const auto t_wait = std::chrono::steady_clock::now();
     if (!finished && (rc = finish_frame(ctx, n_dev))) return rc;
-    if (host_timing()) {  // $B200RT_HOST_TIMING: where a synchronous call's host time goes
+    if (host_timing_on()) {  // $B200RT_HOST_TIMING: where a synchronous call's host time goes
         const auto t_end = std::chrono::steady_clock::now();
         auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
-        fprintf(stderr, "rt_render_v1: setup %.1f us, enqueue %.1f us, wait %.1f us, device e0->e1 %.1f us\n",
-                us(t_call, t_enq), us(t_enq, t_wait), us(t_wait, t_end), 1e3 * ctx->last_ms);
+        fprintf(stderr,
+                "rt_render_v1: setup %.1f us, first launch at %.1f, enqueue %.1f us, wait %.1f us (expansion team "
+                "%.1f .. %.1f), syncs %.1f %.1f, elapsed %.1f, end %.1f; device e0->e1 %.1f us\n",
+                us(t_call, t_enq), us(t_call, g_t_first_launch), us(t_enq, t_wait), us(t_wait, t_end),
+                us(t_call, g_t_team_start), us(t_call, g_t_team_end), us(t_call, g_t_sync1), us(t_call, g_t_sync2),
+                us(t_call, g_t_elapsed), us(t_call, t_end), 1e3 * ctx->last_ms);
     }
     return upload_sky_all(ctx);
 }
@@ -1407,6 +1470,7 @@ int rt_trace_rays_v1(rt_ctx *ctx, const double *origins, const double *dirs, int
     double *d_o = (double *)d.rays_in.p, *d_d = d_o + 3 * n_rays;
     RT_CK(cudaMemcpyAsync(d_o, origins, in_b, cudaMemcpyHostToDevice, d.st));
     RT_CK(cudaMemcpyAsync(d_d, dirs, in_b, cudaMemcpyHostToDevice, d.st));
+    if ((rc = settle_last_ms(ctx))) return rc;
     RT_CK(cudaEventRecord(d.e0, d.st));
     cudaError_t e;
     if (precision == RT_PREC_FP64)
@@ -1541,6 +1605,9 @@ int rt_last_d2h_bytes(rt_ctx *ctx, int64_t *bytes) {
 
 int rt_last_kernel_ms(rt_ctx *ctx, float *ms) {
     if (!ctx || !ms) return fail(RT_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    int rc;
+    if ((rc = settle_last_ms(ctx))) return rc;
     *ms = ctx->last_ms;
     return RT_OK;
 }
@@ -1662,6 +1729,7 @@ int rt_render_async_v1(rt_ctx *ctx, int32_t slot, uint32_t *pixels, int32_t widt
         if ((rc = d.slot_frame[slot].ensure(px_bytes))) return rc;
         rt::FrameArgs fa = frame_args((uint32_t *)d.slot_frame[slot].p, width, nullptr, width, height, cam_pos, yaw,
                                       pitch, vdist, shadow_samples, bounce_limit, 0, 1, RT_DEFAULT_BLOCK_ROWS);
+        if ((rc = settle_last_ms(ctx))) return rc;
         RT_CK(cudaEventRecord(d.e0, d.st));
         if ((rc = launch_frame(ctx, d, fa, precision, d.st))) return rc;
         RT_CK(cudaEventRecord(d.e1, d.st));

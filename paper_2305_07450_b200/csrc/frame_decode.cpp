@@ -14,6 +14,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 namespace {
@@ -34,9 +36,24 @@ struct Lut {
 };
 const Lut g_lut;
 
-bool have_avx2() {
-    static const bool on = __builtin_cpu_supports("avx2") && __builtin_cpu_supports("popcnt");
-    return on;
+// The widest expander the CPU runs; $B200RT_CODEC_ISA (scalar | avx2 |
+// avx512) picks a narrower one (the CPU tests run each).
+enum Isa { kScalar, kAvx2, kAvx512 };
+Isa codec_isa() {
+    static const Isa isa = [] {
+        const bool a2 = __builtin_cpu_supports("avx2") && __builtin_cpu_supports("popcnt");
+        const bool a512 = a2 && __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw") &&
+                          __builtin_cpu_supports("avx512vl") && __builtin_cpu_supports("avx512vbmi") &&
+                          __builtin_cpu_supports("avx512vpopcntdq");
+        Isa best = a512 ? kAvx512 : a2 ? kAvx2 : kScalar;
+        if (const char *e = std::getenv("B200RT_CODEC_ISA")) {
+            const std::string v(e);
+            if (v == "scalar") best = kScalar;
+            if (v == "avx2" && a2) best = kAvx2;
+        }
+        return best;
+    }();
+    return isa;
 }
 
 // A row's header words (frame_codec.h).
@@ -139,22 +156,82 @@ __attribute__((target("avx2,popcnt"))) void row_avx2(const Row &r, const uint32_
     }
 }
 
-// a row's widened literals: [0] a readable word before them, 24 spare words
+// AVX-512 (VBMI + VPOPCNTDQ): 16 pixels a step.  Lane j's literal index is
+// popcount(m & (2^(j+1) - 1)) - 1 (no table); lanes before the first literal
+// keep the previous pixel (a merge-masked permute).
+constexpr uint32_t kPrefix[16] = {0x1,   0x3,   0x7,   0xf,   0x1f,   0x3f,   0x7f,   0xff,
+                                  0x1ff, 0x3ff, 0x7ff, 0xfff, 0x1fff, 0x3fff, 0x7fff, 0xffff};
+#define RT_AVX512 __attribute__((target("avx512f,avx512bw,avx512vl,avx512vbmi,avx512vpopcntdq,popcnt")))
+
+RT_AVX512 inline __m512i half_avx512(unsigned m, const uint32_t *&lit) {
+    const __m512i cnt = _mm512_popcnt_epi32(_mm512_and_si512(_mm512_set1_epi32((int)m), _mm512_loadu_si512(kPrefix)));
+    const __mmask16 k = _mm512_test_epi32_mask(cnt, cnt);
+    const __m512i idx = _mm512_sub_epi32(cnt, _mm512_set1_epi32(1));
+    const __m512i v = _mm512_mask_permutexvar_epi32(_mm512_set1_epi32((int)lit[-1]), k, idx, _mm512_loadu_si512(lit));
+    lit += __builtin_popcount(m);
+    return v;
+}
+
+RT_AVX512 void unpack_avx512(const uint32_t *src, int n, uint32_t *dst) {
+    const uint8_t *b = reinterpret_cast<const uint8_t *>(src);
+    alignas(64) uint8_t sel[64];
+    for (int k = 0; k < 16; k++)
+        for (int t = 0; t < 4; t++) sel[4 * k + t] = (uint8_t)(t < 3 ? 3 * k + t : 0);
+    const __m512i idx = _mm512_load_si512(sel);
+    const __m512i alpha = _mm512_set1_epi32((int)0xff000000u);
+    int i = 0;
+    for (; i + 16 <= n; i += 16) {  // (reads 16 bytes past the 48 used: inside the row's stride or the pad)
+        const __m512i v = _mm512_loadu_si512(b + 3 * i);
+        _mm512_storeu_si512(dst + i, _mm512_or_si512(_mm512_permutexvar_epi8(idx, v), alpha));
+    }
+    for (; i < n; i++) dst[i] = widen(b + 3 * i);
+}
+
+RT_AVX512 void row_avx512(const Row &r, const uint32_t *lit, int w, uint32_t *out) {
+    const uint32_t *next = r.masks;
+    const int words = w / 32;
+    for (int j = 0; j < words; j++) {
+        const uint32_t wd = mask_word(r, j, next);
+        uint32_t *o = out + 32 * j;
+        if (wd == 0) {  // 32 repeats of the pixel to the left
+            const __m512i prev = _mm512_set1_epi32((int)lit[-1]);
+            _mm512_storeu_si512(o, prev);
+            _mm512_storeu_si512(o + 16, prev);
+            continue;
+        }
+        _mm512_storeu_si512(o, half_avx512(wd & 0xffffu, lit));
+        _mm512_storeu_si512(o + 16, half_avx512(wd >> 16, lit));
+    }
+    const int rest = w - 32 * words;
+    if (rest > 0) {  // the last, partial mask word: masked stores
+        const uint32_t wd = mask_word(r, words, next);
+        uint32_t *o = out + 32 * words;
+        const int lo = rest < 16 ? rest : 16;
+        _mm512_mask_storeu_epi32(o, (__mmask16)((1u << lo) - 1u), half_avx512(wd & 0xffffu, lit));
+        if (rest > 16) _mm512_mask_storeu_epi32(o + 16, (__mmask16)((1u << (rest - 16)) - 1u), half_avx512(wd >> 16, lit));
+    }
+}
+
+// a row's widened literals: [0] a readable word before them, 40 spare words
 thread_local std::vector<uint32_t> t_scratch;
 
-int64_t expand_row(const uint32_t *base, int width, uint32_t *out, bool avx2) {
+int64_t expand_row(const uint32_t *base, int width, uint32_t *out, Isa isa) {
     const Row r = parse(base, width);
     const uint32_t *lit = r.lits;  // (unpacked: lit[-1] is a header or mask word, readable)
     if (r.packed) {
-        if (t_scratch.size() < (size_t)width + 24) t_scratch.assign((size_t)width + 24, 0u);
+        if (t_scratch.size() < (size_t)width + 40) t_scratch.assign((size_t)width + 40, 0u);
         uint32_t *s = t_scratch.data() + 1;
-        if (avx2)
+        if (isa == kAvx512)
+            unpack_avx512(r.lits, r.n, s);
+        else if (isa == kAvx2)
             unpack_avx2(r.lits, r.n, s);
         else
             unpack_scalar(r.lits, r.n, s);
         lit = s;
     }
-    if (avx2)
+    if (isa == kAvx512)
+        row_avx512(r, lit, width, out);
+    else if (isa == kAvx2)
         row_avx2(r, lit, width, out);
     else
         row_scalar(r, lit, width, out);
@@ -167,10 +244,10 @@ namespace rt {
 
 int64_t decode_rows_serial(const uint32_t *host, int width, int y0, int y1, uint32_t *dst, int64_t pitch) {
     const int64_t stride = codec_row_stride(width);
-    const bool avx2 = have_avx2();
+    const Isa isa = codec_isa();
     int64_t total = 0;
     for (int y = y0; y < y1; y++)
-        total += expand_row(host + codec_rows_offset(0) + (size_t)y * stride, width, dst + (size_t)y * pitch, avx2);
+        total += expand_row(host + codec_rows_offset(0) + (size_t)y * stride, width, dst + (size_t)y * pitch, isa);
     return total;
 }
 

@@ -120,3 +120,26 @@ def test_expand_rejects_bad_sizes():
     assert lib.rt_frame_expand_v1(buf.ctypes.data, 0, 1, out.ctypes.data, 1, 1, None) != 0
     assert lib.rt_frame_expand_v1(buf.ctypes.data, 4, 1, out.ctypes.data, 3, 1, None) != 0
     assert lib.rt_frame_expand_v1(None, 4, 1, out.ctypes.data, 4, 1, None) != 0
+
+
+@pytest.mark.parametrize("isa", ["scalar", "avx2"])
+def test_expand_narrower_isas(isa):
+    """The AVX2 and scalar expanders ($B200RT_CODEC_ISA, read once per
+    process) on the same frames as the default (AVX-512 where the CPU has it)."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, test_codec as t\n"
+        "for w in (1, 7, 8, 9, 33, 65, 1025):\n"
+        "    for opaque in (False, True):\n"
+        "        f = t.runs_frame(np.random.default_rng(w), 9, w, 3.0, opaque)\n"
+        "        buf, n = t.encode(f)\n"
+        "        out, m = t.expand(buf, w, 9, threads=2)\n"
+        "        assert m == n and (out == f).all(), (w, opaque)\n"
+    )
+    env = dict(os.environ, B200RT_CODEC_ISA=isa)
+    here = os.path.dirname(os.path.abspath(__file__))
+    env["PYTHONPATH"] = os.pathsep.join([here, os.path.dirname(here), env.get("PYTHONPATH", "")])
+    subprocess.run([sys.executable, "-c", code], env=env, check=True, cwd=here, timeout=120)

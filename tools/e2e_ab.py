@@ -30,7 +30,9 @@ def main():
     cams = [rt.Camera(position=cam.position, yaw=cam.yaw + 1e-4 * i, pitch=cam.pitch, fov=cam.fov) for i in range(2)]
     fb = rt.Framebuffer.create(cfg.width, cfg.height)
     base = _native.get_options()
-    specs = ["default"] + a.set
+    # (with explicit sets there is no "default" run: in interleaved rounds it
+    # would inherit whatever option the previous set left on the context)
+    specs = a.set if a.set else ["default"]
     times = {spec: [] for spec in specs}
     kernel = {}
 

@@ -96,3 +96,96 @@ def test_codec_pipelined_frames_equal_raw():
     pipe.drain()
     for fb, w in zip(fbs, want):
         np.testing.assert_array_equal(fb.pixels, w)
+
+
+def test_codec_rgba_byte_order():
+    """Option rgba (the frame server's R,G,B,A bytes): alpha is still the top
+    byte, so rows travel packed; the frame equals the raw copy's."""
+    scene, cam, params = _small(200, 120, samples=16, bounces=2, sky=True)
+    try:
+        raw, _ = _frame(scene, cam, params, codec=0, rgba=1)
+        enc, enc_bytes = _frame(scene, cam, params, codec=1, rgba=1)
+    finally:
+        _native.set_options(rgba=0)
+    np.testing.assert_array_equal(enc, raw)
+    assert (enc >> 24 == 0xFF).all()
+    assert enc_bytes < 200 * 120 * 4
+
+
+def test_codec_pipeline_mixed_sizes_and_depth4():
+    """Slots of different frame sizes in flight at once (each slot keeps its own
+    mapped buffer and expands into its own framebuffer)."""
+    c = rt.CONFIGS["C3"]
+    scene = c.scene()
+    sizes = [(320, 180), (97, 61), (640, 360), (1, 9), (333, 251), (160, 90)]
+    cam = c.camera()
+    want = []
+    for w, h in sizes:
+        p = rt.RenderParams(width=w, height=h, shadow_samples=16, bounce_limit=2)
+        raw, _ = _frame(scene, cam, p, codec=0)
+        want.append(raw)
+    _native.set_options(codec=1)
+    pipe = rt.FramePipeline(depth=4)
+    fbs = []
+    for w, h in sizes:
+        p = rt.RenderParams(width=w, height=h, shadow_samples=16, bounce_limit=2)
+        fb = rt.Framebuffer.create(w, h)
+        fb.pixels[:] = 0x5A5A5A5A
+        fbs.append(fb)
+        pipe.submit(scene, cam, p, fb)
+    pipe.drain()
+    for fb, w in zip(fbs, want):
+        np.testing.assert_array_equal(fb.pixels, w)
+
+
+def test_codec_two_threads_two_contexts():
+    """render_frame on the shared context and a FramePipeline (its own context)
+    from two Python threads at once: each expansion team writes its own frame."""
+    import threading
+
+    c = rt.CONFIGS["C2"]
+    scene, cam, params = c.scene(), c.camera(), c.params()
+    want, _ = _frame(scene, cam, params, codec=0)
+    _native.set_options(codec=1)
+    errors = []
+
+    def sync_loop():
+        try:
+            fb = rt.Framebuffer.create(c.width, c.height)
+            for _ in range(20):
+                fb.pixels[:] = 0
+                rt.render_frame(scene, cam, params, fb)
+                np.testing.assert_array_equal(fb.pixels, want)
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    def pipe_loop():
+        try:
+            pipe = rt.FramePipeline(depth=2)
+            fbs = [rt.Framebuffer.create(c.width, c.height) for _ in range(20)]
+            for fb in fbs:
+                pipe.submit(scene, cam, params, fb)
+            pipe.drain()
+            for fb in fbs:
+                np.testing.assert_array_equal(fb.pixels, want)
+            pipe.close()
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+
+    ts = [threading.Thread(target=sync_loop), threading.Thread(target=pipe_loop)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+
+
+def test_codec_reports_fewer_bytes_and_device_time():
+    """rt_last_d2h_bytes: the compressed run's bytes; rt_last_kernel_ms still
+    reports the frame's device time (read after the early return)."""
+    c = rt.CONFIGS["C2"]
+    scene, cam, params = c.scene(), c.camera(), c.params()
+    _, enc_bytes = _frame(scene, cam, params, codec=1)
+    ms = rt.last_kernel_ms()
+    assert 0.01 < ms < 5.0
+    assert 100_000 < enc_bytes < 1_000_000

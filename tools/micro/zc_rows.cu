@@ -20,6 +20,12 @@ __global__ void grid_stride(unsigned *out, long n) {
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) out[i] = (unsigned)i;
 }
 
+static unsigned *g_dev = nullptr;
+unsigned *dsrc_dev() {
+    if (!g_dev) cudaMalloc(&g_dev, 64u << 20);
+    return g_dev;
+}
+
 template <typename F>
 float time_us(F f) {
     cudaEvent_t a, b;
@@ -58,6 +64,13 @@ int main() {
         }
     float e = time_us([] {});
     printf("empty event pair %.1f us\n", e);
+    // zero-copy kernel time against size (one CTA of 256 per 32 KB): the intercept is the fixed cost
+    for (double kb : {0.0, 4.0, 16.0, 64.0, 128.0, 256.0, 512.0}) {
+        const long n = (long)(kb * 256);
+        float t = time_us([&] { grid_stride<<<std::max(1L, n / 8192), 256>>>(d, n); });
+        float tr = time_us([&] { grid_stride<<<std::max(1L, n / 8192), 256>>>(dsrc_dev(), n); });
+        printf("zero-copy %6.1f KB: %6.1f us   (same kernel into device memory %6.1f us)\n", kb, t, tr);
+    }
     // the same sizes by the copy engine, device -> pinned host
     unsigned *dsrc;
     cudaMalloc(&dsrc, bytes);

@@ -36,6 +36,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # SMs x FP32 lanes x FMA x max SM clock
+# instruction issue: 148 SMs x 4 schedulers x 1 warp instruction per cycle at 1965 MHz
+ISSUE_PEAK_WARP_INST_PER_S = 148 * 4 * 1.965e9
 L2_FLUSH_BYTES = 256 << 20
 EXTRA_CONFIGS = ("C1", "P720", "P1080", "P4K", "C3", "C4", "C5", "C5_512")
 
@@ -775,6 +777,11 @@ def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True, config_key
                 per_kernel[k]["counter_flops_fp64"] = c64
                 per_kernel[k]["counter_achieved"] = (cf + c64) / (ms * 1e-3) / 1e12
                 per_kernel[k]["model_over_counter"] = flops[k] / (cf + c64)
+            wi = counters.get(k, {}).get("warp_inst")
+            if wi:  # the instruction-issue roofline (what bounds a divergent per-pixel chain)
+                per_kernel[k]["issue"] = {"warp_inst_per_launch": wi, "achieved": wi / (ms * 1e-3),
+                                          "peak": ISSUE_PEAK_WARP_INST_PER_S, "unit": "warp inst/s",
+                                          "frac": wi / (ms * 1e-3) / ISSUE_PEAK_WARP_INST_PER_S}
     out = {
         "bound": "fp32",
         "kernel": kernel,
@@ -802,6 +809,17 @@ def roofline(wcc, phases, work, ms_frame, samples, peak, culled=True, config_key
         out["counter_achieved"] = per_kernel[kernel]["counter_achieved"]
         out["model_over_counter"] = per_kernel[kernel]["model_over_counter"]
         out["counter_source"] = counters.get("_source") or _load_profile("ncu_flops.json").get("_source")
+    if per_kernel.get(kernel, {}).get("issue"):
+        # beside the FP32 roofline: the same kernel against instruction issue
+        # (148 SMs x 4 schedulers x 1 warp instruction per cycle) — its FP32
+        # fraction is bounded by its instruction mix, its issue
+        # fraction by latency
+        iss = per_kernel[kernel]["issue"]
+        out["issue_roofline"] = {"bound": "instruction issue", "kernel": kernel, "achieved": iss["achieved"],
+                                 "peak": iss["peak"], "unit": "warp inst/s", "frac": iss["frac"],
+                                 "warp_inst_per_launch": iss["warp_inst_per_launch"],
+                                 "source": "smsp__inst_executed from profiles/ncu_flops.json (per launch) over "
+                                           "this run's kernel time; peak 148 x 4 x 1.965 GHz"}
     return out
 
 

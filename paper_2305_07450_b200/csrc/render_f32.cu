@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, RT_F32_TILE_MIN_BLOCKS)
     render_f32_tile_kernel(const FrameArgs fa, const SceneArgs<float> sa, const ParamScene<MAXS> ps,
                            const MegaCull mc) {
     int x, ly;
-    thread_pixel_hot_first(mc.hot, x, ly);
+    thread_pixel_hot_first(mc.hot, mc.hot_div, x, ly);
     shade_pixel<BMAX>(ps, fa, sa, mc, x, ly);
     if (fa.peer_out) __threadfence_system();
 }

@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, MAXS <= 8 ? RT_TRACE_MIN_BLOCKS : 6)
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 8) wa.count_next[threadIdx.x] = 0;
 
     int x, ly;
-    thread_pixel_hot_first(wa.hot, x, ly);
+    thread_pixel_hot_first(wa.hot, wa.hot_div, x, ly);
     int y = 0;
     bool alive = x < fa.width && ly < fa.local_rows;
     if (alive) {

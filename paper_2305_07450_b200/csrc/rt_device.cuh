@@ -60,6 +60,7 @@ struct MegaCull {
     float grid_lo[3], grid_inv[3];
     int grid_dim[3];
     int4 hot;  // the tile kernel's hot tile rectangle (tile_of_block); x < 0: bottom rows first
+    unsigned long long hot_div[3];  // tile_of_block's divisors as multipliers (tile_divisor)
 };
 
 // The spheres whose primary-ray box holds pixel (x, y) (all when no boxes).
@@ -123,6 +124,7 @@ struct WaveArgs {
                        // [(2q + r) lane_cap]; lengths count[3] and count[0]
     unsigned lane_cap; // (0: off)
     int4 hot;          // the trace's hot tile rectangle (tile_of_block); x < 0: bottom rows first
+    unsigned long long hot_div[3];  // tile_of_block's divisors as multipliers (tile_divisor)
     int compact;       // many-sphere trace: pack the CTA's live rays between bounces (render_fused_f32.cu)
 };
 // FP64 culled wavefront (render_fused_f64.cu): queues in float64
@@ -205,7 +207,15 @@ __device__ __forceinline__ void thread_pixel_bottom_first(int &x, int &ly) {
 // linear block index onto the tiles (the hardware dispatches CTAs in
 // index order): the costliest tiles start early and the cheap ones fill the
 // last wave.
-__device__ __forceinline__ void tile_of_block(int4 h, int &tx, int &ty) {
+// The divisors of tile_of_block (the grid width W, the rectangle's width rw
+// and W - rw) as multipliers formed on the host: q = (j m) >> 32 with
+// m = floor(2^32 / d) + 1 is j / d exactly while j d < 2^32 (j < 2^20 tiles,
+// d < 2^12) — one wide multiply instead of the generic division sequence,
+// which every thread of the trace ran (~4% of its instructions).
+inline unsigned long long tile_divisor(int d) { return d > 0 ? (1ull << 32) / (unsigned)d + 1ull : 0ull; }
+__device__ __forceinline__ int tdiv(int j, unsigned long long m) { return (int)(((unsigned long long)j * m) >> 32); }
+
+__device__ __forceinline__ void tile_of_block(int4 h, const unsigned long long *dv, int &tx, int &ty) {
     const int W = gridDim.x, H = gridDim.y, b = blockIdx.y * W + blockIdx.x;
     if (h.x < 0) {
         tx = blockIdx.x;
@@ -214,32 +224,36 @@ __device__ __forceinline__ void tile_of_block(int4 h, int &tx, int &ty) {
     }
     const int rw = h.z - h.x + 1, rh = h.w - h.y + 1, area = rw * rh;
     if (b < area) {
-        tx = h.x + b % rw;
-        ty = h.w - b / rw;
+        const int q = tdiv(b, dv[1]);
+        tx = h.x + (b - q * rw);
+        ty = h.w - q;
         return;
     }
     int j = b - area;
     const int below = (H - 1 - h.w) * W;  // full rows under the rectangle
     if (j < below) {
-        ty = H - 1 - j / W;
-        tx = j % W;
+        const int q = tdiv(j, dv[0]);
+        ty = H - 1 - q;
+        tx = j - q * W;
         return;
     }
     j -= below;
     const int side = W - rw, beside = side * rh;  // the rectangle's rows, left and right of it
     if (j < beside) {
-        ty = h.w - j / side;
-        const int k = j % side;
+        const int q = tdiv(j, dv[2]);
+        ty = h.w - q;
+        const int k = j - q * side;
         tx = k < h.x ? k : k + rw;
         return;
     }
     j -= beside;
-    ty = h.y - 1 - j / W;  // full rows above it
-    tx = j % W;
+    const int q = tdiv(j, dv[0]);
+    ty = h.y - 1 - q;  // full rows above it
+    tx = j - q * W;
 }
-__device__ __forceinline__ void thread_pixel_hot_first(int4 h, int &x, int &ly) {
+__device__ __forceinline__ void thread_pixel_hot_first(int4 h, const unsigned long long *dv, int &x, int &ly) {
     int tx, ty;
-    tile_of_block(h, tx, ty);
+    tile_of_block(h, dv, tx, ty);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     x = tx * kTileW + (warp & 1) * 8 + (lane & 7);
     ly = ty * kTileH + (warp >> 1) * 4 + (lane >> 3);

@@ -844,6 +844,12 @@ int launch_frame(rt_ctx *ctx, Dev &d, rt::FrameArgs fa, int precision, cudaStrea
             }
         }
         wa.hot = fused ? hot_rect(ctx, d, fa) : make_int4(-1, -1, -1, -1);
+        if (wa.hot.x >= 0) {
+            const int tw = (fa.width + rt::kTileW - 1) / rt::kTileW, rw = wa.hot.z - wa.hot.x + 1;
+            wa.hot_div[0] = rt::tile_divisor(tw);
+            wa.hot_div[1] = rt::tile_divisor(rw);
+            wa.hot_div[2] = rt::tile_divisor(tw - rw);
+        }
         wa.compact = ctx->compact;
         wa.work = nullptr;
         if (ctx->count_work) {

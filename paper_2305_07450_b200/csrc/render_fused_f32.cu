@@ -603,21 +603,29 @@ __device__ __forceinline__ void resolve_hit(const FrameArgs &fa, const SceneArgs
     // the records do not change after the trace, except the coefficients the
     // countdown's samplers store: the prefetched ones serve unless those landed
     const int have = (pre && (!several || packed)) ? pre->n : 0;
-    float4 rk[kMaxBounce + 1];  // every record load in flight before the first use
+    auto coeff = [&](int k, float w) {
+        float c = w;
+        if (k == kh && !several) c = sc;
+        if ((pm >> k) & 1) c = (float)((int)((counts >> (16 * k)) & 0xffffu) - 1) / (float)n;
+        return c;
+    };
+    float3 c;
+    if (have >= m) {  // every record prefetched (frames of up to kPre - 1 bounces): registers only
+        c = unwind_upto<kPre>(
+            m, (info >> 8) & 1, f3(px.x, px.y, px.z), sa,
+            [&](int k) { return Record{__float_as_int(pre->r[k].x), pre->r[k].y, pre->r[k].z, coeff(k, pre->r[k].w)}; },
+            mat4);
+    } else {
+        float4 rk[kMaxBounce + 1];  // every record load in flight before the first use
 #pragma unroll
-    for (int k = 0; k < kPre; k++)
-        if (k < have) rk[k] = pre->r[k];
+        for (int k = 0; k < kPre; k++)
+            if (k < have) rk[k] = pre->r[k];
 #pragma unroll 4
-    for (int k = have; k < m; k++) rk[k] = __ldcg(wa.rec + (int64_t)k * n_pix + lp);
-    const float3 c = unwind(
-        m, (info >> 8) & 1, f3(px.x, px.y, px.z), sa,
-        [&](int k) {
-            float c = rk[k].w;
-            if (k == kh && !several) c = sc;
-            if ((pm >> k) & 1) c = (float)((int)((counts >> (16 * k)) & 0xffffu) - 1) / (float)n;
-            return Record{__float_as_int(rk[k].x), rk[k].y, rk[k].z, c};
-        },
-        mat4);
+        for (int k = have; k < m; k++) rk[k] = __ldcg(wa.rec + (int64_t)k * n_pix + lp);
+        c = unwind(
+            m, (info >> 8) & 1, f3(px.x, px.y, px.z), sa,
+            [&](int k) { return Record{__float_as_int(rk[k].x), rk[k].y, rk[k].z, coeff(k, rk[k].w)}; }, mat4);
+    }
     const int ly = lp / fa.width, x = lp - ly * fa.width;
     store_pixel(fa, x, map_row(ly, fa), c);
     if (fa.peer_out) __threadfence_system();

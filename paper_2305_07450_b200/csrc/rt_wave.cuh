@@ -250,6 +250,32 @@ __device__ __forceinline__ float3 unwind(int m, bool exhausted, float3 tail, con
     return col;
 }
 
+// The same for m <= N records, fully unrolled: get(k) sees compile-time k,
+// so records held in a register array stay in registers.
+template <int N, class Get>
+__device__ __forceinline__ float3 unwind_upto(int m, bool exhausted, float3 tail, const SceneArgs<float> &sa, Get get,
+                                              const float4 *mat4 = nullptr) {
+    float3 col = tail;
+#pragma unroll
+    for (int k = N - 1; k >= 0; k--) {
+        if (k >= m) continue;
+        const Record r = get(k);
+        float lum = fminf(sa.ambient + r.sc * r.dfs * (1.f - sa.ambient), 1.f);
+        float sp = r.sc * r.s;
+        const float4 mt = mat4 ? mat4[r.idx] : __ldg(reinterpret_cast<const float4 *>(sa.mat + 8 * r.idx));
+        float br = mt.x, bg = mt.y, bb = mt.z;
+        if (!(exhausted && k == m - 1)) {
+            float rr = mt.w;
+            br = br * (1.f - rr) + col.x * rr;
+            bg = bg * (1.f - rr) + col.y * rr;
+            bb = bb * (1.f - rr) + col.z * rr;
+        }
+        col = f3(clamp01(br * lum + sa.lc[0] * sp), clamp01(bg * lum + sa.lc[1] * sp),
+                 clamp01(bb * lum + sa.lc[2] * sp));
+    }
+    return col;
+}
+
 __device__ __forceinline__ void store_pixel(const FrameArgs &fa, int x, int y, float3 c) {
     fa.out[(int64_t)y * fa.out_pitch + x] = pack_color(c.x, c.y, c.z, fa.rgba);
     if (fa.radiance) {

@@ -1,5 +1,5 @@
 """Pipelined frames/s (FramePipeline, the frame server's loop) under option
-sets, interleaved rounds: python tools/pipeline_ab.py C2 --set async_priority=0 --set async_priority=1"""
+sets, interleaved rounds: python tools/pipeline_ab.py C2 --set codec=0 --set codec=1"""
 import argparse
 import os
 import statistics

@@ -205,7 +205,9 @@ int rt_host_unregister(rt_ctx *ctx, void *ptr);
  *                 C2 moves 0.33 MB instead of 3.7 (rt_last_d2h_bytes).  Off:
  *                 the raw copy.  Rows wider than 6,144 pixels always copy raw;
  *   "codec_threads" host threads expanding a compressed frame (0, default:
- *                 up to 16 of the OpenMP pool). */
+ *                 up to 16 of the OpenMP pool);
+ *   "codec_parts" a one-band frame's encode in this many launches, each
+ *                 expanded as it lands (0, default: 2 from 2 MB, else 1). */
 int rt_set_option(rt_ctx *ctx, const char *name, int32_t value);
 /* Executed-work tallies since the last reset (option "count_work"), in this
  * order: hits, per-hit cull tests, hits that sampled, shadow rays, sphere

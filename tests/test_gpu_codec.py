@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(autouse=True)
 def _restore_options():
     yield
-    _native.set_options(codec=1, bands=0, codec_threads=0)
+    _native.set_options(codec=1, bands=0, codec_threads=0, codec_parts=0)
 
 
 def _frame(scene, cam, params, precision=None, radiance=None, **opts):
@@ -189,3 +189,18 @@ def test_codec_reports_fewer_bytes_and_device_time():
     ms = rt.last_kernel_ms()
     assert 0.01 < ms < 5.0
     assert 100_000 < enc_bytes < 1_000_000
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 8])
+def test_codec_encode_parts(parts):
+    """A one-band frame's encode cut into parts (option codec_parts), each
+    expanded as it lands: the same frame."""
+    c = rt.CONFIGS["C2"]
+    scene, cam, params = c.scene(), c.camera(), c.params()
+    raw, _ = _frame(scene, cam, params, codec=0)
+    enc, _ = _frame(scene, cam, params, codec=1, bands=1, codec_parts=parts)
+    np.testing.assert_array_equal(enc, raw)
+    small = _small(97, 61, samples=8, bounces=1)
+    raw, _ = _frame(*small, codec=0)
+    enc, _ = _frame(*small, codec=1, bands=1, codec_parts=parts)
+    np.testing.assert_array_equal(enc, raw)

@@ -17,7 +17,7 @@ objects work unchanged.
 and becomes the number of row-block partitions, spread over up to that many
 GPUs; as in the reference the pixels do not depend on it.
 
-`precision` (keyword, default "fp32", or $B200RT_PRECISION) picks the FP32
+`precision` (keyword, default "fp32", or $B200RT_PRECISION as the first frame finds it) picks the FP32
 product kernel or the FP64 validation kernel that reproduces the reference
 bit for bit.
 """
@@ -70,11 +70,17 @@ def default_precision() -> str:
     return os.environ.get("B200RT_PRECISION", "fp32")
 
 
+_DEFAULT_PREC = []  # $B200RT_PRECISION, read on the first frame (an environ lookup costs ~1 us)
+
+
 def _prec(precision) -> int:
-    p = precision or default_precision()
-    if p not in _native.PRECISIONS:
-        raise ValueError(f"precision must be one of {sorted(_native.PRECISIONS)}, got {p!r}")
-    return _native.PRECISIONS[p]
+    if precision is None:
+        if not _DEFAULT_PREC:
+            _DEFAULT_PREC.append(_prec(default_precision()))
+        return _DEFAULT_PREC[0]
+    if precision not in _native.PRECISIONS:
+        raise ValueError(f"precision must be one of {sorted(_native.PRECISIONS)}, got {precision!r}")
+    return _native.PRECISIONS[precision]
 
 
 def _scene_argv(ps):

@@ -164,7 +164,7 @@ cudaError_t launch_encode_rows(const uint32_t *frame, int64_t pitch, int width, 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, encode_rows, frame, pitch, width, y0, y1, d_host + codec_rows_offset(height));
+    return cudaLaunchKernelEx(&cfg, encode_rows, frame, pitch, width, y0, y1, d_host + kCodecPad);
 }
 
 }  // namespace rt

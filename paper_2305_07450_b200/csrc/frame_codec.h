@@ -42,8 +42,6 @@ constexpr int kCodecMaxWidth = 16384;
 inline size_t codec_host_bytes(int width, int height) {
     return sizeof(uint32_t) * (2 * (size_t)kCodecPad + (size_t)height * codec_row_stride(width));
 }
-// (the rows start kCodecPad words into the buffer)
-inline size_t codec_rows_offset(int) { return kCodecPad; }
 
 // Encode rows [y0, y1) of a height-row frame (row pitch in pixels) into the
 // mapped host buffer whose device address is d_host (layout above), launched

@@ -247,7 +247,7 @@ int64_t decode_rows_serial(const uint32_t *host, int width, int y0, int y1, uint
     const Isa isa = codec_isa();
     int64_t total = 0;
     for (int y = y0; y < y1; y++)
-        total += expand_row(host + codec_rows_offset(0) + (size_t)y * stride, width, dst + (size_t)y * pitch, isa);
+        total += expand_row(host + kCodecPad + (size_t)y * stride, width, dst + (size_t)y * pitch, isa);
     return total;
 }
 

@@ -268,7 +268,9 @@ int rt_copy_to_host(rt_ctx *ctx, int32_t slot, void *host_dst, const void *d_src
  * host frame host_frame (same layout: pixel (x, y) at y * width + x), on
  * `stream` (null: the context's stream), and wait for it.  With one process
  * per GPU and host_frame a page-locked buffer shared by them, every GPU
- * copies its own rows over its own PCIe link. */
+ * copies its own rows over its own PCIe link.  With option
+ * "codec" (default) the rows cross compressed and this process's threads
+ * expand them (rt_last_d2h_bytes: what crossed). */
 int rt_copy_partition_to_host(rt_ctx *ctx, int32_t slot, uint32_t *host_frame, const uint32_t *d_frame, int32_t width,
                               int32_t height, int32_t part, int32_t n_parts, int32_t block_rows, void *stream);
 

@@ -28,13 +28,17 @@ __device__ __forceinline__ unsigned lanemask_lt_() {
 constexpr int kRows = 1;
 
 __global__ void __launch_bounds__(kCodecThreads)
-    encode_rows(const uint32_t *__restrict__ frame, int64_t pitch, int width, int y0, int y1,
-                uint32_t *__restrict__ out) {
+    encode_rows(const uint32_t *__restrict__ frame, int64_t pitch, int width, int y0, int y1, int part, int n_parts,
+                int block_rows, uint32_t *__restrict__ out) {
     extern __shared__ uint32_t sm[];
     __shared__ int s_n[kRows], s_nz[kRows], s_opaque[kRows];
     const int nc = rt::codec_mask_words(width), nb = rt::codec_bitmap_words(width);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = kCodecThreads / 32;
-    const int r0 = y0 + blockIdx.x * kRows, rows = min(kRows, y1 - r0);
+    // this CTA's row: the blockIdx-th of rows [y0, y1) — or, for a partition of
+    // block_rows-row blocks dealt round-robin over n_parts, of its blocks
+    const int b = blockIdx.x * kRows;
+    const int r0 = n_parts > 1 ? y0 + ((b / block_rows) * n_parts + part) * block_rows + b % block_rows : y0 + b;
+    const int rows = min(kRows, y1 - r0);
     uint32_t *spx = sm;                      // [kRows][width] the rows' pixels
     uint32_t *slit = spx + kRows * width;    // [kRows][width] their literals, compacted
     uint32_t *smask = slit + kRows * width;  // [kRows][nc] mask word per chunk of 32 pixels
@@ -146,8 +150,15 @@ __global__ void __launch_bounds__(kCodecThreads)
 namespace rt {
 
 cudaError_t launch_encode_rows(const uint32_t *frame, int64_t pitch, int width, int height, int y0, int y1,
-                               uint32_t *d_host, cudaStream_t st) {
+                               uint32_t *d_host, cudaStream_t st, int part, int n_parts, int block_rows) {
     if (y1 <= y0) return cudaSuccess;
+    // rows of the partition (blocks j = part, part + n_parts, ... of block_rows rows)
+    int rows = y1 - y0;
+    if (n_parts > 1) {
+        rows = 0;
+        for (int j = part; j * block_rows < y1 - y0; j += n_parts) rows += std::min(block_rows, y1 - y0 - j * block_rows);
+        if (rows == 0) return cudaSuccess;
+    }
     const int nc = codec_mask_words(width);
     const size_t smem = sizeof(uint32_t) * kRows * (2 * (size_t)width + 3 * (size_t)nc + codec_bitmap_words(width));
     if (smem > 48 * 1024) {  // rows wider than ~1,400 pixels (up to kCodecMaxWidth: 206 KB)
@@ -155,7 +166,7 @@ cudaError_t launch_encode_rows(const uint32_t *frame, int64_t pitch, int width, 
         if (e != cudaSuccess) return e;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((y1 - y0 + kRows - 1) / kRows);
+    cfg.gridDim = dim3((rows + kRows - 1) / kRows);
     cfg.blockDim = dim3(kCodecThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -164,7 +175,8 @@ cudaError_t launch_encode_rows(const uint32_t *frame, int64_t pitch, int width, 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, encode_rows, frame, pitch, width, y0, y1, d_host + kCodecPad);
+    return cudaLaunchKernelEx(&cfg, encode_rows, frame, pitch, width, y0, y1, part, n_parts, block_rows,
+                              d_host + kCodecPad);
 }
 
 }  // namespace rt

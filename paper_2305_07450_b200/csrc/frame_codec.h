@@ -45,9 +45,12 @@ inline size_t codec_host_bytes(int width, int height) {
 
 // Encode rows [y0, y1) of a height-row frame (row pitch in pixels) into the
 // mapped host buffer whose device address is d_host (layout above), launched
-// as a programmatic dependent of the stream's previous kernel.
+// as a programmatic dependent of the stream's previous kernel.  n_parts > 1:
+// only partition `part`'s rows — blocks of block_rows rows dealt round-robin
+// over n_parts, counted from y0 (the multi-GPU row partition).
 cudaError_t launch_encode_rows(const uint32_t *frame, int64_t pitch, int width, int height, int y0, int y1,
-                               uint32_t *d_host, cudaStream_t st);
+                               uint32_t *d_host, cudaStream_t st, int part = 0, int n_parts = 1,
+                               int block_rows = 8);
 
 // Expand rows [y0, y1) of the buffer host into dst (row pitch in pixels) on
 // this thread; returns the words those rows moved over PCIe.

@@ -151,6 +151,7 @@ struct Dev {
     // compressed transfer (option codec): the mapped host buffer of
     // rt_render_v1's frames and of each slot, and what a slot's wait expands
     HBuf codec_host;
+    HBuf part_codec;  // rt_copy_partition_to_host's
     HBuf slot_codec[kSlots];
     struct SlotOut {
         uint32_t *pixels = nullptr;
@@ -1037,6 +1038,7 @@ int rt_ctx_destroy(rt_ctx *ctx) {
             d.slot_codec[k].release();
         }
         d.codec_host.release();
+        d.part_codec.release();
         if (d.copy_st) cudaStreamDestroy(d.copy_st);
         if (d.e0) cudaEventDestroy(d.e0);
         if (d.e1) cudaEventDestroy(d.e1);
@@ -1803,7 +1805,27 @@ int rt_copy_partition_to_host(rt_ctx *ctx, int32_t slot, uint32_t *host_frame, c
     Dev &d = ctx->devs[slot];
     RT_CK(cudaSetDevice(d.id));
     cudaStream_t st = stream ? (cudaStream_t)stream : d.st;
-    int rc = copy_partition(host_frame, d_frame, sizeof(uint32_t), width, height, part, n_parts, block_rows, st);
+    int rc;
+    if (ctx->codec && width <= rt::kCodecMaxWidth) {
+        // compressed (option codec, frame_codec.h): the partition's rows encoded
+        // into mapped host memory, then expanded block by block by host threads
+        if ((rc = d.part_codec.ensure(rt::codec_host_bytes(width, height)))) return rc;
+        RT_CK(rt::launch_encode_rows(d_frame, width, width, height, 0, height, (uint32_t *)d.part_codec.dp, st, part,
+                                     n_parts, block_rows));
+        RT_CK(cudaStreamSynchronize(st));
+        const int n_blocks = (height + block_rows - 1) / block_rows;
+        const int mine = n_blocks > part ? (n_blocks - part + n_parts - 1) / n_parts : 0;
+        int64_t words = 0;
+#pragma omp parallel for num_threads(std::max(1, std::min(codec_threads(ctx), mine))) schedule(dynamic) reduction(+ : words)
+        for (int i = 0; i < mine; i++) {
+            const int y0 = (part + i * n_parts) * block_rows;
+            words += rt::decode_rows_serial((const uint32_t *)d.part_codec.p, width, y0, std::min(height, y0 + block_rows),
+                                            host_frame, width);
+        }
+        ctx->last_d2h_bytes = (int64_t)sizeof(uint32_t) * words;
+        return RT_OK;
+    }
+    rc = copy_partition(host_frame, d_frame, sizeof(uint32_t), width, height, part, n_parts, block_rows, st);
     if (rc) return rc;
     RT_CK(cudaStreamSynchronize(st));
     return RT_OK;

@@ -204,3 +204,43 @@ def test_codec_encode_parts(parts):
     raw, _ = _frame(*small, codec=0)
     enc, _ = _frame(*small, codec=1, bands=1, codec_parts=parts)
     np.testing.assert_array_equal(enc, raw)
+
+
+@pytest.mark.parametrize("n_parts,size", [(1, (1280, 720)), (3, (1280, 720)), (2, (97, 61)), (5, (333, 19))])
+def test_codec_partition_copies(n_parts, size):
+    """rt_copy_partition_to_host (the multi-GPU host-frame gather) with the
+    compressed transfer: each partition's interleaved 8-row blocks land in a
+    host frame exactly as the raw 2-D copies put them."""
+    import ctypes
+
+    w, h = size
+    lib = _native.load()
+    ctx = _native.Context((0,))
+    try:
+        c = rt.CONFIGS["C2"]
+        ps = rt.pack_scene(c.scene())
+        P = _native.ptr
+        _native.check(lib.rt_set_scene_v1(ctx.handle, ps.n_bodies, P(ps.kinds), P(ps.positions), P(ps.sizes),
+                                          P(ps.colors), P(ps.refls), P(ps.light_pos), ps.light_radius,
+                                          P(ps.light_color), ps.ambient, ps.max_refl, P(ps.sky), ps.sky_w, ps.sky_h,
+                                          int(ps.has_sky)), "rt_set_scene_v1")
+        d_frame = ctypes.c_void_p()
+        _native.check(lib.rt_device_malloc(0, 4 * w * h, ctypes.byref(d_frame)), "rt_device_malloc")
+        cam = c.camera()
+        cp = np.array(cam.position, dtype=np.float64)
+        _native.check(lib.rt_render_device_v1(ctx.handle, 0, d_frame, w, None, w, h, P(cp), cam.yaw, cam.pitch,
+                                              rt.camera_viewport_distance(cam.fov), 16, 2, 0, 1, 8,
+                                              _native.RT_PREC_FP32, None), "rt_render_device_v1")
+        frames = []
+        for codec in (0, 1):
+            ctx.set_option("codec", codec)
+            host = np.full(w * h, 0x5A5A5A5A, dtype=np.uint32)
+            for part in range(n_parts):
+                _native.check(lib.rt_copy_partition_to_host(ctx.handle, 0, P(host), d_frame, w, h, part, n_parts, 8,
+                                                            None), "rt_copy_partition_to_host")
+            frames.append(host)
+        np.testing.assert_array_equal(frames[1], frames[0])
+        assert (frames[0] != 0x5A5A5A5A).all()
+        lib.rt_device_free(d_frame)
+    finally:
+        ctx.close()

@@ -25,13 +25,22 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_two_rank_bench_row_bands():
+def _run_two_ranks():
     env = dict(os.environ, B200RT_BENCH_SHARE_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps",
            "2", "--warmup", "3", "--no-extra", "--no-cpu-baseline"]
-    proc = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
-    assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
+    return subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+
+
+def test_two_rank_bench_row_bands():
+    proc = _run_two_ranks()
+    if proc.returncode != 0:
+        # a free port can be taken between the probe and the rendezvous: one
+        # more launch on a fresh port (the first run's output stays in the message)
+        first = proc.stdout[-1500:] + proc.stderr[-1500:]
+        proc = _run_two_ranks()
+        assert proc.returncode == 0, "first run:\n" + first + "\nsecond run:\n" + proc.stdout[-3000:] + proc.stderr[-3000:]
     lines = [l for l in proc.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, proc.stdout[-3000:]  # rank 0 alone prints
     d = json.loads(lines[0])

@@ -164,9 +164,10 @@ int rt_host_unregister(rt_ctx *ctx, void *ptr);
  *   "count_work"  tally the executed work of the culled pass (rt_work_counts);
  *   "bands"       rt_render_v1 on one device renders this many contiguous row
  *                 bands (1-8), each on its own stream (band 0 at the highest
- *                 priority), and copies each to the host as soon as it is
- *                 done; 0 (default) = by frame size: 1 below 1 MB, 2 below
- *                 24 MB, else 6;
+ *                 priority), and moves each to the host as soon as it is
+ *                 done; 0 (default) = by frame size: with option "codec" 1
+ *                 below 6 MB, 2 below 24 MB, else 6; raw, 1 below 1 MB, 2
+ *                 below 24 MB, else 6;
  *   "band_first"  permille of the frame's rows in band 0 (0, default: equal
  *                 bands; the others always share the rest equally);
  *   "boxes"       (default on, with "cull") FP32 megakernel frames (under 8

@@ -1,3 +1,4 @@
+"""C5 stress scenes (256 and 512 spheres): device frame time of the culled path, a quick A/B probe."""
 import sys, time
 sys.path.insert(0, '.')
 import paper_2305_07450_b200 as rt

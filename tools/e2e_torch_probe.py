@@ -1,3 +1,4 @@
+"""render_frame end to end with and without torch imported and its CUDA context active in the same process (the bench imports torch)."""
 import sys, time, statistics, os
 sys.path.insert(0, '/root/repo')
 if len(sys.argv) > 1 and sys.argv[1] == 'torch':

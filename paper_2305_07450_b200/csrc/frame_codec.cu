@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kCodecThreads)
     // a load per step measured 2x slower: its latencies add up)
     for (int r = 0; r < rows; r++) {
         const uint4 *src = reinterpret_cast<const uint4 *>(frame + (int64_t)(r0 + r) * pitch);
-        if ((width & 3) == 0 && (pitch & 3) == 0) {
+        if ((width & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {  // (a caller's frame may be offset)
 #pragma unroll 4
             for (int i = threadIdx.x; i < width / 4; i += kCodecThreads)
                 reinterpret_cast<uint4 *>(spx + r * width)[i] = __ldcg(src + i);

@@ -244,3 +244,30 @@ def test_codec_partition_copies(n_parts, size):
         lib.rt_device_free(d_frame)
     finally:
         ctx.close()
+
+
+def test_codec_partition_copy_from_an_offset_device_frame():
+    """rt_copy_partition_to_host from a device frame that starts 4 bytes into
+    its allocation (a caller's pointer need not be 16-byte aligned)."""
+    import ctypes
+
+    import torch
+
+    w, h = 64, 24
+    lib = _native.load()
+    ctx = _native.Context((0,))
+    try:
+        frame = (np.arange(w * h, dtype=np.uint32) // 5) | np.uint32(0xFF000000)
+        buf = torch.zeros(w * h + 4, dtype=torch.int32, device="cuda")
+        buf[1:1 + w * h] = torch.from_numpy(frame.view(np.int32)).cuda()
+        torch.cuda.synchronize()
+        d_frame = ctypes.c_void_p(buf.data_ptr() + 4)
+        for codec in (0, 1):
+            ctx.set_option("codec", codec)
+            host = np.zeros(w * h, dtype=np.uint32)
+            for part in range(3):
+                _native.check(lib.rt_copy_partition_to_host(ctx.handle, 0, _native.ptr(host), d_frame, w, h, part, 3,
+                                                            8, None), "rt_copy_partition_to_host")
+            np.testing.assert_array_equal(host, frame)
+    finally:
+        ctx.close()
